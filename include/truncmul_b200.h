@@ -1,0 +1,158 @@
+/*
+ * truncmul_b200 — C ABI of the B200-native full / low / high integer products.
+ *
+ * This is the drop-in boundary for the reference's product entry points
+ * (arxiv 1703.00640 artifact, /root/reference/proj/core):
+ *
+ *   products.hpp:36-45   struct Params          -> tmg_params
+ *   products.hpp:48      required_precision     -> tmg_required_precision
+ *   products.hpp:52-53   default_lambda         -> tmg_default_lambda
+ *   products.hpp:60      validate_params        -> tmg_validate_params
+ *   products.hpp:67-68   select_params          -> tmg_select_params
+ *   products.hpp:91-93   full_product / low_product / high_product
+ *                        -> tmg_full_product / tmg_low_product /
+ *                           tmg_high_product  (host limb arrays)
+ *                        -> tmg_product_device  (device-resident limbs)
+ *   errors.hpp:9-67      exception classes  -> TMG_ERR_* return codes
+ *
+ * Operands and results are little-endian arrays of 64-bit limbs (the
+ * reference's BigInt::to_limbs / from_limbs, bigint.hpp:118-120).  Operands
+ * hold ceil(n/64) limbs; results hold tmg_output_limbs(mode, n) limbs:
+ *   full: ceil(2n/64)   low: ceil(n/64)   high: ceil((n+1)/64)
+ *
+ * Every function returns TMG_OK (0) or a TMG_ERR_* code; tmg_last_error()
+ * gives the message of the calling thread's last failure.  No function
+ * throws across the ABI.  There is no CPU fallback: products run on the GPU
+ * and fail with TMG_ERR_CUDA when no device is usable.
+ */
+#ifndef TRUNCMUL_B200_H_
+#define TRUNCMUL_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Mode (products.hpp:14) */
+enum {
+  TMG_MODE_FULL = 0,
+  TMG_MODE_LOW = 1,
+  TMG_MODE_HIGH = 2,
+  TMG_MODE_ORACLE_FALLBACK = 3
+};
+
+/* Backend (convolution.hpp:13).  Only the FFT backend is implemented on the
+ * GPU; EXACT parameter sets are accepted by the parameter functions and
+ * refused by the product functions with TMG_ERR_UNSUPPORTED. */
+enum { TMG_BACKEND_EXACT = 0, TMG_BACKEND_FFT = 1 };
+
+/* Parameter selection policy.  REFERENCE reproduces params.cpp exactly;
+ * ACCURATE additionally bounds the predicted rounding error of an FP64 FFT
+ * below the 0.25 tripwire and ranks lengths by GPU cost. */
+enum { TMG_POLICY_REFERENCE = 0, TMG_POLICY_ACCURATE = 1 };
+
+/* Error codes (errors.hpp) */
+enum {
+  TMG_OK = 0,
+  TMG_ERR_INPUT_OUT_OF_RANGE = 1,   /* InputOutOfRange */
+  TMG_ERR_NO_VALID_PARAMS = 2,      /* NoValidParams */
+  TMG_ERR_UNSUPPORTED_LENGTH = 3,   /* UnsupportedLength */
+  TMG_ERR_PRECISION_FAILURE = 4,    /* ConvolutionPrecisionFailure */
+  TMG_ERR_PLAN_MISMATCH = 5,        /* PlanMismatch */
+  TMG_ERR_UNSUPPORTED = 6,          /* parameter set the GPU path refuses */
+  TMG_ERR_CUDA = 7,                 /* CUDA runtime failure / no device */
+  TMG_ERR_INTERNAL = 8
+};
+
+/* Params (products.hpp:36-45) */
+typedef struct tmg_params {
+  int64_t n;
+  int32_t b;
+  int64_t N;
+  int64_t lambda;
+  int32_t p;
+  int32_t mode;
+  int32_t backend;
+  int32_t signed_split;
+} tmg_params;
+
+/* Per-product statistics filled by the product functions. */
+typedef struct tmg_stats {
+  double max_round_err; /* max distance of a pre-rounding value to an integer */
+  double max_abs;       /* max magnitude of a pre-rounding value */
+  uint32_t flags;       /* raw device flag word */
+  int64_t transform_length;
+  int32_t passes;       /* 1 = fused single CTA, 2 or 3 = multi-pass */
+  int32_t kernels;      /* kernels launched for the product */
+} tmg_stats;
+
+typedef struct tmg_context tmg_context;
+
+const char* tmg_last_error(void);
+const char* tmg_version(void);
+
+/* ---- parameters (host only; no GPU needed) ---- */
+int tmg_required_precision(int32_t mode, int32_t b, int64_t N, int32_t* out);
+int tmg_default_lambda(int32_t mode, int32_t backend, int32_t b, int32_t p,
+                       int64_t* out);
+int tmg_validate_params(const tmg_params* params);
+int tmg_select_params(int64_t n, int32_t mode, int32_t backend,
+                      int64_t fallback_cutoff, int32_t policy,
+                      tmg_params* out);
+int64_t tmg_output_limbs(int32_t mode, int64_t n);
+/* Predicted standard deviation of the FP64 rounding error (policy model). */
+double tmg_predicted_sigma(const tmg_params* params);
+
+/* ---- context ---- */
+int tmg_context_create(int device, tmg_context** out);
+void tmg_context_destroy(tmg_context* ctx);
+/* Optional: run subsequent work on a caller-owned cudaStream_t. */
+int tmg_context_set_stream(tmg_context* ctx, void* stream);
+int tmg_synchronize(tmg_context* ctx);
+
+/* ---- products on host limb arrays (H2D, kernels, D2H inside) ----
+ * params must be an FFT-backend parameter set of the matching mode, or an
+ * ORACLE_FALLBACK set (operands below the cutoff: GPU schoolbook product). */
+int tmg_full_product(tmg_context* ctx, const tmg_params* params,
+                     const uint64_t* u, const uint64_t* v, uint64_t* out,
+                     tmg_stats* stats);
+int tmg_low_product(tmg_context* ctx, const tmg_params* params,
+                    const uint64_t* u, const uint64_t* v, uint64_t* out,
+                    tmg_stats* stats);
+int tmg_high_product(tmg_context* ctx, const tmg_params* params,
+                     const uint64_t* u, const uint64_t* v, uint64_t* out,
+                     tmg_stats* stats);
+
+/* Batched: count independent products of the same params; operands and
+ * results are packed back to back.  flags_out (optional, count words)
+ * receives each product's device flag word. */
+int tmg_product_batched(tmg_context* ctx, const tmg_params* params,
+                        const uint64_t* u, const uint64_t* v, int64_t count,
+                        uint64_t* out, uint32_t* flags_out, tmg_stats* stats);
+
+/* ---- device-resident variants (enqueue only; no host synchronisation) ----
+ * d_u, d_v, d_out are device pointers.  Errors detected on the device are
+ * reported by the next tmg_check(). */
+int tmg_product_device(tmg_context* ctx, const tmg_params* params,
+                       const uint64_t* d_u, const uint64_t* d_v,
+                       uint64_t* d_out, int64_t count);
+int tmg_check(tmg_context* ctx, tmg_stats* stats);
+
+/* Pinned host buffers for the end-to-end path. */
+int tmg_host_alloc(size_t bytes, void** out);
+void tmg_host_free(void* p);
+int tmg_device_alloc(size_t bytes, void** out);
+void tmg_device_free(void* p);
+int tmg_memcpy_h2d(tmg_context* ctx, void* dst, const void* src, size_t bytes);
+int tmg_memcpy_d2h(tmg_context* ctx, void* dst, const void* src, size_t bytes);
+
+/* Kernels launched by the last product call (for launch accounting). */
+int32_t tmg_last_kernel_count(tmg_context* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TRUNCMUL_B200_H_ */

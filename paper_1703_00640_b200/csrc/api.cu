@@ -1,0 +1,626 @@
+// Context, launch orchestration and the extern "C" boundary
+// (include/truncmul_b200.h).  The launch sequence of one product follows the
+// reference's pipeline order (products_f64.cpp:106-171):
+//   split -> pre-map -> forward transforms -> pointwise -> inverse ->
+//   post-map -> round/accumulate -> carry, with the tripwires of
+//   products_f64.cpp:16-27 and 137-169 reported through a device status word.
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+
+#include "../../include/truncmul_b200.h"
+#include "kernels.cuh"
+#include "params.hpp"
+#include "plan.hpp"
+
+namespace tmg {
+
+#define TMG_CUDA(call)                                                     \
+  do {                                                                     \
+    cudaError_t e_ = (call);                                               \
+    if (e_ != cudaSuccess)                                                 \
+      throw Error(TMG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+thread_local std::string g_last_error;
+
+struct ScanSlot {
+  DevBuf state;     // look-back words
+  DevBuf ctr;       // ticket / done counters
+  uint32_t epoch = 0;
+  ScanState next(size_t blocks) {
+    state.ensure(std::max<size_t>(blocks, 1) * 8);
+    if (!ctr.p) {
+      ctr.ensure(64);
+      TMG_CUDA(cudaMemset(ctr.p, 0, 64));
+      TMG_CUDA(cudaMemset(state.p, 0, state.bytes));
+    }
+    ScanState s;
+    s.state = state.as<unsigned long long>();
+    s.ctr = ctr.as<unsigned long long>();
+    s.epoch = ++epoch;
+    return s;
+  }
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  TwiddleCache tw;
+  std::map<std::tuple<int64_t, int32_t, int64_t, int64_t, int32_t>, std::unique_ptr<Plan>> plans;
+  DevBuf work_t, work_c, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags;
+  ScanSlot scan_u, scan_v, scan_c;
+  DevStatus* h_status = nullptr;  // pinned
+  int32_t last_kernels = 0;
+  int64_t last_L = 0;
+  int32_t last_passes = 0;
+
+  Plan& plan_for(const Params& p) {
+    auto key = std::make_tuple(p.n, p.b, p.N, p.lambda, int32_t(p.mode));
+    auto it = plans.find(key);
+    if (it != plans.end()) return *it->second;
+    validate_params(p);
+    auto pl = build_plan(p, tw);
+    Plan& ref = *pl;
+    plans.emplace(key, std::move(pl));
+    return ref;
+  }
+};
+
+namespace {
+
+void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    throw Error(TMG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    TMG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(bytes)));
+}
+
+// Enqueue one batch of products (device pointers) on the context stream.
+void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
+             uint64_t* dout, int64_t count, uint32_t* pflags) {
+  const Params& p = pl.params;
+  cudaStream_t st = cx.stream;
+  DevStatus* status = cx.status.as<DevStatus>();
+  cx.last_L = pl.L;
+  cx.last_passes = pl.kind;
+  if (pl.kind == 0)
+    throw Error(TMG_ERR_UNSUPPORTED, "fallback products run through the host entry points");
+  if (pl.kind == 1) {
+    SmallArgs a;
+    a.u = du;
+    a.v = dv;
+    a.out = dout;
+    a.pflags = pflags;
+    a.nlimbs = pl.nlimbs;
+    a.n = p.n;
+    a.out_limbs = pl.out_limbs;
+    a.L = pl.L;
+    a.count = pl.count;
+    a.lead = pl.lead;
+    a.K = pl.K;
+    a.ML = pl.ML;
+    a.shift_s = pl.shift_s;
+    a.scale = 1.0 / (4.0 * double(pl.L));
+    a.fwd = pl.fwd;
+    a.inv = pl.inv;
+    a.mc = pl.mc;
+    a.status = status;
+    set_smem(k_small_product, pl.small_smem);
+    k_small_product<<<unsigned(count), pl.small_threads, pl.small_smem, st>>>(a);
+    check_launch("k_small_product");
+    cx.last_kernels = 1;
+    return;
+  }
+  // multi-pass, one product at a time
+  const int64_t L = pl.L;
+  cx.work_t.ensure(size_t(L) * 16);
+  cx.work_c.ensure(size_t(L) * 8 + 64);
+  const int64_t cwords = (pl.count + 31) / 32 + 1;
+  cx.cbu.ensure(size_t(cwords) * 4);
+  cx.cbv.ensure(size_t(cwords) * 4);
+  cx.aux.ensure(64);
+  int kernels = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    const uint64_t* u = du + i * pl.nlimbs;
+    const uint64_t* v = dv + i * pl.nlimbs;
+    uint64_t* out = dout + i * pl.out_limbs;
+    // split carry scan
+    {
+      SplitScanArgs a;
+      a.u = u;
+      a.v = v;
+      a.nlimbs = pl.nlimbs;
+      a.n = p.n;
+      a.b = p.b;
+      a.count = pl.count;
+      a.lead = pl.lead;
+      a.cbits_u = cx.cbu.as<uint32_t>();
+      a.cbits_v = cx.cbv.as<uint32_t>();
+      const unsigned blocks = unsigned((pl.count + kSplitThreads * 32 - 1) / (kSplitThreads * 32));
+      a.scan_u = cx.scan_u.next(blocks);
+      a.scan_v = cx.scan_v.next(blocks);
+      a.status = status;
+      k_split_scan<<<dim3(blocks, 2), kSplitThreads, 0, st>>>(a);
+      check_launch("k_split_scan");
+      ++kernels;
+    }
+    double2* T = cx.work_t.as<double2>();
+    {
+      F1Args a;
+      a.u = u;
+      a.v = v;
+      a.nlimbs = pl.nlimbs;
+      a.b = p.b;
+      a.count = pl.count;
+      a.lead = pl.lead;
+      a.cbits_u = cx.cbu.as<uint32_t>();
+      a.cbits_v = cx.cbv.as<uint32_t>();
+      a.out = T;
+      a.ncols = uint32_t(L / pl.A);
+      a.logc = pl.logc_f1;
+      a.fft = pl.fA;
+      a.tw = pl.twL;
+      a.mc = pl.mc;
+      a.aux = cx.aux.as<double>();
+      set_smem(k_f1, pl.smem_f1);
+      k_f1<<<a.ncols >> a.logc, pl.thr_f1, pl.smem_f1, st>>>(a);
+      check_launch("k_f1");
+      ++kernels;
+    }
+    if (pl.kind == 3) {
+      ColArgs a;
+      a.data = T;
+      a.g.os = int64_t(pl.B) * pl.C;
+      a.g.rs = pl.C;
+      a.g.cs = pl.C;
+      a.g.cw = pl.C;
+      a.g.ncols = pl.C;
+      a.logc = pl.logc_f2;
+      a.fft = pl.fB;
+      a.tw = pl.twL;
+      a.inv = 0;
+      a.to = 0;
+      a.tc = 1;
+      a.tmul = pl.A;
+      set_smem(k_col, pl.smem_f2);
+      k_col<<<dim3(pl.C >> a.logc, pl.A), pl.thr_f2, pl.smem_f2, st>>>(a);
+      check_launch("k_col(f2)");
+      ++kernels;
+    }
+    {
+      MidArgs a;
+      a.data = T;
+      a.A = pl.A;
+      a.B = pl.B;
+      a.C = pl.C;
+      a.fwd = pl.fC;
+      a.inv = pl.iC;
+      a.tw = pl.twL;
+      a.L = uint32_t(L);
+      a.scale = 1.0 / (4.0 * double(L));
+      set_smem(k_mid, pl.smem_mid);
+      const unsigned grid = (pl.A * pl.B) / 2 + 1;
+      k_mid<<<grid, pl.thr_mid, pl.smem_mid, st>>>(a);
+      check_launch("k_mid");
+      ++kernels;
+    }
+    if (pl.kind == 3) {
+      ColArgs a;
+      a.data = T;
+      a.g.os = int64_t(pl.B) * pl.C;
+      a.g.rs = pl.C;
+      a.g.cs = pl.C;
+      a.g.cw = pl.C / 2;
+      a.g.ncols = pl.C / 2;
+      a.logc = pl.logc_i2;
+      a.fft = pl.iB;
+      a.tw = pl.twL;
+      a.inv = 1;
+      a.to = 1;
+      a.tc = 0;
+      a.tmul = pl.C;
+      set_smem(k_col, pl.smem_i2);
+      k_col<<<dim3((pl.C / 2) >> a.logc, pl.A), pl.thr_i2, pl.smem_i2, st>>>(a);
+      check_launch("k_col(i2)");
+      ++kernels;
+    }
+    double2* coef = cx.work_c.as<double2>();
+    {
+      ILastArgs a;
+      a.data = T;
+      a.coef = coef;
+      a.g.os = 0;
+      a.g.rs = int64_t(pl.B) * pl.C;
+      a.g.cs = pl.C;
+      a.g.cw = pl.C / 2;
+      a.g.ncols = pl.B * (pl.C / 2);
+      a.logc = pl.logc_il;
+      a.fft = pl.iA;
+      set_smem(k_ilast, pl.smem_il);
+      k_ilast<<<a.g.ncols >> a.logc, pl.thr_il, pl.smem_il, st>>>(a);
+      check_launch("k_ilast");
+      ++kernels;
+    }
+    {
+      CarryArgs a;
+      a.w = reinterpret_cast<const double*>(coef);
+      a.out = out;
+      a.n = p.n;
+      a.out_limbs = pl.out_limbs;
+      a.K = pl.K;
+      a.ML = pl.ML;
+      a.shift_s = pl.shift_s;
+      a.mc = pl.mc;
+      a.aux = cx.aux.as<double>();
+      const int64_t LB = kCarryThreads * kCarryPerThread;
+      const unsigned blocks = unsigned((pl.ML + LB - 1) / LB);
+      a.scan = cx.scan_c.next(blocks);
+      a.status = status;
+      a.hstate = nullptr;
+      set_smem(k_carry, pl.smem_carry);
+      k_carry<<<blocks, kCarryThreads, pl.smem_carry, st>>>(a);
+      check_launch("k_carry");
+      ++kernels;
+    }
+  }
+  cx.last_kernels = kernels;
+}
+
+void reset_status(Context& cx) {
+  TMG_CUDA(cudaMemsetAsync(cx.status.p, 0, sizeof(DevStatus), cx.stream));
+}
+
+// Reads the status word and maps device flags onto the reference's errors.
+int finish(Context& cx, const Plan* pl, tmg_stats* stats) {
+  TMG_CUDA(cudaMemcpyAsync(cx.h_status, cx.status.p, sizeof(DevStatus),
+                           cudaMemcpyDeviceToHost, cx.stream));
+  TMG_CUDA(cudaStreamSynchronize(cx.stream));
+  DevStatus s = *cx.h_status;
+  double e, m;
+  std::memcpy(&e, &s.max_err_bits, 8);
+  std::memcpy(&m, &s.max_abs_bits, 8);
+  if (stats) {
+    stats->max_round_err = e;
+    stats->max_abs = m;
+    stats->flags = s.flags;
+    stats->transform_length = cx.last_L;
+    stats->passes = cx.last_passes;
+    stats->kernels = cx.last_kernels;
+  }
+  uint32_t f = s.flags;
+  if (s.high_topbit && s.high_lownz) f |= kFlagHighRange;
+  if (f & kFlagInputRange)
+    throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "split: operand outside [0, 2^n)");
+  if (f & kFlagOverflow)
+    throw Error(TMG_ERR_PRECISION_FAILURE,
+                "float pipeline coefficient overflowed the exact-integer range");
+  if (f & kFlagTripwire)
+    throw Error(TMG_ERR_PRECISION_FAILURE,
+                "float pipeline rounding tripwire: residual above a quarter");
+  if (f & kFlagLowNotDivisible)
+    throw Error(TMG_ERR_PRECISION_FAILURE,
+                "low product recombination is not divisible by the chunk base");
+  if (f & kFlagHighRange)
+    throw Error(TMG_ERR_PRECISION_FAILURE, "high product left its admissible range");
+  if (f & kFlagNegative)
+    throw Error(TMG_ERR_PRECISION_FAILURE, "full product recombined negative");
+  if (f & kFlagFullOverflow)
+    throw Error(TMG_ERR_PRECISION_FAILURE, "full product exceeded 2n bits");
+  if (f & kFlagCarryRange)
+    throw Error(TMG_ERR_INTERNAL, "carry propagation left its range");
+  (void)pl;
+  return TMG_OK;
+}
+
+Params from_c(const tmg_params* p) {
+  Params q;
+  q.n = p->n;
+  q.b = p->b;
+  q.N = p->N;
+  q.lambda = p->lambda;
+  q.p = p->p;
+  q.mode = PMode(p->mode);
+  q.backend = Backend(p->backend);
+  q.signed_split = p->signed_split != 0;
+  return q;
+}
+
+void to_c(const Params& q, tmg_params* p) {
+  p->n = q.n;
+  p->b = q.b;
+  p->N = q.N;
+  p->lambda = q.lambda;
+  p->p = q.p;
+  p->mode = int32_t(q.mode);
+  p->backend = int32_t(q.backend);
+  p->signed_split = q.signed_split ? 1 : 0;
+}
+
+void init_context(Context& cx, int device) {
+  cx.device = device;
+  TMG_CUDA(cudaSetDevice(device));
+  TMG_CUDA(cudaStreamCreateWithFlags(&cx.stream, cudaStreamNonBlocking));
+  cx.own_stream = true;
+  cx.status.ensure(sizeof(DevStatus));
+  TMG_CUDA(cudaMemset(cx.status.p, 0, sizeof(DevStatus)));
+  TMG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cx.h_status), sizeof(DevStatus),
+                         cudaHostAllocDefault));
+}
+
+// One product (or batch) from host limb arrays.
+int host_product(Context& cx, const Params& p, int32_t want_mode,
+                 const uint64_t* u, const uint64_t* v, int64_t count,
+                 uint64_t* out, uint32_t* flags_out, tmg_stats* stats) {
+  if (int32_t(p.mode) != want_mode && p.mode != PMode::kOracleFallback)
+    throw Error(TMG_ERR_INPUT_OUT_OF_RANGE,
+                "product: params were built for a different mode");
+  PMode eff = p.mode;
+  Params q = p;
+  if (eff == PMode::kOracleFallback) q.mode = PMode::kOracleFallback;
+  Plan& pl = cx.plan_for(q);
+  const int64_t nl = pl.nlimbs;
+  const int64_t OLr = output_limbs(PMode(want_mode), p.n);
+  TMG_CUDA(cudaSetDevice(cx.device));
+  cx.dop_u.ensure(size_t(count * nl) * 8 + 8);
+  cx.dop_v.ensure(size_t(count * nl) * 8 + 8);
+  const int64_t OLk = (pl.kind == 0) ? pl.out_limbs : OLr;
+  (void)OLk;
+  // the fallback plan computes the full product; truncate afterwards
+  const int64_t OLdev = (pl.kind == 0) ? 2 * nl : pl.out_limbs;
+  cx.dop_out.ensure(size_t(count * OLdev) * 8 + 8);
+  if (flags_out) cx.pflags.ensure(size_t(count) * 4 + 4);
+  reset_status(cx);
+  TMG_CUDA(cudaMemcpyAsync(cx.dop_u.p, u, size_t(count * nl) * 8, cudaMemcpyHostToDevice, cx.stream));
+  TMG_CUDA(cudaMemcpyAsync(cx.dop_v.p, v, size_t(count * nl) * 8, cudaMemcpyHostToDevice, cx.stream));
+  if (pl.kind == 0) {
+    // exact product on the GPU, truncated on the host side of the copy
+    DevBuf prod;
+    prod.ensure(size_t(count * 2 * nl) * 8);
+    for (int64_t i = 0; i < count; ++i) {
+      BaseArgs a{cx.dop_u.as<uint64_t>() + i * nl, cx.dop_v.as<uint64_t>() + i * nl,
+                 prod.as<uint64_t>() + i * 2 * nl, nl};
+      k_basecase<<<1, 256, size_t(6 * nl) * 8 + 64, cx.stream>>>(a);
+      check_launch("k_basecase");
+    }
+    std::vector<uint64_t> h(size_t(count * 2 * nl));
+    TMG_CUDA(cudaMemcpyAsync(h.data(), prod.p, h.size() * 8, cudaMemcpyDeviceToHost, cx.stream));
+    TMG_CUDA(cudaStreamSynchronize(cx.stream));
+    cx.last_kernels = int32_t(count);
+    cx.last_L = 0;
+    cx.last_passes = 0;
+    for (int64_t i = 0; i < count; ++i) {
+      const uint64_t* P = h.data() + i * 2 * nl;
+      uint64_t* o = out + i * OLr;
+      // input range check (InputOutOfRange, split.cpp:215-220)
+      const uint64_t* ui = u + i * nl;
+      const uint64_t* vi = v + i * nl;
+      if ((p.n & 63) && ((ui[nl - 1] | vi[nl - 1]) >> (p.n & 63)))
+        throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "split: operand outside [0, 2^n)");
+      if (want_mode == TMG_MODE_FULL) {
+        for (int64_t k = 0; k < OLr; ++k) o[k] = k < 2 * nl ? P[k] : 0;
+      } else if (want_mode == TMG_MODE_LOW) {
+        for (int64_t k = 0; k < OLr; ++k) o[k] = P[k];
+        if (p.n & 63) o[OLr - 1] &= (uint64_t(1) << (p.n & 63)) - 1;
+      } else {
+        // oracle_high_set(...).front() = floor(uv / 2^n)
+        const int64_t q = p.n >> 6;
+        const int r = int(p.n & 63);
+        for (int64_t k = 0; k < OLr; ++k) {
+          uint64_t lo = (q + k < 2 * nl) ? P[q + k] : 0;
+          uint64_t hi = (q + k + 1 < 2 * nl) ? P[q + k + 1] : 0;
+          o[k] = r ? ((lo >> r) | (hi << (64 - r))) : lo;
+        }
+        if ((p.n + 1) & 63) o[OLr - 1] &= (uint64_t(1) << ((p.n + 1) & 63)) - 1;
+      }
+      if (flags_out) flags_out[i] = 0;
+    }
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->kernels = int32_t(count);
+    }
+    return TMG_OK;
+  }
+  enqueue(cx, pl, cx.dop_u.as<uint64_t>(), cx.dop_v.as<uint64_t>(), cx.dop_out.as<uint64_t>(),
+          count, flags_out ? cx.pflags.as<uint32_t>() : nullptr);
+  TMG_CUDA(cudaMemcpyAsync(out, cx.dop_out.p, size_t(count * pl.out_limbs) * 8,
+                           cudaMemcpyDeviceToHost, cx.stream));
+  if (flags_out)
+    TMG_CUDA(cudaMemcpyAsync(flags_out, cx.pflags.p, size_t(count) * 4, cudaMemcpyDeviceToHost,
+                             cx.stream));
+  return finish(cx, &pl, stats);
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code();
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TMG_ERR_INTERNAL;
+  }
+}
+
+}  // namespace
+}  // namespace tmg
+
+using namespace tmg;
+
+struct tmg_context {
+  Context cx;
+};
+
+extern "C" {
+
+const char* tmg_last_error(void) { return g_last_error.c_str(); }
+const char* tmg_version(void) { return "truncmul_b200 0.1 (sm_100a)"; }
+
+int tmg_required_precision(int32_t mode, int32_t b, int64_t N, int32_t* out) {
+  return guarded([&] {
+    *out = required_precision(PMode(mode), b, N);
+    return TMG_OK;
+  });
+}
+
+int tmg_default_lambda(int32_t mode, int32_t backend, int32_t b, int32_t p, int64_t* out) {
+  return guarded([&] {
+    *out = default_lambda(PMode(mode), Backend(backend), b, p);
+    return TMG_OK;
+  });
+}
+
+int tmg_validate_params(const tmg_params* params) {
+  return guarded([&] {
+    validate_params(from_c(params));
+    return TMG_OK;
+  });
+}
+
+int tmg_select_params(int64_t n, int32_t mode, int32_t backend, int64_t fallback_cutoff,
+                      int32_t policy, tmg_params* out) {
+  return guarded([&] {
+    Params q = select_params(n, PMode(mode), Backend(backend), fallback_cutoff, Policy(policy));
+    to_c(q, out);
+    return TMG_OK;
+  });
+}
+
+int64_t tmg_output_limbs(int32_t mode, int64_t n) { return output_limbs(PMode(mode), n); }
+
+double tmg_predicted_sigma(const tmg_params* p) {
+  if (p->mode == TMG_MODE_ORACLE_FALLBACK) return 0.0;
+  return predicted_sigma(PMode(p->mode), p->b, p->N);
+}
+
+int tmg_context_create(int device, tmg_context** out) {
+  return guarded([&] {
+    auto c = std::make_unique<tmg_context>();
+    init_context(c->cx, device);
+    *out = c.release();
+    return TMG_OK;
+  });
+}
+
+void tmg_context_destroy(tmg_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->cx.device);
+  cudaStreamSynchronize(ctx->cx.stream);
+  if (ctx->cx.own_stream && ctx->cx.stream) cudaStreamDestroy(ctx->cx.stream);
+  if (ctx->cx.h_status) cudaFreeHost(ctx->cx.h_status);
+  delete ctx;
+}
+
+int tmg_context_set_stream(tmg_context* ctx, void* stream) {
+  return guarded([&] {
+    if (ctx->cx.own_stream && ctx->cx.stream) cudaStreamDestroy(ctx->cx.stream);
+    ctx->cx.stream = static_cast<cudaStream_t>(stream);
+    ctx->cx.own_stream = false;
+    return TMG_OK;
+  });
+}
+
+int tmg_synchronize(tmg_context* ctx) {
+  return guarded([&] {
+    TMG_CUDA(cudaStreamSynchronize(ctx->cx.stream));
+    return TMG_OK;
+  });
+}
+
+int tmg_full_product(tmg_context* ctx, const tmg_params* params, const uint64_t* u,
+                     const uint64_t* v, uint64_t* out, tmg_stats* stats) {
+  return guarded([&] {
+    return host_product(ctx->cx, from_c(params), TMG_MODE_FULL, u, v, 1, out, nullptr, stats);
+  });
+}
+
+int tmg_low_product(tmg_context* ctx, const tmg_params* params, const uint64_t* u,
+                    const uint64_t* v, uint64_t* out, tmg_stats* stats) {
+  return guarded([&] {
+    return host_product(ctx->cx, from_c(params), TMG_MODE_LOW, u, v, 1, out, nullptr, stats);
+  });
+}
+
+int tmg_high_product(tmg_context* ctx, const tmg_params* params, const uint64_t* u,
+                     const uint64_t* v, uint64_t* out, tmg_stats* stats) {
+  return guarded([&] {
+    return host_product(ctx->cx, from_c(params), TMG_MODE_HIGH, u, v, 1, out, nullptr, stats);
+  });
+}
+
+int tmg_product_batched(tmg_context* ctx, const tmg_params* params, const uint64_t* u,
+                        const uint64_t* v, int64_t count, uint64_t* out, uint32_t* flags_out,
+                        tmg_stats* stats) {
+  return guarded([&] {
+    Params q = from_c(params);
+    const int32_t m = q.mode == PMode::kOracleFallback ? TMG_MODE_FULL : int32_t(q.mode);
+    return host_product(ctx->cx, q, m, u, v, count, out, flags_out, stats);
+  });
+}
+
+int tmg_product_device(tmg_context* ctx, const tmg_params* params, const uint64_t* d_u,
+                       const uint64_t* d_v, uint64_t* d_out, int64_t count) {
+  return guarded([&] {
+    Params q = from_c(params);
+    if (q.mode == PMode::kOracleFallback)
+      throw Error(TMG_ERR_UNSUPPORTED, "device path needs a pipeline parameter set");
+    Plan& pl = ctx->cx.plan_for(q);
+    enqueue(ctx->cx, pl, d_u, d_v, d_out, count, nullptr);
+    return TMG_OK;
+  });
+}
+
+int tmg_check(tmg_context* ctx, tmg_stats* stats) {
+  return guarded([&] {
+    int r = finish(ctx->cx, nullptr, stats);
+    reset_status(ctx->cx);
+    return r;
+  });
+}
+
+int tmg_host_alloc(size_t bytes, void** out) {
+  return guarded([&] {
+    TMG_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocDefault));
+    return TMG_OK;
+  });
+}
+void tmg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+int tmg_device_alloc(size_t bytes, void** out) {
+  return guarded([&] {
+    TMG_CUDA(cudaMalloc(out, bytes));
+    return TMG_OK;
+  });
+}
+void tmg_device_free(void* p) {
+  if (p) cudaFree(p);
+}
+int tmg_memcpy_h2d(tmg_context* ctx, void* dst, const void* src, size_t bytes) {
+  return guarded([&] {
+    TMG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->cx.stream));
+    return TMG_OK;
+  });
+}
+int tmg_memcpy_d2h(tmg_context* ctx, void* dst, const void* src, size_t bytes) {
+  return guarded([&] {
+    TMG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->cx.stream));
+    return TMG_OK;
+  });
+}
+int32_t tmg_last_kernel_count(tmg_context* ctx) { return ctx->cx.last_kernels; }
+
+}  // extern "C"

@@ -1,0 +1,117 @@
+// Shared device-side definitions for the truncated-product pipeline.
+//
+// Domain vocabulary follows the reference (arxiv 1703.00640 artifact,
+// /root/reference/proj/core): limbs are little-endian uint64 words of an
+// operand, chunks are the b-bit pieces the operand is split into
+// (split.cpp:267-304), coefficients are the rounded convolution outputs that
+// recombination sums at bit offsets i*b (products_f64.cpp:29-102).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tmg {
+
+// ---------------------------------------------------------------------------
+// Status word written by the kernels and read by the host after a product.
+// The flag bits map onto the reference's exception types (errors.hpp):
+//   kFlagTripwire / kFlagOverflow -> ConvolutionPrecisionFailure
+//       ("rounding tripwire: residual above a quarter" /
+//        "coefficient overflowed the exact-integer range",
+//        products_f64.cpp:16-27)
+//   kFlagLowNotDivisible -> ConvolutionPrecisionFailure
+//       ("low product recombination is not divisible by the chunk base",
+//        products_f64.cpp:137-140)
+//   kFlagHighRange -> ConvolutionPrecisionFailure
+//       ("high product left its admissible range", products_f64.cpp:167-169)
+//   kFlagNegative -> ConvolutionPrecisionFailure
+//       ("full product recombined negative", products_f64.cpp:117-119)
+//   kFlagInputRange -> InputOutOfRange ("split: operand outside [0, 2^n)",
+//       split.cpp:215-220)
+enum : uint32_t {
+  kFlagTripwire = 1u << 0,
+  kFlagOverflow = 1u << 1,
+  kFlagLowNotDivisible = 1u << 2,
+  kFlagHighRange = 1u << 3,
+  kFlagNegative = 1u << 4,
+  kFlagInputRange = 1u << 5,
+  kFlagCarryRange = 1u << 6,   // internal: a limb carry left {-1,0,1}
+  kFlagFullOverflow = 1u << 7, // full product had bits above 2n
+};
+
+struct DevStatus {
+  unsigned long long max_err_bits;  // max |x - round(x)| as double bits
+  unsigned long long max_abs_bits;  // max |x| as double bits
+  unsigned int flags;
+  unsigned int high_topbit;  // high product: bit n of w was set
+  unsigned int high_lownz;   // high product: some bit below n was set
+  unsigned int pad;
+};
+
+// ---------------------------------------------------------------------------
+// Complex helpers (double2 as complex double).
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cconj(double2 a) {
+  return make_double2(a.x, -a.y);
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) {
+  return make_double2(a.x * s, a.y * s);
+}
+
+// ---------------------------------------------------------------------------
+// Carry transfer functions.  A limb (or chunk) maps an incoming carry
+// c in {-1, 0, +1} to an outgoing carry f(c) in {-1, 0, +1}; composing these
+// maps is associative, which is what makes carry propagation a parallel
+// prefix.  Encoding: two bits per input, holding f(c)+1, for c = -1, 0, +1
+// at bit offsets 0, 2, 4.
+__host__ __device__ __forceinline__ uint32_t tf_const(int c) {
+  return uint32_t(c + 1) * 21u;  // 21 = 1 + 4 + 16
+}
+constexpr uint32_t kTfIdentity = 0u | (1u << 2) | (2u << 4);
+// g o f: apply f first, then g.
+__device__ __forceinline__ uint32_t tf_compose(uint32_t f, uint32_t g) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    uint32_t fc = (f >> (2 * c)) & 3u;
+    r |= ((g >> (2 * fc)) & 3u) << (2 * c);
+  }
+  return r;
+}
+__device__ __forceinline__ int tf_apply(uint32_t f, int c) {
+  return int((f >> (2 * (c + 1))) & 3u) - 1;
+}
+
+// Small fast divider for runtime-constant uint32 divisors (n < 2^31).
+struct FastDiv {
+  uint32_t d, m, s;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  uint32_t s = 0;
+  while ((1ull << s) < d) ++s;
+  f.s = s;
+  // m = floor(2^32 * (2^s - d) / d) + 1
+  f.m = uint32_t(((1ull << 32) * ((1ull << s) - d)) / d + 1);
+  return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
+  if (f.s == 0) return x;  // d == 1
+  uint32_t t = __umulhi(x, f.m);
+  return (t + ((x - t) >> 1)) >> (f.s - 1);
+}
+
+}  // namespace tmg

@@ -1,0 +1,327 @@
+// Fused single-CTA product kernel for transform lengths that fit in shared
+// memory (L <= kSmallMaxL).  One CTA computes one whole product:
+//   limbs -> balanced chunks (block carry scan) -> pre-map -> forward FFT of
+//   z = a + i c -> spectral product -> half-length inverse FFT -> post-map ->
+//   rounding tripwire -> recombination with a block carry scan -> limbs.
+// A grid of CTAs runs a batch of independent products of the same size in
+// one launch (the batched configuration).
+//
+// Reference path: products_f64.cpp:106-171 end to end.
+#include "kernels.cuh"
+
+namespace tmg {
+
+namespace {
+
+__device__ __forceinline__ uint64_t window_smem(const uint64_t* limbs,
+                                                int64_t nlimbs, int64_t pos,
+                                                int b) {
+  const uint64_t mask = (b >= 64) ? ~0ull : ((1ull << b) - 1);
+  int64_t idx = pos >> 6;
+  uint32_t sh = uint32_t(pos & 63);
+  uint64_t lo = (idx >= 0 && idx < nlimbs) ? limbs[idx] : 0;
+  uint64_t hi = (idx + 1 >= 0 && idx + 1 < nlimbs) ? limbs[idx + 1] : 0;
+  uint64_t w = (sh == 0) ? lo : ((lo >> sh) | (hi << (64 - sh)));
+  return w & mask;
+}
+
+constexpr int kMaxPer = 18;  // values per thread held across a barrier
+
+}  // namespace
+
+__global__ void __launch_bounds__(512, 1)
+k_small_product(SmallArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int64_t L = a.L;
+  const MapConsts& mc = a.mc;
+  const int b = mc.b;
+  const int64_t N = mc.N;
+
+  double2* buf = reinterpret_cast<double2*>(smem_raw);
+  uint64_t* ul = reinterpret_cast<uint64_t*>(buf + padded_len(uint32_t(L)));
+  uint64_t* vl = ul + a.nlimbs;
+  uint32_t* sw = reinterpret_cast<uint32_t*>(vl + a.nlimbs);  // 32 words
+  double* sd = reinterpret_cast<double*>(sw + 32);             // scalars
+
+  const uint64_t* gu = a.u + int64_t(blockIdx.x) * a.nlimbs;
+  const uint64_t* gv = a.v + int64_t(blockIdx.x) * a.nlimbs;
+  uint64_t* gout = a.out + int64_t(blockIdx.x) * a.out_limbs;
+
+  // 1. operand limbs -> smem; operand range check (bits at/after n).
+  uint32_t flags = 0;
+  for (int64_t i = tid; i < a.nlimbs; i += nthr) {
+    uint64_t x = __ldg(gu + i), y = __ldg(gv + i);
+    ul[i] = x;
+    vl[i] = y;
+    if (i == a.nlimbs - 1 && (a.n & 63)) {
+      uint64_t hm = ~0ull << (a.n & 63);
+      if ((x & hm) | (y & hm)) flags |= kFlagInputRange;
+    }
+  }
+  __syncthreads();
+
+  // 2. balanced split: chunk windows, carry scan over the block.
+  const int64_t count = a.count;
+  const int64_t cpt = (count + nthr - 1) / nthr;
+  const int64_t c0 = int64_t(tid) * cpt;
+  const int64_t c1 = min(count, c0 + cpt);
+  uint32_t fu = kTfIdentity, fv = kTfIdentity;
+  for (int64_t j = c0; j < c1 && j < count - 1; ++j) {
+    uint64_t wu = window_smem(ul, a.nlimbs, j * b - a.lead, b);
+    uint64_t wv = window_smem(vl, a.nlimbs, j * b - a.lead, b);
+    fu = tf_compose(fu, split_tf(wu, b));
+    fv = tf_compose(fv, split_tf(wv, b));
+  }
+  uint32_t aggu, aggv;
+  uint32_t exu = block_scan_tf(fu, sw, &aggu);
+  uint32_t exv = block_scan_tf(fv, sw, &aggv);
+  {
+    int cu = tf_apply(exu, 0), cv = tf_apply(exv, 0);
+    for (int64_t j = c0; j < c1; ++j) {
+      uint64_t wu = window_smem(ul, a.nlimbs, j * b - a.lead, b);
+      uint64_t wv = window_smem(vl, a.nlimbs, j * b - a.lead, b);
+      bool top = (j == count - 1);
+      double du = double(split_digit(wu, cu, b, top));
+      double dv = double(split_digit(wv, cv, b, top));
+      cu = tf_apply(split_tf(wu, b), cu);
+      cv = tf_apply(split_tf(wv, b), cv);
+      if (j < L) buf[padidx(uint32_t(j))] = make_double2(du, dv);
+      if (mc.mode == kModeHigh && top) {
+        sd[0] = du;
+        sd[1] = dv;
+      }
+    }
+    // zero padding of the full product (chunks N..2N-1)
+    for (int64_t j = count + tid; j < L; j += nthr)
+      buf[padidx(uint32_t(j))] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+
+  // 3. pre-map (low: alpha*, high: gamma+ and root channel).
+  if (mc.mode != kModeFull) {
+    if (mc.mode == kModeHigh && tid == 0) {
+      double tu = sd[0], tv = sd[1];
+      auto Du = [&](int64_t i) { return buf[padidx(uint32_t(i))].x; };
+      auto Dv = [&](int64_t i) { return buf[padidx(uint32_t(i))].y; };
+      sd[2] = root_channel(mc, Du, tu) * root_channel(mc, Dv, tv);
+    }
+    double2 nv[kMaxPer];
+    const double tu = (mc.mode == kModeHigh) ? sd[0] : 0.0;
+    const double tv = (mc.mode == kModeHigh) ? sd[1] : 0.0;
+    auto Du = [&](int64_t i) { return buf[padidx(uint32_t(i))].x; };
+    auto Dv = [&](int64_t i) { return buf[padidx(uint32_t(i))].y; };
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k) {
+      int64_t j = tid + int64_t(k) * nthr;
+      if (j < N) nv[k] = make_double2(premap(mc, Du, j, tu), premap(mc, Dv, j, tv));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k) {
+      int64_t j = tid + int64_t(k) * nthr;
+      if (j < N) buf[padidx(uint32_t(j))] = nv[k];
+    }
+    __syncthreads();
+  }
+
+  // 4. forward FFT of z = a + i c, length L.
+  LayRows lay1{1u, 0u};
+  fft_smem<false>(buf, lay1, a.fwd, tid, nthr);
+
+  // 5. spectral product: W_k = (Z_k + conj Z_-k)(Z_k - conj Z_-k)/(4i L),
+  //    then Y_k = (W_k + W_{k+L/2}) + i e^{2 pi i k/L}(W_k - W_{k+L/2}).
+  const uint32_t H = uint32_t(L / 2);
+  for (uint32_t k = tid; k <= H; k += nthr) {
+    uint32_t k2 = (k == 0) ? 0 : uint32_t(L) - k;
+    double2 z1 = buf[padidx(k)], z2 = buf[padidx(k2)];
+    double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
+    double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
+    double2 pq = cmul(p, q);
+    double2 w = make_double2(pq.y * a.scale, -pq.x * a.scale);  // -i * pq * s
+    buf[padidx(k)] = w;
+    if (k2 != k) buf[padidx(k2)] = cconj(w);
+  }
+  __syncthreads();
+  for (uint32_t k = tid; k < H; k += nthr) {
+    double2 w1 = buf[padidx(k)], w2 = buf[padidx(k + H)];
+    double2 e = cadd(w1, w2);
+    double2 o = cmulc(csub(w1, w2), __ldg(a.fwd.tw + k));  // * e^{+2 pi i k/L}
+    buf[padidx(k)] = make_double2(e.x - o.y, e.y + o.x);
+  }
+  __syncthreads();
+
+  // 6. inverse FFT of length L/2: y_m = w_{2m} + i w_{2m+1}.
+  fft_smem<true>(buf, lay1, a.inv, tid, nthr);
+
+  // 7. post-map and rounding.
+  auto W = [&](int64_t j) {
+    double2 y = buf[padidx(uint32_t(j >> 1))];
+    return (j & 1) ? y.y : y.x;
+  };
+  const int64_t M = (mc.mode == kModeFull) ? L : (mc.mode == kModeLow ? N : N + 1);
+  double psi = 0.0;
+  if (mc.mode == kModeHigh) psi = high_psi(mc, W, sd[2]);
+  RoundAcc ra;
+  long long cv[kMaxPer];
+#pragma unroll
+  for (int k = 0; k < kMaxPer; ++k) {
+    int64_t i = tid + int64_t(k) * nthr;
+    if (i < M) {
+      double x;
+      if (mc.mode == kModeFull) x = W(i);
+      else if (mc.mode == kModeLow) x = postmap_low(mc, W, i);
+      else x = postmap_high(mc, W, i, psi);
+      cv[k] = ra.round(x);
+    }
+  }
+  __syncthreads();
+  long long* cb = reinterpret_cast<long long*>(buf);
+#pragma unroll
+  for (int k = 0; k < kMaxPer; ++k) {
+    int64_t i = tid + int64_t(k) * nthr;
+    if (i < M) cb[i] = cv[k];
+  }
+  flags |= ra.flags;
+  // block max of errors
+  {
+    double e = ra.max_err, m = ra.max_abs;
+    for (int off = 16; off > 0; off >>= 1) {
+      e = fmax(e, __shfl_xor_sync(0xffffffffu, e, off));
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    }
+    if ((tid & 31) == 0) status_merge(a.status, e, m, 0);
+  }
+  __syncthreads();
+
+  // 8. recombination e_k at bit k*b, k < K.
+  const int64_t K = a.K;
+  long long c0v = cb[0];
+  if (mc.mode == kModeLow && tid == 0) {
+    if (c0v & ((1ll << b) - 1)) flags |= kFlagLowNotDivisible;
+  }
+  auto E = [&](int64_t k) -> long long {
+    if (mc.mode == kModeLow) {
+      long long e = cb[k + 1];
+      if (k == 0) e += (c0v >> b);
+      return e;
+    }
+    return cb[k];
+  };
+  uint64_t* vlimb = reinterpret_cast<uint64_t*>(cb + M + 1);
+  const int64_t ML = a.ML;
+  const int64_t lpt = (ML + nthr - 1) / nthr;
+  const int64_t m0 = int64_t(tid) * lpt;
+  const int64_t m1 = min(ML, m0 + lpt);
+  const int s_sh = a.shift_s;
+  const int npass = (mc.mode == kModeHigh) ? 2 : 1;
+  __int128 delta = 0;  // high: 2^{s-1} - 1 + (bit s of t)
+  for (int pass = 0; pass < npass; ++pass) {
+    auto lane = [&](int64_t m) -> __int128 {
+      __int128 v = lane_value(E, m, b, K);
+      if (pass == 1 && m >= 0 && m <= 1) {
+        // add the rounding constant delta limbwise into lanes 0 and 1
+        unsigned long long d = (m == 0) ? (unsigned long long)delta
+                                        : (unsigned long long)(delta >> 64);
+        v += (__int128)d;
+      }
+      return v;
+    };
+    uint32_t f = kTfIdentity;
+    __int128 prev = lane(m0 - 1);
+    for (int64_t m = m0; m < m1; ++m) {
+      __int128 cur = lane(m);
+      __int128 s = (__int128)(unsigned long long)cur + (prev >> 64);
+      f = tf_compose(f, limb_tf(s, flags));
+      prev = cur;
+    }
+    uint32_t agg;
+    uint32_t ex = block_scan_tf(f, sw, &agg);
+    int c = tf_apply(ex, 0);
+    prev = lane(m0 - 1);
+    for (int64_t m = m0; m < m1; ++m) {
+      __int128 cur = lane(m);
+      __int128 s = (__int128)(unsigned long long)cur + (prev >> 64);
+      uint32_t tfm = limb_tf(s, flags);
+      vlimb[m] = (unsigned long long)(s + c);
+      c = tf_apply(tfm, c);
+      prev = cur;
+    }
+    if (m1 == ML && m0 < m1) {
+      // final carry out of the top limb: the sign of V
+      sd[4] = double(c);
+    }
+    __syncthreads();
+    if (pass == 0 && npass == 2) {
+      if (tid == 0) {
+        uint64_t lw = vlimb[s_sh >> 6];
+        int bit = int((lw >> (s_sh & 63)) & 1);
+        __int128 dd = ((__int128)1 << (s_sh - 1)) - 1 + bit;
+        sd[5] = 0.0;
+        reinterpret_cast<unsigned long long*>(sd)[6] = (unsigned long long)dd;
+        reinterpret_cast<unsigned long long*>(sd)[7] = (unsigned long long)(dd >> 64);
+      }
+      __syncthreads();
+      delta = (__int128)reinterpret_cast<unsigned long long*>(sd)[6] |
+              ((__int128)reinterpret_cast<unsigned long long*>(sd)[7] << 64);
+      __syncthreads();
+    }
+  }
+  const int sign = int(sd[4]);
+
+  // 9. outputs and range checks.
+  const int64_t OL = a.out_limbs;
+  uint32_t topbit = 0, lownz = 0;
+  if (mc.mode == kModeFull) {
+    if (tid == 0 && sign < 0) flags |= kFlagNegative;
+    const int64_t nb2 = 2 * a.n;  // product bits
+    for (int64_t m = tid; m < ML; m += nthr) {
+      uint64_t x = vlimb[m];
+      if (m < OL) {
+        if (m == OL - 1 && (nb2 & 63) && (x >> (nb2 & 63))) flags |= kFlagFullOverflow;
+        gout[m] = x;
+      } else if (x) {
+        flags |= kFlagFullOverflow;
+      }
+    }
+    for (int64_t m = ML + tid; m < OL; m += nthr) gout[m] = 0;
+  } else if (mc.mode == kModeLow) {
+    for (int64_t m = tid; m < OL; m += nthr) {
+      uint64_t x = m < ML ? vlimb[m] : 0;
+      if (m == OL - 1 && (a.n & 63)) x &= (1ull << (a.n & 63)) - 1;
+      gout[m] = x;
+    }
+  } else {
+    // w = V' >> s must lie in [0, 2^n]
+    if (tid == 0 && sign < 0) flags |= kFlagHighRange;
+    const int64_t q = s_sh >> 6;
+    const int r = s_sh & 63;
+    const int64_t nw = ML - q;
+    for (int64_t m = tid; m < max(nw, OL); m += nthr) {
+      uint64_t x = 0;
+      if (m < nw) {
+        uint64_t lo = vlimb[m + q];
+        uint64_t hi = (m + q + 1 < ML) ? vlimb[m + q + 1] : (sign < 0 ? ~0ull : 0ull);
+        x = r ? ((lo >> r) | (hi << (64 - r))) : lo;
+      }
+      high_classify(x, m, a.n, topbit, lownz, flags);
+      if (m < OL) gout[m] = x & high_mask(m, OL, a.n);
+    }
+  }
+  // block-combine flags; the high range test needs both bits of the block
+  __syncthreads();
+  if (tid == 0) { sw[0] = 0; sw[1] = 0; sw[2] = 0; }
+  __syncthreads();
+  if (topbit) atomicOr(&sw[0], 1u);
+  if (lownz) atomicOr(&sw[1], 1u);
+  if (flags) atomicOr(&sw[2], flags);
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t f = sw[2];
+    if (sw[0] && sw[1]) f |= kFlagHighRange;
+    if (a.pflags) a.pflags[blockIdx.x] = f;
+    if (f) atomicOr(&a.status->flags, f);
+  }
+}
+
+}  // namespace tmg

@@ -1,0 +1,155 @@
+// Kernel argument blocks and declarations.
+#pragma once
+
+#include "common.cuh"
+#include "digits.cuh"
+#include "fft_smem.cuh"
+#include "pipeline.cuh"
+
+namespace tmg {
+
+// Transform lengths up to this run as one fused CTA per product.
+constexpr int64_t kSmallMaxL = 8192;
+
+struct SmallArgs {
+  const uint64_t* u;  // batch of operands, nlimbs words each
+  const uint64_t* v;
+  uint64_t* out;      // batch of outputs, out_limbs words each
+  uint32_t* pflags;   // per-product flag words (may be null)
+  int64_t nlimbs;
+  int64_t n;
+  int64_t out_limbs;
+  int64_t L;      // transform length
+  int64_t count;  // chunks per operand
+  int64_t lead;   // high split shift sigma
+  int64_t K;      // recombination coefficients
+  int64_t ML;     // limbs scanned
+  int32_t shift_s;
+  double scale;   // 1 / (4 L)
+  SubFft fwd;     // length L
+  SubFft inv;     // length L / 2
+  MapConsts mc;
+  DevStatus* status;
+};
+
+size_t small_smem_bytes(int64_t L, int64_t nlimbs);
+
+__global__ void k_small_product(SmallArgs a);
+
+// ---------------------------------------------------------------------------
+// Multi-pass pipeline.  The complex transform of length L = A * B * C runs as
+// column passes over A (and B) and a row pass over C (the "mid" kernel, which
+// also forms the spectral product and starts the inverse).
+
+struct ScanState {
+  unsigned long long* state;  // per-block look-back words
+  unsigned long long* ctr;    // [0] ticket, [1] done
+  uint32_t epoch;
+};
+
+struct SplitScanArgs {
+  const uint64_t* u;
+  const uint64_t* v;
+  int64_t nlimbs;
+  int64_t n;
+  int32_t b;
+  int64_t count;
+  int64_t lead;
+  uint32_t* cbits_u;  // carry-in bit per chunk
+  uint32_t* cbits_v;
+  ScanState scan_u, scan_v;
+  DevStatus* status;
+};
+constexpr int kSplitThreads = 256;
+constexpr int kSplitPerThread = 16;  // chunks per thread
+__global__ void k_split_scan(SplitScanArgs a);
+
+// Column pass geometry: element (outer, row, col) at
+//   outer * os + row * rs + (col / cw) * cs + (col % cw)
+struct ColGeom {
+  int64_t os, rs, cs;
+  uint32_t cw;
+  uint32_t ncols;  // columns per outer matrix
+};
+
+struct F1Args {
+  const uint64_t* u;
+  const uint64_t* v;
+  int64_t nlimbs;
+  int32_t b;
+  int64_t count;
+  int64_t lead;
+  const uint32_t* cbits_u;
+  const uint32_t* cbits_v;
+  double2* out;    // T[k_a][col], row length ncols
+  uint32_t ncols;  // = L / A
+  uint32_t logc;   // columns per CTA = 2^logc
+  SubFft fft;      // length A
+  TwGlobal tw;     // omega_L
+  MapConsts mc;
+  double* aux;     // high: [0] theta_u*theta_v
+};
+__global__ void k_f1(F1Args a);
+
+struct ColArgs {
+  double2* data;  // in place
+  ColGeom g;
+  uint32_t logc;
+  SubFft fft;
+  TwGlobal tw;       // omega_L
+  int32_t inv;       // inverse transform
+  // twiddle after the DFT: omega_L^{((outer * to + col * tc) * k) * tmul}
+  uint32_t to, tc, tmul;
+};
+__global__ void k_col(ColArgs a);
+
+struct MidArgs {
+  double2* data;  // rows of length C at storage index (k_a * B + k_b) * C
+  uint32_t A, B, C;
+  SubFft fwd;   // length C
+  SubFft inv;   // length C / 2
+  TwGlobal tw;  // omega_L
+  uint32_t L;
+  double scale;  // 1 / (4 L)
+};
+__global__ void k_mid(MidArgs a);
+
+struct ILastArgs {
+  const double2* data;  // S[k_a][...] with geometry g (outer = 0)
+  double2* coef;        // y_m = (w_2m, w_2m+1), m = col + ncols * m_a
+  ColGeom g;
+  uint32_t logc;
+  SubFft fft;  // length A (inverse)
+};
+__global__ void k_ilast(ILastArgs a);
+
+struct CarryArgs {
+  const double* w;  // convolution coefficients (L of them)
+  uint64_t* out;
+  int64_t n;
+  int64_t out_limbs;
+  int64_t K;
+  int64_t ML;
+  int32_t shift_s;
+  MapConsts mc;
+  const double* aux;
+  ScanState scan;
+  DevStatus* status;
+  // high: delta resolution
+  unsigned long long* hstate;  // [0] epoch-tagged delta words
+};
+constexpr int kCarryThreads = 256;
+constexpr int kCarryPerThread = 4;
+__global__ void k_carry(CarryArgs a);
+
+// Schoolbook product for operands below the pipeline cutoff (the reference's
+// ORACLE_FALLBACK mode, products.hpp:14-15).
+struct BaseArgs {
+  const uint64_t* u;
+  const uint64_t* v;
+  uint64_t* prod;  // 2 * nlimbs words
+  int64_t nlimbs;
+};
+__global__ void k_basecase(BaseArgs a);
+
+}  // namespace tmg

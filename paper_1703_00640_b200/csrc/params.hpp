@@ -1,0 +1,64 @@
+// Parameter selection for the three products.
+//
+// select_params_reference restates the reference selector
+// (/root/reference/proj/core/src/params.cpp:26-200) line for line: the FP64
+// budget 3b + lg(N)/2 <= 50.5 (2b + lg(2N)/2 for the full product), the
+// covering constraints, and the cheapest 2357-smooth length in the
+// [n/b, 1.15 n/b] window under its CPU transform-cost proxy.
+//
+// select_params_accurate keeps that structure but (1) also requires the
+// predicted standard deviation of the FP64 convolution error to stay below
+// 0.25/7, so the reference's own 0.25 rounding tripwire is not expected to
+// fire (at n = 2^26 the reference choice b = 13 for low/high measures a max
+// error of 0.35 with a correctly rounded double FFT), and
+// (2) ranks candidate lengths by the GPU cost model (bytes moved ~ L).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace tmg {
+
+enum class PMode : int32_t { kFull = 0, kLow = 1, kHigh = 2, kOracleFallback = 3 };
+enum class Backend : int32_t { kExact = 0, kFft = 1 };
+enum class Policy : int32_t { kReference = 0, kAccurate = 1 };
+
+struct Params {
+  int64_t n = 0;
+  int32_t b = 0;
+  int64_t N = 0;
+  int64_t lambda = 0;
+  int32_t p = 0;
+  PMode mode = PMode::kFull;
+  Backend backend = Backend::kExact;
+  bool signed_split = false;
+};
+
+// Error carrying one of the TMG_ERR_* codes.
+class Error : public std::runtime_error {
+ public:
+  Error(int code, const std::string& what) : std::runtime_error(what), code_(code) {}
+  int code() const { return code_; }
+
+ private:
+  int code_;
+};
+
+constexpr int64_t kDefaultFallbackCutoff = 4096;
+
+bool factor_2357(uint64_t n, std::array<uint32_t, 4>& exps);
+bool is_2357_smooth(uint64_t n);
+int32_t lg_ceil(uint64_t n);
+
+int32_t required_precision(PMode mode, int32_t b, int64_t N);
+int64_t default_lambda(PMode mode, Backend backend, int32_t b, int32_t p);
+void validate_params(const Params& params);
+Params select_params(int64_t n, PMode mode, Backend backend,
+                     int64_t fallback_cutoff, Policy policy);
+double predicted_sigma(PMode mode, int32_t b, int64_t N);
+int64_t transform_length(PMode mode, int64_t N);
+int64_t output_limbs(PMode mode, int64_t n);
+
+}  // namespace tmg

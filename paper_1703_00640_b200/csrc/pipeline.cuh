@@ -1,0 +1,294 @@
+// Pieces of the product pipeline shared by the fused single-CTA kernel and
+// the multi-pass kernels: pre-map, post-map, rounding with the reference's
+// tripwire, recombination lanes and carry transfer functions.
+#pragma once
+
+#include "common.cuh"
+#include "digits.cuh"
+
+namespace tmg {
+
+enum Mode : int32_t { kModeFull = 0, kModeLow = 1, kModeHigh = 2 };
+
+// ----------------------------------------------------------------------------
+// Pre-map (alpha* for low, gamma+ for high) at transform index j < N.
+// D(i) returns the balanced digit of chunk i (0 <= i < N); top is chunk N of
+// the high split.  Mirrors apply_series (maps_f64.cpp:48-96) plus the
+// gamma-dagger fold of the top coefficient (maps_f64.cpp:337-347).
+template <class DF>
+__device__ __forceinline__ double premap(const MapConsts& mc, const DF& D,
+                                         int64_t j, double top) {
+  const int64_t N = mc.N;
+  const double Nd = double(N);
+  const int fam = (mc.mode == kModeLow) ? 0 : 2;
+  double acc = 0.0;
+  for (int r = 0; r < mc.lambda; ++r) {
+    int64_t k = j - r;
+    if (k < 0) k += N;
+    double d = D(k);
+    acc += d * series_coef(fam, r, double(k), Nd, mc.cpre[r]);
+  }
+  if (mc.mode == kModeHigh && top != 0.0) {
+    // out[(k + r) mod N] += top * fold[k] * gamma_r(k), k < nfold
+    for (int r = 0; r < mc.lambda; ++r) {
+      int64_t k = j - r;
+      if (k < 0) k += N;
+      if (k < mc.nfold) {
+        acc += top * mc.fold[k] * series_coef(2, r, double(k), Nd, mc.cpre[r]);
+      }
+    }
+  }
+  return acc;
+}
+
+// Root-channel value of a high-split operand (maps_f64.cpp:319-328):
+// theta = sum_d in[N - d] * inv_root^d over the first nroot terms.
+template <class DF>
+__device__ __forceinline__ double root_channel(const MapConsts& mc,
+                                               const DF& D, double top) {
+  double acc = 0.0;
+  for (int d = 0; d < mc.nroot && d <= mc.N; ++d) {
+    double x = (d == 0) ? top : D(mc.N - d);
+    acc += x * mc.ipow[d];
+  }
+  return acc;
+}
+
+// ----------------------------------------------------------------------------
+// Post-map.  W(j) returns convolution coefficient j (0 <= j < N).
+// flat(j) = sum_r W(j - r) * post_r(j - r) for the r keeping j - r in [0, N)
+// (apply_series_flat, maps_f64.cpp:175-187).
+template <class WF>
+__device__ __forceinline__ double post_flat(const MapConsts& mc, const WF& W,
+                                            int64_t j) {
+  const int64_t N = mc.N;
+  const int fam = (mc.mode == kModeLow) ? 1 : 3;
+  int64_t rlo = j - N + 1;
+  if (rlo < 0) rlo = 0;
+  int64_t rhi = mc.lambda - 1;
+  if (rhi > j) rhi = j;
+  double acc = 0.0;
+  for (int64_t r = rlo; r <= rhi; ++r) {
+    int64_t k = j - r;
+    acc += W(k) * series_coef(fam, int(r), double(k), double(N), mc.cpost[r]);
+  }
+  return acc;
+}
+
+// beta* value at index i < N (beta_star_view_f64, maps_f64.cpp:269-281),
+// returned pre-multiplied by 2^b.
+template <class WF>
+__device__ __forceinline__ double postmap_low(const MapConsts& mc, const WF& W,
+                                              int64_t i) {
+  const int64_t N = mc.N;
+  double v = post_flat(mc, W, i);
+  if (i <= mc.lambda - 2) v += post_flat(mc, W, i + N);
+  if (i >= 1 && i <= mc.lambda - 1) v -= post_flat(mc, W, i + N - 1) * mc.step;
+  return v * mc.scale_out;
+}
+
+// Folded buffer of delta-dagger before differencing (maps_f64.cpp:355-362).
+template <class WF>
+__device__ __forceinline__ double high_buf(const MapConsts& mc, const WF& W,
+                                           int64_t i) {
+  const int64_t N = mc.N;
+  double v = post_flat(mc, W, i);
+  for (int64_t j = N + mc.lambda - 2; j >= N; --j) {
+    int64_t o = i - (j - N);
+    if (o >= 0 && o < mc.nfold) v += post_flat(mc, W, j) * mc.fold[o];
+  }
+  return v;
+}
+
+// psi of delta-dagger (maps_f64.cpp:363-371); aux = theta_u * theta_v.
+template <class WF>
+__device__ __forceinline__ double high_psi(const MapConsts& mc, const WF& W,
+                                           double aux) {
+  double hrho = 0.0;
+  for (int d = 1; d <= mc.nhrho && d <= mc.N; ++d)
+    hrho += high_buf(mc, W, mc.N - d) * mc.ipow[d];
+  return (aux - hrho * mc.root_neg_n) / mc.cofactor_scaled;
+}
+
+// delta-dagger value at i in [0, N], pre-multiplied by 2^b
+// (maps_f64.cpp:372-383).
+template <class WF>
+__device__ __forceinline__ double postmap_high(const MapConsts& mc,
+                                               const WF& W, int64_t i,
+                                               double psi) {
+  const int64_t N = mc.N;
+  double v;
+  if (i == N) {
+    v = psi - high_buf(mc, W, N - 1) * mc.step;
+  } else if (i == 0) {
+    v = high_buf(mc, W, 0);
+  } else {
+    v = high_buf(mc, W, i) - high_buf(mc, W, i - 1) * mc.step;
+  }
+  if (i < mc.nfold) v -= psi * mc.fold[i];
+  return v * mc.scale_out;
+}
+
+// ----------------------------------------------------------------------------
+// Rounding with the reference tripwire (products_f64.cpp:16-27): a value is
+// refused when |x| >= 2^53 (or NaN) or when it sits farther than a quarter
+// from the nearest integer.  Returns the rounded integer.
+struct RoundAcc {
+  double max_err = 0.0;
+  double max_abs = 0.0;
+  uint32_t flags = 0;
+  __device__ __forceinline__ long long round(double x) {
+    double ax = fabs(x);
+    if (!(ax < 9007199254740992.0)) {
+      flags |= kFlagOverflow;
+      max_abs = fmax(max_abs, isnan(ax) ? 1e308 : ax);
+      return 0;
+    }
+    double r = rint(x);
+    double e = fabs(x - r);
+    max_err = fmax(max_err, e);
+    max_abs = fmax(max_abs, ax);
+    if (e > 0.25) flags |= kFlagTripwire;
+    return (long long)r;
+  }
+};
+
+__device__ __forceinline__ void status_merge(DevStatus* st, double max_err,
+                                             double max_abs, uint32_t flags) {
+  atomicMax(&st->max_err_bits, (unsigned long long)__double_as_longlong(max_err));
+  atomicMax(&st->max_abs_bits, (unsigned long long)__double_as_longlong(max_abs));
+  if (flags) atomicOr(&st->flags, flags);
+}
+
+// ----------------------------------------------------------------------------
+// Recombination lanes.  Value V = sum_k e_k 2^{k b}; lane m collects the e_k
+// whose bit offset falls in limb m: lane_m = sum e_k << (k b - 64 m), a
+// signed 128-bit quantity (SignedAccumulator, products_f64.cpp:36-66).
+template <class EF>
+__device__ __forceinline__ __int128 lane_value(const EF& E, int64_t m, int b,
+                                               int64_t K) {
+  if (m < 0) return 0;
+  int64_t klo = (64 * m + b - 1) / b;
+  int64_t khi = (64 * m + 64 + b - 1) / b;  // exclusive
+  if (khi > K) khi = K;
+  __int128 acc = 0;
+  for (int64_t k = klo; k < khi; ++k) {
+    int sh = int(k * b - 64 * m);
+    acc += (__int128)E(k) << sh;
+  }
+  return acc;
+}
+
+// Transfer function of limb m with s = lo(lane_m) + hi(lane_{m-1}).
+// f(c) = floor((s + c) / 2^64) for c in {-1, 0, 1}.
+__device__ __forceinline__ uint32_t limb_tf(__int128 s, uint32_t& flags) {
+  long long hi = (long long)(s >> 64);
+  unsigned long long lo = (unsigned long long)s;
+  int fm = int(hi) - (lo == 0 ? 1 : 0);
+  int f0 = int(hi);
+  int fp = int(hi) + (lo == ~0ull ? 1 : 0);
+  if (hi < -1 || hi > 1 || fm < -1 || fp > 1) {
+    flags |= kFlagCarryRange;
+    fm = f0 = fp = 0;
+  }
+  return uint32_t(fm + 1) | (uint32_t(f0 + 1) << 2) | (uint32_t(fp + 1) << 4);
+}
+
+// High product range bookkeeping (products_f64.cpp:167-169): w must lie in
+// [0, 2^n].  Limb m of w is split into the bits below n, bit n, and above n.
+__device__ __forceinline__ void high_classify(uint64_t x, int64_t m, int64_t n,
+                                              uint32_t& topbit,
+                                              uint32_t& lownz,
+                                              uint32_t& flags) {
+  const int64_t bit0 = 64 * m;
+  uint64_t below = 0, atn = 0, above = 0;
+  if (bit0 + 64 <= n) {
+    below = x;
+  } else if (bit0 > n) {
+    above = x;
+  } else {
+    const int o = int(n - bit0);  // 0..63
+    below = o ? (x & ((1ull << o) - 1)) : 0;
+    atn = (x >> o) & 1ull;
+    above = (o == 63) ? 0 : (x >> (o + 1));
+  }
+  if (below) lownz = 1;
+  if (atn) topbit = 1;
+  if (above) flags |= kFlagHighRange;
+}
+__device__ __forceinline__ uint64_t high_mask(int64_t m, int64_t OL,
+                                              int64_t n) {
+  if (m != OL - 1) return ~0ull;
+  const int r = int((n + 1) & 63);
+  return r ? ((1ull << r) - 1) : ~0ull;
+}
+
+// ----------------------------------------------------------------------------
+// Block-wide exclusive scan of transfer functions (blockDim % 32 == 0).
+// Returns the exclusive prefix of this thread; *agg gets the block total.
+__device__ __forceinline__ uint32_t block_scan_tf(uint32_t f, uint32_t* sw,
+                                                  uint32_t* agg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  uint32_t inc = f;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc = tf_compose(o, inc);
+  }
+  uint32_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) excl = kTfIdentity;
+  __syncthreads();
+  if (lane == 31) sw[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t v = lane < nw ? sw[lane] : kTfIdentity;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      uint32_t o = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= off) v = tf_compose(o, v);
+    }
+    sw[lane] = v;
+  }
+  __syncthreads();
+  uint32_t wex = warp > 0 ? sw[warp - 1] : kTfIdentity;
+  *agg = sw[nw - 1];
+  __syncthreads();
+  return tf_compose(wex, excl);
+}
+
+// Decoupled look-back over per-block aggregates (one thread per block).
+// state words: [63:32] epoch, [31:30] flag (1 aggregate, 2 inclusive),
+// [5:0] payload (transfer code, or carry + 1 for inclusive).
+__device__ __forceinline__ int lookback_carry(unsigned long long* state,
+                                              uint32_t blk, uint32_t agg,
+                                              uint32_t epoch) {
+  const unsigned long long ep = (unsigned long long)epoch << 32;
+  int carry_in = 0;
+  if (blk == 0) {
+    carry_in = 0;
+  } else {
+    *(volatile unsigned long long*)(state + blk) = ep | (1ull << 30) | agg;
+    uint32_t E = kTfIdentity;
+    int64_t j = int64_t(blk) - 1;
+    while (true) {
+      unsigned long long w = *(volatile unsigned long long*)(state + j);
+      if ((w >> 32) != epoch) continue;
+      uint32_t flag = uint32_t(w >> 30) & 3u;
+      if (flag == 0) continue;
+      uint32_t pay = uint32_t(w) & 63u;
+      if (flag == 2) {
+        carry_in = tf_apply(E, int(pay) - 1);
+        break;
+      }
+      E = tf_compose(pay, E);
+      --j;
+    }
+  }
+  int out = tf_apply(agg, carry_in);
+  *(volatile unsigned long long*)(state + blk) =
+      ep | (2ull << 30) | uint64_t(out + 1);
+  return carry_in;
+}
+
+}  // namespace tmg

@@ -1,0 +1,385 @@
+// Host-side plan construction: transform shape, radix schedules, exact
+// twiddle tables, map constants (maps_f64.cpp:192-245 of the reference).
+#include "plan.hpp"
+
+#include <cmath>
+#include <cstring>
+
+#include "../../include/truncmul_b200.h"
+
+namespace tmg {
+
+#define TMG_CUDA(call)                                                     \
+  do {                                                                     \
+    cudaError_t e_ = (call);                                               \
+    if (e_ != cudaSuccess)                                                 \
+      throw Error(TMG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+
+void DevBuf::ensure(size_t nbytes) {
+  if (nbytes <= bytes) return;
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+  TMG_CUDA(cudaMalloc(&p, nbytes));
+  bytes = nbytes;
+}
+
+namespace {
+
+// e^{-2 pi i x / R} in long double with octant reduction, rounded once.
+void twiddle(uint64_t x, uint64_t R, double* re, double* im) {
+  x %= R;
+  const unsigned __int128 t = (unsigned __int128)x * 8u;
+  const uint64_t o = uint64_t(t / R);
+  const uint64_t rem = uint64_t(t - (unsigned __int128)o * R);
+  const long double q = 0.785398163397448309615660845819875721L;  // pi/4
+  long double c, s;
+  if ((o & 1) == 0) {
+    long double th = (long double)rem / (long double)R * q;
+    long double ct = cosl(th), st = sinl(th);
+    switch (o) {
+      case 0: c = ct; s = st; break;
+      case 2: c = -st; s = ct; break;
+      case 4: c = -ct; s = -st; break;
+      default: c = st; s = -ct; break;  // 6
+    }
+  } else {
+    long double th = (long double)(R - rem) / (long double)R * q;
+    long double ct = cosl(th), st = sinl(th);
+    switch (o) {
+      case 1: c = st; s = ct; break;
+      case 3: c = -ct; s = st; break;
+      case 5: c = -st; s = -ct; break;
+      default: c = ct; s = -st; break;  // 7
+    }
+  }
+  *re = double(c);
+  *im = double(-s);
+}
+
+std::vector<double2> host_table(uint64_t L, uint64_t step, uint64_t count) {
+  std::vector<double2> t(count);
+  for (uint64_t i = 0; i < count; ++i) {
+    double re, im;
+    twiddle(i * step, L, &re, &im);
+    t[i] = make_double2(re, im);
+  }
+  return t;
+}
+
+std::vector<int> radix_schedule(uint32_t R) {
+  std::array<uint32_t, 4> e;
+  if (!factor_2357(R, e)) throw Error(TMG_ERR_UNSUPPORTED_LENGTH, "radix_schedule: not 2357-smooth");
+  std::vector<int> rad;
+  uint32_t e2 = e[0];
+  while (e2 >= 4) { rad.push_back(16); e2 -= 4; }
+  if (e2 == 3) rad.push_back(8);
+  if (e2 == 2) rad.push_back(4);
+  if (e2 == 1) rad.push_back(2);
+  for (uint32_t i = 0; i < e[1]; ++i) rad.push_back(3);
+  for (uint32_t i = 0; i < e[2]; ++i) rad.push_back(5);
+  for (uint32_t i = 0; i < e[3]; ++i) rad.push_back(7);
+  if (rad.size() > size_t(kMaxStages))
+    throw Error(TMG_ERR_UNSUPPORTED_LENGTH, "radix_schedule: too many stages");
+  return rad;
+}
+
+uint32_t largest_pow2_divisor(uint64_t x) {
+  uint32_t p = 1;
+  while (x % (uint64_t(p) * 2) == 0 && p < (1u << 30)) p *= 2;
+  return p;
+}
+
+// Columns per CTA for a column pass over length R with ncols columns.
+uint32_t pick_logc(uint32_t R, uint64_t ncols, size_t smem_cap) {
+  const uint32_t p2 = largest_pow2_divisor(ncols);
+  uint32_t best = 0;
+  for (uint32_t lc = 0; lc <= 6; ++lc) {
+    const uint32_t c = 1u << lc;
+    if (c > p2) break;
+    const uint64_t thr = (uint64_t(R) * c + 15) / 16;
+    const size_t smem = size_t(padded_len(R * c)) * 16;
+    if (thr > 512 || smem > smem_cap) break;
+    best = lc;
+    if (thr >= 256 && c >= 4) break;
+  }
+  return best;
+}
+
+int threads_for(uint64_t elems) {
+  uint64_t t = (elems + 15) / 16;
+  t = (t + 31) / 32 * 32;
+  if (t < 32) t = 32;
+  return int(t);
+}
+
+}  // namespace
+
+const double2* TwiddleCache::table(uint32_t R) {
+  auto it = tables_.find(R);
+  if (it != tables_.end()) return it->second->as<double2>();
+  auto h = host_table(R, 1, R);
+  auto buf = std::make_unique<DevBuf>();
+  buf->ensure(h.size() * sizeof(double2));
+  TMG_CUDA(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  const double2* p = buf->as<double2>();
+  tables_[R] = std::move(buf);
+  return p;
+}
+
+TwGlobal TwiddleCache::global(uint64_t L) {
+  auto it = glob_.find(L);
+  if (it == glob_.end()) {
+    uint32_t S = 0;
+    while ((uint64_t(1) << (2 * S)) < L) ++S;  // 2^S ~ sqrt(L)
+    const uint64_t nlo = uint64_t(1) << S;
+    const uint64_t nhi = (L + nlo - 1) / nlo;
+    auto lo = host_table(L, 1, nlo);
+    auto hi = host_table(L, nlo, nhi);
+    auto buf = std::make_unique<DevBuf>();
+    buf->ensure((nlo + nhi) * sizeof(double2));
+    TMG_CUDA(cudaMemcpy(buf->p, lo.data(), nlo * sizeof(double2), cudaMemcpyHostToDevice));
+    TMG_CUDA(cudaMemcpy(buf->as<double2>() + nlo, hi.data(), nhi * sizeof(double2),
+                        cudaMemcpyHostToDevice));
+    glob_S_[L] = S;
+    it = glob_.emplace(L, std::move(buf)).first;
+  }
+  TwGlobal g;
+  g.S = glob_S_[L];
+  g.lo = it->second->as<double2>();
+  g.hi = g.lo + (uint64_t(1) << g.S);
+  return g;
+}
+
+SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride) {
+  SubFft s;
+  std::memset(&s, 0, sizeof(s));
+  s.R = R;
+  s.tw = tw;
+  auto rad = radix_schedule(R);
+  s.nst = int32_t(rad.size());
+  uint32_t Ns = 1;
+  for (size_t i = 0; i < rad.size(); ++i) {
+    s.rad[i] = rad[i];
+    s.Ns[i] = Ns;
+    s.twstep[i] = R / (Ns * uint32_t(rad[i])) * tw_stride;
+    s.fdNs[i] = make_fastdiv(Ns);
+    Ns *= uint32_t(rad[i]);
+  }
+  return s;
+}
+
+MapConsts make_map_consts(const Params& p) {
+  MapConsts m;
+  std::memset(&m, 0, sizeof(m));
+  m.mode = int32_t(p.mode);
+  m.b = p.b;
+  m.N = p.N;
+  m.lambda = int32_t(p.lambda);
+  m.step = std::ldexp(1.0, -p.b);
+  m.scale_out = (p.mode == PMode::kFull) ? 1.0 : std::ldexp(1.0, p.b);
+  m.cofactor_scaled = 1.0;
+  if (p.mode == PMode::kFull) return m;
+  if (p.lambda > kMaxLambda) throw Error(TMG_ERR_UNSUPPORTED, "lambda above the GPU limit of 8");
+  // row scales sgn / (r! N^r 2^{rb}) (series.cpp:146-183 closed forms)
+  for (int r = 0; r < p.lambda; ++r) {
+    long double den = 1.0L;
+    for (int i = 1; i <= r; ++i) den *= (long double)i * (long double)p.N;
+    den = ldexpl(den, r * p.b);
+    const long double v = 1.0L / den;
+    const bool odd = (r & 1) != 0;
+    if (p.mode == PMode::kLow) {
+      m.cpre[r] = double(odd ? -v : v);   // alpha
+      m.cpost[r] = double(v);             // beta
+    } else {
+      m.cpre[r] = double(v);              // gamma
+      m.cpost[r] = double(odd ? -v : v);  // delta
+    }
+  }
+  if (p.mode == PMode::kHigh) {
+    const int64_t N = p.N;
+    const int64_t total_bits = N * int64_t(p.b);
+    double inv_root;
+    std::vector<double> fold;
+    if (total_bits >= 64) {
+      inv_root = std::ldexp(1.0, -p.b);
+      const int neg = int(std::min<int64_t>(total_bits, 1100));
+      m.root_neg_n = std::ldexp(1.0, -neg);
+      m.cofactor_scaled = 1.0 - double(N) * m.root_neg_n;
+      for (int64_t i = 0; i < N && i * p.b <= 80; ++i)
+        fold.push_back(std::ldexp(1.0, int(-i * p.b)));
+    } else {
+      // real root of B(X) = X^{N+1} - 2^b X^N + 2^b just below 2^b (Newton,
+      // maps.cpp:31-63), then the double ladders of maps_f64.cpp:226-238.
+      long double top = ldexpl(1.0L, p.b), x = top;
+      for (int it = 0; it < 200; ++it) {
+        long double xn = powl(x, (long double)N);
+        long double val = xn * (x - top) + top;
+        long double slope = powl(x, (long double)(N - 1)) * ((N + 1) * x - N * top);
+        if (slope == 0) break;
+        long double nx = x - val / slope;
+        if (nx > top) nx = top;
+        if (fabsl(nx - x) <= ldexpl(fabsl(x), -62)) { x = nx; break; }
+        x = nx;
+      }
+      const double root = double(x);
+      inv_root = 1.0 / root;
+      double ipow = inv_root;
+      for (int64_t i = 0; i < N; ++i) {
+        fold.push_back(std::ldexp(ipow, p.b));
+        ipow *= inv_root;
+      }
+      double inv_n = 1.0;
+      for (int64_t i = 0; i < N; ++i) inv_n *= inv_root;
+      m.root_neg_n = inv_n;
+      m.cofactor_scaled = 1.0 - double(N) * std::ldexp(inv_n * inv_root, p.b);
+      // the kernels use only the leading entries; keep what fits
+      if (fold.size() > size_t(kMaxFold)) fold.resize(kMaxFold);
+    }
+    if (fold.size() > size_t(kMaxFold)) throw Error(TMG_ERR_UNSUPPORTED, "fold row too long");
+    m.nfold = int32_t(fold.size());
+    for (size_t i = 0; i < fold.size(); ++i) m.fold[i] = fold[i];
+    // root-channel ladders (maps_f64.cpp:291-297, 364-370)
+    double ip = 1.0;
+    int d = 0;
+    m.ipow[0] = 1.0;
+    for (d = 0; d <= N; ++d) {
+      double nxt = ip * inv_root;
+      if (d + 1 < kMaxRootTerms) m.ipow[d + 1] = nxt;
+      ip = nxt;
+      if (ip < 1e-30) break;
+    }
+    const int D = int(std::min<int64_t>(d, N));
+    if (D + 1 > kMaxRootTerms) throw Error(TMG_ERR_UNSUPPORTED, "root ladder too long");
+    m.nroot = D + 1;
+    m.nhrho = D;
+  }
+  return m;
+}
+
+std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
+  auto pl = std::make_unique<Plan>();
+  pl->params = p;
+  pl->nlimbs = (p.n + 63) / 64;
+  pl->out_limbs = output_limbs(p.mode, p.n);
+  if (p.mode == PMode::kOracleFallback) {
+    pl->kind = 0;
+    pl->kernels = 1;
+    return pl;
+  }
+  if (p.backend != Backend::kFft)
+    throw Error(TMG_ERR_UNSUPPORTED, "GPU products run the FFT backend only");
+  if (!p.signed_split)
+    throw Error(TMG_ERR_UNSUPPORTED, "GPU products use the balanced (signed) split");
+  if (p.b > 48) throw Error(TMG_ERR_UNSUPPORTED, "chunk width above 48 bits");
+  const int64_t N = p.N;
+  const int64_t L = transform_length(p.mode, N);
+  pl->L = L;
+  pl->mc = make_map_consts(p);
+  if (L % 4 != 0) throw Error(TMG_ERR_UNSUPPORTED, "transform length must be divisible by 4");
+  if (p.mode != PMode::kFull && N < 2 * p.lambda + pl->mc.nfold + 2)
+    throw Error(TMG_ERR_UNSUPPORTED, "transform length too short for the series maps");
+  pl->count = (p.mode == PMode::kHigh) ? N + 1 : N;
+  pl->lead = (p.mode == PMode::kHigh) ? (N + 1) * int64_t(p.b) - p.n : 0;
+  const int b = p.b;
+  if (p.mode == PMode::kFull) {
+    pl->K = L;
+    pl->ML = ((L - 1) * b + 64 + 63) / 64 + 1;
+    pl->ML = std::max(pl->ML, pl->out_limbs);
+  } else if (p.mode == PMode::kLow) {
+    pl->K = N - 1;
+    pl->ML = pl->out_limbs;
+  } else {
+    pl->K = N + 1;
+    pl->shift_s = int32_t(2 * b + pl->lead);
+    if (pl->shift_s >= 127 || pl->shift_s < 1)
+      throw Error(TMG_ERR_UNSUPPORTED, "high product shift out of range");
+    pl->ML = (N * b + 64 + 64 + 63) / 64 + 1;
+    pl->ML = std::max<int64_t>(pl->ML, pl->out_limbs + (pl->shift_s >> 6) + 2);
+  }
+
+  if (L <= kSmallMaxL) {
+    pl->kind = 1;
+    const double2* t = tw.table(uint32_t(L));
+    pl->fwd = make_subfft(uint32_t(L), t, 1);
+    pl->inv = make_subfft(uint32_t(L / 2), t, 2);
+    pl->small_threads = threads_for(uint64_t(L));
+    pl->small_smem = small_smem_bytes(L, pl->nlimbs);
+    pl->kernels = 1;
+    return pl;
+  }
+
+  // multi-pass: C = row length (even, <= 4096), A (and B) column lengths
+  const uint64_t UL = uint64_t(L);
+  if (UL >= (uint64_t(1) << 32)) throw Error(TMG_ERR_UNSUPPORTED, "transform length above 2^32");
+  uint32_t C = 0;
+  for (uint32_t c = 4096; c >= 16; --c) {
+    if (c % 2 == 0 && UL % c == 0) { C = c; break; }
+  }
+  if (C == 0) throw Error(TMG_ERR_UNSUPPORTED, "no row length divides L");
+  const uint64_t AB = UL / C;
+  uint32_t A = 0, B = 1;
+  if (AB <= 2048) {
+    A = uint32_t(AB);
+    pl->kind = 2;
+  } else {
+    // balanced split: the divisor of AB closest to sqrt(AB), both <= 2048
+    const double root = std::sqrt(double(AB));
+    double bestd = 1e300;
+    for (uint32_t a = 16; a <= 2048; ++a) {
+      if (AB % a || AB / a > 2048 || AB / a < 4 || (a % 4)) continue;
+      const double d = std::fabs(std::log(double(a) / root));
+      if (d < bestd) { bestd = d; A = a; }
+    }
+    if (A == 0) throw Error(TMG_ERR_UNSUPPORTED, "cannot factor the transform length");
+    B = uint32_t(AB / A);
+    pl->kind = 3;
+  }
+  pl->A = A;
+  pl->B = B;
+  pl->C = C;
+  const size_t cap = 200 * 1024;
+  pl->twL = tw.global(UL);
+  const double2* tA = tw.table(A);
+  const double2* tC = tw.table(C);
+  pl->fA = make_subfft(A, tA, 1);
+  pl->iA = pl->fA;
+  pl->fC = make_subfft(C, tC, 1);
+  pl->iC = make_subfft(C / 2, tC, 2);
+  pl->logc_f1 = pick_logc(A, UL / A, cap);
+  pl->thr_f1 = threads_for(uint64_t(A) << pl->logc_f1);
+  pl->smem_f1 = size_t(padded_len(A << pl->logc_f1)) * 16;
+  const uint64_t il_cols = uint64_t(B) * (C / 2);
+  pl->logc_il = pick_logc(A, C / 2, cap);
+  pl->thr_il = threads_for(uint64_t(A) << pl->logc_il);
+  pl->smem_il = size_t(padded_len(A << pl->logc_il)) * 16;
+  (void)il_cols;
+  if (pl->kind == 3) {
+    const double2* tB = tw.table(B);
+    pl->fB = make_subfft(B, tB, 1);
+    pl->iB = pl->fB;
+    pl->logc_f2 = pick_logc(B, C, cap);
+    pl->thr_f2 = threads_for(uint64_t(B) << pl->logc_f2);
+    pl->smem_f2 = size_t(padded_len(B << pl->logc_f2)) * 16;
+    pl->logc_i2 = pick_logc(B, C / 2, cap);
+    pl->thr_i2 = threads_for(uint64_t(B) << pl->logc_i2);
+    pl->smem_i2 = size_t(padded_len(B << pl->logc_i2)) * 16;
+  }
+  pl->thr_mid = threads_for(uint64_t(2) * C);
+  pl->smem_mid = size_t(2) * (padded_len(C) + 4) * 16;
+  const int64_t LB = kCarryThreads * kCarryPerThread;
+  pl->smem_carry = size_t((64 * (LB + 2) + 64 + b) / b + 4) * 8 + size_t(LB + 2) * 8;
+  pl->kernels = (pl->kind == 2) ? 5 : 7;
+  return pl;
+}
+
+size_t small_smem_bytes(int64_t L, int64_t nlimbs) {
+  return size_t(padded_len(uint32_t(L))) * 16 + size_t(2 * nlimbs) * 8 + 32 * 4 + 8 * 8;
+}
+
+}  // namespace tmg

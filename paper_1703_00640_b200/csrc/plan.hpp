@@ -1,0 +1,71 @@
+// Device plans: transform shape, radix schedules, twiddle tables and the
+// map constants of one parameter set.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "kernels.cuh"
+#include "params.hpp"
+
+namespace tmg {
+
+// Owned device allocation.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf();
+  void ensure(size_t nbytes);  // grows, contents not kept
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// Twiddle tables keyed by length, shared by all plans of a context.
+class TwiddleCache {
+ public:
+  const double2* table(uint32_t R);               // omega_R^x, x < R
+  TwGlobal global(uint64_t L);                    // two-level omega_L
+ private:
+  std::map<uint64_t, std::unique_ptr<DevBuf>> tables_;
+  std::map<uint64_t, std::unique_ptr<DevBuf>> glob_;
+  std::map<uint64_t, uint32_t> glob_S_;
+};
+
+SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride = 1);
+MapConsts make_map_consts(const Params& p);
+
+struct Plan {
+  Params params;
+  int kind = 0;  // 1 fused single CTA, 2 two-pass, 3 three-pass, 0 basecase
+  int64_t L = 0;
+  uint32_t A = 1, B = 1, C = 1;
+  int64_t count = 0;  // chunks per operand
+  int64_t lead = 0;
+  int64_t K = 0;      // recombination coefficients
+  int64_t ML = 0;     // limbs scanned by the carry
+  int32_t shift_s = 0;
+  int64_t nlimbs = 0;
+  int64_t out_limbs = 0;
+  MapConsts mc{};
+  // fused
+  SubFft fwd{}, inv{};
+  size_t small_smem = 0;
+  int small_threads = 0;
+  // multi-pass
+  SubFft fA{}, iA{}, fB{}, iB{}, fC{}, iC{};
+  TwGlobal twL{};
+  uint32_t logc_f1 = 0, logc_f2 = 0, logc_i2 = 0, logc_il = 0;
+  size_t smem_f1 = 0, smem_f2 = 0, smem_i2 = 0, smem_il = 0, smem_mid = 0,
+         smem_carry = 0;
+  int thr_f1 = 0, thr_f2 = 0, thr_i2 = 0, thr_il = 0, thr_mid = 0;
+  int kernels = 0;
+};
+
+std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw);
+
+}  // namespace tmg
