@@ -5,6 +5,7 @@
 //   post-map -> round/accumulate -> carry, with the tripwires of
 //   products_f64.cpp:16-27 and 137-169 reported through a device status word.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -33,11 +34,14 @@ struct ScanSlot {
   DevBuf ctr;       // ticket / done counters
   uint32_t epoch = 0;
   ScanState next(size_t blocks) {
-    state.ensure(std::max<size_t>(blocks, 1) * 8);
+    const size_t need = std::max<size_t>(blocks, 1) * 8;
+    if (need > state.bytes) {
+      state.ensure(need);
+      TMG_CUDA(cudaMemset(state.p, 0, state.bytes));
+    }
     if (!ctr.p) {
       ctr.ensure(64);
       TMG_CUDA(cudaMemset(ctr.p, 0, 64));
-      TMG_CUDA(cudaMemset(state.p, 0, state.bytes));
     }
     ScanState s;
     s.state = state.as<unsigned long long>();
@@ -53,8 +57,9 @@ struct Context {
   bool own_stream = false;
   TwiddleCache tw;
   std::map<std::tuple<int64_t, int32_t, int64_t, int64_t, int32_t>, std::unique_ptr<Plan>> plans;
-  DevBuf work_t, work_c, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags;
-  ScanSlot scan_u, scan_v, scan_c;
+  DevBuf work_t, work_c, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf;
+  ScanSlot scan_u, scan_v, scan_c, scan_h;
+  bool debug_sync = false;
   DevStatus* h_status = nullptr;  // pinned
   int32_t last_kernels = 0;
   int64_t last_L = 0;
@@ -74,10 +79,18 @@ struct Context {
 
 namespace {
 
+bool g_debug_sync = getenv("TMG_DEBUG_SYNC") != nullptr;
+
 void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     throw Error(TMG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  if (g_debug_sync) {
+    e = cudaDeviceSynchronize();
+    fprintf(stderr, "[tmg] %s done: %s\n", what, cudaGetErrorString(e));
+    if (e != cudaSuccess)
+      throw Error(TMG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
 }
 
 template <class K>
@@ -268,10 +281,32 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       const unsigned blocks = unsigned((pl.ML + LB - 1) / LB);
       a.scan = cx.scan_c.next(blocks);
       a.status = status;
-      a.hstate = nullptr;
+      if (p.mode == PMode::kHigh) {
+        cx.tbuf.ensure(size_t(pl.ML) * 8 + 64);
+        a.tbuf = cx.tbuf.as<uint64_t>();
+      } else {
+        a.tbuf = nullptr;
+      }
       set_smem(k_carry, pl.smem_carry);
       k_carry<<<blocks, kCarryThreads, pl.smem_carry, st>>>(a);
       check_launch("k_carry");
+      ++kernels;
+    }
+    if (p.mode == PMode::kHigh) {
+      HighRoundArgs a;
+      a.tbuf = cx.tbuf.as<uint64_t>();
+      a.out = out;
+      a.n = p.n;
+      a.out_limbs = pl.out_limbs;
+      a.ML = pl.ML;
+      a.shift_s = pl.shift_s;
+      a.WL = pl.ML - (pl.shift_s >> 6);
+      const int64_t LB = kCarryThreads * kCarryPerThread;
+      const unsigned blocks = unsigned((a.WL + LB - 1) / LB);
+      a.scan = cx.scan_h.next(blocks);
+      a.status = status;
+      k_high_round<<<blocks, kCarryThreads, 0, st>>>(a);
+      check_launch("k_high_round");
       ++kernels;
     }
   }
@@ -301,6 +336,8 @@ int finish(Context& cx, const Plan* pl, tmg_stats* stats) {
   }
   uint32_t f = s.flags;
   if (s.high_topbit && s.high_lownz) f |= kFlagHighRange;
+  cudaError_t ce = cudaGetLastError();
+  if (ce != cudaSuccess) throw Error(TMG_ERR_CUDA, cudaGetErrorString(ce));
   if (f & kFlagInputRange)
     throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "split: operand outside [0, 2^n)");
   if (f & kFlagOverflow)

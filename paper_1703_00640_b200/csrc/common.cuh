@@ -45,7 +45,7 @@ struct DevStatus {
   unsigned int flags;
   unsigned int high_topbit;  // high product: bit n of w was set
   unsigned int high_lownz;   // high product: some bit below n was set
-  unsigned int pad;
+  unsigned int high_sticky;  // high product: t has a set bit below s-1
 };
 
 // ---------------------------------------------------------------------------

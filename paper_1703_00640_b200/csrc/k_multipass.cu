@@ -93,7 +93,7 @@ k_split_scan(SplitScanArgs a) {
   }
   uint32_t agg;
   uint32_t ex = block_scan_tf(f, sw, &agg);
-  if (tid == 0) s_cin = lookback_carry(sc.state, blk, agg, sc.epoch);
+  if (tid == 0) s_cin = lookback_carry(sc.state, blk, agg, sc.epoch, 0);
   __syncthreads();
   int c = tf_apply(ex, s_cin);
   uint32_t bits = 0;
@@ -362,7 +362,6 @@ k_carry(CarryArgs a) {
   __shared__ uint32_t s_blk;
   __shared__ int s_cin;
   __shared__ double s_psi;
-  __shared__ unsigned long long s_delta[2];
   __shared__ uint32_t s_flags, s_top, s_low;
   const int tid = threadIdx.x;
   const MapConsts& mc = a.mc;
@@ -429,76 +428,40 @@ k_carry(CarryArgs a) {
 
   const int64_t m0 = ms + int64_t(tid) * kCarryPerThread;
   const int64_t m1 = min(me, m0 + kCarryPerThread);
-  const bool twopass = (mc.mode == kModeHigh && blk == 0);
-  __int128 delta = 0;
-  int c = 0;
-  for (int pass = 0; pass < (twopass ? 2 : 1); ++pass) {
-    auto lane = [&](int64_t m) -> __int128 {
-      __int128 v = (m < 0) ? (__int128)0 : lane_value(E, m, b, khi);
-      if (pass == 1 && m >= 0 && m <= 1) {
-        unsigned long long d = (m == 0) ? (unsigned long long)delta
-                                        : (unsigned long long)(delta >> 64);
-        v += (__int128)d;
-      }
-      return v;
-    };
-    uint32_t f = kTfIdentity;
-    __int128 prev = lane(m0 - 1);
-    for (int64_t m = m0; m < m1; ++m) {
-      __int128 cur = lane(m);
-      __int128 s = (__int128)(unsigned long long)cur + (prev >> 64);
-      f = tf_compose(f, limb_tf(s, flags));
-      prev = cur;
-    }
-    uint32_t agg;
-    uint32_t ex = block_scan_tf(f, sw, &agg);
-    if (twopass && pass == 0) {
-      if (tid == 0) s_cin = 0;
-    } else if (tid == 0) {
-      s_cin = lookback_carry(a.scan.state, blk, agg, a.scan.epoch);
-    }
-    __syncthreads();
-    c = tf_apply(ex, s_cin);
-    prev = lane(m0 - 1);
-    for (int64_t m = m0; m < m1; ++m) {
-      __int128 cur = lane(m);
-      __int128 s = (__int128)(unsigned long long)cur + (prev >> 64);
-      uint32_t tfm = limb_tf(s, flags);
-      sv[m - ms] = (unsigned long long)(s + c);
-      c = tf_apply(tfm, c);
-      prev = cur;
-    }
-    if (m1 == me && m0 < m1) {
-      // one extra limb (first limb of the next block) for the high shift,
-      // or the sign extension at the very top
-      if (me < a.ML) {
-        __int128 cur = lane(me);
-        __int128 s = (__int128)(unsigned long long)cur + (prev >> 64);
-        sv[me - ms] = (unsigned long long)(s + c);
-      } else {
-        sv[me - ms] = (c < 0) ? ~0ull : 0ull;
-        if (mc.mode == kModeFull && c < 0) flags |= kFlagNegative;
-        if (mc.mode == kModeHigh && c < 0) flags |= kFlagHighRange;
-      }
-    }
-    __syncthreads();
-    if (twopass && pass == 0) {
-      if (tid == 0) {
-        const int s_sh = a.shift_s;
-        uint64_t lw = sv[s_sh >> 6];
-        int bit = int((lw >> (s_sh & 63)) & 1);
-        __int128 dd = ((__int128)1 << (s_sh - 1)) - 1 + bit;
-        s_delta[0] = (unsigned long long)dd;
-        s_delta[1] = (unsigned long long)(dd >> 64);
-      }
-      __syncthreads();
-      delta = (__int128)s_delta[0] | ((__int128)s_delta[1] << 64);
-    }
+  auto lane = [&](int64_t m) -> __int128 {
+    return (m < 0) ? (__int128)0 : lane_value(E, m, b, khi);
+  };
+  uint32_t f = kTfIdentity;
+  __int128 prev = lane(m0 - 1);
+  for (int64_t m = m0; m < m1; ++m) {
+    __int128 cur = lane(m);
+    __int128 s = (__int128)(unsigned long long)cur + (prev >> 64);
+    f = tf_compose(f, limb_tf(s, flags));
+    prev = cur;
   }
+  uint32_t agg;
+  uint32_t ex = block_scan_tf(f, sw, &agg);
+  if (tid == 0) s_cin = lookback_carry(a.scan.state, blk, agg, a.scan.epoch, 0);
+  __syncthreads();
+  int c = tf_apply(ex, s_cin);
+  prev = lane(m0 - 1);
+  for (int64_t m = m0; m < m1; ++m) {
+    __int128 cur = lane(m);
+    __int128 s = (__int128)(unsigned long long)cur + (prev >> 64);
+    uint32_t tfm = limb_tf(s, flags);
+    sv[m - ms] = (unsigned long long)(s + c);
+    c = tf_apply(tfm, c);
+    prev = cur;
+  }
+  if (m1 == me && m0 < m1 && me == a.ML && c < 0) {
+    // sign of the recombined value (carry out of the top limb)
+    if (mc.mode == kModeFull) flags |= kFlagNegative;
+    if (mc.mode == kModeHigh) flags |= kFlagHighRange;
+  }
+  __syncthreads();
 
   // outputs
   const int64_t OL = a.out_limbs;
-  uint32_t topbit = 0, lownz = 0;
   if (mc.mode == kModeFull) {
     const int64_t nb2 = 2 * a.n;
     for (int64_t m = ms + tid; m < me; m += kCarryThreads) {
@@ -519,17 +482,93 @@ k_carry(CarryArgs a) {
       }
     }
   } else {
-    const int s_sh = a.shift_s;
-    const int64_t q = s_sh >> 6;
-    const int r = s_sh & 63;
-    // w limb t = V'[t + q] >> r | V'[t + q + 1] << (64 - r), for t + q in [ms, me)
+    // high: keep all limbs of t; OR the bits strictly below s-1 (sticky)
+    const int64_t sb = a.shift_s - 1;  // bit s-1
+    uint32_t sticky = 0;
     for (int64_t m = ms + tid; m < me; m += kCarryThreads) {
-      const int64_t t = m - q;
-      if (t < 0) continue;
-      uint64_t lo = sv[m - ms], hi = sv[m - ms + 1];
-      uint64_t x = r ? ((lo >> r) | (hi << (64 - r))) : lo;
-      high_classify(x, t, a.n, topbit, lownz, flags);
-      if (t < OL) a.out[t] = x & high_mask(t, OL, a.n);
+      uint64_t x = sv[m - ms];
+      a.tbuf[m] = x;
+      const int64_t bit0 = 64 * m;
+      if (bit0 + 64 <= sb) {
+        if (x) sticky = 1;
+      } else if (bit0 < sb) {
+        if (x & ((1ull << (sb - bit0)) - 1)) sticky = 1;
+      }
+    }
+    if (sticky) atomicOr(&s_low, 1u);
+  }
+  if (flags) atomicOr(&s_flags, flags);
+  __syncthreads();
+  if (tid == 0) {
+    if (s_flags) atomicOr(&a.status->flags, s_flags);
+    if (s_low) atomicOr(&a.status->high_sticky, 1u);
+    __threadfence();
+    if (atomicAdd(a.scan.ctr + 1, 1ull) == gridDim.x - 1) {
+      a.scan.ctr[0] = 0;
+      a.scan.ctr[1] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// High product rounding (products_f64.cpp:162-166): w = round_even(t / 2^s)
+// = (t >> s) + inc, inc = bit_{s-1}(t) & (sticky_{<s-1} | bit_s(t)).  The
+// increment ripples through all-ones limbs of t >> s: a second carry scan
+// with the increment as the carry into limb 0.  Then the range test
+// 0 <= w <= 2^n.
+__global__ void __launch_bounds__(kCarryThreads)
+k_high_round(HighRoundArgs a) {
+  __shared__ uint32_t sw[32];
+  __shared__ uint32_t s_blk;
+  __shared__ int s_cin;
+  __shared__ uint32_t s_flags, s_top, s_low;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_blk = uint32_t(atomicAdd(a.scan.ctr, 1ull));
+    s_flags = 0;
+    s_top = 0;
+    s_low = 0;
+  }
+  __syncthreads();
+  const uint32_t blk = s_blk;
+  const int64_t s = a.shift_s;
+  const int64_t q = s >> 6;
+  const int r = int(s & 63);
+  const uint64_t* t = a.tbuf;
+  auto tl = [&](int64_t m) -> uint64_t { return m < a.ML ? t[m] : 0ull; };
+  const int inc = int((tl((s - 1) >> 6) >> ((s - 1) & 63)) & 1) &
+                  int(a.status->high_sticky != 0 || ((tl(s >> 6) >> (s & 63)) & 1));
+  constexpr int LB = kCarryThreads * kCarryPerThread;
+  const int64_t ms = int64_t(blk) * LB;
+  const int64_t me = min(a.WL, ms + LB);
+  const int64_t m0 = ms + int64_t(tid) * kCarryPerThread;
+  const int64_t m1 = min(me, m0 + kCarryPerThread);
+  uint64_t w0[kCarryPerThread];
+  uint32_t f = kTfIdentity;
+#pragma unroll
+  for (int i = 0; i < kCarryPerThread; ++i) {
+    const int64_t m = m0 + i;
+    if (m < m1) {
+      uint64_t lo = tl(m + q), hi = tl(m + q + 1);
+      w0[i] = r ? ((lo >> r) | (hi << (64 - r))) : lo;
+      f = tf_compose(f, w0[i] == ~0ull ? kTfIdentity : tf_const(0));
+    }
+  }
+  uint32_t agg;
+  uint32_t ex = block_scan_tf(f, sw, &agg);
+  if (tid == 0) s_cin = lookback_carry(a.scan.state, blk, agg, a.scan.epoch, inc);
+  __syncthreads();
+  int c = tf_apply(ex, s_cin);
+  uint32_t flags = 0, topbit = 0, lownz = 0;
+  const int64_t OL = a.out_limbs;
+#pragma unroll
+  for (int i = 0; i < kCarryPerThread; ++i) {
+    const int64_t m = m0 + i;
+    if (m < m1) {
+      const uint64_t x = w0[i] + uint64_t(c);
+      c = (c && w0[i] == ~0ull) ? 1 : 0;
+      high_classify(x, m, a.n, topbit, lownz, flags);
+      if (m < OL) a.out[m] = x & high_mask(m, OL, a.n);
     }
   }
   if (flags) atomicOr(&s_flags, flags);

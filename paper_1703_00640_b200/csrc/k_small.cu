@@ -213,20 +213,9 @@ k_small_product(SmallArgs a) {
   const int64_t lpt = (ML + nthr - 1) / nthr;
   const int64_t m0 = int64_t(tid) * lpt;
   const int64_t m1 = min(ML, m0 + lpt);
-  const int s_sh = a.shift_s;
-  const int npass = (mc.mode == kModeHigh) ? 2 : 1;
-  __int128 delta = 0;  // high: 2^{s-1} - 1 + (bit s of t)
-  for (int pass = 0; pass < npass; ++pass) {
-    auto lane = [&](int64_t m) -> __int128 {
-      __int128 v = lane_value(E, m, b, K);
-      if (pass == 1 && m >= 0 && m <= 1) {
-        // add the rounding constant delta limbwise into lanes 0 and 1
-        unsigned long long d = (m == 0) ? (unsigned long long)delta
-                                        : (unsigned long long)(delta >> 64);
-        v += (__int128)d;
-      }
-      return v;
-    };
+  const int64_t s_sh = a.shift_s;
+  {
+    auto lane = [&](int64_t m) -> __int128 { return lane_value(E, m, b, K); };
     uint32_t f = kTfIdentity;
     __int128 prev = lane(m0 - 1);
     for (int64_t m = m0; m < m1; ++m) {
@@ -247,28 +236,10 @@ k_small_product(SmallArgs a) {
       c = tf_apply(tfm, c);
       prev = cur;
     }
-    if (m1 == ML && m0 < m1) {
-      // final carry out of the top limb: the sign of V
-      sd[4] = double(c);
-    }
+    if (m1 == ML && m0 < m1) sd[4] = double(c);  // sign of V
     __syncthreads();
-    if (pass == 0 && npass == 2) {
-      if (tid == 0) {
-        uint64_t lw = vlimb[s_sh >> 6];
-        int bit = int((lw >> (s_sh & 63)) & 1);
-        __int128 dd = ((__int128)1 << (s_sh - 1)) - 1 + bit;
-        sd[5] = 0.0;
-        reinterpret_cast<unsigned long long*>(sd)[6] = (unsigned long long)dd;
-        reinterpret_cast<unsigned long long*>(sd)[7] = (unsigned long long)(dd >> 64);
-      }
-      __syncthreads();
-      delta = (__int128)reinterpret_cast<unsigned long long*>(sd)[6] |
-              ((__int128)reinterpret_cast<unsigned long long*>(sd)[7] << 64);
-      __syncthreads();
-    }
   }
   const int sign = int(sd[4]);
-
   // 9. outputs and range checks.
   const int64_t OL = a.out_limbs;
   uint32_t topbit = 0, lownz = 0;
@@ -292,21 +263,47 @@ k_small_product(SmallArgs a) {
       gout[m] = x;
     }
   } else {
-    // w = V' >> s must lie in [0, 2^n]
-    if (tid == 0 && sign < 0) flags |= kFlagHighRange;
-    const int64_t q = s_sh >> 6;
-    const int r = s_sh & 63;
-    const int64_t nw = ML - q;
-    for (int64_t m = tid; m < max(nw, OL); m += nthr) {
-      uint64_t x = 0;
-      if (m < nw) {
-        uint64_t lo = vlimb[m + q];
-        uint64_t hi = (m + q + 1 < ML) ? vlimb[m + q + 1] : (sign < 0 ? ~0ull : 0ull);
-        x = r ? ((lo >> r) | (hi << (64 - r))) : lo;
+    // w = round_even(V / 2^s) = (V >> s) + inc (products_f64.cpp:162-166);
+    // inc ripples through all-ones limbs of V >> s (block carry scan)
+    if (tid == 0) {
+      if (sign < 0) flags |= kFlagHighRange;
+      const int64_t sb = s_sh - 1;
+      uint32_t sticky = 0;
+      for (int64_t m = 0; 64 * m < sb && m < ML; ++m) {
+        uint64_t x = vlimb[m];
+        if (64 * m + 64 > sb) x &= (1ull << (sb - 64 * m)) - 1;
+        if (x) { sticky = 1; break; }
       }
+      const int bs1 = int((vlimb[sb >> 6] >> (sb & 63)) & 1);
+      const int bs = int(((s_sh >> 6) < ML ? vlimb[s_sh >> 6] : 0ull) >> (s_sh & 63) & 1);
+      sw[3] = uint32_t(bs1 & int(sticky | uint32_t(bs)));
+    }
+    __syncthreads();
+    const int inc = int(sw[3]);
+    __syncthreads();
+    const int64_t q = s_sh >> 6;
+    const int r = int(s_sh & 63);
+    const int64_t WL = ML - q;
+    const int64_t wpt = (WL + nthr - 1) / nthr;
+    const int64_t w0 = int64_t(tid) * wpt, w1 = min(WL, w0 + wpt);
+    auto wlimb = [&](int64_t m) -> uint64_t {
+      uint64_t lo = vlimb[m + q];
+      uint64_t hi = (m + q + 1 < ML) ? vlimb[m + q + 1] : (sign < 0 ? ~0ull : 0ull);
+      return r ? ((lo >> r) | (hi << (64 - r))) : lo;
+    };
+    uint32_t f = kTfIdentity;
+    for (int64_t m = w0; m < w1; ++m) f = tf_compose(f, wlimb(m) == ~0ull ? kTfIdentity : tf_const(0));
+    uint32_t agg;
+    uint32_t ex = block_scan_tf(f, sw, &agg);
+    int c = tf_apply(ex, inc);
+    for (int64_t m = w0; m < w1; ++m) {
+      const uint64_t x0 = wlimb(m);
+      const uint64_t x = x0 + uint64_t(c);
+      c = (c && x0 == ~0ull) ? 1 : 0;
       high_classify(x, m, a.n, topbit, lownz, flags);
       if (m < OL) gout[m] = x & high_mask(m, OL, a.n);
     }
+    for (int64_t m = WL + tid; m < OL; m += nthr) gout[m] = 0;
   }
   // block-combine flags; the high range test needs both bits of the block
   __syncthreads();

@@ -135,12 +135,24 @@ struct CarryArgs {
   const double* aux;
   ScanState scan;
   DevStatus* status;
-  // high: delta resolution
-  unsigned long long* hstate;  // [0] epoch-tagged delta words
+  uint64_t* tbuf;  // high: all limbs of t (ML words)
 };
 constexpr int kCarryThreads = 256;
 constexpr int kCarryPerThread = 4;
 __global__ void k_carry(CarryArgs a);
+
+struct HighRoundArgs {
+  const uint64_t* tbuf;
+  uint64_t* out;
+  int64_t n;
+  int64_t out_limbs;
+  int64_t ML;   // limbs of t
+  int64_t WL;   // limbs of w examined (covers every bit of t >> s)
+  int32_t shift_s;
+  ScanState scan;
+  DevStatus* status;
+};
+__global__ void k_high_round(HighRoundArgs a);
 
 // Schoolbook product for operands below the pipeline cutoff (the reference's
 // ORACLE_FALLBACK mode, products.hpp:14-15).

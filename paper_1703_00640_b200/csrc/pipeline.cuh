@@ -257,16 +257,17 @@ __device__ __forceinline__ uint32_t block_scan_tf(uint32_t f, uint32_t* sw,
   return tf_compose(wex, excl);
 }
 
-// Decoupled look-back over per-block aggregates (one thread per block).
+// Decoupled look-back over per-block aggregates (one thread per block);
+// carry0 is the carry into block 0.
 // state words: [63:32] epoch, [31:30] flag (1 aggregate, 2 inclusive),
 // [5:0] payload (transfer code, or carry + 1 for inclusive).
 __device__ __forceinline__ int lookback_carry(unsigned long long* state,
                                               uint32_t blk, uint32_t agg,
-                                              uint32_t epoch) {
+                                              uint32_t epoch, int carry0) {
   const unsigned long long ep = (unsigned long long)epoch << 32;
   int carry_in = 0;
   if (blk == 0) {
-    carry_in = 0;
+    carry_in = carry0;
   } else {
     *(volatile unsigned long long*)(state + blk) = ep | (1ull << 30) | agg;
     uint32_t E = kTfIdentity;

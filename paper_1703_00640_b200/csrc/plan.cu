@@ -297,8 +297,7 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   } else {
     pl->K = N + 1;
     pl->shift_s = int32_t(2 * b + pl->lead);
-    if (pl->shift_s >= 127 || pl->shift_s < 1)
-      throw Error(TMG_ERR_UNSUPPORTED, "high product shift out of range");
+    if (pl->shift_s < 1) throw Error(TMG_ERR_UNSUPPORTED, "high product shift out of range");
     pl->ML = (N * b + 64 + 64 + 63) / 64 + 1;
     pl->ML = std::max<int64_t>(pl->ML, pl->out_limbs + (pl->shift_s >> 6) + 2);
   }
@@ -374,7 +373,7 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   pl->smem_mid = size_t(2) * (padded_len(C) + 4) * 16;
   const int64_t LB = kCarryThreads * kCarryPerThread;
   pl->smem_carry = size_t((64 * (LB + 2) + 64 + b) / b + 4) * 8 + size_t(LB + 2) * 8;
-  pl->kernels = (pl->kind == 2) ? 5 : 7;
+  pl->kernels = ((pl->kind == 2) ? 5 : 7) + (p.mode == PMode::kHigh ? 1 : 0);
   return pl;
 }
 

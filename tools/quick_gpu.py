@@ -7,7 +7,7 @@ import paper_1703_00640_b200 as tm
 from oracle import port
 ctx = tm.default_context(0)
 rng = np.random.default_rng(1)
-for n in [8192, 5001, 1<<16, 1<<18, 1000000, 1<<22, 1<<24, 1<<26]:
+for n in [int(x) for x in (sys.argv[1:] or ["8192", "5001", "65536", "262144", "1000000", "4194304"])]:
     nl = (n + 63)//64
     u = rng.integers(0, 2**64, nl, dtype=np.uint64); v = rng.integers(0, 2**64, nl, dtype=np.uint64)
     if n % 64:
