@@ -1,0 +1,395 @@
+"""Benchmark: full / low / high products of n = 2^26-bit integers on B200.
+
+Workload (BASELINE.json configs[2]): u, v = 1048576 uniform random 64-bit
+words each from mt19937_64(seed 3); one step = the full, the low and the high
+product of (u, v).  Metric: input Gbit/s = (bits of u + bits of v) per
+product x 3 products per step / step time, aggregated over all ranks.
+
+  value  device-resident: operands already in HBM, CUDA events on the
+         launching stream around each step, L2 flushed between steps
+  e2e    the public C-ABI host entry points (tmg_{full,low,high}_product):
+         pinned host operands in, H2D + kernels + D2H of the result inside
+         the timed region
+  --impl reference  the CPU oracle port of the reference pipeline
+         (oracle/port.py; the reference itself cannot be built here)
+
+Multi-GPU: the product does not shard at these sizes, so N ranks run N
+independent replicas; value = all ranks' input
+bits / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LOG2N = 26
+SEED = 3
+WORKLOAD = "config3: full/low/high product, n=2^26 bits, u,v = mt19937_64(seed 3) words"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                parts = [p.strip() for p in out.strip().split(",")]
+                if len(parts) >= 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reduce_max(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    import __graft_entry__ as g
+    g.build()
+    import paper_1703_00640_b200 as tm
+    from oracle import port  # operand generator + checker only
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    n = 1 << LOG2N
+    nl = n // 64
+    u, v = port.config_operands(SEED, nl)
+    modes = [tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH]
+    params = {m: tm.select_params(n, m) for m in modes}
+    ctx = tm.Context(local)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream.cuda_stream)
+
+    du = torch.from_numpy(u.view(np.int64)).to(dev)
+    dv = torch.from_numpy(v.view(np.int64)).to(dev)
+    outs = {m: torch.zeros(tm.output_limbs(m, n), dtype=torch.int64, device=dev) for m in modes}
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2
+
+    def step_device():
+        for m in modes:
+            ctx.product_device(params[m], du.data_ptr(), dv.data_ptr(), outs[m].data_ptr(), 1)
+
+    # correctness of the device path against the oracle (untimed)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        step_device()
+    stats = ctx.check()
+    P = port.limbs_to_int(port.oracle_full(u, v))
+    res = {m: tm.from_limbs(outs[m].cpu().numpy().view(np.uint64)) for m in modes}
+    parity = {
+        "full_bit_exact": res[tm.Mode.FULL] == P,
+        "low_bit_exact": res[tm.Mode.LOW] == (P & ((1 << n) - 1)),
+        "high_in_bound": port.is_valid_high(u, v, n, res[tm.Mode.HIGH]),
+    }
+
+    # per-mode error statistics
+    errs = {}
+    for m in modes:
+        with torch.cuda.stream(stream):
+            ctx.product_device(params[m], du.data_ptr(), dv.data_ptr(), outs[m].data_ptr(), 1)
+        s = ctx.check()
+        errs[m.name.lower()] = s.max_round_err
+
+    # warm-up
+    for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            step_device()
+    ctx.check()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev = []
+    kernels_per_step = 0
+    ctx.profile(True)
+    ctx.profile_read()
+    mode_ms = {m: [] for m in modes}
+    step_ms = []
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            marks = []
+            for m in modes:
+                ctx.product_device(params[m], du.data_ptr(), dv.data_ptr(), outs[m].data_ptr(), 1)
+                kernels_per_step += ctx.last_kernel_count()
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                marks.append(e)
+            ev.append((e0, marks))
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    ctx.check()
+    for e0, marks in ev:
+        prev = e0
+        tot = 0.0
+        for m, e in zip(modes, marks):
+            t = prev.elapsed_time(e)
+            mode_ms[m].append(t)
+            tot += t
+            prev = e
+        step_ms.append(tot)
+    total_ms = sum(step_ms)
+    total_ms_max = reduce_max(total_ms, world, dev)
+    bits_per_step = 3 * 2 * n
+    value = world * bits_per_step * args.steps / (total_ms_max * 1e-3) / 1e9
+
+    # kernel breakdown from the library's own events (same stream)
+    agg = {}
+    for name, ms, by in prof:
+        a = agg.setdefault(name, [0.0, 0, 0.0])
+        a[0] += ms
+        a[1] += 1
+        a[2] += by
+    kern = {k: {"ms_per_launch": a[0] / a[1], "launches": a[1],
+                "gbs": (a[2] / a[1]) / (a[0] / a[1] * 1e-3) / 1e9} for k, a in agg.items()}
+    top = max(agg.items(), key=lambda kv: kv[1][0])
+    peak, peak_kind = _peaks()
+    top_ms = top[1][0] / top[1][1]
+    top_bytes = top[1][2] / top[1][1]
+    achieved = top_bytes / (top_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": top[0], "achieved": round(achieved, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": None, "share_of_step": round(top[1][0] / sum(a[0] for a in agg.values()), 3)}
+    # whole-step HBM view: algorithmic bytes of all kernels / step time
+    step_bytes = sum(a[2] for a in agg.values()) / args.steps
+    step_roof = step_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9
+
+    # e2e through the host API with pinned buffers
+    e2e_ms = []
+    hu = torch.from_numpy(u.view(np.int64)).pin_memory()
+    hv = torch.from_numpy(v.view(np.int64)).pin_memory()
+    hout = {m: torch.zeros(tm.output_limbs(m, n), dtype=torch.int64).pin_memory() for m in modes}
+    import ctypes
+    from paper_1703_00640_b200 import _native
+    L = _native.load()
+    P64 = ctypes.POINTER(ctypes.c_uint64)
+    fns = {tm.Mode.FULL: L.tmg_full_product, tm.Mode.LOW: L.tmg_low_product, tm.Mode.HIGH: L.tmg_high_product}
+    cparams = {m: params[m].to_c() for m in modes}
+    st = _native.tmg_stats()
+
+    def e2e_step():
+        for m in modes:
+            rc = fns[m](ctx.handle, ctypes.byref(cparams[m]), ctypes.cast(hu.data_ptr(), P64),
+                        ctypes.cast(hv.data_ptr(), P64), ctypes.cast(hout[m].data_ptr(), P64),
+                        ctypes.byref(st))
+            if rc != 0:
+                raise RuntimeError(_native.last_error())
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        e2e_step()
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e_total = reduce_max(sum(e2e_ms), world, dev)
+    e2e_value = world * bits_per_step * args.steps / (e2e_total * 1e-3) / 1e9
+    e2e_ok = (tm.from_limbs(hout[tm.Mode.FULL].numpy().view(np.uint64)) == P)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(u, v, n, params)
+
+    if rank == 0:
+        med = {m.name.lower(): statistics.median(mode_ms[m]) for m in modes}
+        line = {
+            "metric": "low/high/full product input Gbit/s on 1 B200 at n=2^26; % HBM roofline",
+            "value": round(value, 3),
+            "unit": "Gbit/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(total_ms_max / args.steps, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic",
+            "config": {
+                "workload": WORKLOAD,
+                "n_bits": n,
+                "input_bits_per_step": bits_per_step,
+                "params": {m.name.lower(): {"b": params[m].b, "N": params[m].N, "lambda": params[m].lam,
+                                            "L": params[m].transform_length} for m in modes},
+                "policy": "accurate (DESIGN.md: reference b=13 trips its own 0.25 tripwire at 2^26)",
+                "l2": "flushed between steps (512 MiB write, outside the timed events)",
+                "parallelism": f"replicas{world}",
+            },
+            "per_mode_ms": {k: round(v_, 4) for k, v_ in med.items()},
+            "per_mode_gbits": {k: round(2 * n / (v_ * 1e-3) / 1e9, 3) for k, v_ in med.items()},
+            "ratio_low_full": round(med["low"] / med["full"], 4),
+            "ratio_high_full": round(med["high"] / med["full"], 4),
+            "paper_asymptotic_ratio": 0.75,
+            "max_round_err": {k: round(e, 5) for k, e in errs.items()},
+            "parity": parity,
+            "roofline": roofline,
+            "step_hbm_gbs": round(step_roof, 1),
+            "kernels": {k: {kk: round(vv, 4) for kk, vv in d.items()} for k, d in kern.items()},
+            "e2e": {"value": round(e2e_value, 3), "unit": "Gbit/s",
+                    "h2d_bytes_per_step": 3 * 2 * nl * 8,
+                    "d2h_bytes_per_step": sum(tm.output_limbs(m, n) for m in modes) * 8,
+                    "ms_per_step": round(e2e_total / args.steps, 4), "full_bit_exact": bool(e2e_ok)},
+            "gpu_launches": kernels_per_step,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_baseline(u, v, n, params=None, sample_modes=("full", "low", "high")):
+    """The oracle port of the reference pipeline (numpy pocketfft + C), one
+    thread, on one step of the same workload."""
+    from oracle import port
+    import paper_1703_00640_b200 as tm
+    t0 = time.perf_counter()
+    for mname in sample_modes:
+        m = tm.Mode[mname.upper()]
+        p = params[m] if params else tm.select_params(n, m)
+        port.product(mname, u, v, n, p.b, p.N, p.lam)
+    dt = time.perf_counter() - t0
+    bits = len(sample_modes) * 2 * n
+    return {"value": round(bits / dt / 1e9, 4), "unit": "Gbit/s", "cores": 1, "kind": "port",
+            "seconds": round(dt, 3),
+            "sample": f"one step ({'+'.join(sample_modes)} products, n=2^{LOG2N}) of the oracle port "
+                      "at the GPU's parameters; reference unbuildable here (no gmp.h/FFTW3)"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import numpy as np
+    import paper_1703_00640_b200 as tm
+    from oracle import port
+    n = 1 << LOG2N
+    u, v = port.config_operands(SEED, n // 64)
+    params = {m: tm.select_params(n, m) for m in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH)}
+    for _ in range(args.warmup if args.warmup <= 1 else 1):
+        port.product("full", u, v, n, params[tm.Mode.FULL].b, params[tm.Mode.FULL].N)
+    times = []
+    steps = min(args.steps, 3)
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        for mname in ("full", "low", "high"):
+            p = params[tm.Mode[mname.upper()]]
+            port.product(mname, u, v, n, p.b, p.N, p.lam)
+        times.append(time.perf_counter() - t0)
+    value = 3 * 2 * n * steps / sum(times) / 1e9
+    line = {
+        "impl": "reference",
+        "metric": "low/high/full product input Gbit/s on 1 B200 at n=2^26; % HBM roofline",
+        "value": round(value, 4), "unit": "Gbit/s", "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / steps, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "n_bits": n},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Gbit/s", "cores": 1, "kind": "port",
+                         "sample": f"{steps} step(s) of full+low+high at n=2^26 by the oracle port "
+                                   "(numpy pocketfft for FFTW); the reference needs gmp.h/FFTW3/CMake"},
+        "e2e": {"value": round(value, 4), "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -151,6 +151,14 @@ int tmg_memcpy_d2h(tmg_context* ctx, void* dst, const void* src, size_t bytes);
 /* Kernels launched by the last product call (for launch accounting). */
 int32_t tmg_last_kernel_count(tmg_context* ctx);
 
+/* Per-kernel CUDA-event timing on the context stream.  When enabled every
+ * launch is bracketed by events; tmg_profile_read synchronises, returns up to
+ * max_records (name, milliseconds, algorithmic bytes) and clears the log.
+ * names receives max_records strings of name_stride bytes each. */
+int tmg_profile_enable(tmg_context* ctx, int on);
+int tmg_profile_read(tmg_context* ctx, char* names, int name_stride, double* ms,
+                     double* bytes, int max_records, int* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -175,7 +175,7 @@ def oracle_low(u, v, n: int) -> np.ndarray:
 def oracle_high_set(u, v, n: int) -> list[int]:
     """All w in [0, 2^n] with |uv - 2^n w| < 2^n, ascending (oracle.hpp:39-42)."""
     p = limbs_to_int(gmp_mul(u, v))
-    q, r = divmod(p, 1 << n)
+    q, r = p >> n, p & ((1 << n) - 1)  # bit ops: divmod by 2^n is quadratic
     out = [q]
     if r != 0 and q + 1 <= (1 << n):
         out.append(q + 1)
@@ -185,6 +185,10 @@ def oracle_high_set(u, v, n: int) -> list[int]:
 def is_valid_high(u, v, n: int, w: int) -> bool:
     p = limbs_to_int(gmp_mul(u, v))
     return 0 <= w <= (1 << n) and abs(p - (w << n)) < (1 << n)
+
+
+def low_int(p: int, n: int) -> int:
+    return p & ((1 << n) - 1)
 
 
 # ---------------------------------------------------------------------------
@@ -264,13 +268,13 @@ def low_product(u, v, n: int, b: int, N: int, lam: int, signed_split: bool = Tru
     lib().orc_beta_star(_pd(be), lam, N, b, _pd(w), _pd(low))
     nout = (N * b + b + 128) // 64 + 4
     t, me, ma = _accumulate(low, b, b, nout)
-    if t % (1 << b):
+    if t & ((1 << b) - 1):
         raise ConvolutionPrecisionFailure("low product recombination is not divisible by the chunk base")
     return Result((t >> b) & ((1 << n) - 1), me, ma)
 
 
 def _round_even_shift(t: int, s: int) -> int:
-    q, r = divmod(t, 1 << s)  # floor semantics for negative t
+    q, r = t >> s, t & ((1 << s) - 1)  # floor semantics for negative t
     half = 1 << (s - 1)
     if r > half or (r == half and (q & 1)):
         q += 1

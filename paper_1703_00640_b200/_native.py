@@ -101,6 +101,9 @@ def load():
     L.tmg_memcpy_d2h.argtypes = [vp, vp, vp, ctypes.c_size_t]
     L.tmg_last_kernel_count.argtypes = [vp]
     L.tmg_last_kernel_count.restype = i32
+    L.tmg_profile_enable.argtypes = [vp, ctypes.c_int]
+    L.tmg_profile_read.argtypes = [vp, ctypes.c_char_p, ctypes.c_int, P(ctypes.c_double),
+                                   P(ctypes.c_double), ctypes.c_int, P(ctypes.c_int)]
     _lib = L
     return L
 

@@ -12,6 +12,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <vector>
 
 #include "../../include/truncmul_b200.h"
 #include "kernels.cuh"
@@ -51,8 +52,31 @@ struct ScanSlot {
   }
 };
 
+// Optional per-kernel CUDA-event timing on the launching stream.
+struct Profiler {
+  bool on = false;
+  struct Rec {
+    std::string name;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) throw Error(TMG_ERR_CUDA, "cudaEventCreate");
+    return e;
+  }
+};
+
 struct Context {
   int device = 0;
+  Profiler prof;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   TwiddleCache tw;
@@ -100,6 +124,27 @@ void set_smem(K kernel, size_t bytes) {
                                   int(bytes)));
 }
 
+struct KTimer {
+  Context& cx;
+  Profiler::Rec rec;
+  bool on;
+  KTimer(Context& c, const char* name, double bytes) : cx(c), on(c.prof.on) {
+    if (on) {
+      rec.name = name;
+      rec.bytes = bytes;
+      rec.a = cx.prof.get();
+      rec.b = cx.prof.get();
+      cudaEventRecord(rec.a, cx.stream);
+    }
+  }
+  ~KTimer() {
+    if (on) {
+      cudaEventRecord(rec.b, cx.stream);
+      cx.prof.recs.push_back(rec);
+    }
+  }
+};
+
 // Enqueue one batch of products (device pointers) on the context stream.
 void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
              uint64_t* dout, int64_t count, uint32_t* pflags) {
@@ -131,7 +176,10 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     a.mc = pl.mc;
     a.status = status;
     set_smem(k_small_product, pl.small_smem);
-    k_small_product<<<unsigned(count), pl.small_threads, pl.small_smem, st>>>(a);
+    {
+      KTimer kt(cx, "k_small_product", double(count) * double(2 * pl.nlimbs + pl.out_limbs) * 8.0);
+      k_small_product<<<unsigned(count), pl.small_threads, pl.small_smem, st>>>(a);
+    }
     check_launch("k_small_product");
     cx.last_kernels = 1;
     return;
@@ -165,7 +213,10 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.scan_u = cx.scan_u.next(blocks);
       a.scan_v = cx.scan_v.next(blocks);
       a.status = status;
-      k_split_scan<<<dim3(blocks, 2), kSplitThreads, 0, st>>>(a);
+      {
+        KTimer kt(cx, "k_split_scan", double(2 * pl.nlimbs) * 8.0 + double(2 * pl.count) / 8.0);
+        k_split_scan<<<dim3(blocks, 2), kSplitThreads, 0, st>>>(a);
+      }
       check_launch("k_split_scan");
       ++kernels;
     }
@@ -188,7 +239,10 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.mc = pl.mc;
       a.aux = cx.aux.as<double>();
       set_smem(k_f1, pl.smem_f1);
-      k_f1<<<a.ncols >> a.logc, pl.thr_f1, pl.smem_f1, st>>>(a);
+      {
+        KTimer kt(cx, "k_f1", double(2 * pl.nlimbs) * 8.0 + double(L) * 16.0);
+        k_f1<<<a.ncols >> a.logc, pl.thr_f1, pl.smem_f1, st>>>(a);
+      }
       check_launch("k_f1");
       ++kernels;
     }
@@ -208,7 +262,10 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.tc = 1;
       a.tmul = pl.A;
       set_smem(k_col, pl.smem_f2);
-      k_col<<<dim3(pl.C >> a.logc, pl.A), pl.thr_f2, pl.smem_f2, st>>>(a);
+      {
+        KTimer kt(cx, "k_col_f2", double(L) * 32.0);
+        k_col<<<dim3(pl.C >> a.logc, pl.A), pl.thr_f2, pl.smem_f2, st>>>(a);
+      }
       check_launch("k_col(f2)");
       ++kernels;
     }
@@ -225,7 +282,10 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.scale = 1.0 / (4.0 * double(L));
       set_smem(k_mid, pl.smem_mid);
       const unsigned grid = (pl.A * pl.B) / 2 + 1;
-      k_mid<<<grid, pl.thr_mid, pl.smem_mid, st>>>(a);
+      {
+        KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0);
+        k_mid<<<grid, pl.thr_mid, pl.smem_mid, st>>>(a);
+      }
       check_launch("k_mid");
       ++kernels;
     }
@@ -245,7 +305,10 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.tc = 0;
       a.tmul = pl.C;
       set_smem(k_col, pl.smem_i2);
-      k_col<<<dim3((pl.C / 2) >> a.logc, pl.A), pl.thr_i2, pl.smem_i2, st>>>(a);
+      {
+        KTimer kt(cx, "k_col_i2", double(L) * 16.0);
+        k_col<<<dim3((pl.C / 2) >> a.logc, pl.A), pl.thr_i2, pl.smem_i2, st>>>(a);
+      }
       check_launch("k_col(i2)");
       ++kernels;
     }
@@ -262,7 +325,10 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.logc = pl.logc_il;
       a.fft = pl.iA;
       set_smem(k_ilast, pl.smem_il);
-      k_ilast<<<a.g.ncols >> a.logc, pl.thr_il, pl.smem_il, st>>>(a);
+      {
+        KTimer kt(cx, "k_ilast", double(L) * 16.0);
+        k_ilast<<<a.g.ncols >> a.logc, pl.thr_il, pl.smem_il, st>>>(a);
+      }
       check_launch("k_ilast");
       ++kernels;
     }
@@ -288,7 +354,10 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
         a.tbuf = nullptr;
       }
       set_smem(k_carry, pl.smem_carry);
-      k_carry<<<blocks, kCarryThreads, pl.smem_carry, st>>>(a);
+      {
+        KTimer kt(cx, "k_carry", double(pl.K) * 8.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0);
+        k_carry<<<blocks, kCarryThreads, pl.smem_carry, st>>>(a);
+      }
       check_launch("k_carry");
       ++kernels;
     }
@@ -305,7 +374,10 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       const unsigned blocks = unsigned((a.WL + LB - 1) / LB);
       a.scan = cx.scan_h.next(blocks);
       a.status = status;
-      k_high_round<<<blocks, kCarryThreads, 0, st>>>(a);
+      {
+        KTimer kt(cx, "k_high_round", double(pl.ML) * 8.0 + double(pl.out_limbs) * 8.0);
+        k_high_round<<<blocks, kCarryThreads, 0, st>>>(a);
+      }
       check_launch("k_high_round");
       ++kernels;
     }
@@ -659,5 +731,37 @@ int tmg_memcpy_d2h(tmg_context* ctx, void* dst, const void* src, size_t bytes) {
   });
 }
 int32_t tmg_last_kernel_count(tmg_context* ctx) { return ctx->cx.last_kernels; }
+
+int tmg_profile_enable(tmg_context* ctx, int on) {
+  return guarded([&] {
+    ctx->cx.prof.on = on != 0;
+    return TMG_OK;
+  });
+}
+
+int tmg_profile_read(tmg_context* ctx, char* names, int name_stride, double* ms,
+                     double* bytes, int max_records, int* count) {
+  return guarded([&] {
+    Profiler& P = ctx->cx.prof;
+    TMG_CUDA(cudaStreamSynchronize(ctx->cx.stream));
+    int n = 0;
+    for (auto& r : P.recs) {
+      if (n < max_records) {
+        float t = 0.f;
+        TMG_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        std::strncpy(names + size_t(n) * name_stride, r.name.c_str(), size_t(name_stride - 1));
+        names[size_t(n) * name_stride + name_stride - 1] = 0;
+        ms[n] = double(t);
+        bytes[n] = r.bytes;
+        ++n;
+      }
+      P.pool.push_back(r.a);
+      P.pool.push_back(r.b);
+    }
+    P.recs.clear();
+    *count = n;
+    return TMG_OK;
+  });
+}
 
 }  // extern "C"

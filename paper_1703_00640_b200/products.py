@@ -303,6 +303,25 @@ class Context:
     def last_kernel_count(self) -> int:
         return int(self._lib.tmg_last_kernel_count(self._h))
 
+    def profile(self, on: bool = True) -> None:
+        """Bracket every kernel launch with CUDA events on the context stream."""
+        _check(self._lib.tmg_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self, max_records: int = 4096) -> list[tuple[str, float, float]]:
+        """[(kernel name, milliseconds, algorithmic bytes)] since the last read."""
+        stride = 32
+        names = ctypes.create_string_buffer(stride * max_records)
+        ms = (ctypes.c_double * max_records)()
+        by = (ctypes.c_double * max_records)()
+        cnt = ctypes.c_int(0)
+        _check(self._lib.tmg_profile_read(self._h, names, stride, ms, by, max_records,
+                                          ctypes.byref(cnt)))
+        out = []
+        for i in range(cnt.value):
+            nm = names.raw[i * stride:(i + 1) * stride].split(b"\0", 1)[0].decode()
+            out.append((nm, ms[i], by[i]))
+        return out
+
 
 _default: dict[int, Context] = {}
 _default_lock = threading.Lock()

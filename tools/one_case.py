@@ -18,6 +18,6 @@ r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
 print("gpu done", time.time() - t0, ctx.last_stats, flush=True)
 P = port.limbs_to_int(port.oracle_full(u, v))
 if mode == tm.Mode.FULL: ok = r == P
-elif mode == tm.Mode.LOW: ok = r == P % (1 << n)
+elif mode == tm.Mode.LOW: ok = r == (P & ((1 << n) - 1))
 else: ok = port.is_valid_high(u, v, n, r)
 print("ok", ok, flush=True)

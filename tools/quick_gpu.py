@@ -20,7 +20,7 @@ for n in [int(x) for x in (sys.argv[1:] or ["8192", "5001", "65536", "262144", "
             r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
             dt = time.time() - t0
             if mode == tm.Mode.FULL: ok = r == P
-            elif mode == tm.Mode.LOW: ok = r == P % (1 << n)
+            elif mode == tm.Mode.LOW: ok = r == (P & ((1 << n) - 1))
             else: ok = port.is_valid_high(u, v, n, r)
             s = ctx.last_stats
             print(f"n={n} {mode.name} b={p.b} N={p.N} L={s.transform_length} passes={s.passes} ok={ok} err={s.max_round_err:.4f} t={dt*1e3:.2f}ms", flush=True)
