@@ -128,9 +128,11 @@ struct KTimer {
   Context& cx;
   Profiler::Rec rec;
   bool on;
-  KTimer(Context& c, const char* name, double bytes) : cx(c), on(c.prof.on) {
+  KTimer(Context& c, const char* name, double bytes, int mode = -1)
+      : cx(c), on(c.prof.on) {
     if (on) {
-      rec.name = name;
+      static const char* kPrefix[] = {"full:", "low:", "high:"};
+      rec.name = std::string(mode >= 0 && mode < 3 ? kPrefix[mode] : "") + name;
       rec.bytes = bytes;
       rec.a = cx.prof.get();
       rec.b = cx.prof.get();
@@ -177,7 +179,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     a.status = status;
     set_smem(k_small_product, pl.small_smem);
     {
-      KTimer kt(cx, "k_small_product", double(count) * double(2 * pl.nlimbs + pl.out_limbs) * 8.0);
+      KTimer kt(cx, "k_small_product", double(count) * double(2 * pl.nlimbs + pl.out_limbs) * 8.0, int(p.mode));
       k_small_product<<<unsigned(count), pl.small_threads, pl.small_smem, st>>>(a);
     }
     check_launch("k_small_product");
@@ -214,7 +216,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.scan_v = cx.scan_v.next(blocks);
       a.status = status;
       {
-        KTimer kt(cx, "k_split_scan", double(2 * pl.nlimbs) * 8.0 + double(2 * pl.count) / 8.0);
+        KTimer kt(cx, "k_split_scan", double(2 * pl.nlimbs) * 8.0 + double(2 * pl.count) / 8.0, int(p.mode));
         k_split_scan<<<dim3(blocks, 2), kSplitThreads, 0, st>>>(a);
       }
       check_launch("k_split_scan");
@@ -240,7 +242,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.aux = cx.aux.as<double>();
       set_smem(k_f1, pl.smem_f1);
       {
-        KTimer kt(cx, "k_f1", double(2 * pl.nlimbs) * 8.0 + double(L) * 16.0);
+        KTimer kt(cx, "k_f1", double(2 * pl.nlimbs) * 8.0 + double(L) * 16.0, int(p.mode));
         k_f1<<<a.ncols >> a.logc, pl.thr_f1, pl.smem_f1, st>>>(a);
       }
       check_launch("k_f1");
@@ -263,7 +265,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.tmul = pl.A;
       set_smem(k_col, pl.smem_f2);
       {
-        KTimer kt(cx, "k_col_f2", double(L) * 32.0);
+        KTimer kt(cx, "k_col_f2", double(L) * 32.0, int(p.mode));
         k_col<<<dim3(pl.C >> a.logc, pl.A), pl.thr_f2, pl.smem_f2, st>>>(a);
       }
       check_launch("k_col(f2)");
@@ -283,7 +285,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       set_smem(k_mid, pl.smem_mid);
       const unsigned grid = (pl.A * pl.B) / 2 + 1;
       {
-        KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0);
+        KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode));
         k_mid<<<grid, pl.thr_mid, pl.smem_mid, st>>>(a);
       }
       check_launch("k_mid");
@@ -306,7 +308,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.tmul = pl.C;
       set_smem(k_col, pl.smem_i2);
       {
-        KTimer kt(cx, "k_col_i2", double(L) * 16.0);
+        KTimer kt(cx, "k_col_i2", double(L) * 16.0, int(p.mode));
         k_col<<<dim3((pl.C / 2) >> a.logc, pl.A), pl.thr_i2, pl.smem_i2, st>>>(a);
       }
       check_launch("k_col(i2)");
@@ -326,7 +328,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.fft = pl.iA;
       set_smem(k_ilast, pl.smem_il);
       {
-        KTimer kt(cx, "k_ilast", double(L) * 16.0);
+        KTimer kt(cx, "k_ilast", double(L) * 16.0, int(p.mode));
         k_ilast<<<a.g.ncols >> a.logc, pl.thr_il, pl.smem_il, st>>>(a);
       }
       check_launch("k_ilast");
@@ -355,7 +357,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       }
       set_smem(k_carry, pl.smem_carry);
       {
-        KTimer kt(cx, "k_carry", double(pl.K) * 8.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0);
+        KTimer kt(cx, "k_carry", double(pl.K) * 8.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0, int(p.mode));
         k_carry<<<blocks, kCarryThreads, pl.smem_carry, st>>>(a);
       }
       check_launch("k_carry");
@@ -375,7 +377,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.scan = cx.scan_h.next(blocks);
       a.status = status;
       {
-        KTimer kt(cx, "k_high_round", double(pl.ML) * 8.0 + double(pl.out_limbs) * 8.0);
+        KTimer kt(cx, "k_high_round", double(pl.ML) * 8.0 + double(pl.out_limbs) * 8.0, int(p.mode));
         k_high_round<<<blocks, kCarryThreads, 0, st>>>(a);
       }
       check_launch("k_high_round");
