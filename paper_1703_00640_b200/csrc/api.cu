@@ -211,13 +211,15 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.lead = pl.lead;
       a.cbits_u = cx.cbu.as<uint32_t>();
       a.cbits_v = cx.cbv.as<uint32_t>();
-      const unsigned blocks = unsigned((pl.count + kSplitThreads * 32 - 1) / (kSplitThreads * 32));
+      const unsigned blocks = unsigned((pl.count + kSplitChunks - 1) / kSplitChunks);
+      const size_t ssm = split_scan_smem(p.b);
+      set_smem(k_split_scan, ssm);
       a.scan_u = cx.scan_u.next(blocks);
       a.scan_v = cx.scan_v.next(blocks);
       a.status = status;
       {
         KTimer kt(cx, "k_split_scan", double(2 * pl.nlimbs) * 8.0 + double(2 * pl.count) / 8.0, int(p.mode));
-        k_split_scan<<<dim3(blocks, 2), kSplitThreads, 0, st>>>(a);
+        k_split_scan<<<dim3(blocks, 2), kSplitThreads, ssm, st>>>(a);
       }
       check_launch("k_split_scan");
       ++kernels;

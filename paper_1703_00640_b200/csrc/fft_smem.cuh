@@ -160,6 +160,149 @@ __device__ __forceinline__ void fft_smem(double2* __restrict__ buf, const Lay& l
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pass driver with external source and sink: the first stage reads its
+// butterfly inputs straight from src(item, e) (global memory: every thread
+// issues all of its loads before the first use), the last stage hands its
+// outputs to sink(item, k, value) (global memory with the inter-pass
+// twiddle).  Intermediate stages exchange through shared memory.  With a
+// single stage no shared memory is touched.
+
+template <int RAD, class Lay, class Src>
+__device__ __forceinline__ void stage_load_src(double2 (&x)[kXMax], const Lay& lay,
+                                               uint32_t R, const Src& src, int tid,
+                                               int nthr) {
+  constexpr int NB = (16 + RAD - 1) / RAD;
+  const uint32_t nbf_item = R / RAD;
+  const uint32_t nbf = nbf_item * lay.nitems();
+#pragma unroll
+  for (int it = 0; it < NB; ++it) {
+    uint32_t bf = tid + it * nthr;
+    if (bf < nbf) {
+      uint32_t item, t;
+      lay.split(bf, nbf_item, item, t);
+#pragma unroll
+      for (int q = 0; q < RAD; ++q) x[it * RAD + q] = src(item, t + q * nbf_item);
+    }
+  }
+}
+
+template <int RAD, bool INV, class Lay, class Sink>
+__device__ __forceinline__ void stage_store_sink(double2 (&x)[kXMax], const Lay& lay,
+                                                 uint32_t R, uint32_t Ns,
+                                                 const FastDiv& fdNs, uint32_t twstep,
+                                                 const double2* __restrict__ tw,
+                                                 const Sink& sink, int tid, int nthr) {
+  constexpr int NB = (16 + RAD - 1) / RAD;
+  const uint32_t nbf_item = R / RAD;
+  const uint32_t nbf = nbf_item * lay.nitems();
+#pragma unroll
+  for (int it = 0; it < NB; ++it) {
+    uint32_t bf = tid + it * nthr;
+    if (bf < nbf) {
+      uint32_t item, t;
+      lay.split(bf, nbf_item, item, t);
+      uint32_t tq = fdiv(t, fdNs);
+      uint32_t j = t - tq * Ns;
+      double2* xv = x + it * RAD;
+      if (j != 0) {
+        uint32_t step = j * twstep;
+#pragma unroll
+        for (int q = 1; q < RAD; ++q) {
+          double2 w = __ldg(tw + step * q);
+          xv[q] = INV ? cmulc(xv[q], w) : cmul(xv[q], w);
+        }
+      }
+      dft<RAD, INV>(xv);
+      uint32_t ob = tq * Ns * RAD + j;
+#pragma unroll
+      for (int q = 0; q < RAD; ++q) sink(item, ob + q * Ns, xv[q]);
+    }
+  }
+}
+
+#define TMG_RADIX_SWITCH(rad, CALL) \
+  switch (rad) {                    \
+    case 16: CALL(16); break;       \
+    case 8: CALL(8); break;         \
+    case 4: CALL(4); break;         \
+    case 2: CALL(2); break;         \
+    case 3: CALL(3); break;         \
+    case 5: CALL(5); break;         \
+    default: CALL(7); break;        \
+  }
+
+template <bool INV, class Lay, class Src, class Sink>
+__device__ __forceinline__ void fft_pass(double2* __restrict__ buf, const Lay& lay,
+                                         const SubFft& p, const Src& src,
+                                         const Sink& sink, int tid, int nthr) {
+  double2 x[kXMax];
+  const int last = p.nst - 1;
+  {
+    const int rad = p.rad[0];
+#define TMG_L0(RR) stage_load_src<RR>(x, lay, p.R, src, tid, nthr)
+    TMG_RADIX_SWITCH(rad, TMG_L0)
+#undef TMG_L0
+    __syncthreads();  // src may alias buf
+    const FastDiv fd = p.fdNs[0];
+    if (last == 0) {
+#define TMG_S0(RR) stage_store_sink<RR, INV>(x, lay, p.R, 1u, fd, p.twstep[0], p.tw, sink, tid, nthr)
+      TMG_RADIX_SWITCH(rad, TMG_S0)
+#undef TMG_S0
+      return;
+    }
+#define TMG_S0B(RR) stage_store<RR, INV>(x, buf, lay, p.R, 1u, fd, p.twstep[0], p.tw, tid, nthr)
+    TMG_RADIX_SWITCH(rad, TMG_S0B)
+#undef TMG_S0B
+    __syncthreads();
+  }
+  for (int s = 1; s < last; ++s) {
+    const int rad = p.rad[s];
+#define TMG_LM(RR) stage_load<RR>(x, buf, lay, p.R, tid, nthr)
+    TMG_RADIX_SWITCH(rad, TMG_LM)
+#undef TMG_LM
+    __syncthreads();
+    const uint32_t Ns = p.Ns[s];
+    const uint32_t ts = p.twstep[s];
+    const FastDiv fd = p.fdNs[s];
+#define TMG_SM(RR) stage_store<RR, INV>(x, buf, lay, p.R, Ns, fd, ts, p.tw, tid, nthr)
+    TMG_RADIX_SWITCH(rad, TMG_SM)
+#undef TMG_SM
+    __syncthreads();
+  }
+  {
+    const int rad = p.rad[last];
+#define TMG_LL(RR) stage_load<RR>(x, buf, lay, p.R, tid, nthr)
+    TMG_RADIX_SWITCH(rad, TMG_LL)
+#undef TMG_LL
+    __syncthreads();  // sink may alias buf
+    const uint32_t Ns = p.Ns[last];
+    const uint32_t ts = p.twstep[last];
+    const FastDiv fd = p.fdNs[last];
+#define TMG_SL(RR) stage_store_sink<RR, INV>(x, lay, p.R, Ns, fd, ts, p.tw, sink, tid, nthr)
+    TMG_RADIX_SWITCH(rad, TMG_SL)
+#undef TMG_SL
+  }
+}
+
+// Shared-memory source and sink for fft_pass.
+template <class Lay>
+struct SmemSrc {
+  const double2* buf;
+  Lay lay;
+  __device__ __forceinline__ double2 operator()(uint32_t item, uint32_t e) const {
+    return buf[lay.idx(item, e)];
+  }
+};
+template <class Lay>
+struct SmemSink {
+  double2* buf;
+  Lay lay;
+  __device__ __forceinline__ void operator()(uint32_t item, uint32_t k, double2 v) const {
+    buf[lay.idx(item, k)] = v;
+  }
+};
+
 // Global twiddle omega_L^x for x < L from a two-level table:
 // omega^x = hi[x >> S] * lo[x & (2^S - 1)].
 struct TwGlobal {

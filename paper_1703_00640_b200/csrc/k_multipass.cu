@@ -2,12 +2,13 @@
 //
 //   k_split_scan  carry-in bits of the balanced split (decoupled look-back)
 //   k_f1          limbs -> chunks -> pre-map -> column DFTs over A, twiddle
-//   k_col         generic in-place column pass (forward over B, inverse over B)
+//   k_col         generic column pass (forward over B, inverse over B)
 //   k_mid         row DFTs over C for a conjugate row pair, spectral product,
 //                 half-length inverse row DFT, twiddle
 //   k_ilast       inverse column DFTs over A -> convolution coefficients
 //   k_carry       post-map, rounding tripwire, recombination lanes, carry
 //                 propagation (decoupled look-back), output limbs
+//   k_high_round  round(t / 2^s) of the high product (second carry scan)
 //
 // Reference path: products_f64.cpp:106-171 with the FFTW convolution of
 // convolution.cpp:175-195.
@@ -17,27 +18,22 @@ namespace tmg {
 
 // ---------------------------------------------------------------------------
 // Sequential reader of consecutive b-bit windows of u * 2^lead.
+template <class Ld>
 struct WindowReader {
-  const uint64_t* limbs;
-  int64_t nlimbs;
+  Ld ld;
   int64_t idx;
   uint32_t sh;
   uint64_t cur, nxt;
   int b;
   uint64_t mask;
-  __device__ __forceinline__ uint64_t load(int64_t i) const {
-    return (i >= 0 && i < nlimbs) ? __ldg(limbs + i) : 0ull;
-  }
-  __device__ __forceinline__ void init(const uint64_t* l, int64_t nl,
-                                       int64_t pos, int bb) {
-    limbs = l;
-    nlimbs = nl;
+  __device__ __forceinline__ void init(const Ld& l, int64_t pos, int bb) {
+    ld = l;
     b = bb;
     mask = (1ull << bb) - 1;
     idx = pos >> 6;
     sh = uint32_t(pos & 63);
-    cur = load(idx);
-    nxt = load(idx + 1);
+    cur = ld(idx);
+    nxt = ld(idx + 1);
   }
   __device__ __forceinline__ uint64_t next() {
     uint64_t w = sh ? ((cur >> sh) | (nxt << (64 - sh))) : cur;
@@ -46,9 +42,26 @@ struct WindowReader {
       sh -= 64;
       cur = nxt;
       ++idx;
-      nxt = load(idx + 1);
+      nxt = ld(idx + 1);
     }
     return w & mask;
+  }
+};
+
+struct GlobalLimbs {
+  const uint64_t* limbs;
+  int64_t nlimbs;
+  __device__ __forceinline__ uint64_t operator()(int64_t i) const {
+    return (i >= 0 && i < nlimbs) ? __ldg(limbs + i) : 0ull;
+  }
+};
+
+struct SmemLimbs {
+  const uint64_t* s;  // s[i - i0] for i in [i0, i0 + n)
+  int64_t i0, n;
+  __device__ __forceinline__ uint64_t operator()(int64_t i) const {
+    const int64_t o = i - i0;
+    return (o >= 0 && o < n) ? s[o] : 0ull;
   }
 };
 
@@ -64,9 +77,28 @@ __device__ __forceinline__ double digit_at(const uint64_t* limbs,
   return double(split_digit(w, cbit(cb, j), b, j == count - 1));
 }
 
+__device__ __forceinline__ uint32_t take_ticket(unsigned long long* ctr) {
+  return uint32_t(atomicAdd(ctr, 1ull));
+}
+
+__device__ __forceinline__ void release_ticket(unsigned long long* ctr,
+                                               unsigned grid) {
+  __threadfence();
+  if (atomicAdd(ctr + 1, 1ull) == grid - 1) {
+    ctr[0] = 0;
+    ctr[1] = 0;
+  }
+}
+
 // ---------------------------------------------------------------------------
+// Balanced-split carry bits.  A block covers kSplitChunks chunks: it stages
+// the limbs under them in shared memory with coalesced loads, each thread
+// scans 32 consecutive chunks, and the block carry is resolved by a
+// warp-parallel decoupled look-back (split.cpp:294-298 made parallel).
 __global__ void __launch_bounds__(kSplitThreads)
 k_split_scan(SplitScanArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* sl = reinterpret_cast<uint64_t*>(smem_raw);
   __shared__ uint32_t sw[32];
   __shared__ uint32_t s_blk;
   __shared__ int s_cin;
@@ -75,50 +107,113 @@ k_split_scan(SplitScanArgs a) {
   uint32_t* cbits = isv ? a.cbits_v : a.cbits_u;
   ScanState sc = isv ? a.scan_v : a.scan_u;
   const int tid = threadIdx.x;
-  if (tid == 0) s_blk = uint32_t(atomicAdd(sc.ctr, 1ull));
+  if (tid == 0) s_blk = take_ticket(sc.ctr);
   __syncthreads();
   const uint32_t blk = s_blk;
-  const int64_t base = int64_t(blk) * (kSplitThreads * 32) + int64_t(tid) * 32;
   const int b = a.b;
+  const int64_t c0 = int64_t(blk) * kSplitChunks;
+  const int64_t pos0 = c0 * b - a.lead;
+  const int64_t i0 = pos0 >> 6;
+  const int64_t nl = (int64_t(kSplitChunks) * b + 63) / 64 + 2;
+  for (int64_t i = tid; i < nl; i += kSplitThreads) {
+    const int64_t g = i0 + i;
+    sl[i] = (g >= 0 && g < a.nlimbs) ? __ldg(limbs + g) : 0ull;
+  }
+  __syncthreads();
+  const int64_t base = c0 + int64_t(tid) * 32;
   uint32_t f = kTfIdentity;
-  uint64_t wv[32];
+  uint32_t gen = 0, prop = 0;  // per-chunk generate / propagate bits
   {
-    WindowReader rd;
-    rd.init(limbs, a.nlimbs, base * b - a.lead, b);
-#pragma unroll
+    WindowReader<SmemLimbs> rd;
+    rd.init(SmemLimbs{sl, i0, nl}, base * b - a.lead, b);
+    const uint64_t half = 1ull << (b - 1);
+#pragma unroll 8
     for (int q = 0; q < 32; ++q) {
-      wv[q] = rd.next();
-      if (base + q < a.count - 1) f = tf_compose(f, split_tf(wv[q], b));
+      const uint64_t w = rd.next();
+      if (base + q < a.count - 1) {
+        gen |= uint32_t(w > half) << q;
+        prop |= uint32_t(w == half) << q;
+      }
+    }
+    // thread aggregate: the last non-propagating chunk decides
+    const uint32_t np = ~prop;
+    if (np) {
+      const int last = 31 - __clz(np);
+      f = ((gen >> last) & 1u) ? tf_const(1) : tf_const(0);
     }
   }
   uint32_t agg;
-  uint32_t ex = block_scan_tf(f, sw, &agg);
-  if (tid == 0) s_cin = lookback_carry(sc.state, blk, agg, sc.epoch, 0);
+  const uint32_t ex = block_scan_tf(f, sw, &agg);
+  if (tid < 32) {
+    const int cin = lookback_warp(sc.state, blk, agg, sc.epoch, 0);
+    if (tid == 0) s_cin = cin;
+  }
   __syncthreads();
+  // carry into each chunk: propagate chunks pass the carry through
   int c = tf_apply(ex, s_cin);
   uint32_t bits = 0;
 #pragma unroll
   for (int q = 0; q < 32; ++q) {
     bits |= uint32_t(c) << q;
-    c = tf_apply(split_tf(wv[q], b), c);
+    if (!((prop >> q) & 1u)) c = int((gen >> q) & 1u);
   }
   if (base < a.count) cbits[base >> 5] = bits;
   if (blk == 0 && tid == 0 && (a.n & 63)) {
     uint64_t top = __ldg(limbs + a.nlimbs - 1);
     if (top >> (a.n & 63)) atomicOr(&a.status->flags, uint32_t(kFlagInputRange));
   }
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(sc.ctr + 1, 1ull) == gridDim.x - 1) {
-      sc.ctr[0] = 0;
-      sc.ctr[1] = 0;
-    }
-  }
+  if (tid == 0) release_ticket(sc.ctr, gridDim.x);
 }
+
+size_t split_scan_smem(int b) {
+  return size_t((int64_t(kSplitChunks) * b + 63) / 64 + 2) * 8;
+}
+
+// ---------------------------------------------------------------------------
+// Column-pass sources and sinks.
+__device__ __forceinline__ int64_t col_off(const ColGeom& g, int64_t outer,
+                                           uint32_t row, uint32_t col) {
+  return outer * g.os + int64_t(row) * g.rs + int64_t(col / g.cw) * g.cs +
+         (col % g.cw);
+}
+
+struct ColSrc {
+  const double2* data;
+  ColGeom g;
+  int64_t outer;
+  uint32_t col0;
+  __device__ __forceinline__ double2 operator()(uint32_t item, uint32_t e) const {
+    return data[col_off(g, outer, e, col0 + item)];
+  }
+};
+
+struct ColSink {
+  double2* data;
+  ColGeom g;
+  int64_t outer;
+  uint32_t col0;
+  TwGlobal tw;
+  uint32_t to, tc, tmul;
+  bool inv, twiddle;
+  __device__ __forceinline__ void operator()(uint32_t item, uint32_t k, double2 v) const {
+    const uint32_t col = col0 + item;
+    if (twiddle) {
+      const uint32_t x = (uint32_t(outer) * to + col * tc) * k * tmul;
+      if (x) {
+        const double2 w = tw.get(x);
+        v = inv ? cmulc(v, w) : cmul(v, w);
+      }
+    }
+    data[col_off(g, outer, k, col)] = v;
+  }
+};
 
 // ---------------------------------------------------------------------------
 // F1: split + pre-map + forward column DFT over A (rows j_a, chunk index
 // j = j_a * ncols + col), twiddle omega_L^{col k_a}, store T[k_a][col].
+// Each thread produces whole row segments of c chunks: it streams the
+// c + lambda - 1 digits through a shift register (compile-time indexed, so
+// no local memory) and applies the pre-map as the window slides.
 __global__ void __launch_bounds__(512)
 k_f1(F1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -131,7 +226,9 @@ k_f1(F1Args a) {
   const int b = a.b;
   const int64_t N = mc.N;
   const int lam = (mc.mode == kModeFull) ? 1 : mc.lambda;
+  const double Nd = double(N);
   LayCols lay{a.logc, c - 1};
+  const GlobalLimbs gu{a.u, a.nlimbs}, gv{a.v, a.nlimbs};
 
   double topu = 0.0, topv = 0.0;
   if (mc.mode == kModeHigh && col0 < uint32_t(mc.nfold + mc.lambda)) {
@@ -139,16 +236,12 @@ k_f1(F1Args a) {
     topv = digit_at(a.v, a.nlimbs, b, a.lead, a.count, a.cbits_v, N);
   }
   if (mc.mode == kModeHigh && blockIdx.x == 0 && tid == 0) {
-    auto Du = [&](int64_t i) {
-      return digit_at(a.u, a.nlimbs, b, a.lead, a.count, a.cbits_u, i);
-    };
-    auto Dv = [&](int64_t i) {
-      return digit_at(a.v, a.nlimbs, b, a.lead, a.count, a.cbits_v, i);
-    };
+    auto Du = [&](int64_t i) { return digit_at(a.u, a.nlimbs, b, a.lead, a.count, a.cbits_u, i); };
+    auto Dv = [&](int64_t i) { return digit_at(a.v, a.nlimbs, b, a.lead, a.count, a.cbits_v, i); };
     a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
   }
+  const int fam = (mc.mode == kModeLow) ? 0 : 2;
 
-  // 1. inputs: one thread per row segment of c columns (plus lam-1 halo).
   for (uint32_t row = tid; row < A; row += nthr) {
     const int64_t j0 = int64_t(row) * a.ncols + col0;
     if (mc.mode == kModeFull) {
@@ -156,86 +249,93 @@ k_f1(F1Args a) {
         for (uint32_t q = 0; q < c; ++q) sbuf[lay.idx(q, row)] = make_double2(0.0, 0.0);
         continue;
       }
-      WindowReader ru, rv;
-      ru.init(a.u, a.nlimbs, j0 * b, b);
-      rv.init(a.v, a.nlimbs, j0 * b, b);
-      
+      WindowReader<GlobalLimbs> ru, rv;
+      ru.init(gu, j0 * b, b);
+      rv.init(gv, j0 * b, b);
       for (uint32_t q = 0; q < c; ++q) {
         const int64_t j = j0 + q;
-        uint64_t wu = ru.next(), wv = rv.next();
+        const uint64_t wu = ru.next(), wv = rv.next();
         double du = 0.0, dv = 0.0;
         if (j < N) {
           du = double(split_digit(wu, cbit(a.cbits_u, j), b, j == a.count - 1));
           dv = double(split_digit(wv, cbit(a.cbits_v, j), b, j == a.count - 1));
         }
         sbuf[lay.idx(q, row)] = make_double2(du, dv);
-
-
       }
       continue;
     }
-    // low / high: digits of chunks j0 - (lam-1) .. j0 + c - 1
+    // low / high: window of digits d[j - r], r < lam, in a shift register
     const int64_t js = j0 - (lam - 1);
-    double du[kMaxLambda + 64], dv[kMaxLambda + 64];  // c + lam - 1 <= 72
-    const int cnt = int(c) + lam - 1;
-    if (js >= 0) {
-      WindowReader ru, rv;
-      ru.init(a.u, a.nlimbs, js * b - a.lead, b);
-      rv.init(a.v, a.nlimbs, js * b - a.lead, b);
-      for (int q = 0; q < cnt; ++q) {
-        const int64_t j = js + q;
-        uint64_t wu = ru.next(), wv = rv.next();
-        du[q] = double(split_digit(wu, cbit(a.cbits_u, j), b, j == a.count - 1));
-        dv[q] = double(split_digit(wv, cbit(a.cbits_v, j), b, j == a.count - 1));
-      }
-    } else {
-      for (int q = 0; q < cnt; ++q) {
-        int64_t j = js + q;
-        if (j < 0) j += N;
-        du[q] = digit_at(a.u, a.nlimbs, b, a.lead, a.count, a.cbits_u, j);
-        dv[q] = digit_at(a.v, a.nlimbs, b, a.lead, a.count, a.cbits_v, j);
-      }
+    double wu[kMaxLambda], wv[kMaxLambda];
+#pragma unroll
+    for (int r = 0; r < kMaxLambda; ++r) wu[r] = wv[r] = 0.0;
+    WindowReader<GlobalLimbs> ru, rv;
+    const bool fast = js >= 0;
+    if (fast) {
+      ru.init(gu, js * b - a.lead, b);
+      rv.init(gv, js * b - a.lead, b);
     }
-    for (uint32_t q = 0; q < c; ++q) {
-      const int64_t j = j0 + q;
-      const int o = int(q) + lam - 1;  // position of chunk j in du/dv
-      auto Du = [&](int64_t k) {
-        int64_t d = j - k;
-        if (d < 0) d += N;
-        return du[o - int(d)];
-      };
-      auto Dv = [&](int64_t k) {
-        int64_t d = j - k;
-        if (d < 0) d += N;
-        return dv[o - int(d)];
-      };
-      sbuf[lay.idx(q, row)] =
-          make_double2(premap(mc, Du, j, topu), premap(mc, Dv, j, topv));
+    const int cnt = int(c) + lam - 1;
+    for (int q = 0; q < cnt; ++q) {
+      const int64_t j = js + q;
+      double du, dv;
+      if (fast) {
+        const uint64_t xu = ru.next(), xv = rv.next();
+        du = double(split_digit(xu, cbit(a.cbits_u, j), b, j == a.count - 1));
+        dv = double(split_digit(xv, cbit(a.cbits_v, j), b, j == a.count - 1));
+      } else {
+        const int64_t jj = j < 0 ? j + N : j;
+        du = digit_at(a.u, a.nlimbs, b, a.lead, a.count, a.cbits_u, jj);
+        dv = digit_at(a.v, a.nlimbs, b, a.lead, a.count, a.cbits_v, jj);
+      }
+#pragma unroll
+      for (int r = kMaxLambda - 1; r > 0; --r) {
+        wu[r] = wu[r - 1];
+        wv[r] = wv[r - 1];
+      }
+      wu[0] = du;
+      wv[0] = dv;
+      if (q >= lam - 1) {
+        // transform index j; digit d[(j - r) mod N] sits in w*[r]
+        double au = 0.0, av = 0.0;
+#pragma unroll
+        for (int r = 0; r < kMaxLambda; ++r) {
+          if (r < lam) {
+            int64_t k = j - r;
+            if (k < 0) k += N;
+            const double cf = series_coef(fam, r, double(k), Nd, mc.cpre[r]);
+            au += wu[r] * cf;
+            av += wv[r] * cf;
+          }
+        }
+        if (mc.mode == kModeHigh && j < mc.nfold + mc.lambda) {
+          for (int r = 0; r < mc.lambda; ++r) {
+            int64_t k = j - r;
+            if (k < 0) k += N;
+            if (k < mc.nfold) {
+              const double g = mc.fold[k] * series_coef(2, r, double(k), Nd, mc.cpre[r]);
+              au += topu * g;
+              av += topv * g;
+            }
+          }
+        }
+        sbuf[lay.idx(uint32_t(q - (lam - 1)), row)] = make_double2(au, av);
+      }
     }
   }
   __syncthreads();
 
-  // 2. column DFTs
-  fft_smem<false>(sbuf, lay, a.fft, tid, nthr);
-
-  // 3. twiddle and store
-  const uint32_t tot = A * c;
-  for (uint32_t e = tid; e < tot; e += nthr) {
-    const uint32_t ka = e >> a.logc, q = e & (c - 1);
-    const uint32_t col = col0 + q;
-    double2 z = sbuf[lay.idx(q, ka)];
-    z = cmul(z, a.tw.get(col * ka));
-    a.out[int64_t(ka) * a.ncols + col] = z;
-  }
+  ColGeom g;
+  g.os = 0;
+  g.rs = a.ncols;
+  g.cs = 0;
+  g.cw = 0xffffffffu;
+  g.ncols = a.ncols;
+  ColSink sink{a.out, g, 0, col0, a.tw, 0u, 1u, 1u, false, true};
+  fft_pass<false>(sbuf, lay, a.fft, SmemSrc<LayCols>{sbuf, lay}, sink, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int64_t col_off(const ColGeom& g, int64_t outer,
-                                           uint32_t row, uint32_t col) {
-  return outer * g.os + int64_t(row) * g.rs + int64_t(col / g.cw) * g.cs +
-         (col % g.cw);
-}
-
 __global__ void __launch_bounds__(512)
 k_col(ColArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -244,31 +344,36 @@ k_col(ColArgs a) {
   const uint32_t c = 1u << a.logc;
   const uint32_t col0 = blockIdx.x * c;
   const int64_t outer = blockIdx.y;
-  const uint32_t R = a.fft.R;
   LayCols lay{a.logc, c - 1};
-  const uint32_t tot = R * c;
-  for (uint32_t e = tid; e < tot; e += nthr) {
-    const uint32_t row = e >> a.logc, q = e & (c - 1);
-    sbuf[lay.idx(q, row)] = a.data[col_off(a.g, outer, row, col0 + q)];
-  }
-  __syncthreads();
-  if (a.inv) fft_smem<true>(sbuf, lay, a.fft, tid, nthr);
-  else fft_smem<false>(sbuf, lay, a.fft, tid, nthr);
-  for (uint32_t e = tid; e < tot; e += nthr) {
-    const uint32_t k = e >> a.logc, q = e & (c - 1);
-    const uint32_t col = col0 + q;
-    double2 z = sbuf[lay.idx(q, k)];
-    const uint32_t x = (uint32_t(outer) * a.to + col * a.tc) * k * a.tmul;
-    if (x) {
-      double2 w = a.tw.get(x);
-      z = a.inv ? cmulc(z, w) : cmul(z, w);
-    }
-    a.data[col_off(a.g, outer, k, col)] = z;
-  }
+  ColSrc src{a.data, a.g, outer, col0};
+  ColSink sink{a.data, a.g, outer, col0, a.tw, a.to, a.tc, a.tmul, a.inv != 0, true};
+  if (a.inv) fft_pass<true>(sbuf, lay, a.fft, src, sink, tid, nthr);
+  else fft_pass<false>(sbuf, lay, a.fft, src, sink, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
 // Row pass: conjugate row pair (r, AB - r), r = k_a + A k_b.
+struct RowSrc {
+  const double2* data;
+  int64_t base0, base1;
+  __device__ __forceinline__ double2 operator()(uint32_t item, uint32_t e) const {
+    return data[(item ? base1 : base0) + e];
+  }
+};
+
+struct RowSink {
+  double2* data;
+  int64_t base0, base1;
+  uint32_t r0, r1;
+  TwGlobal tw;
+  __device__ __forceinline__ void operator()(uint32_t item, uint32_t m, double2 v) const {
+    const uint32_t r = item ? r1 : r0;
+    const uint32_t x = 2u * r * m;  // omega_{L/2}^{r m} = omega_L^{2 r m}
+    if (x) v = cmulc(v, tw.get(x));
+    data[(item ? base1 : base0) + m] = v;
+  }
+};
+
 __global__ void __launch_bounds__(512)
 k_mid(MidArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -281,56 +386,52 @@ k_mid(MidArgs a) {
   const uint32_t nrows = (r1 == r0) ? 1 : 2;
   const uint32_t rowstride = padded_len(C) + 4;
   LayRows lay{nrows, rowstride};
-  const uint32_t rr[2] = {r0, r1};
-  int64_t base[2];
-  for (uint32_t i = 0; i < nrows; ++i) {
-    const uint32_t r = rr[i];
-    base[i] = (int64_t(r % a.A) * a.B + (r / a.A)) * int64_t(C);
-  }
-  for (uint32_t e = tid; e < nrows * C; e += nthr) {
-    const uint32_t i = e >= C ? 1 : 0, k = e - i * C;
-    sbuf[lay.idx(i, k)] = a.data[base[i] + k];
-  }
-  __syncthreads();
-  fft_smem<false>(sbuf, lay, a.fwd, tid, nthr);
+  const int64_t base0 = (int64_t(r0 % a.A) * a.B + (r0 / a.A)) * int64_t(C);
+  const int64_t base1 = (int64_t(r1 % a.A) * a.B + (r1 / a.A)) * int64_t(C);
 
-  // spectral product over the pair
+  fft_pass<false>(sbuf, lay, a.fwd, RowSrc{a.data, base0, base1},
+                  SmemSink<LayRows>{sbuf, lay}, tid, nthr);
+  __syncthreads();
+
+  // spectral product over the pair:
+  // W_k = (Z_k + conj Z_-k)(Z_k - conj Z_-k) / (4 i L), W_-k = conj W_k
   const uint32_t brw = (r0 != 0) ? 1u : 0u;  // borrow of -k when r != 0
   for (uint32_t k = tid; k < C; k += nthr) {
-    const uint32_t kp = (C - k - brw) % C;   // partner column
+    const uint32_t kp = (C - k - brw) % C;
     const uint32_t ip = (nrows == 2) ? 1u : 0u;
-    if (nrows == 1 && kp < k) continue;      // self-paired row: once per pair
-    double2 z1 = sbuf[lay.idx(0, k)], z2 = sbuf[lay.idx(ip, kp)];
-    double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
-    double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
-    double2 pq = cmul(p, q);
-    double2 w = make_double2(pq.y * a.scale, -pq.x * a.scale);
+    if (nrows == 1 && kp < k) continue;
+    const double2 z1 = sbuf[lay.idx(0, k)], z2 = sbuf[lay.idx(ip, kp)];
+    const double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
+    const double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
+    const double2 pq = cmul(p, q);
+    const double2 w = make_double2(pq.y * a.scale, -pq.x * a.scale);
     sbuf[lay.idx(0, k)] = w;
     if (!(nrows == 1 && kp == k)) sbuf[lay.idx(ip, kp)] = cconj(w);
   }
   __syncthreads();
+  // Y_k = (W_k + W_{k+L/2}) + i e^{2 pi i k / L} (W_k - W_{k+L/2})
   for (uint32_t e = tid; e < nrows * H; e += nthr) {
     const uint32_t i = e >= H ? 1 : 0, k = e - i * H;
-    const uint32_t r = rr[i];
-    double2 w1 = sbuf[lay.idx(i, k)], w2 = sbuf[lay.idx(i, k + H)];
-    double2 ev = cadd(w1, w2);
-    const uint32_t kk = r + AB * k;  // < L/2
-    double2 o = cmulc(csub(w1, w2), a.tw.get(kk));
+    const uint32_t r = i ? r1 : r0;
+    const double2 w1 = sbuf[lay.idx(i, k)], w2 = sbuf[lay.idx(i, k + H)];
+    const double2 ev = cadd(w1, w2);
+    const double2 o = cmulc(csub(w1, w2), a.tw.get(r + AB * k));
     sbuf[lay.idx(i, k)] = make_double2(ev.x - o.y, ev.y + o.x);
   }
   __syncthreads();
-  fft_smem<true>(sbuf, lay, a.inv, tid, nthr);
-  for (uint32_t e = tid; e < nrows * H; e += nthr) {
-    const uint32_t i = e >= H ? 1 : 0, m = e - i * H;
-    const uint32_t r = rr[i];
-    double2 z = sbuf[lay.idx(i, m)];
-    const uint32_t x = 2u * r * m;  // omega_{L/2}^{r m} = omega_L^{2 r m}
-    if (x) z = cmulc(z, a.tw.get(x));
-    a.data[base[i] + m] = z;
-  }
+  fft_pass<true>(sbuf, lay, a.inv, SmemSrc<LayRows>{sbuf, lay},
+                 RowSink{a.data, base0, base1, r0, r1, a.tw}, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
+struct CoefSink {
+  double2* coef;
+  uint32_t ncols, col0;
+  __device__ __forceinline__ void operator()(uint32_t item, uint32_t ma, double2 v) const {
+    coef[int64_t(ma) * ncols + col0 + item] = v;
+  }
+};
+
 __global__ void __launch_bounds__(512)
 k_ilast(ILastArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -338,23 +439,20 @@ k_ilast(ILastArgs a) {
   const int tid = threadIdx.x, nthr = blockDim.x;
   const uint32_t c = 1u << a.logc;
   const uint32_t col0 = blockIdx.x * c;
-  const uint32_t R = a.fft.R;
   LayCols lay{a.logc, c - 1};
-  const uint32_t tot = R * c;
-  for (uint32_t e = tid; e < tot; e += nthr) {
-    const uint32_t row = e >> a.logc, q = e & (c - 1);
-    sbuf[lay.idx(q, row)] = a.data[col_off(a.g, 0, row, col0 + q)];
-  }
-  __syncthreads();
-  fft_smem<true>(sbuf, lay, a.fft, tid, nthr);
-  for (uint32_t e = tid; e < tot; e += nthr) {
-    const uint32_t ma = e >> a.logc, q = e & (c - 1);
-    a.coef[int64_t(ma) * a.g.ncols + col0 + q] = sbuf[lay.idx(q, ma)];
-  }
+  fft_pass<true>(sbuf, lay, a.fft, ColSrc{a.data, a.g, 0, col0},
+                 CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
 // Post-map, rounding and carry propagation over all limbs.
+//   phase 1  coefficients e_k of the block's lanes: post-map (once per
+//            coefficient; the high product's folded buffer is staged in
+//            shared memory so the differencing reads neighbours from there)
+//            and the rounding tripwire
+//   phase 2  lanes L_m = sum e_k << (kb - 64m), one limb per thread pass
+//   phase 3  per-thread runs of 4 limbs: s_m = lo(L_m) + hi(L_{m-1}),
+//            carry transfer functions, block scan, warp look-back, limbs
 __global__ void __launch_bounds__(kCarryThreads)
 k_carry(CarryArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -362,15 +460,13 @@ k_carry(CarryArgs a) {
   __shared__ uint32_t s_blk;
   __shared__ int s_cin;
   __shared__ double s_psi;
-  __shared__ uint32_t s_flags, s_top, s_low;
+  __shared__ uint32_t s_flags, s_low;
   const int tid = threadIdx.x;
   const MapConsts& mc = a.mc;
   const int b = mc.b;
-  const int64_t N = mc.N;
   if (tid == 0) {
-    s_blk = uint32_t(atomicAdd(a.scan.ctr, 1ull));
+    s_blk = take_ticket(a.scan.ctr);
     s_flags = 0;
-    s_top = 0;
     s_low = 0;
   }
   __syncthreads();
@@ -382,34 +478,48 @@ k_carry(CarryArgs a) {
   const double* gw = a.w;
   auto W = [&](int64_t j) { return __ldg(gw + j); };
 
-  // coefficient window of this block: lanes ms-1 .. me (inclusive)
-  int64_t klo = (64 * (ms - 1) + b - 1) / b;
-  if (ms == 0) klo = 0;
-  int64_t khi = (64 * (me + 1) + 64 + b - 1) / b;
+  // coefficient window of the lanes ms-1 .. me (inclusive)
+  const int64_t klo = (ms == 0) ? 0 : (64 * (ms - 1) + b - 1) / b;
+  int64_t khi = (64 * (me + 1) + b - 1) / b;
   if (khi > K) khi = K;
-  long long* se = reinterpret_cast<long long*>(smem_raw);
-  uint64_t* sv = reinterpret_cast<uint64_t*>(se + (khi - klo) + 1);
+  const int64_t nk = khi > klo ? khi - klo : 0;
+  long long* se = reinterpret_cast<long long*>(smem_raw);                        // nk + 1
+  double* sh = reinterpret_cast<double*>(se + nk + 1);                            // nk + 2
+  unsigned long long* slo = reinterpret_cast<unsigned long long*>(sh + nk + 2);  // LB + 2
+  long long* shi = reinterpret_cast<long long*>(slo + LB + 2);                    // LB + 2
 
   if (mc.mode == kModeHigh && tid == 0) s_psi = high_psi(mc, W, a.aux[0]);
-  __syncthreads();
-  const double psi = s_psi;
   RoundAcc ra;
   uint32_t flags = 0;
   long long c0v = 0;
   if (mc.mode == kModeLow && ms == 0) {
-    // c_0 feeds e_0 (low product shift by b, products_f64.cpp:137-142)
-    RoundAcc r0;
-    c0v = r0.round(postmap_low(mc, W, 0));
-    ra.max_err = r0.max_err;
-    ra.max_abs = r0.max_abs;
-    ra.flags = r0.flags;
+    c0v = ra.round(postmap_low(mc, W, 0));
     if (c0v & ((1ll << b) - 1)) flags |= kFlagLowNotDivisible;
   }
+  if (mc.mode == kModeHigh) {
+    // folded delta-dagger buffer for i in [klo - 1, khi)
+    for (int64_t i = klo - 1 + tid; i < khi; i += kCarryThreads)
+      sh[i - (klo - 1)] = (i >= 0 && i < mc.N) ? high_buf(mc, W, i) : 0.0;
+  }
+  __syncthreads();
+  const double psi = s_psi;
   for (int64_t k = klo + tid; k < khi; k += kCarryThreads) {
     double x;
-    if (mc.mode == kModeFull) x = W(k);
-    else if (mc.mode == kModeLow) x = postmap_low(mc, W, k + 1);
-    else x = postmap_high(mc, W, k, psi);
+    if (mc.mode == kModeFull) {
+      x = W(k);
+    } else if (mc.mode == kModeLow) {
+      x = postmap_low(mc, W, k + 1);
+    } else {
+      const int64_t N = mc.N;
+      const double hk = (k < N) ? sh[k - (klo - 1)] : 0.0;
+      const double hm = (k >= 1) ? sh[k - 1 - (klo - 1)] : 0.0;
+      double v;
+      if (k == N) v = psi - hm * mc.step;
+      else if (k == 0) v = hk;
+      else v = hk - hm * mc.step;
+      if (k < mc.nfold) v -= psi * mc.fold[k];
+      x = v * mc.scale_out;
+    }
     long long e = ra.round(x);
     if (mc.mode == kModeLow && k == 0) e += (c0v >> b);
     se[k - klo] = e;
@@ -424,69 +534,52 @@ k_carry(CarryArgs a) {
     }
     if ((tid & 31) == 0) status_merge(a.status, e, m, 0);
   }
-  auto E = [&](int64_t k) -> long long { return se[k - klo]; };
 
+  // phase 2: lanes of limbs ms-1 .. me
+  auto E = [&](int64_t k) -> long long { return se[k - klo]; };
+  for (int64_t m = ms - 1 + tid; m <= me; m += kCarryThreads) {
+    const __int128 L = (m < 0) ? (__int128)0 : lane_value(E, m, b, khi);
+    slo[m - (ms - 1)] = (unsigned long long)L;
+    shi[m - (ms - 1)] = (long long)(L >> 64);
+  }
+  __syncthreads();
+
+  // phase 3: carries
   const int64_t m0 = ms + int64_t(tid) * kCarryPerThread;
   const int64_t m1 = min(me, m0 + kCarryPerThread);
-  auto lane = [&](int64_t m) -> __int128 {
-    return (m < 0) ? (__int128)0 : lane_value(E, m, b, khi);
+  auto S = [&](int64_t m) -> __int128 {
+    const int64_t o = m - (ms - 1);
+    return (__int128)slo[o] + (__int128)shi[o - 1];
   };
   uint32_t f = kTfIdentity;
-  __int128 prev = lane(m0 - 1);
-  for (int64_t m = m0; m < m1; ++m) {
-    __int128 cur = lane(m);
-    __int128 s = (__int128)(unsigned long long)cur + (prev >> 64);
-    f = tf_compose(f, limb_tf(s, flags));
-    prev = cur;
-  }
+  for (int64_t m = m0; m < m1; ++m) f = tf_compose(f, limb_tf(S(m), flags));
   uint32_t agg;
-  uint32_t ex = block_scan_tf(f, sw, &agg);
-  if (tid == 0) s_cin = lookback_carry(a.scan.state, blk, agg, a.scan.epoch, 0);
+  const uint32_t ex = block_scan_tf(f, sw, &agg);
+  if (tid < 32) {
+    const int cin = lookback_warp(a.scan.state, blk, agg, a.scan.epoch, 0);
+    if (tid == 0) s_cin = cin;
+  }
   __syncthreads();
   int c = tf_apply(ex, s_cin);
-  prev = lane(m0 - 1);
-  for (int64_t m = m0; m < m1; ++m) {
-    __int128 cur = lane(m);
-    __int128 s = (__int128)(unsigned long long)cur + (prev >> 64);
-    uint32_t tfm = limb_tf(s, flags);
-    sv[m - ms] = (unsigned long long)(s + c);
-    c = tf_apply(tfm, c);
-    prev = cur;
-  }
-  if (m1 == me && m0 < m1 && me == a.ML && c < 0) {
-    // sign of the recombined value (carry out of the top limb)
-    if (mc.mode == kModeFull) flags |= kFlagNegative;
-    if (mc.mode == kModeHigh) flags |= kFlagHighRange;
-  }
-  __syncthreads();
-
-  // outputs
   const int64_t OL = a.out_limbs;
-  if (mc.mode == kModeFull) {
-    const int64_t nb2 = 2 * a.n;
-    for (int64_t m = ms + tid; m < me; m += kCarryThreads) {
-      uint64_t x = sv[m - ms];
+  const int64_t sb = a.shift_s - 1;  // high: bit s-1
+  uint32_t sticky = 0;
+  for (int64_t m = m0; m < m1; ++m) {
+    const __int128 s = S(m);
+    const uint32_t tfm = limb_tf(s, flags);
+    const uint64_t x = (unsigned long long)(s + c);
+    c = tf_apply(tfm, c);
+    if (mc.mode == kModeFull) {
+      const int64_t nb2 = 2 * a.n;
       if (m < OL) {
         if (m == OL - 1 && (nb2 & 63) && (x >> (nb2 & 63))) flags |= kFlagFullOverflow;
         a.out[m] = x;
       } else if (x) {
         flags |= kFlagFullOverflow;
       }
-    }
-  } else if (mc.mode == kModeLow) {
-    for (int64_t m = ms + tid; m < me; m += kCarryThreads) {
-      uint64_t x = sv[m - ms];
-      if (m < OL) {
-        if (m == OL - 1 && (a.n & 63)) x &= (1ull << (a.n & 63)) - 1;
-        a.out[m] = x;
-      }
-    }
-  } else {
-    // high: keep all limbs of t; OR the bits strictly below s-1 (sticky)
-    const int64_t sb = a.shift_s - 1;  // bit s-1
-    uint32_t sticky = 0;
-    for (int64_t m = ms + tid; m < me; m += kCarryThreads) {
-      uint64_t x = sv[m - ms];
+    } else if (mc.mode == kModeLow) {
+      if (m < OL) a.out[m] = (m == OL - 1 && (a.n & 63)) ? (x & ((1ull << (a.n & 63)) - 1)) : x;
+    } else {
       a.tbuf[m] = x;
       const int64_t bit0 = 64 * m;
       if (bit0 + 64 <= sb) {
@@ -495,19 +588,26 @@ k_carry(CarryArgs a) {
         if (x & ((1ull << (sb - bit0)) - 1)) sticky = 1;
       }
     }
-    if (sticky) atomicOr(&s_low, 1u);
   }
+  if (m1 == me && m0 < m1 && me == a.ML && c < 0) {
+    // sign of the recombined value (carry out of the top limb)
+    if (mc.mode == kModeFull) flags |= kFlagNegative;
+    if (mc.mode == kModeHigh) flags |= kFlagHighRange;
+  }
+  if (sticky) atomicOr(&s_low, 1u);
   if (flags) atomicOr(&s_flags, flags);
   __syncthreads();
   if (tid == 0) {
     if (s_flags) atomicOr(&a.status->flags, s_flags);
     if (s_low) atomicOr(&a.status->high_sticky, 1u);
-    __threadfence();
-    if (atomicAdd(a.scan.ctr + 1, 1ull) == gridDim.x - 1) {
-      a.scan.ctr[0] = 0;
-      a.scan.ctr[1] = 0;
-    }
+    release_ticket(a.scan.ctr, gridDim.x);
   }
+}
+
+size_t carry_smem(int b) {
+  constexpr int LB = kCarryThreads * kCarryPerThread;
+  const size_t nk = size_t((64 * (LB + 2) + b - 1) / b + 4);
+  return nk * 8 + (nk + 2) * 8 + size_t(2 * (LB + 2)) * 8 + 64;
 }
 
 // ---------------------------------------------------------------------------
@@ -524,7 +624,7 @@ k_high_round(HighRoundArgs a) {
   __shared__ uint32_t s_flags, s_top, s_low;
   const int tid = threadIdx.x;
   if (tid == 0) {
-    s_blk = uint32_t(atomicAdd(a.scan.ctr, 1ull));
+    s_blk = take_ticket(a.scan.ctr);
     s_flags = 0;
     s_top = 0;
     s_low = 0;
@@ -555,8 +655,11 @@ k_high_round(HighRoundArgs a) {
     }
   }
   uint32_t agg;
-  uint32_t ex = block_scan_tf(f, sw, &agg);
-  if (tid == 0) s_cin = lookback_carry(a.scan.state, blk, agg, a.scan.epoch, inc);
+  const uint32_t ex = block_scan_tf(f, sw, &agg);
+  if (tid < 32) {
+    const int cin = lookback_warp(a.scan.state, blk, agg, a.scan.epoch, inc);
+    if (tid == 0) s_cin = cin;
+  }
   __syncthreads();
   int c = tf_apply(ex, s_cin);
   uint32_t flags = 0, topbit = 0, lownz = 0;
@@ -579,57 +682,7 @@ k_high_round(HighRoundArgs a) {
     if (s_flags) atomicOr(&a.status->flags, s_flags);
     if (s_top) atomicOr(&a.status->high_topbit, 1u);
     if (s_low) atomicOr(&a.status->high_lownz, 1u);
-    __threadfence();
-    if (atomicAdd(a.scan.ctr + 1, 1ull) == gridDim.x - 1) {
-      a.scan.ctr[0] = 0;
-      a.scan.ctr[1] = 0;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-__global__ void k_basecase(BaseArgs a) {
-  // column sums as 192-bit accumulators, then one sequential carry pass
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem_raw);
-  const int64_t nl = a.nlimbs;
-  const int64_t nc = 2 * nl;
-  for (int64_t k = threadIdx.x; k < nc; k += blockDim.x) {
-    unsigned long long lo = 0, mid = 0, hi = 0;
-    int64_t i0 = k - (nl - 1);
-    if (i0 < 0) i0 = 0;
-    for (int64_t i = i0; i <= k && i < nl; ++i) {
-      unsigned long long x = a.u[i], y = a.v[k - i];
-      unsigned long long pl = x * y, ph = __umul64hi(x, y);
-      unsigned long long t = lo + pl;
-      unsigned long long c1 = t < lo;
-      lo = t;
-      t = mid + ph;
-      unsigned long long c2 = t < mid;
-      mid = t + c1;
-      c2 += (mid < t);
-      hi += c2;
-    }
-    acc[3 * k] = lo;
-    acc[3 * k + 1] = mid;
-    acc[3 * k + 2] = hi;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long c0 = 0, c1 = 0;  // running carry (128-bit)
-    for (int64_t k = 0; k < nc; ++k) {
-      unsigned long long lo = acc[3 * k], mid = acc[3 * k + 1], hi = acc[3 * k + 2];
-      unsigned long long t = lo + c0;
-      unsigned long long cy = t < lo;
-      a.prod[k] = t;
-      // new carry = mid + hi*2^64 + c1*2^64 + cy
-      unsigned long long n0 = mid + c1;
-      unsigned long long k1 = n0 < mid;
-      unsigned long long n0b = n0 + cy;
-      k1 += n0b < n0;
-      c0 = n0b;
-      c1 = hi + k1;
-    }
+    release_ticket(a.scan.ctr, gridDim.x);
   }
 }
 

@@ -61,8 +61,9 @@ struct SplitScanArgs {
   DevStatus* status;
 };
 constexpr int kSplitThreads = 256;
-constexpr int kSplitPerThread = 16;  // chunks per thread
+constexpr int kSplitChunks = kSplitThreads * 32;  // chunks per block
 __global__ void k_split_scan(SplitScanArgs a);
+size_t split_scan_smem(int b);
 
 // Column pass geometry: element (outer, row, col) at
 //   outer * os + row * rs + (col / cw) * cs + (col % cw)
@@ -140,6 +141,7 @@ struct CarryArgs {
 constexpr int kCarryThreads = 256;
 constexpr int kCarryPerThread = 4;
 __global__ void k_carry(CarryArgs a);
+size_t carry_smem(int b);
 
 struct HighRoundArgs {
   const uint64_t* tbuf;

@@ -257,6 +257,58 @@ __device__ __forceinline__ uint32_t block_scan_tf(uint32_t f, uint32_t* sw,
   return tf_compose(wex, excl);
 }
 
+// Warp-parallel decoupled look-back (called by all 32 lanes of one warp):
+// each round reads the state words of the 32 nearest unresolved
+// predecessors at once, composes their aggregates with a warp reduction and
+// stops at the nearest inclusive prefix.  carry0 is the carry into block 0.
+// Returns the carry into block blk (same value in every lane) and publishes
+// this block's inclusive carry.
+__device__ __forceinline__ int lookback_warp(unsigned long long* state,
+                                             uint32_t blk, uint32_t agg,
+                                             uint32_t epoch, int carry0) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long ep = (unsigned long long)epoch << 32;
+  int carry_in = carry0;
+  if (blk != 0) {
+    if (lane == 0)
+      *(volatile unsigned long long*)(state + blk) = ep | (1ull << 30) | agg;
+    uint32_t E = kTfIdentity;
+    int64_t base = int64_t(blk) - 1;
+    while (true) {
+      const int64_t j = base - lane;
+      unsigned long long w = 0;
+      if (j >= 0) w = *(volatile unsigned long long*)(state + j);
+      const bool valid = (j >= 0) && ((w >> 32) == epoch) && (((w >> 30) & 3u) != 0);
+      const bool incl = valid && (((w >> 30) & 3u) == 2);
+      const uint32_t bi = __ballot_sync(0xffffffffu, incl);
+      const uint32_t bv = __ballot_sync(0xffffffffu, valid);
+      const int first = bi ? (__ffs(bi) - 1) : 32;
+      const uint32_t need = (first == 32) ? 0xffffffffu : ((1u << first) - 1u);
+      if ((bv & need) != need) continue;  // a nearer predecessor is not ready
+      // compose aggregates of lanes [0, first): f_0 o f_1 o ... o f_{first-1}
+      uint32_t f = (lane < first) ? uint32_t(w & 63u) : kTfIdentity;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_down_sync(0xffffffffu, f, off);
+        if (lane + off < 32) f = tf_compose(o, f);
+      }
+      f = __shfl_sync(0xffffffffu, f, 0);
+      E = tf_compose(f, E);
+      if (first < 32) {
+        const int v = int(__shfl_sync(0xffffffffu, uint32_t(w & 63u), first)) - 1;
+        carry_in = tf_apply(E, v);
+        break;
+      }
+      base -= 32;
+    }
+  }
+  if (lane == 0) {
+    const int out = tf_apply(agg, carry_in);
+    *(volatile unsigned long long*)(state + blk) = ep | (2ull << 30) | uint64_t(out + 1);
+  }
+  return carry_in;
+}
+
 // Decoupled look-back over per-block aggregates (one thread per block);
 // carry0 is the carry into block 0.
 // state words: [63:32] epoch, [31:30] flag (1 aggregate, 2 inclusive),

@@ -372,7 +372,8 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   pl->thr_mid = threads_for(uint64_t(2) * C);
   pl->smem_mid = size_t(2) * (padded_len(C) + 4) * 16;
   const int64_t LB = kCarryThreads * kCarryPerThread;
-  pl->smem_carry = size_t((64 * (LB + 2) + 64 + b) / b + 4) * 8 + size_t(LB + 2) * 8;
+  pl->smem_carry = carry_smem(b);
+  (void)LB;
   pl->kernels = ((pl->kind == 2) ? 5 : 7) + (p.mode == PMode::kHigh ? 1 : 0);
   return pl;
 }
