@@ -242,6 +242,9 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.tw = pl.twL;
       a.mc = pl.mc;
       a.aux = cx.aux.as<double>();
+      a.rows_staged = pl.f1_rows;
+      a.nlr = pl.f1_nlr;
+      a.ncb = pl.f1_ncb;
       set_smem(k_f1, pl.smem_f1);
       {
         KTimer kt(cx, "k_f1", double(2 * pl.nlimbs) * 8.0 + double(L) * 16.0, int(p.mode));

@@ -9,6 +9,8 @@
 //   beta*, delta+    maps_f64.cpp:140-188, 269-281, 350-384
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace tmg {
@@ -89,5 +91,50 @@ __device__ __forceinline__ double series_coef(int fam, int r, double k,
   }
   return p * c;
 }
+
+// Same coefficient with the row r known at compile time: the r integer
+// factors are exact doubles (|k + iN| < 2^53) stepped by +-N, so only the
+// products round.
+template <int R>
+__device__ __forceinline__ double coef_r(int fam, double k, double N, double c) {
+  if constexpr (R == 0) {
+    return 1.0;
+  } else {
+    double p = k;
+    if (fam == 0 || fam == 2) {
+      const double st = (fam == 0) ? -N : N;
+      double f = k + double(R) + st;
+#pragma unroll
+      for (int i = 0; i < R - 1; ++i) {
+        p *= f;
+        f += st;
+      }
+    } else {
+      const double st = (fam == 1) ? N : -N;
+      double f = k + st;
+#pragma unroll
+      for (int i = 1; i < R; ++i) {
+        p *= f;
+        f += st;
+      }
+    }
+    return p * c;
+  }
+}
+
+// Compile-time loop r = 0 .. R-1 calling f(std::integral_constant<int, r>).
+template <int R>
+struct RowLoop {
+  template <class F>
+  __device__ __forceinline__ static void run(F&& f) {
+    RowLoop<R - 1>::run(f);
+    f(std::integral_constant<int, R - 1>{});
+  }
+};
+template <>
+struct RowLoop<0> {
+  template <class F>
+  __device__ __forceinline__ static void run(F&&) {}
+};
 
 }  // namespace tmg

@@ -211,13 +211,40 @@ struct ColSink {
 // ---------------------------------------------------------------------------
 // F1: split + pre-map + forward column DFT over A (rows j_a, chunk index
 // j = j_a * ncols + col), twiddle omega_L^{col k_a}, store T[k_a][col].
-// Each thread produces whole row segments of c chunks: it streams the
-// c + lambda - 1 digits through a shift register (compile-time indexed, so
-// no local memory) and applies the pre-map as the window slides.
+//   staging  the limbs and carry words under every row segment are fetched
+//            with independent loads into shared memory
+//   digits   one thread per row segment streams its c + lambda - 1 digits
+//            through a shift register (compile-time indexed) and applies the
+//            pre-map as the window slides
+//   DFT      fft_pass from shared memory; the output twiddle
+//            omega_L^{col k} = hi_col[k >> 6] * lo_col[k & 63] comes from
+//            per-column tables in shared memory
+__host__ __device__ F1Smem f1_smem_layout(uint32_t A, uint32_t c, uint32_t rows_staged, uint32_t nlr,
+                      uint32_t ncb) {
+  F1Smem m;
+  m.buf = size_t(padded_len(A * c)) * 16;
+  m.tw = size_t(tw_smem_len(A)) * 16;
+  m.coltw = size_t(c) * (64 + (A + 63) / 64) * 16;
+  m.limbs = size_t(2) * rows_staged * nlr * 8;
+  m.cbits = size_t(2) * rows_staged * ncb * 4;
+  m.total = m.buf + m.tw + m.coltw + m.limbs + m.cbits;
+  return m;
+}
+
+struct ColTwSink {
+  double2* out;
+  uint32_t ncols, col0, nhi;
+  const double2* ctw;  // per column: 64 lo entries then nhi hi entries
+  __device__ __forceinline__ void operator()(uint32_t item, uint32_t k, double2 v) const {
+    const double2* t = ctw + item * (64 + nhi);
+    if (k) v = cmul(v, cmul(t[64 + (k >> 6)], t[k & 63]));
+    out[int64_t(k) * ncols + col0 + item] = v;
+  }
+};
+
 __global__ void __launch_bounds__(512)
 k_f1(F1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x, nthr = blockDim.x;
   const uint32_t c = 1u << a.logc;
   const uint32_t col0 = blockIdx.x * c;
@@ -227,8 +254,42 @@ k_f1(F1Args a) {
   const int64_t N = mc.N;
   const int lam = (mc.mode == kModeFull) ? 1 : mc.lambda;
   const double Nd = double(N);
+  const F1Smem L = f1_smem_layout(A, c, a.rows_staged, a.nlr, a.ncb);
+  double2* sbuf = reinterpret_cast<double2*>(smem_raw);
+  double2* stw = reinterpret_cast<double2*>(smem_raw + L.buf);
+  double2* sctw = reinterpret_cast<double2*>(smem_raw + L.buf + L.tw);
+  uint64_t* slimb = reinterpret_cast<uint64_t*>(smem_raw + L.buf + L.tw + L.coltw);
+  uint32_t* scb = reinterpret_cast<uint32_t*>(smem_raw + L.buf + L.tw + L.coltw + L.limbs);
   LayCols lay{a.logc, c - 1};
-  const GlobalLimbs gu{a.u, a.nlimbs}, gv{a.v, a.nlimbs};
+  const uint32_t RS = a.rows_staged, NLR = a.nlr, NCB = a.ncb;
+  const int cnt = int(c) + lam - 1;
+
+  // stage limbs and carry words (independent loads, many in flight)
+  for (uint32_t e = tid; e < 2 * RS * NLR; e += nthr) {
+    const uint32_t op = e / (RS * NLR), rem = e - op * RS * NLR;
+    const uint32_t row = rem / NLR, k = rem - row * NLR;
+    const int64_t js = int64_t(row) * a.ncols + col0 - (lam - 1);
+    const int64_t g = ((js * b - a.lead) >> 6) + k;
+    const uint64_t* lp = op ? a.v : a.u;
+    slimb[e] = (g >= 0 && g < a.nlimbs) ? __ldg(lp + g) : 0ull;
+  }
+  for (uint32_t e = tid; e < 2 * RS * NCB; e += nthr) {
+    const uint32_t op = e / (RS * NCB), rem = e - op * RS * NCB;
+    const uint32_t row = rem / NCB, k = rem - row * NCB;
+    const int64_t js = int64_t(row) * a.ncols + col0 - (lam - 1);
+    const int64_t g = (js >> 5) + k;
+    const uint32_t* cp = op ? a.cbits_v : a.cbits_u;
+    scb[e] = (js >= 0 && (g << 5) < a.count) ? __ldg(cp + g) : 0u;
+  }
+  // twiddle tables: omega_A two-level, and per column omega_L^{col k}
+  const TwSmem tw = load_tw_smem(stw, a.fft, tid, nthr);
+  const uint32_t nhi = (A + 63) / 64;
+  for (uint32_t e = tid; e < c * (64 + nhi); e += nthr) {
+    const uint32_t q = e / (64 + nhi), i = e - q * (64 + nhi);
+    const uint32_t col = col0 + q;
+    const uint32_t x = (i < 64) ? col * i : col * 64u * (i - 64);
+    sctw[e] = a.tw.get(x);
+  }
 
   double topu = 0.0, topv = 0.0;
   if (mc.mode == kModeHigh && col0 < uint32_t(mc.nfold + mc.lambda)) {
@@ -240,53 +301,45 @@ k_f1(F1Args a) {
     auto Dv = [&](int64_t i) { return digit_at(a.v, a.nlimbs, b, a.lead, a.count, a.cbits_v, i); };
     a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
   }
+  __syncthreads();
   const int fam = (mc.mode == kModeLow) ? 0 : 2;
 
   for (uint32_t row = tid; row < A; row += nthr) {
     const int64_t j0 = int64_t(row) * a.ncols + col0;
-    if (mc.mode == kModeFull) {
-      if (j0 >= N) {
-        for (uint32_t q = 0; q < c; ++q) sbuf[lay.idx(q, row)] = make_double2(0.0, 0.0);
-        continue;
-      }
-      WindowReader<GlobalLimbs> ru, rv;
-      ru.init(gu, j0 * b, b);
-      rv.init(gv, j0 * b, b);
-      for (uint32_t q = 0; q < c; ++q) {
-        const int64_t j = j0 + q;
-        const uint64_t wu = ru.next(), wv = rv.next();
-        double du = 0.0, dv = 0.0;
-        if (j < N) {
-          du = double(split_digit(wu, cbit(a.cbits_u, j), b, j == a.count - 1));
-          dv = double(split_digit(wv, cbit(a.cbits_v, j), b, j == a.count - 1));
-        }
-        sbuf[lay.idx(q, row)] = make_double2(du, dv);
-      }
+    if (row >= RS || (mc.mode == kModeFull && j0 >= N)) {
+      for (uint32_t q = 0; q < c; ++q) sbuf[lay.idx(q, row)] = make_double2(0.0, 0.0);
       continue;
     }
-    // low / high: window of digits d[j - r], r < lam, in a shift register
     const int64_t js = j0 - (lam - 1);
+    const int64_t i0 = (js * b - a.lead) >> 6;
+    WindowReader<SmemLimbs> ru, rv;
+    ru.init(SmemLimbs{slimb + size_t(row) * NLR, i0, NLR}, js * b - a.lead, b);
+    rv.init(SmemLimbs{slimb + size_t(RS + row) * NLR, i0, NLR}, js * b - a.lead, b);
+    const uint32_t* cbu = scb + size_t(row) * NCB;
+    const uint32_t* cbv = scb + size_t(RS + row) * NCB;
+    const int64_t w0 = js >> 5;
+    const bool fast = js >= 0;
     double wu[kMaxLambda], wv[kMaxLambda];
 #pragma unroll
     for (int r = 0; r < kMaxLambda; ++r) wu[r] = wv[r] = 0.0;
-    WindowReader<GlobalLimbs> ru, rv;
-    const bool fast = js >= 0;
-    if (fast) {
-      ru.init(gu, js * b - a.lead, b);
-      rv.init(gv, js * b - a.lead, b);
-    }
-    const int cnt = int(c) + lam - 1;
     for (int q = 0; q < cnt; ++q) {
       const int64_t j = js + q;
       double du, dv;
       if (fast) {
         const uint64_t xu = ru.next(), xv = rv.next();
-        du = double(split_digit(xu, cbit(a.cbits_u, j), b, j == a.count - 1));
-        dv = double(split_digit(xv, cbit(a.cbits_v, j), b, j == a.count - 1));
+        const int64_t wi = (j >> 5) - w0;
+        const int cu = int((cbu[wi] >> (j & 31)) & 1u);
+        const int cv = int((cbv[wi] >> (j & 31)) & 1u);
+        du = double(split_digit(xu, cu, b, j == a.count - 1));
+        dv = double(split_digit(xv, cv, b, j == a.count - 1));
       } else {
         const int64_t jj = j < 0 ? j + N : j;
         du = digit_at(a.u, a.nlimbs, b, a.lead, a.count, a.cbits_u, jj);
         dv = digit_at(a.v, a.nlimbs, b, a.lead, a.count, a.cbits_v, jj);
+      }
+      if (mc.mode == kModeFull) {
+        sbuf[lay.idx(uint32_t(q), row)] = (j < N) ? make_double2(du, dv) : make_double2(0.0, 0.0);
+        continue;
       }
 #pragma unroll
       for (int r = kMaxLambda - 1; r > 0; --r) {
@@ -298,44 +351,44 @@ k_f1(F1Args a) {
       if (q >= lam - 1) {
         // transform index j; digit d[(j - r) mod N] sits in w*[r]
         double au = 0.0, av = 0.0;
-#pragma unroll
-        for (int r = 0; r < kMaxLambda; ++r) {
+        RowLoop<kMaxLambda>::run([&](auto rc) {
+          constexpr int r = decltype(rc)::value;
           if (r < lam) {
             int64_t k = j - r;
             if (k < 0) k += N;
-            const double cf = series_coef(fam, r, double(k), Nd, mc.cpre[r]);
+            const double cf = coef_r<r>(fam, double(k), Nd, mc.cpre[r]);
             au += wu[r] * cf;
             av += wv[r] * cf;
           }
-        }
+        });
         if (mc.mode == kModeHigh && j < mc.nfold + mc.lambda) {
-          for (int r = 0; r < mc.lambda; ++r) {
-            int64_t k = j - r;
-            if (k < 0) k += N;
-            if (k < mc.nfold) {
-              const double g = mc.fold[k] * series_coef(2, r, double(k), Nd, mc.cpre[r]);
-              au += topu * g;
-              av += topv * g;
+          RowLoop<kMaxLambda>::run([&](auto rc) {
+            constexpr int r = decltype(rc)::value;
+            if (r < lam) {
+              int64_t k = j - r;
+              if (k < 0) k += N;
+              if (k < mc.nfold) {
+                const double g = mc.fold[k] * coef_r<r>(2, double(k), Nd, mc.cpre[r]);
+                au += topu * g;
+                av += topv * g;
+              }
             }
-          }
+          });
         }
         sbuf[lay.idx(uint32_t(q - (lam - 1)), row)] = make_double2(au, av);
       }
     }
   }
   __syncthreads();
-
-  ColGeom g;
-  g.os = 0;
-  g.rs = a.ncols;
-  g.cs = 0;
-  g.cw = 0xffffffffu;
-  g.ncols = a.ncols;
-  ColSink sink{a.out, g, 0, col0, a.tw, 0u, 1u, 1u, false, true};
-  fft_pass<false>(sbuf, lay, a.fft, SmemSrc<LayCols>{sbuf, lay}, sink, tid, nthr);
+  fft_pass<false>(sbuf, lay, a.fft, tw, SmemSrc<LayCols>{sbuf, lay},
+                  ColTwSink{a.out, a.ncols, col0, nhi, sctw}, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
+size_t col_smem_bytes(uint32_t R, uint32_t c) {
+  return size_t(padded_len(R * c)) * 16 + size_t(tw_smem_len(R)) * 16;
+}
+
 __global__ void __launch_bounds__(512)
 k_col(ColArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -345,10 +398,12 @@ k_col(ColArgs a) {
   const uint32_t col0 = blockIdx.x * c;
   const int64_t outer = blockIdx.y;
   LayCols lay{a.logc, c - 1};
+  const TwSmem tw = load_tw_smem(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
+  __syncthreads();
   ColSrc src{a.data, a.g, outer, col0};
   ColSink sink{a.data, a.g, outer, col0, a.tw, a.to, a.tc, a.tmul, a.inv != 0, true};
-  if (a.inv) fft_pass<true>(sbuf, lay, a.fft, src, sink, tid, nthr);
-  else fft_pass<false>(sbuf, lay, a.fft, src, sink, tid, nthr);
+  if (a.inv) fft_pass<true>(sbuf, lay, a.fft, tw, src, sink, tid, nthr);
+  else fft_pass<false>(sbuf, lay, a.fft, tw, src, sink, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
@@ -361,18 +416,24 @@ struct RowSrc {
   }
 };
 
+// Output twiddle omega_L^{2 r m} from per-row two-level tables.
 struct RowSink {
   double2* data;
   int64_t base0, base1;
-  uint32_t r0, r1;
-  TwGlobal tw;
+  const double2* rtw;  // per row: 64 lo entries then nhi hi entries
+  uint32_t nhi;
   __device__ __forceinline__ void operator()(uint32_t item, uint32_t m, double2 v) const {
-    const uint32_t r = item ? r1 : r0;
-    const uint32_t x = 2u * r * m;  // omega_{L/2}^{r m} = omega_L^{2 r m}
-    if (x) v = cmulc(v, tw.get(x));
+    const double2* t = rtw + item * (64 + nhi);
+    if (m) v = cmulc(v, cmul(t[64 + (m >> 6)], t[m & 63]));
     data[(item ? base1 : base0) + m] = v;
   }
 };
+
+size_t mid_smem_bytes(uint32_t C) {
+  const uint32_t H = C / 2;
+  return size_t(2) * (padded_len(C) + 4) * 16 + size_t(tw_smem_len(C)) * 16 +
+         size_t(2) * (64 + (H + 63) / 64) * 16 + 64;
+}
 
 __global__ void __launch_bounds__(512)
 k_mid(MidArgs a) {
@@ -388,8 +449,21 @@ k_mid(MidArgs a) {
   LayRows lay{nrows, rowstride};
   const int64_t base0 = (int64_t(r0 % a.A) * a.B + (r0 / a.A)) * int64_t(C);
   const int64_t base1 = (int64_t(r1 % a.A) * a.B + (r1 / a.A)) * int64_t(C);
+  double2* stw = sbuf + 2 * rowstride;
+  const uint32_t nhiC = (C + 63) / 64;
+  double2* srtw = stw + 64 + nhiC;
+  double2* srow = srtw + 2 * (64 + (H + 63) / 64);  // omega_L^{r} per row
+  const TwSmem tw = load_tw_smem(stw, a.fwd, tid, nthr);
+  const uint32_t nhiH = (H + 63) / 64;
+  for (uint32_t e = tid; e < 2 * (64 + nhiH); e += nthr) {
+    const uint32_t i = e / (64 + nhiH), k = e - i * (64 + nhiH);
+    const uint32_t r2 = 2u * (i ? r1 : r0);
+    const uint32_t x = (k < 64) ? r2 * k : r2 * 64u * (k - 64);
+    srtw[e] = a.tw.get(x);
+  }
+  if (tid < 2) srow[tid] = a.tw.get(tid ? r1 : r0);
 
-  fft_pass<false>(sbuf, lay, a.fwd, RowSrc{a.data, base0, base1},
+  fft_pass<false>(sbuf, lay, a.fwd, tw, RowSrc{a.data, base0, base1},
                   SmemSink<LayRows>{sbuf, lay}, tid, nthr);
   __syncthreads();
 
@@ -409,18 +483,19 @@ k_mid(MidArgs a) {
     if (!(nrows == 1 && kp == k)) sbuf[lay.idx(ip, kp)] = cconj(w);
   }
   __syncthreads();
-  // Y_k = (W_k + W_{k+L/2}) + i e^{2 pi i k / L} (W_k - W_{k+L/2})
+  // Y_k = (W_k + W_{k+L/2}) + i e^{2 pi i k / L} (W_k - W_{k+L/2}),
+  // k = r + AB k_c: omega_L^k = omega_L^r omega_C^{k_c}
   for (uint32_t e = tid; e < nrows * H; e += nthr) {
     const uint32_t i = e >= H ? 1 : 0, k = e - i * H;
-    const uint32_t r = i ? r1 : r0;
     const double2 w1 = sbuf[lay.idx(i, k)], w2 = sbuf[lay.idx(i, k + H)];
     const double2 ev = cadd(w1, w2);
-    const double2 o = cmulc(csub(w1, w2), a.tw.get(r + AB * k));
+    const double2 om = cmul(srow[i], tw.get(k));
+    const double2 o = cmulc(csub(w1, w2), om);
     sbuf[lay.idx(i, k)] = make_double2(ev.x - o.y, ev.y + o.x);
   }
   __syncthreads();
-  fft_pass<true>(sbuf, lay, a.inv, SmemSrc<LayRows>{sbuf, lay},
-                 RowSink{a.data, base0, base1, r0, r1, a.tw}, tid, nthr);
+  fft_pass<true>(sbuf, lay, a.inv, tw, SmemSrc<LayRows>{sbuf, lay},
+                 RowSink{a.data, base0, base1, srtw, nhiH}, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
@@ -440,7 +515,9 @@ k_ilast(ILastArgs a) {
   const uint32_t c = 1u << a.logc;
   const uint32_t col0 = blockIdx.x * c;
   LayCols lay{a.logc, c - 1};
-  fft_pass<true>(sbuf, lay, a.fft, ColSrc{a.data, a.g, 0, col0},
+  const TwSmem tw = load_tw_smem(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
+  __syncthreads();
+  fft_pass<true>(sbuf, lay, a.fft, tw, ColSrc{a.data, a.g, 0, col0},
                  CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
 }
 
@@ -485,30 +562,44 @@ k_carry(CarryArgs a) {
   const int64_t nk = khi > klo ? khi - klo : 0;
   long long* se = reinterpret_cast<long long*>(smem_raw);                        // nk + 1
   double* sh = reinterpret_cast<double*>(se + nk + 1);                            // nk + 2
-  unsigned long long* slo = reinterpret_cast<unsigned long long*>(sh + nk + 2);  // LB + 2
+  double* sww = sh + nk + 2;                                                      // nk + 12
+  unsigned long long* slo = reinterpret_cast<unsigned long long*>(sww + nk + 12); // LB + 2
   long long* shi = reinterpret_cast<long long*>(slo + LB + 2);                    // LB + 2
+
+  // stage the convolution coefficients under this block (coalesced); the
+  // post-maps read their lambda-neighbourhoods from shared memory
+  const int64_t nwt = (mc.mode == kModeFull) ? K : mc.N;
+  const int64_t wlo = max(int64_t(0), klo - int64_t(mc.lambda) - 2);
+  const int64_t whi = min(nwt, khi + 2);
+  const int64_t nw = (mc.mode == kModeFull || whi <= wlo) ? 0 : whi - wlo;
+  for (int64_t j = wlo + tid; j < wlo + nw; j += kCarryThreads) sww[j - wlo] = W(j);
+  auto WS = [&](int64_t j) -> double {
+    const int64_t o = j - wlo;
+    return (o >= 0 && o < nw) ? sww[o] : __ldg(gw + j);
+  };
 
   if (mc.mode == kModeHigh && tid == 0) s_psi = high_psi(mc, W, a.aux[0]);
   RoundAcc ra;
   uint32_t flags = 0;
   long long c0v = 0;
+  __syncthreads();
   if (mc.mode == kModeLow && ms == 0) {
-    c0v = ra.round(postmap_low(mc, W, 0));
+    c0v = ra.round(postmap_low(mc, WS, 0));
     if (c0v & ((1ll << b) - 1)) flags |= kFlagLowNotDivisible;
   }
   if (mc.mode == kModeHigh) {
     // folded delta-dagger buffer for i in [klo - 1, khi)
     for (int64_t i = klo - 1 + tid; i < khi; i += kCarryThreads)
-      sh[i - (klo - 1)] = (i >= 0 && i < mc.N) ? high_buf(mc, W, i) : 0.0;
+      sh[i - (klo - 1)] = (i >= 0 && i < mc.N) ? high_buf(mc, WS, i) : 0.0;
+    __syncthreads();
   }
-  __syncthreads();
   const double psi = s_psi;
   for (int64_t k = klo + tid; k < khi; k += kCarryThreads) {
     double x;
     if (mc.mode == kModeFull) {
       x = W(k);
     } else if (mc.mode == kModeLow) {
-      x = postmap_low(mc, W, k + 1);
+      x = postmap_low(mc, WS, k + 1);
     } else {
       const int64_t N = mc.N;
       const double hk = (k < N) ? sh[k - (klo - 1)] : 0.0;
@@ -607,7 +698,7 @@ k_carry(CarryArgs a) {
 size_t carry_smem(int b) {
   constexpr int LB = kCarryThreads * kCarryPerThread;
   const size_t nk = size_t((64 * (LB + 2) + b - 1) / b + 4);
-  return nk * 8 + (nk + 2) * 8 + size_t(2 * (LB + 2)) * 8 + 64;
+  return nk * 8 + (nk + 2) * 8 + (nk + 12) * 8 + size_t(2 * (LB + 2)) * 8 + 64;
 }
 
 // ---------------------------------------------------------------------------

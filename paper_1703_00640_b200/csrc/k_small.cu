@@ -43,6 +43,8 @@ k_small_product(SmallArgs a) {
   uint64_t* vl = ul + a.nlimbs;
   uint32_t* sw = reinterpret_cast<uint32_t*>(vl + a.nlimbs);  // 32 words
   double* sd = reinterpret_cast<double*>(sw + 32);             // scalars
+  double2* stw = reinterpret_cast<double2*>(sd + 8);            // twiddles
+  const TwSmem tw = load_tw_smem(stw, a.fwd, tid, nthr);
 
   const uint64_t* gu = a.u + int64_t(blockIdx.x) * a.nlimbs;
   const uint64_t* gv = a.v + int64_t(blockIdx.x) * a.nlimbs;
@@ -127,7 +129,7 @@ k_small_product(SmallArgs a) {
 
   // 4. forward FFT of z = a + i c, length L.
   LayRows lay1{1u, 0u};
-  fft_smem<false>(buf, lay1, a.fwd, tid, nthr);
+  fft_smem<false>(buf, lay1, a.fwd, tw, tid, nthr);
 
   // 5. spectral product: W_k = (Z_k + conj Z_-k)(Z_k - conj Z_-k)/(4i L),
   //    then Y_k = (W_k + W_{k+L/2}) + i e^{2 pi i k/L}(W_k - W_{k+L/2}).
@@ -146,13 +148,13 @@ k_small_product(SmallArgs a) {
   for (uint32_t k = tid; k < H; k += nthr) {
     double2 w1 = buf[padidx(k)], w2 = buf[padidx(k + H)];
     double2 e = cadd(w1, w2);
-    double2 o = cmulc(csub(w1, w2), __ldg(a.fwd.tw + k));  // * e^{+2 pi i k/L}
+    double2 o = cmulc(csub(w1, w2), tw.get(k));  // * e^{+2 pi i k/L}
     buf[padidx(k)] = make_double2(e.x - o.y, e.y + o.x);
   }
   __syncthreads();
 
   // 6. inverse FFT of length L/2: y_m = w_{2m} + i w_{2m+1}.
-  fft_smem<true>(buf, lay1, a.inv, tid, nthr);
+  fft_smem<true>(buf, lay1, a.inv, tw, tid, nthr);
 
   // 7. post-map and rounding.
   auto W = [&](int64_t j) {

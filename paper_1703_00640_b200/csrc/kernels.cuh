@@ -33,6 +33,8 @@ struct SmallArgs {
 };
 
 size_t small_smem_bytes(int64_t L, int64_t nlimbs);
+size_t mid_smem_bytes(uint32_t C);
+size_t col_smem_bytes(uint32_t R, uint32_t c);
 
 __global__ void k_small_product(SmallArgs a);
 
@@ -89,8 +91,17 @@ struct F1Args {
   TwGlobal tw;     // omega_L
   MapConsts mc;
   double* aux;     // high: [0] theta_u*theta_v
+  // shared-memory staging of the limbs / carry words under each row segment
+  uint32_t rows_staged;  // rows whose inputs are staged (A, or A/2 for full)
+  uint32_t nlr;          // limbs per row segment
+  uint32_t ncb;          // carry words per row segment
 };
 __global__ void k_f1(F1Args a);
+struct F1Smem {
+  size_t buf, tw, coltw, limbs, cbits, total;
+};
+__host__ __device__ F1Smem f1_smem_layout(uint32_t A, uint32_t c, uint32_t rows_staged, uint32_t nlr,
+                      uint32_t ncb);
 
 struct ColArgs {
   double2* data;  // in place
@@ -139,7 +150,7 @@ struct CarryArgs {
   uint64_t* tbuf;  // high: all limbs of t (ML words)
 };
 constexpr int kCarryThreads = 256;
-constexpr int kCarryPerThread = 4;
+constexpr int kCarryPerThread = 2;
 __global__ void k_carry(CarryArgs a);
 size_t carry_smem(int b);
 

@@ -21,22 +21,26 @@ __device__ __forceinline__ double premap(const MapConsts& mc, const DF& D,
   const int64_t N = mc.N;
   const double Nd = double(N);
   const int fam = (mc.mode == kModeLow) ? 0 : 2;
+  const int lam = mc.lambda;
   double acc = 0.0;
-  for (int r = 0; r < mc.lambda; ++r) {
-    int64_t k = j - r;
-    if (k < 0) k += N;
-    double d = D(k);
-    acc += d * series_coef(fam, r, double(k), Nd, mc.cpre[r]);
-  }
-  if (mc.mode == kModeHigh && top != 0.0) {
-    // out[(k + r) mod N] += top * fold[k] * gamma_r(k), k < nfold
-    for (int r = 0; r < mc.lambda; ++r) {
+  RowLoop<kMaxLambda>::run([&](auto rc) {
+    constexpr int r = decltype(rc)::value;
+    if (r < lam) {
       int64_t k = j - r;
       if (k < 0) k += N;
-      if (k < mc.nfold) {
-        acc += top * mc.fold[k] * series_coef(2, r, double(k), Nd, mc.cpre[r]);
-      }
+      acc += D(k) * coef_r<r>(fam, double(k), Nd, mc.cpre[r]);
     }
+  });
+  if (mc.mode == kModeHigh && top != 0.0 && j < mc.nfold + lam) {
+    // out[(k + r) mod N] += top * fold[k] * gamma_r(k), k < nfold
+    RowLoop<kMaxLambda>::run([&](auto rc) {
+      constexpr int r = decltype(rc)::value;
+      if (r < lam) {
+        int64_t k = j - r;
+        if (k < 0) k += N;
+        if (k < mc.nfold) acc += top * mc.fold[k] * coef_r<r>(2, double(k), Nd, mc.cpre[r]);
+      }
+    });
   }
   return acc;
 }
@@ -62,16 +66,15 @@ template <class WF>
 __device__ __forceinline__ double post_flat(const MapConsts& mc, const WF& W,
                                             int64_t j) {
   const int64_t N = mc.N;
+  const double Nd = double(N);
   const int fam = (mc.mode == kModeLow) ? 1 : 3;
-  int64_t rlo = j - N + 1;
-  if (rlo < 0) rlo = 0;
-  int64_t rhi = mc.lambda - 1;
-  if (rhi > j) rhi = j;
+  const int lam = mc.lambda;
   double acc = 0.0;
-  for (int64_t r = rlo; r <= rhi; ++r) {
-    int64_t k = j - r;
-    acc += W(k) * series_coef(fam, int(r), double(k), double(N), mc.cpost[r]);
-  }
+  RowLoop<kMaxLambda>::run([&](auto rc) {
+    constexpr int r = decltype(rc)::value;
+    const int64_t k = j - r;
+    if (r < lam && k >= 0 && k < N) acc += W(k) * coef_r<r>(fam, double(k), Nd, mc.cpost[r]);
+  });
   return acc;
 }
 

@@ -161,6 +161,7 @@ SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride) {
   std::memset(&s, 0, sizeof(s));
   s.R = R;
   s.tw = tw;
+  s.twlen = R * tw_stride;
   auto rad = radix_schedule(R);
   s.nst = int32_t(rad.size());
   uint32_t Ns = 1;
@@ -350,27 +351,47 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   pl->iA = pl->fA;
   pl->fC = make_subfft(C, tC, 1);
   pl->iC = make_subfft(C / 2, tC, 2);
-  pl->logc_f1 = pick_logc(A, UL / A, cap);
-  pl->thr_f1 = threads_for(uint64_t(A) << pl->logc_f1);
-  pl->smem_f1 = size_t(padded_len(A << pl->logc_f1)) * 16;
-  const uint64_t il_cols = uint64_t(B) * (C / 2);
+  {
+    // F1: columns per CTA so that the FFT buffer, the twiddle tables and the
+    // staged limbs / carry words fit one CTA's shared memory
+    const uint32_t lam = (p.mode == PMode::kFull) ? 1u : uint32_t(p.lambda);
+    const uint32_t p2 = largest_pow2_divisor(UL / A);
+    uint32_t best = 0;
+    for (uint32_t lc = 0; lc <= 6; ++lc) {
+      const uint32_t c = 1u << lc;
+      if (c > p2) break;
+      const uint32_t cnt = c + lam - 1;
+      const uint32_t nlr = (cnt * uint32_t(b) + 63) / 64 + 2;
+      const uint32_t ncb = (cnt + 31) / 32 + 1;
+      const uint32_t rows = (p.mode == PMode::kFull) ? (A + 1) / 2 : A;
+      const uint64_t thr = (uint64_t(A) * c + 15) / 16;
+      if (thr > 512 || f1_smem_layout(A, c, rows, nlr, ncb).total > 220 * 1024) break;
+      best = lc;
+      pl->f1_nlr = nlr;
+      pl->f1_ncb = ncb;
+      pl->f1_rows = rows;
+      if (thr >= 256 && c >= 4) break;
+    }
+    pl->logc_f1 = best;
+    pl->thr_f1 = threads_for(uint64_t(A) << best);
+    pl->smem_f1 = f1_smem_layout(A, 1u << best, pl->f1_rows, pl->f1_nlr, pl->f1_ncb).total;
+  }
   pl->logc_il = pick_logc(A, C / 2, cap);
   pl->thr_il = threads_for(uint64_t(A) << pl->logc_il);
-  pl->smem_il = size_t(padded_len(A << pl->logc_il)) * 16;
-  (void)il_cols;
+  pl->smem_il = col_smem_bytes(A, 1u << pl->logc_il);
   if (pl->kind == 3) {
     const double2* tB = tw.table(B);
     pl->fB = make_subfft(B, tB, 1);
     pl->iB = pl->fB;
     pl->logc_f2 = pick_logc(B, C, cap);
     pl->thr_f2 = threads_for(uint64_t(B) << pl->logc_f2);
-    pl->smem_f2 = size_t(padded_len(B << pl->logc_f2)) * 16;
+    pl->smem_f2 = col_smem_bytes(B, 1u << pl->logc_f2);
     pl->logc_i2 = pick_logc(B, C / 2, cap);
     pl->thr_i2 = threads_for(uint64_t(B) << pl->logc_i2);
-    pl->smem_i2 = size_t(padded_len(B << pl->logc_i2)) * 16;
+    pl->smem_i2 = col_smem_bytes(B, 1u << pl->logc_i2);
   }
   pl->thr_mid = threads_for(uint64_t(2) * C);
-  pl->smem_mid = size_t(2) * (padded_len(C) + 4) * 16;
+  pl->smem_mid = mid_smem_bytes(C);
   const int64_t LB = kCarryThreads * kCarryPerThread;
   pl->smem_carry = carry_smem(b);
   (void)LB;
@@ -379,7 +400,8 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
 }
 
 size_t small_smem_bytes(int64_t L, int64_t nlimbs) {
-  return size_t(padded_len(uint32_t(L))) * 16 + size_t(2 * nlimbs) * 8 + 32 * 4 + 8 * 8;
+  return size_t(padded_len(uint32_t(L))) * 16 + size_t(2 * nlimbs) * 8 + 32 * 4 + 8 * 8 +
+         size_t(tw_smem_len(uint32_t(L))) * 16;
 }
 
 }  // namespace tmg
