@@ -81,7 +81,7 @@ struct Context {
   bool own_stream = false;
   TwiddleCache tw;
   std::map<std::tuple<int64_t, int32_t, int64_t, int64_t, int32_t>, std::unique_ptr<Plan>> plans;
-  DevBuf work_t, work_c, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf;
+  DevBuf work_t, work_c, work_z, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf;
   ScanSlot scan_u, scan_v, scan_c, scan_h;
   bool debug_sync = false;
   DevStatus* h_status = nullptr;  // pinned
@@ -190,6 +190,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
   const int64_t L = pl.L;
   cx.work_t.ensure(size_t(L) * 16);
   cx.work_c.ensure(size_t(L) * 8 + 64);
+  cx.work_z.ensure(size_t(p.N) * 16 + 64);
   const int64_t cwords = (pl.count + 31) / 32 + 1;
   cx.cbu.ensure(size_t(cwords) * 4);
   cx.cbv.ensure(size_t(cwords) * 4);
@@ -199,34 +200,42 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     const uint64_t* u = du + i * pl.nlimbs;
     const uint64_t* v = dv + i * pl.nlimbs;
     uint64_t* out = dout + i * pl.out_limbs;
-    // split carry scan
+    // balanced split + pre-map (both operands)
     {
-      SplitScanArgs a;
+      ZgenArgs a;
       a.u = u;
       a.v = v;
       a.nlimbs = pl.nlimbs;
       a.n = p.n;
       a.b = p.b;
       a.count = pl.count;
+      a.N = p.N;
       a.lead = pl.lead;
       a.cbits_u = cx.cbu.as<uint32_t>();
       a.cbits_v = cx.cbv.as<uint32_t>();
-      const unsigned blocks = unsigned((pl.count + kSplitChunks - 1) / kSplitChunks);
-      const size_t ssm = split_scan_smem(p.b);
-      set_smem(k_split_scan, ssm);
-      a.scan_u = cx.scan_u.next(blocks);
-      a.scan_v = cx.scan_v.next(blocks);
+      a.z = cx.work_z.as<double2>();
+      a.mc = pl.mc;
+      const unsigned blocks = unsigned((pl.count + kZgenChunks - 1) / kZgenChunks);
+      a.scan = cx.scan_u.next(blocks);
       a.status = status;
+      set_smem(k_zgen, pl.smem_zgen);
       {
-        KTimer kt(cx, "k_split_scan", double(2 * pl.nlimbs) * 8.0 + double(2 * pl.count) / 8.0, int(p.mode));
-        k_split_scan<<<dim3(blocks, 2), kSplitThreads, ssm, st>>>(a);
+        KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * 16.0, int(p.mode));
+        k_zgen<<<blocks, kZgenThreads, pl.smem_zgen, st>>>(a);
       }
-      check_launch("k_split_scan");
+      check_launch("k_zgen");
       ++kernels;
     }
     double2* T = cx.work_t.as<double2>();
     {
       F1Args a;
+      a.z = cx.work_z.as<double2>();
+      a.out = T;
+      a.ncols = uint32_t(L / pl.A);
+      a.logc = pl.logc_f1;
+      a.fft = pl.fA;
+      a.tw = pl.twL;
+      a.mc = pl.mc;
       a.u = u;
       a.v = v;
       a.nlimbs = pl.nlimbs;
@@ -235,19 +244,10 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.lead = pl.lead;
       a.cbits_u = cx.cbu.as<uint32_t>();
       a.cbits_v = cx.cbv.as<uint32_t>();
-      a.out = T;
-      a.ncols = uint32_t(L / pl.A);
-      a.logc = pl.logc_f1;
-      a.fft = pl.fA;
-      a.tw = pl.twL;
-      a.mc = pl.mc;
       a.aux = cx.aux.as<double>();
-      a.rows_staged = pl.f1_rows;
-      a.nlr = pl.f1_nlr;
-      a.ncb = pl.f1_ncb;
       set_smem(k_f1, pl.smem_f1);
       {
-        KTimer kt(cx, "k_f1", double(2 * pl.nlimbs) * 8.0 + double(L) * 16.0, int(p.mode));
+        KTimer kt(cx, "k_f1", double(p.N) * 16.0 + double(L) * 16.0, int(p.mode));
         k_f1<<<a.ncols >> a.logc, pl.thr_f1, pl.smem_f1, st>>>(a);
       }
       check_launch("k_f1");

@@ -42,6 +42,17 @@ struct TwTable {
   __device__ __forceinline__ double2 get(uint32_t x) const { return __ldg(t + x); }
 };
 
+// Full table staged in shared memory (one exact entry per twiddle).
+struct TwFull {
+  const double2* t;
+  __device__ __forceinline__ double2 get(uint32_t x) const { return t[x]; }
+};
+__device__ __forceinline__ TwFull load_tw_full(double2* dst, const SubFft& p, int tid,
+                                               int nthr) {
+  for (uint32_t i = tid; i < p.twlen; i += nthr) dst[i] = __ldg(p.tw + i);
+  return TwFull{dst};
+}
+
 // Two-level shared-memory table: omega^x = hi[x >> 6] * lo[x & 63].
 struct TwSmem {
   const double2* lo;

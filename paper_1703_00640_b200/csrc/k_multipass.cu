@@ -1,7 +1,7 @@
 // Multi-pass product pipeline for transform lengths beyond one CTA.
 //
-//   k_split_scan  carry-in bits of the balanced split (decoupled look-back)
-//   k_f1          limbs -> chunks -> pre-map -> column DFTs over A, twiddle
+//   k_zgen        (k_zgen.cu) balanced split + pre-map, carry look-back
+//   k_f1          column DFTs over A of the pre-mapped coefficients, twiddle
 //   k_col         generic column pass (forward over B, inverse over B)
 //   k_mid         row DFTs over C for a conjugate row pair, spectral product,
 //                 half-length inverse row DFT, twiddle
@@ -91,85 +91,6 @@ __device__ __forceinline__ void release_ticket(unsigned long long* ctr,
 }
 
 // ---------------------------------------------------------------------------
-// Balanced-split carry bits.  A block covers kSplitChunks chunks: it stages
-// the limbs under them in shared memory with coalesced loads, each thread
-// scans 32 consecutive chunks, and the block carry is resolved by a
-// warp-parallel decoupled look-back (split.cpp:294-298 made parallel).
-__global__ void __launch_bounds__(kSplitThreads)
-k_split_scan(SplitScanArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* sl = reinterpret_cast<uint64_t*>(smem_raw);
-  __shared__ uint32_t sw[32];
-  __shared__ uint32_t s_blk;
-  __shared__ int s_cin;
-  const bool isv = blockIdx.y == 1;
-  const uint64_t* limbs = isv ? a.v : a.u;
-  uint32_t* cbits = isv ? a.cbits_v : a.cbits_u;
-  ScanState sc = isv ? a.scan_v : a.scan_u;
-  const int tid = threadIdx.x;
-  if (tid == 0) s_blk = take_ticket(sc.ctr);
-  __syncthreads();
-  const uint32_t blk = s_blk;
-  const int b = a.b;
-  const int64_t c0 = int64_t(blk) * kSplitChunks;
-  const int64_t pos0 = c0 * b - a.lead;
-  const int64_t i0 = pos0 >> 6;
-  const int64_t nl = (int64_t(kSplitChunks) * b + 63) / 64 + 2;
-  for (int64_t i = tid; i < nl; i += kSplitThreads) {
-    const int64_t g = i0 + i;
-    sl[i] = (g >= 0 && g < a.nlimbs) ? __ldg(limbs + g) : 0ull;
-  }
-  __syncthreads();
-  const int64_t base = c0 + int64_t(tid) * 32;
-  uint32_t f = kTfIdentity;
-  uint32_t gen = 0, prop = 0;  // per-chunk generate / propagate bits
-  {
-    WindowReader<SmemLimbs> rd;
-    rd.init(SmemLimbs{sl, i0, nl}, base * b - a.lead, b);
-    const uint64_t half = 1ull << (b - 1);
-#pragma unroll 8
-    for (int q = 0; q < 32; ++q) {
-      const uint64_t w = rd.next();
-      if (base + q < a.count - 1) {
-        gen |= uint32_t(w > half) << q;
-        prop |= uint32_t(w == half) << q;
-      }
-    }
-    // thread aggregate: the last non-propagating chunk decides
-    const uint32_t np = ~prop;
-    if (np) {
-      const int last = 31 - __clz(np);
-      f = ((gen >> last) & 1u) ? tf_const(1) : tf_const(0);
-    }
-  }
-  uint32_t agg;
-  const uint32_t ex = block_scan_tf(f, sw, &agg);
-  if (tid < 32) {
-    const int cin = lookback_warp(sc.state, blk, agg, sc.epoch, 0);
-    if (tid == 0) s_cin = cin;
-  }
-  __syncthreads();
-  // carry into each chunk: propagate chunks pass the carry through
-  int c = tf_apply(ex, s_cin);
-  uint32_t bits = 0;
-#pragma unroll
-  for (int q = 0; q < 32; ++q) {
-    bits |= uint32_t(c) << q;
-    if (!((prop >> q) & 1u)) c = int((gen >> q) & 1u);
-  }
-  if (base < a.count) cbits[base >> 5] = bits;
-  if (blk == 0 && tid == 0 && (a.n & 63)) {
-    uint64_t top = __ldg(limbs + a.nlimbs - 1);
-    if (top >> (a.n & 63)) atomicOr(&a.status->flags, uint32_t(kFlagInputRange));
-  }
-  if (tid == 0) release_ticket(sc.ctr, gridDim.x);
-}
-
-size_t split_scan_smem(int b) {
-  return size_t((int64_t(kSplitChunks) * b + 63) / 64 + 2) * 8;
-}
-
-// ---------------------------------------------------------------------------
 // Column-pass sources and sinks.
 __device__ __forceinline__ int64_t col_off(const ColGeom& g, int64_t outer,
                                            uint32_t row, uint32_t col) {
@@ -209,184 +130,87 @@ struct ColSink {
 };
 
 // ---------------------------------------------------------------------------
-// F1: split + pre-map + forward column DFT over A (rows j_a, chunk index
-// j = j_a * ncols + col), twiddle omega_L^{col k_a}, store T[k_a][col].
-//   staging  the limbs and carry words under every row segment are fetched
-//            with independent loads into shared memory
-//   digits   one thread per row segment streams its c + lambda - 1 digits
-//            through a shift register (compile-time indexed) and applies the
-//            pre-map as the window slides
-//   DFT      fft_pass from shared memory; the output twiddle
-//            omega_L^{col k} = hi_col[k >> 6] * lo_col[k & 63] comes from
-//            per-column tables in shared memory
-__host__ __device__ F1Smem f1_smem_layout(uint32_t A, uint32_t c, uint32_t rows_staged, uint32_t nlr,
-                      uint32_t ncb) {
-  F1Smem m;
-  m.buf = size_t(padded_len(A * c)) * 16;
-  m.tw = size_t(tw_smem_len(A)) * 16;
-  m.coltw = size_t(c) * (64 + (A + 63) / 64) * 16;
-  m.limbs = size_t(2) * rows_staged * nlr * 8;
-  m.cbits = size_t(2) * rows_staged * ncb * 4;
-  m.total = m.buf + m.tw + m.coltw + m.limbs + m.cbits;
-  return m;
-}
-
-struct ColTwSink {
-  double2* out;
-  uint32_t ncols, col0, nhi;
-  const double2* ctw;  // per column: 64 lo entries then nhi hi entries
-  __device__ __forceinline__ void operator()(uint32_t item, uint32_t k, double2 v) const {
-    const double2* t = ctw + item * (64 + nhi);
-    if (k) v = cmul(v, cmul(t[64 + (k >> 6)], t[k & 63]));
-    out[int64_t(k) * ncols + col0 + item] = v;
+// F1: forward column DFTs over A of the pre-mapped coefficients z_j
+// (j = j_a * ncols + col; zero for j >= N, the full product's padding), the
+// high product's top-chunk fold added on the fly, twiddle omega_L^{col k_a},
+// store T[k_a][col].
+struct ZSrc {
+  const double2* z;
+  int64_t N;
+  uint32_t ncols, col0;
+  const MapConsts* mc;
+  double topu, topv;
+  __device__ __forceinline__ double2 operator()(uint32_t item, uint32_t e) const {
+    const int64_t j = int64_t(e) * ncols + col0 + item;
+    if (j >= N) return make_double2(0.0, 0.0);
+    double2 v = z[j];
+    if (mc->mode == kModeHigh && j < mc->nfold + mc->lambda) {
+      // gamma-dagger fold of the top coefficient (maps_f64.cpp:337-347)
+      const int lam = mc->lambda;
+      RowLoop<kMaxLambda>::run([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        if (r < lam) {
+          int64_t k = j - r;
+          if (k < 0) k += N;
+          if (k < mc->nfold) {
+            const double g = mc->fold[k] * coef_r<r>(2, double(k), double(N), mc->cpre[r]);
+            v.x += topu * g;
+            v.y += topv * g;
+          }
+        }
+      });
+    }
+    return v;
   }
 };
+
+struct F1Sink {
+  double2* out;
+  uint32_t ncols, col0;
+  TwGlobal tw;
+  __device__ __forceinline__ void operator()(uint32_t item, uint32_t k, double2 v) const {
+    const uint32_t col = col0 + item;
+    const uint32_t x = col * k;
+    if (x) v = cmul(v, tw.get(x));
+    out[int64_t(k) * ncols + col] = v;
+  }
+};
+
+size_t f1_smem_bytes(uint32_t A, uint32_t c) {
+  return size_t(padded_len(A * c)) * 16 + size_t(A) * 16;
+}
 
 __global__ void __launch_bounds__(512)
 k_f1(F1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x, nthr = blockDim.x;
   const uint32_t c = 1u << a.logc;
   const uint32_t col0 = blockIdx.x * c;
   const uint32_t A = a.fft.R;
   const MapConsts& mc = a.mc;
-  const int b = a.b;
   const int64_t N = mc.N;
-  const int lam = (mc.mode == kModeFull) ? 1 : mc.lambda;
-  const double Nd = double(N);
-  const F1Smem L = f1_smem_layout(A, c, a.rows_staged, a.nlr, a.ncb);
-  double2* sbuf = reinterpret_cast<double2*>(smem_raw);
-  double2* stw = reinterpret_cast<double2*>(smem_raw + L.buf);
-  double2* sctw = reinterpret_cast<double2*>(smem_raw + L.buf + L.tw);
-  uint64_t* slimb = reinterpret_cast<uint64_t*>(smem_raw + L.buf + L.tw + L.coltw);
-  uint32_t* scb = reinterpret_cast<uint32_t*>(smem_raw + L.buf + L.tw + L.coltw + L.limbs);
   LayCols lay{a.logc, c - 1};
-  const uint32_t RS = a.rows_staged, NLR = a.nlr, NCB = a.ncb;
-  const int cnt = int(c) + lam - 1;
-
-  // stage limbs and carry words (independent loads, many in flight)
-  for (uint32_t e = tid; e < 2 * RS * NLR; e += nthr) {
-    const uint32_t op = e / (RS * NLR), rem = e - op * RS * NLR;
-    const uint32_t row = rem / NLR, k = rem - row * NLR;
-    const int64_t js = int64_t(row) * a.ncols + col0 - (lam - 1);
-    const int64_t g = ((js * b - a.lead) >> 6) + k;
-    const uint64_t* lp = op ? a.v : a.u;
-    slimb[e] = (g >= 0 && g < a.nlimbs) ? __ldg(lp + g) : 0ull;
-  }
-  for (uint32_t e = tid; e < 2 * RS * NCB; e += nthr) {
-    const uint32_t op = e / (RS * NCB), rem = e - op * RS * NCB;
-    const uint32_t row = rem / NCB, k = rem - row * NCB;
-    const int64_t js = int64_t(row) * a.ncols + col0 - (lam - 1);
-    const int64_t g = (js >> 5) + k;
-    const uint32_t* cp = op ? a.cbits_v : a.cbits_u;
-    scb[e] = (js >= 0 && (g << 5) < a.count) ? __ldg(cp + g) : 0u;
-  }
-  // twiddle tables: omega_A two-level, and per column omega_L^{col k}
-  const TwSmem tw = load_tw_smem(stw, a.fft, tid, nthr);
-  const uint32_t nhi = (A + 63) / 64;
-  for (uint32_t e = tid; e < c * (64 + nhi); e += nthr) {
-    const uint32_t q = e / (64 + nhi), i = e - q * (64 + nhi);
-    const uint32_t col = col0 + q;
-    const uint32_t x = (i < 64) ? col * i : col * 64u * (i - 64);
-    sctw[e] = a.tw.get(x);
-  }
-
+  const TwFull tw = load_tw_full(sbuf + padded_len(A * c), a.fft, tid, nthr);
   double topu = 0.0, topv = 0.0;
   if (mc.mode == kModeHigh && col0 < uint32_t(mc.nfold + mc.lambda)) {
-    topu = digit_at(a.u, a.nlimbs, b, a.lead, a.count, a.cbits_u, N);
-    topv = digit_at(a.v, a.nlimbs, b, a.lead, a.count, a.cbits_v, N);
+    topu = digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, N);
+    topv = digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, N);
   }
   if (mc.mode == kModeHigh && blockIdx.x == 0 && tid == 0) {
-    auto Du = [&](int64_t i) { return digit_at(a.u, a.nlimbs, b, a.lead, a.count, a.cbits_u, i); };
-    auto Dv = [&](int64_t i) { return digit_at(a.v, a.nlimbs, b, a.lead, a.count, a.cbits_v, i); };
+    auto Du = [&](int64_t i) { return digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, i); };
+    auto Dv = [&](int64_t i) { return digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, i); };
     a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
   }
   __syncthreads();
-  const int fam = (mc.mode == kModeLow) ? 0 : 2;
-
-  for (uint32_t row = tid; row < A; row += nthr) {
-    const int64_t j0 = int64_t(row) * a.ncols + col0;
-    if (row >= RS || (mc.mode == kModeFull && j0 >= N)) {
-      for (uint32_t q = 0; q < c; ++q) sbuf[lay.idx(q, row)] = make_double2(0.0, 0.0);
-      continue;
-    }
-    const int64_t js = j0 - (lam - 1);
-    const int64_t i0 = (js * b - a.lead) >> 6;
-    WindowReader<SmemLimbs> ru, rv;
-    ru.init(SmemLimbs{slimb + size_t(row) * NLR, i0, NLR}, js * b - a.lead, b);
-    rv.init(SmemLimbs{slimb + size_t(RS + row) * NLR, i0, NLR}, js * b - a.lead, b);
-    const uint32_t* cbu = scb + size_t(row) * NCB;
-    const uint32_t* cbv = scb + size_t(RS + row) * NCB;
-    const int64_t w0 = js >> 5;
-    const bool fast = js >= 0;
-    double wu[kMaxLambda], wv[kMaxLambda];
-#pragma unroll
-    for (int r = 0; r < kMaxLambda; ++r) wu[r] = wv[r] = 0.0;
-    for (int q = 0; q < cnt; ++q) {
-      const int64_t j = js + q;
-      double du, dv;
-      if (fast) {
-        const uint64_t xu = ru.next(), xv = rv.next();
-        const int64_t wi = (j >> 5) - w0;
-        const int cu = int((cbu[wi] >> (j & 31)) & 1u);
-        const int cv = int((cbv[wi] >> (j & 31)) & 1u);
-        du = double(split_digit(xu, cu, b, j == a.count - 1));
-        dv = double(split_digit(xv, cv, b, j == a.count - 1));
-      } else {
-        const int64_t jj = j < 0 ? j + N : j;
-        du = digit_at(a.u, a.nlimbs, b, a.lead, a.count, a.cbits_u, jj);
-        dv = digit_at(a.v, a.nlimbs, b, a.lead, a.count, a.cbits_v, jj);
-      }
-      if (mc.mode == kModeFull) {
-        sbuf[lay.idx(uint32_t(q), row)] = (j < N) ? make_double2(du, dv) : make_double2(0.0, 0.0);
-        continue;
-      }
-#pragma unroll
-      for (int r = kMaxLambda - 1; r > 0; --r) {
-        wu[r] = wu[r - 1];
-        wv[r] = wv[r - 1];
-      }
-      wu[0] = du;
-      wv[0] = dv;
-      if (q >= lam - 1) {
-        // transform index j; digit d[(j - r) mod N] sits in w*[r]
-        double au = 0.0, av = 0.0;
-        RowLoop<kMaxLambda>::run([&](auto rc) {
-          constexpr int r = decltype(rc)::value;
-          if (r < lam) {
-            int64_t k = j - r;
-            if (k < 0) k += N;
-            const double cf = coef_r<r>(fam, double(k), Nd, mc.cpre[r]);
-            au += wu[r] * cf;
-            av += wv[r] * cf;
-          }
-        });
-        if (mc.mode == kModeHigh && j < mc.nfold + mc.lambda) {
-          RowLoop<kMaxLambda>::run([&](auto rc) {
-            constexpr int r = decltype(rc)::value;
-            if (r < lam) {
-              int64_t k = j - r;
-              if (k < 0) k += N;
-              if (k < mc.nfold) {
-                const double g = mc.fold[k] * coef_r<r>(2, double(k), Nd, mc.cpre[r]);
-                au += topu * g;
-                av += topv * g;
-              }
-            }
-          });
-        }
-        sbuf[lay.idx(uint32_t(q - (lam - 1)), row)] = make_double2(au, av);
-      }
-    }
-  }
-  __syncthreads();
-  fft_pass<false>(sbuf, lay, a.fft, tw, SmemSrc<LayCols>{sbuf, lay},
-                  ColTwSink{a.out, a.ncols, col0, nhi, sctw}, tid, nthr);
+  const int64_t Nz = (mc.mode == kModeFull) ? N : N;  // z holds N entries
+  fft_pass<false>(sbuf, lay, a.fft, tw, ZSrc{a.z, Nz, a.ncols, col0, &a.mc, topu, topv},
+                  F1Sink{a.out, a.ncols, col0, a.tw}, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
 size_t col_smem_bytes(uint32_t R, uint32_t c) {
-  return size_t(padded_len(R * c)) * 16 + size_t(tw_smem_len(R)) * 16;
+  return size_t(padded_len(R * c)) * 16 + size_t(R) * 16;
 }
 
 __global__ void __launch_bounds__(512)
@@ -398,7 +222,7 @@ k_col(ColArgs a) {
   const uint32_t col0 = blockIdx.x * c;
   const int64_t outer = blockIdx.y;
   LayCols lay{a.logc, c - 1};
-  const TwSmem tw = load_tw_smem(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
+  const TwFull tw = load_tw_full(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
   __syncthreads();
   ColSrc src{a.data, a.g, outer, col0};
   ColSink sink{a.data, a.g, outer, col0, a.tw, a.to, a.tc, a.tmul, a.inv != 0, true};
@@ -416,23 +240,20 @@ struct RowSrc {
   }
 };
 
-// Output twiddle omega_L^{2 r m} from per-row two-level tables.
 struct RowSink {
   double2* data;
   int64_t base0, base1;
-  const double2* rtw;  // per row: 64 lo entries then nhi hi entries
-  uint32_t nhi;
+  uint32_t r0, r1;
+  TwGlobal tw;
   __device__ __forceinline__ void operator()(uint32_t item, uint32_t m, double2 v) const {
-    const double2* t = rtw + item * (64 + nhi);
-    if (m) v = cmulc(v, cmul(t[64 + (m >> 6)], t[m & 63]));
+    const uint32_t x = 2u * (item ? r1 : r0) * m;  // omega_{L/2}^{r m} = omega_L^{2 r m}
+    if (x) v = cmulc(v, tw.get(x));
     data[(item ? base1 : base0) + m] = v;
   }
 };
 
 size_t mid_smem_bytes(uint32_t C) {
-  const uint32_t H = C / 2;
-  return size_t(2) * (padded_len(C) + 4) * 16 + size_t(tw_smem_len(C)) * 16 +
-         size_t(2) * (64 + (H + 63) / 64) * 16 + 64;
+  return size_t(2) * (padded_len(C) + 4) * 16 + size_t(C) * 16;
 }
 
 __global__ void __launch_bounds__(512)
@@ -449,19 +270,7 @@ k_mid(MidArgs a) {
   LayRows lay{nrows, rowstride};
   const int64_t base0 = (int64_t(r0 % a.A) * a.B + (r0 / a.A)) * int64_t(C);
   const int64_t base1 = (int64_t(r1 % a.A) * a.B + (r1 / a.A)) * int64_t(C);
-  double2* stw = sbuf + 2 * rowstride;
-  const uint32_t nhiC = (C + 63) / 64;
-  double2* srtw = stw + 64 + nhiC;
-  double2* srow = srtw + 2 * (64 + (H + 63) / 64);  // omega_L^{r} per row
-  const TwSmem tw = load_tw_smem(stw, a.fwd, tid, nthr);
-  const uint32_t nhiH = (H + 63) / 64;
-  for (uint32_t e = tid; e < 2 * (64 + nhiH); e += nthr) {
-    const uint32_t i = e / (64 + nhiH), k = e - i * (64 + nhiH);
-    const uint32_t r2 = 2u * (i ? r1 : r0);
-    const uint32_t x = (k < 64) ? r2 * k : r2 * 64u * (k - 64);
-    srtw[e] = a.tw.get(x);
-  }
-  if (tid < 2) srow[tid] = a.tw.get(tid ? r1 : r0);
+  const TwFull tw = load_tw_full(sbuf + 2 * rowstride, a.fwd, tid, nthr);
 
   fft_pass<false>(sbuf, lay, a.fwd, tw, RowSrc{a.data, base0, base1},
                   SmemSink<LayRows>{sbuf, lay}, tid, nthr);
@@ -483,19 +292,18 @@ k_mid(MidArgs a) {
     if (!(nrows == 1 && kp == k)) sbuf[lay.idx(ip, kp)] = cconj(w);
   }
   __syncthreads();
-  // Y_k = (W_k + W_{k+L/2}) + i e^{2 pi i k / L} (W_k - W_{k+L/2}),
-  // k = r + AB k_c: omega_L^k = omega_L^r omega_C^{k_c}
+  // Y_k = (W_k + W_{k+L/2}) + i e^{2 pi i k / L} (W_k - W_{k+L/2})
   for (uint32_t e = tid; e < nrows * H; e += nthr) {
     const uint32_t i = e >= H ? 1 : 0, k = e - i * H;
+    const uint32_t r = i ? r1 : r0;
     const double2 w1 = sbuf[lay.idx(i, k)], w2 = sbuf[lay.idx(i, k + H)];
     const double2 ev = cadd(w1, w2);
-    const double2 om = cmul(srow[i], tw.get(k));
-    const double2 o = cmulc(csub(w1, w2), om);
+    const double2 o = cmulc(csub(w1, w2), a.tw.get(r + AB * k));
     sbuf[lay.idx(i, k)] = make_double2(ev.x - o.y, ev.y + o.x);
   }
   __syncthreads();
   fft_pass<true>(sbuf, lay, a.inv, tw, SmemSrc<LayRows>{sbuf, lay},
-                 RowSink{a.data, base0, base1, srtw, nhiH}, tid, nthr);
+                 RowSink{a.data, base0, base1, r0, r1, a.tw}, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
@@ -515,7 +323,7 @@ k_ilast(ILastArgs a) {
   const uint32_t c = 1u << a.logc;
   const uint32_t col0 = blockIdx.x * c;
   LayCols lay{a.logc, c - 1};
-  const TwSmem tw = load_tw_smem(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
+  const TwFull tw = load_tw_full(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
   __syncthreads();
   fft_pass<true>(sbuf, lay, a.fft, tw, ColSrc{a.data, a.g, 0, col0},
                  CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);

@@ -49,24 +49,6 @@ struct ScanState {
   uint32_t epoch;
 };
 
-struct SplitScanArgs {
-  const uint64_t* u;
-  const uint64_t* v;
-  int64_t nlimbs;
-  int64_t n;
-  int32_t b;
-  int64_t count;
-  int64_t lead;
-  uint32_t* cbits_u;  // carry-in bit per chunk
-  uint32_t* cbits_v;
-  ScanState scan_u, scan_v;
-  DevStatus* status;
-};
-constexpr int kSplitThreads = 256;
-constexpr int kSplitChunks = kSplitThreads * 32;  // chunks per block
-__global__ void k_split_scan(SplitScanArgs a);
-size_t split_scan_smem(int b);
-
 // Column pass geometry: element (outer, row, col) at
 //   outer * os + row * rs + (col / cw) * cs + (col % cw)
 struct ColGeom {
@@ -75,7 +57,39 @@ struct ColGeom {
   uint32_t ncols;  // columns per outer matrix
 };
 
+// Balanced split + pre-map of both operands (k_zgen.cu).
+struct ZgenArgs {
+  const uint64_t* u;
+  const uint64_t* v;
+  int64_t nlimbs;
+  int64_t n;
+  int32_t b;
+  int64_t count;  // chunks per operand (N, or N + 1 for the high split)
+  int64_t N;      // transform chunks
+  int64_t lead;
+  uint32_t* cbits_u;  // carry-in bit per chunk
+  uint32_t* cbits_v;
+  double2* z;         // pre-mapped coefficients (N entries)
+  MapConsts mc;
+  ScanState scan;
+  DevStatus* status;
+};
+constexpr int kZgenThreads = 256;
+constexpr int kZgenPer = 16;
+constexpr int kZgenChunks = kZgenThreads * kZgenPer;
+__global__ void k_zgen(ZgenArgs a);
+size_t zgen_smem(int b);
+
+// F1: forward column DFTs over A of the pre-mapped coefficients.
 struct F1Args {
+  const double2* z;
+  double2* out;    // T[k_a][col], row length ncols
+  uint32_t ncols;  // = L / A
+  uint32_t logc;   // columns per CTA = 2^logc
+  SubFft fft;      // length A
+  TwGlobal tw;     // omega_L
+  MapConsts mc;
+  // high product: top-chunk fold (maps_f64.cpp:337-347) and root channel
   const uint64_t* u;
   const uint64_t* v;
   int64_t nlimbs;
@@ -84,24 +98,10 @@ struct F1Args {
   int64_t lead;
   const uint32_t* cbits_u;
   const uint32_t* cbits_v;
-  double2* out;    // T[k_a][col], row length ncols
-  uint32_t ncols;  // = L / A
-  uint32_t logc;   // columns per CTA = 2^logc
-  SubFft fft;      // length A
-  TwGlobal tw;     // omega_L
-  MapConsts mc;
-  double* aux;     // high: [0] theta_u*theta_v
-  // shared-memory staging of the limbs / carry words under each row segment
-  uint32_t rows_staged;  // rows whose inputs are staged (A, or A/2 for full)
-  uint32_t nlr;          // limbs per row segment
-  uint32_t ncb;          // carry words per row segment
+  double* aux;  // [0] theta_u * theta_v
 };
 __global__ void k_f1(F1Args a);
-struct F1Smem {
-  size_t buf, tw, coltw, limbs, cbits, total;
-};
-__host__ __device__ F1Smem f1_smem_layout(uint32_t A, uint32_t c, uint32_t rows_staged, uint32_t nlr,
-                      uint32_t ncb);
+size_t f1_smem_bytes(uint32_t A, uint32_t c);
 
 struct ColArgs {
   double2* data;  // in place

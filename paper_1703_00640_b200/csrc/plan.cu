@@ -103,7 +103,7 @@ uint32_t pick_logc(uint32_t R, uint64_t ncols, size_t smem_cap) {
     const uint32_t c = 1u << lc;
     if (c > p2) break;
     const uint64_t thr = (uint64_t(R) * c + 15) / 16;
-    const size_t smem = size_t(padded_len(R * c)) * 16;
+    const size_t smem = size_t(padded_len(R * c)) * 16 + size_t(R) * 16;
     if (thr > 512 || smem > smem_cap) break;
     best = lc;
     if (thr >= 256 && c >= 4) break;
@@ -351,31 +351,9 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   pl->iA = pl->fA;
   pl->fC = make_subfft(C, tC, 1);
   pl->iC = make_subfft(C / 2, tC, 2);
-  {
-    // F1: columns per CTA so that the FFT buffer, the twiddle tables and the
-    // staged limbs / carry words fit one CTA's shared memory
-    const uint32_t lam = (p.mode == PMode::kFull) ? 1u : uint32_t(p.lambda);
-    const uint32_t p2 = largest_pow2_divisor(UL / A);
-    uint32_t best = 0;
-    for (uint32_t lc = 0; lc <= 6; ++lc) {
-      const uint32_t c = 1u << lc;
-      if (c > p2) break;
-      const uint32_t cnt = c + lam - 1;
-      const uint32_t nlr = (cnt * uint32_t(b) + 63) / 64 + 2;
-      const uint32_t ncb = (cnt + 31) / 32 + 1;
-      const uint32_t rows = (p.mode == PMode::kFull) ? (A + 1) / 2 : A;
-      const uint64_t thr = (uint64_t(A) * c + 15) / 16;
-      if (thr > 512 || f1_smem_layout(A, c, rows, nlr, ncb).total > 220 * 1024) break;
-      best = lc;
-      pl->f1_nlr = nlr;
-      pl->f1_ncb = ncb;
-      pl->f1_rows = rows;
-      if (thr >= 256 && c >= 4) break;
-    }
-    pl->logc_f1 = best;
-    pl->thr_f1 = threads_for(uint64_t(A) << best);
-    pl->smem_f1 = f1_smem_layout(A, 1u << best, pl->f1_rows, pl->f1_nlr, pl->f1_ncb).total;
-  }
+  pl->logc_f1 = pick_logc(A, UL / A, cap);
+  pl->thr_f1 = threads_for(uint64_t(A) << pl->logc_f1);
+  pl->smem_f1 = f1_smem_bytes(A, 1u << pl->logc_f1);
   pl->logc_il = pick_logc(A, C / 2, cap);
   pl->thr_il = threads_for(uint64_t(A) << pl->logc_il);
   pl->smem_il = col_smem_bytes(A, 1u << pl->logc_il);
@@ -396,6 +374,7 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   pl->smem_carry = carry_smem(b);
   (void)LB;
   pl->kernels = ((pl->kind == 2) ? 5 : 7) + (p.mode == PMode::kHigh ? 1 : 0);
+  pl->smem_zgen = zgen_smem(b);
   return pl;
 }
 

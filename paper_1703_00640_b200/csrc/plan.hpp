@@ -63,7 +63,7 @@ struct Plan {
   size_t smem_f1 = 0, smem_f2 = 0, smem_i2 = 0, smem_il = 0, smem_mid = 0,
          smem_carry = 0;
   int thr_f1 = 0, thr_f2 = 0, thr_i2 = 0, thr_il = 0, thr_mid = 0;
-  uint32_t f1_rows = 0, f1_nlr = 0, f1_ncb = 0;
+  size_t smem_zgen = 0;
   int kernels = 0;
 };
 
