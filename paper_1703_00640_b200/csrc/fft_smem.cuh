@@ -29,7 +29,43 @@ struct SubFft {
   FastDiv fdNs[kMaxStages];
   const double2* tw;  // omega_T^x, x in [0, T), forward sign (T = R * stride)
   uint32_t twlen;     // T
+  // Per-stage twiddle table, q-major: stage s, butterfly offset j < Ns,
+  // q = 1..rad-1 at stab[toff[s] + (q * qmul[s] - 1) * Ns[s] + j] holds
+  // omega_{Ns rad}^{j q} exactly (consecutive j -> consecutive entries, so
+  // the reads of a warp are bank-conflict free).
+  const double2* stab;
+  uint32_t stablen;
+  uint32_t toff[kMaxStages];
+  uint32_t qmul[kMaxStages];
 };
+
+// Per-stage accessors used inside stage_store: get(j, q) = omega_{Ns r}^{j q}.
+struct TwQStage {
+  const double2* base;
+  uint32_t Ns, qmul;
+  __device__ __forceinline__ double2 get(uint32_t j, uint32_t q) const {
+    return base[(q * qmul - 1) * Ns + j];
+  }
+};
+template <class TW>
+struct TwQFlat {
+  TW tw;
+  uint32_t step;
+  __device__ __forceinline__ double2 get(uint32_t j, uint32_t q) const { return tw.get(j * q * step); }
+};
+
+// Stage table staged in shared memory.
+struct TwStage {
+  const double2* t;
+  __device__ __forceinline__ TwQStage stage(const SubFft& p, int s) const {
+    return TwQStage{t + p.toff[s], p.Ns[s], p.qmul[s]};
+  }
+};
+__device__ __forceinline__ TwStage load_tw_stage(double2* dst, const SubFft& p, int tid,
+                                                 int nthr) {
+  for (uint32_t i = tid; i < p.stablen; i += nthr) dst[i] = __ldg(p.stab + i);
+  return TwStage{dst};
+}
 
 __device__ __forceinline__ uint32_t padidx(uint32_t i) { return i + (i >> 4); }
 __host__ __device__ inline uint32_t padded_len(uint32_t n) {
@@ -40,12 +76,18 @@ __host__ __device__ inline uint32_t padded_len(uint32_t n) {
 struct TwTable {
   const double2* t;
   __device__ __forceinline__ double2 get(uint32_t x) const { return __ldg(t + x); }
+  __device__ __forceinline__ TwQFlat<TwTable> stage(const SubFft& p, int s) const {
+    return TwQFlat<TwTable>{*this, p.twstep[s]};
+  }
 };
 
 // Full table staged in shared memory (one exact entry per twiddle).
 struct TwFull {
   const double2* t;
   __device__ __forceinline__ double2 get(uint32_t x) const { return t[x]; }
+  __device__ __forceinline__ TwQFlat<TwFull> stage(const SubFft& p, int s) const {
+    return TwQFlat<TwFull>{*this, p.twstep[s]};
+  }
 };
 __device__ __forceinline__ TwFull load_tw_full(double2* dst, const SubFft& p, int tid,
                                                int nthr) {
@@ -59,6 +101,9 @@ struct TwSmem {
   const double2* hi;
   __device__ __forceinline__ double2 get(uint32_t x) const {
     return cmul(hi[x >> 6], lo[x & 63]);
+  }
+  __device__ __forceinline__ TwQFlat<TwSmem> stage(const SubFft& p, int s) const {
+    return TwQFlat<TwSmem>{*this, p.twstep[s]};
   }
 };
 __host__ __device__ inline uint32_t tw_smem_len(uint32_t T) { return 64 + (T + 63) / 64; }
@@ -128,12 +173,11 @@ __device__ __forceinline__ void stage_load(double2 (&x)[kXMax], const Lay& lay,
 }
 
 // Twiddle, DFT and stores of one stage (outputs to sink(item, k, value)).
-template <int RAD, bool INV, class Lay, class TW, class Sink>
+template <int RAD, bool INV, class Lay, class TWQ, class Sink>
 __device__ __forceinline__ void stage_store(double2 (&x)[kXMax], const Lay& lay,
                                             uint32_t R, uint32_t Ns,
-                                            const FastDiv& fdNs, uint32_t twstep,
-                                            const TW& tw, const Sink& sink,
-                                            int tid, int nthr) {
+                                            const FastDiv& fdNs, const TWQ& twq,
+                                            const Sink& sink, int tid, int nthr) {
   constexpr int NB = (16 + RAD - 1) / RAD;
   const uint32_t nbf_item = R / RAD;
   const uint32_t nbf = nbf_item * lay.nitems();
@@ -147,10 +191,9 @@ __device__ __forceinline__ void stage_store(double2 (&x)[kXMax], const Lay& lay,
       uint32_t j = t - tq * Ns;
       double2* xv = x + it * RAD;
       if (j != 0) {
-        uint32_t step = j * twstep;
 #pragma unroll
         for (int q = 1; q < RAD; ++q) {
-          double2 w = tw.get(step * q);
+          double2 w = twq.get(j, uint32_t(q));
           xv[q] = INV ? cmulc(xv[q], w) : cmul(xv[q], w);
         }
       }
@@ -219,14 +262,14 @@ __device__ __forceinline__ void fft_pass(double2* __restrict__ buf, const Lay& l
     }
     __syncthreads();
     const uint32_t Ns = p.Ns[s];
-    const uint32_t ts = p.twstep[s];
+    const auto twq = tw.stage(p, s);
     const FastDiv fd = p.fdNs[s];
     if (s == last) {
-#define TMG_S(RR) stage_store<RR, INV>(x, lay, p.R, Ns, fd, ts, tw, sink, tid, nthr)
+#define TMG_S(RR) stage_store<RR, INV>(x, lay, p.R, Ns, fd, twq, sink, tid, nthr)
       TMG_RADIX_SWITCH(rad, TMG_S)
 #undef TMG_S
     } else {
-#define TMG_S(RR) stage_store<RR, INV>(x, lay, p.R, Ns, fd, ts, tw, ssink, tid, nthr)
+#define TMG_S(RR) stage_store<RR, INV>(x, lay, p.R, Ns, fd, twq, ssink, tid, nthr)
       TMG_RADIX_SWITCH(rad, TMG_S)
 #undef TMG_S
       __syncthreads();

@@ -177,7 +177,7 @@ struct F1Sink {
 };
 
 size_t f1_smem_bytes(uint32_t A, uint32_t c) {
-  return size_t(padded_len(A * c)) * 16 + size_t(A) * 16;
+  return size_t(padded_len(A * c)) * 16 + size_t(A) * 16;  // data + stage table (< A)
 }
 
 __global__ void __launch_bounds__(512)
@@ -191,7 +191,7 @@ k_f1(F1Args a) {
   const MapConsts& mc = a.mc;
   const int64_t N = mc.N;
   LayCols lay{a.logc, c - 1};
-  const TwFull tw = load_tw_full(sbuf + padded_len(A * c), a.fft, tid, nthr);
+  const TwStage tw = load_tw_stage(sbuf + padded_len(A * c), a.fft, tid, nthr);
   double topu = 0.0, topv = 0.0;
   if (mc.mode == kModeHigh && col0 < uint32_t(mc.nfold + mc.lambda)) {
     topu = digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, N);
@@ -222,7 +222,7 @@ k_col(ColArgs a) {
   const uint32_t col0 = blockIdx.x * c;
   const int64_t outer = blockIdx.y;
   LayCols lay{a.logc, c - 1};
-  const TwFull tw = load_tw_full(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
+  const TwStage tw = load_tw_stage(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
   __syncthreads();
   ColSrc src{a.data, a.g, outer, col0};
   ColSink sink{a.data, a.g, outer, col0, a.tw, a.to, a.tc, a.tmul, a.inv != 0, true};
@@ -252,8 +252,8 @@ struct RowSink {
   }
 };
 
-size_t mid_smem_bytes(uint32_t C) {
-  return size_t(2) * (padded_len(C) + 4) * 16 + size_t(C) * 16;
+size_t mid_smem_bytes(uint32_t C, uint32_t inv_stablen) {
+  return size_t(2) * (padded_len(C) + 4) * 16 + size_t(C) * 16 + size_t(inv_stablen) * 16;
 }
 
 __global__ void __launch_bounds__(512)
@@ -270,7 +270,11 @@ k_mid(MidArgs a) {
   LayRows lay{nrows, rowstride};
   const int64_t base0 = (int64_t(r0 % a.A) * a.B + (r0 / a.A)) * int64_t(C);
   const int64_t base1 = (int64_t(r1 % a.A) * a.B + (r1 / a.A)) * int64_t(C);
-  const TwFull tw = load_tw_full(sbuf + 2 * rowstride, a.fwd, tid, nthr);
+  double2* stw = sbuf + 2 * rowstride;
+  const TwStage tw = load_tw_stage(stw, a.fwd, tid, nthr);
+  const TwStage twi = (a.inv.stab == a.fwd.stab)
+                          ? tw
+                          : load_tw_stage(stw + a.fwd.stablen, a.inv, tid, nthr);
 
   fft_pass<false>(sbuf, lay, a.fwd, tw, RowSrc{a.data, base0, base1},
                   SmemSink<LayRows>{sbuf, lay}, tid, nthr);
@@ -302,7 +306,7 @@ k_mid(MidArgs a) {
     sbuf[lay.idx(i, k)] = make_double2(ev.x - o.y, ev.y + o.x);
   }
   __syncthreads();
-  fft_pass<true>(sbuf, lay, a.inv, tw, SmemSrc<LayRows>{sbuf, lay},
+  fft_pass<true>(sbuf, lay, a.inv, twi, SmemSrc<LayRows>{sbuf, lay},
                  RowSink{a.data, base0, base1, r0, r1, a.tw}, tid, nthr);
 }
 
@@ -323,7 +327,7 @@ k_ilast(ILastArgs a) {
   const uint32_t c = 1u << a.logc;
   const uint32_t col0 = blockIdx.x * c;
   LayCols lay{a.logc, c - 1};
-  const TwFull tw = load_tw_full(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
+  const TwStage tw = load_tw_stage(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
   __syncthreads();
   fft_pass<true>(sbuf, lay, a.fft, tw, ColSrc{a.data, a.g, 0, col0},
                  CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);

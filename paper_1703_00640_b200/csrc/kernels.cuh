@@ -33,7 +33,7 @@ struct SmallArgs {
 };
 
 size_t small_smem_bytes(int64_t L, int64_t nlimbs);
-size_t mid_smem_bytes(uint32_t C);
+size_t mid_smem_bytes(uint32_t C, uint32_t inv_stablen);
 size_t col_smem_bytes(uint32_t R, uint32_t c);
 
 __global__ void k_small_product(SmallArgs a);

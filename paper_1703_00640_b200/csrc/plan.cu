@@ -156,7 +156,34 @@ TwGlobal TwiddleCache::global(uint64_t L) {
   return g;
 }
 
-SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride) {
+const double2* TwiddleCache::stage_table(uint32_t R) {
+  auto it = stages_.find(R);
+  if (it != stages_.end()) return it->second->as<double2>();
+  auto rad = radix_schedule(R);
+  std::vector<double2> h;
+  uint32_t Ns = 1;
+  for (size_t s = 0; s < rad.size(); ++s) {
+    const uint32_t r = uint32_t(rad[s]);
+    if (s > 0) {
+      for (uint32_t q = 1; q < r; ++q)
+        for (uint32_t j = 0; j < Ns; ++j) {
+          double re, im;
+          twiddle(uint64_t(j) * q, uint64_t(Ns) * r, &re, &im);
+          h.push_back(make_double2(re, im));
+        }
+    }
+    Ns *= r;
+  }
+  if (h.empty()) h.push_back(make_double2(1.0, 0.0));
+  auto buf = std::make_unique<DevBuf>();
+  buf->ensure(h.size() * sizeof(double2));
+  TMG_CUDA(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  const double2* p = buf->as<double2>();
+  stages_[R] = std::move(buf);
+  return p;
+}
+
+SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride, TwiddleCache* cache) {
   SubFft s;
   std::memset(&s, 0, sizeof(s));
   s.R = R;
@@ -164,15 +191,41 @@ SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride) {
   s.twlen = R * tw_stride;
   auto rad = radix_schedule(R);
   s.nst = int32_t(rad.size());
-  uint32_t Ns = 1;
+  uint32_t Ns = 1, off = 0;
   for (size_t i = 0; i < rad.size(); ++i) {
     s.rad[i] = rad[i];
     s.Ns[i] = Ns;
     s.twstep[i] = R / (Ns * uint32_t(rad[i])) * tw_stride;
     s.fdNs[i] = make_fastdiv(Ns);
+    s.toff[i] = off;
+    s.qmul[i] = 1;
+    if (i > 0) off += Ns * (uint32_t(rad[i]) - 1);
     Ns *= uint32_t(rad[i]);
   }
+  s.stablen = off > 0 ? off : 1;
+  s.stab = cache ? cache->stage_table(R) : nullptr;
   return s;
+}
+
+// Inverse sub-transform whose stage twiddles are read from the forward
+// table of another length (same Ns per stage, radix dividing the forward
+// radix); returns false when the schedules do not line up.
+bool map_stages(SubFft& inv, const SubFft& fwd) {
+  for (int i = 1; i < inv.nst; ++i) {
+    bool found = false;
+    for (int f = 1; f < fwd.nst; ++f) {
+      if (fwd.Ns[f] == inv.Ns[i] && fwd.rad[f] % inv.rad[i] == 0) {
+        inv.toff[i] = fwd.toff[f];
+        inv.qmul[i] = uint32_t(fwd.rad[f] / inv.rad[i]);
+        found = true;
+        break;
+      }
+    }
+    if (!found) return false;
+  }
+  inv.stab = fwd.stab;
+  inv.stablen = fwd.stablen;
+  return true;
 }
 
 MapConsts make_map_consts(const Params& p) {
@@ -306,8 +359,8 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   if (L <= kSmallMaxL) {
     pl->kind = 1;
     const double2* t = tw.table(uint32_t(L));
-    pl->fwd = make_subfft(uint32_t(L), t, 1);
-    pl->inv = make_subfft(uint32_t(L / 2), t, 2);
+    pl->fwd = make_subfft(uint32_t(L), t, 1, nullptr);
+    pl->inv = make_subfft(uint32_t(L / 2), t, 2, nullptr);
     pl->small_threads = threads_for(uint64_t(L));
     pl->small_smem = small_smem_bytes(L, pl->nlimbs);
     pl->kernels = 1;
@@ -347,10 +400,11 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   pl->twL = tw.global(UL);
   const double2* tA = tw.table(A);
   const double2* tC = tw.table(C);
-  pl->fA = make_subfft(A, tA, 1);
+  pl->fA = make_subfft(A, tA, 1, &tw);
   pl->iA = pl->fA;
-  pl->fC = make_subfft(C, tC, 1);
-  pl->iC = make_subfft(C / 2, tC, 2);
+  pl->fC = make_subfft(C, tC, 1, &tw);
+  pl->iC = make_subfft(C / 2, tC, 2, &tw);
+  pl->mid_shared_table = map_stages(pl->iC, pl->fC);
   pl->logc_f1 = pick_logc(A, UL / A, cap);
   pl->thr_f1 = threads_for(uint64_t(A) << pl->logc_f1);
   pl->smem_f1 = f1_smem_bytes(A, 1u << pl->logc_f1);
@@ -359,7 +413,7 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   pl->smem_il = col_smem_bytes(A, 1u << pl->logc_il);
   if (pl->kind == 3) {
     const double2* tB = tw.table(B);
-    pl->fB = make_subfft(B, tB, 1);
+    pl->fB = make_subfft(B, tB, 1, &tw);
     pl->iB = pl->fB;
     pl->logc_f2 = pick_logc(B, C, cap);
     pl->thr_f2 = threads_for(uint64_t(B) << pl->logc_f2);
@@ -369,7 +423,7 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
     pl->smem_i2 = col_smem_bytes(B, 1u << pl->logc_i2);
   }
   pl->thr_mid = threads_for(uint64_t(2) * C);
-  pl->smem_mid = mid_smem_bytes(C);
+  pl->smem_mid = mid_smem_bytes(C, pl->mid_shared_table ? 0u : pl->iC.stablen);
   const int64_t LB = kCarryThreads * kCarryPerThread;
   pl->smem_carry = carry_smem(b);
   (void)LB;

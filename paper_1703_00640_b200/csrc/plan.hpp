@@ -30,13 +30,15 @@ class TwiddleCache {
  public:
   const double2* table(uint32_t R);               // omega_R^x, x < R
   TwGlobal global(uint64_t L);                    // two-level omega_L
+  const double2* stage_table(uint32_t R);         // per-stage q-major table
  private:
+  std::map<uint64_t, std::unique_ptr<DevBuf>> stages_;
   std::map<uint64_t, std::unique_ptr<DevBuf>> tables_;
   std::map<uint64_t, std::unique_ptr<DevBuf>> glob_;
   std::map<uint64_t, uint32_t> glob_S_;
 };
 
-SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride = 1);
+SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride, TwiddleCache* cache);
 MapConsts make_map_consts(const Params& p);
 
 struct Plan {
@@ -64,6 +66,7 @@ struct Plan {
          smem_carry = 0;
   int thr_f1 = 0, thr_f2 = 0, thr_i2 = 0, thr_il = 0, thr_mid = 0;
   size_t smem_zgen = 0;
+  bool mid_shared_table = false;
   int kernels = 0;
 };
 
