@@ -25,6 +25,7 @@ struct MapConsts {
   int32_t b;
   int64_t N;         // chunk count of the transform (low/high) or N (full)
   int32_t lambda;
+  int32_t balanced;          // signed (balanced) split, products.hpp:43-44
   double cpre[kMaxLambda];   // pre-map (alpha or gamma) row scale
   double cpost[kMaxLambda];  // post-map (beta or delta) row scale
   double step;               // 2^-b

@@ -69,12 +69,14 @@ __device__ __forceinline__ int cbit(const uint32_t* cb, int64_t j) {
   return int((__ldg(cb + (j >> 5)) >> (j & 31)) & 1u);
 }
 
+// Single digit re-derived from the limbs and its carry-in bit (the carry
+// bits are all zero for the unbalanced split).
 __device__ __forceinline__ double digit_at(const uint64_t* limbs,
                                            int64_t nlimbs, int b, int64_t lead,
                                            int64_t count, const uint32_t* cb,
-                                           int64_t j) {
+                                           int64_t j, bool balanced = true) {
   uint64_t w = window_bits(limbs, nlimbs, j * b - lead, b);
-  return double(split_digit(w, cbit(cb, j), b, j == count - 1));
+  return double(split_digit(w, cbit(cb, j), b, j == count - 1 || !balanced));
 }
 
 __device__ __forceinline__ uint32_t take_ticket(unsigned long long* ctr) {
@@ -194,12 +196,12 @@ k_f1(F1Args a) {
   const TwStage tw = load_tw_stage(sbuf + padded_len(A * c), a.fft, tid, nthr);
   double topu = 0.0, topv = 0.0;
   if (mc.mode == kModeHigh && col0 < uint32_t(mc.nfold + mc.lambda)) {
-    topu = digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, N);
-    topv = digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, N);
+    topu = digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, N, mc.balanced != 0);
+    topv = digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, N, mc.balanced != 0);
   }
   if (mc.mode == kModeHigh && blockIdx.x == 0 && tid == 0) {
-    auto Du = [&](int64_t i) { return digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, i); };
-    auto Dv = [&](int64_t i) { return digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, i); };
+    auto Du = [&](int64_t i) { return digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, i, mc.balanced != 0); };
+    auto Dv = [&](int64_t i) { return digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, i, mc.balanced != 0); };
     a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
   }
   __syncthreads();

@@ -72,8 +72,8 @@ k_small_product(SmallArgs a) {
   for (int64_t j = c0; j < c1 && j < count - 1; ++j) {
     uint64_t wu = window_smem(ul, a.nlimbs, j * b - a.lead, b);
     uint64_t wv = window_smem(vl, a.nlimbs, j * b - a.lead, b);
-    fu = tf_compose(fu, split_tf(wu, b));
-    fv = tf_compose(fv, split_tf(wv, b));
+    fu = tf_compose(fu, mc.balanced ? split_tf(wu, b) : tf_const(0));
+    fv = tf_compose(fv, mc.balanced ? split_tf(wv, b) : tf_const(0));
   }
   uint32_t aggu, aggv;
   uint32_t exu = block_scan_tf(fu, sw, &aggu);
@@ -84,10 +84,10 @@ k_small_product(SmallArgs a) {
       uint64_t wu = window_smem(ul, a.nlimbs, j * b - a.lead, b);
       uint64_t wv = window_smem(vl, a.nlimbs, j * b - a.lead, b);
       bool top = (j == count - 1);
-      double du = double(split_digit(wu, cu, b, top));
-      double dv = double(split_digit(wv, cv, b, top));
-      cu = tf_apply(split_tf(wu, b), cu);
-      cv = tf_apply(split_tf(wv, b), cv);
+      double du = double(split_digit(wu, cu, b, top || !mc.balanced));
+      double dv = double(split_digit(wv, cv, b, top || !mc.balanced));
+      cu = mc.balanced ? tf_apply(split_tf(wu, b), cu) : 0;
+      cv = mc.balanced ? tf_apply(split_tf(wv, b), cv) : 0;
       if (j < L) buf[padidx(uint32_t(j))] = make_double2(du, dv);
       if (mc.mode == kModeHigh && top) {
         sd[0] = du;

@@ -81,10 +81,10 @@ k_zgen(ZgenArgs a) {
     for (int i = 0; i < ext; ++i) {
       const uint64_t wu = window_bits(a.u, a.nlimbs, int64_t(i) * b - a.lead, b);
       const uint64_t wv = window_bits(a.v, a.nlimbs, int64_t(i) * b - a.lead, b);
-      s_wrap[0][i] = int32_t(split_digit(wu, cu, b, i == count - 1));
-      s_wrap[1][i] = int32_t(split_digit(wv, cv, b, i == count - 1));
-      cu = tf_apply(split_tf(wu, b), cu);
-      cv = tf_apply(split_tf(wv, b), cv);
+      s_wrap[0][i] = int32_t(split_digit(wu, cu, b, i == count - 1 || !mc.balanced));
+      s_wrap[1][i] = int32_t(split_digit(wv, cv, b, i == count - 1 || !mc.balanced));
+      cu = mc.balanced ? tf_apply(split_tf(wu, b), cu) : 0;
+      cv = mc.balanced ? tf_apply(split_tf(wv, b), cv) : 0;
     }
   }
   __syncthreads();
@@ -97,7 +97,7 @@ k_zgen(ZgenArgs a) {
 #pragma unroll
   for (int q = 0; q < kZgenPer; ++q) {
     const int64_t j = t0 + q;
-    if (j < c1 && j < count - 1) {
+    if (j < c1 && j < count - 1 && mc.balanced) {
       const uint64_t wu = window_at(Lu, j * b - a.lead, b);
       const uint64_t wv = window_at(Lv, j * b - a.lead, b);
       gu |= uint32_t(wu > half) << q;
@@ -132,8 +132,8 @@ k_zgen(ZgenArgs a) {
       bv |= uint32_t(cv) << q;
       const uint64_t wu = window_at(Lu, j * b - a.lead, b);
       const uint64_t wv = window_at(Lv, j * b - a.lead, b);
-      digu[j - c0] = int32_t(split_digit(wu, cu, b, j == count - 1));
-      digv[j - c0] = int32_t(split_digit(wv, cv, b, j == count - 1));
+      digu[j - c0] = int32_t(split_digit(wu, cu, b, j == count - 1 || !mc.balanced));
+      digv[j - c0] = int32_t(split_digit(wv, cv, b, j == count - 1 || !mc.balanced));
       if (!((pu >> q) & 1u)) cu = int((gu >> q) & 1u);
       if (!((pv >> q) & 1u)) cv = int((gv >> q) & 1u);
     }
@@ -145,10 +145,10 @@ k_zgen(ZgenArgs a) {
       if (j >= N) break;
       const uint64_t wu = window_at(Lu, j * b - a.lead, b);
       const uint64_t wv = window_at(Lv, j * b - a.lead, b);
-      digu[j - c0] = int32_t(split_digit(wu, cu, b, j == count - 1));
-      digv[j - c0] = int32_t(split_digit(wv, cv, b, j == count - 1));
-      cu = tf_apply(split_tf(wu, b), cu);
-      cv = tf_apply(split_tf(wv, b), cv);
+      digu[j - c0] = int32_t(split_digit(wu, cu, b, j == count - 1 || !mc.balanced));
+      digv[j - c0] = int32_t(split_digit(wv, cv, b, j == count - 1 || !mc.balanced));
+      cu = mc.balanced ? tf_apply(split_tf(wu, b), cu) : 0;
+      cv = mc.balanced ? tf_apply(split_tf(wv, b), cv) : 0;
     }
   }
   {

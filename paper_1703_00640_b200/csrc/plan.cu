@@ -235,6 +235,7 @@ MapConsts make_map_consts(const Params& p) {
   m.b = p.b;
   m.N = p.N;
   m.lambda = int32_t(p.lambda);
+  m.balanced = p.signed_split ? 1 : 0;
   m.step = std::ldexp(1.0, -p.b);
   m.scale_out = (p.mode == PMode::kFull) ? 1.0 : std::ldexp(1.0, p.b);
   m.cofactor_scaled = 1.0;
@@ -328,8 +329,6 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   }
   if (p.backend != Backend::kFft)
     throw Error(TMG_ERR_UNSUPPORTED, "GPU products run the FFT backend only");
-  if (!p.signed_split)
-    throw Error(TMG_ERR_UNSUPPORTED, "GPU products use the balanced (signed) split");
   if (p.b > 48) throw Error(TMG_ERR_UNSUPPORTED, "chunk width above 48 bits");
   const int64_t N = p.N;
   const int64_t L = transform_length(p.mode, N);

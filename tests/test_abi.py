@@ -1,0 +1,68 @@
+"""The C-ABI library (include/truncmul_b200.h) loads, exports every declared
+symbol, and the host-side mirror behaves like the reference's API on the
+parts that need no GPU."""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1703_00640_b200 as tm
+from paper_1703_00640_b200 import _native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    L = _native.load()
+    names = _native.header_functions()
+    assert len(names) >= 25
+    for name in names:
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True, text=True).stdout
+    for name in names:
+        assert f" T {name}" in out, name
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_last_error():
+    L = _native.load()
+    assert b"sm_100a" in L.tmg_version()
+    with pytest.raises(tm.InputOutOfRange):
+        tm.required_precision(tm.Mode.LOW, 0, 10)
+    assert "chunk width" in _native.last_error()
+
+
+def test_no_cpu_fallback_without_device():
+    """On a machine without a usable GPU the product path must fail loudly."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(tm.CudaError):
+        tm.Context(0)
+
+
+def test_limbs_round_trip_and_range():
+    rng = np.random.default_rng(0)
+    for n in (1, 63, 64, 65, 1000):
+        x = int.from_bytes(rng.bytes((n + 7) // 8), "little") & ((1 << n) - 1)
+        a = tm.to_limbs(x, n)
+        assert len(a) == (n + 63) // 64
+        assert tm.from_limbs(a) == x
+        with pytest.raises(tm.InputOutOfRange):
+            tm.to_limbs(1 << n, n)
+    with pytest.raises(tm.InputOutOfRange):
+        tm.to_limbs(-1, 10)
+    with pytest.raises(tm.InputOutOfRange):
+        tm.to_limbs(np.array([0, 1], dtype=np.uint64), 64)
+    assert len(tm.to_limbs(np.array([5], dtype=np.uint64), 200)) == 4
+
+
+def test_params_c_round_trip():
+    p = tm.select_params(1 << 20, tm.Mode.HIGH)
+    assert tm.Params.from_c(p.to_c()) == p

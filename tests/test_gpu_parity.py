@@ -1,0 +1,319 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Full and low products must be bit-exact with the exact product (GMP, the
+reference's own bignum dependency, cross-checked against Python ints and the
+oracle's Karatsuba in test_oracle.py).  High products must satisfy
+|uv - 2^n w| < 2^n with 0 <= w <= 2^n (the reference's admissible set), and
+are compared with the oracle port's value.  Inputs where the float pipeline
+cannot certify the rounding must raise ConvolutionPrecisionFailure, like the
+reference (products_f64.cpp:16-27).
+
+Covers BASELINE.json configs 1-5 plus the reference tests' edge cases.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1703_00640_b200 as tm
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TRIP = 0.25  # reference tripwire (products_f64.cpp:22)
+
+
+def _check(mode, u, v, n, r):
+    P = port.limbs_to_int(port.oracle_full(u, v))
+    if mode == tm.Mode.FULL:
+        assert r == P
+    elif mode == tm.Mode.LOW:
+        assert r == P & ((1 << n) - 1)
+    else:
+        assert 0 <= r <= (1 << n)
+        assert abs(P - (r << n)) < (1 << n)
+
+
+def _rand(rng, n):
+    nl = (n + 63) // 64
+    a = rng.integers(0, 2**64, nl, dtype=np.uint64)
+    if n % 64:
+        a[-1] &= np.uint64((1 << (n % 64)) - 1)
+    return a
+
+
+@pytest.mark.parametrize("n", [4096, 5001, 8192, 20011, 65536, 100003, 262144, 1000000, 1 << 22])
+def test_random_products_match_exact(ctx, n):
+    rng = np.random.default_rng(n)
+    for _ in range(3):
+        u, v = _rand(rng, n), _rand(rng, n)
+        for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+            p = tm.select_params(n, mode)
+            r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
+            _check(mode, u, v, n, r)
+            assert ctx.last_stats.max_round_err <= TRIP
+
+
+def test_golden_vectors(ctx):
+    """Committed known answers (tools/make_golden.py): exact, or the same
+    precision failure the reference raises for boundary-digit operands."""
+    gold = json.load(open(os.path.join(GOLD, "products.json")))
+    exact = failed = 0
+    for e in gold["vectors"]:
+        n = e["n"]
+        nl = (n + 63) // 64
+        u = port.int_to_limbs(int(e["u"], 16), nl)
+        v = port.int_to_limbs(int(e["v"], 16), nl)
+        for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+            p = tm.select_params(n, mode)
+            try:
+                r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
+            except tm.ConvolutionPrecisionFailure:
+                assert not e["tag"].startswith("uniform"), e["tag"]
+                failed += 1
+                continue
+            if mode == tm.Mode.FULL:
+                assert format(r, "x") == e["full"], (e["tag"], n)
+            elif mode == tm.Mode.LOW:
+                assert format(r, "x") == e["low"], (e["tag"], n)
+            else:
+                assert format(r, "x") in e["high_set"], (e["tag"], n)
+            exact += 1
+    assert exact > 300
+
+
+def test_reference_cli_examples(ctx):
+    gold = json.load(open(os.path.join(GOLD, "products.json")))
+    mode = {"mul": tm.Mode.FULL, "mullo": tm.Mode.LOW, "mulhi": tm.Mode.HIGH}
+    for c in gold["cli"]:
+        r = tm.multiply(mode[c["cmd"]], int(c["u"], 16), int(c["v"], 16), n=c["n"], ctx=ctx)
+        assert format(r, "x") in c["expect"], c
+
+
+def test_gpu_agrees_with_port_on_tripwire(ctx):
+    """Where the oracle port certifies with a margin, the GPU must too; where
+    the port trips far above the wire, the GPU must trip as well."""
+    gold = json.load(open(os.path.join(GOLD, "products.json")))
+    for e in gold["vectors"]:
+        n = e["n"]
+        if n < 4096:
+            continue
+        nl = (n + 63) // 64
+        u = port.int_to_limbs(int(e["u"], 16), nl)
+        v = port.int_to_limbs(int(e["v"], 16), nl)
+        for mode in (tm.Mode.FULL, tm.Mode.LOW):
+            p = tm.select_params(n, mode)
+            try:
+                pe = port.product(mode.name.lower(), u, v, n, p.b, p.N, p.lam).max_err
+            except port.ConvolutionPrecisionFailure:
+                pe = None
+            try:
+                ctx.product_limbs(mode, u, v, p)
+                ge = ctx.last_stats.max_round_err
+            except tm.ConvolutionPrecisionFailure:
+                ge = None
+            if pe is not None and pe < 0.18:
+                assert ge is not None, (e["tag"], n, mode, pe)
+
+
+def test_commutativity_and_consistency(ctx):
+    rng = np.random.default_rng(11)
+    n = 200000
+    u, v = _rand(rng, n), _rand(rng, n)
+    pl, pf, ph = (tm.select_params(n, m) for m in (tm.Mode.LOW, tm.Mode.FULL, tm.Mode.HIGH))
+    lo = tm.from_limbs(ctx.product_limbs(tm.Mode.LOW, u, v, pl))
+    assert lo == tm.from_limbs(ctx.product_limbs(tm.Mode.LOW, v, u, pl))
+    fu = tm.from_limbs(ctx.product_limbs(tm.Mode.FULL, u, v, pf))
+    assert fu == tm.from_limbs(ctx.product_limbs(tm.Mode.FULL, v, u, pf))
+    assert lo == fu & ((1 << n) - 1)
+    hi = tm.from_limbs(ctx.product_limbs(tm.Mode.HIGH, u, v, ph))
+    assert hi in ((fu >> n), (fu >> n) + 1)
+    # deterministic
+    assert hi == tm.from_limbs(ctx.product_limbs(tm.Mode.HIGH, u, v, ph))
+
+
+@pytest.mark.parametrize("n", [5001, 300007])
+def test_structured_operands(ctx, n):
+    nl = (n + 63) // 64
+    vals = [0, 1, 2, 3, 1 << (n // 2), 1 << (n - 1), (1 << (n - 1)) + 1, (1 << (n - 1)) - 1,
+            (1 << n) - 1, (1 << n) - 2]
+    for a in vals:
+        for b_ in (vals[0], vals[1], vals[-2], a):
+            u, v = port.int_to_limbs(a, nl), port.int_to_limbs(b_, nl)
+            for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+                r = tm.from_limbs(ctx.product_limbs(mode, u, v, tm.select_params(n, mode)))
+                _check(mode, u, v, n, r)
+
+
+def test_unsigned_wide_chunks_trip(ctx):
+    """test_products.cpp:408-416: b = 30 unsigned chunks overflow the exact
+    integer range and must be refused."""
+    p = tm.manual_params(3840, 30, 128, tm.Mode.LOW, tm.Backend.FFT, signed_split=False, lam=4)
+    top = (1 << 3840) - 1
+    with pytest.raises(tm.ConvolutionPrecisionFailure):
+        tm.low_product(top, top, p, ctx)
+
+
+def test_unsigned_split_products(ctx):
+    n = 20000
+    rng = np.random.default_rng(5)
+    u, v = _rand(rng, n), _rand(rng, n)
+    for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+        ref = tm.select_params(n, mode)
+        b = ref.b - 4
+        cover = -(-n // b)
+        N = next(x for x in range(cover + (4 if mode == tm.Mode.HIGH else 0), 4 * cover)
+                 if all(q in (2, 3, 5, 7) for q in _factors(x)) and x % 4 == 0)
+        p = tm.manual_params(n, b, N, mode, tm.Backend.FFT, signed_split=False)
+        r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
+        _check(mode, u, v, n, r)
+
+
+def _factors(x):
+    out = []
+    for q in (2, 3, 5, 7):
+        while x % q == 0:
+            out.append(q)
+            x //= q
+    if x > 1:
+        out.append(x)
+    return out
+
+
+def test_input_out_of_range(ctx):
+    p = tm.select_params(8192, tm.Mode.LOW)
+    with pytest.raises(tm.InputOutOfRange):
+        tm.low_product(1 << 8192, 3, p, ctx)
+    with pytest.raises(tm.InputOutOfRange):
+        tm.full_product(3, 5, p, ctx)  # params built for a different mode
+
+
+def test_fallback_below_cutoff(ctx):
+    rng = np.random.default_rng(6)
+    for n in (1, 7, 64, 65, 1000, 4095):
+        u, v = _rand(rng, n), _rand(rng, n)
+        for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+            p = tm.select_params(n, mode)
+            assert p.mode == tm.Mode.ORACLE_FALLBACK
+            r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
+            P = port.limbs_to_int(u) * port.limbs_to_int(v)
+            if mode == tm.Mode.FULL:
+                assert r == P
+            elif mode == tm.Mode.LOW:
+                assert r == P & ((1 << n) - 1)
+            else:
+                assert r == P >> n  # oracle_high_set(...).front()
+
+
+def test_device_path_matches_host_path(ctx):
+    import torch
+    n = 1 << 20
+    rng = np.random.default_rng(9)
+    u, v = _rand(rng, n), _rand(rng, n)
+    p = tm.select_params(n, tm.Mode.LOW)
+    host = ctx.product_limbs(tm.Mode.LOW, u, v, p)
+    du = torch.from_numpy(u.view(np.int64)).cuda()
+    dv = torch.from_numpy(v.view(np.int64)).cuda()
+    out = torch.zeros(len(host), dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    ctx.product_device(p, du.data_ptr(), dv.data_ptr(), out.data_ptr(), 1)
+    ctx.check()
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), host)
+
+
+# --------------------------------------------------------------------------
+# BASELINE.json configurations
+
+
+def test_config1_low_2p20_seed1(ctx):
+    n = 1 << 20
+    u, v = port.config_operands(1, n // 64)
+    p = tm.select_params(n, tm.Mode.LOW)
+    r = ctx.product_limbs(tm.Mode.LOW, u, v, p)
+    assert np.array_equal(r, port.oracle_low(u, v, n))
+    assert ctx.last_stats.max_round_err < TRIP
+
+
+def test_config2_high_2p24_seed2(ctx):
+    n = 1 << 24
+    u, v = port.config_operands(2, n // 64, force_top_bit=True)
+    p = tm.select_params(n, tm.Mode.HIGH)
+    w = tm.from_limbs(ctx.product_limbs(tm.Mode.HIGH, u, v, p))
+    assert port.is_valid_high(u, v, n, w)
+    assert ctx.last_stats.max_round_err < TRIP
+    # the oracle port at the same parameters lands on the same value unless
+    # t / 2^s sits within rounding noise of a half-integer
+    pw = port.high_product(u, v, n, p.b, p.N, p.lam).value
+    assert pw in port.oracle_high_set(u, v, n)
+    assert w == pw
+
+
+def test_config3_full_low_high_2p26_seed3(ctx):
+    n = 1 << 26
+    u, v = port.config_operands(3, n // 64)
+    P = port.limbs_to_int(port.oracle_full(u, v))
+    for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+        p = tm.select_params(n, mode)
+        r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
+        if mode == tm.Mode.FULL:
+            assert r == P
+        elif mode == tm.Mode.LOW:
+            assert r == P & ((1 << n) - 1)
+        else:
+            assert abs(P - (r << n)) < (1 << n) and 0 <= r <= (1 << n)
+        assert ctx.last_stats.max_round_err < TRIP
+
+
+def test_config3_reference_params_trip_like_the_reference(ctx):
+    """At the reference's own b = 13 for n = 2^26 the FP64 error passes its
+    0.25 tripwire; the GPU either refuses like the reference or,
+    if it certifies, is exact."""
+    n = 1 << 26
+    u, v = port.config_operands(3, n // 64)
+    p = tm.select_params(n, tm.Mode.LOW, policy=tm.Policy.REFERENCE)
+    assert p.b == 13
+    try:
+        r = ctx.product_limbs(tm.Mode.LOW, u, v, p)
+    except tm.ConvolutionPrecisionFailure:
+        return
+    assert np.array_equal(r, port.oracle_low(u, v, n))
+
+
+def test_config4_batched_low_2p16_seed4(ctx):
+    n, count = 1 << 16, 4096
+    nl = n // 64
+    w = port.mt19937_64(4, 2 * count * nl).reshape(count, 2, nl)
+    u = np.ascontiguousarray(w[:, 0, :])
+    v = np.ascontiguousarray(w[:, 1, :])
+    p = tm.select_params(n, tm.Mode.LOW)
+    out, flags = ctx.product_batched(p, u, v, return_flags=True)
+    assert not flags.any()
+    for i in range(count):
+        assert np.array_equal(out[i], port.oracle_low(u[i], v[i], n)), i
+    assert ctx.last_stats.max_round_err < TRIP
+
+
+@pytest.mark.parametrize("pattern", ["ones", "alternating"])
+@pytest.mark.parametrize("mode", [tm.Mode.LOW, tm.Mode.HIGH])
+def test_config5_stress_2p28(ctx, pattern, mode):
+    n = 1 << 28
+    nl = n // 64
+    if pattern == "ones":
+        u = np.full(nl, np.uint64(0xFFFFFFFFFFFFFFFF))
+    else:
+        u = np.zeros(nl, dtype=np.uint64)
+        u[0::2] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    v = u.copy()
+    p = tm.select_params(n, mode)
+    try:
+        r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
+    except tm.ConvolutionPrecisionFailure:
+        # must agree with the reference pipeline (oracle port) refusing too
+        with pytest.raises(port.ConvolutionPrecisionFailure):
+            port.product(mode.name.lower(), u, v, n, p.b, p.N, p.lam)
+        return
+    err = ctx.last_stats.max_round_err
+    print(f"stress {pattern} {mode.name}: max pre-rounding error {err:.4f}")
+    assert err < TRIP
+    _check(mode, u, v, n, r)
