@@ -3,6 +3,7 @@
 #include "plan.hpp"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/truncmul_b200.h"
@@ -376,7 +377,9 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   if (C == 0) throw Error(TMG_ERR_UNSUPPORTED, "no row length divides L");
   const uint64_t AB = UL / C;
   uint32_t A = 0, B = 1;
-  if (AB <= 2048) {
+  // TMG_FORCE_3PASS (testing): split even short column lengths into A x B
+  static const bool force3 = getenv("TMG_FORCE_3PASS") != nullptr;
+  if (AB <= 2048 && !(force3 && AB >= 64)) {
     A = uint32_t(AB);
     pl->kind = 2;
   } else {

@@ -263,9 +263,10 @@ class Context:
         c = params.to_c()
         st = tmg_stats()
         P64 = ctypes.POINTER(ctypes.c_uint64)
-        _check(fn(self._h, ctypes.byref(c), ul.ctypes.data_as(P64), vl.ctypes.data_as(P64),
-                  out.ctypes.data_as(P64), ctypes.byref(st)))
-        self._stats(st)
+        rc = fn(self._h, ctypes.byref(c), ul.ctypes.data_as(P64), vl.ctypes.data_as(P64),
+                out.ctypes.data_as(P64), ctypes.byref(st))
+        self._stats(st)  # filled before a precision failure is reported too
+        _check(rc)
         return out
 
     def product_batched(self, params: Params, u: np.ndarray, v: np.ndarray,
