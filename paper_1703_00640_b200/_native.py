@@ -104,6 +104,7 @@ def load():
     L.tmg_profile_enable.argtypes = [vp, ctypes.c_int]
     L.tmg_profile_read.argtypes = [vp, ctypes.c_char_p, ctypes.c_int, P(ctypes.c_double),
                                    P(ctypes.c_double), ctypes.c_int, P(ctypes.c_int)]
+    L.tmg_debug_read.argtypes = [vp, ctypes.c_int, vp, P(ctypes.c_size_t)]
     _lib = L
     return L
 

@@ -24,8 +24,10 @@ namespace tmg {
 #define TMG_CUDA(call)                                                     \
   do {                                                                     \
     cudaError_t e_ = (call);                                               \
-    if (e_ != cudaSuccess)                                                 \
+    if (e_ != cudaSuccess) {                                               \
+      (void)cudaGetLastError(); /* clear a non-sticky error */             \
       throw Error(TMG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    }                                                                      \
   } while (0)
 
 thread_local std::string g_last_error;
@@ -738,6 +740,18 @@ int tmg_memcpy_d2h(tmg_context* ctx, void* dst, const void* src, size_t bytes) {
   });
 }
 int32_t tmg_last_kernel_count(tmg_context* ctx) { return ctx->cx.last_kernels; }
+
+int tmg_debug_read(tmg_context* ctx, int which, void* host, size_t* bytes) {
+  return guarded([&] {
+    Context& cx = ctx->cx;
+    const DevBuf& B = (which == 0) ? cx.work_z : cx.work_c;
+    if (which != 0 && which != 1) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "debug_read: which");
+    *bytes = std::min(*bytes, B.bytes);
+    TMG_CUDA(cudaMemcpyAsync(host, B.p, *bytes, cudaMemcpyDeviceToHost, cx.stream));
+    TMG_CUDA(cudaStreamSynchronize(cx.stream));
+    return TMG_OK;
+  });
+}
 
 int tmg_profile_enable(tmg_context* ctx, int on) {
   return guarded([&] {

@@ -33,6 +33,8 @@ struct SmallArgs {
 };
 
 size_t small_smem_bytes(int64_t L, int64_t nlimbs);
+// opt-in dynamic shared memory per CTA on sm_100 (227 KB)
+constexpr size_t kMaxDynSmem = 232448;
 size_t mid_smem_bytes(uint32_t C, uint32_t inv_stablen);
 size_t col_smem_bytes(uint32_t R, uint32_t c);
 

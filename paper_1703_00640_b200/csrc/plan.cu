@@ -13,8 +13,10 @@ namespace tmg {
 #define TMG_CUDA(call)                                                     \
   do {                                                                     \
     cudaError_t e_ = (call);                                               \
-    if (e_ != cudaSuccess)                                                 \
+    if (e_ != cudaSuccess) {                                               \
+      (void)cudaGetLastError(); /* clear a non-sticky error */             \
       throw Error(TMG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    }                                                                      \
   } while (0)
 
 DevBuf::~DevBuf() {
@@ -212,20 +214,24 @@ SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride, TwiddleCac
 // table of another length (same Ns per stage, radix dividing the forward
 // radix); returns false when the schedules do not line up.
 bool map_stages(SubFft& inv, const SubFft& fwd) {
-  for (int i = 1; i < inv.nst; ++i) {
+  // all-or-nothing: a partial mapping would leave stages indexing the
+  // forward table's offsets inside the inverse's own table
+  SubFft m = inv;
+  for (int i = 1; i < m.nst; ++i) {
     bool found = false;
     for (int f = 1; f < fwd.nst; ++f) {
-      if (fwd.Ns[f] == inv.Ns[i] && fwd.rad[f] % inv.rad[i] == 0) {
-        inv.toff[i] = fwd.toff[f];
-        inv.qmul[i] = uint32_t(fwd.rad[f] / inv.rad[i]);
+      if (fwd.Ns[f] == m.Ns[i] && fwd.rad[f] % m.rad[i] == 0) {
+        m.toff[i] = fwd.toff[f];
+        m.qmul[i] = uint32_t(fwd.rad[f] / m.rad[i]);
         found = true;
         break;
       }
     }
     if (!found) return false;
   }
-  inv.stab = fwd.stab;
-  inv.stablen = fwd.stablen;
+  m.stab = fwd.stab;
+  m.stablen = fwd.stablen;
+  inv = m;
   return true;
 }
 
@@ -370,9 +376,18 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   // multi-pass: C = row length (even, <= 4096), A (and B) column lengths
   const uint64_t UL = uint64_t(L);
   if (UL >= (uint64_t(1) << 32)) throw Error(TMG_ERR_UNSUPPORTED, "transform length above 2^32");
+  // the largest even row length whose row pass (two rows plus the stage
+  // twiddles, shared between the forward and inverse schedules when they
+  // line up) fits in one CTA's shared memory
   uint32_t C = 0;
   for (uint32_t c = 4096; c >= 16; --c) {
-    if (c % 2 == 0 && UL % c == 0) { C = c; break; }
+    if (c % 2 || UL % c) continue;
+    SubFft f = make_subfft(c, nullptr, 1, nullptr);
+    SubFft i = make_subfft(c / 2, nullptr, 2, nullptr);
+    const bool shared = map_stages(i, f);
+    if (mid_smem_bytes(c, shared ? 0u : i.stablen) > kMaxDynSmem) continue;
+    C = c;
+    break;
   }
   if (C == 0) throw Error(TMG_ERR_UNSUPPORTED, "no row length divides L");
   const uint64_t AB = UL / C;

@@ -317,3 +317,42 @@ def test_config5_stress_2p28(ctx, pattern, mode):
     print(f"stress {pattern} {mode.name}: max pre-rounding error {err:.4f}")
     assert err < TRIP
     _check(mode, u, v, n, r)
+
+
+# --------------------------------------------------------------------------
+# plan shapes: every radix placement of the multi-pass row/column transforms
+
+
+def _plan_shape_lengths(limit):
+    """Smooth lengths whose row length C (largest even divisor <= 4096) and
+    column length A differ in radix structure: radix 4/8 before odd radices,
+    odd C/2 schedules, forward/inverse stage tables that do and do not share."""
+    seen, out = set(), []
+    for N in sorted(2**a * 3**b * 5**c * 7**d for a in range(2, 21) for b in range(4)
+                    for c in range(3) for d in range(3)):
+        if not (8193 <= N <= (1 << 20)):
+            continue
+        C = next(c for c in range(4096, 15, -1) if c % 2 == 0 and N % c == 0)
+        key = (C, min(N // C, 64))
+        if key not in seen:
+            seen.add(key)
+            out.append(N)
+    rng = np.random.default_rng(11)
+    return [int(x) for x in rng.choice(out, size=min(limit, len(out)), replace=False)]
+
+
+@pytest.mark.parametrize("N", _plan_shape_lengths(48))
+def test_plan_shapes_exact(ctx, N):
+    rng = np.random.default_rng(N)
+    for mode, b, Nn in ((tm.Mode.LOW, 12, N), (tm.Mode.FULL, 16, N // 2)):
+        n = Nn * b - 5
+        p = tm.manual_params(n, b, Nn, mode)
+        nl = (n + 63) // 64
+        u = port.int_to_limbs(int.from_bytes(rng.bytes(nl * 8), "little") & ((1 << n) - 1), nl)
+        v = port.int_to_limbs(int.from_bytes(rng.bytes(nl * 8), "little") & ((1 << n) - 1), nl)
+        r = ctx.product_limbs(mode, u, v, p)
+        if mode == tm.Mode.LOW:
+            assert np.array_equal(r, port.oracle_low(u, v, n)), (N, mode)
+        else:
+            assert np.array_equal(r, port.oracle_full(u, v)[:len(r)]), (N, mode)
+        assert ctx.last_stats.max_round_err < TRIP
