@@ -105,6 +105,16 @@ struct Context {
 
 namespace {
 
+// 1 / (4 L) as an unevaluated pair: L = 2^k m with m odd is rarely a power
+// of two, and a single rounded constant would scale every coefficient by the
+// same relative error.
+void spectral_scale(int64_t L, double* hi, double* lo) {
+  const long double v = 1.0L / (4.0L * (long double)L);
+  *hi = double(v);
+  *lo = double(v - (long double)(*hi));
+}
+
+
 bool g_debug_sync = getenv("TMG_DEBUG_SYNC") != nullptr;
 
 void check_launch(const char* what) {
@@ -174,7 +184,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     a.K = pl.K;
     a.ML = pl.ML;
     a.shift_s = pl.shift_s;
-    a.scale = 1.0 / (4.0 * double(pl.L));
+    spectral_scale(pl.L, &a.scale, &a.scale_lo);
     a.fwd = pl.fwd;
     a.inv = pl.inv;
     a.mc = pl.mc;
@@ -288,7 +298,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.inv = pl.iC;
       a.tw = pl.twL;
       a.L = uint32_t(L);
-      a.scale = 1.0 / (4.0 * double(L));
+      spectral_scale(L, &a.scale, &a.scale_lo);
       set_smem(k_mid, pl.smem_mid);
       const unsigned grid = (pl.A * pl.B) / 2 + 1;
       {

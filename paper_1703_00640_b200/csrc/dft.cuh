@@ -33,6 +33,17 @@ __device__ __forceinline__ void dft4(double2& x0, double2& x1, double2& x2,
   x3 = csub(t1, t3);
 }
 
+// Multiplying by an irrational constant: every constant is carried as an
+// unevaluated pair hi + lo (lo = the rounding error of hi, from 70-digit
+// evaluations), so the product rounds once against the exact constant.  The
+// nearest doubles of cos/sin(2 pi j/P) are biased (e.g. 1/sqrt2 rounds up by
+// 0.44 ulp), and a butterfly network that multiplies by them at every stage
+// accumulates a coherent gain error of several 2^-53 -- large enough to
+// matter for structured operands at the reference's chunk widths.
+__device__ __forceinline__ double mul_hl(double x, double hi, double lo) {
+  return fma(x, hi, x * lo);
+}
+
 // Odd prime radix via the symmetric pair formulation:
 //   X_k = x0 + sum_j cos(2pi jk/p) t_j  -/+ i sum_j sin(2pi jk/p) s_j
 // with t_j = x_j + x_{p-j}, s_j = x_j - x_{p-j}.
@@ -40,31 +51,41 @@ template <int P>
 struct OddTrig;
 template <>
 struct OddTrig<3> {
-  __device__ static constexpr double c(int j) { return -0.5; }
-  __device__ static constexpr double s(int j) {
-    return 0.8660254037844386467637232;
-  }
+  __device__ static constexpr double c(int) { return -0.5; }
+  __device__ static constexpr double cl(int) { return 0.0; }
+  __device__ static constexpr double s(int) { return 0.8660254037844386; }
+  __device__ static constexpr double sl(int) { return 5.0175421109034514e-17; }
 };
 template <>
 struct OddTrig<5> {
   __device__ static constexpr double c(int j) {
-    return j == 1 ? 0.3090169943749474241022934 : -0.8090169943749474241022934;
+    return j == 1 ? 0.30901699437494745 : -0.8090169943749475;
+  }
+  __device__ static constexpr double cl(int j) {
+    return j == 1 ? -2.716057601841253e-17 : 2.716057601841253e-17;
   }
   __device__ static constexpr double s(int j) {
-    return j == 1 ? 0.9510565162951535721164393 : 0.587785252292473129168706;
+    return j == 1 ? 0.9510565162951535 : 0.5877852522924731;
+  }
+  __device__ static constexpr double sl(int j) {
+    return j == 1 ? 4.0934500900087295e-17 : -7.93475083819002e-18;
   }
 };
 template <>
 struct OddTrig<7> {
   __device__ static constexpr double c(int j) {
-    return j == 1   ? 0.6234898018587335305250049
-           : j == 2 ? -0.2225209339563144042889026
-                    : -0.9009688679024191262361023;
+    return j == 1 ? 0.6234898018587335 : j == 2 ? -0.2225209339563144 : -0.9009688679024191;
+  }
+  __device__ static constexpr double cl(int j) {
+    return j == 1 ? 4.716099920540896e-17
+                  : j == 2 ? -1.1412494827220627e-17 : 1.9762646853069492e-17;
   }
   __device__ static constexpr double s(int j) {
-    return j == 1   ? 0.7818314824680298087084445
-           : j == 2 ? 0.9749279121818236070181317
-                    : 0.4338837391175581204757683;
+    return j == 1 ? 0.7818314824680298 : j == 2 ? 0.9749279121818236 : 0.4338837391175581;
+  }
+  __device__ static constexpr double sl(int j) {
+    return j == 1 ? 5.074320362582868e-18
+                  : j == 2 ? -1.232383765062425e-17 : 7.407189078946677e-20;
   }
 };
 
@@ -77,35 +98,51 @@ __device__ __forceinline__ void dft_odd(double2* x) {
     t[j - 1] = cadd(x[j], x[P - j]);
     s[j - 1] = csub(x[j], x[P - j]);
   }
-  double2 x0 = x[0];
+  const double2 x0 = x[0];
   double2 sum = x0;
 #pragma unroll
   for (int j = 0; j < H; ++j) sum = cadd(sum, t[j]);
   x[0] = sum;
 #pragma unroll
   for (int k = 1; k <= H; ++k) {
-    double2 a = x0, b = make_double2(0.0, 0.0);
+    // cos/sin(2 pi j k / P) with jk reduced into the first half-turn
+    double cj[H], cjl[H], sj[H], sjl[H];
 #pragma unroll
     for (int j = 1; j <= H; ++j) {
-      // cos/sin(2 pi j k / P): reduce jk mod P into the first half-turn
-      constexpr int dummy = 0;
-      (void)dummy;
-      int m = (j * k) % P;
-      double cj, sj;
-      if (m <= H) {
-        cj = OddTrig<P>::c(m);
-        sj = OddTrig<P>::s(m);
-      } else {
-        cj = OddTrig<P>::c(P - m);
-        sj = -OddTrig<P>::s(P - m);
+      const int m = (j * k) % P;
+      const bool lo = m <= H;
+      const int mm = lo ? m : P - m;
+      cj[j - 1] = OddTrig<P>::c(mm);
+      cjl[j - 1] = OddTrig<P>::cl(mm);
+      sj[j - 1] = lo ? OddTrig<P>::s(mm) : -OddTrig<P>::s(mm);
+      sjl[j - 1] = lo ? OddTrig<P>::sl(mm) : -OddTrig<P>::sl(mm);
+    }
+    double2 a, b;
+    if constexpr (P == 3) {
+      a = make_double2(fma(-0.5, t[0].x, x0.x), fma(-0.5, t[0].y, x0.y));
+      b = make_double2(mul_hl(s[0].x, sj[0], sjl[0]), mul_hl(s[0].y, sj[0], sjl[0]));
+    } else {
+      // the lo parts first (small), then the hi products, then x0
+      a = make_double2(cjl[0] * t[0].x, cjl[0] * t[0].y);
+      b = make_double2(sjl[0] * s[0].x, sjl[0] * s[0].y);
+#pragma unroll
+      for (int j = 1; j < H; ++j) {
+        a.x = fma(cjl[j], t[j].x, a.x);
+        a.y = fma(cjl[j], t[j].y, a.y);
+        b.x = fma(sjl[j], s[j].x, b.x);
+        b.y = fma(sjl[j], s[j].y, b.y);
       }
-      a.x = fma(cj, t[j - 1].x, a.x);
-      a.y = fma(cj, t[j - 1].y, a.y);
-      b.x = fma(sj, s[j - 1].x, b.x);
-      b.y = fma(sj, s[j - 1].y, b.y);
+#pragma unroll
+      for (int j = 0; j < H; ++j) {
+        a.x = fma(cj[j], t[j].x, a.x);
+        a.y = fma(cj[j], t[j].y, a.y);
+        b.x = fma(sj[j], s[j].x, b.x);
+        b.y = fma(sj[j], s[j].y, b.y);
+      }
+      a = cadd(a, x0);
     }
     // forward: X_k = a - i b ; X_{P-k} = a + i b
-    double2 ib = make_double2(-b.y, b.x);
+    const double2 ib = make_double2(-b.y, b.x);
     if (INV) {
       x[k] = cadd(a, ib);
       x[P - k] = csub(a, ib);
@@ -116,20 +153,22 @@ __device__ __forceinline__ void dft_odd(double2* x) {
   }
 }
 
+constexpr double kR2 = 0.7071067811865476, kR2l = -4.833646656726457e-17;  // 1/sqrt2
+constexpr double kC1 = 0.9238795325112867, kC1l = 1.7645047084336677e-17;  // cos pi/8
+constexpr double kS1 = 0.3826834323650898, kS1l = -1.0050772696461588e-17; // sin pi/8
+
 // omega_8^k multipliers (forward: e^{-i pi k/4})
 template <bool INV>
 __device__ __forceinline__ double2 w8_1(double2 a) {
-  constexpr double r = 0.7071067811865475244008444;
   // forward: (1 - i)/sqrt2 * a ; inverse: (1 + i)/sqrt2 * a
-  return INV ? make_double2((a.x - a.y) * r, (a.x + a.y) * r)
-             : make_double2((a.x + a.y) * r, (a.y - a.x) * r);
+  return INV ? make_double2(mul_hl(a.x - a.y, kR2, kR2l), mul_hl(a.x + a.y, kR2, kR2l))
+             : make_double2(mul_hl(a.x + a.y, kR2, kR2l), mul_hl(a.y - a.x, kR2, kR2l));
 }
 template <bool INV>
 __device__ __forceinline__ double2 w8_3(double2 a) {
-  constexpr double r = 0.7071067811865475244008444;
   // forward: (-1 - i)/sqrt2 * a ; inverse: (-1 + i)/sqrt2 * a
-  return INV ? make_double2((-a.x - a.y) * r, (a.x - a.y) * r)
-             : make_double2((a.y - a.x) * r, (-a.x - a.y) * r);
+  return INV ? make_double2(mul_hl(-a.x - a.y, kR2, kR2l), mul_hl(a.x - a.y, kR2, kR2l))
+             : make_double2(mul_hl(a.y - a.x, kR2, kR2l), mul_hl(-a.x - a.y, kR2, kR2l));
 }
 
 template <bool INV>
@@ -152,28 +191,34 @@ __device__ __forceinline__ void dft8(double2* x) {
   x[7] = csub(e3, o3);
 }
 
+// (a.x + i a.y)(c - i s) with c = ch + cl, s = sh + sl
+__device__ __forceinline__ double2 rot_hl(double2 a, double ch, double cl, double sh,
+                                          double sl) {
+  double re = fma(a.x, cl, a.y * sl);
+  re = fma(a.y, sh, re);
+  re = fma(a.x, ch, re);
+  double im = fma(a.y, cl, -a.x * sl);
+  im = fma(-a.x, sh, im);
+  im = fma(a.y, ch, im);
+  return make_double2(re, im);
+}
+
 // omega_16^j * a for j = 0..9 (compile-time j)
 template <bool INV>
 __device__ __forceinline__ double2 w16(double2 a, int j) {
-  constexpr double C1 = 0.9238795325112867561281832;
-  constexpr double S1 = 0.38268343236508977172846;
-  constexpr double R2 = 0.7071067811865475244008444;
-  double c, s;  // e^{-2 pi i j/16} = c - i s (forward)
+  const double sg = INV ? -1.0 : 1.0;  // e^{-+2 pi i j/16} = c -+ i s
   switch (j) {
     case 0: return a;
-    case 1: c = C1; s = S1; break;
-    case 2: c = R2; s = R2; break;
-    case 3: c = S1; s = C1; break;
+    case 1: return rot_hl(a, kC1, kC1l, sg * kS1, sg * kS1l);
+    case 2: return w8_1<INV>(a);
+    case 3: return rot_hl(a, kS1, kS1l, sg * kC1, sg * kC1l);
     case 4: return mul_mi<INV>(a);
-    case 5: c = -S1; s = C1; break;
-    case 6: c = -R2; s = R2; break;
-    case 7: c = -C1; s = S1; break;
+    case 5: return rot_hl(a, -kS1, -kS1l, sg * kC1, sg * kC1l);
+    case 6: return w8_3<INV>(a);
+    case 7: return rot_hl(a, -kC1, -kC1l, sg * kS1, sg * kS1l);
     case 8: return make_double2(-a.x, -a.y);
-    default: c = -C1; s = -S1; break;  // 9
+    default: return rot_hl(a, -kC1, -kC1l, -sg * kS1, -sg * kS1l);  // 9
   }
-  if (INV) s = -s;
-  // (a.x + i a.y)(c - i s) = (a.x c + a.y s) + i (a.y c - a.x s)
-  return make_double2(fma(a.x, c, a.y * s), fma(a.y, c, -a.x * s));
 }
 
 template <bool INV>

@@ -138,4 +138,21 @@ struct RowLoop<0> {
   __device__ __forceinline__ static void run(F&&) {}
 };
 
+// r = R-1 .. 0: the series maps accumulate their small high-order rows
+// first so that only the last term (row 0, the largest) rounds at the
+// magnitude of the result.
+template <int R>
+struct RowLoopDown {
+  template <class F>
+  __device__ __forceinline__ static void run(F&& f) {
+    f(std::integral_constant<int, R - 1>{});
+    RowLoopDown<R - 1>::run(f);
+  }
+};
+template <>
+struct RowLoopDown<0> {
+  template <class F>
+  __device__ __forceinline__ static void run(F&&) {}
+};
+
 }  // namespace tmg

@@ -293,7 +293,8 @@ k_mid(MidArgs a) {
     const double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
     const double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
     const double2 pq = cmul(p, q);
-    const double2 w = make_double2(pq.y * a.scale, -pq.x * a.scale);
+    const double2 w = make_double2(mul_hl(pq.y, a.scale, a.scale_lo),
+                                   -mul_hl(pq.x, a.scale, a.scale_lo));
     sbuf[lay.idx(0, k)] = w;
     if (!(nrows == 1 && kp == k)) sbuf[lay.idx(ip, kp)] = cconj(w);
   }

@@ -140,7 +140,7 @@ k_small_product(SmallArgs a) {
     double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
     double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
     double2 pq = cmul(p, q);
-    double2 w = make_double2(pq.y * a.scale, -pq.x * a.scale);  // -i * pq * s
+    double2 w = make_double2(mul_hl(pq.y, a.scale, a.scale_lo), -mul_hl(pq.x, a.scale, a.scale_lo));  // -i * pq * s
     buf[padidx(k)] = w;
     if (k2 != k) buf[padidx(k2)] = cconj(w);
   }

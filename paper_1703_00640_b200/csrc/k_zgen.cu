@@ -190,7 +190,7 @@ k_zgen(ZgenArgs a) {
   };
   for (int64_t j = c0 + ext + tid; j < ce + ext; j += kZgenThreads) {
     double au = 0.0, av = 0.0;
-    RowLoop<kMaxLambda>::run([&](auto rc) {
+    RowLoopDown<kMaxLambda>::run([&](auto rc) {
       constexpr int r = decltype(rc)::value;
       if (r < lam) {
         const int64_t i = j - r;  // chunk, in [c0, c1 + ext)

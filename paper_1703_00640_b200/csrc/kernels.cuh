@@ -25,7 +25,7 @@ struct SmallArgs {
   int64_t K;      // recombination coefficients
   int64_t ML;     // limbs scanned
   int32_t shift_s;
-  double scale;   // 1 / (4 L)
+  double scale, scale_lo;  // 1 / (4 L) as hi + lo
   SubFft fwd;     // length L
   SubFft inv;     // length L / 2
   MapConsts mc;
@@ -124,7 +124,7 @@ struct MidArgs {
   SubFft inv;   // length C / 2
   TwGlobal tw;  // omega_L
   uint32_t L;
-  double scale;  // 1 / (4 L)
+  double scale, scale_lo;  // 1 / (4 L) as hi + lo
 };
 __global__ void k_mid(MidArgs a);
 

@@ -23,7 +23,7 @@ __device__ __forceinline__ double premap(const MapConsts& mc, const DF& D,
   const int fam = (mc.mode == kModeLow) ? 0 : 2;
   const int lam = mc.lambda;
   double acc = 0.0;
-  RowLoop<kMaxLambda>::run([&](auto rc) {
+  RowLoopDown<kMaxLambda>::run([&](auto rc) {
     constexpr int r = decltype(rc)::value;
     if (r < lam) {
       int64_t k = j - r;
@@ -70,7 +70,7 @@ __device__ __forceinline__ double post_flat(const MapConsts& mc, const WF& W,
   const int fam = (mc.mode == kModeLow) ? 1 : 3;
   const int lam = mc.lambda;
   double acc = 0.0;
-  RowLoop<kMaxLambda>::run([&](auto rc) {
+  RowLoopDown<kMaxLambda>::run([&](auto rc) {
     constexpr int r = decltype(rc)::value;
     const int64_t k = j - r;
     if (r < lam && k >= 0 && k < N) acc += W(k) * coef_r<r>(fam, double(k), Nd, mc.cpost[r]);

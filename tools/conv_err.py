@@ -95,6 +95,12 @@ def main():
         print(f"  {name:10s} max|err| = {np.abs(e).max():.4g} ({np.abs(e).max() / ulp:.2f} ulp of max, "
               f"x2^b {np.abs(e).max() * scale:.4f})  rms {np.sqrt((e ** 2).mean()) / ulp:.3f} ulp  "
               f"mean {e.mean() / ulp:+.4f} ulp")
+    # a global scale bias shows up as e ~ slope * w
+    for name, e in (("gpu fft", eg), ("numpy fft", en)):
+        slope = float((e * exf).sum() / (exf * exf).sum())
+        res = e - slope * exf
+        print(f"  {name:10s} scale bias {slope / 2.0**-53:+.3f} x 2^-53; after removing it max "
+              f"{np.abs(res).max() / ulp:.2f} ulp rms {np.sqrt((res ** 2).mean()) / ulp:.3f} ulp")
     # where are the worst errors
     idx = np.argsort(-np.abs(eg))[:8]
     print("  worst gpu k:", idx.tolist(), (eg[idx] / ulp).round(2).tolist())
