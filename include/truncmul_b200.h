@@ -86,7 +86,15 @@ typedef struct tmg_stats {
   int64_t transform_length;
   int32_t passes;       /* 1 = fused single CTA, 2 or 3 = multi-pass */
   int32_t kernels;      /* kernels launched for the product */
+  int32_t attempts;     /* 1, or 2+ after escalation */
+  int32_t b;            /* chunk width of the attempt that produced the result */
+  int64_t N;            /* chunk count of that attempt */
+  double first_round_err; /* residual of the first attempt (tripwire value) */
 } tmg_stats;
+
+/* stats.flags bit: the product was recomputed at a lower chunk width after
+ * the first attempt refused (see tmg_context_set_escalation). */
+#define TMG_STAT_ESCALATED (1u << 24)
 
 typedef struct tmg_context tmg_context;
 
@@ -147,6 +155,16 @@ int tmg_device_alloc(size_t bytes, void** out);
 void tmg_device_free(void* p);
 int tmg_memcpy_h2d(tmg_context* ctx, void* dst, const void* src, size_t bytes);
 int tmg_memcpy_d2h(tmg_context* ctx, void* dst, const void* src, size_t bytes);
+
+/* Escalation (default 0 = off, the reference's behaviour): when the float
+ * pipeline of a single host-buffer product refuses (rounding tripwire,
+ * overflow, recombination check -- TMG_ERR_PRECISION_FAILURE), recompute it
+ * at chunk width b - 1 with a fresh N and lambda, up to max_escalations
+ * times.  Structured operands (long runs of equal limbs) concentrate the
+ * spectrum and can exceed the random-input error model the parameters are
+ * chosen by (paper section 5); escalation turns that refusal into an exact
+ * result.  Batched and device-pointer calls never escalate. */
+int tmg_context_set_escalation(tmg_context* ctx, int max_escalations);
 
 /* Kernels launched by the last product call (for launch accounting). */
 int32_t tmg_last_kernel_count(tmg_context* ctx);

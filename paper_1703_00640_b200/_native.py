@@ -47,7 +47,14 @@ class tmg_stats(ctypes.Structure):
         ("transform_length", ctypes.c_int64),
         ("passes", ctypes.c_int32),
         ("kernels", ctypes.c_int32),
+        ("attempts", ctypes.c_int32),
+        ("b", ctypes.c_int32),
+        ("N", ctypes.c_int64),
+        ("first_round_err", ctypes.c_double),
     ]
+
+
+TMG_STAT_ESCALATED = 1 << 24
 
 
 def header_functions() -> list[str]:
@@ -84,6 +91,7 @@ def load():
     L.tmg_context_destroy.argtypes = [vp]
     L.tmg_context_destroy.restype = None
     L.tmg_context_set_stream.argtypes = [vp, vp]
+    L.tmg_context_set_escalation.argtypes = [vp, ctypes.c_int]
     L.tmg_synchronize.argtypes = [vp]
     for name in ("tmg_full_product", "tmg_low_product", "tmg_high_product"):
         getattr(L, name).argtypes = [vp, P(tmg_params), u64p, u64p, u64p, P(tmg_stats)]

@@ -78,6 +78,7 @@ struct Profiler {
 
 struct Context {
   int device = 0;
+  int escalations = 0;  // re-runs at b - 1 after a precision failure
   Profiler prof;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -488,9 +489,9 @@ void init_context(Context& cx, int device) {
 }
 
 // One product (or batch) from host limb arrays.
-int host_product(Context& cx, const Params& p, int32_t want_mode,
-                 const uint64_t* u, const uint64_t* v, int64_t count,
-                 uint64_t* out, uint32_t* flags_out, tmg_stats* stats) {
+int host_product_once(Context& cx, const Params& p, int32_t want_mode,
+                      const uint64_t* u, const uint64_t* v, int64_t count,
+                      uint64_t* out, uint32_t* flags_out, tmg_stats* stats) {
   if (int32_t(p.mode) != want_mode && p.mode != PMode::kOracleFallback)
     throw Error(TMG_ERR_INPUT_OUT_OF_RANGE,
                 "product: params were built for a different mode");
@@ -568,6 +569,48 @@ int host_product(Context& cx, const Params& p, int32_t want_mode,
     TMG_CUDA(cudaMemcpyAsync(flags_out, cx.pflags.p, size_t(count) * 4, cudaMemcpyDeviceToHost,
                              cx.stream));
   return finish(cx, &pl, stats);
+}
+
+// One product from host buffers.  With escalation enabled on the context, a
+// single product whose float pipeline refused (tripwire / overflow /
+// recombination check) -- or, stricter than the reference's "> 1/4" wire,
+// whose residual reached a quarter -- is recomputed at chunk width b - 1, up
+// to cx.escalations times; the stats then describe the attempt that
+// produced the result, with TMG_STAT_ESCALATED set and the first attempt's
+// residual kept.
+int host_product(Context& cx, const Params& p, int32_t want_mode,
+                 const uint64_t* u, const uint64_t* v, int64_t count,
+                 uint64_t* out, uint32_t* flags_out, tmg_stats* stats) {
+  Params q = p;
+  double first_err = -1.0;
+  for (int attempt = 0;; ++attempt) {
+    tmg_stats st;
+    std::memset(&st, 0, sizeof(st));
+    const bool can = attempt < cx.escalations && count == 1 &&
+                     q.mode != PMode::kOracleFallback && q.backend == Backend::kFft &&
+                     q.b > (q.mode == PMode::kFull ? 1 : 4);
+    bool refused = false;
+    try {
+      host_product_once(cx, q, want_mode, u, v, count, out, flags_out, &st);
+      refused = can && !(st.max_round_err < 0.25);
+    } catch (const Error& e) {
+      if (stats) *stats = st;
+      if (!(can && e.code() == TMG_ERR_PRECISION_FAILURE)) throw;
+      refused = true;
+    }
+    if (first_err < 0) first_err = st.max_round_err;
+    if (refused) {
+      q = params_with_chunk(q.n, q.mode, q.b - 1);
+      continue;
+    }
+    st.attempts = attempt + 1;
+    st.first_round_err = first_err;
+    st.b = q.b;
+    st.N = q.N;
+    if (attempt > 0) st.flags |= TMG_STAT_ESCALATED;
+    if (stats) *stats = st;
+    return TMG_OK;
+  }
 }
 
 template <class F>
@@ -750,6 +793,15 @@ int tmg_memcpy_d2h(tmg_context* ctx, void* dst, const void* src, size_t bytes) {
   });
 }
 int32_t tmg_last_kernel_count(tmg_context* ctx) { return ctx->cx.last_kernels; }
+
+int tmg_context_set_escalation(tmg_context* ctx, int max_escalations) {
+  return guarded([&] {
+    if (max_escalations < 0 || max_escalations > 8)
+      throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "escalation count must be in [0, 8]");
+    ctx->cx.escalations = max_escalations;
+    return TMG_OK;
+  });
+}
 
 int tmg_debug_read(tmg_context* ctx, int which, void* host, size_t* bytes) {
   return guarded([&] {

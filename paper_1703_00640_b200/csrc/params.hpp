@@ -58,6 +58,9 @@ void validate_params(const Params& params);
 Params select_params(int64_t n, PMode mode, Backend backend,
                      int64_t fallback_cutoff, Policy policy);
 double predicted_sigma(PMode mode, int32_t b, int64_t N);
+// FFT parameters for n at a given chunk width (the escalation step after a
+// tripwire: same n and mode, b one lower, a fresh smooth N and lambda).
+Params params_with_chunk(int64_t n, PMode mode, int32_t b);
 int64_t transform_length(PMode mode, int64_t N);
 int64_t output_limbs(PMode mode, int64_t n);
 

@@ -215,18 +215,33 @@ class Stats:
     transform_length: int = 0
     passes: int = 0
     kernels: int = 0
+    attempts: int = 0
+    b: int = 0
+    N: int = 0
+    first_round_err: float = 0.0
+
+    @property
+    def escalated(self) -> bool:
+        return bool(self.flags & _native.TMG_STAT_ESCALATED)
 
 
 class Context:
     """One CUDA device, one stream, cached plans and workspaces."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, escalation: int = 0):
         self._lib = _native.load()
         h = ctypes.c_void_p()
         _check(self._lib.tmg_context_create(device, ctypes.byref(h)))
         self._h = h
         self.device = device
         self.last_stats = Stats()
+        if escalation:
+            self.set_escalation(escalation)
+
+    def set_escalation(self, max_escalations: int) -> None:
+        """Recompute a refused single product at b - 1 (up to n times);
+        0 keeps the reference behaviour (raise ConvolutionPrecisionFailure)."""
+        _check(self._lib.tmg_context_set_escalation(self._h, int(max_escalations)))
 
     def close(self) -> None:
         if self._h:
@@ -251,7 +266,7 @@ class Context:
 
     def _stats(self, s: tmg_stats) -> Stats:
         self.last_stats = Stats(s.max_round_err, s.max_abs, s.flags, s.transform_length,
-                                s.passes, s.kernels)
+                                s.passes, s.kernels, s.attempts, s.b, s.N, s.first_round_err)
         return self.last_stats
 
     def product_limbs(self, mode: Mode, u, v, params: Params) -> np.ndarray:
