@@ -217,8 +217,19 @@ def coeff_table(fam: str, lam: int, N: int, b: int) -> np.ndarray:
     return t
 
 
+# Threads for the convolution FFTs.  None: numpy's pocketfft, one thread (the
+# checker); an int: scipy's pocketfft with that many workers (the timed CPU
+# baseline of bench.py, which uses every host thread it can).
+FFT_WORKERS = None
+
+
 def cyclic_convolve(a: np.ndarray, c: np.ndarray) -> np.ndarray:
+    """convolution.cpp:175-195 (FFTW r2c, pointwise product, c2r, 1/L)."""
     n = len(a)
+    if FFT_WORKERS:
+        import scipy.fft as sf
+        return sf.irfft(sf.rfft(a, workers=FFT_WORKERS) * sf.rfft(c, workers=FFT_WORKERS),
+                        n=n, workers=FFT_WORKERS)
     return np.fft.irfft(np.fft.rfft(a) * np.fft.rfft(c), n=n)
 
 
