@@ -4,11 +4,11 @@
  * This is the drop-in boundary for the reference's product entry points
  * (arxiv 1703.00640 artifact, /root/reference/proj/core):
  *
- *   products.hpp:36-45   struct Params          -> tmg_params
- *   products.hpp:48      required_precision     -> tmg_required_precision
- *   products.hpp:52-53   default_lambda         -> tmg_default_lambda
- *   products.hpp:60      validate_params        -> tmg_validate_params
- *   products.hpp:67-68   select_params          -> tmg_select_params
+ *   products.hpp:25-34   struct Params          -> tmg_params
+ *   products.hpp:39-40   required_precision     -> tmg_required_precision
+ *   products.hpp:42-45   default_lambda         -> tmg_default_lambda
+ *   products.hpp:47-53   validate_params        -> tmg_validate_params
+ *   products.hpp:55-62   select_params          -> tmg_select_params
  *   products.hpp:91-93   full_product / low_product / high_product
  *                        -> tmg_full_product / tmg_low_product /
  *                           tmg_high_product  (host limb arrays)
@@ -16,7 +16,7 @@
  *   errors.hpp:9-67      exception classes  -> TMG_ERR_* return codes
  *
  * Operands and results are little-endian arrays of 64-bit limbs (the
- * reference's BigInt::to_limbs / from_limbs, bigint.hpp:118-120).  Operands
+ * reference's BigInt::to_limbs / from_limbs, bigint.hpp:113-115).  Operands
  * hold ceil(n/64) limbs; results hold tmg_output_limbs(mode, n) limbs:
  *   full: ceil(2n/64)   low: ceil(n/64)   high: ceil((n+1)/64)
  *
@@ -43,7 +43,7 @@ enum {
   TMG_MODE_ORACLE_FALLBACK = 3
 };
 
-/* Backend (convolution.hpp:13).  Only the FFT backend is implemented on the
+/* Backend (convolution.hpp:12).  Only the FFT backend is implemented on the
  * GPU; EXACT parameter sets are accepted by the parameter functions and
  * refused by the product functions with TMG_ERR_UNSUPPORTED. */
 enum { TMG_BACKEND_EXACT = 0, TMG_BACKEND_FFT = 1 };
@@ -66,7 +66,7 @@ enum {
   TMG_ERR_INTERNAL = 8
 };
 
-/* Params (products.hpp:36-45) */
+/* Params (products.hpp:25-34) */
 typedef struct tmg_params {
   int64_t n;
   int32_t b;

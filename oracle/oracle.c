@@ -27,7 +27,7 @@ typedef unsigned __int128 u128;
 typedef __int128 i128;
 
 /* ------------------------------------------------------------------------ */
-/* std::mt19937_64 (the generator of gen_inputs.cpp:224-228)                 */
+/* std::mt19937_64 (the generator of gen_inputs.cpp:76-83)                 */
 void orc_mt19937_64(uint64_t seed, uint64_t* out, int64_t count) {
   enum { NN = 312, MM = 156 };
   const uint64_t MATRIX_A = 0xB5026F5AA96619E9ULL;
@@ -63,7 +63,7 @@ void orc_mt19937_64(uint64_t seed, uint64_t* out, int64_t count) {
 }
 
 /* ------------------------------------------------------------------------ */
-/* split.cpp:267-304 (chunk_store): windows of u * 2^lead, balanced digits in
+/* split.cpp:66-102 (chunk_store): windows of u * 2^lead, balanced digits in
  * (-2^{b-1}, 2^{b-1}] below the top chunk, which absorbs the carry. */
 static uint64_t load_limb(const uint64_t* lp, int64_t nl, int64_t i) {
   return (i >= 0 && i < nl) ? lp[i] : 0;
@@ -449,7 +449,7 @@ int orc_round_accumulate(const double* vals, int64_t count, int scale, int b,
 }
 
 /* ------------------------------------------------------------------------ */
-/* oracle.cpp:10-120 (limb_mul): schoolbook below 24 limbs, Karatsuba above,
+/* oracle.cpp:69-130 (limb_mul): schoolbook below 24 limbs, Karatsuba above,
  * on plain little-endian limb arrays (no shared code with GMP). */
 static void school_mul(const uint64_t* a, int64_t na, const uint64_t* b, int64_t nb,
                        uint64_t* r) {

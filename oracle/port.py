@@ -3,7 +3,7 @@
 Restates the reference's float pipeline (arxiv 1703.00640 artifact,
 /root/reference/proj/core/src/products_f64.cpp:106-171) on the CPU:
 
-    split (split.cpp:267-304)  -> oracle.c orc_split
+    split (split.cpp:66-102)  -> oracle.c orc_split
     alpha*/gamma+ (maps_f64.cpp:259-348) -> oracle.c
     real cyclic convolution    -> numpy.fft.rfft/irfft (pocketfft), standing in
                                   for the reference's FFTW r2c/c2r plans
@@ -13,9 +13,9 @@ Restates the reference's float pipeline (arxiv 1703.00640 artifact,
     round_accumulate + SignedAccumulator (products_f64.cpp:16-102) -> oracle.c
 
 plus independent exact products for checking (oracle_full / oracle_low /
-oracle_high_set of oracle.hpp:29-46): GMP's mpn_mul (GMP 6.3.0, the
+oracle_high_set of oracle.hpp:20-35): GMP's mpn_mul (GMP 6.3.0, the
 reference's own bignum dependency, through the system libgmp.so.10) and
-oracle.c's hand-rolled Karatsuba restating oracle.cpp:10-120.
+oracle.c's hand-rolled Karatsuba restating oracle.cpp:69-130.
 
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
 leg may import this module.  The product path never does.
@@ -97,7 +97,7 @@ def int_to_limbs(x: int, nlimbs: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
-# inputs (gen_inputs.cpp:224-228 uses std::mt19937_64 words in order)
+# inputs (gen_inputs.cpp:76-83 uses std::mt19937_64 words in order)
 
 
 def mt19937_64(seed: int, count: int) -> np.ndarray:
@@ -173,7 +173,7 @@ def oracle_low(u, v, n: int) -> np.ndarray:
 
 
 def oracle_high_set(u, v, n: int) -> list[int]:
-    """All w in [0, 2^n] with |uv - 2^n w| < 2^n, ascending (oracle.hpp:39-42)."""
+    """All w in [0, 2^n] with |uv - 2^n w| < 2^n, ascending (oracle.hpp:27-31)."""
     p = limbs_to_int(gmp_mul(u, v))
     q, r = p >> n, p & ((1 << n) - 1)  # bit ops: divmod by 2^n is quadratic
     out = [q]

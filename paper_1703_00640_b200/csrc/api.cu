@@ -532,7 +532,7 @@ int host_product_once(Context& cx, const Params& p, int32_t want_mode,
     for (int64_t i = 0; i < count; ++i) {
       const uint64_t* P = h.data() + i * 2 * nl;
       uint64_t* o = out + i * OLr;
-      // input range check (InputOutOfRange, split.cpp:215-220)
+      // input range check (InputOutOfRange, split.cpp:13-20)
       const uint64_t* ui = u + i * nl;
       const uint64_t* vi = v + i * nl;
       if ((p.n & 63) && ((ui[nl - 1] | vi[nl - 1]) >> (p.n & 63)))

@@ -3,7 +3,7 @@
 // Domain vocabulary follows the reference (arxiv 1703.00640 artifact,
 // /root/reference/proj/core): limbs are little-endian uint64 words of an
 // operand, chunks are the b-bit pieces the operand is split into
-// (split.cpp:267-304), coefficients are the rounded convolution outputs that
+// (split.cpp:66-102), coefficients are the rounded convolution outputs that
 // recombination sums at bit offsets i*b (products_f64.cpp:29-102).
 #pragma once
 
@@ -27,7 +27,7 @@ namespace tmg {
 //   kFlagNegative -> ConvolutionPrecisionFailure
 //       ("full product recombined negative", products_f64.cpp:117-119)
 //   kFlagInputRange -> InputOutOfRange ("split: operand outside [0, 2^n)",
-//       split.cpp:215-220)
+//       split.cpp:13-20)
 enum : uint32_t {
   kFlagTripwire = 1u << 0,
   kFlagOverflow = 1u << 1,

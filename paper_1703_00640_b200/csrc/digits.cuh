@@ -2,7 +2,7 @@
 // pre/post maps of the low and high products, as device functions.
 //
 // Reference semantics:
-//   split            split.cpp:267-304 (chunk_store: windows of u*2^lead,
+//   split            split.cpp:66-102 (chunk_store: windows of u*2^lead,
 //                    balanced digits in (-2^{b-1}, 2^{b-1}], unbalanced top)
 //   series coeffs    series.cpp:146-170 (alpha/beta/gamma/delta closed forms)
 //   alpha*, gamma+   maps_f64.cpp:48-136, 317-348
@@ -56,7 +56,7 @@ __device__ __forceinline__ uint64_t window_bits(const uint64_t* __restrict__ lim
 }
 
 // Transfer code of a chunk for the balanced-split carry chain
-// (split.cpp:294-298): generate if window > 2^{b-1}, propagate if equal.
+// (split.cpp:88-95): generate if window > 2^{b-1}, propagate if equal.
 __device__ __forceinline__ uint32_t split_tf(uint64_t w, int b) {
   const uint64_t half = 1ull << (b - 1);
   return w > half ? tf_const(1) : (w == half ? kTfIdentity : tf_const(0));

@@ -11,7 +11,7 @@
 // mod N.  The carry-in bit of every chunk is kept for the few places that
 // re-derive single digits later (F1's high-product fold and root channel).
 //
-// Reference: split.cpp:267-304 (chunk_store), maps_f64.cpp:48-136 and
+// Reference: split.cpp:66-102 (chunk_store), maps_f64.cpp:48-136 and
 // 317-348 (alpha*, gamma+).
 #include "kernels.cuh"
 

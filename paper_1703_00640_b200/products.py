@@ -4,9 +4,9 @@ Reference interface (arxiv 1703.00640 artifact, /root/reference/proj/core):
 
     enum class Mode { kFull, kLow, kHigh, kOracleFallback }   products.hpp:14
     struct Params { n, b, N, lambda, p, mode, backend, signed_split }
-                                                              products.hpp:36-45
+                                                              products.hpp:25-34
     required_precision / default_lambda / validate_params / select_params
-                                                              products.hpp:48-68
+                                                              products.hpp:39-62
     full_product / low_product / high_product               products.hpp:91-93
     exceptions                                                errors.hpp
 
@@ -101,7 +101,7 @@ class Policy(enum.IntEnum):
     ACCURATE = 1   # + FP64 error model and GPU cost ranking
 
 
-DEFAULT_FALLBACK_CUTOFF = 4096  # products.hpp:48
+DEFAULT_FALLBACK_CUTOFF = 4096  # products.hpp:37
 
 
 @dataclass(frozen=True)
@@ -180,7 +180,7 @@ def manual_params(n: int, b: int, N: int, mode: Mode, backend: Backend = Backend
 
 def to_limbs(x, n: int) -> np.ndarray:
     """Little-endian uint64 limbs of x, exactly ceil(n/64) of them.  Raises
-    InputOutOfRange outside [0, 2^n) (split.cpp:215-220)."""
+    InputOutOfRange outside [0, 2^n) (split.cpp:13-20)."""
     nl = (n + 63) // 64
     if isinstance(x, np.ndarray):
         a = np.ascontiguousarray(x, dtype=np.uint64)
@@ -351,7 +351,7 @@ def default_context(device: int = 0) -> Context:
 
 
 # ---------------------------------------------------------------------------
-# products (products.hpp:80-93)
+# products (products.hpp:81-93)
 
 
 def _run(mode: Mode, u, v, params: Params, ctx: Context | None) -> np.ndarray:
@@ -373,17 +373,17 @@ def high_product_limbs(u, v, params: Params, ctx: Context | None = None) -> np.n
 
 
 def full_product(u, v, params: Params, ctx: Context | None = None) -> int:
-    """u v exactly (Alg. 1, products.hpp:88)."""
+    """u v exactly (Alg. 1, products.hpp:91)."""
     return from_limbs(full_product_limbs(u, v, params, ctx))
 
 
 def low_product(u, v, params: Params, ctx: Context | None = None) -> int:
-    """u v mod 2^n (Alg. 2, products.hpp:89)."""
+    """u v mod 2^n (Alg. 2, products.hpp:92)."""
     return from_limbs(low_product_limbs(u, v, params, ctx))
 
 
 def high_product(u, v, params: Params, ctx: Context | None = None) -> int:
-    """w with |u v - 2^n w| < 2^n, 0 <= w <= 2^n (Alg. 3, products.hpp:90)."""
+    """w with |u v - 2^n w| < 2^n, 0 <= w <= 2^n (Alg. 3, products.hpp:93)."""
     return from_limbs(high_product_limbs(u, v, params, ctx))
 
 

@@ -4,7 +4,7 @@ arithmetic and cross-checked against GMP (oracle/port.py).
 
     python tools/make_golden.py
 
-Inputs follow the reference generator's kinds (gen_inputs.cpp:222-314):
+Inputs follow the reference generator's kinds (gen_inputs.cpp:10-100):
 uniform words from std::mt19937_64, the STRUCTURED boundary list, and the
 ADVERSARIAL chunk patterns near the balanced-split boundary.
 """
@@ -19,7 +19,7 @@ from oracle import port  # noqa: E402
 
 
 def structured_values(n):
-    """gen_inputs.cpp:237-260."""
+    """gen_inputs.cpp:23-46."""
     vals = []
 
     def push(v):
@@ -43,7 +43,7 @@ def structured_values(n):
 
 
 def adversarial_value(words, n, b):
-    """Chunks near the balanced boundary 2^(b-1) (gen_inputs.cpp:265-282),
+    """Chunks near the balanced boundary 2^(b-1) (gen_inputs.cpp:48-68),
     driven by the given mt19937_64 words."""
     chunks = (n + b - 1) // b
     v = 0
