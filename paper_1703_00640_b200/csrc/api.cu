@@ -78,6 +78,7 @@ struct Profiler {
 
 struct Context {
   int device = 0;
+  int num_sms = 148;
   int escalations = 0;  // re-runs at b - 1 after a precision failure
   Profiler prof;
   cudaStream_t stream = nullptr;
@@ -300,11 +301,18 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.tw = pl.twL;
       a.L = uint32_t(L);
       spectral_scale(L, &a.scale, &a.scale_lo);
-      set_smem(k_mid, pl.smem_mid);
-      const unsigned grid = (pl.A * pl.B) / 2 + 1;
-      {
+      const unsigned npairs = (pl.A * pl.B) / 2 + 1;
+      static const bool no_ct = getenv("TMG_NO_CT") != nullptr;
+      if (pl.C == 4096 && pl.mid_shared_table && !no_ct) {
+        // compile-time schedule, persistent over row pairs
+        set_smem(k_mid_4096, pl.smem_mid);
+        const unsigned grid = std::min<unsigned>(npairs, unsigned(cx.num_sms));
         KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode));
-        k_mid<<<grid, pl.thr_mid, pl.smem_mid, st>>>(a);
+        k_mid_4096<<<grid, kMidCtThreads, pl.smem_mid, st>>>(a);
+      } else {
+        set_smem(k_mid, pl.smem_mid);
+        KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode));
+        k_mid<<<npairs, pl.thr_mid, pl.smem_mid, st>>>(a);
       }
       check_launch("k_mid");
       ++kernels;
@@ -480,6 +488,7 @@ void to_c(const Params& q, tmg_params* p) {
 void init_context(Context& cx, int device) {
   cx.device = device;
   TMG_CUDA(cudaSetDevice(device));
+  TMG_CUDA(cudaDeviceGetAttribute(&cx.num_sms, cudaDevAttrMultiProcessorCount, device));
   TMG_CUDA(cudaStreamCreateWithFlags(&cx.stream, cudaStreamNonBlocking));
   cx.own_stream = true;
   cx.status.ensure(sizeof(DevStatus));

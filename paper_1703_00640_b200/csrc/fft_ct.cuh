@@ -1,0 +1,126 @@
+// Compile-time radix schedules for the hot transform shapes.
+//
+// The generic passes of fft_smem.cuh dispatch every stage on a runtime radix
+// and read the stage geometry from the kernel parameters; for the shapes the
+// product sizes hit most (rows of 4096 = 16 x 16 x 16 forward and
+// 2048 = 16 x 16 x 8 inverse) the whole schedule is known at compile time:
+// butterfly counts, strides, Ns and the twiddle-table offsets become
+// immediates, every loop unrolls, and the kernel carries only the code of the
+// stages it runs.  Numerics are those of the generic pass (same stage tables,
+// same in-register DFTs, same order of operations).
+#pragma once
+
+#include "fft_smem.cuh"
+
+namespace tmg {
+
+template <int R0, int R1 = 0, int R2 = 0, int R3 = 0>
+struct Sched {
+  static constexpr int nst = R1 == 0 ? 1 : R2 == 0 ? 2 : R3 == 0 ? 3 : 4;
+  __host__ __device__ static constexpr int rad(int s) {
+    return s == 0 ? R0 : s == 1 ? R1 : s == 2 ? R2 : R3;
+  }
+  __host__ __device__ static constexpr uint32_t ns(int s) {
+    return s == 0 ? 1u : uint32_t(rad(s - 1)) * ns(s - 1);
+  }
+  static constexpr uint32_t R = uint32_t(R0) * (R1 ? R1 : 1) * (R2 ? R2 : 1) * (R3 ? R3 : 1);
+  // offset of stage s in the q-major stage table (make_subfft, plan.cu)
+  __host__ __device__ static constexpr uint32_t toff(int s) {
+    return s <= 1 ? 0u : toff(s - 1) + ns(s - 1) * uint32_t(rad(s - 1) - 1);
+  }
+};
+
+// Row layout with one or two rows (a conjugate pair) of compile-time length.
+struct RowPair {
+  uint32_t rowstride, nrows;
+  __device__ __forceinline__ uint32_t idx(uint32_t item, uint32_t e) const {
+    return item * rowstride + padidx(e);
+  }
+};
+
+template <int RAD, uint32_t R, int NTHR, class Src>
+__device__ __forceinline__ void ct_load(double2 (&x)[16], const RowPair& lay, const Src& src,
+                                        int tid) {
+  constexpr uint32_t nbi = R / RAD;
+  static_assert(2 * nbi <= uint32_t(NTHR) || RAD * ((2 * nbi + NTHR - 1) / NTHR) <= 16,
+                "register block");
+  constexpr int NB = int((2 * nbi + NTHR - 1) / NTHR);
+#pragma unroll
+  for (int it = 0; it < NB; ++it) {
+    const uint32_t bf = uint32_t(tid) + uint32_t(it) * NTHR;
+    if (bf < nbi * lay.nrows) {
+      const uint32_t item = bf >= nbi ? 1u : 0u;
+      const uint32_t t = bf - item * nbi;
+#pragma unroll
+      for (int q = 0; q < RAD; ++q) x[it * RAD + q] = src(item, t + q * nbi);
+    }
+  }
+}
+
+template <int RAD, bool INV, uint32_t R, uint32_t NS, int NTHR, class Sink>
+__device__ __forceinline__ void ct_store(double2 (&x)[16], const RowPair& lay,
+                                         const double2* __restrict__ stab, uint32_t qmul,
+                                         const Sink& sink, int tid) {
+  constexpr uint32_t nbi = R / RAD;
+  constexpr int NB = int((2 * nbi + NTHR - 1) / NTHR);
+#pragma unroll
+  for (int it = 0; it < NB; ++it) {
+    const uint32_t bf = uint32_t(tid) + uint32_t(it) * NTHR;
+    if (bf < nbi * lay.nrows) {
+      const uint32_t item = bf >= nbi ? 1u : 0u;
+      const uint32_t t = bf - item * nbi;
+      const uint32_t tq = t / NS;
+      const uint32_t j = t - tq * NS;
+      double2* xv = x + it * RAD;
+      if (NS > 1 && j != 0) {
+#pragma unroll
+        for (int q = 1; q < RAD; ++q) {
+          const double2 w = stab[(uint32_t(q) * qmul - 1) * NS + j];
+          xv[q] = INV ? cmulc(xv[q], w) : cmul(xv[q], w);
+        }
+      }
+      dft<RAD, INV>(xv);
+      const uint32_t ob = tq * NS * RAD + j;
+#pragma unroll
+      for (int q = 0; q < RAD; ++q) sink(item, ob + q * NS, xv[q]);
+    }
+  }
+}
+
+// Stages S .. nst-1 of schedule SC, through the caller's register block x
+// (one block for every stage: separate per-stage arrays defeat ptxas's
+// register promotion and land in local memory).  Stage 0 reads src, the last stage
+// writes sink, the others exchange through buf (RowPair layout).  toff and
+// qmul of each stage come from the plan (the inverse of a row pass reads the
+// forward table through the qmul mapping, plan.cu map_stages).
+template <bool INV, class SC, int S, int NTHR, class Src, class Sink>
+__device__ __forceinline__ void ct_stages(double2 (&x)[16], double2* __restrict__ buf,
+                                          const RowPair& lay, const double2* __restrict__ stab,
+                                          const SubFft& p, const Src& src, const Sink& sink,
+                                          int tid) {
+  constexpr int RAD = SC::rad(S);
+  constexpr uint32_t NS = SC::ns(S);
+  constexpr uint32_t R = SC::R;
+  constexpr bool last = S + 1 == SC::nst;
+  if constexpr (S == 0) {
+    ct_load<RAD, R, NTHR>(x, lay, src, tid);
+  } else {
+    ct_load<RAD, R, NTHR>(x, lay, SmemSrc<RowPair>{buf, lay}, tid);
+  }
+  __syncthreads();
+  const double2* st = stab + p.toff[S];
+  if constexpr (last) {
+    ct_store<RAD, INV, R, NS, NTHR>(x, lay, st, p.qmul[S], sink, tid);
+  } else {
+    ct_store<RAD, INV, R, NS, NTHR>(x, lay, st, p.qmul[S], SmemSink<RowPair>{buf, lay}, tid);
+    __syncthreads();
+    ct_stages<INV, SC, S + 1, NTHR>(x, buf, lay, stab, p, src, sink, tid);
+  }
+}
+
+// L2 prefetch of a contiguous global range (bytes multiple of 16).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+}  // namespace tmg

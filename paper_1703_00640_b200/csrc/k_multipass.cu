@@ -13,6 +13,7 @@
 // Reference path: products_f64.cpp:106-171 with the FFTW convolution of
 // convolution.cpp:175-195.
 #include "kernels.cuh"
+#include "fft_ct.cuh"
 
 namespace tmg {
 
@@ -311,6 +312,88 @@ k_mid(MidArgs a) {
   __syncthreads();
   fft_pass<true>(sbuf, lay, a.inv, twi, SmemSrc<LayRows>{sbuf, lay},
                  RowSink{a.data, base0, base1, r0, r1, a.tw}, tid, nthr);
+}
+
+// ---------------------------------------------------------------------------
+// Row pass specialised for C = 4096 (forward 16 x 16 x 16, inverse
+// 2048 = 16 x 16 x 8 reading the forward stage table): persistent CTAs (one
+// per SM, the row pair fills shared memory), the stage table staged once per
+// CTA, and the next pair's two rows prefetched into L2 while the current
+// pair computes, so the first stage's loads do not wait on HBM.
+template <int NTHR>
+__device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restrict__ sbuf,
+                                              const double2* __restrict__ stab, uint32_t r0,
+                                              int tid) {
+  using Fwd = Sched<16, 16, 16>;
+  using Inv = Sched<16, 16, 8>;
+  constexpr uint32_t C = 4096, H = 2048;
+  const uint32_t AB = a.A * a.B;
+  const uint32_t r1 = (AB - r0) % AB;
+  const uint32_t nrows = (r1 == r0) ? 1 : 2;
+  const RowPair lay{padded_len(C) + 4, nrows};
+  const int64_t base0 = (int64_t(r0 % a.A) * a.B + (r0 / a.A)) * int64_t(C);
+  const int64_t base1 = (int64_t(r1 % a.A) * a.B + (r1 / a.A)) * int64_t(C);
+  double2 x[16];
+  ct_stages<false, Fwd, 0, NTHR>(x, sbuf, lay, stab, a.fwd, RowSrc{a.data, base0, base1},
+                                 SmemSink<RowPair>{sbuf, lay}, tid);
+  __syncthreads();
+  // spectral product over the pair (see k_mid)
+  const uint32_t brw = (r0 != 0) ? 1u : 0u;
+#pragma unroll 2
+  for (uint32_t k = tid; k < C; k += NTHR) {
+    const uint32_t kp = (C - k - brw) & (C - 1);
+    const uint32_t ip = (nrows == 2) ? 1u : 0u;
+    if (nrows == 1 && kp < k) continue;
+    const double2 z1 = sbuf[lay.idx(0, k)], z2 = sbuf[lay.idx(ip, kp)];
+    const double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
+    const double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
+    const double2 pq = cmul(p, q);
+    const double2 w = make_double2(mul_hl(pq.y, a.scale, a.scale_lo),
+                                   -mul_hl(pq.x, a.scale, a.scale_lo));
+    sbuf[lay.idx(0, k)] = w;
+    if (!(nrows == 1 && kp == k)) sbuf[lay.idx(ip, kp)] = cconj(w);
+  }
+  __syncthreads();
+#pragma unroll 2
+  for (uint32_t e = tid; e < nrows * H; e += NTHR) {
+    const uint32_t i = e >= H ? 1 : 0, k = e - i * H;
+    const uint32_t r = i ? r1 : r0;
+    const double2 w1 = sbuf[lay.idx(i, k)], w2 = sbuf[lay.idx(i, k + H)];
+    const double2 ev = cadd(w1, w2);
+    const double2 o = cmulc(csub(w1, w2), a.tw.get(r + AB * k));
+    sbuf[lay.idx(i, k)] = make_double2(ev.x - o.y, ev.y + o.x);
+  }
+  __syncthreads();
+  ct_stages<true, Inv, 0, NTHR>(x, sbuf, lay, stab, a.inv, SmemSrc<RowPair>{sbuf, lay},
+                                RowSink{a.data, base0, base1, r0, r1, a.tw}, tid);
+}
+
+__global__ void __launch_bounds__(kMidCtThreads)
+k_mid_4096(MidArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sbuf = reinterpret_cast<double2*>(smem_raw);
+  const int tid = threadIdx.x;
+  constexpr uint32_t C = 4096;
+  const uint32_t AB = a.A * a.B;
+  const uint32_t npairs = AB / 2 + 1;
+  double2* stw = sbuf + 2 * (padded_len(C) + 4);
+  for (uint32_t i = tid; i < a.fwd.stablen; i += kMidCtThreads) stw[i] = __ldg(a.fwd.stab + i);
+  auto row_base = [&](uint32_t r) {
+    return a.data + (int64_t(r % a.A) * a.B + (r / a.A)) * int64_t(C);
+  };
+  if (tid == 0 && blockIdx.x < npairs) {
+    prefetch_l2(row_base(blockIdx.x), C * 16);
+    prefetch_l2(row_base((AB - blockIdx.x) % AB), C * 16);
+  }
+  __syncthreads();
+  for (uint32_t r0 = blockIdx.x; r0 < npairs; r0 += gridDim.x) {
+    const uint32_t nx = r0 + gridDim.x;
+    if (tid == 0 && nx < npairs) {
+      prefetch_l2(row_base(nx), C * 16);
+      prefetch_l2(row_base((AB - nx) % AB), C * 16);
+    }
+    mid_pair_4096<kMidCtThreads>(a, sbuf, stw, r0, tid);
+  }
 }
 
 // ---------------------------------------------------------------------------

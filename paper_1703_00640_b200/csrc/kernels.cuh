@@ -127,6 +127,9 @@ struct MidArgs {
   double scale, scale_lo;  // 1 / (4 L) as hi + lo
 };
 __global__ void k_mid(MidArgs a);
+// C = 4096 row pass with compile-time schedules, persistent over row pairs.
+constexpr int kMidCtThreads = 512;
+__global__ void k_mid_4096(MidArgs a);
 
 struct ILastArgs {
   const double2* data;  // S[k_a][...] with geometry g (outer = 0)
