@@ -85,7 +85,7 @@ struct Context {
   bool own_stream = false;
   TwiddleCache tw;
   std::map<std::tuple<int64_t, int32_t, int64_t, int64_t, int32_t>, std::unique_ptr<Plan>> plans;
-  DevBuf work_t, work_c, work_z, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf;
+  DevBuf work_t, work_c, work_z, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf, aggs;
   ScanSlot scan_u, scan_v, scan_c, scan_h;
   bool debug_sync = false;
   DevStatus* h_status = nullptr;  // pinned
@@ -381,13 +381,38 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       } else {
         a.tbuf = nullptr;
       }
-      set_smem(k_carry, pl.smem_carry);
-      {
-        KTimer kt(cx, "k_carry", double(pl.K) * 8.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0, int(p.mode));
-        k_carry<<<blocks, kCarryThreads, pl.smem_carry, st>>>(a);
+      static const bool old_carry = getenv("TMG_OLD_CARRY") != nullptr;
+      const int lam = (p.mode == PMode::kFull) ? 0 : int(pl.mc.lambda);
+      const size_t smem2 = carry2_smem(int(p.b), lam);
+      if (!old_carry && smem2 <= kMaxDynSmem) {
+        const unsigned blocks2 = unsigned((pl.ML + kC2Limbs - 1) / kC2Limbs);
+        cx.aggs.ensure(size_t(blocks2) * 4 + 16);
+        a.aggs = cx.aggs.as<uint32_t>();
+        a.sbuf = cx.work_t.p;  // the transform buffer is free after k_ilast
+        CarryLanesFn lanes = carry_lanes_kernel(lam);
+        set_smem(lanes, smem2);
+        {
+          KTimer kt(cx, "k_carry_lanes", double(pl.K) * 8.0 + double(pl.ML) * 16.0, int(p.mode));
+          lanes<<<blocks2, kC2Threads, smem2, st>>>(a);
+        }
+        check_launch("k_carry_lanes");
+        {
+          KTimer kt(cx, "k_carry_apply",
+                    double(pl.ML) * 16.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0,
+                    int(p.mode));
+          k_carry_apply<<<blocks2, kC2Threads, 0, st>>>(a);
+        }
+        check_launch("k_carry_apply");
+        kernels += 2;
+      } else {
+        set_smem(k_carry, pl.smem_carry);
+        {
+          KTimer kt(cx, "k_carry", double(pl.K) * 8.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0, int(p.mode));
+          k_carry<<<blocks, kCarryThreads, pl.smem_carry, st>>>(a);
+        }
+        check_launch("k_carry");
+        ++kernels;
       }
-      check_launch("k_carry");
-      ++kernels;
     }
     if (p.mode == PMode::kHigh) {
       HighRoundArgs a;

@@ -1,0 +1,335 @@
+// Post-map, rounding and carry propagation as two kernels without
+// inter-block waiting.
+//
+//   k_carry_lanes  every block owns kC2Limbs consecutive limbs; each thread
+//                  the coefficients whose bit offsets k b land in its
+//                  kC2PerThread limbs.  It post-maps them (beta* low, delta+
+//                  high; nothing for the full product), rounds them with the
+//                  reference's tripwire, forms the signed 128-bit lanes
+//                  lane_m = sum e_k << (k b - 64 m) and the limb sums
+//                  s_m = lo(lane_m) + hi(lane_{m-1}), writes s_m to scratch
+//                  and the block's composed carry transfer function to
+//                  aggs[blk].
+//   k_carry_apply  carry-in of a block = the composition of the aggregates
+//                  before it (read in parallel, no look-back), then a block
+//                  scan of the limb transfer functions and the output limbs.
+//
+// Compared with the single-pass look-back kernel (k_carry), no block ever
+// waits on another: the lanes kernel runs at full occupancy and its
+// aggregate is final when it is written.
+//
+// The post-map runs in scatter form: each convolution value w_i meets its
+// row coefficients P_r(i) c_r (r < lambda, built with the same
+// multiplications as coef_r) and adds into a circular bank of lambda
+// accumulators, output j = i + r; output j is complete when i = j (row 0,
+// added last).  Every output therefore sums its rows in the order
+// r = lambda-1 .. 0 with the same fused multiply-adds as post_flat, so the
+// values are bit-identical to the generic path.  The few outputs that also
+// see the wrap of the cyclic maps (low: j <= lambda - 1; high: i below the
+// fold, k = N) go through the generic helpers.
+//
+// Reference: products_f64.cpp:29-102 (SignedAccumulator, round_accumulate),
+// maps_f64.cpp:140-188, 269-281, 350-384 (beta*, delta+).
+#include "kernels.cuh"
+
+namespace tmg {
+
+namespace {
+
+constexpr int kT = kC2Threads;
+constexpr int kPT = kC2PerThread;
+
+__device__ __forceinline__ int64_t kfirst(int64_t m, int b, int64_t K) {  // first k of lane m
+  const int64_t k = (64 * m + b - 1) / b;
+  return k < K ? k : K;
+}
+
+// Rounded coefficients e_k of one thread's run [k0, k1) into se[k - kbase].
+template <int LAM>
+__device__ __forceinline__ void coeffs_run(const CarryArgs& a, const double* __restrict__ sww,
+                                           int64_t wlo, int64_t nw, int64_t k0, int64_t k1,
+                                           long long* __restrict__ se, int64_t kbase,
+                                           RoundAcc& ra, double psi, long long c0v) {
+  const MapConsts& mc = a.mc;
+  auto WS = [&](int64_t j) -> double {
+    const int64_t o = j - wlo;
+    return (o >= 0 && o < nw) ? sww[o] : __ldg(a.w + j);
+  };
+  if constexpr (LAM == 0) {
+    for (int64_t k = k0; k < k1; ++k) se[k - kbase] = ra.round(sww[k - wlo]);
+  } else {
+    if (k0 >= k1) return;
+    const int b = mc.b;
+    const int64_t N = mc.N;
+    const bool low = mc.mode == kModeLow;
+    const double Nd = double(N);
+    const double st = low ? Nd : -Nd;  // beta: k + i N, delta: k - i N
+    const double step = mc.step, sc = mc.scale_out;
+    double cr[LAM];
+#pragma unroll
+    for (int r = 0; r < LAM; ++r) cr[r] = mc.cpost[r];
+    // post_flat outputs j: low j = k + 1 over [k0 + 1, k1 + 1); high the
+    // folded buffer hbuf(i) over [k0 - 1, k1) (x_k needs hbuf(k), hbuf(k-1))
+    const int64_t j0 = low ? k0 + 1 : k0 - 1;
+    const int64_t j1 = low ? k1 + 1 : k1;
+    const int64_t hslow = int64_t(mc.nfold) + LAM - 2;  // hbuf(i) = post_flat(i) from here on
+    double acc[LAM];
+#pragma unroll
+    for (int r = 0; r < LAM; ++r) acc[r] = 0.0;
+    double hprev = 0.0;
+    for (int64_t base = j0 - (LAM - 1); base < j1; base += LAM) {
+#pragma unroll
+      for (int u = 0; u < LAM; ++u) {
+        const int64_t i = base + u;
+        if (i < j1) {
+          if (i >= 0 && i < N) {
+            // rows r = LAM-1 .. 1 of w_i go to outputs i + r; row 0 to i
+            const double wi = sww[i - wlo];
+            const double kd = double(i);
+            double p = kd, f = kd + st;
+            double cf[LAM];
+            cf[0] = 1.0;
+#pragma unroll
+            for (int r = 1; r < LAM; ++r) {
+              cf[r] = p * cr[r];
+              p *= f;
+              f += st;
+            }
+#pragma unroll
+            for (int r = LAM - 1; r >= 1; --r) acc[(u + r) % LAM] = fma(wi, cf[r], acc[(u + r) % LAM]);
+            acc[u] = acc[u] + wi;
+          }
+          // output j = i is complete
+          const double pf = acc[u];
+          acc[u] = 0.0;
+          if (i >= j0) {
+            if (low) {
+              const int64_t k = i - 1;
+              const double x = (i <= LAM - 1) ? postmap_low(mc, WS, i) : pf * sc;
+              long long e = ra.round(x);
+              if (k == 0) e += (c0v >> b);
+              se[k - kbase] = e;
+            } else {
+              const double hb = (i < hslow && i < N) ? high_buf(mc, WS, i) : pf;
+              if (i >= k0) {
+                const int64_t k = i;
+                double v = (k == N) ? psi - hprev * step : hb - hprev * step;
+                if (k < mc.nfold) v -= psi * mc.fold[k];
+                se[k - kbase] = ra.round(v * sc);
+              }
+              hprev = (i >= 0 && i < N) ? hb : 0.0;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int LAM>
+__global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t sw[32];
+  __shared__ long long s_hi[kT];
+  __shared__ double s_psi;
+  __shared__ uint32_t s_flags;
+  const int tid = threadIdx.x;
+  const MapConsts& mc = a.mc;
+  const int b = mc.b;
+  const int64_t K = a.K;
+  const int64_t blk = blockIdx.x;
+  const int64_t ms = blk * kC2Limbs;
+  const int64_t me = min(a.ML, ms + kC2Limbs);
+  const int64_t kbase = kfirst(ms > 0 ? ms - 1 : 0, b, K);
+  const int64_t kend = kfirst(me, b, K);
+  // staged convolution window (post-map neighbourhood: lambda below, one above)
+  const int64_t nwt = (mc.mode == kModeFull) ? K : mc.N;
+  const int64_t wlo = max(int64_t(0), kbase - LAM - 1);
+  const int64_t whi = min(nwt, kend + 2);
+  const int64_t nw = whi > wlo ? whi - wlo : 0;
+  double* sww = reinterpret_cast<double*>(smem_raw);
+  long long* se = reinterpret_cast<long long*>(sww + (nw + 1));
+  for (int64_t j = wlo + tid; j < whi; j += kT) sww[j - wlo] = __ldg(a.w + j);
+  if (tid == 0) {
+    s_flags = 0;
+    s_psi = (mc.mode == kModeHigh) ? high_psi(mc, [&](int64_t j) { return __ldg(a.w + j); },
+                                              a.aux[0])
+                                   : 0.0;
+  }
+  __syncthreads();
+  RoundAcc ra;
+  uint32_t flags = 0;
+  long long c0v = 0;
+  const int64_t m0 = ms + int64_t(tid) * kPT;
+  if (mc.mode == kModeLow && ms == 0 && tid == 0) {
+    auto WS = [&](int64_t j) -> double {
+      const int64_t o = j - wlo;
+      return (o >= 0 && o < nw) ? sww[o] : __ldg(a.w + j);
+    };
+    c0v = ra.round(postmap_low(mc, WS, 0));
+    if (c0v & ((1ll << b) - 1)) flags |= kFlagLowNotDivisible;
+  }
+  // this thread's coefficients (thread 0 also those of lane ms - 1)
+  const int64_t kr0 = (tid == 0) ? kbase : kfirst(m0, b, K);
+  const int64_t kr1 = kfirst(min(m0 + kPT, me), b, K);
+  if (m0 < me) coeffs_run<LAM>(a, sww, wlo, nw, kr0, kr1, se, kbase, ra, s_psi, c0v);
+  // lanes of the thread's limbs
+  unsigned long long lo[kPT];
+  long long hi[kPT];
+#pragma unroll
+  for (int q = 0; q < kPT; ++q) {
+    const int64_t m = m0 + q;
+    __int128 L = 0;
+    if (m < me) {
+      const int64_t ka = kfirst(m, b, K), kb = kfirst(m + 1, b, K);
+      for (int64_t k = ka; k < kb; ++k) L += (__int128)se[k - kbase] << int(k * b - 64 * m);
+    }
+    lo[q] = (unsigned long long)L;
+    hi[q] = (long long)(L >> 64);
+  }
+  long long hin = 0;  // hi(lane_{m0 - 1})
+  if (tid == 0 && ms > 0) {
+    const int64_t m = ms - 1;
+    __int128 L = 0;
+    const int64_t ka = kfirst(m, b, K), kb = kfirst(m + 1, b, K);
+    for (int64_t k = ka; k < kb; ++k) L += (__int128)se[k - kbase] << int(k * b - 64 * m);
+    hin = (long long)(L >> 64);
+  }
+  s_hi[tid] = hi[kPT - 1];
+  __syncthreads();
+  if (tid > 0) hin = s_hi[tid - 1];
+  uint32_t f = kTfIdentity;
+  ulonglong2* sm = reinterpret_cast<ulonglong2*>(a.sbuf);
+#pragma unroll
+  for (int q = 0; q < kPT; ++q) {
+    const int64_t m = m0 + q;
+    if (m < me) {
+      const __int128 s = (__int128)lo[q] + (__int128)(q == 0 ? hin : hi[q - 1]);
+      f = tf_compose(f, limb_tf(s, flags));
+      sm[m] = make_ulonglong2((unsigned long long)s, (unsigned long long)(long long)(s >> 64));
+    }
+  }
+  uint32_t agg;
+  (void)block_scan_tf(f, sw, &agg);
+  if (tid == 0) a.aggs[blk] = agg;
+  flags |= ra.flags;
+  {
+    double e = ra.max_err, m = ra.max_abs;
+    for (int off = 16; off > 0; off >>= 1) {
+      e = fmax(e, __shfl_xor_sync(0xffffffffu, e, off));
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    }
+    if ((tid & 31) == 0) status_merge(a.status, e, m, 0);
+  }
+  if (flags) atomicOr(&s_flags, flags);
+  __syncthreads();
+  if (tid == 0 && s_flags) atomicOr(&a.status->flags, s_flags);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
+  __shared__ uint32_t sw[32];
+  __shared__ uint32_t s_flags, s_low;
+  const int tid = threadIdx.x;
+  const MapConsts& mc = a.mc;
+  const int64_t blk = blockIdx.x;
+  const int64_t ms = blk * kC2Limbs;
+  const int64_t me = min(a.ML, ms + kC2Limbs);
+  if (tid == 0) {
+    s_flags = 0;
+    s_low = 0;
+  }
+  // carry into the block: aggregates of blocks 0 .. blk-1 in order
+  uint32_t g = kTfIdentity;
+  {
+    const int64_t Q = (blk + kT - 1) / kT;
+    const int64_t i0 = int64_t(tid) * Q, i1 = min(blk, i0 + Q);
+    for (int64_t i = i0; i < i1; ++i) g = tf_compose(g, __ldg(a.aggs + i));
+  }
+  uint32_t pre;
+  (void)block_scan_tf(g, sw, &pre);
+  const int cin = tf_apply(pre, 0);
+  // limbs of this thread
+  const int64_t m0 = ms + int64_t(tid) * kPT;
+  const ulonglong2* sm = reinterpret_cast<const ulonglong2*>(a.sbuf);
+  __int128 s[kPT];
+  uint32_t flags = 0, f = kTfIdentity;
+#pragma unroll
+  for (int q = 0; q < kPT; ++q) {
+    const int64_t m = m0 + q;
+    s[q] = 0;
+    if (m < me) {
+      const ulonglong2 v = sm[m];
+      s[q] = (__int128)(long long)v.y * ((__int128)1 << 64) + (__int128)v.x;
+      f = tf_compose(f, limb_tf(s[q], flags));
+    }
+  }
+  uint32_t agg;
+  const uint32_t ex = block_scan_tf(f, sw, &agg);
+  int c = tf_apply(ex, cin);
+  const int64_t OL = a.out_limbs;
+  const int64_t sb = a.shift_s - 1;  // high: bit s-1
+  uint32_t sticky = 0;
+#pragma unroll
+  for (int q = 0; q < kPT; ++q) {
+    const int64_t m = m0 + q;
+    if (m < me) {
+      const uint32_t tfm = limb_tf(s[q], flags);
+      const uint64_t x = (unsigned long long)(s[q] + c);
+      c = tf_apply(tfm, c);
+      if (mc.mode == kModeFull) {
+        const int64_t nb2 = 2 * a.n;
+        if (m < OL) {
+          if (m == OL - 1 && (nb2 & 63) && (x >> (nb2 & 63))) flags |= kFlagFullOverflow;
+          a.out[m] = x;
+        } else if (x) {
+          flags |= kFlagFullOverflow;
+        }
+      } else if (mc.mode == kModeLow) {
+        if (m < OL) a.out[m] = (m == OL - 1 && (a.n & 63)) ? (x & ((1ull << (a.n & 63)) - 1)) : x;
+      } else {
+        a.tbuf[m] = x;
+        const int64_t bit0 = 64 * m;
+        if (bit0 + 64 <= sb) {
+          if (x) sticky = 1;
+        } else if (bit0 < sb) {
+          if (x & ((1ull << (sb - bit0)) - 1)) sticky = 1;
+        }
+      }
+      if (m == a.ML - 1 && c < 0) {
+        // sign of the recombined value (carry out of the top limb)
+        if (mc.mode == kModeFull) flags |= kFlagNegative;
+        if (mc.mode == kModeHigh) flags |= kFlagHighRange;
+      }
+    }
+  }
+  if (sticky) atomicOr(&s_low, 1u);
+  if (flags) atomicOr(&s_flags, flags);
+  __syncthreads();
+  if (tid == 0) {
+    if (s_flags) atomicOr(&a.status->flags, s_flags);
+    if (s_low) atomicOr(&a.status->high_sticky, 1u);
+  }
+}
+
+size_t carry2_smem(int b, int lam) {
+  const int64_t nk = (64 * int64_t(kC2Limbs + 1) + b - 1) / b + 4;
+  return size_t(nk + lam + 8) * 8 + size_t(nk + 4) * 8 + 64;
+}
+
+CarryLanesFn carry_lanes_kernel(int lam) {
+  switch (lam) {
+    case 0: return k_carry_lanes<0>;
+    case 1: return k_carry_lanes<1>;
+    case 2: return k_carry_lanes<2>;
+    case 3: return k_carry_lanes<3>;
+    case 4: return k_carry_lanes<4>;
+    case 5: return k_carry_lanes<5>;
+    case 6: return k_carry_lanes<6>;
+    case 7: return k_carry_lanes<7>;
+    default: return k_carry_lanes<8>;
+  }
+}
+
+}  // namespace tmg

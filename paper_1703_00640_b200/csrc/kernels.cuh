@@ -153,11 +153,21 @@ struct CarryArgs {
   ScanState scan;
   DevStatus* status;
   uint64_t* tbuf;  // high: all limbs of t (ML words)
+  // two-kernel carry (k_carry2.cu)
+  void* sbuf;       // limb sums s_m, 16 B per limb
+  uint32_t* aggs;   // per-block carry transfer functions
 };
 constexpr int kCarryThreads = 256;
 constexpr int kCarryPerThread = 2;
 __global__ void k_carry(CarryArgs a);
 size_t carry_smem(int b);
+constexpr int kC2Threads = 256;
+constexpr int kC2PerThread = 4;
+constexpr int kC2Limbs = kC2Threads * kC2PerThread;
+typedef void (*CarryLanesFn)(CarryArgs);
+CarryLanesFn carry_lanes_kernel(int lam);
+__global__ void k_carry_apply(CarryArgs a);
+size_t carry2_smem(int b, int lam);
 
 struct HighRoundArgs {
   const uint64_t* tbuf;
