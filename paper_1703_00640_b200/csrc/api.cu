@@ -384,7 +384,8 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       static const bool old_carry = getenv("TMG_OLD_CARRY") != nullptr;
       const int lam = (p.mode == PMode::kFull) ? 0 : int(pl.mc.lambda);
       const size_t smem2 = carry2_smem(int(p.b), lam);
-      if (!old_carry && smem2 <= kMaxDynSmem) {
+      if (!old_carry && smem2 <= kMaxDynSmem && 64 * pl.ML + 64 < (int64_t(1) << 32)) {
+        a.fb = make_fastdiv(uint32_t(p.b));
         const unsigned blocks2 = unsigned((pl.ML + kC2Limbs - 1) / kC2Limbs);
         cx.aggs.ensure(size_t(blocks2) * 4 + 16);
         a.aggs = cx.aggs.as<uint32_t>();

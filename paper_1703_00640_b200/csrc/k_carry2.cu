@@ -39,9 +39,39 @@ namespace {
 constexpr int kT = kC2Threads;
 constexpr int kPT = kC2PerThread;
 
-__device__ __forceinline__ int64_t kfirst(int64_t m, int b, int64_t K) {  // first k of lane m
-  const int64_t k = (64 * m + b - 1) / b;
+// First coefficient of lane m, ceil(64 m / b), clamped to K.  The host
+// takes this path only when every bit offset fits in 32 bits
+// (64 ML + 64 < 2^32), so a 32-bit reciprocal division (FastDiv) replaces
+// the 64-bit one.
+__device__ __forceinline__ int64_t kfirst(int64_t m, const FastDiv& fb, int64_t K) {
+  const uint32_t num = uint32_t(64 * m) + fb.d - 1u;
+  const int64_t k = int64_t(fdiv(num, fb));
   return k < K ? k : K;
+}
+
+// acc += e << sh for 0 <= sh < 64 on a signed 128-bit (lo, hi) pair.
+__device__ __forceinline__ void add_shifted(unsigned long long& lo, long long& hi, long long e,
+                                            uint32_t sh) {
+  const unsigned long long l = (unsigned long long)e << sh;
+  const long long h = (e >> 1) >> (63 - sh);  // arithmetic; sh = 0 gives the sign word
+  const unsigned long long nlo = lo + l;
+  hi += h + (nlo < lo ? 1 : 0);
+  lo = nlo;
+}
+
+// Lane m = sum_{k in lane m} e_k << (k b - 64 m) from se[k - kbase].
+__device__ __forceinline__ void lane_of(const long long* __restrict__ se, int64_t kbase,
+                                        int64_t m, int64_t ka, int64_t kb, int b,
+                                        unsigned long long& lo, long long& hi) {
+  lo = 0;
+  hi = 0;
+  const int n = int(kb - ka);
+  const long long* p = se + (ka - kbase);
+  uint32_t sh = uint32_t(ka * b - 64 * m);
+  for (int i = 0; i < n; ++i) {
+    add_shifted(lo, hi, p[i], sh);
+    sh += uint32_t(b);
+  }
 }
 
 // Rounded coefficients e_k of one thread's run [k0, k1) into se[k - kbase].
@@ -140,8 +170,8 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
   const int64_t blk = blockIdx.x;
   const int64_t ms = blk * kC2Limbs;
   const int64_t me = min(a.ML, ms + kC2Limbs);
-  const int64_t kbase = kfirst(ms > 0 ? ms - 1 : 0, b, K);
-  const int64_t kend = kfirst(me, b, K);
+  const int64_t kbase = kfirst(ms > 0 ? ms - 1 : 0, a.fb, K);
+  const int64_t kend = kfirst(me, a.fb, K);
   // staged convolution window (post-map neighbourhood: lambda below, one above)
   const int64_t nwt = (mc.mode == kModeFull) ? K : mc.N;
   const int64_t wlo = max(int64_t(0), kbase - LAM - 1);
@@ -149,7 +179,19 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
   const int64_t nw = whi > wlo ? whi - wlo : 0;
   double* sww = reinterpret_cast<double*>(smem_raw);
   long long* se = reinterpret_cast<long long*>(sww + (nw + 1));
-  for (int64_t j = wlo + tid; j < whi; j += kT) sww[j - wlo] = __ldg(a.w + j);
+  {
+    // all loads of a thread in flight before the stores
+    constexpr int U = 8;
+    int64_t j = wlo + tid;
+    for (; j + (U - 1) * kT < whi; j += U * kT) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldg(a.w + j + u * kT);
+#pragma unroll
+      for (int u = 0; u < U; ++u) sww[j + u * kT - wlo] = v[u];
+    }
+    for (; j < whi; j += kT) sww[j - wlo] = __ldg(a.w + j);
+  }
   if (tid == 0) {
     s_flags = 0;
     s_psi = (mc.mode == kModeHigh) ? high_psi(mc, [&](int64_t j) { return __ldg(a.w + j); },
@@ -170,30 +212,30 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
     if (c0v & ((1ll << b) - 1)) flags |= kFlagLowNotDivisible;
   }
   // this thread's coefficients (thread 0 also those of lane ms - 1)
-  const int64_t kr0 = (tid == 0) ? kbase : kfirst(m0, b, K);
-  const int64_t kr1 = kfirst(min(m0 + kPT, me), b, K);
+  const int64_t kr0 = (tid == 0) ? kbase : kfirst(m0, a.fb, K);
+  const int64_t kr1 = kfirst(min(m0 + kPT, me), a.fb, K);
   if (m0 < me) coeffs_run<LAM>(a, sww, wlo, nw, kr0, kr1, se, kbase, ra, s_psi, c0v);
   // lanes of the thread's limbs
   unsigned long long lo[kPT];
   long long hi[kPT];
+  {
+    int64_t ka = kfirst(m0, a.fb, K);
 #pragma unroll
-  for (int q = 0; q < kPT; ++q) {
-    const int64_t m = m0 + q;
-    __int128 L = 0;
-    if (m < me) {
-      const int64_t ka = kfirst(m, b, K), kb = kfirst(m + 1, b, K);
-      for (int64_t k = ka; k < kb; ++k) L += (__int128)se[k - kbase] << int(k * b - 64 * m);
+    for (int q = 0; q < kPT; ++q) {
+      const int64_t m = m0 + q;
+      lo[q] = 0;
+      hi[q] = 0;
+      if (m < me) {
+        const int64_t kb = kfirst(m + 1, a.fb, K);
+        lane_of(se, kbase, m, ka, kb, b, lo[q], hi[q]);
+        ka = kb;
+      }
     }
-    lo[q] = (unsigned long long)L;
-    hi[q] = (long long)(L >> 64);
   }
   long long hin = 0;  // hi(lane_{m0 - 1})
   if (tid == 0 && ms > 0) {
-    const int64_t m = ms - 1;
-    __int128 L = 0;
-    const int64_t ka = kfirst(m, b, K), kb = kfirst(m + 1, b, K);
-    for (int64_t k = ka; k < kb; ++k) L += (__int128)se[k - kbase] << int(k * b - 64 * m);
-    hin = (long long)(L >> 64);
+    unsigned long long l0;
+    lane_of(se, kbase, ms - 1, kbase, kfirst(ms, a.fb, K), b, l0, hin);
   }
   s_hi[tid] = hi[kPT - 1];
   __syncthreads();

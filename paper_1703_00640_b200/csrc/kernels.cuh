@@ -156,6 +156,7 @@ struct CarryArgs {
   // two-kernel carry (k_carry2.cu)
   void* sbuf;       // limb sums s_m, 16 B per limb
   uint32_t* aggs;   // per-block carry transfer functions
+  FastDiv fb;       // division by b
 };
 constexpr int kCarryThreads = 256;
 constexpr int kCarryPerThread = 2;
