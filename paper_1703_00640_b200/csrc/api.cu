@@ -85,7 +85,7 @@ struct Context {
   bool own_stream = false;
   TwiddleCache tw;
   std::map<std::tuple<int64_t, int32_t, int64_t, int64_t, int32_t>, std::unique_ptr<Plan>> plans;
-  DevBuf work_t, work_c, work_z, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf, aggs;
+  DevBuf work_t, work_c, work_z, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf, aggs, zaggs;
   ScanSlot scan_u, scan_v, scan_c, scan_h;
   bool debug_sync = false;
   DevStatus* h_status = nullptr;  // pinned
@@ -232,13 +232,21 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       const unsigned blocks = unsigned((pl.count + kZgenChunks - 1) / kZgenChunks);
       a.scan = cx.scan_u.next(blocks);
       a.status = status;
-      set_smem(k_zgen, pl.smem_zgen);
+      cx.zaggs.ensure(size_t(blocks) * 4 + 16);
+      a.aggs = cx.zaggs.as<uint32_t>();
+      {
+        KTimer kt(cx, "k_zstat", double(2 * pl.nlimbs) * 8.0, int(p.mode));
+        k_zstat<<<(blocks + 255) / 256, 256, 0, st>>>(a);
+      }
+      check_launch("k_zstat");
+      ZgenFn zg = zgen_kernel(int(p.b));
+      set_smem(zg, pl.smem_zgen);
       {
         KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * 16.0, int(p.mode));
-        k_zgen<<<blocks, kZgenThreads, pl.smem_zgen, st>>>(a);
+        zg<<<blocks, kZgenThreads, pl.smem_zgen, st>>>(a);
       }
       check_launch("k_zgen");
-      ++kernels;
+      kernels += 2;
     }
     double2* T = cx.work_t.as<double2>();
     {

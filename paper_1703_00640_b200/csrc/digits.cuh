@@ -55,6 +55,46 @@ __device__ __forceinline__ uint64_t window_bits(const uint64_t* __restrict__ lim
   return w & mask;
 }
 
+// Sequential reader of consecutive b-bit windows of u * 2^lead.
+template <class Ld>
+struct WindowReader {
+  Ld ld;
+  int64_t idx;
+  uint32_t sh;
+  uint64_t cur, nxt;
+  int b;
+  uint64_t mask;
+  __device__ __forceinline__ void init(const Ld& l, int64_t pos, int bb) {
+    ld = l;
+    b = bb;
+    mask = (1ull << bb) - 1;
+    idx = pos >> 6;
+    sh = uint32_t(pos & 63);
+    cur = ld(idx);
+    nxt = ld(idx + 1);
+  }
+  __device__ __forceinline__ uint64_t next() {
+    uint64_t w = sh ? ((cur >> sh) | (nxt << (64 - sh))) : cur;
+    sh += b;
+    if (sh >= 64) {
+      sh -= 64;
+      cur = nxt;
+      ++idx;
+      nxt = ld(idx + 1);
+    }
+    return w & mask;
+  }
+};
+
+struct GlobalLimbs {
+  const uint64_t* limbs;
+  int64_t nlimbs;
+  __device__ __forceinline__ uint64_t operator()(int64_t i) const {
+    return (i >= 0 && i < nlimbs) ? __ldg(limbs + i) : 0ull;
+  }
+};
+
+
 // Transfer code of a chunk for the balanced-split carry chain
 // (split.cpp:88-95): generate if window > 2^{b-1}, propagate if equal.
 __device__ __forceinline__ uint32_t split_tf(uint64_t w, int b) {

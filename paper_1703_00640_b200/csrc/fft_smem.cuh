@@ -277,6 +277,31 @@ __device__ __forceinline__ void fft_pass(double2* __restrict__ buf, const Lay& l
   }
 }
 
+// Whole transform in shared memory with one radix dispatch per stage: the
+// code holds each radix's load / twiddle / DFT / store once (the fft_pass
+// form inlines them separately for the first, middle and last stage of each
+// source and sink type).  Expects the data in buf and a barrier before the
+// call; ends with a barrier.
+template <bool INV, class Lay, class TW>
+__device__ __forceinline__ void fft_smem_compact(double2* __restrict__ buf, const Lay lay,
+                                              const SubFft& p, const TW tw, int tid, int nthr) {
+  double2 x[kXMax];
+  const SmemSrc<Lay> ssrc{buf, lay};
+  const SmemSink<Lay> ssink{buf, lay};
+  for (int s = 0; s < p.nst; ++s) {
+    const uint32_t Ns = p.Ns[s];
+    const auto twq = tw.stage(p, s);
+    const FastDiv fd = p.fdNs[s];
+#define TMG_ST(RR)                                                              \
+  stage_load<RR>(x, lay, p.R, ssrc, tid, nthr);                                 \
+  __syncthreads();                                                              \
+  stage_store<RR, INV>(x, lay, p.R, Ns, fd, twq, ssink, tid, nthr);             \
+  __syncthreads();
+    TMG_RADIX_SWITCH(p.rad[s], TMG_ST)
+#undef TMG_ST
+  }
+}
+
 // Whole transform in shared memory (natural order in and out), ends with a
 // barrier.
 template <bool INV, class Lay, class TW>

@@ -17,46 +17,6 @@
 
 namespace tmg {
 
-// ---------------------------------------------------------------------------
-// Sequential reader of consecutive b-bit windows of u * 2^lead.
-template <class Ld>
-struct WindowReader {
-  Ld ld;
-  int64_t idx;
-  uint32_t sh;
-  uint64_t cur, nxt;
-  int b;
-  uint64_t mask;
-  __device__ __forceinline__ void init(const Ld& l, int64_t pos, int bb) {
-    ld = l;
-    b = bb;
-    mask = (1ull << bb) - 1;
-    idx = pos >> 6;
-    sh = uint32_t(pos & 63);
-    cur = ld(idx);
-    nxt = ld(idx + 1);
-  }
-  __device__ __forceinline__ uint64_t next() {
-    uint64_t w = sh ? ((cur >> sh) | (nxt << (64 - sh))) : cur;
-    sh += b;
-    if (sh >= 64) {
-      sh -= 64;
-      cur = nxt;
-      ++idx;
-      nxt = ld(idx + 1);
-    }
-    return w & mask;
-  }
-};
-
-struct GlobalLimbs {
-  const uint64_t* limbs;
-  int64_t nlimbs;
-  __device__ __forceinline__ uint64_t operator()(int64_t i) const {
-    return (i >= 0 && i < nlimbs) ? __ldg(limbs + i) : 0ull;
-  }
-};
-
 struct SmemLimbs {
   const uint64_t* s;  // s[i - i0] for i in [i0, i0 + n)
   int64_t i0, n;
@@ -179,6 +139,41 @@ struct F1Sink {
   }
 };
 
+// Tile <-> shared memory copies of a column pass: element (item, e) of the
+// R x c tile, consecutive threads on consecutive items (columns) so each
+// warp touches c-element row segments; 8 transfers per thread in flight.
+template <class Lay, class Src>
+__device__ __forceinline__ void tile_load(double2* __restrict__ buf, const Lay& lay, uint32_t R,
+                                          uint32_t c, const Src& src, int tid, int nthr) {
+  const uint32_t n = R * c, lc = 31 - __clz(c);
+  constexpr int U = 8;
+  uint32_t i = tid;
+  for (; i + (U - 1) * nthr < n; i += U * nthr) {
+    double2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t t = i + u * nthr;
+      v[u] = src(t & (c - 1), t >> lc);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t t = i + u * nthr;
+      buf[lay.idx(t & (c - 1), t >> lc)] = v[u];
+    }
+  }
+  for (; i < n; i += nthr) buf[lay.idx(i & (c - 1), i >> lc)] = src(i & (c - 1), i >> lc);
+}
+template <class Lay, class Sink>
+__device__ __forceinline__ void tile_store(const double2* __restrict__ buf, const Lay& lay,
+                                           uint32_t R, uint32_t c, const Sink& sink, int tid,
+                                           int nthr) {
+  const uint32_t n = R * c, lc = 31 - __clz(c);
+  for (uint32_t i = tid; i < n; i += nthr) {
+    const uint32_t item = i & (c - 1), e = i >> lc;
+    sink(item, e, buf[lay.idx(item, e)]);
+  }
+}
+
 size_t f1_smem_bytes(uint32_t A, uint32_t c) {
   return size_t(padded_len(A * c)) * 16 + size_t(A) * 16;  // data + stage table (< A)
 }
@@ -205,10 +200,12 @@ k_f1(F1Args a) {
     auto Dv = [&](int64_t i) { return digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, i, mc.balanced != 0); };
     a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
   }
+  // tile -> shared memory: all loads of a thread in flight together
+  const ZSrc src{a.z, N, a.ncols, col0, &a.mc, topu, topv};
+  tile_load(sbuf, lay, A, c, src, tid, nthr);
   __syncthreads();
-  const int64_t Nz = (mc.mode == kModeFull) ? N : N;  // z holds N entries
-  fft_pass<false>(sbuf, lay, a.fft, tw, ZSrc{a.z, Nz, a.ncols, col0, &a.mc, topu, topv},
-                  F1Sink{a.out, a.ncols, col0, a.tw}, tid, nthr);
+  fft_smem_compact<false>(sbuf, lay, a.fft, tw, tid, nthr);
+  tile_store(sbuf, lay, A, c, F1Sink{a.out, a.ncols, col0, a.tw}, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
@@ -229,8 +226,11 @@ k_col(ColArgs a) {
   __syncthreads();
   ColSrc src{a.data, a.g, outer, col0};
   ColSink sink{a.data, a.g, outer, col0, a.tw, a.to, a.tc, a.tmul, a.inv != 0, true};
-  if (a.inv) fft_pass<true>(sbuf, lay, a.fft, tw, src, sink, tid, nthr);
-  else fft_pass<false>(sbuf, lay, a.fft, tw, src, sink, tid, nthr);
+  tile_load(sbuf, lay, a.fft.R, c, src, tid, nthr);
+  __syncthreads();
+  if (a.inv) fft_smem_compact<true>(sbuf, lay, a.fft, tw, tid, nthr);
+  else fft_smem_compact<false>(sbuf, lay, a.fft, tw, tid, nthr);
+  tile_store(sbuf, lay, a.fft.R, c, sink, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
@@ -414,9 +414,10 @@ k_ilast(ILastArgs a) {
   const uint32_t col0 = blockIdx.x * c;
   LayCols lay{a.logc, c - 1};
   const TwStage tw = load_tw_stage(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
+  tile_load(sbuf, lay, a.fft.R, c, ColSrc{a.data, a.g, 0, col0}, tid, nthr);
   __syncthreads();
-  fft_pass<true>(sbuf, lay, a.fft, tw, ColSrc{a.data, a.g, 0, col0},
-                 CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
+  fft_smem_compact<true>(sbuf, lay, a.fft, tw, tid, nthr);
+  tile_store(sbuf, lay, a.fft.R, c, CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------

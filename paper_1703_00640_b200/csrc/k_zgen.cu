@@ -1,9 +1,11 @@
 // Balanced split + pre-map as one streaming pass (both operands at once).
 //
-// A block owns kZgenChunks consecutive chunks.  It stages the limbs under
-// them (coalesced), derives every chunk's carry status, resolves the carry
-// into the block with a warp-parallel decoupled look-back over the paired
-// (u, v) chains, writes the balanced digits to shared memory (plus the
+// A block owns kZgenChunks consecutive chunks.  It stages the operand bits
+// under them in shared memory (coalesced; 32-bit words when b <= 32 so each
+// b-bit window is one funnel shift), takes every window once into
+// registers, derives the chunks' carry statuses, resolves the carry into the
+// block from the per-block aggregates of k_zstat (composed in parallel, no
+// look-back wait), writes the balanced digits to shared memory (plus the
 // first lambda-1 digits of the next block, whose carry it now knows), and
 // emits the pre-mapped coefficients z_j = (alpha*U)_j + i (alpha*V)_j (gamma+
 // without its top-coefficient fold for the high product; the full product
@@ -15,39 +17,109 @@
 // 317-348 (alpha*, gamma+).
 #include "kernels.cuh"
 
+#include <type_traits>
+
 namespace tmg {
 
 namespace {
 
-struct StagedLimbs {
-  const uint64_t* s;
-  int64_t i0, n;
-  __device__ __forceinline__ uint64_t operator()(int64_t i) const {
-    const int64_t o = i - i0;
-    return (o >= 0 && o < n) ? s[o] : 0ull;
+// Operand bits as a shared-memory array of W-bit words (W = 32 or 64)
+// starting at word wbase (words outside the operand read as zero).
+template <bool W32>
+struct StagedBits {
+  using Word = typename std::conditional<W32, uint32_t, uint64_t>::type;
+  static constexpr int kW = W32 ? 32 : 64;
+  static constexpr int kLog = W32 ? 5 : 6;
+  const Word* s;
+  // b-bit window at bit offset rel (>= 0) from the first staged word
+  __device__ __forceinline__ uint64_t window(uint32_t rel, uint64_t mask) const {
+    const uint32_t wi = rel >> kLog, sh = rel & (kW - 1);
+    if constexpr (W32) {
+      return uint64_t(__funnelshift_r(s[wi], s[wi + 1], sh)) & mask;
+    } else {
+      const uint64_t lo = s[wi], hi = s[wi + 1];
+      return (sh ? ((lo >> sh) | (hi << (64 - sh))) : lo) & mask;
+    }
   }
 };
 
-__device__ __forceinline__ uint64_t window_at(const StagedLimbs& L, int64_t pos, int b) {
-  const int64_t idx = pos >> 6;
-  const uint32_t sh = uint32_t(pos & 63);
-  const uint64_t lo = L(idx), hi = L(idx + 1);
-  const uint64_t w = sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
-  return w & ((1ull << b) - 1);
+template <bool W32>
+__device__ __forceinline__ typename StagedBits<W32>::Word load_word(const uint64_t* limbs,
+                                                                    int64_t nlimbs,
+                                                                    int64_t wi) {
+  if constexpr (W32) {
+    return (wi >= 0 && wi < 2 * nlimbs) ? __ldg(reinterpret_cast<const uint32_t*>(limbs) + wi)
+                                        : 0u;
+  } else {
+    return (wi >= 0 && wi < nlimbs) ? __ldg(limbs + wi) : 0ull;
+  }
+}
+
+// Staged words per operand: the chunks of one block plus the lambda-1 digits
+// of the next, the sub-word offset and one word of look-ahead.
+__host__ __device__ inline int64_t zgen_words(int b, int kw) {
+  return (int64_t(kZgenChunks + kMaxLambda) * b + kw - 1) / kw + 3;
 }
 
 }  // namespace
 
 size_t zgen_smem(int b) {
-  const size_t nl = size_t((int64_t(kZgenChunks + kMaxLambda) * b + 63) / 64 + 3);
-  return 2 * nl * 8 + size_t(2) * (kZgenChunks + kMaxLambda) * 4 + 64;
+  const int kw = b <= 32 ? 32 : 64;
+  return 2 * size_t(zgen_words(b, kw)) * (kw / 8) + size_t(2) * (kZgenChunks + kMaxLambda) * 4 +
+         64;
 }
 
+// Carry transfer function of each block of kZgenChunks chunks for both
+// operands' balanced-split chains (split.cpp:88-95).  A chunk whose window
+// differs from 2^{b-1} decides its carry-out (1 above, 0 below) whatever
+// comes in, so a block's aggregate is fixed by its last such chunk: one
+// thread per block searches backwards from the block's end (one window for
+// random operands; the whole block only when every window equals 2^{b-1}).
+__global__ void __launch_bounds__(256)
+k_zstat(ZgenArgs a) {
+  const int64_t blk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t count = a.count;
+  const int64_t nblk = (count + kZgenChunks - 1) / kZgenChunks;
+  if (blk >= nblk) return;
+  const int b = a.b;
+  const uint64_t half = 1ull << (b - 1);
+  const int64_t c0 = blk * kZgenChunks;
+  // statuses exist for chunks below the (unbalanced) top chunk only
+  const int64_t c1 = min(count - 1, c0 + kZgenChunks);
+  uint32_t fu = kTfIdentity, fv = kTfIdentity;
+  if (a.mc.balanced) {
+    bool du = false, dv = false;
+    for (int64_t j = c1 - 1; j >= c0 && !(du && dv); --j) {
+      const int64_t pos = j * b - a.lead;
+      if (!du) {
+        const uint64_t w = window_bits(a.u, a.nlimbs, pos, b);
+        if (w != half) {
+          fu = tf_const(w > half ? 1 : 0);
+          du = true;
+        }
+      }
+      if (!dv) {
+        const uint64_t w = window_bits(a.v, a.nlimbs, pos, b);
+        if (w != half) {
+          fv = tf_const(w > half ? 1 : 0);
+          dv = true;
+        }
+      }
+    }
+  } else {
+    fu = fv = tf_const(0);
+  }
+  a.aggs[blk] = tf2_pack(fu, fv);
+}
+
+template <bool W32>
 __global__ void __launch_bounds__(kZgenThreads)
-k_zgen(ZgenArgs a) {
+k_zgen_t(ZgenArgs a) {
+  using SB = StagedBits<W32>;
+  using Word = typename SB::Word;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t sw[32];
-  __shared__ uint32_t s_blk, s_cin;
+  __shared__ uint32_t s_cin;
   __shared__ int32_t s_wrap[2][kMaxLambda];
   const int tid = threadIdx.x;
   const MapConsts& mc = a.mc;
@@ -56,24 +128,21 @@ k_zgen(ZgenArgs a) {
   const int64_t count = a.count;
   const int lam = (mc.mode == kModeFull) ? 1 : mc.lambda;
   const int ext = lam - 1;
-  const int64_t nl = (int64_t(kZgenChunks + kMaxLambda) * b + 63) / 64 + 3;
-  uint64_t* slu = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* slv = slu + nl;
-  int32_t* digu = reinterpret_cast<int32_t*>(slv + nl);
+  const int64_t nwd = zgen_words(b, SB::kW);
+  Word* su = reinterpret_cast<Word*>(smem_raw);
+  Word* sv = su + nwd;
+  int32_t* digu = reinterpret_cast<int32_t*>(sv + nwd);
   int32_t* digv = digu + (kZgenChunks + kMaxLambda);
 
-  if (tid == 0) s_blk = uint32_t(atomicAdd(a.scan.ctr, 1ull));
-  __syncthreads();
-  const uint32_t blk = s_blk;
+  const uint32_t blk = blockIdx.x;
   const int64_t c0 = int64_t(blk) * kZgenChunks;
-  const int64_t c1 = min(count, c0 + kZgenChunks);
-  const int64_t pos0 = c0 * b - a.lead;
-  const int64_t i0 = pos0 >> 6;
-  for (int64_t i = tid; i < nl; i += kZgenThreads) {
-    const int64_t g = i0 + i;
-    const bool in = g >= 0 && g < a.nlimbs;
-    slu[i] = in ? __ldg(a.u + g) : 0ull;
-    slv[i] = in ? __ldg(a.v + g) : 0ull;
+  const int64_t c1 = min(count, c0 + int64_t(kZgenChunks));
+  const int64_t bit0 = c0 * b - a.lead;
+  const int64_t wbase = bit0 >> SB::kLog;  // floor, bit0 may be negative
+  const uint32_t off0 = uint32_t(bit0 - (wbase << SB::kLog));
+  for (int64_t i = tid; i < nwd; i += kZgenThreads) {
+    su[i] = load_word<W32>(a.u, a.nlimbs, wbase + i);
+    sv[i] = load_word<W32>(a.v, a.nlimbs, wbase + i);
   }
   // digits of chunks 0 .. lam-2 (the wrap of the cyclic pre-map), carry 0 in
   if (tid == 0 && mc.mode != kModeFull && c1 + ext > N) {
@@ -88,22 +157,32 @@ k_zgen(ZgenArgs a) {
     }
   }
   __syncthreads();
-  const StagedLimbs Lu{slu, i0, nl}, Lv{slv, i0, nl};
+  const SB Lu{su}, Lv{sv};
   const uint64_t half = 1ull << (b - 1);
+  const uint64_t mask = (1ull << b) - 1;
 
-  // statuses of this thread's kZgenPer chunks
-  const int64_t t0 = c0 + int64_t(tid) * kZgenPer;
-  uint32_t gu = 0, pu = 0, gv = 0, pv = 0;
+  // this thread's kZgenPer windows, taken once
+  const uint32_t q0 = uint32_t(tid) * kZgenPer;  // chunk offset in the block
+  const int64_t t0 = c0 + q0;
+  using Win = typename std::conditional<W32, uint32_t, uint64_t>::type;
+  Win wu[kZgenPer], wv[kZgenPer];
 #pragma unroll
   for (int q = 0; q < kZgenPer; ++q) {
-    const int64_t j = t0 + q;
-    if (j < c1 && j < count - 1 && mc.balanced) {
-      const uint64_t wu = window_at(Lu, j * b - a.lead, b);
-      const uint64_t wv = window_at(Lv, j * b - a.lead, b);
-      gu |= uint32_t(wu > half) << q;
-      pu |= uint32_t(wu == half) << q;
-      gv |= uint32_t(wv > half) << q;
-      pv |= uint32_t(wv == half) << q;
+    const uint32_t rel = off0 + (q0 + q) * uint32_t(b);
+    wu[q] = Win(Lu.window(rel, mask));
+    wv[q] = Win(Lv.window(rel, mask));
+  }
+  uint32_t gu = 0, pu = 0, gv = 0, pv = 0;
+  if (mc.balanced) {
+#pragma unroll
+    for (int q = 0; q < kZgenPer; ++q) {
+      const int64_t j = t0 + q;
+      if (j < c1 && j < count - 1) {
+        gu |= uint32_t(wu[q] > half) << q;
+        pu |= uint32_t(wu[q] == half) << q;
+        gv |= uint32_t(wv[q] > half) << q;
+        pv |= uint32_t(wv[q] == half) << q;
+      }
     }
   }
   auto agg_of = [](uint32_t g, uint32_t p) -> uint32_t {
@@ -114,9 +193,16 @@ k_zgen(ZgenArgs a) {
   };
   uint32_t agg2;
   const uint32_t ex2 = block_scan_tf2(tf2_pack(agg_of(gu, pu), agg_of(gv, pv)), sw, &agg2);
-  if (tid < 32) {
-    const uint32_t cin = lookback_warp2(a.scan.state, blk, agg2, a.scan.epoch, 5u);
-    if (tid == 0) s_cin = cin;
+  // carry into the block: the aggregates of the blocks before it (k_zstat),
+  // composed in order by the whole block
+  {
+    uint32_t g = kTf2Identity;
+    const uint32_t Q = (blk + kZgenThreads - 1) / kZgenThreads;
+    const uint32_t i0 = uint32_t(tid) * Q, i1 = min(blk, i0 + Q);
+    for (uint32_t i = i0; i < i1; ++i) g = tf2_compose(g, __ldg(a.aggs + i));
+    uint32_t pre;
+    (void)block_scan_tf2(g, sw, &pre);
+    if (tid == 0) s_cin = tf2_apply(pre, 5u);  // both chains start with carry 0
   }
   __syncthreads();
   const uint32_t cc = tf2_apply(ex2, s_cin);
@@ -130,10 +216,9 @@ k_zgen(ZgenArgs a) {
     if (j < c1) {
       bu |= uint32_t(cu) << q;
       bv |= uint32_t(cv) << q;
-      const uint64_t wu = window_at(Lu, j * b - a.lead, b);
-      const uint64_t wv = window_at(Lv, j * b - a.lead, b);
-      digu[j - c0] = int32_t(split_digit(wu, cu, b, j == count - 1 || !mc.balanced));
-      digv[j - c0] = int32_t(split_digit(wv, cv, b, j == count - 1 || !mc.balanced));
+      const bool top = j == count - 1 || !mc.balanced;
+      digu[q0 + q] = int32_t(split_digit(wu[q], cu, b, top));
+      digv[q0 + q] = int32_t(split_digit(wv[q], cv, b, top));
       if (!((pu >> q) & 1u)) cu = int((gu >> q) & 1u);
       if (!((pv >> q) & 1u)) cv = int((gv >> q) & 1u);
     }
@@ -143,12 +228,13 @@ k_zgen(ZgenArgs a) {
     for (int q = 0; q < ext; ++q) {
       const int64_t j = c1 + q;
       if (j >= N) break;
-      const uint64_t wu = window_at(Lu, j * b - a.lead, b);
-      const uint64_t wv = window_at(Lv, j * b - a.lead, b);
-      digu[j - c0] = int32_t(split_digit(wu, cu, b, j == count - 1 || !mc.balanced));
-      digv[j - c0] = int32_t(split_digit(wv, cv, b, j == count - 1 || !mc.balanced));
-      cu = mc.balanced ? tf_apply(split_tf(wu, b), cu) : 0;
-      cv = mc.balanced ? tf_apply(split_tf(wv, b), cv) : 0;
+      const uint32_t rel = off0 + uint32_t(j - c0) * uint32_t(b);
+      const uint64_t xu = Lu.window(rel, mask), xv = Lv.window(rel, mask);
+      const bool top = j == count - 1 || !mc.balanced;
+      digu[j - c0] = int32_t(split_digit(xu, cu, b, top));
+      digv[j - c0] = int32_t(split_digit(xv, cv, b, top));
+      cu = mc.balanced ? tf_apply(split_tf(xu, b), cu) : 0;
+      cv = mc.balanced ? tf_apply(split_tf(xv, b), cv) : 0;
     }
   }
   {
@@ -165,13 +251,6 @@ k_zgen(ZgenArgs a) {
       atomicOr(&a.status->flags, uint32_t(kFlagInputRange));
   }
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(a.scan.ctr + 1, 1ull) == gridDim.x - 1) {
-      a.scan.ctr[0] = 0;
-      a.scan.ctr[1] = 0;
-    }
-  }
 
   // outputs
   const int64_t ce = min(c1, N);
@@ -182,27 +261,34 @@ k_zgen(ZgenArgs a) {
   }
   const double Nd = double(N);
   const int fam = (mc.mode == kModeLow) ? 0 : 2;
-  auto Du = [&](int64_t i) -> double {
-    return (i < N) ? double(digu[i - c0]) : double(s_wrap[0][i - N]);
-  };
-  auto Dv = [&](int64_t i) -> double {
-    return (i < N) ? double(digv[i - c0]) : double(s_wrap[1][i - N]);
-  };
-  for (int64_t j = c0 + ext + tid; j < ce + ext; j += kZgenThreads) {
+  const int32_t nloc = int32_t(ce - c0);  // local chunks with a digit in this block
+  const int32_t nN = int32_t(N - c0);     // local index of chunk N (wrap start)
+  for (int32_t jl = ext + tid; jl < nloc + ext; jl += kZgenThreads) {
     double au = 0.0, av = 0.0;
+    const double jd = double(c0 + jl);
     RowLoopDown<kMaxLambda>::run([&](auto rc) {
       constexpr int r = decltype(rc)::value;
       if (r < lam) {
-        const int64_t i = j - r;  // chunk, in [c0, c1 + ext)
-        int64_t k = i;
-        if (k >= N) k -= N;
-        const double cf = coef_r<r>(fam, double(k), Nd, mc.cpre[r]);
-        au += Du(i) * cf;
-        av += Dv(i) * cf;
+        const int32_t il = jl - r;  // local chunk, in [0, nloc + ext)
+        double du, dv, kd = jd - double(r);
+        if (il < nN) {
+          du = double(digu[il]);
+          dv = double(digv[il]);
+        } else {
+          du = double(s_wrap[0][il - nN]);
+          dv = double(s_wrap[1][il - nN]);
+          kd -= Nd;
+        }
+        const double cf = coef_r<r>(fam, kd, Nd, mc.cpre[r]);
+        au += du * cf;
+        av += dv * cf;
       }
     });
+    const int64_t j = c0 + jl;
     a.z[j >= N ? j - N : j] = make_double2(au, av);
   }
 }
+
+ZgenFn zgen_kernel(int b) { return b <= 32 ? k_zgen_t<true> : k_zgen_t<false>; }
 
 }  // namespace tmg

@@ -75,11 +75,14 @@ struct ZgenArgs {
   MapConsts mc;
   ScanState scan;
   DevStatus* status;
+  uint32_t* aggs;  // per-block carry transfer functions (k_zstat)
 };
 constexpr int kZgenThreads = 256;
 constexpr int kZgenPer = 16;
 constexpr int kZgenChunks = kZgenThreads * kZgenPer;
-__global__ void k_zgen(ZgenArgs a);
+__global__ void k_zstat(ZgenArgs a);
+typedef void (*ZgenFn)(ZgenArgs);
+ZgenFn zgen_kernel(int b);
 size_t zgen_smem(int b);
 
 // F1: forward column DFTs over A of the pre-mapped coefficients.
