@@ -116,6 +116,18 @@ void spectral_scale(int64_t L, double* hi, double* lo) {
   *lo = double(v - (long double)(*hi));
 }
 
+// z layout shared by k_zgen (writer) and k_f1 (reader).
+ZTile ztile(const Plan& pl, int64_t L) {
+  static const bool natural = getenv("TMG_Z_NATURAL") != nullptr;
+  ZTile t;
+  const uint32_t ncols = uint32_t(L / pl.A);
+  t.fdcols = make_fastdiv(ncols);
+  t.logc = pl.logc_f1;
+  t.zrows = uint32_t((pl.params.N + ncols - 1) / ncols);
+  t.natural = natural ? 1u : 0u;
+  return t;
+}
+
 
 bool g_debug_sync = getenv("TMG_DEBUG_SYNC") != nullptr;
 
@@ -204,7 +216,8 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
   const int64_t L = pl.L;
   cx.work_t.ensure(size_t(L) * 16);
   cx.work_c.ensure(size_t(L) * 8 + 64);
-  cx.work_z.ensure(size_t(p.N) * 16 + 64);
+  // z: N entries, plus up to one row of F1's tiling slack (ZTile)
+  cx.work_z.ensure((size_t(p.N) + (pl.kind >= 2 ? size_t(L / pl.A) : 0)) * 16 + 64);
   const int64_t cwords = (pl.count + 31) / 32 + 1;
   cx.cbu.ensure(size_t(cwords) * 4);
   cx.cbv.ensure(size_t(cwords) * 4);
@@ -229,6 +242,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.cbits_v = cx.cbv.as<uint32_t>();
       a.z = cx.work_z.as<double2>();
       a.mc = pl.mc;
+      a.zt = ztile(pl, L);
       const unsigned blocks = unsigned((pl.count + kZgenChunks - 1) / kZgenChunks);
       a.scan = cx.scan_u.next(blocks);
       a.status = status;
@@ -252,6 +266,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     {
       F1Args a;
       a.z = cx.work_z.as<double2>();
+      a.zt = ztile(pl, L);
       a.out = T;
       a.ncols = uint32_t(L / pl.A);
       a.logc = pl.logc_f1;
@@ -311,7 +326,16 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       spectral_scale(L, &a.scale, &a.scale_lo);
       const unsigned npairs = (pl.A * pl.B) / 2 + 1;
       static const bool no_ct = getenv("TMG_NO_CT") != nullptr;
-      if (pl.C == 4096 && pl.mid_shared_table && !no_ct) {
+      static const bool mid8 = getenv("TMG_MID8") != nullptr;
+      if (pl.C == 4096 && pl.mid8_ok && mid8 && !no_ct) {
+        a.fwd = pl.fC8;
+        a.inv = pl.iC8;
+        const size_t sm8 = mid_smem_bytes(4096, 0);
+        set_smem(k_mid_4096_r8, sm8);
+        const unsigned grid = std::min<unsigned>(npairs, unsigned(cx.num_sms));
+        KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode));
+        k_mid_4096_r8<<<grid, kMid8Threads, sm8, st>>>(a);
+      } else if (pl.C == 4096 && pl.mid_shared_table && !no_ct) {
         // compile-time schedule, persistent over row pairs
         set_smem(k_mid_4096, pl.smem_mid);
         const unsigned grid = std::min<unsigned>(npairs, unsigned(cx.num_sms));

@@ -90,6 +90,12 @@ struct ColSink {
     }
     data[col_off(g, outer, k, col)] = v;
   }
+  __device__ __forceinline__ double2 pre(uint32_t item, uint32_t k) const {
+    return tw.get((uint32_t(outer) * to + (col0 + item) * tc) * k * tmul);
+  }
+  __device__ __forceinline__ void put(uint32_t item, uint32_t k, double2 v, double2 w) const {
+    data[col_off(g, outer, k, col0 + item)] = inv ? cmulc(v, w) : cmul(v, w);
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -99,6 +105,7 @@ struct ColSink {
 // store T[k_a][col].
 struct ZSrc {
   const double2* z;
+  ZTile zt;
   int64_t N;
   uint32_t ncols, col0;
   const MapConsts* mc;
@@ -106,7 +113,8 @@ struct ZSrc {
   __device__ __forceinline__ double2 operator()(uint32_t item, uint32_t e) const {
     const int64_t j = int64_t(e) * ncols + col0 + item;
     if (j >= N) return make_double2(0.0, 0.0);
-    double2 v = z[j];
+    // tile of this CTA: rows consecutive, 2^logc columns per row
+    double2 v = zt.natural ? z[j] : z[((col0 >> zt.logc) * zt.zrows + e) * (1u << zt.logc) + item];
     if (mc->mode == kModeHigh && j < mc->nfold + mc->lambda) {
       // gamma-dagger fold of the top coefficient (maps_f64.cpp:337-347)
       const int lam = mc->lambda;
@@ -137,6 +145,13 @@ struct F1Sink {
     if (x) v = cmul(v, tw.get(x));
     out[int64_t(k) * ncols + col] = v;
   }
+  // omega^0 = (1, 0) exactly, so x = 0 multiplies exactly
+  __device__ __forceinline__ double2 pre(uint32_t item, uint32_t k) const {
+    return tw.get((col0 + item) * k);
+  }
+  __device__ __forceinline__ void put(uint32_t item, uint32_t k, double2 v, double2 w) const {
+    out[int64_t(k) * ncols + col0 + item] = cmul(v, w);
+  }
 };
 
 // Tile <-> shared memory copies of a column pass: element (item, e) of the
@@ -163,16 +178,48 @@ __device__ __forceinline__ void tile_load(double2* __restrict__ buf, const Lay& 
   }
   for (; i < n; i += nthr) buf[lay.idx(i & (c - 1), i >> lc)] = src(i & (c - 1), i >> lc);
 }
+// Sinks with a twiddle expose pre(item, e) (the twiddle, fetched early) and
+// put(item, e, v, w); the store loop keeps 8 elements' fetches in flight.
+template <class Sink>
+struct TileSinkPre {
+  static constexpr bool value = false;
+};
 template <class Lay, class Sink>
 __device__ __forceinline__ void tile_store(const double2* __restrict__ buf, const Lay& lay,
                                            uint32_t R, uint32_t c, const Sink& sink, int tid,
                                            int nthr) {
   const uint32_t n = R * c, lc = 31 - __clz(c);
-  for (uint32_t i = tid; i < n; i += nthr) {
+  constexpr int U = 8;
+  uint32_t i = tid;
+  for (; i + (U - 1) * nthr < n; i += U * nthr) {
+    double2 v[U], w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t t = i + u * nthr;
+      v[u] = buf[lay.idx(t & (c - 1), t >> lc)];
+      if constexpr (TileSinkPre<Sink>::value) w[u] = sink.pre(t & (c - 1), t >> lc);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t t = i + u * nthr;
+      if constexpr (TileSinkPre<Sink>::value) sink.put(t & (c - 1), t >> lc, v[u], w[u]);
+      else sink(t & (c - 1), t >> lc, v[u]);
+    }
+  }
+  for (; i < n; i += nthr) {
     const uint32_t item = i & (c - 1), e = i >> lc;
     sink(item, e, buf[lay.idx(item, e)]);
   }
 }
+
+template <>
+struct TileSinkPre<F1Sink> {
+  static constexpr bool value = true;
+};
+template <>
+struct TileSinkPre<ColSink> {
+  static constexpr bool value = true;
+};
 
 size_t f1_smem_bytes(uint32_t A, uint32_t c) {
   return size_t(padded_len(A * c)) * 16 + size_t(A) * 16;  // data + stage table (< A)
@@ -201,7 +248,7 @@ k_f1(F1Args a) {
     a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
   }
   // tile -> shared memory: all loads of a thread in flight together
-  const ZSrc src{a.z, N, a.ncols, col0, &a.mc, topu, topv};
+  const ZSrc src{a.z, a.zt, N, a.ncols, col0, &a.mc, topu, topv};
   tile_load(sbuf, lay, A, c, src, tid, nthr);
   __syncthreads();
   fft_smem_compact<false>(sbuf, lay, a.fft, tw, tid, nthr);
@@ -320,12 +367,10 @@ k_mid(MidArgs a) {
 // per SM, the row pair fills shared memory), the stage table staged once per
 // CTA, and the next pair's two rows prefetched into L2 while the current
 // pair computes, so the first stage's loads do not wait on HBM.
-template <int NTHR>
+template <int NTHR, class Fwd, class Inv>
 __device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restrict__ sbuf,
                                               const double2* __restrict__ stab, uint32_t r0,
                                               int tid) {
-  using Fwd = Sched<16, 16, 16>;
-  using Inv = Sched<16, 16, 8>;
   constexpr uint32_t C = 4096, H = 2048;
   const uint32_t AB = a.A * a.B;
   const uint32_t r1 = (AB - r0) % AB;
@@ -368,8 +413,8 @@ __device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restr
                                 RowSink{a.data, base0, base1, r0, r1, a.tw}, tid);
 }
 
-__global__ void __launch_bounds__(kMidCtThreads)
-k_mid_4096(MidArgs a) {
+template <int NTHR, class Fwd, class Inv>
+__device__ __forceinline__ void mid_4096_body(const MidArgs& a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x;
@@ -377,7 +422,7 @@ k_mid_4096(MidArgs a) {
   const uint32_t AB = a.A * a.B;
   const uint32_t npairs = AB / 2 + 1;
   double2* stw = sbuf + 2 * (padded_len(C) + 4);
-  for (uint32_t i = tid; i < a.fwd.stablen; i += kMidCtThreads) stw[i] = __ldg(a.fwd.stab + i);
+  for (uint32_t i = tid; i < a.fwd.stablen; i += NTHR) stw[i] = __ldg(a.fwd.stab + i);
   auto row_base = [&](uint32_t r) {
     return a.data + (int64_t(r % a.A) * a.B + (r / a.A)) * int64_t(C);
   };
@@ -392,8 +437,20 @@ k_mid_4096(MidArgs a) {
       prefetch_l2(row_base(nx), C * 16);
       prefetch_l2(row_base((AB - nx) % AB), C * 16);
     }
-    mid_pair_4096<kMidCtThreads>(a, sbuf, stw, r0, tid);
+    mid_pair_4096<NTHR, Fwd, Inv>(a, sbuf, stw, r0, tid);
   }
+}
+
+__global__ void __launch_bounds__(kMidCtThreads)
+k_mid_4096(MidArgs a) {
+  mid_4096_body<kMidCtThreads, Sched<16, 16, 16>, Sched<16, 16, 8>>(a);
+}
+
+// 32-warp variant: radix-8 schedules (4096 = 8^4, 2048 = 8 x 8 x 8 x 4),
+// one butterfly of at most 8 values per thread and stage, 64 registers.
+__global__ void __launch_bounds__(kMid8Threads)
+k_mid_4096_r8(MidArgs a) {
+  mid_4096_body<kMid8Threads, Sched<8, 8, 8, 8>, Sched<8, 8, 8, 4>>(a);
 }
 
 // ---------------------------------------------------------------------------

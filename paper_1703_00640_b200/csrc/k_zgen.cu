@@ -256,7 +256,7 @@ k_zgen_t(ZgenArgs a) {
   const int64_t ce = min(c1, N);
   if (mc.mode == kModeFull) {
     for (int64_t j = c0 + tid; j < ce; j += kZgenThreads)
-      a.z[j] = make_double2(double(digu[j - c0]), double(digv[j - c0]));
+      a.z[a.zt.index(uint32_t(j))] = make_double2(double(digu[j - c0]), double(digv[j - c0]));
     return;
   }
   const double Nd = double(N);
@@ -285,7 +285,7 @@ k_zgen_t(ZgenArgs a) {
       }
     });
     const int64_t j = c0 + jl;
-    a.z[j >= N ? j - N : j] = make_double2(au, av);
+    a.z[a.zt.index(uint32_t(j >= N ? j - N : j))] = make_double2(au, av);
   }
 }
 

@@ -59,6 +59,25 @@ struct ColGeom {
   uint32_t ncols;  // columns per outer matrix
 };
 
+// Layout of the pre-mapped coefficients z (N entries): element
+// j = row * ncols + col sits in the tile of k_f1's CTA that owns col --
+// tiles of 2^logc columns x zrows rows, row-major inside the tile -- so the
+// first column pass reads its whole tile contiguously.  zrows = ceil(N /
+// ncols) (the full product's upper half is zero and not stored).  natural
+// keeps z[j] at j (diagnostics).
+struct ZTile {
+  FastDiv fdcols;  // division by ncols
+  uint32_t logc;
+  uint32_t zrows;
+  uint32_t natural;
+  __device__ __forceinline__ uint32_t index(uint32_t j) const {
+    if (natural) return j;
+    const uint32_t row = fdiv(j, fdcols);
+    const uint32_t col = j - row * fdcols.d;
+    return ((col >> logc) * zrows + row) * (1u << logc) + (col & ((1u << logc) - 1));
+  }
+};
+
 // Balanced split + pre-map of both operands (k_zgen.cu).
 struct ZgenArgs {
   const uint64_t* u;
@@ -76,6 +95,7 @@ struct ZgenArgs {
   ScanState scan;
   DevStatus* status;
   uint32_t* aggs;  // per-block carry transfer functions (k_zstat)
+  ZTile zt;        // layout of z as k_f1 reads it
 };
 constexpr int kZgenThreads = 256;
 constexpr int kZgenPer = 16;
@@ -88,6 +108,7 @@ size_t zgen_smem(int b);
 // F1: forward column DFTs over A of the pre-mapped coefficients.
 struct F1Args {
   const double2* z;
+  ZTile zt;
   double2* out;    // T[k_a][col], row length ncols
   uint32_t ncols;  // = L / A
   uint32_t logc;   // columns per CTA = 2^logc
@@ -133,6 +154,8 @@ __global__ void k_mid(MidArgs a);
 // C = 4096 row pass with compile-time schedules, persistent over row pairs.
 constexpr int kMidCtThreads = 512;
 __global__ void k_mid_4096(MidArgs a);
+constexpr int kMid8Threads = 1024;
+__global__ void k_mid_4096_r8(MidArgs a);
 
 struct ILastArgs {
   const double2* data;  // S[k_a][...] with geometry g (outer = 0)

@@ -75,11 +75,14 @@ std::vector<double2> host_table(uint64_t L, uint64_t step, uint64_t count) {
   return t;
 }
 
-std::vector<int> radix_schedule(uint32_t R) {
+// maxrad 16 (default) or 8: the largest power-of-two radix used.
+std::vector<int> radix_schedule(uint32_t R, int maxrad = 16) {
   std::array<uint32_t, 4> e;
   if (!factor_2357(R, e)) throw Error(TMG_ERR_UNSUPPORTED_LENGTH, "radix_schedule: not 2357-smooth");
   std::vector<int> rad;
   uint32_t e2 = e[0];
+  if (maxrad == 8)
+    while (e2 >= 3) { rad.push_back(8); e2 -= 3; }
   while (e2 >= 4) { rad.push_back(16); e2 -= 4; }
   if (e2 == 3) rad.push_back(8);
   if (e2 == 2) rad.push_back(4);
@@ -159,10 +162,11 @@ TwGlobal TwiddleCache::global(uint64_t L) {
   return g;
 }
 
-const double2* TwiddleCache::stage_table(uint32_t R) {
-  auto it = stages_.find(R);
+const double2* TwiddleCache::stage_table(uint32_t R, int maxrad) {
+  const uint64_t key = (uint64_t(R) << 8) | uint64_t(maxrad);
+  auto it = stages_.find(key);
   if (it != stages_.end()) return it->second->as<double2>();
-  auto rad = radix_schedule(R);
+  auto rad = radix_schedule(R, maxrad);
   std::vector<double2> h;
   uint32_t Ns = 1;
   for (size_t s = 0; s < rad.size(); ++s) {
@@ -182,17 +186,18 @@ const double2* TwiddleCache::stage_table(uint32_t R) {
   buf->ensure(h.size() * sizeof(double2));
   TMG_CUDA(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
   const double2* p = buf->as<double2>();
-  stages_[R] = std::move(buf);
+  stages_[key] = std::move(buf);
   return p;
 }
 
-SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride, TwiddleCache* cache) {
+SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride, TwiddleCache* cache,
+                   int maxrad) {
   SubFft s;
   std::memset(&s, 0, sizeof(s));
   s.R = R;
   s.tw = tw;
   s.twlen = R * tw_stride;
-  auto rad = radix_schedule(R);
+  auto rad = radix_schedule(R, maxrad);
   s.nst = int32_t(rad.size());
   uint32_t Ns = 1, off = 0;
   for (size_t i = 0; i < rad.size(); ++i) {
@@ -206,7 +211,7 @@ SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride, TwiddleCac
     Ns *= uint32_t(rad[i]);
   }
   s.stablen = off > 0 ? off : 1;
-  s.stab = cache ? cache->stage_table(R) : nullptr;
+  s.stab = cache ? cache->stage_table(R, maxrad) : nullptr;
   return s;
 }
 
@@ -422,10 +427,18 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   pl->fC = make_subfft(C, tC, 1, &tw);
   pl->iC = make_subfft(C / 2, tC, 2, &tw);
   pl->mid_shared_table = map_stages(pl->iC, pl->fC);
-  pl->logc_f1 = pick_logc(A, UL / A, cap);
+  if (C == 4096) {
+    // radix-8 schedules for the 32-warp row pass (k_mid_4096_r8)
+    pl->fC8 = make_subfft(C, tC, 1, &tw, 8);
+    pl->iC8 = make_subfft(C / 2, tC, 2, &tw, 8);
+    pl->mid8_ok = map_stages(pl->iC8, pl->fC8);
+  }
+  // TMG_COL_LOGC (testing): cap the columns per CTA of the column passes
+  static const int col_logc_cap = getenv("TMG_COL_LOGC") ? atoi(getenv("TMG_COL_LOGC")) : 6;
+  pl->logc_f1 = std::min<uint32_t>(pick_logc(A, UL / A, cap), uint32_t(col_logc_cap));
   pl->thr_f1 = threads_for(uint64_t(A) << pl->logc_f1);
   pl->smem_f1 = f1_smem_bytes(A, 1u << pl->logc_f1);
-  pl->logc_il = pick_logc(A, C / 2, cap);
+  pl->logc_il = std::min<uint32_t>(pick_logc(A, C / 2, cap), uint32_t(col_logc_cap));
   pl->thr_il = threads_for(uint64_t(A) << pl->logc_il);
   pl->smem_il = col_smem_bytes(A, 1u << pl->logc_il);
   if (pl->kind == 3) {

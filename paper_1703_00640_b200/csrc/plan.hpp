@@ -30,7 +30,7 @@ class TwiddleCache {
  public:
   const double2* table(uint32_t R);               // omega_R^x, x < R
   TwGlobal global(uint64_t L);                    // two-level omega_L
-  const double2* stage_table(uint32_t R);         // per-stage q-major table
+  const double2* stage_table(uint32_t R, int maxrad = 16);  // per-stage q-major table
  private:
   std::map<uint64_t, std::unique_ptr<DevBuf>> stages_;
   std::map<uint64_t, std::unique_ptr<DevBuf>> tables_;
@@ -38,7 +38,8 @@ class TwiddleCache {
   std::map<uint64_t, uint32_t> glob_S_;
 };
 
-SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride, TwiddleCache* cache);
+SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride, TwiddleCache* cache,
+                   int maxrad = 16);
 MapConsts make_map_consts(const Params& p);
 
 struct Plan {
@@ -67,6 +68,8 @@ struct Plan {
   int thr_f1 = 0, thr_f2 = 0, thr_i2 = 0, thr_il = 0, thr_mid = 0;
   size_t smem_zgen = 0;
   bool mid_shared_table = false;
+  SubFft fC8{}, iC8{};  // C = 4096 with radix <= 8 (k_mid_4096_r8)
+  bool mid8_ok = false;
   int kernels = 0;
 };
 

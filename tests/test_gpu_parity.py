@@ -382,3 +382,36 @@ def test_plan_shapes_exact(ctx, N):
         else:
             assert np.array_equal(r, port.oracle_full(u, v)[:len(r)]), (N, mode)
         assert ctx.last_stats.max_round_err < TRIP
+
+
+@pytest.mark.parametrize("b", [7, 8, 9, 10])
+@pytest.mark.parametrize("mode", [tm.Mode.LOW, tm.Mode.HIGH])
+def test_multipass_series_lengths(ctx, b, mode):
+    """Multi-pass products at small chunk widths: lambda = 6..8 rows of the
+    series maps (the carry kernel is instantiated per lambda)."""
+    rng = np.random.default_rng(100 * b + int(mode))
+    n = 1 << 17
+    N = 1
+    while N * b < n + 64:
+        N *= 2
+    p = tm.manual_params(n, b, N, mode)
+    assert p.lam == max(4, (52 + b - 1) // b)
+    nl = n // 64
+    u = rng.integers(0, 2**64, nl, dtype=np.uint64)
+    v = rng.integers(0, 2**64, nl, dtype=np.uint64)
+    r = ctx.product_limbs(mode, u, v, p)
+    assert ctx.last_stats.transform_length > 8192 and ctx.last_stats.passes >= 2
+    _check(mode, u, v, n, tm.from_limbs(r))
+    assert ctx.last_stats.max_round_err < TRIP
+
+
+def test_wide_chunks_refuse_on_the_64_bit_window_path(ctx):
+    """b > 32 takes the split kernel's 64-bit window path; at a multi-pass
+    length such chunks overflow the exact double range and must refuse."""
+    n, b, N = 40 * 6000, 40, 6144
+    p = tm.manual_params(n, b, N, tm.Mode.FULL)
+    rng = np.random.default_rng(5)
+    nl = (n + 63) // 64
+    u = port.int_to_limbs(int.from_bytes(rng.bytes(nl * 8), "little") & ((1 << n) - 1), nl)
+    with pytest.raises(tm.ConvolutionPrecisionFailure):
+        ctx.product_limbs(tm.Mode.FULL, u, u, p)
