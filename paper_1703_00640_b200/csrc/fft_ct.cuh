@@ -38,22 +38,25 @@ struct RowPair {
   }
 };
 
+// Each row of the pair is owned by one half of the CTA (threads
+// [0, NTHR/2) row 0, [NTHR/2, NTHR) row 1), which syncs on its own named
+// barrier: the halves run their stages independently and overlap each
+// other's stalls; only the spectral step couples the rows.
+template <int NTHR>
+__device__ __forceinline__ void ct_sync(int tid) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + (tid >= NTHR / 2 ? 1 : 0)), "r"(NTHR / 2) : "memory");
+}
+
 template <int RAD, uint32_t R, int NTHR, class Src>
 __device__ __forceinline__ void ct_load(double2 (&x)[16], const RowPair& lay, const Src& src,
                                         int tid) {
   constexpr uint32_t nbi = R / RAD;
-  static_assert(2 * nbi <= uint32_t(NTHR) || RAD * ((2 * nbi + NTHR - 1) / NTHR) <= 16,
-                "register block");
-  constexpr int NB = int((2 * nbi + NTHR - 1) / NTHR);
+  static_assert(nbi <= uint32_t(NTHR / 2), "one butterfly per thread and stage");
+  const uint32_t item = tid >= NTHR / 2 ? 1u : 0u;
+  const uint32_t t = uint32_t(tid) - item * (NTHR / 2);
+  if (t < nbi && item < lay.nrows) {
 #pragma unroll
-  for (int it = 0; it < NB; ++it) {
-    const uint32_t bf = uint32_t(tid) + uint32_t(it) * NTHR;
-    if (bf < nbi * lay.nrows) {
-      const uint32_t item = bf >= nbi ? 1u : 0u;
-      const uint32_t t = bf - item * nbi;
-#pragma unroll
-      for (int q = 0; q < RAD; ++q) x[it * RAD + q] = src(item, t + q * nbi);
-    }
+    for (int q = 0; q < RAD; ++q) x[q] = src(item, t + q * nbi);
   }
 }
 
@@ -62,16 +65,13 @@ __device__ __forceinline__ void ct_store(double2 (&x)[16], const RowPair& lay,
                                          const double2* __restrict__ stab, uint32_t qmul,
                                          const Sink& sink, int tid) {
   constexpr uint32_t nbi = R / RAD;
-  constexpr int NB = int((2 * nbi + NTHR - 1) / NTHR);
-#pragma unroll
-  for (int it = 0; it < NB; ++it) {
-    const uint32_t bf = uint32_t(tid) + uint32_t(it) * NTHR;
-    if (bf < nbi * lay.nrows) {
-      const uint32_t item = bf >= nbi ? 1u : 0u;
-      const uint32_t t = bf - item * nbi;
+  const uint32_t item = tid >= NTHR / 2 ? 1u : 0u;
+  const uint32_t t = uint32_t(tid) - item * (NTHR / 2);
+  {
+    if (t < nbi && item < lay.nrows) {
       const uint32_t tq = t / NS;
       const uint32_t j = t - tq * NS;
-      double2* xv = x + it * RAD;
+      double2* xv = x;
       if (NS > 1 && j != 0) {
 #pragma unroll
         for (int q = 1; q < RAD; ++q) {
@@ -107,13 +107,13 @@ __device__ __forceinline__ void ct_stages(double2 (&x)[16], double2* __restrict_
   } else {
     ct_load<RAD, R, NTHR>(x, lay, SmemSrc<RowPair>{buf, lay}, tid);
   }
-  __syncthreads();
+  ct_sync<NTHR>(tid);
   const double2* st = stab + p.toff[S];
   if constexpr (last) {
     ct_store<RAD, INV, R, NS, NTHR>(x, lay, st, p.qmul[S], sink, tid);
   } else {
     ct_store<RAD, INV, R, NS, NTHR>(x, lay, st, p.qmul[S], SmemSink<RowPair>{buf, lay}, tid);
-    __syncthreads();
+    ct_sync<NTHR>(tid);
     ct_stages<INV, SC, S + 1, NTHR>(x, buf, lay, stab, p, src, sink, tid);
   }
 }
