@@ -282,10 +282,11 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.cbits_u = cx.cbu.as<uint32_t>();
       a.cbits_v = cx.cbv.as<uint32_t>();
       a.aux = cx.aux.as<double>();
-      set_smem(k_f1, pl.smem_f1);
+      auto f1k = pl.colpp ? k_f1_pp : k_f1;
+      set_smem(f1k, pl.smem_f1);
       {
         KTimer kt(cx, "k_f1", double(p.N) * 16.0 + double(L) * 16.0, int(p.mode));
-        k_f1<<<a.ncols >> a.logc, pl.thr_f1, pl.smem_f1, st>>>(a);
+        f1k<<<a.ncols >> a.logc, pl.thr_f1, pl.smem_f1, st>>>(a);
       }
       check_launch("k_f1");
       ++kernels;
@@ -305,10 +306,11 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.to = 0;
       a.tc = 1;
       a.tmul = pl.A;
-      set_smem(k_col, pl.smem_f2);
+      auto colk = pl.colpp ? k_col_pp : k_col;
+      set_smem(colk, pl.smem_f2);
       {
         KTimer kt(cx, "k_col_f2", double(L) * 32.0, int(p.mode));
-        k_col<<<dim3(pl.C >> a.logc, pl.A), pl.thr_f2, pl.smem_f2, st>>>(a);
+        colk<<<dim3(pl.C >> a.logc, pl.A), pl.thr_f2, pl.smem_f2, st>>>(a);
       }
       check_launch("k_col(f2)");
       ++kernels;
@@ -364,10 +366,11 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.to = 1;
       a.tc = 0;
       a.tmul = pl.C;
-      set_smem(k_col, pl.smem_i2);
+      auto colk = pl.colpp ? k_col_pp : k_col;
+      set_smem(colk, pl.smem_i2);
       {
         KTimer kt(cx, "k_col_i2", double(L) * 16.0, int(p.mode));
-        k_col<<<dim3((pl.C / 2) >> a.logc, pl.A), pl.thr_i2, pl.smem_i2, st>>>(a);
+        colk<<<dim3((pl.C / 2) >> a.logc, pl.A), pl.thr_i2, pl.smem_i2, st>>>(a);
       }
       check_launch("k_col(i2)");
       ++kernels;
@@ -384,10 +387,11 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.g.ncols = pl.B * (pl.C / 2);
       a.logc = pl.logc_il;
       a.fft = pl.iA;
-      set_smem(k_ilast, pl.smem_il);
+      auto ilk = pl.colpp ? k_ilast_pp : k_ilast;
+      set_smem(ilk, pl.smem_il);
       {
         KTimer kt(cx, "k_ilast", double(L) * 16.0, int(p.mode));
-        k_ilast<<<a.g.ncols >> a.logc, pl.thr_il, pl.smem_il, st>>>(a);
+        ilk<<<a.g.ncols >> a.logc, pl.thr_il, pl.smem_il, st>>>(a);
       }
       check_launch("k_ilast");
       ++kernels;

@@ -302,6 +302,67 @@ __device__ __forceinline__ void fft_smem_compact(double2* __restrict__ buf, cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// Ping-pong transform for the column passes: stage s reads buffer a and
+// writes buffer b (then they swap), so loads and stores of a stage never
+// conflict -- one barrier per stage -- and a thread holds one butterfly of
+// at most 8 values at a time (radix <= 8 schedules), which lets a CTA run
+// 1024 threads at 64 registers.  Stage twiddles are read through L1 from
+// the global stage table (q-major, same layout and values as TwStage).
+// Returns the buffer holding the result; expects a barrier before the call
+// and ends with one.
+template <int RAD, bool INV, class Lay>
+__device__ __forceinline__ void stage_pp(const double2* __restrict__ a, double2* __restrict__ b,
+                                         const Lay& lay, const SubFft& p, int s, int tid,
+                                         int nthr) {
+  const uint32_t R = p.R, Ns = p.Ns[s];
+  const uint32_t nbi = R / RAD;
+  const uint32_t nbf = nbi * lay.nitems();
+  const FastDiv fd = p.fdNs[s];
+  const double2* __restrict__ st = p.stab + p.toff[s];
+  const uint32_t qm = p.qmul[s];
+  for (uint32_t bf = tid; bf < nbf; bf += nthr) {
+    uint32_t item, t;
+    lay.split(bf, nbi, item, t);
+    double2 x[RAD];
+#pragma unroll
+    for (int q = 0; q < RAD; ++q) x[q] = a[lay.idx(item, t + q * nbi)];
+    const uint32_t tq = fdiv(t, fd);
+    const uint32_t j = t - tq * Ns;
+    if (j != 0) {
+#pragma unroll
+      for (int q = 1; q < RAD; ++q) {
+        const double2 w = __ldg(st + (uint32_t(q) * qm - 1) * Ns + j);
+        x[q] = INV ? cmulc(x[q], w) : cmul(x[q], w);
+      }
+    }
+    dft<RAD, INV>(x);
+    const uint32_t ob = tq * Ns * RAD + j;
+#pragma unroll
+    for (int q = 0; q < RAD; ++q) b[lay.idx(item, ob + q * Ns)] = x[q];
+  }
+}
+
+template <bool INV, class Lay>
+__device__ __forceinline__ double2* fft_pp(double2* a, double2* b, const Lay lay,
+                                           const SubFft& p, int tid, int nthr) {
+  for (int s = 0; s < p.nst; ++s) {
+    switch (p.rad[s]) {
+      case 8: stage_pp<8, INV>(a, b, lay, p, s, tid, nthr); break;
+      case 4: stage_pp<4, INV>(a, b, lay, p, s, tid, nthr); break;
+      case 2: stage_pp<2, INV>(a, b, lay, p, s, tid, nthr); break;
+      case 3: stage_pp<3, INV>(a, b, lay, p, s, tid, nthr); break;
+      case 5: stage_pp<5, INV>(a, b, lay, p, s, tid, nthr); break;
+      default: stage_pp<7, INV>(a, b, lay, p, s, tid, nthr); break;
+    }
+    __syncthreads();
+    double2* t = a;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
 // Whole transform in shared memory (natural order in and out), ends with a
 // barrier.
 template <bool INV, class Lay, class TW>

@@ -281,6 +281,60 @@ k_col(ColArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Ping-pong column passes (fft_pp): two tiles in shared memory, one barrier
+// per stage, 1024 threads at 64 registers, radix <= 8 schedules, stage
+// twiddles through L1.  Same tiles, sources and sinks as above.
+size_t colpp_smem_bytes(uint32_t R, uint32_t c) { return 2 * size_t(padded_len(R * c)) * 16; }
+
+__global__ void __launch_bounds__(kColPPThreads, 1)
+k_f1_pp(F1Args a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* b0 = reinterpret_cast<double2*>(smem_raw);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const uint32_t c = 1u << a.logc;
+  const uint32_t col0 = blockIdx.x * c;
+  const uint32_t A = a.fft.R;
+  double2* b1 = b0 + padded_len(A * c);
+  const MapConsts& mc = a.mc;
+  const int64_t N = mc.N;
+  LayCols lay{a.logc, c - 1};
+  double topu = 0.0, topv = 0.0;
+  if (mc.mode == kModeHigh && col0 < uint32_t(mc.nfold + mc.lambda)) {
+    topu = digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, N, mc.balanced != 0);
+    topv = digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, N, mc.balanced != 0);
+  }
+  if (mc.mode == kModeHigh && blockIdx.x == 0 && tid == 0) {
+    auto Du = [&](int64_t i) { return digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, i, mc.balanced != 0); };
+    auto Dv = [&](int64_t i) { return digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, i, mc.balanced != 0); };
+    a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
+  }
+  const ZSrc src{a.z, a.zt, N, a.ncols, col0, &a.mc, topu, topv};
+  tile_load(b0, lay, A, c, src, tid, nthr);
+  __syncthreads();
+  const double2* res = fft_pp<false>(b0, b1, lay, a.fft, tid, nthr);
+  tile_store(res, lay, A, c, F1Sink{a.out, a.ncols, col0, a.tw}, tid, nthr);
+}
+
+__global__ void __launch_bounds__(kColPPThreads, 1)
+k_col_pp(ColArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* b0 = reinterpret_cast<double2*>(smem_raw);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const uint32_t c = 1u << a.logc;
+  const uint32_t col0 = blockIdx.x * c;
+  const int64_t outer = blockIdx.y;
+  double2* b1 = b0 + padded_len(a.fft.R * c);
+  LayCols lay{a.logc, c - 1};
+  ColSrc src{a.data, a.g, outer, col0};
+  ColSink sink{a.data, a.g, outer, col0, a.tw, a.to, a.tc, a.tmul, a.inv != 0, true};
+  tile_load(b0, lay, a.fft.R, c, src, tid, nthr);
+  __syncthreads();
+  const double2* res = a.inv ? fft_pp<true>(b0, b1, lay, a.fft, tid, nthr)
+                             : fft_pp<false>(b0, b1, lay, a.fft, tid, nthr);
+  tile_store(res, lay, a.fft.R, c, sink, tid, nthr);
+}
+
+// ---------------------------------------------------------------------------
 // Row pass: conjugate row pair (r, AB - r), r = k_a + A k_b.
 struct RowSrc {
   const double2* data;
@@ -476,6 +530,22 @@ k_ilast(ILastArgs a) {
   fft_smem_compact<true>(sbuf, lay, a.fft, tw, tid, nthr);
   tile_store(sbuf, lay, a.fft.R, c, CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
 }
+
+__global__ void __launch_bounds__(kColPPThreads, 1)
+k_ilast_pp(ILastArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* b0 = reinterpret_cast<double2*>(smem_raw);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const uint32_t c = 1u << a.logc;
+  const uint32_t col0 = blockIdx.x * c;
+  double2* b1 = b0 + padded_len(a.fft.R * c);
+  LayCols lay{a.logc, c - 1};
+  tile_load(b0, lay, a.fft.R, c, ColSrc{a.data, a.g, 0, col0}, tid, nthr);
+  __syncthreads();
+  const double2* res = fft_pp<true>(b0, b1, lay, a.fft, tid, nthr);
+  tile_store(res, lay, a.fft.R, c, CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
+}
+
 
 // ---------------------------------------------------------------------------
 // Post-map, rounding and carry propagation over all limbs.

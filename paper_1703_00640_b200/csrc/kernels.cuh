@@ -140,6 +140,11 @@ struct ColArgs {
   uint32_t to, tc, tmul;
 };
 __global__ void k_col(ColArgs a);
+// ping-pong column passes (fft_pp)
+constexpr int kColPPThreads = 1024;
+__global__ void k_f1_pp(F1Args a);
+__global__ void k_col_pp(ColArgs a);
+size_t colpp_smem_bytes(uint32_t R, uint32_t c);
 
 struct MidArgs {
   double2* data;  // rows of length C at storage index (k_a * B + k_b) * C
@@ -165,6 +170,7 @@ struct ILastArgs {
   SubFft fft;  // length A (inverse)
 };
 __global__ void k_ilast(ILastArgs a);
+__global__ void k_ilast_pp(ILastArgs a);
 
 struct CarryArgs {
   const double* w;  // convolution coefficients (L of them)

@@ -452,6 +452,54 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
     pl->thr_i2 = threads_for(uint64_t(B) << pl->logc_i2);
     pl->smem_i2 = col_smem_bytes(B, 1u << pl->logc_i2);
   }
+  // Ping-pong column passes (k_*_pp): radix <= 8 schedules, two tiles in
+  // shared memory, up to 1024 threads.  Used whenever the two tiles of at
+  // least one column fit (TMG_NO_PP keeps the single-buffer passes).
+  static const bool no_pp = getenv("TMG_NO_PP") != nullptr;
+  auto pp_logc = [&](uint32_t R, uint64_t ncols) -> int {
+    const uint32_t p2 = largest_pow2_divisor(ncols);
+    int best = -1;
+    for (uint32_t lc = 0; lc <= 6 && (1u << lc) <= p2; ++lc)
+      if (colpp_smem_bytes(R, 1u << lc) <= size_t(220) * 1024) best = int(lc);
+    return best;
+  };
+  auto pp_threads = [](uint32_t R, uint32_t lc) {
+    uint64_t t = ((uint64_t(R) << lc) / 8 + 31) / 32 * 32;
+    return int(std::min<uint64_t>(kColPPThreads, std::max<uint64_t>(128, t)));
+  };
+  pl->colpp = false;
+  if (!no_pp) {
+    const int lf1 = pp_logc(A, UL / A), lil = pp_logc(A, C / 2);
+    int lf2 = 0, li2 = 0;
+    if (pl->kind == 3) {
+      lf2 = pp_logc(B, C);
+      li2 = pp_logc(B, C / 2);
+    }
+    // only when the two tiles hold as many columns as the single-buffer
+    // pass (fewer columns mean shorter global segments, which costs more
+    // than the extra warps gain: A = 1792 measured 126 -> 166 us)
+    if (lf1 >= int(pl->logc_f1) && lil >= int(pl->logc_il) && lf2 >= 0 && li2 >= 0) {
+      pl->colpp = true;
+      pl->fA = make_subfft(A, tA, 1, &tw, 8);
+      pl->iA = pl->fA;
+      pl->logc_f1 = uint32_t(std::min(lf1, col_logc_cap));
+      pl->thr_f1 = pp_threads(A, pl->logc_f1);
+      pl->smem_f1 = colpp_smem_bytes(A, 1u << pl->logc_f1);
+      pl->logc_il = uint32_t(std::min(lil, col_logc_cap));
+      pl->thr_il = pp_threads(A, pl->logc_il);
+      pl->smem_il = colpp_smem_bytes(A, 1u << pl->logc_il);
+      if (pl->kind == 3) {
+        pl->fB = make_subfft(B, tw.table(B), 1, &tw, 8);
+        pl->iB = pl->fB;
+        pl->logc_f2 = uint32_t(lf2);
+        pl->thr_f2 = pp_threads(B, pl->logc_f2);
+        pl->smem_f2 = colpp_smem_bytes(B, 1u << pl->logc_f2);
+        pl->logc_i2 = uint32_t(li2);
+        pl->thr_i2 = pp_threads(B, pl->logc_i2);
+        pl->smem_i2 = colpp_smem_bytes(B, 1u << pl->logc_i2);
+      }
+    }
+  }
   pl->thr_mid = threads_for(uint64_t(2) * C);
   pl->smem_mid = mid_smem_bytes(C, pl->mid_shared_table ? 0u : pl->iC.stablen);
   const int64_t LB = kCarryThreads * kCarryPerThread;

@@ -70,6 +70,7 @@ struct Plan {
   bool mid_shared_table = false;
   SubFft fC8{}, iC8{};  // C = 4096 with radix <= 8 (k_mid_4096_r8)
   bool mid8_ok = false;
+  bool colpp = false;  // column passes use the ping-pong kernels (k_*_pp)
   int kernels = 0;
 };
 
