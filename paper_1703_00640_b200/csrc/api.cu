@@ -85,7 +85,7 @@ struct Context {
   bool own_stream = false;
   TwiddleCache tw;
   std::map<std::tuple<int64_t, int32_t, int64_t, int64_t, int32_t>, std::unique_ptr<Plan>> plans;
-  DevBuf work_t, work_c, work_z, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf, aggs, zaggs;
+  DevBuf work_t, work_c, work_z, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf, aggs, zaggs, haggs;
   ScanSlot scan_u, scan_v, scan_c, scan_h;
   bool debug_sync = false;
   DevStatus* h_status = nullptr;  // pinned
@@ -464,12 +464,19 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       const unsigned blocks = unsigned((a.WL + LB - 1) / LB);
       a.scan = cx.scan_h.next(blocks);
       a.status = status;
+      cx.haggs.ensure(size_t(blocks) * 4 + 16);
+      a.aggs = cx.haggs.as<uint32_t>();
+      {
+        KTimer kt(cx, "k_high_agg", double(pl.ML) * 8.0, int(p.mode));
+        k_high_agg<<<blocks, kCarryThreads, 0, st>>>(a);
+      }
+      check_launch("k_high_agg");
       {
         KTimer kt(cx, "k_high_round", double(pl.ML) * 8.0 + double(pl.out_limbs) * 8.0, int(p.mode));
         k_high_round<<<blocks, kCarryThreads, 0, st>>>(a);
       }
       check_launch("k_high_round");
-      ++kernels;
+      kernels += 2;
     }
   }
   cx.last_kernels = kernels;

@@ -194,9 +194,10 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
   }
   if (tid == 0) {
     s_flags = 0;
-    s_psi = (mc.mode == kModeHigh) ? high_psi(mc, [&](int64_t j) { return __ldg(a.w + j); },
-                                              a.aux[0])
-                                   : 0.0;
+    // psi enters only x_N and the fold region k < nfold (delta+,
+    // maps_f64.cpp:363-383): the first and the last block
+    const bool need_psi = mc.mode == kModeHigh && (kbase < mc.nfold || kend > mc.N);
+    s_psi = need_psi ? high_psi(mc, [&](int64_t j) { return __ldg(a.w + j); }, a.aux[0]) : 0.0;
   }
   __syncthreads();
   RoundAcc ra;

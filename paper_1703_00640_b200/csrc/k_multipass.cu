@@ -733,6 +733,33 @@ size_t carry_smem(int b) {
 // increment ripples through all-ones limbs of t >> s: a second carry scan
 // with the increment as the carry into limb 0.  Then the range test
 // 0 <= w <= 2^n.
+// Limb m of t >> s (t in tbuf, ML limbs).
+__device__ __forceinline__ uint64_t high_shifted(const HighRoundArgs& a, int64_t m) {
+  const int64_t q = int64_t(a.shift_s) >> 6;
+  const int r = int(a.shift_s & 63);
+  const uint64_t lo = (m + q < a.ML) ? a.tbuf[m + q] : 0ull;
+  const uint64_t hi = (m + q + 1 < a.ML) ? a.tbuf[m + q + 1] : 0ull;
+  return r ? ((lo >> r) | (hi << (64 - r))) : lo;
+}
+
+// Per-block transfer function of the increment chain of k_high_round: an
+// increment passes a limb of t >> s only if the limb is all ones.
+__global__ void __launch_bounds__(kCarryThreads)
+k_high_agg(HighRoundArgs a) {
+  __shared__ uint32_t s_all;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_all = 1;
+  __syncthreads();
+  constexpr int LB = kCarryThreads * kCarryPerThread;
+  const int64_t ms = int64_t(blockIdx.x) * LB;
+  const int64_t me = min(a.WL, ms + LB);
+  bool all = true;
+  for (int64_t m = ms + tid; m < me; m += kCarryThreads) all &= high_shifted(a, m) == ~0ull;
+  if (!__all_sync(0xffffffffu, all) && (tid & 31) == 0) s_all = 0;
+  __syncthreads();
+  if (tid == 0) a.aggs[blockIdx.x] = s_all ? kTfIdentity : tf_const(0);
+}
+
 __global__ void __launch_bounds__(kCarryThreads)
 k_high_round(HighRoundArgs a) {
   __shared__ uint32_t sw[32];
@@ -741,13 +768,11 @@ k_high_round(HighRoundArgs a) {
   __shared__ uint32_t s_flags, s_top, s_low;
   const int tid = threadIdx.x;
   if (tid == 0) {
-    s_blk = take_ticket(a.scan.ctr);
     s_flags = 0;
     s_top = 0;
     s_low = 0;
   }
-  __syncthreads();
-  const uint32_t blk = s_blk;
+  const uint32_t blk = blockIdx.x;
   const int64_t s = a.shift_s;
   const int64_t q = s >> 6;
   const int r = int(s & 63);
@@ -773,9 +798,15 @@ k_high_round(HighRoundArgs a) {
   }
   uint32_t agg;
   const uint32_t ex = block_scan_tf(f, sw, &agg);
-  if (tid < 32) {
-    const int cin = lookback_warp(a.scan.state, blk, agg, a.scan.epoch, inc);
-    if (tid == 0) s_cin = cin;
+  {
+    // increment into this block: the aggregates before it (k_high_agg)
+    uint32_t g = kTfIdentity;
+    const uint32_t Q = (blk + kCarryThreads - 1) / kCarryThreads;
+    const uint32_t i0 = uint32_t(tid) * Q, i1 = min(blk, i0 + Q);
+    for (uint32_t i = i0; i < i1; ++i) g = tf_compose(g, __ldg(a.aggs + i));
+    uint32_t pre;
+    (void)block_scan_tf(g, sw, &pre);
+    if (tid == 0) s_cin = tf_apply(pre, inc);
   }
   __syncthreads();
   int c = tf_apply(ex, s_cin);
@@ -799,7 +830,6 @@ k_high_round(HighRoundArgs a) {
     if (s_flags) atomicOr(&a.status->flags, s_flags);
     if (s_top) atomicOr(&a.status->high_topbit, 1u);
     if (s_low) atomicOr(&a.status->high_lownz, 1u);
-    release_ticket(a.scan.ctr, gridDim.x);
   }
 }
 

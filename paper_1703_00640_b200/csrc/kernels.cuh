@@ -212,7 +212,9 @@ struct HighRoundArgs {
   int32_t shift_s;
   ScanState scan;
   DevStatus* status;
+  uint32_t* aggs;  // per-block increment transfer functions (k_high_agg)
 };
+__global__ void k_high_agg(HighRoundArgs a);
 __global__ void k_high_round(HighRoundArgs a);
 
 // Schoolbook product for operands below the pipeline cutoff (the reference's
