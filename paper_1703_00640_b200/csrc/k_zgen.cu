@@ -86,7 +86,7 @@ k_zstat(ZgenArgs a) {
   const int64_t c0 = blk * kZgenChunks;
   // statuses exist for chunks below the (unbalanced) top chunk only
   const int64_t c1 = min(count - 1, c0 + kZgenChunks);
-  uint32_t fu = kTfIdentity, fv = kTfIdentity;
+  uint32_t fu = 2, fv = 2;  // propagate (identity)
   if (a.mc.balanced) {
     bool du = false, dv = false;
     for (int64_t j = c1 - 1; j >= c0 && !(du && dv); --j) {
@@ -94,22 +94,22 @@ k_zstat(ZgenArgs a) {
       if (!du) {
         const uint64_t w = window_bits(a.u, a.nlimbs, pos, b);
         if (w != half) {
-          fu = tf_const(w > half ? 1 : 0);
+          fu = w > half ? 1u : 0u;
           du = true;
         }
       }
       if (!dv) {
         const uint64_t w = window_bits(a.v, a.nlimbs, pos, b);
         if (w != half) {
-          fv = tf_const(w > half ? 1 : 0);
+          fv = w > half ? 1u : 0u;
           dv = true;
         }
       }
     }
   } else {
-    fu = fv = tf_const(0);
+    fu = fv = 0;
   }
-  a.aggs[blk] = tf2_pack(fu, fv);
+  a.aggs[blk] = fu | (fv << 2);
 }
 
 template <bool W32>
@@ -185,28 +185,29 @@ k_zgen_t(ZgenArgs a) {
       }
     }
   }
-  auto agg_of = [](uint32_t g, uint32_t p) -> uint32_t {
+  // kill / generate / propagate of this thread's run: its last non-P chunk
+  auto kgp_of = [](uint32_t g, uint32_t p) -> uint32_t {
     const uint32_t np = ~p & 0xffffu;
-    if (!np) return kTfIdentity;
+    if (!np) return 2u;
     const int last = 31 - __clz(np);
-    return ((g >> last) & 1u) ? tf_const(1) : tf_const(0);
+    return (g >> last) & 1u;
   };
   uint32_t agg2;
-  const uint32_t ex2 = block_scan_tf2(tf2_pack(agg_of(gu, pu), agg_of(gv, pv)), sw, &agg2);
+  const uint32_t ex2 = block_scan_kgp(kgp_of(gu, pu) | (kgp_of(gv, pv) << 2), sw, &agg2);
   // carry into the block: the aggregates of the blocks before it (k_zstat),
   // composed in order by the whole block
   {
-    uint32_t g = kTf2Identity;
+    uint32_t g = kKgpIdentity;
     const uint32_t Q = (blk + kZgenThreads - 1) / kZgenThreads;
     const uint32_t i0 = uint32_t(tid) * Q, i1 = min(blk, i0 + Q);
-    for (uint32_t i = i0; i < i1; ++i) g = tf2_compose(g, __ldg(a.aggs + i));
+    for (uint32_t i = i0; i < i1; ++i) g = kgp_compose(g, __ldg(a.aggs + i));
     uint32_t pre;
-    (void)block_scan_tf2(g, sw, &pre);
-    if (tid == 0) s_cin = tf2_apply(pre, 5u);  // both chains start with carry 0
+    (void)block_scan_kgp(g, sw, &pre);
+    if (tid == 0) s_cin = kgp_compose(0u, pre);  // both chains start with carry 0
   }
   __syncthreads();
-  const uint32_t cc = tf2_apply(ex2, s_cin);
-  int cu = int(cc & 3u) - 1, cv = int((cc >> 2) & 3u) - 1;
+  const uint32_t cc = kgp_compose(s_cin, ex2);
+  int cu = int(cc & 1u), cv = int((cc >> 2) & 1u);
 
   // digits and carry-in bits
   uint32_t bu = 0, bv = 0;

@@ -366,6 +366,49 @@ __device__ __forceinline__ uint32_t tf2_apply(uint32_t f, uint32_t cc) {
 }
 __device__ __forceinline__ uint32_t tf2_pack(uint32_t fu, uint32_t fv) { return fu | (fv << 6); }
 
+// ----------------------------------------------------------------------------
+// Kill / generate / propagate codes of the balanced split's carry chains
+// (carries are 0 or 1 there): 0 = K (carry out 0), 1 = G (carry out 1),
+// 2 = P (carry out = carry in); two operands packed in bits [0,2) and [2,4).
+// Composition "f then g" keeps g unless g propagates; applying f to carries
+// c (codes 0 / 1 per operand) is kgp_compose(c, f).
+constexpr uint32_t kKgpIdentity = 2u | (2u << 2);
+__device__ __forceinline__ uint32_t kgp_compose(uint32_t f, uint32_t g) {
+  const uint32_t pm = (g >> 1) & ~g & 0x5u;  // fields of g equal to P (binary 10)
+  const uint32_t M = pm | (pm << 1);
+  return (g & ~M) | (f & M);
+}
+
+__device__ __forceinline__ uint32_t block_scan_kgp(uint32_t f, uint32_t* sw, uint32_t* agg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  uint32_t inc = f;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc = kgp_compose(o, inc);
+  }
+  uint32_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) excl = kKgpIdentity;
+  __syncthreads();
+  if (lane == 31) sw[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t v = lane < nw ? sw[lane] : kKgpIdentity;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= off) v = kgp_compose(o, v);
+    }
+    sw[lane] = v;
+  }
+  __syncthreads();
+  const uint32_t wex = warp > 0 ? sw[warp - 1] : kKgpIdentity;
+  *agg = sw[nw - 1];
+  __syncthreads();
+  return kgp_compose(wex, excl);
+}
+
 // Block-wide exclusive scan of paired transfer functions.
 __device__ __forceinline__ uint32_t block_scan_tf2(uint32_t f, uint32_t* sw,
                                                    uint32_t* agg) {
