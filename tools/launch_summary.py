@@ -3,8 +3,9 @@ per-kernel shares of the product step.
 
     python tools/launch_summary.py LAUNCHES.csv > profiles/rNN_launch_summary.md
 
-Products are the runs of tmg:: kernels that start at k_zgen; bench.py issues
-them as full, low, high per step (high is the run containing k_high_round).
+Products are the runs of tmg:: kernels that start at k_zstat (the split's
+carry aggregates); bench.py issues them as full, low, high per step (high is
+the run containing k_high_round).
 """
 import collections
 import csv
@@ -17,17 +18,27 @@ def main():
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr, data = rows[hi], rows[hi + 1:]
     ki, mi, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
-    seq = [(r[ki].split("(")[0].replace("tmg::", ""), float(r[vi].replace(",", "")) / 1e3)
+    def norm(name):
+        # "void tmg::<unnamed>::k_carry_lanes<5>(tmg::CarryArgs)" -> "k_carry_lanes<5>"
+        name = name.split("(")[0]
+        if name.startswith("void "):
+            name = name[5:]
+        return name.replace("tmg::", "").replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
+
+    seq = [(norm(r[ki]), float(r[vi].replace(",", "")) / 1e3)
            for r in data if r[mi] == "gpu__time_duration.sum"]
     other = [t for k, t in seq if not k.startswith("k_")]
     groups, cur = [], []
+    prev = None
     for k, t in seq:
         if not k.startswith("k_"):
             continue
-        if k in ("k_zgen", "k_small_product", "k_basecase") and cur:
+        starts = k in ("k_zstat", "k_small_product", "k_basecase") or (k.startswith("k_zgen") and prev != "k_zstat")
+        if starts and cur:
             groups.append(cur)
             cur = []
         cur.append((k, t))
+        prev = k
     if cur:
         groups.append(cur)
     per = collections.defaultdict(list)
