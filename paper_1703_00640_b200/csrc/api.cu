@@ -253,7 +253,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
         k_zstat<<<(blocks + 255) / 256, 256, 0, st>>>(a);
       }
       check_launch("k_zstat");
-      ZgenFn zg = zgen_kernel(int(p.b));
+      ZgenFn zg = zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda));
       set_smem(zg, pl.smem_zgen);
       {
         KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * 16.0, int(p.mode));

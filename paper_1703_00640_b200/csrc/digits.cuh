@@ -163,6 +163,34 @@ __device__ __forceinline__ double coef_r(int fam, double k, double N, double c) 
   }
 }
 
+// coef_r with the row known only after unrolling (r is a loop constant of a
+// fully unrolled loop): the same multiplications as coef_r<R>.
+__device__ __forceinline__ double coef_rt(int fam, int R, double k, double N, double c) {
+  double p = k;
+  if (fam == 0 || fam == 2) {
+    const double st = (fam == 0) ? -N : N;
+    double f = k + double(R) + st;
+#pragma unroll
+    for (int i = 0; i < kMaxLambda - 1; ++i) {
+      if (i < R - 1) {
+        p *= f;
+        f += st;
+      }
+    }
+  } else {
+    const double st = (fam == 1) ? N : -N;
+    double f = k + st;
+#pragma unroll
+    for (int i = 1; i < kMaxLambda; ++i) {
+      if (i < R) {
+        p *= f;
+        f += st;
+      }
+    }
+  }
+  return p * c;
+}
+
 // Compile-time loop r = 0 .. R-1 calling f(std::integral_constant<int, r>).
 template <int R>
 struct RowLoop {

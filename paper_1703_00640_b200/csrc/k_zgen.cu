@@ -65,8 +65,7 @@ __host__ __device__ inline int64_t zgen_words(int b, int kw) {
 
 size_t zgen_smem(int b) {
   const int kw = b <= 32 ? 32 : 64;
-  return 2 * size_t(zgen_words(b, kw)) * (kw / 8) + size_t(2) * (kZgenChunks + kMaxLambda) * 4 +
-         64;
+  return 2 * size_t(zgen_words(b, kw)) * (kw / 8) + size_t(kZgenChunks + kMaxLambda) * 8 + 64;
 }
 
 // Carry transfer function of each block of kZgenChunks chunks for both
@@ -112,7 +111,9 @@ k_zstat(ZgenArgs a) {
   a.aggs[blk] = fu | (fv << 2);
 }
 
-template <bool W32>
+// LAM: the series length lambda (rows of the pre-map), 0 for the full
+// product (the digits themselves).
+template <bool W32, int LAM>
 __global__ void __launch_bounds__(kZgenThreads)
 k_zgen_t(ZgenArgs a) {
   using SB = StagedBits<W32>;
@@ -120,19 +121,19 @@ k_zgen_t(ZgenArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t sw[32];
   __shared__ uint32_t s_cin;
-  __shared__ int32_t s_wrap[2][kMaxLambda];
+
   const int tid = threadIdx.x;
   const MapConsts& mc = a.mc;
   const int b = a.b;
   const int64_t N = a.N;
   const int64_t count = a.count;
-  const int lam = (mc.mode == kModeFull) ? 1 : mc.lambda;
-  const int ext = lam - 1;
+  constexpr int lam = LAM > 0 ? LAM : 1;
+  constexpr int ext = lam - 1;
   const int64_t nwd = zgen_words(b, SB::kW);
   Word* su = reinterpret_cast<Word*>(smem_raw);
   Word* sv = su + nwd;
-  int32_t* digu = reinterpret_cast<int32_t*>(sv + nwd);
-  int32_t* digv = digu + (kZgenChunks + kMaxLambda);
+  // digits of the block's chunks (and the next lam-1), u and v packed
+  int2* dig = reinterpret_cast<int2*>(sv + nwd);
 
   const uint32_t blk = blockIdx.x;
   const int64_t c0 = int64_t(blk) * kZgenChunks;
@@ -143,18 +144,6 @@ k_zgen_t(ZgenArgs a) {
   for (int64_t i = tid; i < nwd; i += kZgenThreads) {
     su[i] = load_word<W32>(a.u, a.nlimbs, wbase + i);
     sv[i] = load_word<W32>(a.v, a.nlimbs, wbase + i);
-  }
-  // digits of chunks 0 .. lam-2 (the wrap of the cyclic pre-map), carry 0 in
-  if (tid == 0 && mc.mode != kModeFull && c1 + ext > N) {
-    int cu = 0, cv = 0;
-    for (int i = 0; i < ext; ++i) {
-      const uint64_t wu = window_bits(a.u, a.nlimbs, int64_t(i) * b - a.lead, b);
-      const uint64_t wv = window_bits(a.v, a.nlimbs, int64_t(i) * b - a.lead, b);
-      s_wrap[0][i] = int32_t(split_digit(wu, cu, b, i == count - 1 || !mc.balanced));
-      s_wrap[1][i] = int32_t(split_digit(wv, cv, b, i == count - 1 || !mc.balanced));
-      cu = mc.balanced ? tf_apply(split_tf(wu, b), cu) : 0;
-      cv = mc.balanced ? tf_apply(split_tf(wv, b), cv) : 0;
-    }
   }
   __syncthreads();
   const SB Lu{su}, Lv{sv};
@@ -218,8 +207,8 @@ k_zgen_t(ZgenArgs a) {
       bu |= uint32_t(cu) << q;
       bv |= uint32_t(cv) << q;
       const bool top = j == count - 1 || !mc.balanced;
-      digu[q0 + q] = int32_t(split_digit(wu[q], cu, b, top));
-      digv[q0 + q] = int32_t(split_digit(wv[q], cv, b, top));
+      dig[q0 + q] = make_int2(int32_t(split_digit(wu[q], cu, b, top)),
+                              int32_t(split_digit(wv[q], cv, b, top)));
       if (!((pu >> q) & 1u)) cu = int((gu >> q) & 1u);
       if (!((pv >> q) & 1u)) cv = int((gv >> q) & 1u);
     }
@@ -232,8 +221,8 @@ k_zgen_t(ZgenArgs a) {
       const uint32_t rel = off0 + uint32_t(j - c0) * uint32_t(b);
       const uint64_t xu = Lu.window(rel, mask), xv = Lv.window(rel, mask);
       const bool top = j == count - 1 || !mc.balanced;
-      digu[j - c0] = int32_t(split_digit(xu, cu, b, top));
-      digv[j - c0] = int32_t(split_digit(xv, cv, b, top));
+      dig[j - c0] = make_int2(int32_t(split_digit(xu, cu, b, top)),
+                              int32_t(split_digit(xv, cv, b, top)));
       cu = mc.balanced ? tf_apply(split_tf(xu, b), cu) : 0;
       cv = mc.balanced ? tf_apply(split_tf(xv, b), cv) : 0;
     }
@@ -251,45 +240,76 @@ k_zgen_t(ZgenArgs a) {
     if ((__ldg(a.u + a.nlimbs - 1) | __ldg(a.v + a.nlimbs - 1)) & hm)
       atomicOr(&a.status->flags, uint32_t(kFlagInputRange));
   }
+  const int64_t ce = min(c1, N);
+  const int32_t nloc = int32_t(ce - c0);  // local chunks with a digit in this block
+  const int32_t nN = int32_t(N - c0);     // local index of chunk N (wrap start)
+  __syncthreads();
+  // the wrap of the cyclic pre-map: digits of chunks 0 .. lam-2 (carry 0 in)
+  // follow chunk N-1 (they replace chunk N's digit, which the pre-map does
+  // not use -- the high product folds it in k_f1)
+  if (LAM > 1 && tid == 0 && c1 + ext > N) {
+    int cu = 0, cv = 0;
+    for (int i = 0; i < ext; ++i) {
+      const uint64_t wu = window_bits(a.u, a.nlimbs, int64_t(i) * b - a.lead, b);
+      const uint64_t wv = window_bits(a.v, a.nlimbs, int64_t(i) * b - a.lead, b);
+      dig[nN + i] = make_int2(int32_t(split_digit(wu, cu, b, i == count - 1 || !mc.balanced)),
+                              int32_t(split_digit(wv, cv, b, i == count - 1 || !mc.balanced)));
+      cu = mc.balanced ? tf_apply(split_tf(wu, b), cu) : 0;
+      cv = mc.balanced ? tf_apply(split_tf(wv, b), cv) : 0;
+    }
+  }
   __syncthreads();
 
   // outputs
-  const int64_t ce = min(c1, N);
-  if (mc.mode == kModeFull) {
-    for (int64_t j = c0 + tid; j < ce; j += kZgenThreads)
-      a.z[a.zt.index(uint32_t(j))] = make_double2(double(digu[j - c0]), double(digv[j - c0]));
-    return;
-  }
-  const double Nd = double(N);
-  const int fam = (mc.mode == kModeLow) ? 0 : 2;
-  const int32_t nloc = int32_t(ce - c0);  // local chunks with a digit in this block
-  const int32_t nN = int32_t(N - c0);     // local index of chunk N (wrap start)
-  for (int32_t jl = ext + tid; jl < nloc + ext; jl += kZgenThreads) {
-    double au = 0.0, av = 0.0;
-    const double jd = double(c0 + jl);
-    RowLoopDown<kMaxLambda>::run([&](auto rc) {
-      constexpr int r = decltype(rc)::value;
-      if (r < lam) {
+  if constexpr (LAM == 0) {
+    for (int32_t jl = tid; jl < nloc; jl += kZgenThreads) {
+      const int2 d = dig[jl];
+      a.z[a.zt.index(uint32_t(c0 + jl))] = make_double2(double(d.x), double(d.y));
+    }
+  } else {
+    const double Nd = double(N);
+    constexpr int fam_low = 0, fam_high = 2;
+    const bool low = mc.mode == kModeLow;
+    double cr[LAM];
+#pragma unroll
+    for (int r = 0; r < LAM; ++r) cr[r] = mc.cpre[r];
+    for (int32_t jl = ext + tid; jl < nloc + ext; jl += kZgenThreads) {
+      double au = 0.0, av = 0.0;
+      const double jd = double(c0 + jl);
+#pragma unroll
+      for (int r = LAM - 1; r >= 0; --r) {
         const int32_t il = jl - r;  // local chunk, in [0, nloc + ext)
-        double du, dv, kd = jd - double(r);
-        if (il < nN) {
-          du = double(digu[il]);
-          dv = double(digv[il]);
-        } else {
-          du = double(s_wrap[0][il - nN]);
-          dv = double(s_wrap[1][il - nN]);
-          kd -= Nd;
-        }
-        const double cf = coef_r<r>(fam, kd, Nd, mc.cpre[r]);
-        au += du * cf;
-        av += dv * cf;
+        const int2 d = dig[il];
+        const double kd = jd - double(r) - (il >= nN ? Nd : 0.0);
+        double cf;
+        if (r == 0) cf = 1.0;
+        else cf = low ? coef_rt(fam_low, r, kd, Nd, cr[r]) : coef_rt(fam_high, r, kd, Nd, cr[r]);
+        au += double(d.x) * cf;
+        av += double(d.y) * cf;
       }
-    });
-    const int64_t j = c0 + jl;
-    a.z[a.zt.index(uint32_t(j >= N ? j - N : j))] = make_double2(au, av);
+      const int64_t j = c0 + jl;
+      a.z[a.zt.index(uint32_t(j >= N ? j - N : j))] = make_double2(au, av);
+    }
   }
 }
 
-ZgenFn zgen_kernel(int b) { return b <= 32 ? k_zgen_t<true> : k_zgen_t<false>; }
+template <bool W32>
+ZgenFn zgen_kernel_l(int lam) {
+  switch (lam) {
+    case 0: return k_zgen_t<W32, 0>;
+    case 1: return k_zgen_t<W32, 1>;
+    case 2: return k_zgen_t<W32, 2>;
+    case 3: return k_zgen_t<W32, 3>;
+    case 4: return k_zgen_t<W32, 4>;
+    case 5: return k_zgen_t<W32, 5>;
+    case 6: return k_zgen_t<W32, 6>;
+    case 7: return k_zgen_t<W32, 7>;
+    default: return k_zgen_t<W32, 8>;
+  }
+}
+
+ZgenFn zgen_kernel(int b, int lam) {
+  return b <= 32 ? zgen_kernel_l<true>(lam) : zgen_kernel_l<false>(lam);
+}
 
 }  // namespace tmg

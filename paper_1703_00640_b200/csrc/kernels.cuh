@@ -102,7 +102,7 @@ constexpr int kZgenPer = 16;
 constexpr int kZgenChunks = kZgenThreads * kZgenPer;
 __global__ void k_zstat(ZgenArgs a);
 typedef void (*ZgenFn)(ZgenArgs);
-ZgenFn zgen_kernel(int b);
+ZgenFn zgen_kernel(int b, int lam);
 size_t zgen_smem(int b);
 
 // F1: forward column DFTs over A of the pre-mapped coefficients.
