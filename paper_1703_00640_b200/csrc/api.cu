@@ -85,7 +85,7 @@ struct Context {
   bool own_stream = false;
   TwiddleCache tw;
   std::map<std::tuple<int64_t, int32_t, int64_t, int64_t, int32_t>, std::unique_ptr<Plan>> plans;
-  DevBuf work_t, work_c, work_z, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf, aggs, zaggs, haggs;
+  DevBuf work_t, work_c, work_z, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf, aggs, zaggs, haggs, ticket;
   ScanSlot scan_u, scan_v, scan_c, scan_h;
   bool debug_sync = false;
   DevStatus* h_status = nullptr;  // pinned
@@ -143,9 +143,13 @@ void check_launch(const char* what) {
   }
 }
 
+// Opt in to the dynamic shared memory a launch needs.  The 48 KB default
+// covers static + dynamic together, so any sizeable request is opted in
+// (a kernel with a few KB of static arrays fails at dynamic sizes just
+// under 48 KB otherwise).
 template <class K>
 void set_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024)
+  if (bytes > 16 * 1024)
     TMG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(bytes)));
 }
@@ -419,14 +423,24 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       }
       static const bool old_carry = getenv("TMG_OLD_CARRY") != nullptr;
       const int lam = (p.mode == PMode::kFull) ? 0 : int(pl.mc.lambda);
-      const size_t smem2 = carry2_smem(int(p.b), lam);
+      // limbs per thread: 4 when the block's coefficient window stays small
+      // (wide chunks), else 2 (more CTAs per SM for narrow chunks)
+      const int pt = carry2_smem(int(p.b), lam, 4) <= size_t(64) * 1024 ? 4 : 2;
+      const size_t smem2 = carry2_smem(int(p.b), lam, pt);
       if (!old_carry && smem2 <= kMaxDynSmem && 64 * pl.ML + 64 < (int64_t(1) << 32)) {
         a.fb = make_fastdiv(uint32_t(p.b));
-        const unsigned blocks2 = unsigned((pl.ML + kC2Limbs - 1) / kC2Limbs);
-        cx.aggs.ensure(size_t(blocks2) * 4 + 16);
+        const int64_t limbs = int64_t(kC2Threads) * pt;
+        const unsigned blocks2 = unsigned((pl.ML + limbs - 1) / limbs);
+        cx.aggs.ensure(size_t(blocks2) * 8 + 16);
         a.aggs = cx.aggs.as<uint32_t>();
+        a.cins = reinterpret_cast<int*>(a.aggs + blocks2);
+        if (!cx.ticket.p) {
+          cx.ticket.ensure(64);
+          TMG_CUDA(cudaMemsetAsync(cx.ticket.p, 0, 64, st));
+        }
+        a.ticket = cx.ticket.as<uint32_t>();
         a.sbuf = cx.work_t.p;  // the transform buffer is free after k_ilast
-        CarryLanesFn lanes = carry_lanes_kernel(lam);
+        CarryLanesFn lanes = carry_lanes_kernel(lam, pt);
         set_smem(lanes, smem2);
         {
           KTimer kt(cx, "k_carry_lanes", double(pl.K) * 8.0 + double(pl.ML) * 16.0, int(p.mode));
@@ -437,7 +451,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
           KTimer kt(cx, "k_carry_apply",
                     double(pl.ML) * 16.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0,
                     int(p.mode));
-          k_carry_apply<<<blocks2, kC2Threads, 0, st>>>(a);
+          carry_apply_kernel(pt)<<<blocks2, kC2Threads, 0, st>>>(a);
         }
         check_launch("k_carry_apply");
         kernels += 2;

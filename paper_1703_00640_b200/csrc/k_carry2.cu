@@ -1,18 +1,18 @@
 // Post-map, rounding and carry propagation as two kernels without
 // inter-block waiting.
 //
-//   k_carry_lanes  every block owns kC2Limbs consecutive limbs; each thread
-//                  the coefficients whose bit offsets k b land in its
-//                  kC2PerThread limbs.  It post-maps them (beta* low, delta+
+//   k_carry_lanes  every block owns 256 x PT consecutive limbs (PT = 2 or 4
+//                  by the window size); each thread the coefficients whose
+//                  bit offsets k b land in its PT limbs.  It post-maps them (beta* low, delta+
 //                  high; nothing for the full product), rounds them with the
 //                  reference's tripwire, forms the signed 128-bit lanes
 //                  lane_m = sum e_k << (k b - 64 m) and the limb sums
 //                  s_m = lo(lane_m) + hi(lane_{m-1}), writes s_m to scratch
 //                  and the block's composed carry transfer function to
-//                  aggs[blk].
-//   k_carry_apply  carry-in of a block = the composition of the aggregates
-//                  before it (read in parallel, no look-back), then a block
-//                  scan of the limb transfer functions and the output limbs.
+//                  aggs[blk]; the last block to finish scans the aggregates
+//                  into every block's carry-in (cins).
+//   k_carry_apply  from the block's carry-in, a block scan of the limb
+//                  transfer functions and the output limbs.
 //
 // Compared with the single-pass look-back kernel (k_carry), no block ever
 // waits on another: the lanes kernel runs at full occupancy and its
@@ -37,7 +37,6 @@ namespace tmg {
 namespace {
 
 constexpr int kT = kC2Threads;
-constexpr int kPT = kC2PerThread;
 
 // First coefficient of lane m, ceil(64 m / b), clamped to K.  The host
 // takes this path only when every bit offset fits in 32 bits
@@ -156,8 +155,9 @@ __device__ __forceinline__ void coeffs_run(const CarryArgs& a, const double* __r
   }
 }
 
-template <int LAM>
+template <int LAM, int kPT>
 __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
+  constexpr int64_t kLimbs = int64_t(kT) * kPT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t sw[32];
   __shared__ long long s_hi[kT];
@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
   const int b = mc.b;
   const int64_t K = a.K;
   const int64_t blk = blockIdx.x;
-  const int64_t ms = blk * kC2Limbs;
-  const int64_t me = min(a.ML, ms + kC2Limbs);
+  const int64_t ms = blk * kLimbs;
+  const int64_t me = min(a.ML, ms + kLimbs);
   const int64_t kbase = kfirst(ms > 0 ? ms - 1 : 0, a.fb, K);
   const int64_t kend = kfirst(me, a.fb, K);
   // staged convolution window (post-map neighbourhood: lambda below, one above)
@@ -265,34 +265,49 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
     if ((tid & 31) == 0) status_merge(a.status, e, m, 0);
   }
   if (flags) atomicOr(&s_flags, flags);
+  // the last block to finish turns the per-block functions into each
+  // block's carry-in (one exclusive scan instead of a prefix per block)
+  __shared__ uint32_t s_last;
+  if (tid == 0) {
+    __threadfence();
+    s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  }
   __syncthreads();
   if (tid == 0 && s_flags) atomicOr(&a.status->flags, s_flags);
+  if (s_last) {
+    __threadfence();
+    const uint32_t B = gridDim.x;
+    const uint32_t Q = (B + kT - 1) / kT;
+    const uint32_t i0 = uint32_t(tid) * Q, i1 = min(B, i0 + Q);
+    uint32_t g = kTfIdentity;
+    for (uint32_t i = i0; i < i1; ++i) g = tf_compose(g, __ldcg(a.aggs + i));
+    uint32_t tot;
+    uint32_t ex = block_scan_tf(g, sw, &tot);
+    for (uint32_t i = i0; i < i1; ++i) {
+      a.cins[i] = tf_apply(ex, 0);
+      ex = tf_compose(ex, __ldcg(a.aggs + i));
+    }
+    if (tid == 0) *a.ticket = 0;
+  }
 }
 
 }  // namespace
 
+template <int kPT>
 __global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
+  constexpr int64_t kLimbs = int64_t(kT) * kPT;
   __shared__ uint32_t sw[32];
   __shared__ uint32_t s_flags, s_low;
   const int tid = threadIdx.x;
   const MapConsts& mc = a.mc;
   const int64_t blk = blockIdx.x;
-  const int64_t ms = blk * kC2Limbs;
-  const int64_t me = min(a.ML, ms + kC2Limbs);
+  const int64_t ms = blk * kLimbs;
+  const int64_t me = min(a.ML, ms + kLimbs);
   if (tid == 0) {
     s_flags = 0;
     s_low = 0;
   }
-  // carry into the block: aggregates of blocks 0 .. blk-1 in order
-  uint32_t g = kTfIdentity;
-  {
-    const int64_t Q = (blk + kT - 1) / kT;
-    const int64_t i0 = int64_t(tid) * Q, i1 = min(blk, i0 + Q);
-    for (int64_t i = i0; i < i1; ++i) g = tf_compose(g, __ldg(a.aggs + i));
-  }
-  uint32_t pre;
-  (void)block_scan_tf(g, sw, &pre);
-  const int cin = tf_apply(pre, 0);
+  const int cin = __ldg(a.cins + blk);  // carry into the block (k_carry_lanes)
   // limbs of this thread
   const int64_t m0 = ms + int64_t(tid) * kPT;
   const ulonglong2* sm = reinterpret_cast<const ulonglong2*>(a.sbuf);
@@ -356,23 +371,27 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
   }
 }
 
-size_t carry2_smem(int b, int lam) {
-  const int64_t nk = (64 * int64_t(kC2Limbs + 1) + b - 1) / b + 4;
+size_t carry2_smem(int b, int lam, int pt) {
+  const int64_t nk = (64 * int64_t(kC2Threads * pt + 1) + b - 1) / b + 4;
   return size_t(nk + lam + 8) * 8 + size_t(nk + 4) * 8 + 64;
 }
 
-CarryLanesFn carry_lanes_kernel(int lam) {
+template <int PT>
+CarryLanesFn lanes_pt(int lam) {
   switch (lam) {
-    case 0: return k_carry_lanes<0>;
-    case 1: return k_carry_lanes<1>;
-    case 2: return k_carry_lanes<2>;
-    case 3: return k_carry_lanes<3>;
-    case 4: return k_carry_lanes<4>;
-    case 5: return k_carry_lanes<5>;
-    case 6: return k_carry_lanes<6>;
-    case 7: return k_carry_lanes<7>;
-    default: return k_carry_lanes<8>;
+    case 0: return k_carry_lanes<0, PT>;
+    case 1: return k_carry_lanes<1, PT>;
+    case 2: return k_carry_lanes<2, PT>;
+    case 3: return k_carry_lanes<3, PT>;
+    case 4: return k_carry_lanes<4, PT>;
+    case 5: return k_carry_lanes<5, PT>;
+    case 6: return k_carry_lanes<6, PT>;
+    case 7: return k_carry_lanes<7, PT>;
+    default: return k_carry_lanes<8, PT>;
   }
 }
+
+CarryLanesFn carry_lanes_kernel(int lam, int pt) { return pt == 4 ? lanes_pt<4>(lam) : lanes_pt<2>(lam); }
+CarryLanesFn carry_apply_kernel(int pt) { return pt == 4 ? k_carry_apply<4> : k_carry_apply<2>; }
 
 }  // namespace tmg

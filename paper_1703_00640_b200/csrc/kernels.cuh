@@ -188,6 +188,8 @@ struct CarryArgs {
   // two-kernel carry (k_carry2.cu)
   void* sbuf;       // limb sums s_m, 16 B per limb
   uint32_t* aggs;   // per-block carry transfer functions
+  int* cins;        // per-block carry-in (written by the last lanes block)
+  uint32_t* ticket; // completion counter of k_carry_lanes (zero between launches)
   FastDiv fb;       // division by b
 };
 constexpr int kCarryThreads = 256;
@@ -195,12 +197,10 @@ constexpr int kCarryPerThread = 2;
 __global__ void k_carry(CarryArgs a);
 size_t carry_smem(int b);
 constexpr int kC2Threads = 256;
-constexpr int kC2PerThread = 4;
-constexpr int kC2Limbs = kC2Threads * kC2PerThread;
 typedef void (*CarryLanesFn)(CarryArgs);
-CarryLanesFn carry_lanes_kernel(int lam);
-__global__ void k_carry_apply(CarryArgs a);
-size_t carry2_smem(int b, int lam);
+CarryLanesFn carry_lanes_kernel(int lam, int pt);
+CarryLanesFn carry_apply_kernel(int pt);
+size_t carry2_smem(int b, int lam, int pt);
 
 struct HighRoundArgs {
   const uint64_t* tbuf;
