@@ -480,6 +480,11 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.status = status;
       cx.haggs.ensure(size_t(blocks) * 4 + 16);
       a.aggs = cx.haggs.as<uint32_t>();
+      if (!cx.ticket.p) {
+        cx.ticket.ensure(64);
+        TMG_CUDA(cudaMemsetAsync(cx.ticket.p, 0, 64, st));
+      }
+      a.ticket = cx.ticket.as<uint32_t>() + 1;
       {
         KTimer kt(cx, "k_high_agg", double(pl.ML) * 8.0, int(p.mode));
         k_high_agg<<<blocks, kCarryThreads, 0, st>>>(a);

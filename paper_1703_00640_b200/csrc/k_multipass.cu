@@ -830,6 +830,18 @@ k_high_round(HighRoundArgs a) {
     if (s_flags) atomicOr(&a.status->flags, s_flags);
     if (s_top) atomicOr(&a.status->high_topbit, 1u);
     if (s_low) atomicOr(&a.status->high_lownz, 1u);
+    // the last block settles this product's range test (w in [0, 2^n]) and
+    // clears the high-product words for the next product on the stream
+    __threadfence();
+    if (atomicAdd(a.ticket, 1u) == gridDim.x - 1) {
+      __threadfence();
+      volatile DevStatus* st = a.status;
+      if (st->high_topbit && st->high_lownz) atomicOr(&a.status->flags, uint32_t(kFlagHighRange));
+      st->high_topbit = 0;
+      st->high_lownz = 0;
+      st->high_sticky = 0;
+      *a.ticket = 0;
+    }
   }
 }
 

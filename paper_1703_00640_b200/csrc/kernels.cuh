@@ -213,6 +213,7 @@ struct HighRoundArgs {
   ScanState scan;
   DevStatus* status;
   uint32_t* aggs;  // per-block increment transfer functions (k_high_agg)
+  uint32_t* ticket;  // completion counter (zero between launches)
 };
 __global__ void k_high_agg(HighRoundArgs a);
 __global__ void k_high_round(HighRoundArgs a);
