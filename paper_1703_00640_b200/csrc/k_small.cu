@@ -111,12 +111,11 @@ k_small_product(SmallArgs a) {
     double2 nv[kMaxPer];
     const double tu = (mc.mode == kModeHigh) ? sd[0] : 0.0;
     const double tv = (mc.mode == kModeHigh) ? sd[1] : 0.0;
-    auto Du = [&](int64_t i) { return buf[padidx(uint32_t(i))].x; };
-    auto Dv = [&](int64_t i) { return buf[padidx(uint32_t(i))].y; };
+    auto D2 = [&](int64_t i) { return buf[padidx(uint32_t(i))]; };
 #pragma unroll
     for (int k = 0; k < kMaxPer; ++k) {
       int64_t j = tid + int64_t(k) * nthr;
-      if (j < N) nv[k] = make_double2(premap(mc, Du, j, tu), premap(mc, Dv, j, tv));
+      if (j < N) nv[k] = premap2(mc, D2, j, tu, tv);
     }
     __syncthreads();
 #pragma unroll
@@ -163,17 +162,45 @@ k_small_product(SmallArgs a) {
   };
   const int64_t M = (mc.mode == kModeFull) ? L : (mc.mode == kModeLow ? N : N + 1);
   double psi = 0.0;
-  if (mc.mode == kModeHigh) psi = high_psi(mc, W, sd[2]);
+  if (mc.mode == kModeHigh) {
+    // once per product (maps_f64.cpp:363-371), shared through sd[3]
+    if (tid == 0) sd[3] = high_psi(mc, W, sd[2]);
+    __syncthreads();
+    psi = sd[3];
+  }
   RoundAcc ra;
   long long cv[kMaxPer];
+  // full / low: strided elements; high: kMaxPer consecutive elements per
+  // thread so the folded buffer hbuf(i - 1) of x_i is the previous hbuf(i)
+  const bool runs = mc.mode == kModeHigh;
+  auto elem = [&](int k) -> int64_t {
+    return runs ? int64_t(tid) * kMaxPer + k : tid + int64_t(k) * nthr;
+  };
+  double hprev = 0.0;
+  if (runs && int64_t(tid) * kMaxPer < M) {
+    const int64_t i0 = int64_t(tid) * kMaxPer;
+    hprev = (i0 >= 1 && i0 - 1 < N) ? high_buf(mc, W, i0 - 1) : 0.0;
+  }
 #pragma unroll
   for (int k = 0; k < kMaxPer; ++k) {
-    int64_t i = tid + int64_t(k) * nthr;
+    const int64_t i = elem(k);
     if (i < M) {
       double x;
-      if (mc.mode == kModeFull) x = W(i);
-      else if (mc.mode == kModeLow) x = postmap_low(mc, W, i);
-      else x = postmap_high(mc, W, i, psi);
+      if (mc.mode == kModeFull) {
+        x = W(i);
+      } else if (mc.mode == kModeLow) {
+        x = postmap_low(mc, W, i);
+      } else {
+        // postmap_high (maps_f64.cpp:372-383) with hbuf(i - 1) carried over
+        const double hk = (i < N) ? high_buf(mc, W, i) : 0.0;
+        double v;
+        if (i == N) v = psi - hprev * mc.step;
+        else if (i == 0) v = hk;
+        else v = hk - hprev * mc.step;
+        if (i < mc.nfold) v -= psi * mc.fold[i];
+        x = v * mc.scale_out;
+        hprev = hk;
+      }
       cv[k] = ra.round(x);
     }
   }
@@ -181,7 +208,7 @@ k_small_product(SmallArgs a) {
   long long* cb = reinterpret_cast<long long*>(buf);
 #pragma unroll
   for (int k = 0; k < kMaxPer; ++k) {
-    int64_t i = tid + int64_t(k) * nthr;
+    const int64_t i = elem(k);
     if (i < M) cb[i] = cv[k];
   }
   flags |= ra.flags;

@@ -45,6 +45,45 @@ __device__ __forceinline__ double premap(const MapConsts& mc, const DF& D,
   return acc;
 }
 
+// premap of both operands at once (D2(i) = (digit of u, digit of v)): the
+// series coefficients are computed once for the pair.  Same values as two
+// premap calls (a fold term with top = 0 adds an exact zero).
+template <class DF2>
+__device__ __forceinline__ double2 premap2(const MapConsts& mc, const DF2& D2, int64_t j,
+                                           double topu, double topv) {
+  const int64_t N = mc.N;
+  const double Nd = double(N);
+  const int fam = (mc.mode == kModeLow) ? 0 : 2;
+  const int lam = mc.lambda;
+  double au = 0.0, av = 0.0;
+  RowLoopDown<kMaxLambda>::run([&](auto rc) {
+    constexpr int r = decltype(rc)::value;
+    if (r < lam) {
+      int64_t k = j - r;
+      if (k < 0) k += N;
+      const double cf = coef_r<r>(fam, double(k), Nd, mc.cpre[r]);
+      const double2 d = D2(k);
+      au += d.x * cf;
+      av += d.y * cf;
+    }
+  });
+  if (mc.mode == kModeHigh && j < mc.nfold + lam) {
+    RowLoop<kMaxLambda>::run([&](auto rc) {
+      constexpr int r = decltype(rc)::value;
+      if (r < lam) {
+        int64_t k = j - r;
+        if (k < 0) k += N;
+        if (k < mc.nfold) {
+          const double g = mc.fold[k] * coef_r<r>(2, double(k), Nd, mc.cpre[r]);
+          if (topu != 0.0) au += topu * g;
+          if (topv != 0.0) av += topv * g;
+        }
+      }
+    });
+  }
+  return make_double2(au, av);
+}
+
 // Root-channel value of a high-split operand (maps_f64.cpp:319-328):
 // theta = sum_d in[N - d] * inv_root^d over the first nroot terms.
 template <class DF>
