@@ -207,10 +207,15 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     a.inv = pl.inv;
     a.mc = pl.mc;
     a.status = status;
-    set_smem(k_small_product, pl.small_smem);
+    static const bool one_cta = getenv("TMG_SMALL_1CTA") != nullptr;
+    // the 2-CTA variant only pays when two CTAs' shared memory fits an SM
+    // (228 KB, 1 KB reserved per CTA); otherwise its spills cost for nothing
+    const bool two = pl.small_threads <= 384 && 2 * (pl.small_smem + 1024) <= size_t(228) * 1024;
+    auto sk = (two && !one_cta) ? k_small_product_2 : k_small_product;
+    set_smem(sk, pl.small_smem);
     {
       KTimer kt(cx, "k_small_product", double(count) * double(2 * pl.nlimbs + pl.out_limbs) * 8.0, int(p.mode));
-      k_small_product<<<unsigned(count), pl.small_threads, pl.small_smem, st>>>(a);
+      sk<<<unsigned(count), pl.small_threads, pl.small_smem, st>>>(a);
     }
     check_launch("k_small_product");
     cx.last_kernels = 1;

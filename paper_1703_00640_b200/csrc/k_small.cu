@@ -29,8 +29,24 @@ constexpr int kMaxPer = 18;  // values per thread held across a barrier
 
 }  // namespace
 
+template <int MAXT, int MINB>
+__device__ __forceinline__ void small_product_body(const SmallArgs& a);
+
+// Two instantiations: up to 512 threads at 128 registers (one CTA per SM),
+// and up to 384 threads at <= 85 registers so that two CTAs share an SM --
+// products of L <= 6144 (config 4's 2^16-bit batch) are latency-bound at one
+// 10-warp CTA per SM.
 __global__ void __launch_bounds__(512, 1)
 k_small_product(SmallArgs a) {
+  small_product_body<512, 1>(a);
+}
+__global__ void __launch_bounds__(384, 2)
+k_small_product_2(SmallArgs a) {
+  small_product_body<384, 2>(a);
+}
+
+template <int MAXT, int MINB>
+__device__ __forceinline__ void small_product_body(const SmallArgs& a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int64_t L = a.L;

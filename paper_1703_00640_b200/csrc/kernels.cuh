@@ -39,6 +39,7 @@ size_t mid_smem_bytes(uint32_t C, uint32_t inv_stablen);
 size_t col_smem_bytes(uint32_t R, uint32_t c);
 
 __global__ void k_small_product(SmallArgs a);
+__global__ void k_small_product_2(SmallArgs a);  // <= 384 threads, 2 CTAs per SM
 
 // ---------------------------------------------------------------------------
 // Multi-pass pipeline.  The complex transform of length L = A * B * C runs as
