@@ -86,7 +86,7 @@ struct Context {
   TwiddleCache tw;
   std::map<std::tuple<int64_t, int32_t, int64_t, int64_t, int32_t>, std::unique_ptr<Plan>> plans;
   DevBuf work_t, work_c, work_z, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf, aggs, zaggs, haggs, ticket;
-  ScanSlot scan_u, scan_v, scan_c, scan_h;
+  ScanSlot scan_c;  // look-back state of the single-pass carry (k_carry)
   bool debug_sync = false;
   DevStatus* h_status = nullptr;  // pinned
   int32_t last_kernels = 0;
@@ -253,7 +253,6 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.mc = pl.mc;
       a.zt = ztile(pl, L);
       const unsigned blocks = unsigned((pl.count + kZgenChunks - 1) / kZgenChunks);
-      a.scan = cx.scan_u.next(blocks);
       a.status = status;
       cx.zaggs.ensure(size_t(blocks) * 4 + 16);
       a.aggs = cx.zaggs.as<uint32_t>();
@@ -337,16 +336,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       spectral_scale(L, &a.scale, &a.scale_lo);
       const unsigned npairs = (pl.A * pl.B) / 2 + 1;
       static const bool no_ct = getenv("TMG_NO_CT") != nullptr;
-      static const bool mid8 = getenv("TMG_MID8") != nullptr;
-      if (pl.C == 4096 && pl.mid8_ok && mid8 && !no_ct) {
-        a.fwd = pl.fC8;
-        a.inv = pl.iC8;
-        const size_t sm8 = mid_smem_bytes(4096, 0);
-        set_smem(k_mid_4096_r8, sm8);
-        const unsigned grid = std::min<unsigned>(npairs, unsigned(cx.num_sms));
-        KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode));
-        k_mid_4096_r8<<<grid, kMid8Threads, sm8, st>>>(a);
-      } else if (pl.C == 4096 && pl.mid_shared_table && !no_ct) {
+      if (pl.C == 4096 && pl.mid_shared_table && !no_ct) {
         // compile-time schedule, persistent over row pairs
         set_smem(k_mid_4096, pl.smem_mid);
         const unsigned grid = std::min<unsigned>(npairs, unsigned(cx.num_sms));
@@ -481,7 +471,6 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       a.WL = pl.ML - (pl.shift_s >> 6);
       const int64_t LB = kCarryThreads * kCarryPerThread;
       const unsigned blocks = unsigned((a.WL + LB - 1) / LB);
-      a.scan = cx.scan_h.next(blocks);
       a.status = status;
       cx.haggs.ensure(size_t(blocks) * 4 + 16);
       a.aggs = cx.haggs.as<uint32_t>();

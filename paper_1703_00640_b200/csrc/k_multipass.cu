@@ -500,13 +500,6 @@ k_mid_4096(MidArgs a) {
   mid_4096_body<kMidCtThreads, Sched<16, 16, 16>, Sched<16, 16, 8>>(a);
 }
 
-// 32-warp variant: radix-8 schedules (4096 = 8^4, 2048 = 8 x 8 x 8 x 4),
-// one butterfly of at most 8 values per thread and stage, 64 registers.
-__global__ void __launch_bounds__(kMid8Threads)
-k_mid_4096_r8(MidArgs a) {
-  mid_4096_body<kMid8Threads, Sched<8, 8, 8, 8>, Sched<8, 8, 8, 4>>(a);
-}
-
 // ---------------------------------------------------------------------------
 struct CoefSink {
   double2* coef;

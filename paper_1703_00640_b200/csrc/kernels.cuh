@@ -93,7 +93,6 @@ struct ZgenArgs {
   uint32_t* cbits_v;
   double2* z;         // pre-mapped coefficients (N entries)
   MapConsts mc;
-  ScanState scan;
   DevStatus* status;
   uint32_t* aggs;  // per-block carry transfer functions (k_zstat)
   ZTile zt;        // layout of z as k_f1 reads it
@@ -160,8 +159,6 @@ __global__ void k_mid(MidArgs a);
 // C = 4096 row pass with compile-time schedules, persistent over row pairs.
 constexpr int kMidCtThreads = 512;
 __global__ void k_mid_4096(MidArgs a);
-constexpr int kMid8Threads = 1024;
-__global__ void k_mid_4096_r8(MidArgs a);
 
 struct ILastArgs {
   const double2* data;  // S[k_a][...] with geometry g (outer = 0)
@@ -211,7 +208,6 @@ struct HighRoundArgs {
   int64_t ML;   // limbs of t
   int64_t WL;   // limbs of w examined (covers every bit of t >> s)
   int32_t shift_s;
-  ScanState scan;
   DevStatus* status;
   uint32_t* aggs;  // per-block increment transfer functions (k_high_agg)
   uint32_t* ticket;  // completion counter (zero between launches)

@@ -299,6 +299,49 @@ __device__ __forceinline__ uint32_t block_scan_tf(uint32_t f, uint32_t* sw,
   return tf_compose(wex, excl);
 }
 
+// ----------------------------------------------------------------------------
+// Kill / generate / propagate codes of the balanced split's carry chains
+// (carries are 0 or 1 there): 0 = K (carry out 0), 1 = G (carry out 1),
+// 2 = P (carry out = carry in); two operands packed in bits [0,2) and [2,4).
+// Composition "f then g" keeps g unless g propagates; applying f to carries
+// c (codes 0 / 1 per operand) is kgp_compose(c, f).
+constexpr uint32_t kKgpIdentity = 2u | (2u << 2);
+__device__ __forceinline__ uint32_t kgp_compose(uint32_t f, uint32_t g) {
+  const uint32_t pm = (g >> 1) & ~g & 0x5u;  // fields of g equal to P (binary 10)
+  const uint32_t M = pm | (pm << 1);
+  return (g & ~M) | (f & M);
+}
+
+__device__ __forceinline__ uint32_t block_scan_kgp(uint32_t f, uint32_t* sw, uint32_t* agg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  uint32_t inc = f;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc = kgp_compose(o, inc);
+  }
+  uint32_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) excl = kKgpIdentity;
+  __syncthreads();
+  if (lane == 31) sw[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t v = lane < nw ? sw[lane] : kKgpIdentity;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= off) v = kgp_compose(o, v);
+    }
+    sw[lane] = v;
+  }
+  __syncthreads();
+  const uint32_t wex = warp > 0 ? sw[warp - 1] : kKgpIdentity;
+  *agg = sw[nw - 1];
+  __syncthreads();
+  return kgp_compose(wex, excl);
+}
+
 // Warp-parallel decoupled look-back (called by all 32 lanes of one warp):
 // each round reads the state words of the 32 nearest unresolved
 // predecessors at once, composes their aggregates with a warp reduction and
@@ -349,183 +392,6 @@ __device__ __forceinline__ int lookback_warp(unsigned long long* state,
     *(volatile unsigned long long*)(state + blk) = ep | (2ull << 30) | uint64_t(out + 1);
   }
   return carry_in;
-}
-
-// Decoupled look-back over per-block aggregates (one thread per block);
-// carry0 is the carry into block 0.
-// state words: [63:32] epoch, [31:30] flag (1 aggregate, 2 inclusive),
-// [5:0] payload (transfer code, or carry + 1 for inclusive).
-__device__ __forceinline__ int lookback_carry(unsigned long long* state,
-                                              uint32_t blk, uint32_t agg,
-                                              uint32_t epoch, int carry0) {
-  const unsigned long long ep = (unsigned long long)epoch << 32;
-  int carry_in = 0;
-  if (blk == 0) {
-    carry_in = carry0;
-  } else {
-    *(volatile unsigned long long*)(state + blk) = ep | (1ull << 30) | agg;
-    uint32_t E = kTfIdentity;
-    int64_t j = int64_t(blk) - 1;
-    while (true) {
-      unsigned long long w = *(volatile unsigned long long*)(state + j);
-      if ((w >> 32) != epoch) continue;
-      uint32_t flag = uint32_t(w >> 30) & 3u;
-      if (flag == 0) continue;
-      uint32_t pay = uint32_t(w) & 63u;
-      if (flag == 2) {
-        carry_in = tf_apply(E, int(pay) - 1);
-        break;
-      }
-      E = tf_compose(pay, E);
-      --j;
-    }
-  }
-  int out = tf_apply(agg, carry_in);
-  *(volatile unsigned long long*)(state + blk) =
-      ep | (2ull << 30) | uint64_t(out + 1);
-  return carry_in;
-}
-
-}  // namespace tmg
-
-namespace tmg {
-
-// ----------------------------------------------------------------------------
-// Two independent carry chains (operands u and v) scanned together: the
-// transfer codes of both chains sit side by side (bits 0-5 and 6-11) and the
-// carries as codes c+1 (bits 0-1 and 2-3).
-constexpr uint32_t kTf2Identity = kTfIdentity | (kTfIdentity << 6);
-__device__ __forceinline__ uint32_t tf2_compose(uint32_t f, uint32_t g) {
-  return tf_compose(f & 63u, g & 63u) | (tf_compose(f >> 6, g >> 6) << 6);
-}
-__device__ __forceinline__ uint32_t tf2_apply(uint32_t f, uint32_t cc) {
-  const int a = tf_apply(f & 63u, int(cc & 3u) - 1);
-  const int b = tf_apply(f >> 6, int((cc >> 2) & 3u) - 1);
-  return uint32_t(a + 1) | (uint32_t(b + 1) << 2);
-}
-__device__ __forceinline__ uint32_t tf2_pack(uint32_t fu, uint32_t fv) { return fu | (fv << 6); }
-
-// ----------------------------------------------------------------------------
-// Kill / generate / propagate codes of the balanced split's carry chains
-// (carries are 0 or 1 there): 0 = K (carry out 0), 1 = G (carry out 1),
-// 2 = P (carry out = carry in); two operands packed in bits [0,2) and [2,4).
-// Composition "f then g" keeps g unless g propagates; applying f to carries
-// c (codes 0 / 1 per operand) is kgp_compose(c, f).
-constexpr uint32_t kKgpIdentity = 2u | (2u << 2);
-__device__ __forceinline__ uint32_t kgp_compose(uint32_t f, uint32_t g) {
-  const uint32_t pm = (g >> 1) & ~g & 0x5u;  // fields of g equal to P (binary 10)
-  const uint32_t M = pm | (pm << 1);
-  return (g & ~M) | (f & M);
-}
-
-__device__ __forceinline__ uint32_t block_scan_kgp(uint32_t f, uint32_t* sw, uint32_t* agg) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  uint32_t inc = f;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
-    if (lane >= off) inc = kgp_compose(o, inc);
-  }
-  uint32_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
-  if (lane == 0) excl = kKgpIdentity;
-  __syncthreads();
-  if (lane == 31) sw[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t v = lane < nw ? sw[lane] : kKgpIdentity;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t o = __shfl_up_sync(0xffffffffu, v, off);
-      if (lane >= off) v = kgp_compose(o, v);
-    }
-    sw[lane] = v;
-  }
-  __syncthreads();
-  const uint32_t wex = warp > 0 ? sw[warp - 1] : kKgpIdentity;
-  *agg = sw[nw - 1];
-  __syncthreads();
-  return kgp_compose(wex, excl);
-}
-
-// Block-wide exclusive scan of paired transfer functions.
-__device__ __forceinline__ uint32_t block_scan_tf2(uint32_t f, uint32_t* sw,
-                                                   uint32_t* agg) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  uint32_t inc = f;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
-    if (lane >= off) inc = tf2_compose(o, inc);
-  }
-  uint32_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
-  if (lane == 0) excl = kTf2Identity;
-  __syncthreads();
-  if (lane == 31) sw[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t v = lane < nw ? sw[lane] : kTf2Identity;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      uint32_t o = __shfl_up_sync(0xffffffffu, v, off);
-      if (lane >= off) v = tf2_compose(o, v);
-    }
-    sw[lane] = v;
-  }
-  __syncthreads();
-  uint32_t wex = warp > 0 ? sw[warp - 1] : kTf2Identity;
-  *agg = sw[nw - 1];
-  __syncthreads();
-  return tf2_compose(wex, excl);
-}
-
-// Warp-parallel decoupled look-back for paired chains (see lookback_warp);
-// carry codes in and out.  State payload: 12-bit aggregate or 4-bit carry
-// code.
-__device__ __forceinline__ uint32_t lookback_warp2(unsigned long long* state,
-                                                   uint32_t blk, uint32_t agg,
-                                                   uint32_t epoch, uint32_t cc0) {
-  const int lane = threadIdx.x & 31;
-  const unsigned long long ep = (unsigned long long)epoch << 32;
-  uint32_t cin = cc0;
-  if (blk != 0) {
-    if (lane == 0)
-      *(volatile unsigned long long*)(state + blk) = ep | (1ull << 30) | agg;
-    uint32_t E = kTf2Identity;
-    int64_t base = int64_t(blk) - 1;
-    while (true) {
-      const int64_t j = base - lane;
-      unsigned long long w = 0;
-      if (j >= 0) w = *(volatile unsigned long long*)(state + j);
-      const bool valid = (j >= 0) && ((w >> 32) == epoch) && (((w >> 30) & 3u) != 0);
-      const bool incl = valid && (((w >> 30) & 3u) == 2);
-      const uint32_t bi = __ballot_sync(0xffffffffu, incl);
-      const uint32_t bv = __ballot_sync(0xffffffffu, valid);
-      const int first = bi ? (__ffs(bi) - 1) : 32;
-      const uint32_t need = (first == 32) ? 0xffffffffu : ((1u << first) - 1u);
-      if ((bv & need) != need) continue;
-      uint32_t f = (lane < first) ? uint32_t(w & 0xfffu) : kTf2Identity;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t o = __shfl_down_sync(0xffffffffu, f, off);
-        if (lane + off < 32) f = tf2_compose(o, f);
-      }
-      f = __shfl_sync(0xffffffffu, f, 0);
-      E = tf2_compose(f, E);
-      if (first < 32) {
-        const uint32_t v = __shfl_sync(0xffffffffu, uint32_t(w & 0xfu), first);
-        cin = tf2_apply(E, v);
-        break;
-      }
-      base -= 32;
-    }
-  }
-  if (lane == 0) {
-    const uint32_t out = tf2_apply(agg, cin);
-    *(volatile unsigned long long*)(state + blk) = ep | (2ull << 30) | out;
-  }
-  return cin;
 }
 
 }  // namespace tmg

@@ -427,12 +427,6 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   pl->fC = make_subfft(C, tC, 1, &tw);
   pl->iC = make_subfft(C / 2, tC, 2, &tw);
   pl->mid_shared_table = map_stages(pl->iC, pl->fC);
-  if (C == 4096) {
-    // radix-8 schedules for the 32-warp row pass (k_mid_4096_r8)
-    pl->fC8 = make_subfft(C, tC, 1, &tw, 8);
-    pl->iC8 = make_subfft(C / 2, tC, 2, &tw, 8);
-    pl->mid8_ok = map_stages(pl->iC8, pl->fC8);
-  }
   // TMG_COL_LOGC (testing): cap the columns per CTA of the column passes
   static const int col_logc_cap = getenv("TMG_COL_LOGC") ? atoi(getenv("TMG_COL_LOGC")) : 6;
   pl->logc_f1 = std::min<uint32_t>(pick_logc(A, UL / A, cap), uint32_t(col_logc_cap));

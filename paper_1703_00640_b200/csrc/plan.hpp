@@ -68,8 +68,6 @@ struct Plan {
   int thr_f1 = 0, thr_f2 = 0, thr_i2 = 0, thr_il = 0, thr_mid = 0;
   size_t smem_zgen = 0;
   bool mid_shared_table = false;
-  SubFft fC8{}, iC8{};  // C = 4096 with radix <= 8 (k_mid_4096_r8)
-  bool mid8_ok = false;
   bool colpp = false;  // column passes use the ping-pong kernels (k_*_pp)
   int kernels = 0;
 };
