@@ -76,6 +76,22 @@ struct Profiler {
   }
 };
 
+// Per-product scratch of the multi-pass pipeline: transform buffers, split
+// carry bits, aggregates, completion tickets and the product's status word.
+// The context owns one for single products; a batch runs its products on up
+// to kMaxBatchStreams workspaces, each on its own stream.
+struct Workspace {
+  DevBuf work_t, work_c, work_z, cbu, cbv, aux, tbuf, aggs, zaggs, haggs, ticket, status;
+  ScanSlot scan_c;  // look-back state of the single-pass carry (k_carry)
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+  ~Workspace() {
+    if (done) cudaEventDestroy(done);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+constexpr int kMaxBatchStreams = 8;
+
 struct Context {
   int device = 0;
   int num_sms = 148;
@@ -85,8 +101,9 @@ struct Context {
   bool own_stream = false;
   TwiddleCache tw;
   std::map<std::tuple<int64_t, int32_t, int64_t, int64_t, int32_t>, std::unique_ptr<Plan>> plans;
-  DevBuf work_t, work_c, work_z, cbu, cbv, aux, status, dop_u, dop_v, dop_out, pflags, tbuf, aggs, zaggs, haggs, ticket;
-  ScanSlot scan_c;  // look-back state of the single-pass carry (k_carry)
+  DevBuf status, dop_u, dop_v, dop_out, pflags;
+  Workspace ws0;                                  // single products (context stream)
+  std::vector<std::unique_ptr<Workspace>> wsb;    // batch workspaces (own streams)
   bool debug_sync = false;
   DevStatus* h_status = nullptr;  // pinned
   int32_t last_kernels = 0;
@@ -158,24 +175,313 @@ struct KTimer {
   Context& cx;
   Profiler::Rec rec;
   bool on;
-  KTimer(Context& c, const char* name, double bytes, int mode = -1)
-      : cx(c), on(c.prof.on) {
+  KTimer(Context& c, const char* name, double bytes, int mode = -1,
+         cudaStream_t st = nullptr)
+      : cx(c), on(c.prof.on && (st == nullptr || st == c.stream)) {
     if (on) {
       static const char* kPrefix[] = {"full:", "low:", "high:"};
       rec.name = std::string(mode >= 0 && mode < 3 ? kPrefix[mode] : "") + name;
       rec.bytes = bytes;
       rec.a = cx.prof.get();
       rec.b = cx.prof.get();
-      cudaEventRecord(rec.a, cx.stream);
+      cudaEventRecord(rec.a, st ? st : cx.stream);
     }
   }
   ~KTimer() {
     if (on) {
-      cudaEventRecord(rec.b, cx.stream);
+      cudaEventRecord(rec.b, cx.stream);  // only context-stream launches are timed
       cx.prof.recs.push_back(rec);
     }
   }
 };
+
+// Workspace buffers sized for one product of plan pl.
+size_t workspace_bytes(const Plan& pl) {
+  const int64_t L = pl.L;
+  return size_t(L) * 24 + (size_t(pl.params.N) + size_t(L / std::max<uint32_t>(pl.A, 1))) * 16 +
+         size_t(pl.ML) * 8;
+}
+
+void ensure_workspace(Workspace& w, const Plan& pl) {
+  const Params& p = pl.params;
+  const int64_t L = pl.L;
+  w.work_t.ensure(size_t(L) * 16);
+  w.work_c.ensure(size_t(L) * 8 + 64);
+  // z: N entries, plus up to one row of F1's tiling slack (ZTile)
+  w.work_z.ensure((size_t(p.N) + (pl.kind >= 2 ? size_t(L / pl.A) : 0)) * 16 + 64);
+  const int64_t cwords = (pl.count + 31) / 32 + 1;
+  w.cbu.ensure(size_t(cwords) * 4);
+  w.cbv.ensure(size_t(cwords) * 4);
+  w.aux.ensure(64);
+}
+
+// One multi-pass product on stream st with workspace w; device flags,
+// residuals and the high product's range words go to status.  Returns the
+// number of kernels launched.
+int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* status, Plan& pl,
+                    const uint64_t* u, const uint64_t* v, uint64_t* out) {
+  const Params& p = pl.params;
+  const int64_t L = pl.L;
+  int kernels = 0;
+  {
+    // balanced split + pre-map (both operands)
+    {
+      ZgenArgs a;
+      a.u = u;
+      a.v = v;
+      a.nlimbs = pl.nlimbs;
+      a.n = p.n;
+      a.b = p.b;
+      a.count = pl.count;
+      a.N = p.N;
+      a.lead = pl.lead;
+      a.cbits_u = w.cbu.as<uint32_t>();
+      a.cbits_v = w.cbv.as<uint32_t>();
+      a.z = w.work_z.as<double2>();
+      a.mc = pl.mc;
+      a.zt = ztile(pl, L);
+      const unsigned blocks = unsigned((pl.count + kZgenChunks - 1) / kZgenChunks);
+      a.status = status;
+      w.zaggs.ensure(size_t(blocks) * 4 + 16);
+      a.aggs = w.zaggs.as<uint32_t>();
+      {
+        KTimer kt(cx, "k_zstat", double(2 * pl.nlimbs) * 8.0, int(p.mode), st);
+        k_zstat<<<(blocks + 255) / 256, 256, 0, st>>>(a);
+      }
+      check_launch("k_zstat");
+      ZgenFn zg = zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda));
+      set_smem(zg, pl.smem_zgen);
+      {
+        KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * 16.0, int(p.mode), st);
+        zg<<<blocks, kZgenThreads, pl.smem_zgen, st>>>(a);
+      }
+      check_launch("k_zgen");
+      kernels += 2;
+    }
+    double2* T = w.work_t.as<double2>();
+    {
+      F1Args a;
+      a.z = w.work_z.as<double2>();
+      a.zt = ztile(pl, L);
+      a.out = T;
+      a.ncols = uint32_t(L / pl.A);
+      a.logc = pl.logc_f1;
+      a.fft = pl.fA;
+      a.tw = pl.twL;
+      a.mc = pl.mc;
+      a.u = u;
+      a.v = v;
+      a.nlimbs = pl.nlimbs;
+      a.b = p.b;
+      a.count = pl.count;
+      a.lead = pl.lead;
+      a.cbits_u = w.cbu.as<uint32_t>();
+      a.cbits_v = w.cbv.as<uint32_t>();
+      a.aux = w.aux.as<double>();
+      auto f1k = pl.colpp ? k_f1_pp : k_f1;
+      set_smem(f1k, pl.smem_f1);
+      {
+        KTimer kt(cx, "k_f1", double(p.N) * 16.0 + double(L) * 16.0, int(p.mode), st);
+        f1k<<<a.ncols >> a.logc, pl.thr_f1, pl.smem_f1, st>>>(a);
+      }
+      check_launch("k_f1");
+      ++kernels;
+    }
+    if (pl.kind == 3) {
+      ColArgs a;
+      a.data = T;
+      a.g.os = int64_t(pl.B) * pl.C;
+      a.g.rs = pl.C;
+      a.g.cs = pl.C;
+      a.g.cw = pl.C;
+      a.g.ncols = pl.C;
+      a.logc = pl.logc_f2;
+      a.fft = pl.fB;
+      a.tw = pl.twL;
+      a.inv = 0;
+      a.to = 0;
+      a.tc = 1;
+      a.tmul = pl.A;
+      auto colk = pl.colpp ? k_col_pp : k_col;
+      set_smem(colk, pl.smem_f2);
+      {
+        KTimer kt(cx, "k_col_f2", double(L) * 32.0, int(p.mode), st);
+        colk<<<dim3(pl.C >> a.logc, pl.A), pl.thr_f2, pl.smem_f2, st>>>(a);
+      }
+      check_launch("k_col(f2)");
+      ++kernels;
+    }
+    {
+      MidArgs a;
+      a.data = T;
+      a.A = pl.A;
+      a.B = pl.B;
+      a.C = pl.C;
+      a.fwd = pl.fC;
+      a.inv = pl.iC;
+      a.tw = pl.twL;
+      a.L = uint32_t(L);
+      spectral_scale(L, &a.scale, &a.scale_lo);
+      const unsigned npairs = (pl.A * pl.B) / 2 + 1;
+      static const bool no_ct = getenv("TMG_NO_CT") != nullptr;
+      if (pl.C == 4096 && pl.mid_shared_table && !no_ct) {
+        // compile-time schedule, persistent over row pairs
+        set_smem(k_mid_4096, pl.smem_mid);
+        const unsigned grid = std::min<unsigned>(npairs, unsigned(cx.num_sms));
+        KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode), st);
+        k_mid_4096<<<grid, kMidCtThreads, pl.smem_mid, st>>>(a);
+      } else {
+        set_smem(k_mid, pl.smem_mid);
+        KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode), st);
+        k_mid<<<npairs, pl.thr_mid, pl.smem_mid, st>>>(a);
+      }
+      check_launch("k_mid");
+      ++kernels;
+    }
+    if (pl.kind == 3) {
+      ColArgs a;
+      a.data = T;
+      a.g.os = int64_t(pl.B) * pl.C;
+      a.g.rs = pl.C;
+      a.g.cs = pl.C;
+      a.g.cw = pl.C / 2;
+      a.g.ncols = pl.C / 2;
+      a.logc = pl.logc_i2;
+      a.fft = pl.iB;
+      a.tw = pl.twL;
+      a.inv = 1;
+      a.to = 1;
+      a.tc = 0;
+      a.tmul = pl.C;
+      auto colk = pl.colpp ? k_col_pp : k_col;
+      set_smem(colk, pl.smem_i2);
+      {
+        KTimer kt(cx, "k_col_i2", double(L) * 16.0, int(p.mode), st);
+        colk<<<dim3((pl.C / 2) >> a.logc, pl.A), pl.thr_i2, pl.smem_i2, st>>>(a);
+      }
+      check_launch("k_col(i2)");
+      ++kernels;
+    }
+    double2* coef = w.work_c.as<double2>();
+    {
+      ILastArgs a;
+      a.data = T;
+      a.coef = coef;
+      a.g.os = 0;
+      a.g.rs = int64_t(pl.B) * pl.C;
+      a.g.cs = pl.C;
+      a.g.cw = pl.C / 2;
+      a.g.ncols = pl.B * (pl.C / 2);
+      a.logc = pl.logc_il;
+      a.fft = pl.iA;
+      auto ilk = pl.colpp ? k_ilast_pp : k_ilast;
+      set_smem(ilk, pl.smem_il);
+      {
+        KTimer kt(cx, "k_ilast", double(L) * 16.0, int(p.mode), st);
+        ilk<<<a.g.ncols >> a.logc, pl.thr_il, pl.smem_il, st>>>(a);
+      }
+      check_launch("k_ilast");
+      ++kernels;
+    }
+    {
+      CarryArgs a;
+      a.w = reinterpret_cast<const double*>(coef);
+      a.out = out;
+      a.n = p.n;
+      a.out_limbs = pl.out_limbs;
+      a.K = pl.K;
+      a.ML = pl.ML;
+      a.shift_s = pl.shift_s;
+      a.mc = pl.mc;
+      a.aux = w.aux.as<double>();
+      const int64_t LB = kCarryThreads * kCarryPerThread;
+      const unsigned blocks = unsigned((pl.ML + LB - 1) / LB);
+      a.scan = w.scan_c.next(blocks);
+      a.status = status;
+      if (p.mode == PMode::kHigh) {
+        w.tbuf.ensure(size_t(pl.ML) * 8 + 64);
+        a.tbuf = w.tbuf.as<uint64_t>();
+      } else {
+        a.tbuf = nullptr;
+      }
+      static const bool old_carry = getenv("TMG_OLD_CARRY") != nullptr;
+      const int lam = (p.mode == PMode::kFull) ? 0 : int(pl.mc.lambda);
+      // limbs per thread: 4 when the block's coefficient window stays small
+      // (wide chunks), else 2 (more CTAs per SM for narrow chunks)
+      const int pt = carry2_smem(int(p.b), lam, 4) <= size_t(64) * 1024 ? 4 : 2;
+      const size_t smem2 = carry2_smem(int(p.b), lam, pt);
+      if (!old_carry && smem2 <= kMaxDynSmem && 64 * pl.ML + 64 < (int64_t(1) << 32)) {
+        a.fb = make_fastdiv(uint32_t(p.b));
+        const int64_t limbs = int64_t(kC2Threads) * pt;
+        const unsigned blocks2 = unsigned((pl.ML + limbs - 1) / limbs);
+        w.aggs.ensure(size_t(blocks2) * 8 + 16);
+        a.aggs = w.aggs.as<uint32_t>();
+        a.cins = reinterpret_cast<int*>(a.aggs + blocks2);
+        if (!w.ticket.p) {
+          w.ticket.ensure(64);
+          TMG_CUDA(cudaMemsetAsync(w.ticket.p, 0, 64, st));
+        }
+        a.ticket = w.ticket.as<uint32_t>();
+        a.sbuf = w.work_t.p;  // the transform buffer is free after k_ilast
+        CarryLanesFn lanes = carry_lanes_kernel(lam, pt);
+        set_smem(lanes, smem2);
+        {
+          KTimer kt(cx, "k_carry_lanes", double(pl.K) * 8.0 + double(pl.ML) * 16.0, int(p.mode), st);
+          lanes<<<blocks2, kC2Threads, smem2, st>>>(a);
+        }
+        check_launch("k_carry_lanes");
+        {
+          KTimer kt(cx, "k_carry_apply",
+                    double(pl.ML) * 16.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0,
+                    int(p.mode), st);
+          carry_apply_kernel(pt)<<<blocks2, kC2Threads, 0, st>>>(a);
+        }
+        check_launch("k_carry_apply");
+        kernels += 2;
+      } else {
+        set_smem(k_carry, pl.smem_carry);
+        {
+          KTimer kt(cx, "k_carry", double(pl.K) * 8.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0, int(p.mode), st);
+          k_carry<<<blocks, kCarryThreads, pl.smem_carry, st>>>(a);
+        }
+        check_launch("k_carry");
+        ++kernels;
+      }
+    }
+    if (p.mode == PMode::kHigh) {
+      HighRoundArgs a;
+      a.tbuf = w.tbuf.as<uint64_t>();
+      a.out = out;
+      a.n = p.n;
+      a.out_limbs = pl.out_limbs;
+      a.ML = pl.ML;
+      a.shift_s = pl.shift_s;
+      a.WL = pl.ML - (pl.shift_s >> 6);
+      const int64_t LB = kCarryThreads * kCarryPerThread;
+      const unsigned blocks = unsigned((a.WL + LB - 1) / LB);
+      a.status = status;
+      w.haggs.ensure(size_t(blocks) * 4 + 16);
+      a.aggs = w.haggs.as<uint32_t>();
+      if (!w.ticket.p) {
+        w.ticket.ensure(64);
+        TMG_CUDA(cudaMemsetAsync(w.ticket.p, 0, 64, st));
+      }
+      a.ticket = w.ticket.as<uint32_t>() + 1;
+      {
+        KTimer kt(cx, "k_high_agg", double(pl.ML) * 8.0, int(p.mode), st);
+        k_high_agg<<<blocks, kCarryThreads, 0, st>>>(a);
+      }
+      check_launch("k_high_agg");
+      {
+        KTimer kt(cx, "k_high_round", double(pl.ML) * 8.0 + double(pl.out_limbs) * 8.0, int(p.mode), st);
+        k_high_round<<<blocks, kCarryThreads, 0, st>>>(a);
+      }
+      check_launch("k_high_round");
+      kernels += 2;
+    }
+  }
+  return kernels;
+}
 
 // Enqueue one batch of products (device pointers) on the context stream.
 void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
@@ -221,276 +527,51 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     cx.last_kernels = 1;
     return;
   }
-  // multi-pass, one product at a time
-  const int64_t L = pl.L;
-  cx.work_t.ensure(size_t(L) * 16);
-  cx.work_c.ensure(size_t(L) * 8 + 64);
-  // z: N entries, plus up to one row of F1's tiling slack (ZTile)
-  cx.work_z.ensure((size_t(p.N) + (pl.kind >= 2 ? size_t(L / pl.A) : 0)) * 16 + 64);
-  const int64_t cwords = (pl.count + 31) / 32 + 1;
-  cx.cbu.ensure(size_t(cwords) * 4);
-  cx.cbv.ensure(size_t(cwords) * 4);
-  cx.aux.ensure(64);
+  // multi-pass
+  if (count == 1) {
+    ensure_workspace(cx.ws0, pl);
+    cx.last_kernels = enqueue_product(cx, cx.ws0, st, status, pl, du, dv, dout);
+    if (pflags) {
+      k_status_publish<<<1, 1, 0, st>>>(status, pflags, nullptr);
+      check_launch("k_status_publish");
+    }
+    return;
+  }
+  // a batch: products round-robin over up to kMaxBatchStreams workspaces,
+  // each on its own stream with its own status word, published per product
+  // into pflags and merged into the context status
+  const size_t budget = size_t(4) << 30;
+  const int64_t by_mem = int64_t(budget / std::max<size_t>(workspace_bytes(pl), 1));
+  const int S = int(std::max<int64_t>(
+      1, std::min<int64_t>(std::min<int64_t>(count, kMaxBatchStreams), by_mem)));
+  while (int(cx.wsb.size()) < S) {
+    auto w = std::make_unique<Workspace>();
+    TMG_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+    TMG_CUDA(cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming));
+    w->status.ensure(sizeof(DevStatus));
+    cx.wsb.push_back(std::move(w));
+  }
+  cudaEvent_t start = cx.wsb[0]->done;
+  TMG_CUDA(cudaEventRecord(start, st));
+  for (int s2 = 0; s2 < S; ++s2) {
+    Workspace& w = *cx.wsb[s2];
+    ensure_workspace(w, pl);
+    TMG_CUDA(cudaStreamWaitEvent(w.stream, start, 0));
+  }
   int kernels = 0;
   for (int64_t i = 0; i < count; ++i) {
-    const uint64_t* u = du + i * pl.nlimbs;
-    const uint64_t* v = dv + i * pl.nlimbs;
-    uint64_t* out = dout + i * pl.out_limbs;
-    // balanced split + pre-map (both operands)
-    {
-      ZgenArgs a;
-      a.u = u;
-      a.v = v;
-      a.nlimbs = pl.nlimbs;
-      a.n = p.n;
-      a.b = p.b;
-      a.count = pl.count;
-      a.N = p.N;
-      a.lead = pl.lead;
-      a.cbits_u = cx.cbu.as<uint32_t>();
-      a.cbits_v = cx.cbv.as<uint32_t>();
-      a.z = cx.work_z.as<double2>();
-      a.mc = pl.mc;
-      a.zt = ztile(pl, L);
-      const unsigned blocks = unsigned((pl.count + kZgenChunks - 1) / kZgenChunks);
-      a.status = status;
-      cx.zaggs.ensure(size_t(blocks) * 4 + 16);
-      a.aggs = cx.zaggs.as<uint32_t>();
-      {
-        KTimer kt(cx, "k_zstat", double(2 * pl.nlimbs) * 8.0, int(p.mode));
-        k_zstat<<<(blocks + 255) / 256, 256, 0, st>>>(a);
-      }
-      check_launch("k_zstat");
-      ZgenFn zg = zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda));
-      set_smem(zg, pl.smem_zgen);
-      {
-        KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * 16.0, int(p.mode));
-        zg<<<blocks, kZgenThreads, pl.smem_zgen, st>>>(a);
-      }
-      check_launch("k_zgen");
-      kernels += 2;
-    }
-    double2* T = cx.work_t.as<double2>();
-    {
-      F1Args a;
-      a.z = cx.work_z.as<double2>();
-      a.zt = ztile(pl, L);
-      a.out = T;
-      a.ncols = uint32_t(L / pl.A);
-      a.logc = pl.logc_f1;
-      a.fft = pl.fA;
-      a.tw = pl.twL;
-      a.mc = pl.mc;
-      a.u = u;
-      a.v = v;
-      a.nlimbs = pl.nlimbs;
-      a.b = p.b;
-      a.count = pl.count;
-      a.lead = pl.lead;
-      a.cbits_u = cx.cbu.as<uint32_t>();
-      a.cbits_v = cx.cbv.as<uint32_t>();
-      a.aux = cx.aux.as<double>();
-      auto f1k = pl.colpp ? k_f1_pp : k_f1;
-      set_smem(f1k, pl.smem_f1);
-      {
-        KTimer kt(cx, "k_f1", double(p.N) * 16.0 + double(L) * 16.0, int(p.mode));
-        f1k<<<a.ncols >> a.logc, pl.thr_f1, pl.smem_f1, st>>>(a);
-      }
-      check_launch("k_f1");
-      ++kernels;
-    }
-    if (pl.kind == 3) {
-      ColArgs a;
-      a.data = T;
-      a.g.os = int64_t(pl.B) * pl.C;
-      a.g.rs = pl.C;
-      a.g.cs = pl.C;
-      a.g.cw = pl.C;
-      a.g.ncols = pl.C;
-      a.logc = pl.logc_f2;
-      a.fft = pl.fB;
-      a.tw = pl.twL;
-      a.inv = 0;
-      a.to = 0;
-      a.tc = 1;
-      a.tmul = pl.A;
-      auto colk = pl.colpp ? k_col_pp : k_col;
-      set_smem(colk, pl.smem_f2);
-      {
-        KTimer kt(cx, "k_col_f2", double(L) * 32.0, int(p.mode));
-        colk<<<dim3(pl.C >> a.logc, pl.A), pl.thr_f2, pl.smem_f2, st>>>(a);
-      }
-      check_launch("k_col(f2)");
-      ++kernels;
-    }
-    {
-      MidArgs a;
-      a.data = T;
-      a.A = pl.A;
-      a.B = pl.B;
-      a.C = pl.C;
-      a.fwd = pl.fC;
-      a.inv = pl.iC;
-      a.tw = pl.twL;
-      a.L = uint32_t(L);
-      spectral_scale(L, &a.scale, &a.scale_lo);
-      const unsigned npairs = (pl.A * pl.B) / 2 + 1;
-      static const bool no_ct = getenv("TMG_NO_CT") != nullptr;
-      if (pl.C == 4096 && pl.mid_shared_table && !no_ct) {
-        // compile-time schedule, persistent over row pairs
-        set_smem(k_mid_4096, pl.smem_mid);
-        const unsigned grid = std::min<unsigned>(npairs, unsigned(cx.num_sms));
-        KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode));
-        k_mid_4096<<<grid, kMidCtThreads, pl.smem_mid, st>>>(a);
-      } else {
-        set_smem(k_mid, pl.smem_mid);
-        KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode));
-        k_mid<<<npairs, pl.thr_mid, pl.smem_mid, st>>>(a);
-      }
-      check_launch("k_mid");
-      ++kernels;
-    }
-    if (pl.kind == 3) {
-      ColArgs a;
-      a.data = T;
-      a.g.os = int64_t(pl.B) * pl.C;
-      a.g.rs = pl.C;
-      a.g.cs = pl.C;
-      a.g.cw = pl.C / 2;
-      a.g.ncols = pl.C / 2;
-      a.logc = pl.logc_i2;
-      a.fft = pl.iB;
-      a.tw = pl.twL;
-      a.inv = 1;
-      a.to = 1;
-      a.tc = 0;
-      a.tmul = pl.C;
-      auto colk = pl.colpp ? k_col_pp : k_col;
-      set_smem(colk, pl.smem_i2);
-      {
-        KTimer kt(cx, "k_col_i2", double(L) * 16.0, int(p.mode));
-        colk<<<dim3((pl.C / 2) >> a.logc, pl.A), pl.thr_i2, pl.smem_i2, st>>>(a);
-      }
-      check_launch("k_col(i2)");
-      ++kernels;
-    }
-    double2* coef = cx.work_c.as<double2>();
-    {
-      ILastArgs a;
-      a.data = T;
-      a.coef = coef;
-      a.g.os = 0;
-      a.g.rs = int64_t(pl.B) * pl.C;
-      a.g.cs = pl.C;
-      a.g.cw = pl.C / 2;
-      a.g.ncols = pl.B * (pl.C / 2);
-      a.logc = pl.logc_il;
-      a.fft = pl.iA;
-      auto ilk = pl.colpp ? k_ilast_pp : k_ilast;
-      set_smem(ilk, pl.smem_il);
-      {
-        KTimer kt(cx, "k_ilast", double(L) * 16.0, int(p.mode));
-        ilk<<<a.g.ncols >> a.logc, pl.thr_il, pl.smem_il, st>>>(a);
-      }
-      check_launch("k_ilast");
-      ++kernels;
-    }
-    {
-      CarryArgs a;
-      a.w = reinterpret_cast<const double*>(coef);
-      a.out = out;
-      a.n = p.n;
-      a.out_limbs = pl.out_limbs;
-      a.K = pl.K;
-      a.ML = pl.ML;
-      a.shift_s = pl.shift_s;
-      a.mc = pl.mc;
-      a.aux = cx.aux.as<double>();
-      const int64_t LB = kCarryThreads * kCarryPerThread;
-      const unsigned blocks = unsigned((pl.ML + LB - 1) / LB);
-      a.scan = cx.scan_c.next(blocks);
-      a.status = status;
-      if (p.mode == PMode::kHigh) {
-        cx.tbuf.ensure(size_t(pl.ML) * 8 + 64);
-        a.tbuf = cx.tbuf.as<uint64_t>();
-      } else {
-        a.tbuf = nullptr;
-      }
-      static const bool old_carry = getenv("TMG_OLD_CARRY") != nullptr;
-      const int lam = (p.mode == PMode::kFull) ? 0 : int(pl.mc.lambda);
-      // limbs per thread: 4 when the block's coefficient window stays small
-      // (wide chunks), else 2 (more CTAs per SM for narrow chunks)
-      const int pt = carry2_smem(int(p.b), lam, 4) <= size_t(64) * 1024 ? 4 : 2;
-      const size_t smem2 = carry2_smem(int(p.b), lam, pt);
-      if (!old_carry && smem2 <= kMaxDynSmem && 64 * pl.ML + 64 < (int64_t(1) << 32)) {
-        a.fb = make_fastdiv(uint32_t(p.b));
-        const int64_t limbs = int64_t(kC2Threads) * pt;
-        const unsigned blocks2 = unsigned((pl.ML + limbs - 1) / limbs);
-        cx.aggs.ensure(size_t(blocks2) * 8 + 16);
-        a.aggs = cx.aggs.as<uint32_t>();
-        a.cins = reinterpret_cast<int*>(a.aggs + blocks2);
-        if (!cx.ticket.p) {
-          cx.ticket.ensure(64);
-          TMG_CUDA(cudaMemsetAsync(cx.ticket.p, 0, 64, st));
-        }
-        a.ticket = cx.ticket.as<uint32_t>();
-        a.sbuf = cx.work_t.p;  // the transform buffer is free after k_ilast
-        CarryLanesFn lanes = carry_lanes_kernel(lam, pt);
-        set_smem(lanes, smem2);
-        {
-          KTimer kt(cx, "k_carry_lanes", double(pl.K) * 8.0 + double(pl.ML) * 16.0, int(p.mode));
-          lanes<<<blocks2, kC2Threads, smem2, st>>>(a);
-        }
-        check_launch("k_carry_lanes");
-        {
-          KTimer kt(cx, "k_carry_apply",
-                    double(pl.ML) * 16.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0,
-                    int(p.mode));
-          carry_apply_kernel(pt)<<<blocks2, kC2Threads, 0, st>>>(a);
-        }
-        check_launch("k_carry_apply");
-        kernels += 2;
-      } else {
-        set_smem(k_carry, pl.smem_carry);
-        {
-          KTimer kt(cx, "k_carry", double(pl.K) * 8.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0, int(p.mode));
-          k_carry<<<blocks, kCarryThreads, pl.smem_carry, st>>>(a);
-        }
-        check_launch("k_carry");
-        ++kernels;
-      }
-    }
-    if (p.mode == PMode::kHigh) {
-      HighRoundArgs a;
-      a.tbuf = cx.tbuf.as<uint64_t>();
-      a.out = out;
-      a.n = p.n;
-      a.out_limbs = pl.out_limbs;
-      a.ML = pl.ML;
-      a.shift_s = pl.shift_s;
-      a.WL = pl.ML - (pl.shift_s >> 6);
-      const int64_t LB = kCarryThreads * kCarryPerThread;
-      const unsigned blocks = unsigned((a.WL + LB - 1) / LB);
-      a.status = status;
-      cx.haggs.ensure(size_t(blocks) * 4 + 16);
-      a.aggs = cx.haggs.as<uint32_t>();
-      if (!cx.ticket.p) {
-        cx.ticket.ensure(64);
-        TMG_CUDA(cudaMemsetAsync(cx.ticket.p, 0, 64, st));
-      }
-      a.ticket = cx.ticket.as<uint32_t>() + 1;
-      {
-        KTimer kt(cx, "k_high_agg", double(pl.ML) * 8.0, int(p.mode));
-        k_high_agg<<<blocks, kCarryThreads, 0, st>>>(a);
-      }
-      check_launch("k_high_agg");
-      {
-        KTimer kt(cx, "k_high_round", double(pl.ML) * 8.0 + double(pl.out_limbs) * 8.0, int(p.mode));
-        k_high_round<<<blocks, kCarryThreads, 0, st>>>(a);
-      }
-      check_launch("k_high_round");
-      kernels += 2;
-    }
+    Workspace& w = *cx.wsb[i % S];
+    DevStatus* ws = w.status.as<DevStatus>();
+    TMG_CUDA(cudaMemsetAsync(ws, 0, sizeof(DevStatus), w.stream));
+    kernels += enqueue_product(cx, w, w.stream, ws, pl, du + i * pl.nlimbs, dv + i * pl.nlimbs,
+                               dout + i * pl.out_limbs);
+    k_status_publish<<<1, 1, 0, w.stream>>>(ws, pflags ? pflags + i : nullptr, status);
+    check_launch("k_status_publish");
+  }
+  for (int s2 = 0; s2 < S; ++s2) {
+    Workspace& w = *cx.wsb[s2];
+    TMG_CUDA(cudaEventRecord(w.done, w.stream));
+    TMG_CUDA(cudaStreamWaitEvent(st, w.done, 0));
   }
   cx.last_kernels = kernels;
 }
@@ -897,7 +978,7 @@ int tmg_context_set_escalation(tmg_context* ctx, int max_escalations) {
 int tmg_debug_read(tmg_context* ctx, int which, void* host, size_t* bytes) {
   return guarded([&] {
     Context& cx = ctx->cx;
-    const DevBuf& B = (which == 0) ? cx.work_z : cx.work_c;
+    const DevBuf& B = (which == 0) ? cx.ws0.work_z : cx.ws0.work_c;
     if (which != 0 && which != 1) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "debug_read: which");
     *bytes = std::min(*bytes, B.bytes);
     TMG_CUDA(cudaMemcpyAsync(host, B.p, *bytes, cudaMemcpyDeviceToHost, cx.stream));

@@ -838,4 +838,19 @@ k_high_round(HighRoundArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// One batched product's status (its own word): the device flag word goes to
+// flag_out (the batched API's per-product flags) and the status merges into
+// the context's (residuals by max, flags by or).
+__global__ void k_status_publish(const DevStatus* src, uint32_t* flag_out, DevStatus* merge) {
+  uint32_t f = src->flags;
+  if (src->high_topbit && src->high_lownz) f |= kFlagHighRange;
+  if (flag_out) *flag_out = f;
+  if (merge) {
+    atomicMax(&merge->max_err_bits, src->max_err_bits);
+    atomicMax(&merge->max_abs_bits, src->max_abs_bits);
+    if (f) atomicOr(&merge->flags, f);
+  }
+}
+
 }  // namespace tmg

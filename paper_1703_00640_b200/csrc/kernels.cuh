@@ -213,6 +213,7 @@ struct HighRoundArgs {
   uint32_t* ticket;  // completion counter (zero between launches)
 };
 __global__ void k_high_agg(HighRoundArgs a);
+__global__ void k_status_publish(const DevStatus* src, uint32_t* flag_out, DevStatus* merge);
 __global__ void k_high_round(HighRoundArgs a);
 
 // Schoolbook product for operands below the pipeline cutoff (the reference's

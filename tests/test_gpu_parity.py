@@ -415,3 +415,22 @@ def test_wide_chunks_refuse_on_the_64_bit_window_path(ctx):
     u = port.int_to_limbs(int.from_bytes(rng.bytes(nl * 8), "little") & ((1 << n) - 1), nl)
     with pytest.raises(tm.ConvolutionPrecisionFailure):
         ctx.product_limbs(tm.Mode.FULL, u, u, p)
+
+
+@pytest.mark.parametrize("mode", [tm.Mode.LOW, tm.Mode.FULL, tm.Mode.HIGH])
+def test_batched_multipass_products(ctx, mode):
+    """A batch whose transform exceeds one CTA (L > 8192) runs its products
+    concurrently on the batch workspaces; every product exact, per-product
+    flags zero."""
+    n, count = 1 << 17, 24
+    nl = n // 64
+    w = port.mt19937_64(17 + int(mode), 2 * count * nl).reshape(count, 2, nl)
+    u = np.ascontiguousarray(w[:, 0, :])
+    v = np.ascontiguousarray(w[:, 1, :])
+    p = tm.select_params(n, mode)
+    out, flags = ctx.product_batched(p, u, v, return_flags=True)
+    assert ctx.last_stats.transform_length > 8192
+    assert not flags.any()
+    for i in range(count):
+        _check(mode, u[i], v[i], n, tm.from_limbs(out[i]))
+    assert ctx.last_stats.max_round_err < TRIP
