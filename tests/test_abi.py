@@ -66,3 +66,30 @@ def test_limbs_round_trip_and_range():
 def test_params_c_round_trip():
     p = tm.select_params(1 << 20, tm.Mode.HIGH)
     assert tm.Params.from_c(p.to_c()) == p
+
+
+def _build_c_demo(tmp_path):
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_1703_00640_b200")
+    exe = str(tmp_path / "c_abi_demo")
+    subprocess.run(["gcc", "-std=c11", "-O2", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "examples", "c_abi_demo.c"), "-L", lib, "-ltruncmul_b200",
+                    "-Wl,-rpath," + lib, "-o", exe], check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_c_demo_compiles_against_the_header(tmp_path):
+    """The header is plain C: a C program that uses the ABI builds and links."""
+    assert os.path.exists(_build_c_demo(tmp_path))
+
+
+@pytest.mark.gpu
+def test_c_demo_runs(tmp_path):
+    """Full/low/high products from C against a schoolbook product, the
+    precision refusal and its escalation."""
+    import subprocess
+    r = subprocess.run([_build_c_demo(tmp_path)], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK" in r.stdout

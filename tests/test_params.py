@@ -121,3 +121,12 @@ def test_output_limbs():
     assert tm.output_limbs(Mode.LOW, 65) == 2
     assert tm.output_limbs(Mode.HIGH, 64) == 2
     assert tm.output_limbs(Mode.HIGH, 63) == 1
+
+
+@pytest.mark.parametrize("n", list(range(4096, 4600, 37)) + [5001, 7777, 12345, 20011])
+@pytest.mark.parametrize("mode", [Mode.FULL, Mode.LOW, Mode.HIGH])
+def test_accurate_policy_lengths_suit_the_gpu(n, mode):
+    """The accurate (GPU) policy only picks transform lengths divisible by 4
+    (small n used to admit odd 2357-smooth N such as 175)."""
+    p = tm.select_params(n, mode, policy=Policy.ACCURATE)
+    assert p.transform_length % 4 == 0
