@@ -16,6 +16,7 @@
 
 #include "../../include/truncmul_b200.h"
 #include "kernels.cuh"
+#include <unordered_map>
 #include "params.hpp"
 #include "plan.hpp"
 
@@ -146,6 +147,40 @@ ZTile ztile(const Plan& pl, int64_t L) {
 }
 
 
+
+// Every kernel of a product goes out through launch(): with programmatic
+// dependent launch (default; TMG_NO_PDL turns it off) the next kernel on the
+// stream is scheduled while the current one drains and waits in pdl_wait()
+// (common.cuh) for its data, which hides the launch gap between the
+// pipeline's dependent kernels.
+bool g_pdl = getenv("TMG_NO_PDL") == nullptr;
+
+// Launch sites that go without PDL: the first column pass, whose 150-190 KB
+// CTAs scheduled early share SMs with the draining split kernel (measured
+// +7 % on the 2^26 full product).  TMG_PDL_SKIP (testing) replaces the list.
+bool pdl_skip(const char* site) {
+  static const char* skip = getenv("TMG_PDL_SKIP") ? getenv("TMG_PDL_SKIP") : "f1";
+  if (!site) return false;
+  const std::string list = std::string(",") + skip + ",";
+  return list.find(std::string(",") + site + ",") != std::string::npos;
+}
+
+template <class Arg>
+void launch(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+            const Arg& arg, const char* site = nullptr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (g_pdl && !pdl_skip(site)) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TMG_CUDA(cudaLaunchKernelEx(&cfg, kernel, arg));
+}
+
 bool g_debug_sync = getenv("TMG_DEBUG_SYNC") != nullptr;
 
 void check_launch(const char* what) {
@@ -164,11 +199,19 @@ void check_launch(const char* what) {
 // covers static + dynamic together, so any sizeable request is opted in
 // (a kernel with a few KB of static arrays fails at dynamic sizes just
 // under 48 KB otherwise).
+// The attribute is per function: remember what each kernel has been granted
+// (a driver call per launch costs more than the small products' kernels).
 template <class K>
 void set_smem(K kernel, size_t bytes) {
-  if (bytes > 16 * 1024)
-    TMG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(bytes)));
+  if (bytes <= 16 * 1024) return;
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> granted;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& g = granted[reinterpret_cast<const void*>(kernel)];
+  if (bytes <= g) return;
+  TMG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(bytes)));
+  g = bytes;
 }
 
 struct KTimer {
@@ -246,14 +289,14 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.aggs = w.zaggs.as<uint32_t>();
       {
         KTimer kt(cx, "k_zstat", double(2 * pl.nlimbs) * 8.0, int(p.mode), st);
-        k_zstat<<<(blocks + 255) / 256, 256, 0, st>>>(a);
+        launch(k_zstat, dim3((blocks + 255) / 256), dim3(256), 0, st, a, "zstat");
       }
       check_launch("k_zstat");
       ZgenFn zg = zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda));
       set_smem(zg, pl.smem_zgen);
       {
         KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * 16.0, int(p.mode), st);
-        zg<<<blocks, kZgenThreads, pl.smem_zgen, st>>>(a);
+        launch(zg, dim3(blocks), dim3(kZgenThreads), pl.smem_zgen, st, a, "zgen");
       }
       check_launch("k_zgen");
       kernels += 2;
@@ -282,7 +325,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       set_smem(f1k, pl.smem_f1);
       {
         KTimer kt(cx, "k_f1", double(p.N) * 16.0 + double(L) * 16.0, int(p.mode), st);
-        f1k<<<a.ncols >> a.logc, pl.thr_f1, pl.smem_f1, st>>>(a);
+        launch(f1k, dim3(a.ncols >> a.logc), dim3(pl.thr_f1), pl.smem_f1, st, a, "f1");
       }
       check_launch("k_f1");
       ++kernels;
@@ -306,7 +349,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       set_smem(colk, pl.smem_f2);
       {
         KTimer kt(cx, "k_col_f2", double(L) * 32.0, int(p.mode), st);
-        colk<<<dim3(pl.C >> a.logc, pl.A), pl.thr_f2, pl.smem_f2, st>>>(a);
+        launch(colk, dim3(dim3(pl.C >> a.logc, pl.A)), dim3(pl.thr_f2), pl.smem_f2, st, a, "col");
       }
       check_launch("k_col(f2)");
       ++kernels;
@@ -329,11 +372,11 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         set_smem(k_mid_4096, pl.smem_mid);
         const unsigned grid = std::min<unsigned>(npairs, unsigned(cx.num_sms));
         KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode), st);
-        k_mid_4096<<<grid, kMidCtThreads, pl.smem_mid, st>>>(a);
+        launch(k_mid_4096, dim3(grid), dim3(kMidCtThreads), pl.smem_mid, st, a, "mid");
       } else {
         set_smem(k_mid, pl.smem_mid);
         KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode), st);
-        k_mid<<<npairs, pl.thr_mid, pl.smem_mid, st>>>(a);
+        launch(k_mid, dim3(npairs), dim3(pl.thr_mid), pl.smem_mid, st, a, "mid");
       }
       check_launch("k_mid");
       ++kernels;
@@ -357,7 +400,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       set_smem(colk, pl.smem_i2);
       {
         KTimer kt(cx, "k_col_i2", double(L) * 16.0, int(p.mode), st);
-        colk<<<dim3((pl.C / 2) >> a.logc, pl.A), pl.thr_i2, pl.smem_i2, st>>>(a);
+        launch(colk, dim3(dim3((pl.C / 2) >> a.logc, pl.A)), dim3(pl.thr_i2), pl.smem_i2, st, a, "col");
       }
       check_launch("k_col(i2)");
       ++kernels;
@@ -378,7 +421,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       set_smem(ilk, pl.smem_il);
       {
         KTimer kt(cx, "k_ilast", double(L) * 16.0, int(p.mode), st);
-        ilk<<<a.g.ncols >> a.logc, pl.thr_il, pl.smem_il, st>>>(a);
+        launch(ilk, dim3(a.g.ncols >> a.logc), dim3(pl.thr_il), pl.smem_il, st, a, "ilast");
       }
       check_launch("k_ilast");
       ++kernels;
@@ -427,14 +470,14 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         set_smem(lanes, smem2);
         {
           KTimer kt(cx, "k_carry_lanes", double(pl.K) * 8.0 + double(pl.ML) * 16.0, int(p.mode), st);
-          lanes<<<blocks2, kC2Threads, smem2, st>>>(a);
+          launch(lanes, dim3(blocks2), dim3(kC2Threads), smem2, st, a, "lanes");
         }
         check_launch("k_carry_lanes");
         {
           KTimer kt(cx, "k_carry_apply",
                     double(pl.ML) * 16.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0,
                     int(p.mode), st);
-          carry_apply_kernel(pt)<<<blocks2, kC2Threads, 0, st>>>(a);
+          launch(carry_apply_kernel(pt), dim3(blocks2), dim3(kC2Threads), 0, st, a, "apply");
         }
         check_launch("k_carry_apply");
         kernels += 2;
@@ -442,7 +485,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         set_smem(k_carry, pl.smem_carry);
         {
           KTimer kt(cx, "k_carry", double(pl.K) * 8.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0, int(p.mode), st);
-          k_carry<<<blocks, kCarryThreads, pl.smem_carry, st>>>(a);
+          launch(k_carry, dim3(blocks), dim3(kCarryThreads), pl.smem_carry, st, a, "carry");
         }
         check_launch("k_carry");
         ++kernels;
@@ -469,12 +512,12 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.ticket = w.ticket.as<uint32_t>() + 1;
       {
         KTimer kt(cx, "k_high_agg", double(pl.ML) * 8.0, int(p.mode), st);
-        k_high_agg<<<blocks, kCarryThreads, 0, st>>>(a);
+        launch(k_high_agg, dim3(blocks), dim3(kCarryThreads), 0, st, a, "hagg");
       }
       check_launch("k_high_agg");
       {
         KTimer kt(cx, "k_high_round", double(pl.ML) * 8.0 + double(pl.out_limbs) * 8.0, int(p.mode), st);
-        k_high_round<<<blocks, kCarryThreads, 0, st>>>(a);
+        launch(k_high_round, dim3(blocks), dim3(kCarryThreads), 0, st, a, "hround");
       }
       check_launch("k_high_round");
       kernels += 2;
@@ -521,7 +564,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     set_smem(sk, pl.small_smem);
     {
       KTimer kt(cx, "k_small_product", double(count) * double(2 * pl.nlimbs + pl.out_limbs) * 8.0, int(p.mode));
-      sk<<<unsigned(count), pl.small_threads, pl.small_smem, st>>>(a);
+      launch(sk, dim3(unsigned(count)), dim3(pl.small_threads), pl.small_smem, st, a, "small");
     }
     check_launch("k_small_product");
     cx.last_kernels = 1;

@@ -49,6 +49,18 @@ struct DevStatus {
 };
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (sm_90+).  Kernels of a product are launched
+// with the programmatic-serialization attribute (api.cu launch()): the next
+// kernel may be scheduled once every CTA of the current one has executed
+// pdl_trigger(), runs its prologue (constant tables, arguments), and
+// pdl_wait() blocks until the predecessor grid has completed and its memory
+// is visible.  Launched without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
 // Complex helpers (double2 as complex double).
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
   return make_double2(a.x + b.x, a.y + b.y);

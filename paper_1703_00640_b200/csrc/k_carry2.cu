@@ -157,6 +157,8 @@ __device__ __forceinline__ void coeffs_run(const CarryArgs& a, const double* __r
 
 template <int LAM, int kPT>
 __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int64_t kLimbs = int64_t(kT) * kPT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t sw[32];
@@ -295,6 +297,8 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
 
 template <int kPT>
 __global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int64_t kLimbs = int64_t(kT) * kPT;
   __shared__ uint32_t sw[32];
   __shared__ uint32_t s_flags, s_low;

@@ -236,7 +236,9 @@ k_f1(F1Args a) {
   const MapConsts& mc = a.mc;
   const int64_t N = mc.N;
   LayCols lay{a.logc, c - 1};
+  pdl_trigger();
   const TwStage tw = load_tw_stage(sbuf + padded_len(A * c), a.fft, tid, nthr);
+  pdl_wait();
   double topu = 0.0, topv = 0.0;
   if (mc.mode == kModeHigh && col0 < uint32_t(mc.nfold + mc.lambda)) {
     topu = digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, N, mc.balanced != 0);
@@ -269,7 +271,9 @@ k_col(ColArgs a) {
   const uint32_t col0 = blockIdx.x * c;
   const int64_t outer = blockIdx.y;
   LayCols lay{a.logc, c - 1};
+  pdl_trigger();
   const TwStage tw = load_tw_stage(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
+  pdl_wait();
   __syncthreads();
   ColSrc src{a.data, a.g, outer, col0};
   ColSink sink{a.data, a.g, outer, col0, a.tw, a.to, a.tc, a.tmul, a.inv != 0, true};
@@ -288,6 +292,8 @@ size_t colpp_smem_bytes(uint32_t R, uint32_t c) { return 2 * size_t(padded_len(R
 
 __global__ void __launch_bounds__(kColPPThreads, 1)
 k_f1_pp(F1Args a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* b0 = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -317,6 +323,8 @@ k_f1_pp(F1Args a) {
 
 __global__ void __launch_bounds__(kColPPThreads, 1)
 k_col_pp(ColArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* b0 = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -362,6 +370,8 @@ size_t mid_smem_bytes(uint32_t C, uint32_t inv_stablen) {
 
 __global__ void __launch_bounds__(512)
 k_mid(MidArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -476,7 +486,9 @@ __device__ __forceinline__ void mid_4096_body(const MidArgs& a) {
   const uint32_t AB = a.A * a.B;
   const uint32_t npairs = AB / 2 + 1;
   double2* stw = sbuf + 2 * (padded_len(C) + 4);
+  pdl_trigger();
   for (uint32_t i = tid; i < a.fwd.stablen; i += NTHR) stw[i] = __ldg(a.fwd.stab + i);
+  pdl_wait();
   auto row_base = [&](uint32_t r) {
     return a.data + (int64_t(r % a.A) * a.B + (r / a.A)) * int64_t(C);
   };
@@ -517,7 +529,9 @@ k_ilast(ILastArgs a) {
   const uint32_t c = 1u << a.logc;
   const uint32_t col0 = blockIdx.x * c;
   LayCols lay{a.logc, c - 1};
+  pdl_trigger();
   const TwStage tw = load_tw_stage(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
+  pdl_wait();
   tile_load(sbuf, lay, a.fft.R, c, ColSrc{a.data, a.g, 0, col0}, tid, nthr);
   __syncthreads();
   fft_smem_compact<true>(sbuf, lay, a.fft, tw, tid, nthr);
@@ -526,6 +540,8 @@ k_ilast(ILastArgs a) {
 
 __global__ void __launch_bounds__(kColPPThreads, 1)
 k_ilast_pp(ILastArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* b0 = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -551,6 +567,8 @@ k_ilast_pp(ILastArgs a) {
 //            carry transfer functions, block scan, warp look-back, limbs
 __global__ void __launch_bounds__(kCarryThreads)
 k_carry(CarryArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t sw[32];
   __shared__ uint32_t s_blk;
@@ -739,6 +757,8 @@ __device__ __forceinline__ uint64_t high_shifted(const HighRoundArgs& a, int64_t
 // increment passes a limb of t >> s only if the limb is all ones.
 __global__ void __launch_bounds__(kCarryThreads)
 k_high_agg(HighRoundArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ uint32_t s_all;
   const int tid = threadIdx.x;
   if (tid == 0) s_all = 1;
@@ -755,6 +775,8 @@ k_high_agg(HighRoundArgs a) {
 
 __global__ void __launch_bounds__(kCarryThreads)
 k_high_round(HighRoundArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ uint32_t sw[32];
   __shared__ uint32_t s_blk;
   __shared__ int s_cin;
@@ -843,6 +865,8 @@ k_high_round(HighRoundArgs a) {
 // flag_out (the batched API's per-product flags) and the status merges into
 // the context's (residuals by max, flags by or).
 __global__ void k_status_publish(const DevStatus* src, uint32_t* flag_out, DevStatus* merge) {
+  pdl_trigger();
+  pdl_wait();
   uint32_t f = src->flags;
   if (src->high_topbit && src->high_lownz) f |= kFlagHighRange;
   if (flag_out) *flag_out = f;

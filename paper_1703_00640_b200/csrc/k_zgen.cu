@@ -76,6 +76,8 @@ size_t zgen_smem(int b) {
 // random operands; the whole block only when every window equals 2^{b-1}).
 __global__ void __launch_bounds__(256)
 k_zstat(ZgenArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t blk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t count = a.count;
   const int64_t nblk = (count + kZgenChunks - 1) / kZgenChunks;
@@ -116,6 +118,8 @@ k_zstat(ZgenArgs a) {
 template <bool W32, int LAM>
 __global__ void __launch_bounds__(kZgenThreads)
 k_zgen_t(ZgenArgs a) {
+  pdl_trigger();
+  pdl_wait();
   using SB = StagedBits<W32>;
   using Word = typename SB::Word;
   extern __shared__ __align__(16) unsigned char smem_raw[];
