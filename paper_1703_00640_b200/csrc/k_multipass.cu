@@ -157,11 +157,10 @@ struct F1Sink {
 // Tile <-> shared memory copies of a column pass: element (item, e) of the
 // R x c tile, consecutive threads on consecutive items (columns) so each
 // warp touches c-element row segments; 8 transfers per thread in flight.
-template <class Lay, class Src>
+template <int U = 8, class Lay, class Src>
 __device__ __forceinline__ void tile_load(double2* __restrict__ buf, const Lay& lay, uint32_t R,
                                           uint32_t c, const Src& src, int tid, int nthr) {
   const uint32_t n = R * c, lc = 31 - __clz(c);
-  constexpr int U = 8;
   uint32_t i = tid;
   for (; i + (U - 1) * nthr < n; i += U * nthr) {
     double2 v[U];
@@ -184,12 +183,13 @@ template <class Sink>
 struct TileSinkPre {
   static constexpr bool value = false;
 };
-template <class Lay, class Sink>
+// U: transfers in flight per thread (8; 4 in the 1024-thread ping-pong
+// kernels, whose 64-register budget holds 4 values and 4 twiddles).
+template <int U = 8, class Lay, class Sink>
 __device__ __forceinline__ void tile_store(const double2* __restrict__ buf, const Lay& lay,
                                            uint32_t R, uint32_t c, const Sink& sink, int tid,
                                            int nthr) {
   const uint32_t n = R * c, lc = 31 - __clz(c);
-  constexpr int U = 8;
   uint32_t i = tid;
   for (; i + (U - 1) * nthr < n; i += U * nthr) {
     double2 v[U], w[U];
@@ -315,14 +315,17 @@ k_f1_pp(F1Args a) {
     a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
   }
   const ZSrc src{a.z, a.zt, N, a.ncols, col0, &a.mc, topu, topv};
-  tile_load(b0, lay, A, c, src, tid, nthr);
+  tile_load<4>(b0, lay, A, c, src, tid, nthr);
   __syncthreads();
   const double2* res = fft_pp<false>(b0, b1, lay, a.fft, tid, nthr);
-  tile_store(res, lay, A, c, F1Sink{a.out, a.ncols, col0, a.tw}, tid, nthr);
+  tile_store<4>(res, lay, A, c, F1Sink{a.out, a.ncols, col0, a.tw}, tid, nthr);
 }
 
+// INV at compile time: one transform direction per instantiation keeps the
+// kernel within its 64 registers.
+template <bool INV>
 __global__ void __launch_bounds__(kColPPThreads, 1)
-k_col_pp(ColArgs a) {
+k_col_pp_t(ColArgs a) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -335,12 +338,13 @@ k_col_pp(ColArgs a) {
   LayCols lay{a.logc, c - 1};
   ColSrc src{a.data, a.g, outer, col0};
   ColSink sink{a.data, a.g, outer, col0, a.tw, a.to, a.tc, a.tmul, a.inv != 0, true};
-  tile_load(b0, lay, a.fft.R, c, src, tid, nthr);
+  tile_load<4>(b0, lay, a.fft.R, c, src, tid, nthr);
   __syncthreads();
-  const double2* res = a.inv ? fft_pp<true>(b0, b1, lay, a.fft, tid, nthr)
-                             : fft_pp<false>(b0, b1, lay, a.fft, tid, nthr);
-  tile_store(res, lay, a.fft.R, c, sink, tid, nthr);
+  const double2* res = fft_pp<INV>(b0, b1, lay, a.fft, tid, nthr);
+  tile_store<4>(res, lay, a.fft.R, c, sink, tid, nthr);
 }
+
+ColFn col_pp_kernel(bool inv) { return inv ? k_col_pp_t<true> : k_col_pp_t<false>; }
 
 // ---------------------------------------------------------------------------
 // Row pass: conjugate row pair (r, AB - r), r = k_a + A k_b.
@@ -549,10 +553,10 @@ k_ilast_pp(ILastArgs a) {
   const uint32_t col0 = blockIdx.x * c;
   double2* b1 = b0 + padded_len(a.fft.R * c);
   LayCols lay{a.logc, c - 1};
-  tile_load(b0, lay, a.fft.R, c, ColSrc{a.data, a.g, 0, col0}, tid, nthr);
+  tile_load<4>(b0, lay, a.fft.R, c, ColSrc{a.data, a.g, 0, col0}, tid, nthr);
   __syncthreads();
   const double2* res = fft_pp<true>(b0, b1, lay, a.fft, tid, nthr);
-  tile_store(res, lay, a.fft.R, c, CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
+  tile_store<4>(res, lay, a.fft.R, c, CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
 }
 
 

@@ -143,7 +143,8 @@ __global__ void k_col(ColArgs a);
 // ping-pong column passes (fft_pp)
 constexpr int kColPPThreads = 1024;
 __global__ void k_f1_pp(F1Args a);
-__global__ void k_col_pp(ColArgs a);
+typedef void (*ColFn)(ColArgs);
+ColFn col_pp_kernel(bool inv);
 size_t colpp_smem_bytes(uint32_t R, uint32_t c);
 
 struct MidArgs {
