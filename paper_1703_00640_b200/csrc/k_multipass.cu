@@ -154,6 +154,12 @@ struct F1Sink {
   }
 };
 
+// transfers in flight per thread in the single-buffer column passes
+#ifndef TMG_COL_U
+#define TMG_COL_U 4
+#endif
+constexpr int kColU = TMG_COL_U;
+
 // Tile <-> shared memory copies of a column pass: element (item, e) of the
 // R x c tile, consecutive threads on consecutive items (columns) so each
 // warp touches c-element row segments; 8 transfers per thread in flight.
@@ -251,10 +257,10 @@ k_f1(F1Args a) {
   }
   // tile -> shared memory: all loads of a thread in flight together
   const ZSrc src{a.z, a.zt, N, a.ncols, col0, &a.mc, topu, topv};
-  tile_load(sbuf, lay, A, c, src, tid, nthr);
+  tile_load<kColU>(sbuf, lay, A, c, src, tid, nthr);
   __syncthreads();
   fft_smem_compact<false>(sbuf, lay, a.fft, tw, tid, nthr);
-  tile_store(sbuf, lay, A, c, F1Sink{a.out, a.ncols, col0, a.tw}, tid, nthr);
+  tile_store<kColU>(sbuf, lay, A, c, F1Sink{a.out, a.ncols, col0, a.tw}, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
@@ -277,11 +283,11 @@ k_col(ColArgs a) {
   __syncthreads();
   ColSrc src{a.data, a.g, outer, col0};
   ColSink sink{a.data, a.g, outer, col0, a.tw, a.to, a.tc, a.tmul, a.inv != 0, true};
-  tile_load(sbuf, lay, a.fft.R, c, src, tid, nthr);
+  tile_load<kColU>(sbuf, lay, a.fft.R, c, src, tid, nthr);
   __syncthreads();
   if (a.inv) fft_smem_compact<true>(sbuf, lay, a.fft, tw, tid, nthr);
   else fft_smem_compact<false>(sbuf, lay, a.fft, tw, tid, nthr);
-  tile_store(sbuf, lay, a.fft.R, c, sink, tid, nthr);
+  tile_store<kColU>(sbuf, lay, a.fft.R, c, sink, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
@@ -536,10 +542,10 @@ k_ilast(ILastArgs a) {
   pdl_trigger();
   const TwStage tw = load_tw_stage(sbuf + padded_len(a.fft.R * c), a.fft, tid, nthr);
   pdl_wait();
-  tile_load(sbuf, lay, a.fft.R, c, ColSrc{a.data, a.g, 0, col0}, tid, nthr);
+  tile_load<kColU>(sbuf, lay, a.fft.R, c, ColSrc{a.data, a.g, 0, col0}, tid, nthr);
   __syncthreads();
   fft_smem_compact<true>(sbuf, lay, a.fft, tw, tid, nthr);
-  tile_store(sbuf, lay, a.fft.R, c, CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
+  tile_store<kColU>(sbuf, lay, a.fft.R, c, CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
 }
 
 __global__ void __launch_bounds__(kColPPThreads, 1)
