@@ -82,7 +82,7 @@ struct Profiler {
 // The context owns one for single products; a batch runs its products on up
 // to kMaxBatchStreams workspaces, each on its own stream.
 struct Workspace {
-  DevBuf work_t, work_c, work_z, cbu, cbv, aux, tbuf, aggs, zaggs, haggs, ticket, status;
+  DevBuf work_t, work_c, work_z, cbu, cbv, aux, tbuf, aggs, zaggs, ticket, hticket, status;
   ScanSlot scan_c;  // look-back state of the single-pass carry (k_carry)
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
@@ -503,13 +503,16 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       const int64_t LB = kCarryThreads * kCarryPerThread;
       const unsigned blocks = unsigned((a.WL + LB - 1) / LB);
       a.status = status;
-      w.haggs.ensure(size_t(blocks) * 4 + 16);
-      a.aggs = w.haggs.as<uint32_t>();
       if (!w.ticket.p) {
         w.ticket.ensure(64);
         TMG_CUDA(cudaMemsetAsync(w.ticket.p, 0, 64, st));
       }
-      a.ticket = w.ticket.as<uint32_t>() + 1;
+      if (!w.hticket.p) {
+        w.hticket.ensure(64);
+        TMG_CUDA(cudaMemsetAsync(w.hticket.p, 0, 4, st));
+        TMG_CUDA(cudaMemsetAsync(w.hticket.as<uint32_t>() + 1, 0xff, 4, st));
+      }
+      a.ticket = w.hticket.as<uint32_t>();
       {
         KTimer kt(cx, "k_high_agg", double(pl.ML) * 8.0, int(p.mode), st);
         launch(k_high_agg, dim3(blocks), dim3(kCarryThreads), 0, st, a, "hagg");

@@ -780,7 +780,9 @@ k_high_agg(HighRoundArgs a) {
   for (int64_t m = ms + tid; m < me; m += kCarryThreads) all &= high_shifted(a, m) == ~0ull;
   if (!__all_sync(0xffffffffu, all) && (tid & 31) == 0) s_all = 0;
   __syncthreads();
-  if (tid == 0) a.aggs[blockIdx.x] = s_all ? kTfIdentity : tf_const(0);
+  // the increment passes a block only if all its limbs are ones: the first
+  // block that stops it is all k_high_round needs
+  if (tid == 0 && !s_all) atomicMin(a.ticket + 1, uint32_t(blockIdx.x));
 }
 
 __global__ void __launch_bounds__(kCarryThreads)
@@ -823,16 +825,9 @@ k_high_round(HighRoundArgs a) {
   }
   uint32_t agg;
   const uint32_t ex = block_scan_tf(f, sw, &agg);
-  {
-    // increment into this block: the aggregates before it (k_high_agg)
-    uint32_t g = kTfIdentity;
-    const uint32_t Q = (blk + kCarryThreads - 1) / kCarryThreads;
-    const uint32_t i0 = uint32_t(tid) * Q, i1 = min(blk, i0 + Q);
-    for (uint32_t i = i0; i < i1; ++i) g = tf_compose(g, __ldg(a.aggs + i));
-    uint32_t pre;
-    (void)block_scan_tf(g, sw, &pre);
-    if (tid == 0) s_cin = tf_apply(pre, inc);
-  }
+  // increment into this block: inc unless an earlier block has a limb of
+  // t >> s that is not all ones (first such block from k_high_agg)
+  if (tid == 0) s_cin = (__ldcg(a.ticket + 1) >= blk) ? inc : 0;
   __syncthreads();
   int c = tf_apply(ex, s_cin);
   uint32_t flags = 0, topbit = 0, lownz = 0;
@@ -865,6 +860,7 @@ k_high_round(HighRoundArgs a) {
       st->high_topbit = 0;
       st->high_lownz = 0;
       st->high_sticky = 0;
+      a.ticket[1] = 0xffffffffu;  // first-stop block, for the next product
       *a.ticket = 0;
     }
   }

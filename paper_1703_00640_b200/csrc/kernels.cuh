@@ -210,8 +210,8 @@ struct HighRoundArgs {
   int64_t WL;   // limbs of w examined (covers every bit of t >> s)
   int32_t shift_s;
   DevStatus* status;
-  uint32_t* aggs;  // per-block increment transfer functions (k_high_agg)
-  uint32_t* ticket;  // completion counter (zero between launches)
+  uint32_t* ticket;  // [0] completion counter (zero between launches),
+                     // [1] first block stopping the increment (~0 between launches)
 };
 __global__ void k_high_agg(HighRoundArgs a);
 __global__ void k_status_publish(const DevStatus* src, uint32_t* flag_out, DevStatus* merge);
