@@ -61,27 +61,31 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
         self._nv = None
+        self.errors = []
 
     def _run(self):
-        nv = self._nv
-        h = nv.nvmlDeviceGetHandleByIndex(self.device)
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        nv, h, mx = self._nv, self._h, self._mx
         while not self._stop.is_set():
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 util = nv.nvmlDeviceGetUtilizationRates(h).gpu
                 self.samples.append((sm, mx, rs, util))
-            except Exception:
-                pass
-            self._stop.wait(0.002)
+            except Exception as e:  # noqa: BLE001 - recorded, not fatal
+                self.errors.append(repr(e))
+            self._stop.wait(0.001)
 
     def start(self):
+        # NVML init and the device handle are taken here, before the timed
+        # region starts, so the sampling thread begins at once
         try:
             import pynvml as nv
             nv.nvmlInit()
             self._nv = nv
-        except Exception:
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self._mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.errors.append(repr(e))
             return
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
@@ -91,9 +95,12 @@ class ClockSampler:
         if self._t:
             self._t.join(timeout=2)
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
+                    "errors": self.errors[:3]}
         nv = self._nv
-        sm = [s[0] for s in self.samples]
+        # median over the samples taken while the GPU was busy
+        busy = [s for s in self.samples if s[3] > 0] or self.samples
+        sm = [s[0] for s in busy]
         reasons = sorted({name for s in self.samples for name, attr in self.REASONS
                           if s[2] & getattr(nv, attr, 0)})
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
