@@ -69,8 +69,7 @@ class ClockSampler:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                util = nv.nvmlDeviceGetUtilizationRates(h).gpu
-                self.samples.append((sm, mx, rs, util))
+                self.samples.append((sm, mx, rs, 1))
             except Exception as e:  # noqa: BLE001 - recorded, not fatal
                 self.errors.append(repr(e))
             self._stop.wait(0.001)
@@ -475,7 +474,7 @@ def run_reference(args, world, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

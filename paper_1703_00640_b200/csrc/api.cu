@@ -309,6 +309,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.out = T;
       a.ncols = uint32_t(L / pl.A);
       a.logc = pl.logc_f1;
+      a.stw = pl.f1_stw ? 1u : 0u;
       a.fft = pl.fA;
       a.tw = pl.twL;
       a.mc = pl.mc;

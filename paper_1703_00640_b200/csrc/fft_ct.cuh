@@ -60,6 +60,14 @@ __device__ __forceinline__ void ct_load(double2 (&x)[16], const RowPair& lay, co
   }
 }
 
+// Sinks that take a per-butterfly factor (SinkPrep<Sink>::value) get
+// pre = sink.prep(item, ob) before the stage's twiddles and DFT, so its
+// loads overlap them, and put(item, ob + q NS, q, v, pre) per output.
+template <class Sink>
+struct SinkPrep {
+  static constexpr bool value = false;
+};
+
 template <int RAD, bool INV, uint32_t R, uint32_t NS, int NTHR, class Sink>
 __device__ __forceinline__ void ct_store(double2 (&x)[16], const RowPair& lay,
                                          const double2* __restrict__ stab, uint32_t qmul,
@@ -71,18 +79,32 @@ __device__ __forceinline__ void ct_store(double2 (&x)[16], const RowPair& lay,
     if (t < nbi && item < lay.nrows) {
       const uint32_t tq = t / NS;
       const uint32_t j = t - tq * NS;
-      double2* xv = x;
-      if (NS > 1 && j != 0) {
-#pragma unroll
-        for (int q = 1; q < RAD; ++q) {
-          const double2 w = stab[(uint32_t(q) * qmul - 1) * NS + j];
-          xv[q] = INV ? cmulc(xv[q], w) : cmul(xv[q], w);
-        }
-      }
-      dft<RAD, INV>(xv);
       const uint32_t ob = tq * NS * RAD + j;
+      double2* xv = x;
+      if constexpr (SinkPrep<Sink>::value) {
+        const auto pre = sink.prep(item, ob);
+        if (NS > 1 && j != 0) {
 #pragma unroll
-      for (int q = 0; q < RAD; ++q) sink(item, ob + q * NS, xv[q]);
+          for (int q = 1; q < RAD; ++q) {
+            const double2 w = stab[(uint32_t(q) * qmul - 1) * NS + j];
+            xv[q] = INV ? cmulc(xv[q], w) : cmul(xv[q], w);
+          }
+        }
+        dft<RAD, INV>(xv);
+#pragma unroll
+        for (int q = 0; q < RAD; ++q) sink.put(item, ob + q * NS, uint32_t(q), xv[q], pre);
+      } else {
+        if (NS > 1 && j != 0) {
+#pragma unroll
+          for (int q = 1; q < RAD; ++q) {
+            const double2 w = stab[(uint32_t(q) * qmul - 1) * NS + j];
+            xv[q] = INV ? cmulc(xv[q], w) : cmul(xv[q], w);
+          }
+        }
+        dft<RAD, INV>(xv);
+#pragma unroll
+        for (int q = 0; q < RAD; ++q) sink(item, ob + q * NS, xv[q]);
+      }
     }
   }
 }

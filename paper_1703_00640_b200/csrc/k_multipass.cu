@@ -227,6 +227,70 @@ struct TileSinkPre<ColSink> {
   static constexpr bool value = true;
 };
 
+// Inter-pass twiddles of the first column pass without global loads at
+// store time.  With nthr a multiple of c, thread tid always stores column
+// item = tid & (c - 1) at rows k = k0 + D s (k0 = tid >> logc,
+// D = nthr >> logc), so omega_L^{col k} = omega_L^{col k0} * omega_L^{col D s}:
+// one factor per thread (base) and a c x S table per CTA (step), both taken
+// from the exact two-level global table at kernel entry, where their latency
+// hides behind the tile load.  The store then reads two shared-memory values
+// per element instead of two global ones.  x = 0 factors are (1, 0) exactly,
+// so untwiddled elements stay exact.
+__host__ __device__ inline uint32_t f1_tw_S(uint32_t A, uint32_t c, uint32_t nthr) {
+  return (A * c + nthr - 1) / nthr;
+}
+size_t f1_tw_bytes(uint32_t A, uint32_t c, uint32_t nthr) {
+  return (nthr % c) ? 0 : (size_t(nthr) + size_t(c) * f1_tw_S(A, c, nthr)) * 16;
+}
+
+struct F1Tw {
+  double2* base;  // nthr entries
+  double2* step;  // S x c entries, step[(s << logc) + item]
+  uint32_t S;
+};
+
+__device__ __forceinline__ F1Tw f1_tw_stage(double2* dst, const F1Sink& sink, uint32_t A,
+                                           uint32_t logc, int tid, int nthr) {
+  const uint32_t c = 1u << logc;
+  F1Tw t{dst, dst + nthr, f1_tw_S(A, c, uint32_t(nthr))};
+  const uint32_t item = uint32_t(tid) & (c - 1), k0 = uint32_t(tid) >> logc;
+  const uint32_t D = uint32_t(nthr) >> logc;
+  const uint32_t xb = (sink.col0 + item) * k0;
+  t.base[tid] = (k0 < A && xb) ? sink.tw.get(xb) : make_double2(1.0, 0.0);
+  for (uint32_t i = tid; i < (t.S << logc); i += nthr) {
+    const uint32_t x = (sink.col0 + (i & (c - 1))) * D * (i >> logc);
+    t.step[i] = x ? sink.tw.get(x) : make_double2(1.0, 0.0);
+  }
+  return t;
+}
+
+template <int U, class Lay>
+__device__ __forceinline__ void f1_store(const double2* __restrict__ buf, const Lay& lay,
+                                         uint32_t A, uint32_t logc, const F1Sink& sink,
+                                         const F1Tw& t, int tid, int nthr) {
+  const uint32_t c = 1u << logc;
+  const uint32_t item = uint32_t(tid) & (c - 1), k0 = uint32_t(tid) >> logc;
+  const uint32_t D = uint32_t(nthr) >> logc;
+  const double2 b = t.base[tid];
+  double2* out = sink.out + (sink.col0 + item);
+  for (uint32_t s0 = 0; s0 < t.S; s0 += U) {
+    double2 v[U], w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t s = s0 + u, k = k0 + D * s;
+      if (s < t.S && k < A) {
+        v[u] = buf[lay.idx(item, k)];
+        w[u] = t.step[(s << logc) + item];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t s = s0 + u, k = k0 + D * s;
+      if (s < t.S && k < A) out[int64_t(k) * sink.ncols] = cmul(v[u], cmul(b, w[u]));
+    }
+  }
+}
+
 size_t f1_smem_bytes(uint32_t A, uint32_t c) {
   return size_t(padded_len(A * c)) * 16 + size_t(A) * 16;  // data + stage table (< A)
 }
@@ -256,11 +320,16 @@ k_f1(F1Args a) {
     a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
   }
   // tile -> shared memory: all loads of a thread in flight together
+  const F1Sink sink{a.out, a.ncols, col0, a.tw};
+  const bool stw = a.stw != 0;
+  F1Tw ftw{};
+  if (stw) ftw = f1_tw_stage(sbuf + padded_len(A * c) + A, sink, A, a.logc, tid, nthr);
   const ZSrc src{a.z, a.zt, N, a.ncols, col0, &a.mc, topu, topv};
   tile_load<kColU>(sbuf, lay, A, c, src, tid, nthr);
   __syncthreads();
   fft_smem_compact<false>(sbuf, lay, a.fft, tw, tid, nthr);
-  tile_store<kColU>(sbuf, lay, A, c, F1Sink{a.out, a.ncols, col0, a.tw}, tid, nthr);
+  if (stw) f1_store<kColU>(sbuf, lay, A, a.logc, sink, ftw, tid, nthr);
+  else tile_store<kColU>(sbuf, lay, A, c, sink, tid, nthr);
 }
 
 // ---------------------------------------------------------------------------
@@ -320,11 +389,16 @@ k_f1_pp(F1Args a) {
     auto Dv = [&](int64_t i) { return digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, i, mc.balanced != 0); };
     a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
   }
+  const F1Sink sink{a.out, a.ncols, col0, a.tw};
+  const bool stw = a.stw != 0;
+  F1Tw ftw{};
+  if (stw) ftw = f1_tw_stage(b1 + padded_len(A * c), sink, A, a.logc, tid, nthr);
   const ZSrc src{a.z, a.zt, N, a.ncols, col0, &a.mc, topu, topv};
   tile_load<4>(b0, lay, A, c, src, tid, nthr);
   __syncthreads();
   const double2* res = fft_pp<false>(b0, b1, lay, a.fft, tid, nthr);
-  tile_store<4>(res, lay, A, c, F1Sink{a.out, a.ncols, col0, a.tw}, tid, nthr);
+  if (stw) f1_store<4>(res, lay, A, a.logc, sink, ftw, tid, nthr);
+  else tile_store<4>(res, lay, A, c, sink, tid, nthr);
 }
 
 // INV at compile time: one transform direction per instantiation keeps the
@@ -374,8 +448,39 @@ struct RowSink {
   }
 };
 
+// Output twiddles of the C = 4096 row pass: the last inverse stage's thread
+// stores m = ob + q NS (q < RAD) of its row, and
+// omega_L^{2 r m} = omega_L^{2 r ob} * omega_L^{2 r NS q}: the first factor
+// is fetched (two-level global table) before the stage's DFT, the second
+// comes from a per-pair table qt[item * RAD + q] staged in shared memory,
+// so the store does no global twiddle loads.  Both factors are (1, 0)
+// exactly at x = 0.
+template <uint32_t RAD>
+struct RowSinkQ {
+  double2* data;
+  int64_t base0, base1;
+  uint32_t r0, r1;
+  TwGlobal tw;
+  const double2* qt;
+  __device__ __forceinline__ double2 prep(uint32_t item, uint32_t ob) const {
+    const uint32_t x = 2u * (item ? r1 : r0) * ob;
+    return x ? tw.get(x) : make_double2(1.0, 0.0);
+  }
+  __device__ __forceinline__ void put(uint32_t item, uint32_t m, uint32_t q, double2 v,
+                                      double2 b) const {
+    v = cmulc(v, cmul(b, qt[item * RAD + q]));
+    data[(item ? base1 : base0) + m] = v;
+  }
+};
+template <uint32_t RAD>
+struct SinkPrep<RowSinkQ<RAD>> {
+  static constexpr bool value = true;
+};
+constexpr uint32_t kMidQEntries = 32;  // 2 rows x last-stage radix (<= 16)
+
 size_t mid_smem_bytes(uint32_t C, uint32_t inv_stablen) {
-  return size_t(2) * (padded_len(C) + 4) * 16 + size_t(C) * 16 + size_t(inv_stablen) * 16;
+  return size_t(2) * (padded_len(C) + 4) * 16 + size_t(C) * 16 + size_t(inv_stablen) * 16 +
+         size_t(kMidQEntries) * 16;
 }
 
 __global__ void __launch_bounds__(512)
@@ -443,8 +548,8 @@ k_mid(MidArgs a) {
 // pair computes, so the first stage's loads do not wait on HBM.
 template <int NTHR, class Fwd, class Inv>
 __device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restrict__ sbuf,
-                                              const double2* __restrict__ stab, uint32_t r0,
-                                              int tid) {
+                                              const double2* __restrict__ stab,
+                                              double2* __restrict__ qt, uint32_t r0, int tid) {
   constexpr uint32_t C = 4096, H = 2048;
   const uint32_t AB = a.A * a.B;
   const uint32_t r1 = (AB - r0) % AB;
@@ -456,6 +561,15 @@ __device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restr
   ct_stages<false, Fwd, 0, NTHR>(x, sbuf, lay, stab, a.fwd, RowSrc{a.data, base0, base1},
                                  SmemSink<RowPair>{sbuf, lay}, tid);
   __syncthreads();
+  // per-pair table of the output twiddles' second factor (RowSinkQ)
+  constexpr uint32_t RL = uint32_t(Inv::rad(Inv::nst - 1));
+  constexpr uint32_t NSL = Inv::ns(Inv::nst - 1);
+  static_assert(2 * RL <= kMidQEntries, "output twiddle table");
+  if (uint32_t(tid) < 2 * RL) {
+    const uint32_t it = uint32_t(tid) / RL, q = uint32_t(tid) - it * RL;
+    const uint32_t xq = 2u * (it ? r1 : r0) * NSL * q;
+    qt[tid] = xq ? a.tw.get(xq) : make_double2(1.0, 0.0);
+  }
   // spectral product over the pair (see k_mid)
   const uint32_t brw = (r0 != 0) ? 1u : 0u;
 #pragma unroll 2
@@ -484,7 +598,7 @@ __device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restr
   }
   __syncthreads();
   ct_stages<true, Inv, 0, NTHR>(x, sbuf, lay, stab, a.inv, SmemSrc<RowPair>{sbuf, lay},
-                                RowSink{a.data, base0, base1, r0, r1, a.tw}, tid);
+                                RowSinkQ<RL>{a.data, base0, base1, r0, r1, a.tw, qt}, tid);
 }
 
 template <int NTHR, class Fwd, class Inv>
@@ -513,7 +627,7 @@ __device__ __forceinline__ void mid_4096_body(const MidArgs& a) {
       prefetch_l2(row_base(nx), C * 16);
       prefetch_l2(row_base((AB - nx) % AB), C * 16);
     }
-    mid_pair_4096<NTHR, Fwd, Inv>(a, sbuf, stw, r0, tid);
+    mid_pair_4096<NTHR, Fwd, Inv>(a, sbuf, stw, stw + C, r0, tid);
   }
 }
 

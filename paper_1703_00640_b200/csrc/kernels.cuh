@@ -112,6 +112,7 @@ struct F1Args {
   double2* out;    // T[k_a][col], row length ncols
   uint32_t ncols;  // = L / A
   uint32_t logc;   // columns per CTA = 2^logc
+  uint32_t stw;    // inter-pass twiddles staged per CTA (f1_tw_bytes reserved)
   SubFft fft;      // length A
   TwGlobal tw;     // omega_L
   MapConsts mc;
@@ -128,6 +129,8 @@ struct F1Args {
 };
 __global__ void k_f1(F1Args a);
 size_t f1_smem_bytes(uint32_t A, uint32_t c);
+// staged inter-pass twiddles of the first column pass (0 when nthr % c != 0)
+size_t f1_tw_bytes(uint32_t A, uint32_t c, uint32_t nthr);
 
 struct ColArgs {
   double2* data;  // in place

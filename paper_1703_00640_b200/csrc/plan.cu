@@ -431,7 +431,8 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   static const int col_logc_cap = getenv("TMG_COL_LOGC") ? atoi(getenv("TMG_COL_LOGC")) : 6;
   pl->logc_f1 = std::min<uint32_t>(pick_logc(A, UL / A, cap), uint32_t(col_logc_cap));
   pl->thr_f1 = threads_for(uint64_t(A) << pl->logc_f1);
-  pl->smem_f1 = f1_smem_bytes(A, 1u << pl->logc_f1);
+  pl->smem_f1 = f1_smem_bytes(A, 1u << pl->logc_f1) +
+                f1_tw_bytes(A, 1u << pl->logc_f1, uint32_t(pl->thr_f1));
   pl->logc_il = std::min<uint32_t>(pick_logc(A, C / 2, cap), uint32_t(col_logc_cap));
   pl->thr_il = threads_for(uint64_t(A) << pl->logc_il);
   pl->smem_il = col_smem_bytes(A, 1u << pl->logc_il);
@@ -478,7 +479,8 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
       pl->iA = pl->fA;
       pl->logc_f1 = uint32_t(std::min(lf1, col_logc_cap));
       pl->thr_f1 = pp_threads(A, pl->logc_f1);
-      pl->smem_f1 = colpp_smem_bytes(A, 1u << pl->logc_f1);
+      pl->smem_f1 = colpp_smem_bytes(A, 1u << pl->logc_f1) +
+                    f1_tw_bytes(A, 1u << pl->logc_f1, uint32_t(pl->thr_f1));
       pl->logc_il = uint32_t(std::min(lil, col_logc_cap));
       pl->thr_il = pp_threads(A, pl->logc_il);
       pl->smem_il = colpp_smem_bytes(A, 1u << pl->logc_il);
@@ -493,6 +495,14 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
         pl->smem_i2 = colpp_smem_bytes(B, 1u << pl->logc_i2);
       }
     }
+  }
+  {
+    // staged F1 twiddles where the thread count is a multiple of the
+    // columns per CTA and the extra table still fits
+    const uint32_t c1 = 1u << pl->logc_f1;
+    const size_t extra = f1_tw_bytes(A, c1, uint32_t(pl->thr_f1));
+    pl->f1_stw = extra > 0 && pl->smem_f1 <= kMaxDynSmem;
+    if (!pl->f1_stw) pl->smem_f1 -= extra;
   }
   pl->thr_mid = threads_for(uint64_t(2) * C);
   pl->smem_mid = mid_smem_bytes(C, pl->mid_shared_table ? 0u : pl->iC.stablen);

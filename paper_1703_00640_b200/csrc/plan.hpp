@@ -65,6 +65,7 @@ struct Plan {
   uint32_t logc_f1 = 0, logc_f2 = 0, logc_i2 = 0, logc_il = 0;
   size_t smem_f1 = 0, smem_f2 = 0, smem_i2 = 0, smem_il = 0, smem_mid = 0,
          smem_carry = 0;
+  bool f1_stw = false;  // k_f1 stages its inter-pass twiddles per CTA
   int thr_f1 = 0, thr_f2 = 0, thr_i2 = 0, thr_il = 0, thr_mid = 0;
   size_t smem_zgen = 0;
   bool mid_shared_table = false;
