@@ -43,6 +43,16 @@ struct StagedBits {
   }
 };
 
+// Digit slot of local chunk i: one pad slot per 16, so that the 16
+// consecutive digits a thread writes land in distinct banks across a warp.
+__device__ __forceinline__ int32_t zpad(int32_t i) { return i + (i >> 4); }
+
+// Exact int32 -> double on the FP64 pipe (2^52 + 2^31 magic), in place of
+// the quarter-rate I2F.
+__device__ __forceinline__ double i2d_exact(int32_t x) {
+  return __hiloint2double(0x43300000, int(uint32_t(x) ^ 0x80000000u)) - 4503601774854144.0;
+}
+
 template <bool W32>
 __device__ __forceinline__ typename StagedBits<W32>::Word load_word(const uint64_t* limbs,
                                                                     int64_t nlimbs,
@@ -65,7 +75,8 @@ __host__ __device__ inline int64_t zgen_words(int b, int kw) {
 
 size_t zgen_smem(int b) {
   const int kw = b <= 32 ? 32 : 64;
-  return 2 * size_t(zgen_words(b, kw)) * (kw / 8) + size_t(kZgenChunks + kMaxLambda) * 8 + 64;
+  return 2 * size_t(zgen_words(b, kw)) * (kw / 8) +
+         size_t((kZgenChunks + kMaxLambda) * 17 / 16 + 2) * 8 + 64;
 }
 
 // Carry transfer function of each block of kZgenChunks chunks for both
@@ -211,7 +222,7 @@ k_zgen_t(ZgenArgs a) {
       bu |= uint32_t(cu) << q;
       bv |= uint32_t(cv) << q;
       const bool top = j == count - 1 || !mc.balanced;
-      dig[q0 + q] = make_int2(int32_t(split_digit(wu[q], cu, b, top)),
+      dig[zpad(q0 + q)] = make_int2(int32_t(split_digit(wu[q], cu, b, top)),
                               int32_t(split_digit(wv[q], cv, b, top)));
       if (!((pu >> q) & 1u)) cu = int((gu >> q) & 1u);
       if (!((pv >> q) & 1u)) cv = int((gv >> q) & 1u);
@@ -225,7 +236,7 @@ k_zgen_t(ZgenArgs a) {
       const uint32_t rel = off0 + uint32_t(j - c0) * uint32_t(b);
       const uint64_t xu = Lu.window(rel, mask), xv = Lv.window(rel, mask);
       const bool top = j == count - 1 || !mc.balanced;
-      dig[j - c0] = make_int2(int32_t(split_digit(xu, cu, b, top)),
+      dig[zpad(j - c0)] = make_int2(int32_t(split_digit(xu, cu, b, top)),
                               int32_t(split_digit(xv, cv, b, top)));
       cu = mc.balanced ? tf_apply(split_tf(xu, b), cu) : 0;
       cv = mc.balanced ? tf_apply(split_tf(xv, b), cv) : 0;
@@ -256,7 +267,7 @@ k_zgen_t(ZgenArgs a) {
     for (int i = 0; i < ext; ++i) {
       const uint64_t wu = window_bits(a.u, a.nlimbs, int64_t(i) * b - a.lead, b);
       const uint64_t wv = window_bits(a.v, a.nlimbs, int64_t(i) * b - a.lead, b);
-      dig[nN + i] = make_int2(int32_t(split_digit(wu, cu, b, i == count - 1 || !mc.balanced)),
+      dig[zpad(nN + i)] = make_int2(int32_t(split_digit(wu, cu, b, i == count - 1 || !mc.balanced)),
                               int32_t(split_digit(wv, cv, b, i == count - 1 || !mc.balanced)));
       cu = mc.balanced ? tf_apply(split_tf(wu, b), cu) : 0;
       cv = mc.balanced ? tf_apply(split_tf(wv, b), cv) : 0;
@@ -267,7 +278,7 @@ k_zgen_t(ZgenArgs a) {
   // outputs
   if constexpr (LAM == 0) {
     for (int32_t jl = tid; jl < nloc; jl += kZgenThreads) {
-      const int2 d = dig[jl];
+      const int2 d = dig[zpad(jl)];
       a.z[a.zt.index(uint32_t(c0 + jl))] = make_double2(double(d.x), double(d.y));
     }
   } else {
@@ -277,13 +288,42 @@ k_zgen_t(ZgenArgs a) {
     double cr[LAM];
 #pragma unroll
     for (int r = 0; r < LAM; ++r) cr[r] = mc.cpre[r];
+    if (nloc + ext <= nN) {
+      // No output of this block wraps (block-uniform).  Row r of output j
+      // uses coef_r(j - r) = ((j - r) g_1 ... g_{r-1}) c_r with g_i = j -/+ i N:
+      // the exact integer factors are formed once per output and the products
+      // run in coef_rt's order (bit-identical); digits convert on the FP64 pipe.
+      const double sgN = low ? -Nd : Nd;
+      for (int32_t jl = ext + tid; jl < nloc + ext; jl += kZgenThreads) {
+        const double jd = double(c0 + jl);
+        double g[LAM > 1 ? LAM - 1 : 1];
+#pragma unroll
+        for (int i = 1; i < LAM - 1; ++i) g[i] = jd + double(i) * sgN;
+        double au = 0.0, av = 0.0;
+#pragma unroll
+        for (int r = LAM - 1; r >= 0; --r) {
+          double cf = 1.0;
+          if (r > 0) {
+            double pp = jd - double(r);
+#pragma unroll
+            for (int i = 1; i < r; ++i) pp *= g[i];
+            cf = pp * cr[r];
+          }
+          const int2 d = dig[zpad(jl - r)];
+          au += i2d_exact(d.x) * cf;
+          av += i2d_exact(d.y) * cf;
+        }
+        a.z[a.zt.index(uint32_t(c0 + jl))] = make_double2(au, av);
+      }
+      return;
+    }
     for (int32_t jl = ext + tid; jl < nloc + ext; jl += kZgenThreads) {
       double au = 0.0, av = 0.0;
       const double jd = double(c0 + jl);
 #pragma unroll
       for (int r = LAM - 1; r >= 0; --r) {
         const int32_t il = jl - r;  // local chunk, in [0, nloc + ext)
-        const int2 d = dig[il];
+        const int2 d = dig[zpad(il)];
         const double kd = jd - double(r) - (il >= nN ? Nd : 0.0);
         double cf;
         if (r == 0) cf = 1.0;
