@@ -452,8 +452,9 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       const int lam = (p.mode == PMode::kFull) ? 0 : int(pl.mc.lambda);
       // limbs per thread: 4 when the block's coefficient window stays small
       // (wide chunks), else 2 (more CTAs per SM for narrow chunks)
-      const int pt = carry2_smem(int(p.b), lam, 4) <= size_t(64) * 1024 ? 4 : 2;
-      const size_t smem2 = carry2_smem(int(p.b), lam, pt);
+      const bool hb = p.mode == PMode::kHigh;
+      const int pt = carry2_smem(int(p.b), lam, 4, hb) <= size_t(64) * 1024 ? 4 : 2;
+      const size_t smem2 = carry2_smem(int(p.b), lam, pt, hb);
       if (!old_carry && smem2 <= kMaxDynSmem && 64 * pl.ML + 64 < (int64_t(1) << 32)) {
         a.fb = make_fastdiv(uint32_t(p.b));
         const int64_t limbs = int64_t(kC2Threads) * pt;

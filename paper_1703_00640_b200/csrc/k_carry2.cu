@@ -2,15 +2,16 @@
 // inter-block waiting.
 //
 //   k_carry_lanes  every block owns 256 x PT consecutive limbs (PT = 2 or 4
-//                  by the window size); each thread the coefficients whose
-//                  bit offsets k b land in its PT limbs.  It post-maps them (beta* low, delta+
-//                  high; nothing for the full product), rounds them with the
-//                  reference's tripwire, forms the signed 128-bit lanes
-//                  lane_m = sum e_k << (k b - 64 m) and the limb sums
-//                  s_m = lo(lane_m) + hi(lane_{m-1}), writes s_m to scratch
-//                  and the block's composed carry transfer function to
-//                  aggs[blk]; the last block to finish scans the aggregates
-//                  into every block's carry-in (cins).
+//                  by the window size) and the coefficients whose bit
+//                  offsets k b land in them.  The block post-maps them (beta*
+//                  low, delta+ high; nothing for the full product) and rounds
+//                  them with the reference's tripwire, one coefficient per
+//                  thread and pass; each thread then forms the signed 128-bit
+//                  lanes lane_m = sum e_k << (k b - 64 m) of its PT limbs and
+//                  the limb sums s_m = lo(lane_m) + hi(lane_{m-1}), writes s_m
+//                  to scratch and the block's composed carry transfer
+//                  function to aggs[blk]; the last block to finish scans the
+//                  aggregates into every block's carry-in (cins).
 //   k_carry_apply  from the block's carry-in, a block scan of the limb
 //                  transfer functions and the output limbs.
 //
@@ -18,15 +19,11 @@
 // waits on another: the lanes kernel runs at full occupancy and its
 // aggregate is final when it is written.
 //
-// The post-map runs in scatter form: each convolution value w_i meets its
-// row coefficients P_r(i) c_r (r < lambda, built with the same
-// multiplications as coef_r) and adds into a circular bank of lambda
-// accumulators, output j = i + r; output j is complete when i = j (row 0,
-// added last).  Every output therefore sums its rows in the order
-// r = lambda-1 .. 0 with the same fused multiply-adds as post_flat, so the
-// values are bit-identical to the generic path.  The few outputs that also
-// see the wrap of the cyclic maps (low: j <= lambda - 1; high: i below the
-// fold, k = N) go through the generic helpers.
+// The post-map runs in gather form with the operation order of post_flat:
+// output j sums its rows r = lambda-1 .. 0 with the same fused
+// multiply-adds, so the values are bit-identical to the generic path.  The
+// few outputs that also see the wrap of the cyclic maps (low: j <= lambda - 1;
+// high: i below the fold, k = N) go through the generic helpers.
 //
 // Reference: products_f64.cpp:29-102 (SignedAccumulator, round_accumulate),
 // maps_f64.cpp:140-188, 269-281, 350-384 (beta*, delta+).
@@ -73,21 +70,27 @@ __device__ __forceinline__ void lane_of(const long long* __restrict__ se, int64_
   }
 }
 
-// Rounded coefficients e_k of one thread's run [k0, k1) into se[k - kbase].
+// Rounded coefficients e_k, k in [kbase, kend), of the whole block into
+// se[k - kbase]: one coefficient per thread and pass (gather form), so the
+// work is spread evenly over the block.  Output j of the flat post-map sums
+// its rows as acc = fma(w_{j-r}, P_r(j-r) c_r, acc) for r = lambda-1 .. 1 and
+// adds w_j last (post_flat's order, bit-identical values).  The high product's differencing
+// x_k = hbuf(k) - hbuf(k-1) step reads hbuf from shared memory (shb), written
+// in a first pass.  The wrap outputs go through the generic helpers as before.
 template <int LAM>
-__device__ __forceinline__ void coeffs_run(const CarryArgs& a, const double* __restrict__ sww,
-                                           int64_t wlo, int64_t nw, int64_t k0, int64_t k1,
-                                           long long* __restrict__ se, int64_t kbase,
-                                           RoundAcc& ra, double psi, long long c0v) {
+__device__ __forceinline__ void coeffs_block(const CarryArgs& a, const double* __restrict__ sww,
+                                             int64_t wlo, int64_t nw, int64_t kbase,
+                                             int64_t kend, long long* __restrict__ se,
+                                             double* __restrict__ shb, RoundAcc& ra, double psi,
+                                             uint32_t& flags, int tid) {
   const MapConsts& mc = a.mc;
   auto WS = [&](int64_t j) -> double {
     const int64_t o = j - wlo;
     return (o >= 0 && o < nw) ? sww[o] : __ldg(a.w + j);
   };
   if constexpr (LAM == 0) {
-    for (int64_t k = k0; k < k1; ++k) se[k - kbase] = ra.round(sww[k - wlo]);
+    for (int64_t k = kbase + tid; k < kend; k += kT) se[k - kbase] = ra.round(sww[k - wlo]);
   } else {
-    if (k0 >= k1) return;
     const int b = mc.b;
     const int64_t N = mc.N;
     const bool low = mc.mode == kModeLow;
@@ -97,59 +100,52 @@ __device__ __forceinline__ void coeffs_run(const CarryArgs& a, const double* __r
     double cr[LAM];
 #pragma unroll
     for (int r = 0; r < LAM; ++r) cr[r] = mc.cpost[r];
-    // post_flat outputs j: low j = k + 1 over [k0 + 1, k1 + 1); high the
-    // folded buffer hbuf(i) over [k0 - 1, k1) (x_k needs hbuf(k), hbuf(k-1))
-    const int64_t j0 = low ? k0 + 1 : k0 - 1;
-    const int64_t j1 = low ? k1 + 1 : k1;
-    const int64_t hslow = int64_t(mc.nfold) + LAM - 2;  // hbuf(i) = post_flat(i) from here on
-    double acc[LAM];
+    // flat post-map output j (inputs outside [0, N) contribute nothing)
+    auto pf = [&](int64_t j) -> double {
+      double acc = 0.0;
 #pragma unroll
-    for (int r = 0; r < LAM; ++r) acc[r] = 0.0;
-    double hprev = 0.0;
-    for (int64_t base = j0 - (LAM - 1); base < j1; base += LAM) {
+      for (int r = LAM - 1; r >= 1; --r) {
+        const int64_t i = j - r;
+        if (i >= 0 && i < N) {
+          const double id = double(i);
+          double p = id, f = id + st;
 #pragma unroll
-      for (int u = 0; u < LAM; ++u) {
-        const int64_t i = base + u;
-        if (i < j1) {
-          if (i >= 0 && i < N) {
-            // rows r = LAM-1 .. 1 of w_i go to outputs i + r; row 0 to i
-            const double wi = sww[i - wlo];
-            const double kd = double(i);
-            double p = kd, f = kd + st;
-            double cf[LAM];
-            cf[0] = 1.0;
-#pragma unroll
-            for (int r = 1; r < LAM; ++r) {
-              cf[r] = p * cr[r];
-              p *= f;
-              f += st;
-            }
-#pragma unroll
-            for (int r = LAM - 1; r >= 1; --r) acc[(u + r) % LAM] = fma(wi, cf[r], acc[(u + r) % LAM]);
-            acc[u] = acc[u] + wi;
+          for (int t = 1; t < r; ++t) {
+            p *= f;
+            f += st;
           }
-          // output j = i is complete
-          const double pf = acc[u];
-          acc[u] = 0.0;
-          if (i >= j0) {
-            if (low) {
-              const int64_t k = i - 1;
-              const double x = (i <= LAM - 1) ? postmap_low(mc, WS, i) : pf * sc;
-              long long e = ra.round(x);
-              if (k == 0) e += (c0v >> b);
-              se[k - kbase] = e;
-            } else {
-              const double hb = (i < hslow && i < N) ? high_buf(mc, WS, i) : pf;
-              if (i >= k0) {
-                const int64_t k = i;
-                double v = (k == N) ? psi - hprev * step : hb - hprev * step;
-                if (k < mc.nfold) v -= psi * mc.fold[k];
-                se[k - kbase] = ra.round(v * sc);
-              }
-              hprev = (i >= 0 && i < N) ? hb : 0.0;
-            }
-          }
+          acc = fma(sww[i - wlo], p * cr[r], acc);
         }
+      }
+      if (j >= 0 && j < N) acc = acc + sww[j - wlo];
+      return acc;
+    };
+    if (low) {
+      for (int64_t k = kbase + tid; k < kend; k += kT) {
+        const int64_t i = k + 1;
+        const double x = (i <= LAM - 1) ? postmap_low(mc, WS, i) : pf(i) * sc;
+        long long e = ra.round(x);
+        if (k == 0) {
+          const long long c0v = ra.round(postmap_low(mc, WS, 0));
+          if (c0v & ((1ll << b) - 1)) flags |= kFlagLowNotDivisible;
+          e += (c0v >> b);
+        }
+        se[k - kbase] = e;
+      }
+    } else {
+      const int64_t hslow = int64_t(mc.nfold) + LAM - 2;  // hbuf(i) = post_flat(i) from here on
+      // shb[i - kbase + 1] = hbuf(i) for i in [kbase - 1, kend), zero outside [0, N)
+      for (int64_t i = kbase - 1 + tid; i < kend; i += kT) {
+        double hb = 0.0;
+        if (i >= 0 && i < N) hb = (i < hslow) ? high_buf(mc, WS, i) : pf(i);
+        shb[i - kbase + 1] = hb;
+      }
+      __syncthreads();
+      for (int64_t k = kbase + tid; k < kend; k += kT) {
+        const double hp = shb[k - kbase];
+        double v = (k == N) ? psi - hp * step : shb[k - kbase + 1] - hp * step;
+        if (k < mc.nfold) v -= psi * mc.fold[k];
+        se[k - kbase] = ra.round(v * sc);
       }
     }
   }
@@ -165,6 +161,7 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
   __shared__ long long s_hi[kT];
   __shared__ double s_psi;
   __shared__ uint32_t s_flags;
+  __shared__ double2 s_red[kT / 32];
   const int tid = threadIdx.x;
   const MapConsts& mc = a.mc;
   const int b = mc.b;
@@ -204,20 +201,11 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
   __syncthreads();
   RoundAcc ra;
   uint32_t flags = 0;
-  long long c0v = 0;
   const int64_t m0 = ms + int64_t(tid) * kPT;
-  if (mc.mode == kModeLow && ms == 0 && tid == 0) {
-    auto WS = [&](int64_t j) -> double {
-      const int64_t o = j - wlo;
-      return (o >= 0 && o < nw) ? sww[o] : __ldg(a.w + j);
-    };
-    c0v = ra.round(postmap_low(mc, WS, 0));
-    if (c0v & ((1ll << b) - 1)) flags |= kFlagLowNotDivisible;
-  }
-  // this thread's coefficients (thread 0 also those of lane ms - 1)
-  const int64_t kr0 = (tid == 0) ? kbase : kfirst(m0, a.fb, K);
-  const int64_t kr1 = kfirst(min(m0 + kPT, me), a.fb, K);
-  if (m0 < me) coeffs_run<LAM>(a, sww, wlo, nw, kr0, kr1, se, kbase, ra, s_psi, c0v);
+  // the block's coefficients (those of lane ms - 1 included)
+  double* shb = reinterpret_cast<double*>(se + (kend - kbase) + 2);
+  coeffs_block<LAM>(a, sww, wlo, nw, kbase, kend, se, shb, ra, s_psi, flags, tid);
+  __syncthreads();
   // lanes of the thread's limbs
   unsigned long long lo[kPT];
   long long hi[kPT];
@@ -264,7 +252,7 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
       e = fmax(e, __shfl_xor_sync(0xffffffffu, e, off));
       m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
     }
-    if ((tid & 31) == 0) status_merge(a.status, e, m, 0);
+    if ((tid & 31) == 0) s_red[tid >> 5] = make_double2(e, m);
   }
   if (flags) atomicOr(&s_flags, flags);
   // the last block to finish turns the per-block functions into each
@@ -275,7 +263,16 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
     s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
   }
   __syncthreads();
-  if (tid == 0 && s_flags) atomicOr(&a.status->flags, s_flags);
+  if (tid == 0) {
+    // one status update per block
+    double e = 0.0, m = 0.0;
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) {
+      e = fmax(e, s_red[w].x);
+      m = fmax(m, s_red[w].y);
+    }
+    status_merge(a.status, e, m, s_flags);
+  }
   if (s_last) {
     __threadfence();
     const uint32_t B = gridDim.x;
@@ -375,9 +372,9 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
   }
 }
 
-size_t carry2_smem(int b, int lam, int pt) {
+size_t carry2_smem(int b, int lam, int pt, bool hbuf) {
   const int64_t nk = (64 * int64_t(kC2Threads * pt + 1) + b - 1) / b + 4;
-  return size_t(nk + lam + 8) * 8 + size_t(nk + 4) * 8 + 64;
+  return size_t(nk + lam + 8) * 8 + size_t(nk + 4) * 8 + (hbuf ? size_t(nk + 4) * 8 : 0) + 64;
 }
 
 template <int PT>
