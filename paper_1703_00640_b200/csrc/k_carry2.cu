@@ -91,6 +91,48 @@ __device__ __forceinline__ void coeffs_block(const CarryArgs& a, const double* _
   if constexpr (LAM == 0) {
     for (int64_t k = kbase + tid; k < kend; k += kT) se[k - kbase] = ra.round(sww[k - wlo]);
   } else {
+    // Blocks whose post-map inputs all lie in [0, N) away from the wrap
+    // outputs (block-uniform) take the same arithmetic without bound checks,
+    // 32-bit indices and exact FP64 index conversions.
+    const int64_t N0 = mc.N;
+    const int64_t hs0 = int64_t(mc.nfold) + LAM - 2;
+    const bool lowm = mc.mode == kModeLow;
+    const bool interior = kbase >= LAM + 1 && kend + 1 <= N0 && kend - wlo < (int64_t(1) << 31) &&
+                          (lowm || kbase - 1 >= hs0);
+    if (interior) {
+      const double st = lowm ? double(N0) : -double(N0);
+      const double step = mc.step, sc = mc.scale_out;
+      double cr[LAM];
+#pragma unroll
+      for (int r = 0; r < LAM; ++r) cr[r] = mc.cpost[r];
+      const double* wb = sww - wlo;  // wb[i] = w_i inside the window
+      const uint32_t kb32 = uint32_t(kbase);
+      auto pfd = [&](uint32_t j) -> double {
+        const double jd = __hiloint2double(0x43300000, int(j)) - 4503599627370496.0;
+        double acc = 0.0;
+#pragma unroll
+        for (int r = LAM - 1; r >= 1; --r) {
+          const double id = jd - double(r);
+          double p = id, f = id + st;
+#pragma unroll
+          for (int t = 1; t < r; ++t) {
+            p *= f;
+            f += st;
+          }
+          acc = fma(wb[j - r], p * cr[r], acc);
+        }
+        return acc + wb[j];
+      };
+      const uint32_t nk = uint32_t(kend - kbase);
+      if (lowm) {
+        for (uint32_t q = tid; q < nk; q += kT) se[q] = ra.round(pfd(kb32 + q + 1) * sc);
+      } else {
+        for (uint32_t q = tid; q < nk + 1; q += kT) shb[q] = pfd(kb32 + q - 1);
+        __syncthreads();
+        for (uint32_t q = tid; q < nk; q += kT) se[q] = ra.round((shb[q + 1] - shb[q] * step) * sc);
+      }
+      return;
+    }
     const int b = mc.b;
     const int64_t N = mc.N;
     const bool low = mc.mode == kModeLow;

@@ -181,6 +181,21 @@ struct RoundAcc {
   uint32_t flags = 0;
   __device__ __forceinline__ long long round(double x) {
     double ax = fabs(x);
+    if (ax < 2251799813685248.0) {
+      // |x| < 2^51: adding 1.5 * 2^52 rounds x to the nearest integer (ties
+      // to even, as rint) and leaves it in the low mantissa bits -- no
+      // FRND / F2I on the quarter-rate conversion path
+      const double t = x + 6755399441055744.0;
+      const double r = t - 6755399441055744.0;
+      const double e = fabs(x - r);
+      max_err = fmax(max_err, e);
+      max_abs = fmax(max_abs, ax);
+      if (e > 0.25) flags |= kFlagTripwire;
+      return __double_as_longlong(t) - 0x4338000000000000ll;
+    }
+    return round_wide(x, ax);
+  }
+  __device__ __forceinline__ long long round_wide(double x, double ax) {
     if (!(ax < 9007199254740992.0)) {
       flags |= kFlagOverflow;
       max_abs = fmax(max_abs, isnan(ax) ? 1e308 : ax);
