@@ -322,7 +322,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.cbits_u = w.cbu.as<uint32_t>();
       a.cbits_v = w.cbv.as<uint32_t>();
       a.aux = w.aux.as<double>();
-      auto f1k = pl.colpp ? k_f1_pp : k_f1;
+      auto f1k = pl.colct ? pl.colct->f1 : pl.colpp ? k_f1_pp : k_f1;
       set_smem(f1k, pl.smem_f1);
       {
         KTimer kt(cx, "k_f1", double(p.N) * 16.0 + double(L) * 16.0, int(p.mode), st);
@@ -418,7 +418,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.g.ncols = pl.B * (pl.C / 2);
       a.logc = pl.logc_il;
       a.fft = pl.iA;
-      auto ilk = pl.colpp ? k_ilast_pp : k_ilast;
+      auto ilk = pl.colct ? pl.colct->ilast : pl.colpp ? k_ilast_pp : k_ilast;
       set_smem(ilk, pl.smem_il);
       {
         KTimer kt(cx, "k_ilast", double(L) * 16.0, int(p.mode), st);

@@ -681,6 +681,210 @@ k_ilast_pp(ILastArgs a) {
 
 
 // ---------------------------------------------------------------------------
+// Column passes with compile-time radix schedules (the column analogue of
+// k_mid_4096).  A CTA owns c = 2^LOGC consecutive columns of length R
+// (interleaved in shared memory, LayCols).  Every stage's butterflies are
+// spread over the NTHR threads, NB = ceil(c R / (RAD NTHR)) per thread, with
+// strides, butterfly counts and stage-table offsets known at compile time.
+// The first stage loads straight from global memory (all of a thread's
+// loads in flight together), the last stores straight to global memory, so
+// the tile never makes a separate staging pass through shared memory.
+// Numerics are those of the generic passes (same stage tables, same
+// in-register DFTs).
+template <int RAD, int NB, uint32_t R, int LOGC, int NTHR, class Src>
+__device__ __forceinline__ void cc_load(double2 (&x)[16], const Src& src, int tid) {
+  constexpr uint32_t nbi = R / RAD, nbf = nbi << LOGC;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const uint32_t bf = uint32_t(tid) + uint32_t(i) * NTHR;
+    if (nbf % NTHR == 0 || bf < nbf) {
+      const uint32_t item = bf & ((1u << LOGC) - 1), t = bf >> LOGC;
+#pragma unroll
+      for (int q = 0; q < RAD; ++q) x[i * RAD + q] = src(item, t + q * nbi);
+    }
+  }
+}
+
+template <int RAD, int NB, bool INV, uint32_t R, uint32_t NS, int LOGC, int NTHR, class Sink>
+__device__ __forceinline__ void cc_store(double2 (&x)[16], const double2* __restrict__ stab,
+                                         uint32_t qmul, const Sink& sink, int tid) {
+  constexpr uint32_t nbi = R / RAD, nbf = nbi << LOGC;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const uint32_t bf = uint32_t(tid) + uint32_t(i) * NTHR;
+    if (nbf % NTHR == 0 || bf < nbf) {
+      const uint32_t item = bf & ((1u << LOGC) - 1), t = bf >> LOGC;
+      const uint32_t tq = t / NS, j = t - tq * NS;
+      const uint32_t ob = tq * NS * RAD + j;
+      double2* xv = x + i * RAD;
+      if constexpr (SinkPrep<Sink>::value) {
+        const auto pre = sink.prep(item, ob);
+        if (NS > 1 && j != 0) {
+#pragma unroll
+          for (int q = 1; q < RAD; ++q) {
+            const double2 w = stab[(uint32_t(q) * qmul - 1) * NS + j];
+            xv[q] = INV ? cmulc(xv[q], w) : cmul(xv[q], w);
+          }
+        }
+        dft<RAD, INV>(xv);
+#pragma unroll
+        for (int q = 0; q < RAD; ++q) sink.put(item, ob + q * NS, uint32_t(q), xv[q], pre);
+      } else {
+        if (NS > 1 && j != 0) {
+#pragma unroll
+          for (int q = 1; q < RAD; ++q) {
+            const double2 w = stab[(uint32_t(q) * qmul - 1) * NS + j];
+            xv[q] = INV ? cmulc(xv[q], w) : cmul(xv[q], w);
+          }
+        }
+        dft<RAD, INV>(xv);
+#pragma unroll
+        for (int q = 0; q < RAD; ++q) sink(item, ob + q * NS, xv[q]);
+      }
+    }
+  }
+}
+
+template <bool INV, class SC, int S, int LOGC, int NTHR, class Src, class Sink>
+__device__ __forceinline__ void cc_stages(double2 (&x)[16], double2* __restrict__ buf,
+                                          const LayCols& lay, const double2* __restrict__ stab,
+                                          const SubFft& p, const Src& src, const Sink& sink,
+                                          int tid) {
+  constexpr int RAD = SC::rad(S);
+  constexpr uint32_t NS = SC::ns(S);
+  constexpr uint32_t R = SC::R;
+  constexpr uint32_t nbf = (R / RAD) << LOGC;
+  constexpr int NB = int((nbf + NTHR - 1) / NTHR);
+  static_assert(NB * RAD <= 16, "register block");
+  constexpr bool last = S + 1 == SC::nst;
+  if constexpr (S == 0) {
+    cc_load<RAD, NB, R, LOGC, NTHR>(x, src, tid);
+  } else {
+    cc_load<RAD, NB, R, LOGC, NTHR>(x, SmemSrc<LayCols>{buf, lay}, tid);
+  }
+  __syncthreads();
+  const double2* st = stab + p.toff[S];
+  if constexpr (last) {
+    cc_store<RAD, NB, INV, R, NS, LOGC, NTHR>(x, st, p.qmul[S], sink, tid);
+  } else {
+    cc_store<RAD, NB, INV, R, NS, LOGC, NTHR>(x, st, p.qmul[S], SmemSink<LayCols>{buf, lay}, tid);
+    __syncthreads();
+    cc_stages<INV, SC, S + 1, LOGC, NTHR>(x, buf, lay, stab, p, src, sink, tid);
+  }
+}
+
+// First column pass's sink: T[k][col] = v omega_L^{col k} with
+// omega_L^{col (ob + q NS)} = omega_L^{col ob} * omega_L^{col NS q}; the
+// first factor is fetched before the last stage's DFT (prep), the second
+// comes from a per-CTA table qt[item * RADL + q].
+template <uint32_t RADL>
+struct F1SinkQ {
+  double2* out;
+  uint32_t ncols, col0;
+  TwGlobal tw;
+  const double2* qt;
+  __device__ __forceinline__ double2 prep(uint32_t item, uint32_t ob) const {
+    const uint32_t x = (col0 + item) * ob;
+    return x ? tw.get(x) : make_double2(1.0, 0.0);
+  }
+  __device__ __forceinline__ void put(uint32_t item, uint32_t k, uint32_t q, double2 v,
+                                      double2 b) const {
+    out[int64_t(k) * ncols + col0 + item] = cmul(v, cmul(b, qt[item * RADL + q]));
+  }
+};
+template <uint32_t RADL>
+struct SinkPrep<F1SinkQ<RADL>> {
+  static constexpr bool value = true;
+};
+
+template <class SC>
+__host__ __device__ constexpr uint32_t ct_last_rad() { return uint32_t(SC::rad(SC::nst - 1)); }
+template <class SC>
+__host__ __device__ constexpr uint32_t ct_last_ns() { return SC::ns(SC::nst - 1); }
+
+size_t colct_smem_bytes(uint32_t R, uint32_t c, uint32_t stablen, uint32_t radl) {
+  return size_t(padded_len(R * c)) * 16 + size_t(stablen) * 16 + size_t(c) * radl * 16;
+}
+
+template <class SC, int LOGC, int NTHR>
+__global__ void __launch_bounds__(NTHR, 1) k_f1_ct(F1Args a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sbuf = reinterpret_cast<double2*>(smem_raw);
+  constexpr uint32_t c = 1u << LOGC, R = SC::R;
+  constexpr uint32_t RL = ct_last_rad<SC>(), NSL = ct_last_ns<SC>();
+  const int tid = threadIdx.x;
+  const uint32_t col0 = blockIdx.x * c;
+  const MapConsts& mc = a.mc;
+  const int64_t N = mc.N;
+  double2* stab = sbuf + padded_len(R * c);
+  double2* qt = stab + a.fft.stablen;
+  const TwGlobal tw = a.tw;
+  pdl_trigger();
+  for (uint32_t i = tid; i < a.fft.stablen; i += NTHR) stab[i] = __ldg(a.fft.stab + i);
+  if (uint32_t(tid) < c * RL) {
+    const uint32_t it = uint32_t(tid) / RL, q = uint32_t(tid) - it * RL;
+    const uint32_t x = (col0 + it) * NSL * q;
+    qt[tid] = x ? tw.get(x) : make_double2(1.0, 0.0);
+  }
+  pdl_wait();
+  double topu = 0.0, topv = 0.0;
+  if (mc.mode == kModeHigh && col0 < uint32_t(mc.nfold + mc.lambda)) {
+    topu = digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, N, mc.balanced != 0);
+    topv = digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, N, mc.balanced != 0);
+  }
+  if (mc.mode == kModeHigh && blockIdx.x == 0 && tid == 0) {
+    auto Du = [&](int64_t i) { return digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, i, mc.balanced != 0); };
+    auto Dv = [&](int64_t i) { return digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, i, mc.balanced != 0); };
+    a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
+  }
+  const LayCols lay{uint32_t(LOGC), c - 1};
+  double2 x[16];
+  cc_stages<false, SC, 0, LOGC, NTHR>(x, sbuf, lay, stab, a.fft,
+                                      ZSrc{a.z, a.zt, N, a.ncols, col0, &a.mc, topu, topv},
+                                      F1SinkQ<RL>{a.out, a.ncols, col0, tw, qt}, tid);
+}
+
+template <class SC, int LOGC, int NTHR>
+__global__ void __launch_bounds__(NTHR, 1) k_ilast_ct(ILastArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sbuf = reinterpret_cast<double2*>(smem_raw);
+  constexpr uint32_t c = 1u << LOGC, R = SC::R;
+  const int tid = threadIdx.x;
+  const uint32_t col0 = blockIdx.x * c;
+  double2* stab = sbuf + padded_len(R * c);
+  pdl_trigger();
+  for (uint32_t i = tid; i < a.fft.stablen; i += NTHR) stab[i] = __ldg(a.fft.stab + i);
+  pdl_wait();
+  const LayCols lay{uint32_t(LOGC), c - 1};
+  double2 x[16];
+  cc_stages<true, SC, 0, LOGC, NTHR>(x, sbuf, lay, stab, a.fft, ColSrc{a.data, a.g, 0, col0},
+                                     CoefSink{a.coef, a.g.ncols, col0}, tid);
+}
+
+// Compiled column shapes: {R, radices (maxrad 16 schedule), LOGC, NTHR}.
+#define TMG_COLCT(R_, LOGC_, NTHR_, ...)                                             \
+  {R_, LOGC_, NTHR_, {__VA_ARGS__}, k_f1_ct<Sched<__VA_ARGS__>, LOGC_, NTHR_>,      \
+   k_ilast_ct<Sched<__VA_ARGS__>, LOGC_, NTHR_>, ct_last_rad<Sched<__VA_ARGS__>>()}
+static const ColCtShape kColCtShapes[] = {
+    TMG_COLCT(1792, 2, 512, 16, 16, 7),
+    TMG_COLCT(1400, 2, 512, 8, 5, 5, 7),
+};
+#undef TMG_COLCT
+
+const ColCtShape* colct_shape(uint32_t R, const int32_t* rad, int nst) {
+  static const bool off = getenv("TMG_NO_COLCT") != nullptr;
+  if (off) return nullptr;
+  for (const ColCtShape& sh : kColCtShapes) {
+    if (sh.R != R) continue;
+    bool ok = true;
+    int n = 0;
+    for (; n < 4 && sh.rad[n]; ++n) ok = ok && n < nst && sh.rad[n] == rad[n];
+    if (ok && n == nst) return &sh;
+  }
+  return nullptr;
+}
+
+// ---------------------------------------------------------------------------
 // Post-map, rounding and carry propagation over all limbs.
 //   phase 1  coefficients e_k of the block's lanes: post-map (once per
 //            coefficient; the high product's folded buffer is staged in

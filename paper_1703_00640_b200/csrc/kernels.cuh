@@ -173,6 +173,21 @@ struct ILastArgs {
 };
 __global__ void k_ilast(ILastArgs a);
 __global__ void k_ilast_pp(ILastArgs a);
+// Compile-time column passes (k_f1_ct / k_ilast_ct) for the hot lengths.
+using F1Fn = void (*)(F1Args);
+using ILastFn = void (*)(ILastArgs);
+struct ColCtShape {
+  uint32_t R;
+  int logc, nthr;
+  int rad[4];
+  F1Fn f1;
+  ILastFn ilast;
+  uint32_t radl;  // radix of the last stage (F1 output twiddle table)
+};
+// The compiled shape for column length R with the given radix schedule, or
+// nullptr (TMG_NO_COLCT disables them).
+const ColCtShape* colct_shape(uint32_t R, const int32_t* rad, int nst);
+size_t colct_smem_bytes(uint32_t R, uint32_t c, uint32_t stablen, uint32_t radl);
 
 struct CarryArgs {
   const double* w;  // convolution coefficients (L of them)

@@ -496,7 +496,31 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
       }
     }
   }
-  {
+  // Compile-time column passes where the column length and its radix-16
+  // schedule match a compiled shape (two-pass plans only).
+  pl->colct = nullptr;
+  if (pl->kind == 2) {
+    SubFft f16 = make_subfft(A, tA, 1, &tw);
+    const ColCtShape* sh = colct_shape(A, f16.rad, f16.nst);
+    if (sh) {
+      const uint32_t cc = 1u << sh->logc;
+      const size_t sf = colct_smem_bytes(A, cc, f16.stablen, sh->radl);
+      const size_t si = colct_smem_bytes(A, cc, f16.stablen, 0);
+      if ((UL / A) % cc == 0 && (C / 2) % cc == 0 && sf <= kMaxDynSmem) {
+        pl->colct = sh;
+        pl->colpp = false;
+        pl->fA = f16;
+        pl->iA = f16;
+        pl->logc_f1 = pl->logc_il = uint32_t(sh->logc);
+        pl->thr_f1 = pl->thr_il = sh->nthr;
+        pl->smem_f1 = sf;
+        pl->smem_il = si;
+      }
+    }
+  }
+  if (pl->colct) {
+    pl->f1_stw = false;
+  } else {
     // staged F1 twiddles where the thread count is a multiple of the
     // columns per CTA and the extra table still fits
     const uint32_t c1 = 1u << pl->logc_f1;
