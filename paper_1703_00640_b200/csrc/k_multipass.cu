@@ -807,7 +807,7 @@ size_t colct_smem_bytes(uint32_t R, uint32_t c, uint32_t stablen, uint32_t radl)
 }
 
 template <class SC, int LOGC, int NTHR>
-__global__ void __launch_bounds__(NTHR, 1) k_f1_ct(F1Args a) {
+__global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1)) k_f1_ct(F1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   constexpr uint32_t c = 1u << LOGC, R = SC::R;
@@ -845,7 +845,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_f1_ct(F1Args a) {
 }
 
 template <class SC, int LOGC, int NTHR>
-__global__ void __launch_bounds__(NTHR, 1) k_ilast_ct(ILastArgs a) {
+__global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1)) k_ilast_ct(ILastArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   constexpr uint32_t c = 1u << LOGC, R = SC::R;
@@ -868,14 +868,18 @@ __global__ void __launch_bounds__(NTHR, 1) k_ilast_ct(ILastArgs a) {
 static const ColCtShape kColCtShapes[] = {
     TMG_COLCT(1792, 2, 512, 16, 16, 7),
     TMG_COLCT(1400, 2, 512, 8, 5, 5, 7),
+    TMG_COLCT(1792, 1, 256, 16, 16, 7),
+    TMG_COLCT(1400, 1, 256, 8, 5, 5, 7),
 };
 #undef TMG_COLCT
 
 const ColCtShape* colct_shape(uint32_t R, const int32_t* rad, int nst) {
   static const bool off = getenv("TMG_NO_COLCT") != nullptr;
+  // TMG_COLCT_LOGC (testing): only shapes with this many columns per CTA
+  static const int want_logc = getenv("TMG_COLCT_LOGC") ? atoi(getenv("TMG_COLCT_LOGC")) : -1;
   if (off) return nullptr;
   for (const ColCtShape& sh : kColCtShapes) {
-    if (sh.R != R) continue;
+    if (sh.R != R || (want_logc >= 0 && sh.logc != want_logc)) continue;
     bool ok = true;
     int n = 0;
     for (; n < 4 && sh.rad[n]; ++n) ok = ok && n < nst && sh.rad[n] == rad[n];
