@@ -179,6 +179,7 @@ using ILastFn = void (*)(ILastArgs);
 struct ColCtShape {
   uint32_t R;
   int logc, nthr;
+  int maxrad;  // radix_schedule's largest power-of-two radix (16 or 8)
   int rad[4];
   F1Fn f1;
   ILastFn ilast;
@@ -186,7 +187,7 @@ struct ColCtShape {
 };
 // The compiled shape for column length R with the given radix schedule, or
 // nullptr (TMG_NO_COLCT disables them).
-const ColCtShape* colct_shape(uint32_t R, const int32_t* rad, int nst);
+const ColCtShape* colct_shape(uint32_t R, int maxrad, const int32_t* rad, int nst);
 size_t colct_smem_bytes(uint32_t R, uint32_t c, uint32_t stablen, uint32_t radl);
 
 struct CarryArgs {

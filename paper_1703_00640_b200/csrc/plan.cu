@@ -500,8 +500,10 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   // schedule match a compiled shape (two-pass plans only).
   pl->colct = nullptr;
   if (pl->kind == 2) {
-    SubFft f16 = make_subfft(A, tA, 1, &tw);
-    const ColCtShape* sh = colct_shape(A, f16.rad, f16.nst);
+    // TMG_COLCT_MAXRAD (testing): 8 selects radix-8 shapes, if compiled
+    static const int mr = getenv("TMG_COLCT_MAXRAD") ? atoi(getenv("TMG_COLCT_MAXRAD")) : 16;
+    SubFft f16 = make_subfft(A, tA, 1, &tw, mr);
+    const ColCtShape* sh = colct_shape(A, mr, f16.rad, f16.nst);
     if (sh) {
       const uint32_t cc = 1u << sh->logc;
       const size_t sf = colct_smem_bytes(A, cc, f16.stablen, sh->radl);
