@@ -46,6 +46,22 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _traffic(kernel):
+    """DRAM bytes per launch of `kernel` ("full:k_mid", ...) from the newest
+    committed ncu --set full capture summary (profiles/*_traffic.json,
+    tools/ncu_traffic.py), or (None, None)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    if not files:
+        return None, None
+    try:
+        with open(files[-1]) as f:
+            d = json.load(f)["per_launch"]
+        return round(d[kernel]["dram_bytes"]), os.path.relpath(files[-1], ROOT)
+    except Exception:
+        return None, None
+
+
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled through NVML every
     few milliseconds while the timed region runs."""
@@ -250,9 +266,12 @@ def run_ours(args, world, rank, local):
     top_ms = top[1][0] / top[1][1]
     top_bytes = top[1][2] / top[1][1]
     achieved = top_bytes / (top_ms * 1e-3) / 1e9
+    traffic, traffic_src = _traffic(top[0])
     roofline = {"bound": "hbm", "kernel": top[0], "achieved": round(achieved, 1), "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": None, "share_of_step": round(top[1][0] / sum(a[0] for a in agg.values()), 3)}
+                "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_bytes": round(top_bytes),
+                "share_of_step": round(top[1][0] / sum(a[0] for a in agg.values()), 3)}
     # whole-step HBM view: algorithmic bytes of all kernels / step time
     step_bytes = sum(a[2] for a in agg.values()) / prof_steps
     step_roof = step_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9
