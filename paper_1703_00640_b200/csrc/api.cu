@@ -326,7 +326,15 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       set_smem(f1k, pl.smem_f1);
       {
         KTimer kt(cx, "k_f1", double(p.N) * 16.0 + double(L) * 16.0, int(p.mode), st);
-        launch(f1k, dim3(a.ncols >> a.logc), dim3(pl.thr_f1), pl.smem_f1, st, a, "f1");
+        // the compile-time passes are persistent (one wave of CTAs)
+        // TMG_F1_WAVES (testing): persistent CTAs per SM slot (0: one per tile)
+        static const int f1w = getenv("TMG_F1_WAVES") ? atoi(getenv("TMG_F1_WAVES")) : 1;
+        const unsigned tiles = a.ncols >> a.logc;
+        const unsigned grid =
+            (pl.colct && f1w > 0)
+                ? std::min<unsigned>(tiles, unsigned(f1w * cx.num_sms * (pl.colct->nthr <= 256 ? 2 : 1)))
+                : tiles;
+        launch(f1k, dim3(grid), dim3(pl.thr_f1), pl.smem_f1, st, a, "f1");
       }
       check_launch("k_f1");
       ++kernels;
@@ -422,7 +430,14 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       set_smem(ilk, pl.smem_il);
       {
         KTimer kt(cx, "k_ilast", double(L) * 16.0, int(p.mode), st);
-        launch(ilk, dim3(a.g.ncols >> a.logc), dim3(pl.thr_il), pl.smem_il, st, a, "ilast");
+        // TMG_IL_WAVES (testing): persistent CTAs per SM slot (0: one per tile)
+        static const int ilw = getenv("TMG_IL_WAVES") ? atoi(getenv("TMG_IL_WAVES")) : 0;
+        const unsigned tiles = a.g.ncols >> a.logc;
+        const unsigned grid =
+            (pl.colct && ilw > 0)
+                ? std::min<unsigned>(tiles, unsigned(ilw * cx.num_sms * (pl.colct->nthr <= 256 ? 2 : 1)))
+                : tiles;
+        launch(ilk, dim3(grid), dim3(pl.thr_il), pl.smem_il, st, a, "ilast");
       }
       check_launch("k_ilast");
       ++kernels;

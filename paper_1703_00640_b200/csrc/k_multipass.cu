@@ -803,9 +803,15 @@ template <class SC>
 __host__ __device__ constexpr uint32_t ct_last_ns() { return SC::ns(SC::nst - 1); }
 
 size_t colct_smem_bytes(uint32_t R, uint32_t c, uint32_t stablen, uint32_t radl) {
-  return size_t(padded_len(R * c)) * 16 + size_t(stablen) * 16 + size_t(c) * radl * 16;
+  return size_t(padded_len(R * c)) * 16 + size_t(stablen) * 16 + 2 * size_t(c) * radl * 16;
 }
 
+// Both kernels are persistent: a CTA stages the stage table once and walks
+// the tiles tile = blockIdx.x + i gridDim.x, prefetching the next tile into
+// L2 while the current one computes.  F1's output-twiddle table depends on
+// the tile's columns: it is double-buffered by tile parity, so a tile's
+// table is written while the previous tile's last stage may still read the
+// other one.
 template <class SC, int LOGC, int NTHR, int P>
 __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1)) k_f1_ct(F1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -813,35 +819,49 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1)) k_f1_ct(F1Args a)
   constexpr uint32_t c = 1u << LOGC, R = SC::R;
   constexpr uint32_t RL = ct_last_rad<SC>(), NSL = ct_last_ns<SC>();
   const int tid = threadIdx.x;
-  const uint32_t col0 = blockIdx.x * c;
   const MapConsts& mc = a.mc;
   const int64_t N = mc.N;
   double2* stab = sbuf + padded_len(R * c);
-  double2* qt = stab + a.fft.stablen;
+  double2* qt2 = stab + a.fft.stablen;
   const TwGlobal tw = a.tw;
+  const uint32_t ntiles = a.ncols >> LOGC;
   pdl_trigger();
   for (uint32_t i = tid; i < a.fft.stablen; i += NTHR) stab[i] = __ldg(a.fft.stab + i);
-  if (uint32_t(tid) < c * RL) {
-    const uint32_t it = uint32_t(tid) / RL, q = uint32_t(tid) - it * RL;
-    const uint32_t x = (col0 + it) * NSL * q;
-    qt[tid] = x ? tw.get(x) : make_double2(1.0, 0.0);
-  }
   pdl_wait();
-  double topu = 0.0, topv = 0.0;
-  if (mc.mode == kModeHigh && col0 < uint32_t(mc.nfold + mc.lambda)) {
-    topu = digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, N, mc.balanced != 0);
-    topv = digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, N, mc.balanced != 0);
-  }
   if (mc.mode == kModeHigh && blockIdx.x == 0 && tid == 0) {
     auto Du = [&](int64_t i) { return digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, i, mc.balanced != 0); };
     auto Dv = [&](int64_t i) { return digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, i, mc.balanced != 0); };
-    a.aux[0] = root_channel(mc, Du, topu) * root_channel(mc, Dv, topv);
+    double tu = 0.0, tv = 0.0;
+    if (0 < uint32_t(mc.nfold + mc.lambda)) {
+      tu = Du(N);
+      tv = Dv(N);
+    }
+    a.aux[0] = root_channel(mc, Du, tu) * root_channel(mc, Dv, tv);
   }
   const LayCols lay{uint32_t(LOGC), c - 1};
-  double2 x[P];
-  cc_stages<false, SC, 0, LOGC, NTHR, P>(x, sbuf, lay, stab, a.fft,
-                                      ZSrc{a.z, a.zt, N, a.ncols, col0, &a.mc, topu, topv},
-                                      F1SinkQ<RL>{a.out, a.ncols, col0, tw, qt}, tid);
+  const uint64_t tile_bytes = uint64_t(a.zt.zrows) * c * 16;
+  uint32_t par = 0;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, par ^= 1u) {
+    const uint32_t col0 = tile * c;
+    const uint32_t nx = tile + gridDim.x;
+    if (tid == 0 && nx < ntiles && !a.zt.natural)
+      prefetch_l2(a.z + uint64_t(nx) * a.zt.zrows * c, uint32_t(tile_bytes));
+    double2* qt = qt2 + par * (c * RL);
+    if (uint32_t(tid) < c * RL) {
+      const uint32_t it = uint32_t(tid) / RL, q = uint32_t(tid) - it * RL;
+      const uint32_t x = (col0 + it) * NSL * q;
+      qt[tid] = x ? tw.get(x) : make_double2(1.0, 0.0);
+    }
+    double topu = 0.0, topv = 0.0;
+    if (mc.mode == kModeHigh && col0 < uint32_t(mc.nfold + mc.lambda)) {
+      topu = digit_at(a.u, a.nlimbs, a.b, a.lead, a.count, a.cbits_u, N, mc.balanced != 0);
+      topv = digit_at(a.v, a.nlimbs, a.b, a.lead, a.count, a.cbits_v, N, mc.balanced != 0);
+    }
+    double2 x[P];
+    cc_stages<false, SC, 0, LOGC, NTHR, P>(x, sbuf, lay, stab, a.fft,
+                                           ZSrc{a.z, a.zt, N, a.ncols, col0, &a.mc, topu, topv},
+                                           F1SinkQ<RL>{a.out, a.ncols, col0, tw, qt}, tid);
+  }
 }
 
 template <class SC, int LOGC, int NTHR, int P>
@@ -850,15 +870,24 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1)) k_ilast_ct(ILastA
   double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   constexpr uint32_t c = 1u << LOGC, R = SC::R;
   const int tid = threadIdx.x;
-  const uint32_t col0 = blockIdx.x * c;
   double2* stab = sbuf + padded_len(R * c);
+  const uint32_t ntiles = a.g.ncols >> LOGC;
   pdl_trigger();
   for (uint32_t i = tid; i < a.fft.stablen; i += NTHR) stab[i] = __ldg(a.fft.stab + i);
   pdl_wait();
   const LayCols lay{uint32_t(LOGC), c - 1};
-  double2 x[P];
-  cc_stages<true, SC, 0, LOGC, NTHR, P>(x, sbuf, lay, stab, a.fft, ColSrc{a.data, a.g, 0, col0},
-                                     CoefSink{a.coef, a.g.ncols, col0}, tid);
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t col0 = tile * c;
+    const uint32_t nx = tile + gridDim.x;
+    if (nx < ntiles) {
+      // the next tile's row segments (c consecutive columns each) into L2
+      for (uint32_t e = tid; e < R; e += NTHR)
+        prefetch_l2(a.data + col_off(a.g, 0, e, nx * c), c * 16);
+    }
+    double2 x[P];
+    cc_stages<true, SC, 0, LOGC, NTHR, P>(x, sbuf, lay, stab, a.fft, ColSrc{a.data, a.g, 0, col0},
+                                          CoefSink{a.coef, a.g.ncols, col0}, tid);
+  }
 }
 
 // Compiled column shapes: {R, radices (maxrad 16 schedule), LOGC, NTHR}.
