@@ -248,8 +248,58 @@ __device__ __forceinline__ void dft16(double2* x) {
 }
 
 template <int R, bool INV>
+__device__ __forceinline__ void dft(double2* x);
+
+__host__ __device__ constexpr int inv_mod(int a, int m) {
+  int r = 1;
+  while ((a * r) % m != 1) ++r;
+  return r;
+}
+
+// Composite radix P = P1 P2 with gcd(P1, P2) = 1 by the prime-factor
+// (Good-Thomas) algorithm: input n = (n1 P2 + n2 P1) mod P, output
+// k = (k1 P2 t2 + k2 P1 t1) mod P with t2 = P2^-1 mod P1, t1 = P1^-1 mod P2,
+// so omega_P^{nk} = omega_P1^{n1 k1} omega_P2^{n2 k2}: P2 DFTs of length P1,
+// then P1 DFTs of length P2, with no twiddle multiplications in between (all
+// index maps are compile-time register renames).
+template <int P1, int P2, bool INV>
+__device__ __forceinline__ void dft_pfa(double2* x) {
+  constexpr int P = P1 * P2;
+  constexpr int t2 = inv_mod(P2 % P1, P1), t1 = inv_mod(P1 % P2, P2);
+  double2 y[P];
+#pragma unroll
+  for (int n2 = 0; n2 < P2; ++n2) {
+    double2 a[P1];
+#pragma unroll
+    for (int n1 = 0; n1 < P1; ++n1) a[n1] = x[(n1 * P2 + n2 * P1) % P];
+    dft<P1, INV>(a);
+#pragma unroll
+    for (int k1 = 0; k1 < P1; ++k1) y[n2 * P1 + k1] = a[k1];
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < P1; ++k1) {
+    double2 c[P2];
+#pragma unroll
+    for (int n2 = 0; n2 < P2; ++n2) c[n2] = y[n2 * P1 + k1];
+    dft<P2, INV>(c);
+#pragma unroll
+    for (int k2 = 0; k2 < P2; ++k2) x[(k1 * P2 * t2 + k2 * P1 * t1) % P] = c[k2];
+  }
+}
+
+template <int R, bool INV>
 __device__ __forceinline__ void dft(double2* x) {
-  if constexpr (R == 2) {
+  if constexpr (R == 6) {
+    dft_pfa<2, 3, INV>(x);
+  } else if constexpr (R == 10) {
+    dft_pfa<2, 5, INV>(x);
+  } else if constexpr (R == 12) {
+    dft_pfa<4, 3, INV>(x);
+  } else if constexpr (R == 14) {
+    dft_pfa<2, 7, INV>(x);
+  } else if constexpr (R == 15) {
+    dft_pfa<3, 5, INV>(x);
+  } else if constexpr (R == 2) {
     dft2<INV>(x[0], x[1]);
   } else if constexpr (R == 4) {
     dft4<INV>(x[0], x[1], x[2], x[3]);

@@ -895,8 +895,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1)) k_ilast_ct(ILastA
   {R_, LOGC_, NTHR_, MAXRAD_, {__VA_ARGS__}, k_f1_ct<Sched<__VA_ARGS__>, LOGC_, NTHR_, P_>, \
    k_ilast_ct<Sched<__VA_ARGS__>, LOGC_, NTHR_, P_>, ct_last_rad<Sched<__VA_ARGS__>>()}
 // (A radix-8, 1024-thread instantiation of 1792 = 8 x 8 x 4 x 7 measured
-// 86.6 / 47.7 us against 84.5 / 45.5 us for the 16 x 16 x 7 one.)
+// 86.6 / 47.7 us against 84.5 / 45.5 us for the 16 x 16 x 7 one; a
+// 560-thread one of 1400 equal at 96 registers.)  The first shape of a
+// length is the one used; the composite radices 10 and 12 (prime-factor
+// DFTs, dft.cuh) give three-stage schedules for 1728 = 12^3 and
+// 1440 = 12 x 12 x 10, one butterfly per thread and stage at 576 threads.
 static const ColCtShape kColCtShapes[] = {
+    TMG_COLCT(1728, 2, 576, 12, 0, 12, 12, 12),
+    TMG_COLCT(1440, 2, 576, 12, 0, 12, 12, 10),
     TMG_COLCT(1792, 2, 512, 16, 16, 16, 16, 7),
     TMG_COLCT(1400, 2, 512, 16, 16, 8, 5, 5, 7),
     TMG_COLCT(1792, 1, 256, 16, 16, 16, 16, 7),
@@ -904,19 +910,22 @@ static const ColCtShape kColCtShapes[] = {
 };
 #undef TMG_COLCT
 
-const ColCtShape* colct_shape(uint32_t R, int maxrad, const int32_t* rad, int nst) {
+const ColCtShape* colct_for(uint32_t R) {
   static const bool off = getenv("TMG_NO_COLCT") != nullptr;
   // TMG_COLCT_LOGC (testing): only shapes with this many columns per CTA
   static const int want_logc = getenv("TMG_COLCT_LOGC") ? atoi(getenv("TMG_COLCT_LOGC")) : -1;
   if (off) return nullptr;
-  for (const ColCtShape& sh : kColCtShapes) {
-    if (sh.R != R || sh.maxrad != maxrad || (want_logc >= 0 && sh.logc != want_logc)) continue;
-    bool ok = true;
-    int n = 0;
-    for (; n < 4 && sh.rad[n]; ++n) ok = ok && n < nst && sh.rad[n] == rad[n];
-    if (ok && n == nst) return &sh;
-  }
+  for (const ColCtShape& sh : kColCtShapes)
+    if (sh.R == R && (want_logc < 0 || sh.logc == want_logc)) return &sh;
   return nullptr;
+}
+
+int colct_stages(uint32_t R) {
+  const ColCtShape* sh = colct_for(R);
+  if (!sh) return 0;
+  int n = 0;
+  while (n < 4 && sh->rad[n]) ++n;
+  return n;
 }
 
 // ---------------------------------------------------------------------------

@@ -179,15 +179,17 @@ using ILastFn = void (*)(ILastArgs);
 struct ColCtShape {
   uint32_t R;
   int logc, nthr;
-  int maxrad;  // radix_schedule's largest power-of-two radix (16 or 8)
+  int maxrad;  // unused (0): schedules are explicit
   int rad[4];
   F1Fn f1;
   ILastFn ilast;
   uint32_t radl;  // radix of the last stage (F1 output twiddle table)
 };
-// The compiled shape for column length R with the given radix schedule, or
-// nullptr (TMG_NO_COLCT disables them).
-const ColCtShape* colct_shape(uint32_t R, int maxrad, const int32_t* rad, int nst);
+// The compiled shape for column length R, or nullptr (TMG_NO_COLCT disables
+// them); colct_stages(R) is its stage count (0 without one) for the
+// parameter policy's cost model.
+const ColCtShape* colct_for(uint32_t R);
+int colct_stages(uint32_t R);
 size_t colct_smem_bytes(uint32_t R, uint32_t c, uint32_t stablen, uint32_t radl);
 
 struct CarryArgs {

@@ -163,10 +163,14 @@ TwGlobal TwiddleCache::global(uint64_t L) {
 }
 
 const double2* TwiddleCache::stage_table(uint32_t R, int maxrad) {
-  const uint64_t key = (uint64_t(R) << 8) | uint64_t(maxrad);
+  return stage_table(R, radix_schedule(R, maxrad));
+}
+
+const double2* TwiddleCache::stage_table(uint32_t R, const std::vector<int>& rad) {
+  std::string key = std::to_string(R);
+  for (int r : rad) key += "," + std::to_string(r);
   auto it = stages_.find(key);
   if (it != stages_.end()) return it->second->as<double2>();
-  auto rad = radix_schedule(R, maxrad);
   std::vector<double2> h;
   uint32_t Ns = 1;
   for (size_t s = 0; s < rad.size(); ++s) {
@@ -192,12 +196,18 @@ const double2* TwiddleCache::stage_table(uint32_t R, int maxrad) {
 
 SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride, TwiddleCache* cache,
                    int maxrad) {
+  return make_subfft_rad(R, radix_schedule(R, maxrad), tw, tw_stride, cache);
+}
+
+// Sub-transform with an explicit radix schedule (compile-time column passes:
+// composite radices 10 and 12 that the runtime passes do not dispatch).
+SubFft make_subfft_rad(uint32_t R, const std::vector<int>& rad, const double2* tw,
+                       uint32_t tw_stride, TwiddleCache* cache) {
   SubFft s;
   std::memset(&s, 0, sizeof(s));
   s.R = R;
   s.tw = tw;
   s.twlen = R * tw_stride;
-  auto rad = radix_schedule(R, maxrad);
   s.nst = int32_t(rad.size());
   uint32_t Ns = 1, off = 0;
   for (size_t i = 0; i < rad.size(); ++i) {
@@ -211,7 +221,7 @@ SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride, TwiddleCac
     Ns *= uint32_t(rad[i]);
   }
   s.stablen = off > 0 ? off : 1;
-  s.stab = cache ? cache->stage_table(R, maxrad) : nullptr;
+  s.stab = cache ? cache->stage_table(R, rad) : nullptr;
   return s;
 }
 
@@ -500,11 +510,11 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   // schedule match a compiled shape (two-pass plans only).
   pl->colct = nullptr;
   if (pl->kind == 2) {
-    // TMG_COLCT_MAXRAD (testing): 8 selects radix-8 shapes, if compiled
-    static const int mr = getenv("TMG_COLCT_MAXRAD") ? atoi(getenv("TMG_COLCT_MAXRAD")) : 16;
-    SubFft f16 = make_subfft(A, tA, 1, &tw, mr);
-    const ColCtShape* sh = colct_shape(A, mr, f16.rad, f16.nst);
+    const ColCtShape* sh = colct_for(A);
     if (sh) {
+      std::vector<int> rad;
+      for (int i = 0; i < 4 && sh->rad[i]; ++i) rad.push_back(sh->rad[i]);
+      SubFft f16 = make_subfft_rad(A, rad, tA, 1, &tw);
       const uint32_t cc = 1u << sh->logc;
       const size_t sf = colct_smem_bytes(A, cc, f16.stablen, sh->radl);
       const size_t si = colct_smem_bytes(A, cc, f16.stablen, 0);

@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <map>
+#include <string>
 #include <memory>
 #include <vector>
 
@@ -31,8 +32,9 @@ class TwiddleCache {
   const double2* table(uint32_t R);               // omega_R^x, x < R
   TwGlobal global(uint64_t L);                    // two-level omega_L
   const double2* stage_table(uint32_t R, int maxrad = 16);  // per-stage q-major table
+  const double2* stage_table(uint32_t R, const std::vector<int>& rad);
  private:
-  std::map<uint64_t, std::unique_ptr<DevBuf>> stages_;
+  std::map<std::string, std::unique_ptr<DevBuf>> stages_;
   std::map<uint64_t, std::unique_ptr<DevBuf>> tables_;
   std::map<uint64_t, std::unique_ptr<DevBuf>> glob_;
   std::map<uint64_t, uint32_t> glob_S_;
@@ -40,6 +42,8 @@ class TwiddleCache {
 
 SubFft make_subfft(uint32_t R, const double2* tw, uint32_t tw_stride, TwiddleCache* cache,
                    int maxrad = 16);
+SubFft make_subfft_rad(uint32_t R, const std::vector<int>& rad, const double2* tw,
+                       uint32_t tw_stride, TwiddleCache* cache);
 MapConsts make_map_consts(const Params& p);
 
 struct Plan {
