@@ -86,24 +86,20 @@ __device__ __forceinline__ double2 cscale(double2 a, double s) {
 // Carry transfer functions.  A limb (or chunk) maps an incoming carry
 // c in {-1, 0, +1} to an outgoing carry f(c) in {-1, 0, +1}; composing these
 // maps is associative, which is what makes carry propagation a parallel
-// prefix.  Encoding: two bits per input, holding f(c)+1, for c = -1, 0, +1
-// at bit offsets 0, 2, 4.
+// prefix.  Encoding: one byte per input, holding f(c)+1, for c = -1, 0, +1
+// in bytes 0, 1, 2 -- so that composition is one byte permute.
 __host__ __device__ __forceinline__ uint32_t tf_const(int c) {
-  return uint32_t(c + 1) * 21u;  // 21 = 1 + 4 + 16
+  return uint32_t(c + 1) * 0x010101u;
 }
-constexpr uint32_t kTfIdentity = 0u | (1u << 2) | (2u << 4);
-// g o f: apply f first, then g.
+constexpr uint32_t kTfIdentity = 0x020100u;
+// g o f: apply f first, then g.  Byte c of the result is byte f(c)+1 of g:
+// PRMT with f's bytes as selector nibbles.
 __device__ __forceinline__ uint32_t tf_compose(uint32_t f, uint32_t g) {
-  uint32_t r = 0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    uint32_t fc = (f >> (2 * c)) & 3u;
-    r |= ((g >> (2 * fc)) & 3u) << (2 * c);
-  }
-  return r;
+  const uint32_t sel = (f & 0xFu) | ((f >> 4) & 0xF0u) | ((f >> 8) & 0xF00u);
+  return __byte_perm(g, 0u, sel) & 0xFFFFFFu;
 }
 __device__ __forceinline__ int tf_apply(uint32_t f, int c) {
-  return int((f >> (2 * (c + 1))) & 3u) - 1;
+  return int((f >> (8 * (c + 1))) & 0xFFu) - 1;
 }
 
 // Small fast divider for runtime-constant uint32 divisors (n < 2^31).

@@ -63,10 +63,18 @@ __device__ __forceinline__ void lane_of(const long long* __restrict__ se, int64_
   hi = 0;
   const int n = int(kb - ka);
   const long long* p = se + (ka - kbase);
-  uint32_t sh = uint32_t(ka * b - 64 * m);
-  for (int i = 0; i < n; ++i) {
-    add_shifted(lo, hi, p[i], sh);
-    sh += uint32_t(b);
+  uint32_t sh = uint32_t(ka) * uint32_t(b) - 64u * uint32_t(m);  // < 64 (mod 2^32 exact)
+  if (n <= 8) {
+    // at most ceil(64 / b) + 1 terms: unrolled and predicated (b >= 9)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i < n) add_shifted(lo, hi, p[i], sh + uint32_t(i * b));
+    }
+  } else {
+    for (int i = 0; i < n; ++i) {
+      add_shifted(lo, hi, p[i], sh);
+      sh += uint32_t(b);
+    }
   }
 }
 

@@ -248,7 +248,7 @@ __device__ __forceinline__ uint32_t limb_tf(__int128 s, uint32_t& flags) {
     flags |= kFlagCarryRange;
     fm = f0 = fp = 0;
   }
-  return uint32_t(fm + 1) | (uint32_t(f0 + 1) << 2) | (uint32_t(fp + 1) << 4);
+  return uint32_t(fm + 1) | (uint32_t(f0 + 1) << 8) | (uint32_t(fp + 1) << 16);
 }
 
 // High product range bookkeeping (products_f64.cpp:167-169): w must lie in
@@ -386,7 +386,7 @@ __device__ __forceinline__ int lookback_warp(unsigned long long* state,
       const uint32_t need = (first == 32) ? 0xffffffffu : ((1u << first) - 1u);
       if ((bv & need) != need) continue;  // a nearer predecessor is not ready
       // compose aggregates of lanes [0, first): f_0 o f_1 o ... o f_{first-1}
-      uint32_t f = (lane < first) ? uint32_t(w & 63u) : kTfIdentity;
+      uint32_t f = (lane < first) ? uint32_t(w & 0xFFFFFFu) : kTfIdentity;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         const uint32_t o = __shfl_down_sync(0xffffffffu, f, off);
@@ -395,7 +395,7 @@ __device__ __forceinline__ int lookback_warp(unsigned long long* state,
       f = __shfl_sync(0xffffffffu, f, 0);
       E = tf_compose(f, E);
       if (first < 32) {
-        const int v = int(__shfl_sync(0xffffffffu, uint32_t(w & 63u), first)) - 1;
+        const int v = int(__shfl_sync(0xffffffffu, uint32_t(w & 0xFFFFFFu), first)) - 1;
         carry_in = tf_apply(E, v);
         break;
       }
