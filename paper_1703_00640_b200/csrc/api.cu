@@ -442,8 +442,17 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       check_launch("k_ilast");
       ++kernels;
     }
+    // high: k_carry_apply finds the limb that stops the rounding increment
+    // (else k_high_agg does, after the single-pass k_carry)
+    bool high_stop_fused = false;
+    if (p.mode == PMode::kHigh && !w.hticket.p) {
+      w.hticket.ensure(64);
+      TMG_CUDA(cudaMemsetAsync(w.hticket.p, 0, 4, st));
+      TMG_CUDA(cudaMemsetAsync(w.hticket.as<uint32_t>() + 1, 0xff, 4, st));
+    }
     {
       CarryArgs a;
+      a.hstop = (p.mode == PMode::kHigh) ? w.hticket.as<uint32_t>() + 1 : nullptr;
       a.w = reinterpret_cast<const double*>(coef);
       a.out = out;
       a.n = p.n;
@@ -471,6 +480,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       const int pt = carry2_smem(int(p.b), lam, 4, hb) <= size_t(64) * 1024 ? 4 : 2;
       const size_t smem2 = carry2_smem(int(p.b), lam, pt, hb);
       if (!old_carry && smem2 <= kMaxDynSmem && 64 * pl.ML + 64 < (int64_t(1) << 32)) {
+        high_stop_fused = p.mode == PMode::kHigh;
         a.fb = make_fastdiv(uint32_t(p.b));
         const int64_t limbs = int64_t(kC2Threads) * pt;
         const unsigned blocks2 = unsigned((pl.ML + limbs - 1) / limbs);
@@ -517,30 +527,26 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.ML = pl.ML;
       a.shift_s = pl.shift_s;
       a.WL = pl.ML - (pl.shift_s >> 6);
-      const int64_t LB = kCarryThreads * kCarryPerThread;
+      const int64_t LB = kCarryThreads * kHighPerThread;
       const unsigned blocks = unsigned((a.WL + LB - 1) / LB);
       a.status = status;
       if (!w.ticket.p) {
         w.ticket.ensure(64);
         TMG_CUDA(cudaMemsetAsync(w.ticket.p, 0, 64, st));
       }
-      if (!w.hticket.p) {
-        w.hticket.ensure(64);
-        TMG_CUDA(cudaMemsetAsync(w.hticket.p, 0, 4, st));
-        TMG_CUDA(cudaMemsetAsync(w.hticket.as<uint32_t>() + 1, 0xff, 4, st));
-      }
       a.ticket = w.hticket.as<uint32_t>();
-      {
+      if (!high_stop_fused) {
         KTimer kt(cx, "k_high_agg", double(pl.ML) * 8.0, int(p.mode), st);
         launch(k_high_agg, dim3(blocks), dim3(kCarryThreads), 0, st, a, "hagg");
+        check_launch("k_high_agg");
+        ++kernels;
       }
-      check_launch("k_high_agg");
       {
         KTimer kt(cx, "k_high_round", double(pl.ML) * 8.0 + double(pl.out_limbs) * 8.0, int(p.mode), st);
         launch(k_high_round, dim3(blocks), dim3(kCarryThreads), 0, st, a, "hround");
       }
       check_launch("k_high_round");
-      kernels += 2;
+      ++kernels;
     }
   }
   return kernels;

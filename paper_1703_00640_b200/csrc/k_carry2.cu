@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
   pdl_wait();
   constexpr int64_t kLimbs = int64_t(kT) * kPT;
   __shared__ uint32_t sw[32];
-  __shared__ uint32_t s_flags, s_low;
+  __shared__ uint32_t s_flags, s_low, s_hmin;
   const int tid = threadIdx.x;
   const MapConsts& mc = a.mc;
   const int64_t blk = blockIdx.x;
@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
   if (tid == 0) {
     s_flags = 0;
     s_low = 0;
+    s_hmin = 0xffffffffu;
   }
   const int cin = __ldg(a.cins + blk);  // carry into the block (k_carry_lanes)
   // limbs of this thread
@@ -380,6 +381,14 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
   const int64_t OL = a.out_limbs;
   const int64_t sb = a.shift_s - 1;  // high: bit s-1
   uint32_t sticky = 0;
+  // high: the first limb j of w0 = t >> s that is not all ones stops the
+  // rounding increment (k_high_round).  Limb m of t feeds w0_{m-q} (bits
+  // r..63) and w0_{m-q-1} (bits 0..r-1), q = s / 64, r = s % 64, so each
+  // limb nominates the w0 limbs its bits prove not all ones.
+  const int64_t hq = int64_t(a.shift_s) >> 6;
+  const int hr = int(a.shift_s & 63);
+  const int64_t WL = a.ML - hq;
+  uint32_t hmin = 0xffffffffu;
 #pragma unroll
   for (int q = 0; q < kPT; ++q) {
     const int64_t m = m0 + q;
@@ -399,6 +408,14 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
         if (m < OL) a.out[m] = (m == OL - 1 && (a.n & 63)) ? (x & ((1ull << (a.n & 63)) - 1)) : x;
       } else {
         a.tbuf[m] = x;
+        if (hr == 0) {
+          if (x != ~0ull && m - hq >= 0) hmin = min(hmin, uint32_t(m - hq));
+        } else {
+          const uint64_t lowm = (1ull << hr) - 1;
+          if ((x >> hr) != (~0ull >> hr) && m - hq >= 0) hmin = min(hmin, uint32_t(m - hq));
+          if ((x & lowm) != lowm && m - hq - 1 >= 0 && m - hq - 1 < WL)
+            hmin = min(hmin, uint32_t(m - hq - 1));
+        }
         const int64_t bit0 = 64 * m;
         if (bit0 + 64 <= sb) {
           if (x) sticky = 1;
@@ -415,10 +432,18 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
   }
   if (sticky) atomicOr(&s_low, 1u);
   if (flags) atomicOr(&s_flags, flags);
+  if (mc.mode == kModeHigh) {
+    // w0's top limb has zero fill above bit 64 - r: never all ones
+    if (hr != 0 && blk == 0 && tid == 0 && WL > 0) hmin = min(hmin, uint32_t(WL - 1));
+    hmin = __reduce_min_sync(0xffffffffu, hmin);
+    if ((tid & 31) == 0 && hmin != 0xffffffffu) atomicMin(&s_hmin, hmin);
+  }
   __syncthreads();
   if (tid == 0) {
     if (s_flags) atomicOr(&a.status->flags, s_flags);
     if (s_low) atomicOr(&a.status->high_sticky, 1u);
+    // one global update per block
+    if (mc.mode == kModeHigh && s_hmin != 0xffffffffu) atomicMin(a.hstop, s_hmin);
   }
 }
 

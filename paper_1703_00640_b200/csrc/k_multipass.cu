@@ -1125,35 +1125,31 @@ __device__ __forceinline__ uint64_t high_shifted(const HighRoundArgs& a, int64_t
   return r ? ((lo >> r) | (hi << (64 - r))) : lo;
 }
 
-// Per-block transfer function of the increment chain of k_high_round: an
-// increment passes a limb of t >> s only if the limb is all ones.
+// The first limb of w0 = t >> s that is not all ones (atomicMin into
+// ticket[1]): the limb that stops the rounding increment.  The two-kernel
+// carry path computes it in k_carry_apply; this kernel serves the
+// single-pass k_carry path.
 __global__ void __launch_bounds__(kCarryThreads)
 k_high_agg(HighRoundArgs a) {
   pdl_trigger();
   pdl_wait();
-  __shared__ uint32_t s_all;
-  const int tid = threadIdx.x;
-  if (tid == 0) s_all = 1;
-  __syncthreads();
-  constexpr int LB = kCarryThreads * kCarryPerThread;
+  constexpr int LB = kCarryThreads * kHighPerThread;
   const int64_t ms = int64_t(blockIdx.x) * LB;
   const int64_t me = min(a.WL, ms + LB);
-  bool all = true;
-  for (int64_t m = ms + tid; m < me; m += kCarryThreads) all &= high_shifted(a, m) == ~0ull;
-  if (!__all_sync(0xffffffffu, all) && (tid & 31) == 0) s_all = 0;
-  __syncthreads();
-  // the increment passes a block only if all its limbs are ones: the first
-  // block that stops it is all k_high_round needs
-  if (tid == 0 && !s_all) atomicMin(a.ticket + 1, uint32_t(blockIdx.x));
+  uint32_t first = 0xffffffffu;
+  for (int64_t m = ms + threadIdx.x; m < me; m += kCarryThreads)
+    if (high_shifted(a, m) != ~0ull) first = min(first, uint32_t(m));
+  first = __reduce_min_sync(0xffffffffu, first);
+  if ((threadIdx.x & 31) == 0 && first != 0xffffffffu) atomicMin(a.ticket + 1, first);
 }
 
+// w = w0 + inc: the increment enters limb 0 and carries through the all-ones
+// limbs below the first stopping limb f (k_high_agg / k_carry_apply), so
+// limb j adds inc exactly when j <= f.
 __global__ void __launch_bounds__(kCarryThreads)
 k_high_round(HighRoundArgs a) {
   pdl_trigger();
   pdl_wait();
-  __shared__ uint32_t sw[32];
-  __shared__ uint32_t s_blk;
-  __shared__ int s_cin;
   __shared__ uint32_t s_flags, s_top, s_low;
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -1161,6 +1157,7 @@ k_high_round(HighRoundArgs a) {
     s_top = 0;
     s_low = 0;
   }
+  __syncthreads();
   const uint32_t blk = blockIdx.x;
   const int64_t s = a.shift_s;
   const int64_t q = s >> 6;
@@ -1169,37 +1166,27 @@ k_high_round(HighRoundArgs a) {
   auto tl = [&](int64_t m) -> uint64_t { return m < a.ML ? t[m] : 0ull; };
   const int inc = int((tl((s - 1) >> 6) >> ((s - 1) & 63)) & 1) &
                   int(a.status->high_sticky != 0 || ((tl(s >> 6) >> (s & 63)) & 1));
-  constexpr int LB = kCarryThreads * kCarryPerThread;
+  const uint32_t first = __ldcg(a.ticket + 1);
+  constexpr int LB = kCarryThreads * kHighPerThread;
   const int64_t ms = int64_t(blk) * LB;
   const int64_t me = min(a.WL, ms + LB);
-  const int64_t m0 = ms + int64_t(tid) * kCarryPerThread;
-  const int64_t m1 = min(me, m0 + kCarryPerThread);
-  uint64_t w0[kCarryPerThread];
-  uint32_t f = kTfIdentity;
-#pragma unroll
-  for (int i = 0; i < kCarryPerThread; ++i) {
-    const int64_t m = m0 + i;
-    if (m < m1) {
-      uint64_t lo = tl(m + q), hi = tl(m + q + 1);
-      w0[i] = r ? ((lo >> r) | (hi << (64 - r))) : lo;
-      f = tf_compose(f, w0[i] == ~0ull ? kTfIdentity : tf_const(0));
-    }
-  }
-  uint32_t agg;
-  const uint32_t ex = block_scan_tf(f, sw, &agg);
-  // increment into this block: inc unless an earlier block has a limb of
-  // t >> s that is not all ones (first such block from k_high_agg)
-  if (tid == 0) s_cin = (__ldcg(a.ticket + 1) >= blk) ? inc : 0;
-  __syncthreads();
-  int c = tf_apply(ex, s_cin);
+  const int64_t m0 = ms + int64_t(tid) * kHighPerThread;
+  const int64_t m1 = min(me, m0 + kHighPerThread);
   uint32_t flags = 0, topbit = 0, lownz = 0;
   const int64_t OL = a.out_limbs;
+  // the thread's kHighPerThread + 1 limbs of t, loaded together
+  uint64_t tv[kHighPerThread + 1];
 #pragma unroll
-  for (int i = 0; i < kCarryPerThread; ++i) {
+  for (int i = 0; i <= kHighPerThread; ++i) tv[i] = (m0 + i <= m1) ? tl(m0 + i + q) : 0ull;
+#pragma unroll
+  for (int i = 0; i < kHighPerThread; ++i) {
     const int64_t m = m0 + i;
     if (m < m1) {
-      const uint64_t x = w0[i] + uint64_t(c);
-      c = (c && w0[i] == ~0ull) ? 1 : 0;
+      const uint64_t lo = tv[i], hi = tv[i + 1];
+      const uint64_t w0 = r ? ((lo >> r) | (hi << (64 - r))) : lo;
+      const uint64_t x = w0 + uint64_t((inc && uint64_t(m) <= uint64_t(first)) ? 1 : 0);
+      // the increment carried out of the top examined limb: w > 2^n
+      if (inc && m == a.WL - 1 && uint64_t(first) >= uint64_t(a.WL)) flags |= kFlagHighRange;
       high_classify(x, m, a.n, topbit, lownz, flags);
       if (m < OL) a.out[m] = x & high_mask(m, OL, a.n);
     }
@@ -1222,7 +1209,7 @@ k_high_round(HighRoundArgs a) {
       st->high_topbit = 0;
       st->high_lownz = 0;
       st->high_sticky = 0;
-      a.ticket[1] = 0xffffffffu;  // first-stop block, for the next product
+      a.ticket[1] = 0xffffffffu;  // first stopping limb, for the next product
       *a.ticket = 0;
     }
   }

@@ -211,6 +211,7 @@ struct CarryArgs {
   int* cins;        // per-block carry-in (written by the last lanes block)
   uint32_t* ticket; // completion counter of k_carry_lanes (zero between launches)
   FastDiv fb;       // division by b
+  uint32_t* hstop;  // high: first limb of t >> s that is not all ones (atomicMin; ~0 before)
 };
 constexpr int kCarryThreads = 256;
 constexpr int kCarryPerThread = 2;
@@ -232,8 +233,10 @@ struct HighRoundArgs {
   int32_t shift_s;
   DevStatus* status;
   uint32_t* ticket;  // [0] completion counter (zero between launches),
-                     // [1] first block stopping the increment (~0 between launches)
+                     // [1] first limb of t >> s that is not all ones, i.e. the
+                     //     limb that stops the rounding increment (~0 between launches)
 };
+constexpr int kHighPerThread = 8;  // limbs of w per thread in k_high_agg / k_high_round
 __global__ void k_high_agg(HighRoundArgs a);
 __global__ void k_status_publish(const DevStatus* src, uint32_t* flag_out, DevStatus* merge);
 __global__ void k_high_round(HighRoundArgs a);
