@@ -70,12 +70,17 @@ __device__ __forceinline__ typename StagedBits<W32>::Word load_word(const uint64
 __host__ __device__ inline int64_t zgen_words(int b, int kw) {
   return (int64_t(kZgenChunks + kMaxLambda) * b + kw - 1) / kw + 3;
 }
+// staged words reserved per operand: the 16-byte loads of interior blocks
+// start up to 3 words early and round up to a multiple of 4
+__host__ __device__ inline int64_t zgen_words_alloc(int b, int kw) {
+  return (zgen_words(b, kw) + 8 + 3) / 4 * 4;  // keeps the second operand 16-byte aligned
+}
 
 }  // namespace
 
 size_t zgen_smem(int b) {
   const int kw = b <= 32 ? 32 : 64;
-  return 2 * size_t(zgen_words(b, kw)) * (kw / 8) +
+  return 2 * size_t(zgen_words_alloc(b, kw)) * (kw / 8) +
          size_t((kZgenChunks + kMaxLambda) * 17 / 16 + 2) * 8 + 64;
 }
 
@@ -146,19 +151,45 @@ k_zgen_t(ZgenArgs a) {
   constexpr int ext = lam - 1;
   const int64_t nwd = zgen_words(b, SB::kW);
   Word* su = reinterpret_cast<Word*>(smem_raw);
-  Word* sv = su + nwd;
+  Word* sv = su + zgen_words_alloc(b, SB::kW);
   // digits of the block's chunks (and the next lam-1), u and v packed
-  int2* dig = reinterpret_cast<int2*>(sv + nwd);
+  int2* dig = reinterpret_cast<int2*>(sv + zgen_words_alloc(b, SB::kW));
 
   const uint32_t blk = blockIdx.x;
   const int64_t c0 = int64_t(blk) * kZgenChunks;
   const int64_t c1 = min(count, c0 + int64_t(kZgenChunks));
   const int64_t bit0 = c0 * b - a.lead;
-  const int64_t wbase = bit0 >> SB::kLog;  // floor, bit0 may be negative
-  const uint32_t off0 = uint32_t(bit0 - (wbase << SB::kLog));
-  for (int64_t i = tid; i < nwd; i += kZgenThreads) {
-    su[i] = load_word<W32>(a.u, a.nlimbs, wbase + i);
-    sv[i] = load_word<W32>(a.v, a.nlimbs, wbase + i);
+  int64_t wbase = bit0 >> SB::kLog;  // floor, bit0 may be negative
+  uint32_t off0 = uint32_t(bit0 - (wbase << SB::kLog));
+  // Interior blocks (block-uniform): every chunk in [c0, c1 + lam - 1] is a
+  // full balanced non-top chunk, its bits lie inside both operands, and
+  // b <= 30 -- no per-chunk bound or top tests, 32-bit digit arithmetic and
+  // 16-byte staging loads.
+  bool interior = false;
+  if constexpr (W32) {
+    const int64_t w4 = wbase & ~int64_t(3);
+    interior = mc.balanced && b <= 30 && c1 == c0 + kZgenChunks && c1 + ext < count - 1 &&
+               w4 >= 0 && w4 + 4 * ((nwd + 6) / 4) <= 2 * a.nlimbs &&
+               ((reinterpret_cast<uintptr_t>(a.u) | reinterpret_cast<uintptr_t>(a.v)) & 15) == 0;
+    if (interior) {
+      off0 += uint32_t(wbase - w4) * 32u;
+      wbase = w4;
+      const uint4* gu4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.u) + wbase);
+      const uint4* gv4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.v) + wbase);
+      uint4* su4 = reinterpret_cast<uint4*>(su);
+      uint4* sv4 = reinterpret_cast<uint4*>(sv);
+      const int64_t n4 = (nwd + 6) / 4;
+      for (int64_t i = tid; i < n4; i += kZgenThreads) {
+        su4[i] = __ldg(gu4 + i);
+        sv4[i] = __ldg(gv4 + i);
+      }
+    }
+  }
+  if (!interior) {
+    for (int64_t i = tid; i < nwd; i += kZgenThreads) {
+      su[i] = load_word<W32>(a.u, a.nlimbs, wbase + i);
+      sv[i] = load_word<W32>(a.v, a.nlimbs, wbase + i);
+    }
   }
   __syncthreads();
   const SB Lu{su}, Lv{sv};
@@ -177,7 +208,15 @@ k_zgen_t(ZgenArgs a) {
     wv[q] = Win(Lv.window(rel, mask));
   }
   uint32_t gu = 0, pu = 0, gv = 0, pv = 0;
-  if (mc.balanced) {
+  if (interior) {
+#pragma unroll
+    for (int q = 0; q < kZgenPer; ++q) {
+      gu |= uint32_t(wu[q] > half) << q;
+      pu |= uint32_t(wu[q] == half) << q;
+      gv |= uint32_t(wv[q] > half) << q;
+      pv |= uint32_t(wv[q] == half) << q;
+    }
+  } else if (mc.balanced) {
 #pragma unroll
     for (int q = 0; q < kZgenPer; ++q) {
       const int64_t j = t0 + q;
@@ -215,6 +254,20 @@ k_zgen_t(ZgenArgs a) {
 
   // digits and carry-in bits
   uint32_t bu = 0, bv = 0;
+  if (interior) {
+    const int32_t hb = int32_t(half), full = int32_t(1) << b;
+#pragma unroll
+    for (int q = 0; q < kZgenPer; ++q) {
+      bu |= uint32_t(cu) << q;
+      bv |= uint32_t(cv) << q;
+      int32_t xu = int32_t(wu[q]) + cu, xv = int32_t(wv[q]) + cv;
+      xu -= (xu > hb) ? full : 0;
+      xv -= (xv > hb) ? full : 0;
+      dig[zpad(q0 + q)] = make_int2(xu, xv);
+      if (!((pu >> q) & 1u)) cu = int((gu >> q) & 1u);
+      if (!((pv >> q) & 1u)) cv = int((gv >> q) & 1u);
+    }
+  } else {
 #pragma unroll
   for (int q = 0; q < kZgenPer; ++q) {
     const int64_t j = t0 + q;
@@ -227,6 +280,7 @@ k_zgen_t(ZgenArgs a) {
       if (!((pu >> q) & 1u)) cu = int((gu >> q) & 1u);
       if (!((pv >> q) & 1u)) cv = int((gv >> q) & 1u);
     }
+  }
   }
   // the next block's first lam-1 digits (carry out of this block known)
   if (t0 < c1 && t0 + kZgenPer >= c1) {
@@ -277,9 +331,23 @@ k_zgen_t(ZgenArgs a) {
 
   // outputs
   if constexpr (LAM == 0) {
-    for (int32_t jl = tid; jl < nloc; jl += kZgenThreads) {
-      const int2 d = dig[zpad(jl)];
-      a.z[a.zt.index(uint32_t(c0 + jl))] = make_double2(double(d.x), double(d.y));
+    const ZTile& zt = a.zt;
+    const uint32_t row0 = zt.natural ? 0u : fdiv(uint32_t(c0), zt.fdcols);
+    const uint32_t col0 = uint32_t(c0) - row0 * zt.fdcols.d;
+    if (!zt.natural && col0 + uint32_t(nloc) <= zt.fdcols.d) {
+      // the block's chunks lie in one row of the column tiles: index by column
+      const uint32_t cm = (1u << zt.logc) - 1;
+      for (int32_t jl = tid; jl < nloc; jl += kZgenThreads) {
+        const int2 d = dig[zpad(jl)];
+        const uint32_t col = col0 + uint32_t(jl);
+        a.z[((col >> zt.logc) * zt.zrows + row0) * (cm + 1) + (col & cm)] =
+            make_double2(double(d.x), double(d.y));
+      }
+    } else {
+      for (int32_t jl = tid; jl < nloc; jl += kZgenThreads) {
+        const int2 d = dig[zpad(jl)];
+        a.z[zt.index(uint32_t(c0 + jl))] = make_double2(double(d.x), double(d.y));
+      }
     }
   } else {
     const double Nd = double(N);
@@ -294,6 +362,11 @@ k_zgen_t(ZgenArgs a) {
       // the exact integer factors are formed once per output and the products
       // run in coef_rt's order (bit-identical); digits convert on the FP64 pipe.
       const double sgN = low ? -Nd : Nd;
+      const ZTile& zt = a.zt;
+      const uint32_t row0 = zt.natural ? 0u : fdiv(uint32_t(c0), zt.fdcols);
+      const uint32_t col0 = uint32_t(c0) - row0 * zt.fdcols.d;
+      const bool onerow = !zt.natural && col0 + uint32_t(nloc + ext) <= 2 * zt.fdcols.d;
+      const uint32_t cm = (1u << zt.logc) - 1;
       for (int32_t jl = ext + tid; jl < nloc + ext; jl += kZgenThreads) {
         const double jd = double(c0 + jl);
         double g[LAM > 1 ? LAM - 1 : 1];
@@ -313,7 +386,17 @@ k_zgen_t(ZgenArgs a) {
           au += i2d_exact(d.x) * cf;
           av += i2d_exact(d.y) * cf;
         }
-        a.z[a.zt.index(uint32_t(c0 + jl))] = make_double2(au, av);
+        if (onerow) {
+          // z index without a division: the block spans at most two rows
+          uint32_t col = col0 + uint32_t(jl), row = row0;
+          if (col >= zt.fdcols.d) {
+            col -= zt.fdcols.d;
+            ++row;
+          }
+          a.z[((col >> zt.logc) * zt.zrows + row) * (cm + 1) + (col & cm)] = make_double2(au, av);
+        } else {
+          a.z[zt.index(uint32_t(c0 + jl))] = make_double2(au, av);
+        }
       }
       return;
     }
