@@ -570,31 +570,46 @@ __device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restr
     const uint32_t xq = 2u * (it ? r1 : r0) * NSL * q;
     qt[tid] = xq ? a.tw.get(xq) : make_double2(1.0, 0.0);
   }
-  // spectral product over the pair (see k_mid)
-  const uint32_t brw = (r0 != 0) ? 1u : 0u;
-#pragma unroll 2
-  for (uint32_t k = tid; k < C; k += NTHR) {
-    const uint32_t kp = (C - k - brw) & (C - 1);
-    const uint32_t ip = (nrows == 2) ? 1u : 0u;
-    if (nrows == 1 && kp < k) continue;
-    const double2 z1 = sbuf[lay.idx(0, k)], z2 = sbuf[lay.idx(ip, kp)];
+  // spectral product over the pair (see k_mid) fused with the half-length
+  // repack.  For a pair of distinct rows the partner of row 0's index k is
+  // row 1's C-1-k, so one thread reads Z0_k, Z0_{k+H}, Z1_{C-1-k}, Z1_{H-1-k},
+  // forms W0_k, W0_{k+H} (and W1 = conj W0 at the partner indices) and
+  // writes Y0_k and Y1_{H-1-k}: the four slots it reads are read by no other
+  // thread, so the step is in place with one barrier (same arithmetic as the
+  // two-pass form).  The self-paired rows 0 and AB/2 take the two passes.
+  auto spec = [&](double2 z1, double2 z2) {
     const double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
     const double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
     const double2 pq = cmul(p, q);
-    const double2 w = make_double2(mul_hl(pq.y, a.scale, a.scale_lo),
-                                   -mul_hl(pq.x, a.scale, a.scale_lo));
-    sbuf[lay.idx(0, k)] = w;
-    if (!(nrows == 1 && kp == k)) sbuf[lay.idx(ip, kp)] = cconj(w);
-  }
-  __syncthreads();
-#pragma unroll 2
-  for (uint32_t e = tid; e < nrows * H; e += NTHR) {
-    const uint32_t i = e >= H ? 1 : 0, k = e - i * H;
-    const uint32_t r = i ? r1 : r0;
-    const double2 w1 = sbuf[lay.idx(i, k)], w2 = sbuf[lay.idx(i, k + H)];
+    return make_double2(mul_hl(pq.y, a.scale, a.scale_lo), -mul_hl(pq.x, a.scale, a.scale_lo));
+  };
+  auto repack = [&](double2 w1, double2 w2, uint32_t r, uint32_t k) {
     const double2 ev = cadd(w1, w2);
     const double2 o = cmulc(csub(w1, w2), a.tw.get(r + AB * k));
-    sbuf[lay.idx(i, k)] = make_double2(ev.x - o.y, ev.y + o.x);
+    return make_double2(ev.x - o.y, ev.y + o.x);
+  };
+  if (nrows == 2) {
+#pragma unroll 2
+    for (uint32_t k = tid; k < H; k += NTHR) {
+      const uint32_t kq = H - 1 - k;
+      const double2 a0 = sbuf[lay.idx(0, k)], a1 = sbuf[lay.idx(0, k + H)];
+      const double2 b0 = sbuf[lay.idx(1, C - 1 - k)], b1 = sbuf[lay.idx(1, kq)];
+      const double2 wk = spec(a0, b0), wkh = spec(a1, b1);
+      sbuf[lay.idx(0, k)] = repack(wk, wkh, r0, k);
+      sbuf[lay.idx(1, kq)] = repack(cconj(wkh), cconj(wk), r1, kq);
+    }
+  } else {
+    const uint32_t brw = (r0 != 0) ? 1u : 0u;
+    for (uint32_t k = tid; k < C; k += NTHR) {
+      const uint32_t kp = (C - k - brw) & (C - 1);
+      if (kp < k) continue;
+      const double2 w = spec(sbuf[lay.idx(0, k)], sbuf[lay.idx(0, kp)]);
+      sbuf[lay.idx(0, k)] = w;
+      if (kp != k) sbuf[lay.idx(0, kp)] = cconj(w);
+    }
+    __syncthreads();
+    for (uint32_t k = tid; k < H; k += NTHR)
+      sbuf[lay.idx(0, k)] = repack(sbuf[lay.idx(0, k)], sbuf[lay.idx(0, k + H)], r0, k);
   }
   __syncthreads();
   ct_stages<true, Inv, 0, NTHR>(x, sbuf, lay, stab, a.inv, SmemSrc<RowPair>{sbuf, lay},
