@@ -549,7 +549,8 @@ k_mid(MidArgs a) {
 template <int NTHR, class Fwd, class Inv>
 __device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restrict__ sbuf,
                                               const double2* __restrict__ stab,
-                                              double2* __restrict__ qt, uint32_t r0, int tid) {
+                                              double2* __restrict__ qt, uint32_t r0, int tid,
+                                              double2 wc0, double2 wc1) {
   constexpr uint32_t C = 4096, H = 2048;
   const uint32_t AB = a.A * a.B;
   const uint32_t r1 = (AB - r0) % AB;
@@ -583,20 +584,34 @@ __device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restr
     const double2 pq = cmul(p, q);
     return make_double2(mul_hl(pq.y, a.scale, a.scale_lo), -mul_hl(pq.x, a.scale, a.scale_lo));
   };
-  auto repack = [&](double2 w1, double2 w2, uint32_t r, uint32_t k) {
+  auto repack_w = [&](double2 w1, double2 w2, double2 t) {
     const double2 ev = cadd(w1, w2);
-    const double2 o = cmulc(csub(w1, w2), a.tw.get(r + AB * k));
+    const double2 o = cmulc(csub(w1, w2), t);
     return make_double2(ev.x - o.y, ev.y + o.x);
   };
+  auto repack = [&](double2 w1, double2 w2, uint32_t r, uint32_t k) {
+    return repack_w(w1, w2, a.tw.get(r + AB * k));
+  };
   if (nrows == 2) {
-#pragma unroll 2
-    for (uint32_t k = tid; k < H; k += NTHR) {
+    // repack twiddles omega_L^{r + AB k} = omega_L^r omega_C^k: with k = tid +
+    // NTHR s and NTHR = C / 8, omega_C^k = omega_C^tid omega_8^s (row 0), and
+    // row 1's k = H-1-tid-NTHR s gives omega_C^{H-1-tid} omega_8^-s; the
+    // per-thread omega_C factors are fetched once per CTA (wc0, wc1)
+    static_assert(NTHR * 8 == C && H % NTHR == 0, "repack twiddle layout");
+    const double2 t0 = cmul(a.tw.get(r0), wc0), t1 = cmul(a.tw.get(r1), wc1);
+#pragma unroll
+    for (int si = 0; si < int(H / NTHR); ++si) {
+      const uint32_t k = uint32_t(tid) + NTHR * uint32_t(si);
       const uint32_t kq = H - 1 - k;
       const double2 a0 = sbuf[lay.idx(0, k)], a1 = sbuf[lay.idx(0, k + H)];
       const double2 b0 = sbuf[lay.idx(1, C - 1 - k)], b1 = sbuf[lay.idx(1, kq)];
       const double2 wk = spec(a0, b0), wkh = spec(a1, b1);
-      sbuf[lay.idx(0, k)] = repack(wk, wkh, r0, k);
-      sbuf[lay.idx(1, kq)] = repack(cconj(wkh), cconj(wk), r1, kq);
+      const double2 tk = si == 0 ? t0 : si == 1 ? w8_1<false>(t0) : si == 2 ? mul_mi<false>(t0)
+                                                                            : w8_3<false>(t0);
+      const double2 tq = si == 0 ? t1 : si == 1 ? w8_1<true>(t1) : si == 2 ? mul_mi<true>(t1)
+                                                                           : w8_3<true>(t1);
+      sbuf[lay.idx(0, k)] = repack_w(wk, wkh, tk);
+      sbuf[lay.idx(1, kq)] = repack_w(cconj(wkh), cconj(wk), tq);
     }
   } else {
     const uint32_t brw = (r0 != 0) ? 1u : 0u;
@@ -631,6 +646,9 @@ __device__ __forceinline__ void mid_4096_body(const MidArgs& a) {
   auto row_base = [&](uint32_t r) {
     return a.data + (int64_t(r % a.A) * a.B + (r / a.A)) * int64_t(C);
   };
+  // this thread's omega_C^tid and omega_C^{H-1-tid} (repack twiddles)
+  const double2 wc0 = tid ? a.tw.get(AB * uint32_t(tid)) : make_double2(1.0, 0.0);
+  const double2 wc1 = a.tw.get(AB * (C / 2 - 1 - uint32_t(tid)));
   if (tid == 0 && blockIdx.x < npairs) {
     prefetch_l2(row_base(blockIdx.x), C * 16);
     prefetch_l2(row_base((AB - blockIdx.x) % AB), C * 16);
@@ -642,7 +660,7 @@ __device__ __forceinline__ void mid_4096_body(const MidArgs& a) {
       prefetch_l2(row_base(nx), C * 16);
       prefetch_l2(row_base((AB - nx) % AB), C * 16);
     }
-    mid_pair_4096<NTHR, Fwd, Inv>(a, sbuf, stw, stw + C, r0, tid);
+    mid_pair_4096<NTHR, Fwd, Inv>(a, sbuf, stw, stw + C, r0, tid, wc0, wc1);
   }
 }
 
