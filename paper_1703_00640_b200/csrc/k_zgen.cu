@@ -92,12 +92,18 @@ size_t zgen_smem(int b) {
 // random operands; the whole block only when every window equals 2^{b-1}).
 __global__ void __launch_bounds__(256)
 k_zstat(ZgenArgs a) {
+  // Reads only the operands and writes only its own aggregate array, so it
+  // runs under the predecessor's tail and waits for it at the end instead:
+  // its completion still implies the predecessor's, which keeps the
+  // programmatic-launch chain intact for k_zgen and everything after it.
   pdl_trigger();
-  pdl_wait();
   const int64_t blk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t count = a.count;
   const int64_t nblk = (count + kZgenChunks - 1) / kZgenChunks;
-  if (blk >= nblk) return;
+  if (blk >= nblk) {
+    pdl_wait();
+    return;
+  }
   const int b = a.b;
   const uint64_t half = 1ull << (b - 1);
   const int64_t c0 = blk * kZgenChunks;
@@ -127,6 +133,7 @@ k_zstat(ZgenArgs a) {
     fu = fv = 0;
   }
   a.aggs[blk] = fu | (fv << 2);
+  pdl_wait();
 }
 
 // LAM: the series length lambda (rows of the pre-map), 0 for the full
