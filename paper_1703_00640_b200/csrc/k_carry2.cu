@@ -297,11 +297,7 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
   if (tid == 0) a.aggs[blk] = agg;
   flags |= ra.flags;
   {
-    double e = ra.max_err, m = ra.max_abs;
-    for (int off = 16; off > 0; off >>= 1) {
-      e = fmax(e, __shfl_xor_sync(0xffffffffu, e, off));
-      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-    }
+    const double e = warp_max_nonneg(ra.max_err), m = warp_max_nonneg(ra.max_abs);
     if ((tid & 31) == 0) s_red[tid >> 5] = make_double2(e, m);
   }
   if (flags) atomicOr(&s_flags, flags);

@@ -230,11 +230,7 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
   flags |= ra.flags;
   // block max of errors
   {
-    double e = ra.max_err, m = ra.max_abs;
-    for (int off = 16; off > 0; off >>= 1) {
-      e = fmax(e, __shfl_xor_sync(0xffffffffu, e, off));
-      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-    }
+    const double e = warp_max_nonneg(ra.max_err), m = warp_max_nonneg(ra.max_abs);
     if ((tid & 31) == 0) status_merge(a.status, e, m, 0);
   }
   __syncthreads();

@@ -210,6 +210,16 @@ struct RoundAcc {
   }
 };
 
+// Warp maximum of a non-negative double, exact, with two REDUX: the high
+// words first, then the low words of the lanes that hold the maximal high word.
+__device__ __forceinline__ double warp_max_nonneg(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  const uint32_t hi = uint32_t(b >> 32), lo = uint32_t(b);
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+}
+
 __device__ __forceinline__ void status_merge(DevStatus* st, double max_err,
                                              double max_abs, uint32_t flags) {
   atomicMax(&st->max_err_bits, (unsigned long long)__double_as_longlong(max_err));
