@@ -62,9 +62,28 @@ def _traffic(kernel):
         return None, None
 
 
+_SAMPLER_CODE = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+print("ready", mx, flush=True)
+while True:
+    try:
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        print(sm, rs, flush=True)
+    except Exception as e:  # noqa: BLE001
+        print("err", repr(e), flush=True)
+    time.sleep(0.001)
+"""
+
+
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled through NVML every
-    few milliseconds while the timed region runs."""
+    millisecond while the timed region runs, in a separate process (the
+    benchmark's own host thread keeps the interpreter busy enqueueing)."""
 
     REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
                ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
@@ -73,53 +92,44 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-        self._nv = None
+        self.proc = None
+        self.max = None
         self.errors = []
 
-    def _run(self):
-        nv, h, mx = self._nv, self._h, self._mx
-        while not self._stop.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, mx, rs, 1))
-            except Exception as e:  # noqa: BLE001 - recorded, not fatal
-                self.errors.append(repr(e))
-            self._stop.wait(0.001)
-
     def start(self):
-        # NVML init and the device handle are taken here, before the timed
-        # region starts, so the sampling thread begins at once
+        import subprocess
         try:
-            import pynvml as nv
-            nv.nvmlInit()
-            self._nv = nv
-            self._h = nv.nvmlDeviceGetHandleByIndex(self.device)
-            self._mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_CODE, str(self.device)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+            first = self.proc.stdout.readline().split()
+            if not first or first[0] != "ready":
+                raise RuntimeError("sampler did not start: " + " ".join(first))
+            self.max = int(first[1])
         except Exception as e:  # noqa: BLE001
             self.errors.append(repr(e))
-            return
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+            self.proc = None
 
     def stop(self):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=2)
-        if not self.samples:
+        if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
                     "errors": self.errors[:3]}
-        nv = self._nv
-        # median over the samples taken while the GPU was busy
-        busy = [s for s in self.samples if s[3] > 0] or self.samples
-        sm = [s[0] for s in busy]
-        reasons = sorted({name for s in self.samples for name, attr in self.REASONS
-                          if s[2] & getattr(nv, attr, 0)})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
-                "reasons": reasons, "samples": len(self.samples), "source": "nvml"}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        samples = []
+        for line in out.splitlines():
+            f = line.split()
+            if len(f) == 2 and f[0].isdigit():
+                samples.append((int(f[0]), int(f[1])))
+        if not samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["unsampled"]}
+        try:
+            import pynvml as nv
+            reasons = sorted({name for _, rs in samples for name, attr in self.REASONS
+                              if rs & getattr(nv, attr, 0)})
+        except Exception:  # noqa: BLE001
+            reasons = ["unknown"]
+        return {"sm_mhz": statistics.median(s_[0] for s_ in samples), "sm_max_mhz": self.max,
+                "reasons": reasons, "samples": len(samples), "source": "nvml (sampler process)"}
 
 
 def dist_setup():
