@@ -434,3 +434,62 @@ def test_batched_multipass_products(ctx, mode):
     for i in range(count):
         _check(mode, u[i], v[i], n, tm.from_limbs(out[i]))
     assert ctx.last_stats.max_round_err < TRIP
+
+
+# Column lengths with compile-time column passes (k_multipass.cu kColCtShapes):
+# 1728 = 12^3 and 1440 = 12 x 12 x 10 (prime-factor radices), 1792 = 16 x 16 x 7,
+# 1400 = 8 x 5 x 5 x 7; each row length 4096.
+_COLCT = [1728, 1440, 1792, 1400]
+
+
+@pytest.mark.parametrize("A", _COLCT)
+def test_compiled_column_shapes_exact(ctx, A):
+    rng = np.random.default_rng(A)
+    for mode, b, Nn in ((tm.Mode.LOW, 8, A * 4096), (tm.Mode.FULL, 10, A * 2048)):
+        n = Nn * b - 5
+        p = tm.manual_params(n, b, Nn, mode)
+        assert p.transform_length == A * 4096
+        nl = (n + 63) // 64
+        u = port.int_to_limbs(int.from_bytes(rng.bytes(nl * 8), "little") & ((1 << n) - 1), nl)
+        v = port.int_to_limbs(int.from_bytes(rng.bytes(nl * 8), "little") & ((1 << n) - 1), nl)
+        r = ctx.product_limbs(mode, u, v, p)
+        if mode == tm.Mode.LOW:
+            assert np.array_equal(r, port.oracle_low(u, v, n)), (A, mode)
+        else:
+            assert np.array_equal(r, port.oracle_full(u, v)[:len(r)]), (A, mode)
+        assert ctx.last_stats.max_round_err < TRIP
+
+
+_FALLBACK_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+import paper_1703_00640_b200 as tm
+from oracle import port
+ctx = tm.default_context(0)
+n = 1 << 26
+u, v = port.config_operands(3, n // 64)
+P = port.limbs_to_int(port.oracle_full(u, v))
+for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+    p = tm.select_params(n, mode)
+    r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
+    if mode == tm.Mode.FULL:
+        assert r == P
+    elif mode == tm.Mode.LOW:
+        assert r == P & ((1 << n) - 1)
+    else:
+        assert abs(P - (r << n)) < (1 << n) and 0 <= r <= (1 << n)
+print("ok")
+"""
+
+
+def test_generic_passes_at_compiled_lengths():
+    """TMG_NO_COLCT: the runtime-dispatched column passes (radix-16/4/3
+    schedules of 1728 and 1440) give the same products as the compiled
+    prime-factor ones (BASELINE config 3 lengths)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, TMG_NO_COLCT="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _FALLBACK_SNIPPET], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]

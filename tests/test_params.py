@@ -130,3 +130,18 @@ def test_accurate_policy_lengths_suit_the_gpu(n, mode):
     (small n used to admit odd 2357-smooth N such as 175)."""
     p = tm.select_params(n, mode, policy=Policy.ACCURATE)
     assert p.transform_length % 4 == 0
+
+
+def test_accurate_policy_prefers_compiled_column_schedules():
+    """At n = 2^26 the GPU cost model counts the compiled three-stage column
+    schedules (1728 = 12^3, 1440 = 12 x 12 x 10; prime-factor radices), so the
+    full product takes L = 1728 x 4096 and the truncated ones 1440 x 4096."""
+    n = 1 << 26
+    full = tm.select_params(n, Mode.FULL, policy=Policy.ACCURATE)
+    low = tm.select_params(n, Mode.LOW, policy=Policy.ACCURATE)
+    high = tm.select_params(n, Mode.HIGH, policy=Policy.ACCURATE)
+    assert full.transform_length == 1728 * 4096 and full.b == 19
+    assert low.transform_length == 1440 * 4096 and low.b == 12
+    assert high.transform_length == 1440 * 4096 and high.b == 12
+    # the reference policy is untouched by the GPU cost model
+    assert tm.select_params(n, Mode.LOW, policy=Policy.REFERENCE).b == 13
