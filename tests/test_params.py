@@ -112,7 +112,7 @@ def test_accurate_policy_at_benchmark_size():
     assert tm.select_params(n, Mode.LOW, policy=Policy.ACCURATE).b == 12
     assert tm.select_params(n, Mode.HIGH, policy=Policy.ACCURATE).b == 12
     full = tm.select_params(n, Mode.FULL, policy=Policy.ACCURATE)
-    assert full.b == 19 and full.N == 3670016
+    assert full.b == 19 and full.N == 1728 * 2048  # L = 1728 x 4096 (compiled 12^3 columns)
     assert tm.predicted_sigma(tm.select_params(n, Mode.LOW, policy=Policy.REFERENCE)) > 0.25 / 7
 
 
