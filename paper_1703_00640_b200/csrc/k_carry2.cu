@@ -97,7 +97,9 @@ __device__ __forceinline__ void coeffs_block(const CarryArgs& a, const double* _
     return (o >= 0 && o < nw) ? sww[o] : __ldg(a.w + j);
   };
   if constexpr (LAM == 0) {
-    for (int64_t k = kbase + tid; k < kend; k += kT) se[k - kbase] = ra.round(sww[k - wlo]);
+    const double* wk = sww + (kbase - wlo);
+    const int32_t nk = int32_t(kend - kbase);
+    for (int32_t q = tid; q < nk; q += kT) se[q] = ra.round(wk[q]);
   } else {
     // Blocks whose post-map inputs all lie in [0, N) away from the wrap
     // outputs (block-uniform) take the same arithmetic without bound checks,
@@ -231,15 +233,17 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
   {
     // all loads of a thread in flight before the stores
     constexpr int U = 8;
-    int64_t j = wlo + tid;
-    for (; j + (U - 1) * kT < whi; j += U * kT) {
+    const double* wg = a.w + wlo;
+    const int32_t nw32 = int32_t(nw);
+    int32_t o = tid;
+    for (; o + (U - 1) * kT < nw32; o += U * kT) {
       double v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = __ldg(a.w + j + u * kT);
+      for (int u = 0; u < U; ++u) v[u] = __ldg(wg + o + u * kT);
 #pragma unroll
-      for (int u = 0; u < U; ++u) sww[j + u * kT - wlo] = v[u];
+      for (int u = 0; u < U; ++u) sww[o + u * kT] = v[u];
     }
-    for (; j < whi; j += kT) sww[j - wlo] = __ldg(a.w + j);
+    for (; o < nw32; o += kT) sww[o] = __ldg(wg + o);
   }
   if (tid == 0) {
     s_flags = 0;
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
   uint32_t agg;
   (void)block_scan_tf(f, sw, &agg);
   if (tid == 0) a.aggs[blk] = agg;
-  flags |= ra.flags;
+  flags |= ra.all_flags();
   {
     const double e = warp_max_nonneg(ra.max_err), m = warp_max_nonneg(ra.max_abs);
     if ((tid & 31) == 0) s_red[tid >> 5] = make_double2(e, m);

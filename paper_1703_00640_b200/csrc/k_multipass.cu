@@ -1058,7 +1058,7 @@ k_carry(CarryArgs a) {
     se[k - klo] = e;
   }
   __syncthreads();
-  flags |= ra.flags;
+  flags |= ra.all_flags();
   {
     const double e = warp_max_nonneg(ra.max_err), m = warp_max_nonneg(ra.max_abs);
     if ((tid & 31) == 0) status_merge(a.status, e, m, 0);

@@ -227,7 +227,7 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
     const int64_t i = elem(k);
     if (i < M) cb[i] = cv[k];
   }
-  flags |= ra.flags;
+  flags |= ra.all_flags();
   // block max of errors
   {
     const double e = warp_max_nonneg(ra.max_err), m = warp_max_nonneg(ra.max_abs);

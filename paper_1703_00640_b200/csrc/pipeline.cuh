@@ -190,10 +190,14 @@ struct RoundAcc {
       const double e = fabs(x - r);
       max_err = fmax(max_err, e);
       max_abs = fmax(max_abs, ax);
-      if (e > 0.25) flags |= kFlagTripwire;
       return __double_as_longlong(t) - 0x4338000000000000ll;
     }
     return round_wide(x, ax);
+  }
+  // The accumulated flags: the residual tripwire (products_f64.cpp:22) is
+  // settled once from the running maximum instead of per coefficient.
+  __device__ __forceinline__ uint32_t all_flags() const {
+    return flags | (max_err > 0.25 ? uint32_t(kFlagTripwire) : 0u);
   }
   __device__ __forceinline__ long long round_wide(double x, double ax) {
     if (!(ax < 9007199254740992.0)) {
