@@ -332,7 +332,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         const unsigned tiles = a.ncols >> a.logc;
         const unsigned grid =
             (pl.colct && f1w > 0)
-                ? std::min<unsigned>(tiles, unsigned(f1w * cx.num_sms * (pl.colct->nthr <= 256 ? 2 : 1)))
+                ? std::min<unsigned>(tiles, unsigned(f1w * cx.num_sms * (pl.colct->nthr <= 288 ? 2 : 1)))
                 : tiles;
         launch(f1k, dim3(grid), dim3(pl.thr_f1), pl.smem_f1, st, a, "f1");
       }
@@ -426,7 +426,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.g.ncols = pl.B * (pl.C / 2);
       a.logc = pl.logc_il;
       a.fft = pl.iA;
-      auto ilk = pl.colct ? pl.colct->ilast : pl.colpp ? k_ilast_pp : k_ilast;
+      auto ilk = pl.colct_il ? pl.colct_il->ilast : pl.colpp ? k_ilast_pp : k_ilast;
       set_smem(ilk, pl.smem_il);
       {
         KTimer kt(cx, "k_ilast", double(L) * 16.0, int(p.mode), st);
@@ -434,8 +434,8 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         static const int ilw = getenv("TMG_IL_WAVES") ? atoi(getenv("TMG_IL_WAVES")) : 0;
         const unsigned tiles = a.g.ncols >> a.logc;
         const unsigned grid =
-            (pl.colct && ilw > 0)
-                ? std::min<unsigned>(tiles, unsigned(ilw * cx.num_sms * (pl.colct->nthr <= 256 ? 2 : 1)))
+            (pl.colct_il && ilw > 0)
+                ? std::min<unsigned>(tiles, unsigned(ilw * cx.num_sms * (pl.colct_il->nthr <= 288 ? 2 : 1)))
                 : tiles;
         launch(ilk, dim3(grid), dim3(pl.thr_il), pl.smem_il, st, a, "ilast");
       }

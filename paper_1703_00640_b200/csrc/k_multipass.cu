@@ -846,7 +846,7 @@ size_t colct_smem_bytes(uint32_t R, uint32_t c, uint32_t stablen, uint32_t radl)
 // table is written while the previous tile's last stage may still read the
 // other one.
 template <class SC, int LOGC, int NTHR, int P>
-__global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1)) k_f1_ct(F1Args a) {
+__global__ void __launch_bounds__(NTHR, (NTHR <= 288 ? 2 : 1)) k_f1_ct(F1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   constexpr uint32_t c = 1u << LOGC, R = SC::R;
@@ -898,7 +898,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1)) k_f1_ct(F1Args a)
 }
 
 template <class SC, int LOGC, int NTHR, int P>
-__global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1)) k_ilast_ct(ILastArgs a) {
+__global__ void __launch_bounds__(NTHR, (NTHR <= 288 ? 2 : 1)) k_ilast_ct(ILastArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   constexpr uint32_t c = 1u << LOGC, R = SC::R;
@@ -924,37 +924,46 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? 2 : 1)) k_ilast_ct(ILastA
 }
 
 // Compiled column shapes: {R, radices (maxrad 16 schedule), LOGC, NTHR}.
-#define TMG_COLCT(R_, LOGC_, NTHR_, P_, MAXRAD_, ...)                                      \
-  {R_, LOGC_, NTHR_, MAXRAD_, {__VA_ARGS__}, k_f1_ct<Sched<__VA_ARGS__>, LOGC_, NTHR_, P_>, \
+#define TMG_COLCT(R_, LOGC_, NTHR_, P_, USES_, ...)                                       \
+  {R_, LOGC_, NTHR_, USES_, {__VA_ARGS__}, k_f1_ct<Sched<__VA_ARGS__>, LOGC_, NTHR_, P_>, \
    k_ilast_ct<Sched<__VA_ARGS__>, LOGC_, NTHR_, P_>, ct_last_rad<Sched<__VA_ARGS__>>()}
 // (A radix-8, 1024-thread instantiation of 1792 = 8 x 8 x 4 x 7 measured
 // 86.6 / 47.7 us against 84.5 / 45.5 us for the 16 x 16 x 7 one; a
 // 560-thread one of 1400 equal at 96 registers.)  The first shape of a
-// length is the one used; the composite radices 10 and 12 (prime-factor
-// DFTs, dft.cuh) give three-stage schedules for 1728 = 12^3 and
-// 1440 = 12 x 12 x 10, one butterfly per thread and stage at 576 threads.
+// length that serves a pass (uses: 1 = F1, 2 = ilast) is the one used; the
+// composite radices 10 and 12 (prime-factor DFTs, dft.cuh) give
+// three-stage schedules for 1728 = 12^3 and 1440 = 12 x 12 x 10, one
+// butterfly per thread and stage.  Measured at 2^26: two columns per CTA
+// (two CTAs per SM) suit F1 of 1440 (66 -> 62 us) but not ilast (35 -> 39)
+// nor the full product, whose split writes z in F1's tile order (zgen
+// 29 -> 33 us with two columns).
 static const ColCtShape kColCtShapes[] = {
-    TMG_COLCT(1728, 2, 576, 12, 0, 12, 12, 12),
-    TMG_COLCT(1440, 2, 576, 12, 0, 12, 12, 10),
-    TMG_COLCT(1792, 2, 512, 16, 16, 16, 16, 7),
-    TMG_COLCT(1400, 2, 512, 16, 16, 8, 5, 5, 7),
-    TMG_COLCT(1792, 1, 256, 16, 16, 16, 16, 7),
-    TMG_COLCT(1400, 1, 256, 16, 16, 8, 5, 5, 7),
+    TMG_COLCT(1728, 2, 576, 12, 3, 12, 12, 12),
+    TMG_COLCT(1440, 1, 288, 12, 1, 12, 12, 10),
+    TMG_COLCT(1440, 2, 576, 12, 3, 12, 12, 10),
+    TMG_COLCT(1792, 2, 512, 16, 3, 16, 16, 7),
+    TMG_COLCT(1400, 2, 512, 16, 3, 8, 5, 5, 7),
+    TMG_COLCT(1792, 1, 256, 16, 0, 16, 16, 7),
+    TMG_COLCT(1400, 1, 256, 16, 0, 8, 5, 5, 7),
+    TMG_COLCT(1728, 1, 288, 12, 0, 12, 12, 12),
 };
 #undef TMG_COLCT
 
-const ColCtShape* colct_for(uint32_t R) {
+const ColCtShape* colct_for(uint32_t R, int role) {
   static const bool off = getenv("TMG_NO_COLCT") != nullptr;
-  // TMG_COLCT_LOGC (testing): only shapes with this many columns per CTA
+  // TMG_COLCT_LOGC (testing): the shape with this many columns per CTA, for
+  // both passes
   static const int want_logc = getenv("TMG_COLCT_LOGC") ? atoi(getenv("TMG_COLCT_LOGC")) : -1;
   if (off) return nullptr;
-  for (const ColCtShape& sh : kColCtShapes)
-    if (sh.R == R && (want_logc < 0 || sh.logc == want_logc)) return &sh;
+  for (const ColCtShape& sh : kColCtShapes) {
+    if (sh.R != R) continue;
+    if (want_logc >= 0 ? sh.logc == want_logc : (sh.uses & role) != 0) return &sh;
+  }
   return nullptr;
 }
 
 int colct_stages(uint32_t R) {
-  const ColCtShape* sh = colct_for(R);
+  const ColCtShape* sh = colct_for(R, 1);
   if (!sh) return 0;
   int n = 0;
   while (n < 4 && sh->rad[n]) ++n;

@@ -179,16 +179,17 @@ using ILastFn = void (*)(ILastArgs);
 struct ColCtShape {
   uint32_t R;
   int logc, nthr;
-  int maxrad;  // unused (0): schedules are explicit
+  int uses;  // passes served: 1 = first column pass (F1), 2 = last (ilast)
   int rad[4];
   F1Fn f1;
   ILastFn ilast;
   uint32_t radl;  // radix of the last stage (F1 output twiddle table)
 };
-// The compiled shape for column length R, or nullptr (TMG_NO_COLCT disables
-// them); colct_stages(R) is its stage count (0 without one) for the
-// parameter policy's cost model.
-const ColCtShape* colct_for(uint32_t R);
+// The compiled shape serving pass `role` (1 = F1, 2 = ilast) for column
+// length R, or nullptr (TMG_NO_COLCT disables them); colct_stages(R) is the
+// F1 shape's stage count (0 without one) for the parameter policy's cost
+// model.
+const ColCtShape* colct_for(uint32_t R, int role);
 int colct_stages(uint32_t R);
 size_t colct_smem_bytes(uint32_t R, uint32_t c, uint32_t stablen, uint32_t radl);
 

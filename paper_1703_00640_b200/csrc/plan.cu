@@ -509,22 +509,29 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   // Compile-time column passes where the column length and its radix-16
   // schedule match a compiled shape (two-pass plans only).
   pl->colct = nullptr;
+  pl->colct_il = nullptr;
   if (pl->kind == 2) {
-    const ColCtShape* sh = colct_for(A);
-    if (sh) {
+    const ColCtShape* sf1 = colct_for(A, 1);
+    const ColCtShape* sil = colct_for(A, 2);
+    bool same = sf1 && sil;
+    for (int i = 0; same && i < 4; ++i) same = sf1->rad[i] == sil->rad[i];
+    if (same) {
       std::vector<int> rad;
-      for (int i = 0; i < 4 && sh->rad[i]; ++i) rad.push_back(sh->rad[i]);
+      for (int i = 0; i < 4 && sf1->rad[i]; ++i) rad.push_back(sf1->rad[i]);
       SubFft f16 = make_subfft_rad(A, rad, tA, 1, &tw);
-      const uint32_t cc = 1u << sh->logc;
-      const size_t sf = colct_smem_bytes(A, cc, f16.stablen, sh->radl);
-      const size_t si = colct_smem_bytes(A, cc, f16.stablen, 0);
-      if ((UL / A) % cc == 0 && (C / 2) % cc == 0 && sf <= kMaxDynSmem) {
-        pl->colct = sh;
+      const uint32_t cf = 1u << sf1->logc, ci = 1u << sil->logc;
+      const size_t sf = colct_smem_bytes(A, cf, f16.stablen, sf1->radl);
+      const size_t si = colct_smem_bytes(A, ci, f16.stablen, 0);
+      if ((UL / A) % cf == 0 && (C / 2) % ci == 0 && sf <= kMaxDynSmem && si <= kMaxDynSmem) {
+        pl->colct = sf1;
+        pl->colct_il = sil;
         pl->colpp = false;
         pl->fA = f16;
         pl->iA = f16;
-        pl->logc_f1 = pl->logc_il = uint32_t(sh->logc);
-        pl->thr_f1 = pl->thr_il = sh->nthr;
+        pl->logc_f1 = uint32_t(sf1->logc);
+        pl->logc_il = uint32_t(sil->logc);
+        pl->thr_f1 = sf1->nthr;
+        pl->thr_il = sil->nthr;
         pl->smem_f1 = sf;
         pl->smem_il = si;
       }
