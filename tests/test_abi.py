@@ -93,3 +93,38 @@ def test_c_demo_runs(tmp_path):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK" in r.stdout
+
+
+def _build_cpp_demo(tmp_path):
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_1703_00640_b200")
+    exe = str(tmp_path / "cpp_api_demo")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "examples", "cpp_api_demo.cpp"), "-L", lib, "-ltruncmul_b200",
+                    "-Wl,-rpath," + lib, "-o", exe], check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_cpp_api_parameters(tmp_path):
+    """The C++ host API (truncmul_b200.hpp: products.hpp names and errors.hpp
+    exceptions over the C-ABI) builds, and its parameter functions run
+    without a GPU: select/validate/required_precision, the fallback mode and
+    the InputOutOfRange / UnsupportedLength exceptions."""
+    import subprocess
+    env = dict(os.environ, TMG_DEMO_PARAMS_ONLY="1")
+    r = subprocess.run([_build_cpp_demo(tmp_path)], capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "params OK" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_api_products(tmp_path):
+    """Full/low/high products through the C++ host API against a schoolbook
+    product, and the reference's exceptions (InputOutOfRange,
+    ConvolutionPrecisionFailure) raised from C-ABI error codes."""
+    import subprocess
+    r = subprocess.run([_build_cpp_demo(tmp_path)], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK" in r.stdout.splitlines()[-1]
