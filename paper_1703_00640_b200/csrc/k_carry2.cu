@@ -204,7 +204,7 @@ __device__ __forceinline__ void coeffs_block(const CarryArgs& a, const double* _
 }
 
 template <int LAM, int kPT>
-__global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
+__global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
   pdl_trigger();
   pdl_wait();
   constexpr int64_t kLimbs = int64_t(kT) * kPT;
@@ -229,7 +229,13 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
   const int64_t whi = min(nwt, kend + 2);
   const int64_t nw = whi > wlo ? whi - wlo : 0;
   double* sww = reinterpret_cast<double*>(smem_raw);
-  long long* se = reinterpret_cast<long long*>(sww + (nw + 1));
+  // the high product's folded buffer hbuf takes the slot after the staged
+  // window, and its rounded coefficients overwrite the window, which is dead
+  // once hbuf is formed (coeffs_block separates the two by a barrier): no
+  // shared memory beyond the low product's
+  const bool hmode = mc.mode == kModeHigh;
+  long long* se = hmode ? reinterpret_cast<long long*>(sww)
+                        : reinterpret_cast<long long*>(sww + (nw + 1));
   {
     // all loads of a thread in flight before the stores
     constexpr int U = 8;
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(kT) k_carry_lanes(CarryArgs a) {
   uint32_t flags = 0;
   const int64_t m0 = ms + int64_t(tid) * kPT;
   // the block's coefficients (those of lane ms - 1 included)
-  double* shb = reinterpret_cast<double*>(se + (kend - kbase) + 2);
+  double* shb = sww + (nw + 1);
   coeffs_block<LAM>(a, sww, wlo, nw, kbase, kend, se, shb, ra, s_psi, flags, tid);
   __syncthreads();
   // lanes of the thread's limbs
@@ -447,9 +453,9 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
   }
 }
 
-size_t carry2_smem(int b, int lam, int pt, bool hbuf) {
+size_t carry2_smem(int b, int lam, int pt, bool /*hbuf: shares the coefficient slot*/) {
   const int64_t nk = (64 * int64_t(kC2Threads * pt + 1) + b - 1) / b + 4;
-  return size_t(nk + lam + 8) * 8 + size_t(nk + 4) * 8 + (hbuf ? size_t(nk + 4) * 8 : 0) + 64;
+  return size_t(nk + lam + 8) * 8 + size_t(nk + 4) * 8 + 64;
 }
 
 template <int PT>
