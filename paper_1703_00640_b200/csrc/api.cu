@@ -477,7 +477,11 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       // limbs per thread: 4 when the block's coefficient window stays small
       // (wide chunks), else 2 (more CTAs per SM for narrow chunks)
       const bool hb = p.mode == PMode::kHigh;
-      const int pt = carry2_smem(int(p.b), lam, 4, hb) <= size_t(64) * 1024 ? 4 : 2;
+      // TMG_CARRY_PT (testing): force 2 or 4 limbs per thread
+      static const int force_pt = getenv("TMG_CARRY_PT") ? atoi(getenv("TMG_CARRY_PT")) : 0;
+      const int pt = (force_pt == 2 || force_pt == 4)
+                         ? force_pt
+                         : (carry2_smem(int(p.b), lam, 4, hb) <= size_t(64) * 1024 ? 4 : 2);
       const size_t smem2 = carry2_smem(int(p.b), lam, pt, hb);
       if (!old_carry && smem2 <= kMaxDynSmem && 64 * pl.ML + 64 < (int64_t(1) << 32)) {
         high_stop_fused = p.mode == PMode::kHigh;
