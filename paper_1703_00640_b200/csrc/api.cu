@@ -354,7 +354,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.to = 0;
       a.tc = 1;
       a.tmul = pl.A;
-      auto colk = pl.colpp ? col_pp_kernel(false) : k_col;
+      auto colk = pl.colct_b ? pl.colct_b->col : pl.colpp ? col_pp_kernel(false) : k_col;
       set_smem(colk, pl.smem_f2);
       {
         KTimer kt(cx, "k_col_f2", double(L) * 32.0, int(p.mode), st);
@@ -405,7 +405,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.to = 1;
       a.tc = 0;
       a.tmul = pl.C;
-      auto colk = pl.colpp ? col_pp_kernel(true) : k_col;
+      auto colk = pl.colct_b ? pl.colct_b->col : pl.colpp ? col_pp_kernel(true) : k_col;
       set_smem(colk, pl.smem_i2);
       {
         KTimer kt(cx, "k_col_i2", double(L) * 16.0, int(p.mode), st);

@@ -880,10 +880,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 288 ? 2 : 1)) k_f1_ct(F1Args a)
     if (tid == 0 && nx < ntiles && !a.zt.natural)
       prefetch_l2(a.z + uint64_t(nx) * a.zt.zrows * c, uint32_t(tile_bytes));
     double2* qt = qt2 + par * (c * RL);
-    if (uint32_t(tid) < c * RL) {
-      const uint32_t it = uint32_t(tid) / RL, q = uint32_t(tid) - it * RL;
+    for (uint32_t i = tid; i < c * RL; i += NTHR) {
+      const uint32_t it = i / RL, q = i - it * RL;
       const uint32_t x = (col0 + it) * NSL * q;
-      qt[tid] = x ? tw.get(x) : make_double2(1.0, 0.0);
+      qt[i] = x ? tw.get(x) : make_double2(1.0, 0.0);
     }
     double topu = 0.0, topv = 0.0;
     if (mc.mode == kModeHigh && col0 < uint32_t(mc.nfold + mc.lambda)) {
@@ -923,10 +923,75 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 288 ? 2 : 1)) k_ilast_ct(ILastA
   }
 }
 
+// Middle column passes of three-pass plans (over B, in place) with
+// compile-time schedules.  The output twiddle omega_L^{X k}, X = (outer to +
+// col tc) tmul, factors like F1's: omega^{X ob} per butterfly (fetched
+// before the last DFT) times a per-CTA table omega^{X NS q}.
+template <uint32_t RADL>
+struct ColSinkQ {
+  double2* data;
+  ColGeom g;
+  int64_t outer;
+  uint32_t col0;
+  TwGlobal tw;
+  uint32_t to, tc, tmul;
+  bool inv;
+  const double2* qt;
+  __device__ __forceinline__ uint32_t X(uint32_t item) const {
+    return (uint32_t(outer) * to + (col0 + item) * tc) * tmul;
+  }
+  __device__ __forceinline__ double2 prep(uint32_t item, uint32_t ob) const {
+    const uint32_t x = X(item) * ob;
+    return x ? tw.get(x) : make_double2(1.0, 0.0);
+  }
+  __device__ __forceinline__ void put(uint32_t item, uint32_t k, uint32_t q, double2 v,
+                                      double2 b) const {
+    const double2 w = cmul(b, qt[item * RADL + q]);
+    data[col_off(g, outer, k, col0 + item)] = inv ? cmulc(v, w) : cmul(v, w);
+  }
+};
+template <uint32_t RADL>
+struct SinkPrep<ColSinkQ<RADL>> {
+  static constexpr bool value = true;
+};
+
+template <class SC, int LOGC, int NTHR, int P>
+__global__ void __launch_bounds__(NTHR, (NTHR <= 288 ? 2 : 1)) k_col_ct(ColArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sbuf = reinterpret_cast<double2*>(smem_raw);
+  constexpr uint32_t c = 1u << LOGC, R = SC::R;
+  constexpr uint32_t RL = ct_last_rad<SC>(), NSL = ct_last_ns<SC>();
+  const int tid = threadIdx.x;
+  const uint32_t col0 = blockIdx.x * c;
+  const int64_t outer = blockIdx.y;
+  double2* stab = sbuf + padded_len(R * c);
+  double2* qt = stab + a.fft.stablen;
+  pdl_trigger();
+  for (uint32_t i = tid; i < a.fft.stablen; i += NTHR) stab[i] = __ldg(a.fft.stab + i);
+  const ColSinkQ<RL> sink{a.data, a.g, outer, col0, a.tw, a.to, a.tc, a.tmul, a.inv != 0, qt};
+  for (uint32_t i = tid; i < c * RL; i += NTHR) {
+    const uint32_t it = i / RL, q = i - it * RL;
+    const uint32_t x = sink.X(it) * NSL * q;
+    qt[i] = x ? a.tw.get(x) : make_double2(1.0, 0.0);
+  }
+  pdl_wait();
+  const LayCols lay{uint32_t(LOGC), c - 1};
+  double2 x[P];
+  if (a.inv)
+    cc_stages<true, SC, 0, LOGC, NTHR, P>(x, sbuf, lay, stab, a.fft, ColSrc{a.data, a.g, outer, col0},
+                                          sink, tid);
+  else
+    cc_stages<false, SC, 0, LOGC, NTHR, P>(x, sbuf, lay, stab, a.fft,
+                                           ColSrc{a.data, a.g, outer, col0}, sink, tid);
+}
+
 // Compiled column shapes: {R, radices (maxrad 16 schedule), LOGC, NTHR}.
 #define TMG_COLCT(R_, LOGC_, NTHR_, P_, USES_, ...)                                       \
   {R_, LOGC_, NTHR_, USES_, {__VA_ARGS__}, k_f1_ct<Sched<__VA_ARGS__>, LOGC_, NTHR_, P_>, \
-   k_ilast_ct<Sched<__VA_ARGS__>, LOGC_, NTHR_, P_>, ct_last_rad<Sched<__VA_ARGS__>>()}
+   k_ilast_ct<Sched<__VA_ARGS__>, LOGC_, NTHR_, P_>,                                     \
+   k_col_ct<Sched<__VA_ARGS__>, LOGC_, NTHR_, P_>, ct_last_rad<Sched<__VA_ARGS__>>()}
+// Shapes serve passes by `uses`: 1 = F1, 2 = ilast, 4 = the middle (B)
+// column passes of three-pass plans.
 // (A radix-8, 1024-thread instantiation of 1792 = 8 x 8 x 4 x 7 measured
 // 86.6 / 47.7 us against 84.5 / 45.5 us for the 16 x 16 x 7 one; a
 // 560-thread one of 1400 equal at 96 registers.)  The first shape of a
@@ -946,6 +1011,11 @@ static const ColCtShape kColCtShapes[] = {
     TMG_COLCT(1792, 1, 256, 16, 0, 16, 16, 7),
     TMG_COLCT(1400, 1, 256, 16, 0, 8, 5, 5, 7),
     TMG_COLCT(1728, 1, 288, 12, 0, 12, 12, 12),
+    // three-pass plans (2^28): A x B columns around the 4096-point rows
+    TMG_COLCT(64, 6, 256, 16, 7, 16, 4),
+    TMG_COLCT(80, 5, 256, 16, 7, 16, 5),
+    TMG_COLCT(128, 5, 256, 16, 7, 16, 8),
+    TMG_COLCT(70, 5, 256, 16, 7, 14, 5),
 };
 #undef TMG_COLCT
 

@@ -179,11 +179,12 @@ using ILastFn = void (*)(ILastArgs);
 struct ColCtShape {
   uint32_t R;
   int logc, nthr;
-  int uses;  // passes served: 1 = first column pass (F1), 2 = last (ilast)
+  int uses;  // passes served: 1 = F1, 2 = ilast, 4 = middle column passes (k_col_ct)
   int rad[4];
   F1Fn f1;
   ILastFn ilast;
-  uint32_t radl;  // radix of the last stage (F1 output twiddle table)
+  void (*col)(ColArgs);  // middle column pass (three-pass plans)
+  uint32_t radl;  // radix of the last stage (output twiddle table)
 };
 // The compiled shape serving pass `role` (1 = F1, 2 = ilast) for column
 // length R, or nullptr (TMG_NO_COLCT disables them); colct_stages(R) is the

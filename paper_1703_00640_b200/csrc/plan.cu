@@ -510,11 +510,31 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   // schedule match a compiled shape (two-pass plans only).
   pl->colct = nullptr;
   pl->colct_il = nullptr;
-  if (pl->kind == 2) {
+  pl->colct_b = nullptr;
+  if (pl->kind == 2 || pl->kind == 3) {
     const ColCtShape* sf1 = colct_for(A, 1);
     const ColCtShape* sil = colct_for(A, 2);
-    bool same = sf1 && sil;
+    // three-pass plans also need the middle passes' shape over B
+    const ColCtShape* scb = pl->kind == 3 ? colct_for(B, 4) : nullptr;
+    bool same = sf1 && sil && (pl->kind == 2 || scb);
     for (int i = 0; same && i < 4; ++i) same = sf1->rad[i] == sil->rad[i];
+    if (same && scb) {
+      const uint32_t cb = 1u << scb->logc;
+      std::vector<int> radb;
+      for (int i = 0; i < 4 && scb->rad[i]; ++i) radb.push_back(scb->rad[i]);
+      SubFft fb = make_subfft_rad(B, radb, tw.table(B), 1, &tw);
+      const size_t sb = colct_smem_bytes(B, cb, fb.stablen, scb->radl);
+      if (C % cb == 0 && (C / 2) % cb == 0 && sb <= kMaxDynSmem) {
+        pl->colct_b = scb;
+        pl->fB = fb;
+        pl->iB = fb;
+        pl->logc_f2 = pl->logc_i2 = uint32_t(scb->logc);
+        pl->thr_f2 = pl->thr_i2 = scb->nthr;
+        pl->smem_f2 = pl->smem_i2 = sb;
+      } else {
+        same = false;
+      }
+    }
     if (same) {
       std::vector<int> rad;
       for (int i = 0; i < 4 && sf1->rad[i]; ++i) rad.push_back(sf1->rad[i]);

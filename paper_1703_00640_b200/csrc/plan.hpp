@@ -72,6 +72,7 @@ struct Plan {
   bool f1_stw = false;  // k_f1 stages its inter-pass twiddles per CTA
   const ColCtShape* colct = nullptr;     // compile-time first column pass (k_f1_ct)
   const ColCtShape* colct_il = nullptr;  // compile-time last column pass (k_ilast_ct)
+  const ColCtShape* colct_b = nullptr;   // three-pass plans: middle column passes (k_col_ct)
   int thr_f1 = 0, thr_f2 = 0, thr_i2 = 0, thr_il = 0, thr_mid = 0;
   size_t smem_zgen = 0;
   bool mid_shared_table = false;
