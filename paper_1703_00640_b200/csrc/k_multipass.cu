@@ -1011,6 +1011,10 @@ static const ColCtShape kColCtShapes[] = {
     TMG_COLCT(1792, 1, 256, 16, 0, 16, 16, 7),
     TMG_COLCT(1400, 1, 256, 16, 0, 8, 5, 5, 7),
     TMG_COLCT(1728, 1, 288, 12, 0, 12, 12, 12),
+    // 2^24 (BASELINE config 2): 448 x 4096 full, 320 x 4096 low/high
+    TMG_COLCT(448, 4, 512, 16, 3, 16, 4, 7),
+    TMG_COLCT(320, 4, 512, 16, 3, 16, 5, 4),
+    TMG_COLCT(112, 5, 256, 16, 7, 16, 7),  // 2^22 full
     // three-pass plans (2^28): A x B columns around the 4096-point rows
     TMG_COLCT(64, 6, 256, 16, 7, 16, 4),
     TMG_COLCT(80, 5, 256, 16, 7, 16, 5),
