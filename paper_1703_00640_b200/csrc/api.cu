@@ -566,7 +566,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
   cx.last_passes = pl.kind;
   if (pl.kind == 0)
     throw Error(TMG_ERR_UNSUPPORTED, "fallback products run through the host entry points");
-  if (pl.kind == 1) {
+  if (pl.kind == 1 || (pl.small_batch && count >= kSmallBatchMinCount)) {
     SmallArgs a;
     a.u = du;
     a.v = dv;
@@ -590,7 +590,8 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     // the 2-CTA variant only pays when two CTAs' shared memory fits an SM
     // (228 KB, 1 KB reserved per CTA); otherwise its spills cost for nothing
     const bool two = pl.small_threads <= 384 && 2 * (pl.small_smem + 1024) <= size_t(228) * 1024;
-    auto sk = (two && !one_cta) ? k_small_product_2 : k_small_product;
+    auto sk = pl.small_threads > 512 ? k_small_product_big
+                                     : (two && !one_cta) ? k_small_product_2 : k_small_product;
     set_smem(sk, pl.small_smem);
     {
       KTimer kt(cx, "k_small_product", double(count) * double(2 * pl.nlimbs + pl.out_limbs) * 8.0, int(p.mode));

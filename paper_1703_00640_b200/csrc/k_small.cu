@@ -44,6 +44,12 @@ __global__ void __launch_bounds__(384, 2)
 k_small_product_2(SmallArgs a) {
   small_product_body<384, 2>(a);
 }
+// Batches of products just above the single-product cutoff (L <= 12288, the
+// 2^17-bit range): one CTA per product at up to 768 threads.
+__global__ void __launch_bounds__(kSmallBatchMaxThreads, 1)
+k_small_product_big(SmallArgs a) {
+  small_product_body<kSmallBatchMaxThreads, 1>(a);
+}
 
 template <int MAXT, int MINB>
 __device__ __forceinline__ void small_product_body(const SmallArgs& a) {

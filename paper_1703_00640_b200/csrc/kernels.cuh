@@ -10,6 +10,12 @@ namespace tmg {
 
 // Transform lengths up to this run as one fused CTA per product.
 constexpr int64_t kSmallMaxL = 8192;
+// Batches of products up to this length (that fit one CTA's shared memory)
+// run the fused single-CTA kernel, one CTA per product, instead of a
+// multi-pass chain per product (plan.small_batch).
+constexpr int64_t kSmallBatchMaxL = 12288;
+constexpr int kSmallBatchMaxThreads = 768;
+constexpr int64_t kSmallBatchMinCount = 8;
 
 struct SmallArgs {
   const uint64_t* u;  // batch of operands, nlimbs words each
@@ -40,6 +46,7 @@ size_t col_smem_bytes(uint32_t R, uint32_t c);
 
 __global__ void k_small_product(SmallArgs a);
 __global__ void k_small_product_2(SmallArgs a);  // <= 384 threads, 2 CTAs per SM
+__global__ void k_small_product_big(SmallArgs a);  // <= 768 threads (batched L <= 12288)
 
 // ---------------------------------------------------------------------------
 // Multi-pass pipeline.  The complex transform of length L = A * B * C runs as

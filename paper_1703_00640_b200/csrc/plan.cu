@@ -388,6 +388,18 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
     return pl;
   }
 
+  // batches of this length can still run the fused kernel, one CTA per
+  // product, when the whole product fits one CTA's shared memory
+  if (L <= kSmallBatchMaxL && threads_for(uint64_t(L)) <= kSmallBatchMaxThreads &&
+      small_smem_bytes(L, pl->nlimbs) <= kMaxDynSmem) {
+    const double2* t = tw.table(uint32_t(L));
+    pl->fwd = make_subfft(uint32_t(L), t, 1, nullptr);
+    pl->inv = make_subfft(uint32_t(L / 2), t, 2, nullptr);
+    pl->small_threads = threads_for(uint64_t(L));
+    pl->small_smem = small_smem_bytes(L, pl->nlimbs);
+    pl->small_batch = true;
+  }
+
   // multi-pass: C = row length (even, <= 4096), A (and B) column lengths
   const uint64_t UL = uint64_t(L);
   if (UL >= (uint64_t(1) << 32)) throw Error(TMG_ERR_UNSUPPORTED, "transform length above 2^32");

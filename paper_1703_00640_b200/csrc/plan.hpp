@@ -63,6 +63,7 @@ struct Plan {
   SubFft fwd{}, inv{};
   size_t small_smem = 0;
   int small_threads = 0;
+  bool small_batch = false;  // multi-pass plan whose batches run the fused kernel
   // multi-pass
   SubFft fA{}, iA{}, fB{}, iB{}, fC{}, iC{};
   TwGlobal twL{};
