@@ -417,12 +417,15 @@ def test_wide_chunks_refuse_on_the_64_bit_window_path(ctx):
         ctx.product_limbs(tm.Mode.FULL, u, u, p)
 
 
+@pytest.mark.parametrize("lg", [17, 18])
 @pytest.mark.parametrize("mode", [tm.Mode.LOW, tm.Mode.FULL, tm.Mode.HIGH])
-def test_batched_multipass_products(ctx, mode):
-    """A batch whose transform exceeds one CTA (L > 8192) runs its products
-    concurrently on the batch workspaces; every product exact, per-product
-    flags zero."""
-    n, count = 1 << 17, 24
+def test_batched_multipass_products(ctx, mode, lg):
+    """Batches beyond the single-product cutoff (L > 8192): at 2^17 the low
+    and high products (L = 10240) run the fused kernel one CTA per product
+    (k_small_product_big), the full one (L = 12544) and every 2^18 product
+    run multi-pass chains concurrently on the batch workspaces; every
+    product exact, per-product flags zero."""
+    n, count = 1 << lg, 24 if lg == 17 else 10
     nl = n // 64
     w = port.mt19937_64(17 + int(mode), 2 * count * nl).reshape(count, 2, nl)
     u = np.ascontiguousarray(w[:, 0, :])
