@@ -55,13 +55,16 @@ __device__ __forceinline__ double2 premap2(const MapConsts& mc, const DF2& D2, i
   const double Nd = double(N);
   const int fam = (mc.mode == kModeLow) ? 0 : 2;
   const int lam = mc.lambda;
+  // k = j - r (+ N) as an exact double from one conversion of j
+  const double jd = double(j);
   double au = 0.0, av = 0.0;
   RowLoopDown<kMaxLambda>::run([&](auto rc) {
     constexpr int r = decltype(rc)::value;
     if (r < lam) {
       int64_t k = j - r;
-      if (k < 0) k += N;
-      const double cf = coef_r<r>(fam, double(k), Nd, mc.cpre[r]);
+      const bool wrap = k < 0;
+      if (wrap) k += N;
+      const double cf = coef_r<r>(fam, jd - double(r) + (wrap ? Nd : 0.0), Nd, mc.cpre[r]);
       const double2 d = D2(k);
       au += d.x * cf;
       av += d.y * cf;
@@ -108,11 +111,12 @@ __device__ __forceinline__ double post_flat(const MapConsts& mc, const WF& W,
   const double Nd = double(N);
   const int fam = (mc.mode == kModeLow) ? 1 : 3;
   const int lam = mc.lambda;
+  const double jd = double(j);  // k = j - r as an exact double, one conversion
   double acc = 0.0;
   RowLoopDown<kMaxLambda>::run([&](auto rc) {
     constexpr int r = decltype(rc)::value;
     const int64_t k = j - r;
-    if (r < lam && k >= 0 && k < N) acc += W(k) * coef_r<r>(fam, double(k), Nd, mc.cpost[r]);
+    if (r < lam && k >= 0 && k < N) acc += W(k) * coef_r<r>(fam, jd - double(r), Nd, mc.cpost[r]);
   });
   return acc;
 }
