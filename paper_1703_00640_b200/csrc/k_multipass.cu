@@ -1282,19 +1282,22 @@ k_high_round(HighRoundArgs a) {
   constexpr int LB = kCarryThreads * kHighPerThread;
   const int64_t ms = int64_t(blk) * LB;
   const int64_t me = min(a.WL, ms + LB);
-  const int64_t m0 = ms + int64_t(tid) * kHighPerThread;
-  const int64_t m1 = min(me, m0 + kHighPerThread);
   uint32_t flags = 0, topbit = 0, lownz = 0;
   const int64_t OL = a.out_limbs;
-  // the thread's kHighPerThread + 1 limbs of t, loaded together
-  uint64_t tv[kHighPerThread + 1];
-#pragma unroll
-  for (int i = 0; i <= kHighPerThread; ++i) tv[i] = (m0 + i <= m1) ? tl(m0 + i + q) : 0ull;
+  // limbs interleaved over the block (m = ms + tid + i * threads): the
+  // loads of t and the stores of w are coalesced; all loads first
+  uint64_t tlo[kHighPerThread], thi[kHighPerThread];
 #pragma unroll
   for (int i = 0; i < kHighPerThread; ++i) {
-    const int64_t m = m0 + i;
-    if (m < m1) {
-      const uint64_t lo = tv[i], hi = tv[i + 1];
+    const int64_t m = ms + tid + int64_t(i) * kCarryThreads;
+    tlo[i] = (m < me) ? tl(m + q) : 0ull;
+    thi[i] = (m < me) ? tl(m + q + 1) : 0ull;
+  }
+#pragma unroll
+  for (int i = 0; i < kHighPerThread; ++i) {
+    const int64_t m = ms + tid + int64_t(i) * kCarryThreads;
+    if (m < me) {
+      const uint64_t lo = tlo[i], hi = thi[i];
       const uint64_t w0 = r ? ((lo >> r) | (hi << (64 - r))) : lo;
       const uint64_t x = w0 + uint64_t((inc && uint64_t(m) <= uint64_t(first)) ? 1 : 0);
       // the increment carried out of the top examined limb: w > 2^n
