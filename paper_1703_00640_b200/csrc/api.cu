@@ -91,7 +91,8 @@ struct Workspace {
     if (stream) cudaStreamDestroy(stream);
   }
 };
-constexpr int kMaxBatchStreams = 8;
+constexpr int kMaxBatchStreams = 32;
+constexpr int64_t kGraphMinBatch = 4;  // batches replayed as graphs from this size
 
 struct Context {
   int device = 0;
@@ -107,6 +108,39 @@ struct Context {
   std::vector<std::unique_ptr<Workspace>> wsb;    // batch workspaces (own streams)
   bool debug_sync = false;
   DevStatus* h_status = nullptr;  // pinned
+  // Multi-pass batches replayed as CUDA graphs: a batch shape seen once runs
+  // eagerly (allocating every workspace buffer), the second time it is
+  // captured, afterwards replayed.  Keyed on plan, count and pointers;
+  // dropped when any device buffer reallocates.
+  struct BatchKey {
+    const void* plan;
+    int64_t count;
+    const void *u, *v, *out, *flags;
+    bool operator<(const BatchKey& o) const {
+      return std::tie(plan, count, u, v, out, flags) <
+             std::tie(o.plan, o.count, o.u, o.v, o.out, o.flags);
+    }
+  };
+  struct BatchGraph {
+    cudaGraphExec_t exec = nullptr;
+    int kernels = 0;
+  };
+  std::map<BatchKey, BatchGraph> graphs;
+  std::map<BatchKey, int> graph_seen;
+  uint64_t graph_gen = 0;
+  bool graphs_off = false;
+  cudaStream_t cap_stream = nullptr;  // batches are captured here (the context
+                                      // stream may be the legacy default one)
+  void clear_graphs() {
+    for (auto& g : graphs)
+      if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+    graphs.clear();
+    graph_seen.clear();
+  }
+  ~Context() {
+    clear_graphs();
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+  }
   int32_t last_kernels = 0;
   int64_t last_L = 0;
   int32_t last_passes = 0;
@@ -613,7 +647,54 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
   }
   // a batch: products round-robin over up to kMaxBatchStreams workspaces,
   // each on its own stream with its own status word, published per product
-  // into pflags and merged into the context status
+  // into pflags and merged into the context status.  Repeated batch shapes
+  // replay a captured graph (the launches of a batch of small multi-pass
+  // products cost more host time than their kernels run).
+  static const bool no_graph = getenv("TMG_NO_GRAPH") != nullptr;
+  const bool graphable = !no_graph && !cx.graphs_off && !cx.prof.on && !g_debug_sync &&
+                         count >= kGraphMinBatch;
+  Context::BatchKey key{&pl, count, du, dv, dout, pflags};
+  bool capture = false;
+  if (graphable) {
+    const uint64_t gen = g_devbuf_generation.load();
+    if (gen != cx.graph_gen) {
+      cx.clear_graphs();
+      cx.graph_gen = gen;
+    }
+    auto it = cx.graphs.find(key);
+    if (it != cx.graphs.end()) {
+      TMG_CUDA(cudaGraphLaunch(it->second.exec, st));
+      cx.last_kernels = it->second.kernels;
+      return;
+    }
+    capture = cx.graph_seen[key]++ > 0;
+  }
+  const cudaStream_t user_st = st;
+  if (capture) {
+    if (!cx.cap_stream) TMG_CUDA(cudaStreamCreateWithFlags(&cx.cap_stream, cudaStreamNonBlocking));
+    st = cx.cap_stream;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      (void)cudaGetLastError();
+      cx.graphs_off = true;
+      capture = false;
+      st = user_st;
+    }
+  }
+  // an error thrown while capturing must not leave the stream in capture mode
+  struct CaptureGuard {
+    cudaStream_t st;
+    bool* active;
+    Context* cx;
+    ~CaptureGuard() {
+      if (*active) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        (void)cudaGetLastError();
+        cx->graphs_off = true;
+      }
+    }
+  } guard{st, &capture, &cx};
   const size_t budget = size_t(4) << 30;
   const int64_t by_mem = int64_t(budget / std::max<size_t>(workspace_bytes(pl), 1));
   const int S = int(std::max<int64_t>(
@@ -648,6 +729,23 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     TMG_CUDA(cudaStreamWaitEvent(st, w.done, 0));
   }
   cx.last_kernels = kernels;
+  if (capture) {
+    capture = false;  // the guard has nothing left to close
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e1 = cudaStreamEndCapture(st, &g);
+    const cudaError_t e2 = (e1 == cudaSuccess) ? cudaGraphInstantiate(&exec, g, 0) : e1;
+    if (g) cudaGraphDestroy(g);
+    if (e2 != cudaSuccess) {
+      // capture unsupported here: run this batch eagerly, stop capturing
+      (void)cudaGetLastError();
+      cx.graphs_off = true;
+      enqueue(cx, pl, du, dv, dout, count, pflags);
+      return;
+    }
+    cx.graphs[key] = Context::BatchGraph{exec, kernels};
+    TMG_CUDA(cudaGraphLaunch(exec, user_st));
+  }
 }
 
 void reset_status(Context& cx) {

@@ -2,6 +2,8 @@
 // twiddle tables, map constants (maps_f64.cpp:192-245 of the reference).
 #include "plan.hpp"
 
+#include <atomic>
+
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -23,8 +25,12 @@ DevBuf::~DevBuf() {
   if (p) cudaFree(p);
 }
 
+std::atomic<uint64_t> g_devbuf_generation{0};
+
 void DevBuf::ensure(size_t nbytes) {
   if (nbytes <= bytes) return;
+  // a reallocation invalidates every captured graph that used the old buffer
+  if (p) g_devbuf_generation.fetch_add(1);
   if (p) cudaFree(p);
   p = nullptr;
   bytes = 0;

@@ -2,6 +2,7 @@
 // map constants of one parameter set.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <map>
 #include <string>
@@ -14,6 +15,9 @@
 namespace tmg {
 
 // Owned device allocation.
+// Bumped whenever a DevBuf reallocates (captured batch graphs key on it).
+extern std::atomic<uint64_t> g_devbuf_generation;
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;

@@ -496,3 +496,32 @@ def test_generic_passes_at_compiled_lengths():
     r = subprocess.run([sys.executable, "-c", _FALLBACK_SNIPPET], cwd=root, env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+def test_batched_graph_replay(ctx):
+    """Repeated multi-pass batch shapes run eagerly, then are captured, then
+    replayed as a CUDA graph; every call uploads new operands into the same
+    device buffers and must still be exact.  A larger batch in between
+    reallocates the workspaces, which must invalidate the captured graph."""
+    n, count = 1 << 18, 10
+    nl = n // 64
+    p = tm.select_params(n, tm.Mode.LOW)
+    # reps 0-2: eager, capture, replay; the larger batch before rep 3
+    # reallocates; reps 3-5: eager, capture, replay again
+    for rep in range(6):
+        if rep == 3:
+            # grows the batch workspaces (and the context's operand buffers)
+            nb = 1 << 20
+            wb = port.mt19937_64(99, 2 * 4 * (nb // 64)).reshape(4, 2, nb // 64)
+            ub, vb = np.ascontiguousarray(wb[:, 0, :]), np.ascontiguousarray(wb[:, 1, :])
+            pb = tm.select_params(nb, tm.Mode.LOW)
+            outb = ctx.product_batched(pb, ub, vb)
+            for i in range(4):
+                _check(tm.Mode.LOW, ub[i], vb[i], nb, tm.from_limbs(outb[i]))
+        w = port.mt19937_64(40 + rep, 2 * count * nl).reshape(count, 2, nl)
+        u = np.ascontiguousarray(w[:, 0, :])
+        v = np.ascontiguousarray(w[:, 1, :])
+        out, flags = ctx.product_batched(p, u, v, return_flags=True)
+        assert not flags.any()
+        for i in range(count):
+            _check(tm.Mode.LOW, u[i], v[i], n, tm.from_limbs(out[i]))
