@@ -626,10 +626,20 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     const bool two = pl.small_threads <= 384 && 2 * (pl.small_smem + 1024) <= size_t(228) * 1024;
     auto sk = pl.small_threads > 512 ? k_small_product_big
                                      : (two && !one_cta) ? k_small_product_2 : k_small_product;
+    unsigned threads = unsigned(pl.small_threads);
+    // TMG_SMALL_GENERIC (testing): the runtime-dispatched stages at every length
+    static const bool small_generic = getenv("TMG_SMALL_GENERIC") != nullptr;
+    // (a 640-thread 8 x 8 x 8 x 10 variant for the low/high L = 5120 was
+    // slower than the 2-CTA generic kernel: 1.57 / 2.12 ms against 1.40 /
+    // 1.68 ms for 4096 products; the maps prefer two smaller CTAs per SM)
+    if (!small_generic && pl.L == 6144 && p.mode == PMode::kFull) {
+      sk = k_small_6144;
+      threads = 768;
+    }
     set_smem(sk, pl.small_smem);
     {
       KTimer kt(cx, "k_small_product", double(count) * double(2 * pl.nlimbs + pl.out_limbs) * 8.0, int(p.mode));
-      launch(sk, dim3(unsigned(count)), dim3(pl.small_threads), pl.small_smem, st, a, "small");
+      launch(sk, dim3(unsigned(count)), dim3(threads), pl.small_smem, st, a, "small");
     }
     check_launch("k_small_product");
     cx.last_kernels = 1;

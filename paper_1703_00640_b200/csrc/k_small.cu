@@ -8,6 +8,9 @@
 //
 // Reference path: products_f64.cpp:106-171 end to end.
 #include "kernels.cuh"
+#include "fft_ct.cuh"
+
+#include <type_traits>
 
 namespace tmg {
 
@@ -27,9 +30,56 @@ __device__ __forceinline__ uint64_t window_smem(const uint64_t* limbs,
 
 constexpr int kMaxPer = 18;  // values per thread held across a barrier
 
+// Whole transform of length SC::R in shared memory (padded natural layout)
+// with a compile-time radix schedule: every stage's butterflies spread over
+// NTHR threads (NB per thread), stage twiddles omega^{j q step} from the
+// two-level table (step = (R / (NS RAD)) * stride), the register block sized
+// for this schedule only.  Same arithmetic as the generic stages.
+template <bool INV, class SC, int S, int NTHR, int P>
+__device__ __forceinline__ void small_ct_stages(double2 (&x)[P], double2* __restrict__ buf,
+                                                const TwSmem& tw, uint32_t stride, int tid) {
+  constexpr int RAD = SC::rad(S);
+  constexpr uint32_t NS = SC::ns(S);
+  constexpr uint32_t R = SC::R;
+  constexpr uint32_t nbf = R / RAD;
+  constexpr int NB = int((nbf + NTHR - 1) / NTHR);
+  static_assert(NB * RAD <= P, "register block");
+  constexpr uint32_t step = R / (NS * uint32_t(RAD));
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const uint32_t bf = uint32_t(tid) + uint32_t(i) * NTHR;
+    if (nbf % NTHR == 0 || bf < nbf) {
+#pragma unroll
+      for (int q = 0; q < RAD; ++q) x[i * RAD + q] = buf[padidx(bf + q * nbf)];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const uint32_t bf = uint32_t(tid) + uint32_t(i) * NTHR;
+    if (nbf % NTHR == 0 || bf < nbf) {
+      const uint32_t tq = bf / NS, j = bf - tq * NS;
+      double2* xv = x + i * RAD;
+      if (NS > 1 && j != 0) {
+#pragma unroll
+        for (int q = 1; q < RAD; ++q) {
+          const double2 w = tw.get(j * uint32_t(q) * step * stride);
+          xv[q] = INV ? cmulc(xv[q], w) : cmul(xv[q], w);
+        }
+      }
+      dft<RAD, INV>(xv);
+      const uint32_t ob = tq * NS * RAD + j;
+#pragma unroll
+      for (int q = 0; q < RAD; ++q) buf[padidx(ob + q * NS)] = xv[q];
+    }
+  }
+  __syncthreads();
+  if constexpr (S + 1 < SC::nst) small_ct_stages<INV, SC, S + 1, NTHR, P>(x, buf, tw, stride, tid);
+}
+
 }  // namespace
 
-template <int MAXT, int MINB>
+template <int MAXT, int MINB, class SCF = void, class SCI = void>
 __device__ __forceinline__ void small_product_body(const SmallArgs& a);
 
 // Two instantiations: up to 512 threads at 128 registers (one CTA per SM),
@@ -44,6 +94,14 @@ __global__ void __launch_bounds__(384, 2)
 k_small_product_2(SmallArgs a) {
   small_product_body<384, 2>(a);
 }
+// The full product of BASELINE config 4's size (2^16 bits, L = 6144 =
+// 8 x 8 x 8 x 12, inverse 3072 = 8 x 8 x 4 x 12) with compile-time
+// schedules at one 768-thread CTA per SM (4096 products: 1.45 -> 1.07 ms).
+__global__ void __launch_bounds__(768, 1)
+k_small_6144(SmallArgs a) {
+  small_product_body<768, 1, Sched<8, 8, 8, 12>, Sched<8, 8, 4, 12>>(a);
+}
+
 // Batches of products just above the single-product cutoff (L <= 12288, the
 // 2^17-bit range): one CTA per product at up to 768 threads.
 __global__ void __launch_bounds__(kSmallBatchMaxThreads, 1)
@@ -51,7 +109,7 @@ k_small_product_big(SmallArgs a) {
   small_product_body<kSmallBatchMaxThreads, 1>(a);
 }
 
-template <int MAXT, int MINB>
+template <int MAXT, int MINB, class SCF, class SCI>
 __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -150,7 +208,12 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
 
   // 4. forward FFT of z = a + i c, length L.
   LayRows lay1{1u, 0u};
-  fft_smem<false>(buf, lay1, a.fwd, tw, tid, nthr);
+  if constexpr (std::is_void<SCF>::value) {
+    fft_smem<false>(buf, lay1, a.fwd, tw, tid, nthr);
+  } else {
+    double2 xf[16];
+    small_ct_stages<false, SCF, 0, MAXT, 16>(xf, buf, tw, 1u, tid);
+  }
 
   // 5. spectral product: W_k = (Z_k + conj Z_-k)(Z_k - conj Z_-k)/(4i L),
   //    then Y_k = (W_k + W_{k+L/2}) + i e^{2 pi i k/L}(W_k - W_{k+L/2}).
@@ -175,7 +238,12 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
   __syncthreads();
 
   // 6. inverse FFT of length L/2: y_m = w_{2m} + i w_{2m+1}.
-  fft_smem<true>(buf, lay1, a.inv, tw, tid, nthr);
+  if constexpr (std::is_void<SCI>::value) {
+    fft_smem<true>(buf, lay1, a.inv, tw, tid, nthr);
+  } else {
+    double2 xi[16];
+    small_ct_stages<true, SCI, 0, MAXT, 16>(xi, buf, tw, 2u, tid);
+  }
 
   // 7. post-map and rounding.
   auto W = [&](int64_t j) {

@@ -47,6 +47,8 @@ size_t col_smem_bytes(uint32_t R, uint32_t c);
 __global__ void k_small_product(SmallArgs a);
 __global__ void k_small_product_2(SmallArgs a);  // <= 384 threads, 2 CTAs per SM
 __global__ void k_small_product_big(SmallArgs a);  // <= 768 threads (batched L <= 12288)
+// compile-time schedules for the full product at 2^16 bits (768 threads)
+__global__ void k_small_6144(SmallArgs a);
 
 // ---------------------------------------------------------------------------
 // Multi-pass pipeline.  The complex transform of length L = A * B * C runs as

@@ -525,3 +525,18 @@ def test_batched_graph_replay(ctx):
         assert not flags.any()
         for i in range(count):
             _check(tm.Mode.LOW, u[i], v[i], n, tm.from_limbs(out[i]))
+
+
+def test_batched_full_2p16_compiled_small_kernel(ctx):
+    """Full products of 2^16 bits (L = 6144) run the fused kernel with the
+    compile-time 8 x 8 x 8 x 12 schedule (k_small_6144); a batch is exact."""
+    n, count = 1 << 16, 64
+    nl = n // 64
+    w = port.mt19937_64(61, 2 * count * nl).reshape(count, 2, nl)
+    u, v = np.ascontiguousarray(w[:, 0, :]), np.ascontiguousarray(w[:, 1, :])
+    p = tm.select_params(n, tm.Mode.FULL)
+    out, flags = ctx.product_batched(p, u, v, return_flags=True)
+    assert ctx.last_stats.transform_length == 6144
+    assert not flags.any()
+    for i in range(count):
+        _check(tm.Mode.FULL, u[i], v[i], n, tm.from_limbs(out[i]))
