@@ -29,6 +29,7 @@ __device__ __forceinline__ uint64_t window_smem(const uint64_t* limbs,
 }
 
 constexpr int kMaxPer = 18;  // values per thread held across a barrier
+constexpr uint32_t kPreShift = kMaxLambda;  // > lambda - 1: digit slots above the pre-map outputs
 
 // Whole transform of length SC::R in shared memory (padded natural layout)
 // with a compile-time radix schedule: every stage's butterflies spread over
@@ -119,7 +120,9 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
   const int64_t N = mc.N;
 
   double2* buf = reinterpret_cast<double2*>(smem_raw);
-  uint64_t* ul = reinterpret_cast<uint64_t*>(buf + padded_len(uint32_t(L)));
+  // the transform, plus kPreShift slots: the truncated products' digits sit
+  // kPreShift slots up (see the pre-map below)
+  uint64_t* ul = reinterpret_cast<uint64_t*>(buf + padded_len(uint32_t(L) + kPreShift + 1));
   uint64_t* vl = ul + a.nlimbs;
   uint32_t* sw = reinterpret_cast<uint32_t*>(vl + a.nlimbs);  // 32 words
   double* sd = reinterpret_cast<double*>(sw + 32);             // scalars
@@ -168,7 +171,8 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
       double dv = double(split_digit(wv, cv, b, top || !mc.balanced));
       cu = mc.balanced ? tf_apply(split_tf(wu, b), cu) : 0;
       cv = mc.balanced ? tf_apply(split_tf(wv, b), cv) : 0;
-      if (j < L) buf[padidx(uint32_t(j))] = make_double2(du, dv);
+      if (j < L + (mc.mode != kModeFull ? 1 : 0))
+        buf[padidx(uint32_t(j + (mc.mode != kModeFull ? kPreShift : 0)))] = make_double2(du, dv);
       if (mc.mode == kModeHigh && top) {
         sd[0] = du;
         sd[1] = dv;
@@ -184,24 +188,23 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
   if (mc.mode != kModeFull) {
     if (mc.mode == kModeHigh && tid == 0) {
       double tu = sd[0], tv = sd[1];
-      auto Du = [&](int64_t i) { return buf[padidx(uint32_t(i))].x; };
-      auto Dv = [&](int64_t i) { return buf[padidx(uint32_t(i))].y; };
+      auto Du = [&](int64_t i) { return buf[padidx(uint32_t(i + kPreShift))].x; };
+      auto Dv = [&](int64_t i) { return buf[padidx(uint32_t(i + kPreShift))].y; };
       sd[2] = root_channel(mc, Du, tu) * root_channel(mc, Dv, tv);
     }
-    double2 nv[kMaxPer];
     const double tu = (mc.mode == kModeHigh) ? sd[0] : 0.0;
     const double tv = (mc.mode == kModeHigh) ? sd[1] : 0.0;
-    auto D2 = [&](int64_t i) { return buf[padidx(uint32_t(i))]; };
-#pragma unroll
-    for (int k = 0; k < kMaxPer; ++k) {
-      int64_t j = tid + int64_t(k) * nthr;
-      if (j < N) nv[k] = premap2(mc, D2, j, tu, tv);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kMaxPer; ++k) {
-      int64_t j = tid + int64_t(k) * nthr;
-      if (j < N) buf[padidx(uint32_t(j))] = nv[k];
+    // Digit i sits at slot i + kPreShift and z_j goes to slot j: output j
+    // reads slots j + 1 .. j + kPreShift (its cyclic wrap reads digits at or
+    // above N, which no output overwrites), so one pass of nthr outputs can
+    // write after a single barrier without clobbering what a later pass
+    // reads -- and no thread holds more than one output across it.
+    auto D2 = [&](int64_t i) { return buf[padidx(uint32_t(i + kPreShift))]; };
+    for (int64_t j0 = 0; j0 < N; j0 += nthr) {
+      const int64_t j = j0 + tid;
+      const double2 z = (j < N) ? premap2(mc, D2, j, tu, tv) : make_double2(0.0, 0.0);
+      __syncthreads();
+      if (j < N) buf[padidx(uint32_t(j))] = z;
     }
     __syncthreads();
   }

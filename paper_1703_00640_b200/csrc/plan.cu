@@ -596,7 +596,9 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
 }
 
 size_t small_smem_bytes(int64_t L, int64_t nlimbs) {
-  return size_t(padded_len(uint32_t(L))) * 16 + size_t(2 * nlimbs) * 8 + 32 * 4 + 8 * 8 +
+  // the transform plus kMaxLambda + 1 slots for the shifted digits (k_small.cu)
+  return size_t(padded_len(uint32_t(L) + kMaxLambda + 1)) * 16 + size_t(2 * nlimbs) * 8 + 32 * 4 +
+         8 * 8 +
          size_t(tw_smem_len(uint32_t(L))) * 16;
 }
 
