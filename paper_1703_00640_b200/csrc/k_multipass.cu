@@ -1,14 +1,20 @@
 // Multi-pass product pipeline for transform lengths beyond one CTA.
 //
-//   k_zgen        (k_zgen.cu) balanced split + pre-map, carry look-back
-//   k_f1          column DFTs over A of the pre-mapped coefficients, twiddle
-//   k_col         generic column pass (forward over B, inverse over B)
-//   k_mid         row DFTs over C for a conjugate row pair, spectral product,
-//                 half-length inverse row DFT, twiddle
-//   k_ilast       inverse column DFTs over A -> convolution coefficients
-//   k_carry       post-map, rounding tripwire, recombination lanes, carry
-//                 propagation (decoupled look-back), output limbs
-//   k_high_round  round(t / 2^s) of the high product (second carry scan)
+//   k_zstat/k_zgen (k_zgen.cu) balanced split + pre-map; carries composed
+//                 from per-block aggregates
+//   k_f1_ct       first column pass (DFTs over A of the pre-mapped
+//                 coefficients, output twiddle) with a compile-time schedule
+//                 for the hot column lengths; k_f1 / k_f1_pp otherwise
+//   k_col_ct      middle column passes of three-pass plans (over B, in
+//                 place); k_col / the ping-pong variants otherwise
+//   k_mid_4096    row DFTs over C = 4096 for a conjugate row pair, spectral
+//                 product and repack, half-length inverse, output twiddle
+//                 (persistent); k_mid for other row lengths
+//   k_ilast_ct    inverse column DFTs over A -> convolution coefficients;
+//                 k_ilast / k_ilast_pp otherwise
+//   k_carry       single-pass look-back carry (fallback; the default is
+//                 k_carry_lanes + k_carry_apply in k_carry2.cu)
+//   k_high_agg / k_high_round  round(t / 2^s) of the high product
 //
 // Reference path: products_f64.cpp:106-171 with the FFTW convolution of
 // convolution.cpp:175-195.
