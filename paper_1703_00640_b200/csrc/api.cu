@@ -534,17 +534,22 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         CarryLanesFn lanes = carry_lanes_kernel(lam, pt);
         set_smem(lanes, smem2);
         {
-          KTimer kt(cx, "k_carry_lanes", double(pl.K) * 8.0 + double(pl.ML) * 16.0, int(p.mode), st);
+          KTimer kt(cx, "k_carry_lanes",
+                    double(pl.K) * 8.0 + (hb ? double(pl.ML) * 16.0 : double(pl.out_limbs) * 8.0), int(p.mode), st);
           launch(lanes, dim3(blocks2), dim3(kC2Threads), smem2, st, a, "lanes");
         }
         check_launch("k_carry_lanes");
-        {
-          KTimer kt(cx, "k_carry_apply",
-                    double(pl.ML) * 16.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0,
-                    int(p.mode), st);
+        if (hb) {
+          KTimer kt(cx, "k_carry_apply", double(pl.ML) * 24.0, int(p.mode), st);
           launch(carry_apply_kernel(pt), dim3(blocks2), dim3(kC2Threads), 0, st, a, "apply");
+          check_launch("k_carry_apply");
+        } else {
+          // full, low: the lanes kernel wrote the limbs; one warp per block adds its carry-in
+          KTimer kt(cx, "k_carry_patch", 0.0, int(p.mode), st);
+          launch(carry_patch_kernel(pt), dim3((blocks2 + kC2Threads / 32 - 1) / (kC2Threads / 32)), dim3(kC2Threads), 0, st,
+                 a, "patch");
+          check_launch("k_carry_patch");
         }
-        check_launch("k_carry_apply");
         kernels += 2;
       } else {
         set_smem(k_carry, pl.smem_carry);

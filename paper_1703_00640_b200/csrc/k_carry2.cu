@@ -292,19 +292,49 @@ __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
   __syncthreads();
   if (tid > 0) hin = s_hi[tid - 1];
   uint32_t f = kTfIdentity;
+  uint32_t tfq[kPT];
   ulonglong2* sm = reinterpret_cast<ulonglong2*>(a.sbuf);
 #pragma unroll
   for (int q = 0; q < kPT; ++q) {
     const int64_t m = m0 + q;
+    tfq[q] = kTfIdentity;
     if (m < me) {
       const __int128 s = (__int128)lo[q] + (__int128)(q == 0 ? hin : hi[q - 1]);
-      f = tf_compose(f, limb_tf(s, flags));
-      sm[m] = make_ulonglong2((unsigned long long)s, (unsigned long long)(long long)(s >> 64));
+      tfq[q] = limb_tf(s, flags);
+      f = tf_compose(f, tfq[q]);
+      // full, low: lo keeps the low word of s for the output limbs below
+      lo[q] = (unsigned long long)s;
+      if (hmode) sm[m] = make_ulonglong2((unsigned long long)s, (unsigned long long)(long long)(s >> 64));
     }
   }
   uint32_t agg;
-  (void)block_scan_tf(f, sw, &agg);
+  const uint32_t ex = block_scan_tf(f, sw, &agg);
   if (tid == 0) a.aggs[blk] = agg;
+  if (!hmode) {
+    // full and low: the output limbs for a zero carry into the block (the
+    // limb is lo(s_m + c), the carry the limb's transfer function of c);
+    // k_carry_patch adds the carry-in of the blocks where it is not zero.
+    // The full product's limbs at and above out_limbs and its top carry
+    // go to scratch for the range checks.
+    int c = tf_apply(ex, 0);
+    const int64_t OL = a.out_limbs;
+    uint64_t* tail = reinterpret_cast<uint64_t*>(a.sbuf);
+#pragma unroll
+    for (int q = 0; q < kPT; ++q) {
+      const int64_t m = m0 + q;
+      if (m < me) {
+        const uint64_t x = lo[q] + uint64_t(int64_t(c));
+        c = tf_apply(tfq[q], c);
+        if (m < OL) {
+          a.out[m] = (mc.mode == kModeLow && m == OL - 1 && (a.n & 63)) ? (x & ((1ull << (a.n & 63)) - 1))
+                                                                         : x;
+        } else {
+          tail[m] = x;
+        }
+        if (m == a.ML - 1 && mc.mode == kModeFull) tail[a.ML] = uint64_t(int64_t(c));
+      }
+    }
+  }
   flags |= ra.all_flags();
   {
     const double e = warp_max_nonneg(ra.max_err), m = warp_max_nonneg(ra.max_abs);
@@ -453,6 +483,84 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
   }
 }
 
+// Full and low products: k_carry_lanes wrote every limb for a zero carry
+// into its block.  A carry-in d = +-1 adds d to a block's limbs from its
+// first limb up to and including the first one that does not wrap (old
+// value != ~0 for d = 1, != 0 for d = -1).  One warp per block finds that
+// limb 32 limbs at a time (a ballot) and updates the limbs below it.  The
+// update stops at the block end, since the next block's own carry-in already
+// counts a carry through this block.  For the full product the warps of the
+// blocks at and above limb out_limbs - 1 then run the range checks of the
+// recombined value (bits above 2n, the carry out of the top limb).
+template <int kPT>
+__global__ void __launch_bounds__(kC2Threads) k_carry_patch(CarryArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int64_t kLimbs = int64_t(kT) * kPT;
+  const int64_t nblk = (a.ML + kLimbs - 1) / kLimbs;
+  const int64_t blk = (int64_t(blockIdx.x) * kT + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (blk >= nblk) return;
+  const bool full = a.mc.mode == kModeFull;
+  const int64_t OL = a.out_limbs;
+  uint64_t* tail = reinterpret_cast<uint64_t*>(a.sbuf);
+  const int64_t ms = blk * kLimbs, me = min(a.ML, ms + kLimbs);
+  auto at = [&](int64_t m) -> uint64_t* { return m < OL ? a.out + m : tail + m; };
+  const int d = __ldg(a.cins + blk);
+  int64_t stop = ms;  // limbs [ms, stop) get d
+  if (d != 0) {
+    stop = me;
+    const uint64_t wraps = d > 0 ? ~0ull : 0ull;
+    // 4 x 32 limbs in flight per step: a run of wrapping limbs (the full
+    // product's zero limbs above the value) costs few round trips
+    for (int64_t base = ms; base < me; base += 128) {
+      uint64_t x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t m = base + 32 * u + lane;
+        x[u] = m < me ? *at(m) : wraps;
+      }
+      unsigned bal = 0;
+      int u = 0;
+#pragma unroll
+      for (; u < 4; ++u) {
+        bal = __ballot_sync(0xffffffffu, x[u] != wraps);
+        if (bal) break;
+      }
+      if (bal) {
+        stop = base + 32 * u + __ffs(bal);
+        break;
+      }
+    }
+    const int lowbits = int(a.n & 63);
+    for (int64_t m = ms + lane; m < stop; m += 32) {
+      if (!full && m >= OL) break;
+      uint64_t* p = at(m);
+      const uint64_t x = *p + uint64_t(int64_t(d));
+      *p = (!full && m == OL - 1 && lowbits) ? (x & ((1ull << lowbits) - 1)) : x;  // u v mod 2^n
+    }
+    __syncwarp();
+  }
+  if (!full || me <= OL - 1) return;
+  uint32_t flags = 0;
+  const int hb = int((2 * a.n) & 63);
+  for (int64_t m0 = max(ms, OL - 1) + lane; m0 < me; m0 += 256) {
+    uint64_t x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = m0 + 32 * u < me ? *at(m0 + 32 * u) : 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (m0 + 32 * u == OL - 1 ? (hb && (x[u] >> hb)) : x[u] != 0) flags |= kFlagFullOverflow;
+  }
+  if (blk == nblk - 1 && lane == 0) {
+    // sign of the recombined value: the carry out of the top limb
+    const int dend = (d != 0 && stop == me) ? d : 0;
+    if (int64_t(tail[a.ML]) + dend < 0) flags |= kFlagNegative;
+  }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (lane == 0 && flags) atomicOr(&a.status->flags, flags);
+}
+
 size_t carry2_smem(int b, int lam, int pt, bool /*hbuf: shares the coefficient slot*/) {
   const int64_t nk = (64 * int64_t(kC2Threads * pt + 1) + b - 1) / b + 4;
   return size_t(nk + lam + 8) * 8 + size_t(nk + 4) * 8 + 64;
@@ -475,5 +583,6 @@ CarryLanesFn lanes_pt(int lam) {
 
 CarryLanesFn carry_lanes_kernel(int lam, int pt) { return pt == 4 ? lanes_pt<4>(lam) : lanes_pt<2>(lam); }
 CarryLanesFn carry_apply_kernel(int pt) { return pt == 4 ? k_carry_apply<4> : k_carry_apply<2>; }
+CarryLanesFn carry_patch_kernel(int pt) { return pt == 4 ? k_carry_patch<4> : k_carry_patch<2>; }
 
 }  // namespace tmg

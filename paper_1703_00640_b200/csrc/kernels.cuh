@@ -232,6 +232,7 @@ constexpr int kC2Threads = 256;
 typedef void (*CarryLanesFn)(CarryArgs);
 CarryLanesFn carry_lanes_kernel(int lam, int pt);
 CarryLanesFn carry_apply_kernel(int pt);
+CarryLanesFn carry_patch_kernel(int pt);
 size_t carry2_smem(int b, int lam, int pt, bool hbuf);
 
 struct HighRoundArgs {

@@ -146,6 +146,25 @@ def test_structured_operands(ctx, n):
                 _check(mode, u, v, n, r)
 
 
+@pytest.mark.parametrize("n", [(1 << 20) + 3, 3 << 20])
+def test_carry_chains_across_blocks(esc_ctx, n):
+    """Products whose limbs hold long runs of zeros and all-ones: a carry
+    (or borrow) into a carry block walks through many limbs and across
+    blocks (k_carry_patch for full and low, k_carry_apply for high).  The
+    structured spectra may refuse at the policy's b: escalation recomputes."""
+    nl = (n + 63) // 64
+    M = (1 << n) - 1
+    rng = np.random.default_rng(11)
+    r0 = port.limbs_to_int(_rand(rng, n))
+    cases = [(M, M), (M, (1 << (n // 2)) + 1), ((1 << (n - 1)) + (1 << (n // 3)), M - M // 3),
+             (M, 1 << (n - 1)), (r0, M), (M ^ (1 << (n // 2)), M), ((1 << n) - (1 << 1000), M - 5)]
+    for a, b_ in cases:
+        u, v = port.int_to_limbs(a, nl), port.int_to_limbs(b_, nl)
+        for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+            r = tm.from_limbs(esc_ctx.product_limbs(mode, u, v, tm.select_params(n, mode)))
+            _check(mode, u, v, n, r)
+
+
 def test_unsigned_wide_chunks_trip(ctx):
     """test_products.cpp:408-416: b = 30 unsigned chunks overflow the exact
     integer range and must be refused."""
