@@ -97,9 +97,19 @@ __device__ __forceinline__ void coeffs_block(const CarryArgs& a, const double* _
     return (o >= 0 && o < nw) ? sww[o] : __ldg(a.w + j);
   };
   if constexpr (LAM == 0) {
-    const double* wk = sww + (kbase - wlo);
+    // no post-map: each coefficient is read once, straight from global
+    // memory (four loads in flight per thread)
+    const double* wk = a.w + kbase;
     const int32_t nk = int32_t(kend - kbase);
-    for (int32_t q = tid; q < nk; q += kT) se[q] = ra.round(wk[q]);
+    int32_t q = tid;
+    for (; q + 3 * kT < nk; q += 4 * kT) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(wk + q + u * kT);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) se[q + u * kT] = ra.round(v[u]);
+    }
+    for (; q < nk; q += kT) se[q] = ra.round(__ldg(wk + q));
   } else {
     // Blocks whose post-map inputs all lie in [0, N) away from the wrap
     // outputs (block-uniform) take the same arithmetic without bound checks,
@@ -227,7 +237,8 @@ __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
   const int64_t nwt = (mc.mode == kModeFull) ? K : mc.N;
   const int64_t wlo = max(int64_t(0), kbase - LAM - 1);
   const int64_t whi = min(nwt, kend + 2);
-  const int64_t nw = whi > wlo ? whi - wlo : 0;
+  // (the full product reads its coefficients once: no window)
+  const int64_t nw = (LAM > 0 && whi > wlo) ? whi - wlo : 0;
   double* sww = reinterpret_cast<double*>(smem_raw);
   // the high product's folded buffer hbuf takes the slot after the staged
   // window, and its rounded coefficients overwrite the window, which is dead
@@ -563,6 +574,7 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_patch(CarryArgs a) {
 
 size_t carry2_smem(int b, int lam, int pt, bool /*hbuf: shares the coefficient slot*/) {
   const int64_t nk = (64 * int64_t(kC2Threads * pt + 1) + b - 1) / b + 4;
+  if (lam == 0) return size_t(nk + 4) * 8 + 64;  // no staged window
   return size_t(nk + lam + 8) * 8 + size_t(nk + 4) * 8 + 64;
 }
 
