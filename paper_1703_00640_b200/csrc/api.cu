@@ -92,6 +92,8 @@ struct Workspace {
   }
 };
 constexpr int kMaxBatchStreams = 32;
+// k_carry_patch scans the carry aggregates itself up to this many carry blocks
+constexpr unsigned kPatchScanMaxBlocks = 4096;
 constexpr int64_t kGraphMinBatch = 4;  // batches replayed as graphs from this size
 
 struct Context {
@@ -476,8 +478,8 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       check_launch("k_ilast");
       ++kernels;
     }
-    // high: k_carry_apply finds the limb that stops the rounding increment
-    // (else k_high_agg does, after the single-pass k_carry)
+    // high: k_carry_lanes and k_carry_patch nominate the limb that stops the
+    // rounding increment (else k_high_agg does, after the single-pass k_carry)
     bool high_stop_fused = false;
     if (p.mode == PMode::kHigh && !w.hticket.p) {
       w.hticket.ensure(64);
@@ -531,23 +533,26 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         }
         a.ticket = w.ticket.as<uint32_t>();
         a.sbuf = w.work_t.p;  // the transform buffer is free after k_ilast
+        // k_carry_patch composes the block functions itself while that stays
+        // cheap (each patch CTA reads the aggregates before it); above, the
+        // last lanes block scans them into cins
+        // TMG_PATCH_SCAN_MAX (testing) overrides the limit
+        static const long patch_scan_max =
+            getenv("TMG_PATCH_SCAN_MAX") ? atol(getenv("TMG_PATCH_SCAN_MAX")) : long(kPatchScanMaxBlocks);
+        a.lanes_cins = long(blocks2) > patch_scan_max ? 1 : 0;
         CarryLanesFn lanes = carry_lanes_kernel(lam, pt);
         set_smem(lanes, smem2);
         {
-          KTimer kt(cx, "k_carry_lanes",
-                    double(pl.K) * 8.0 + (hb ? double(pl.ML) * 16.0 : double(pl.out_limbs) * 8.0), int(p.mode), st);
+          KTimer kt(cx, "k_carry_lanes", double(pl.K) * 8.0 + double(hb ? pl.ML : pl.out_limbs) * 8.0, int(p.mode),
+                    st);
           launch(lanes, dim3(blocks2), dim3(kC2Threads), smem2, st, a, "lanes");
         }
         check_launch("k_carry_lanes");
-        if (hb) {
-          KTimer kt(cx, "k_carry_apply", double(pl.ML) * 24.0, int(p.mode), st);
-          launch(carry_apply_kernel(pt), dim3(blocks2), dim3(kC2Threads), 0, st, a, "apply");
-          check_launch("k_carry_apply");
-        } else {
-          // full, low: the lanes kernel wrote the limbs; one warp per block adds its carry-in
+        {
+          // the lanes kernel wrote the limbs; one warp per block adds its carry-in
           KTimer kt(cx, "k_carry_patch", 0.0, int(p.mode), st);
-          launch(carry_patch_kernel(pt), dim3((blocks2 + kC2Threads / 32 - 1) / (kC2Threads / 32)), dim3(kC2Threads), 0, st,
-                 a, "patch");
+          launch(carry_patch_kernel(pt), dim3((blocks2 + kC2Threads / 32 - 1) / (kC2Threads / 32)), dim3(kC2Threads),
+                 0, st, a, "patch");
           check_launch("k_carry_patch");
         }
         kernels += 2;

@@ -8,12 +8,16 @@
 //                  them with the reference's tripwire, one coefficient per
 //                  thread and pass; each thread then forms the signed 128-bit
 //                  lanes lane_m = sum e_k << (k b - 64 m) of its PT limbs and
-//                  the limb sums s_m = lo(lane_m) + hi(lane_{m-1}), writes s_m
-//                  to scratch and the block's composed carry transfer
-//                  function to aggs[blk]; the last block to finish scans the
-//                  aggregates into every block's carry-in (cins).
-//   k_carry_apply  from the block's carry-in, a block scan of the limb
-//                  transfer functions and the output limbs.
+//                  the limb sums s_m = lo(lane_m) + hi(lane_{m-1}).  A block
+//                  scan of the limbs' carry transfer functions gives every
+//                  limb for a zero carry into the block, written to the
+//                  output (high: to t); the block's composed function goes
+//                  to aggs[blk].
+//   k_carry_patch  one warp per block: the block's carry-in (the composition
+//                  of the preceding blocks' functions) is added to its first
+//                  limbs, up to the first that does not wrap (usually one
+//                  limb), then the range checks and the high product's
+//                  stopping-limb nominations that read those limbs.
 //
 // Compared with the single-pass look-back kernel (k_carry), no block ever
 // waits on another: the lanes kernel runs at full occupancy and its
@@ -213,6 +217,34 @@ __device__ __forceinline__ void coeffs_block(const CarryArgs& a, const double* _
   }
 }
 
+// High product: limb m of t feeds w0_{m-q} (bits r..63) and w0_{m-q-1}
+// (bits 0..r-1) of w0 = t >> s, q = s / 64, r = s % 64; a limb nominates the
+// w0 limbs its bits prove not all ones (the first such limb stops the
+// rounding increment of k_high_round), and the limbs below bit s - 1 feed
+// the sticky bit.
+struct HighLimbs {
+  int64_t hq, WL, sb;
+  int hr;
+  __device__ explicit HighLimbs(const CarryArgs& a)
+      : hq(int64_t(a.shift_s) >> 6), WL(a.ML - (int64_t(a.shift_s) >> 6)), sb(a.shift_s - 1),
+        hr(int(a.shift_s & 63)) {}
+  __device__ __forceinline__ void see(int64_t m, uint64_t x, uint32_t& hmin, uint32_t& sticky) const {
+    if (hr == 0) {
+      if (x != ~0ull && m - hq >= 0) hmin = min(hmin, uint32_t(m - hq));
+    } else {
+      const uint64_t lowm = (1ull << hr) - 1;
+      if ((x >> hr) != (~0ull >> hr) && m - hq >= 0) hmin = min(hmin, uint32_t(m - hq));
+      if ((x & lowm) != lowm && m - hq - 1 >= 0 && m - hq - 1 < WL) hmin = min(hmin, uint32_t(m - hq - 1));
+    }
+    const int64_t bit0 = 64 * m;
+    if (bit0 + 64 <= sb) {
+      if (x) sticky = 1;
+    } else if (bit0 < sb) {
+      if (x & ((1ull << (sb - bit0)) - 1)) sticky = 1;
+    }
+  }
+};
+
 template <int LAM, int kPT>
 __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
   pdl_trigger();
@@ -262,8 +294,12 @@ __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
     }
     for (; o < nw32; o += kT) sww[o] = __ldg(wg + o);
   }
+  __shared__ uint32_t s_first, s_hmin, s_sticky;
   if (tid == 0) {
     s_flags = 0;
+    s_first = 0xffffffffu;
+    s_hmin = 0xffffffffu;
+    s_sticky = 0;
     // psi enters only x_N and the fold region k < nfold (delta+,
     // maps_f64.cpp:363-383): the first and the last block
     const bool need_psi = mc.mode == kModeHigh && (kbase < mc.nfold || kend > mc.N);
@@ -304,7 +340,6 @@ __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
   if (tid > 0) hin = s_hi[tid - 1];
   uint32_t f = kTfIdentity;
   uint32_t tfq[kPT];
-  ulonglong2* sm = reinterpret_cast<ulonglong2*>(a.sbuf);
 #pragma unroll
   for (int q = 0; q < kPT; ++q) {
     const int64_t m = m0 + q;
@@ -313,38 +348,44 @@ __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
       const __int128 s = (__int128)lo[q] + (__int128)(q == 0 ? hin : hi[q - 1]);
       tfq[q] = limb_tf(s, flags);
       f = tf_compose(f, tfq[q]);
-      // full, low: lo keeps the low word of s for the output limbs below
-      lo[q] = (unsigned long long)s;
-      if (hmode) sm[m] = make_ulonglong2((unsigned long long)s, (unsigned long long)(long long)(s >> 64));
+      lo[q] = (unsigned long long)s;  // the low word of s for the limbs below
     }
   }
   uint32_t agg;
   const uint32_t ex = block_scan_tf(f, sw, &agg);
   if (tid == 0) a.aggs[blk] = agg;
-  if (!hmode) {
-    // full and low: the output limbs for a zero carry into the block (the
-    // limb is lo(s_m + c), the carry the limb's transfer function of c);
-    // k_carry_patch adds the carry-in of the blocks where it is not zero.
-    // The full product's limbs at and above out_limbs and its top carry
-    // go to scratch for the range checks.
+  // The limbs for a zero carry into the block (the limb is lo(s_m + c), the
+  // carry the limb's transfer function of c); k_carry_patch adds the
+  // carry-in of the blocks where it is not zero.  The full product's limbs
+  // at and above out_limbs, and the top carry of the full and the high
+  // product, go to scratch for the range checks.
+  {
     int c = tf_apply(ex, 0);
     const int64_t OL = a.out_limbs;
-    uint64_t* tail = reinterpret_cast<uint64_t*>(a.sbuf);
+    uint64_t* tail = hmode ? a.tbuf : reinterpret_cast<uint64_t*>(a.sbuf);
+    uint32_t first = 0xffffffffu;
 #pragma unroll
     for (int q = 0; q < kPT; ++q) {
       const int64_t m = m0 + q;
       if (m < me) {
         const uint64_t x = lo[q] + uint64_t(int64_t(c));
         c = tf_apply(tfq[q], c);
-        if (m < OL) {
+        if (hmode) {
+          tail[m] = x;
+          lo[q] = x;
+          // a carry-in changes no limb above the first one that is neither
+          // 0 nor all ones
+          if (x + 1 > 1 && first == 0xffffffffu) first = uint32_t(m - ms);
+        } else if (m < OL) {
           a.out[m] = (mc.mode == kModeLow && m == OL - 1 && (a.n & 63)) ? (x & ((1ull << (a.n & 63)) - 1))
                                                                          : x;
         } else {
           tail[m] = x;
         }
-        if (m == a.ML - 1 && mc.mode == kModeFull) tail[a.ML] = uint64_t(int64_t(c));
+        if (m == a.ML - 1 && mc.mode != kModeLow) tail[a.ML] = uint64_t(int64_t(c));
       }
     }
+    if (hmode && first != 0xffffffffu) atomicMin(&s_first, first);
   }
   flags |= ra.all_flags();
   {
@@ -353,13 +394,42 @@ __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
   }
   if (flags) atomicOr(&s_flags, flags);
   // the last block to finish turns the per-block functions into each
-  // block's carry-in (one exclusive scan instead of a prefix per block)
+  // block's carry-in (one exclusive scan instead of a prefix per block);
+  // without lanes_cins, k_carry_patch composes them itself
   __shared__ uint32_t s_last;
   if (tid == 0) {
-    __threadfence();
-    s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    s_last = 0;
+    if (a.lanes_cins) {
+      __threadfence();
+      s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    }
   }
   __syncthreads();
+  if (hmode) {
+    // nominations and sticky bits of the limbs no carry-in can change (all
+    // of block 0's, which has none); k_carry_patch sees the others
+    const HighLimbs hl(a);
+    const int64_t mfix = blk == 0 ? ms : ms + int64_t(s_first) + 1;
+    uint32_t hmin = 0xffffffffu, sticky = 0;
+#pragma unroll
+    for (int q = 0; q < kPT; ++q) {
+      const int64_t m = m0 + q;
+      if (m < me && m >= mfix) hl.see(m, lo[q], hmin, sticky);
+    }
+    // w0's top limb has zero fill above bit 64 - r: never all ones
+    if (hl.hr != 0 && blk == 0 && tid == 0 && hl.WL > 0) hmin = min(hmin, uint32_t(hl.WL - 1));
+    hmin = __reduce_min_sync(0xffffffffu, hmin);
+    sticky = __reduce_or_sync(0xffffffffu, sticky);
+    if ((tid & 31) == 0) {
+      if (hmin != 0xffffffffu) atomicMin(&s_hmin, hmin);
+      if (sticky) s_sticky = 1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (s_hmin != 0xffffffffu) atomicMin(a.hstop, s_hmin);
+      if (s_sticky) atomicOr(&a.status->high_sticky, 1u);
+    }
+  }
   if (tid == 0) {
     // one status update per block
     double e = 0.0, m = 0.0;
@@ -389,120 +459,16 @@ __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
 
 }  // namespace
 
-template <int kPT>
-__global__ void __launch_bounds__(kC2Threads) k_carry_apply(CarryArgs a) {
-  pdl_trigger();
-  pdl_wait();
-  constexpr int64_t kLimbs = int64_t(kT) * kPT;
-  __shared__ uint32_t sw[32];
-  __shared__ uint32_t s_flags, s_low, s_hmin;
-  const int tid = threadIdx.x;
-  const MapConsts& mc = a.mc;
-  const int64_t blk = blockIdx.x;
-  const int64_t ms = blk * kLimbs;
-  const int64_t me = min(a.ML, ms + kLimbs);
-  if (tid == 0) {
-    s_flags = 0;
-    s_low = 0;
-    s_hmin = 0xffffffffu;
-  }
-  const int cin = __ldg(a.cins + blk);  // carry into the block (k_carry_lanes)
-  // limbs of this thread
-  const int64_t m0 = ms + int64_t(tid) * kPT;
-  const ulonglong2* sm = reinterpret_cast<const ulonglong2*>(a.sbuf);
-  __int128 s[kPT];
-  uint32_t flags = 0, f = kTfIdentity;
-#pragma unroll
-  for (int q = 0; q < kPT; ++q) {
-    const int64_t m = m0 + q;
-    s[q] = 0;
-    if (m < me) {
-      const ulonglong2 v = sm[m];
-      s[q] = (__int128)(long long)v.y * ((__int128)1 << 64) + (__int128)v.x;
-      f = tf_compose(f, limb_tf(s[q], flags));
-    }
-  }
-  uint32_t agg;
-  const uint32_t ex = block_scan_tf(f, sw, &agg);
-  int c = tf_apply(ex, cin);
-  const int64_t OL = a.out_limbs;
-  const int64_t sb = a.shift_s - 1;  // high: bit s-1
-  uint32_t sticky = 0;
-  // high: the first limb j of w0 = t >> s that is not all ones stops the
-  // rounding increment (k_high_round).  Limb m of t feeds w0_{m-q} (bits
-  // r..63) and w0_{m-q-1} (bits 0..r-1), q = s / 64, r = s % 64, so each
-  // limb nominates the w0 limbs its bits prove not all ones.
-  const int64_t hq = int64_t(a.shift_s) >> 6;
-  const int hr = int(a.shift_s & 63);
-  const int64_t WL = a.ML - hq;
-  uint32_t hmin = 0xffffffffu;
-#pragma unroll
-  for (int q = 0; q < kPT; ++q) {
-    const int64_t m = m0 + q;
-    if (m < me) {
-      const uint32_t tfm = limb_tf(s[q], flags);
-      const uint64_t x = (unsigned long long)(s[q] + c);
-      c = tf_apply(tfm, c);
-      if (mc.mode == kModeFull) {
-        const int64_t nb2 = 2 * a.n;
-        if (m < OL) {
-          if (m == OL - 1 && (nb2 & 63) && (x >> (nb2 & 63))) flags |= kFlagFullOverflow;
-          a.out[m] = x;
-        } else if (x) {
-          flags |= kFlagFullOverflow;
-        }
-      } else if (mc.mode == kModeLow) {
-        if (m < OL) a.out[m] = (m == OL - 1 && (a.n & 63)) ? (x & ((1ull << (a.n & 63)) - 1)) : x;
-      } else {
-        a.tbuf[m] = x;
-        if (hr == 0) {
-          if (x != ~0ull && m - hq >= 0) hmin = min(hmin, uint32_t(m - hq));
-        } else {
-          const uint64_t lowm = (1ull << hr) - 1;
-          if ((x >> hr) != (~0ull >> hr) && m - hq >= 0) hmin = min(hmin, uint32_t(m - hq));
-          if ((x & lowm) != lowm && m - hq - 1 >= 0 && m - hq - 1 < WL)
-            hmin = min(hmin, uint32_t(m - hq - 1));
-        }
-        const int64_t bit0 = 64 * m;
-        if (bit0 + 64 <= sb) {
-          if (x) sticky = 1;
-        } else if (bit0 < sb) {
-          if (x & ((1ull << (sb - bit0)) - 1)) sticky = 1;
-        }
-      }
-      if (m == a.ML - 1 && c < 0) {
-        // sign of the recombined value (carry out of the top limb)
-        if (mc.mode == kModeFull) flags |= kFlagNegative;
-        if (mc.mode == kModeHigh) flags |= kFlagHighRange;
-      }
-    }
-  }
-  if (sticky) atomicOr(&s_low, 1u);
-  if (flags) atomicOr(&s_flags, flags);
-  if (mc.mode == kModeHigh) {
-    // w0's top limb has zero fill above bit 64 - r: never all ones
-    if (hr != 0 && blk == 0 && tid == 0 && WL > 0) hmin = min(hmin, uint32_t(WL - 1));
-    hmin = __reduce_min_sync(0xffffffffu, hmin);
-    if ((tid & 31) == 0 && hmin != 0xffffffffu) atomicMin(&s_hmin, hmin);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    if (s_flags) atomicOr(&a.status->flags, s_flags);
-    if (s_low) atomicOr(&a.status->high_sticky, 1u);
-    // one global update per block
-    if (mc.mode == kModeHigh && s_hmin != 0xffffffffu) atomicMin(a.hstop, s_hmin);
-  }
-}
-
-// Full and low products: k_carry_lanes wrote every limb for a zero carry
-// into its block.  A carry-in d = +-1 adds d to a block's limbs from its
-// first limb up to and including the first one that does not wrap (old
-// value != ~0 for d = 1, != 0 for d = -1).  One warp per block finds that
-// limb 32 limbs at a time (a ballot) and updates the limbs below it.  The
-// update stops at the block end, since the next block's own carry-in already
-// counts a carry through this block.  For the full product the warps of the
-// blocks at and above limb out_limbs - 1 then run the range checks of the
-// recombined value (bits above 2n, the carry out of the top limb).
+// k_carry_lanes wrote every limb for a zero carry into its block.  A
+// carry-in d = +-1 adds d to a block's limbs from its first limb up to and
+// including the first one that does not wrap (old value != ~0 for d = 1,
+// != 0 for d = -1).  One warp per block finds that limb 32 limbs at a time
+// (a ballot) and updates the limbs below it.  The update stops at the block
+// end, since the next block's own carry-in already counts a carry through
+// this block.  Then the checks that read the final limbs: the full
+// product's range (bits above 2n, carry out of the top limb), and the high
+// product's nominations and sticky bits of the limbs k_carry_lanes left out
+// (up to the first one that is neither 0 nor all ones) and its range.
 template <int kPT>
 __global__ void __launch_bounds__(kC2Threads) k_carry_patch(CarryArgs a) {
   pdl_trigger();
@@ -511,16 +477,39 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_patch(CarryArgs a) {
   const int64_t nblk = (a.ML + kLimbs - 1) / kLimbs;
   const int64_t blk = (int64_t(blockIdx.x) * kT + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (blk >= nblk) return;
-  const bool full = a.mc.mode == kModeFull;
-  const int64_t OL = a.out_limbs;
-  uint64_t* tail = reinterpret_cast<uint64_t*>(a.sbuf);
+  int d;
+  if (a.lanes_cins) {
+    if (blk >= nblk) return;
+    d = __ldcg(a.cins + blk);
+  } else {
+    // carry-in: the composition of the preceding blocks' functions, the
+    // CTA's prefix by a block scan, then the warp's own few
+    __shared__ uint32_t sw[32];
+    const uint32_t b0 = blockIdx.x * (kT / 32);
+    const uint32_t Q = (b0 + kT - 1) / kT;
+    const uint32_t i0 = min(b0, uint32_t(threadIdx.x) * Q), i1 = min(b0, i0 + Q);
+    uint32_t g = kTfIdentity;
+    for (uint32_t i = i0; i < i1; ++i) g = tf_compose(g, __ldcg(a.aggs + i));
+    uint32_t pre;
+    (void)block_scan_tf(g, sw, &pre);
+    if (blk >= nblk) return;
+    for (uint32_t i = b0; i < uint32_t(blk); ++i) pre = tf_compose(pre, __ldcg(a.aggs + i));
+    d = tf_apply(pre, 0);
+  }
+  const int mode = a.mc.mode;
+  const bool full = mode == kModeFull, low = mode == kModeLow, high = mode == kModeHigh;
+  // full, low: limbs below out_limbs are in the output, the rest (full) in
+  // scratch; high: all in tbuf
+  const int64_t OL = a.out_limbs, OLx = high ? 0 : OL;
+  uint64_t* tail = high ? a.tbuf : reinterpret_cast<uint64_t*>(a.sbuf);
   const int64_t ms = blk * kLimbs, me = min(a.ML, ms + kLimbs);
-  auto at = [&](int64_t m) -> uint64_t* { return m < OL ? a.out + m : tail + m; };
-  const int d = __ldg(a.cins + blk);
-  int64_t stop = ms;  // limbs [ms, stop) get d
-  if (d != 0) {
+  auto at = [&](int64_t m) -> uint64_t* { return m < OLx ? a.out + m : tail + m; };
+  // high: the limbs [ms, mhi] are those k_carry_lanes did not see
+  const bool hsee = high && blk > 0;
+  int64_t stop = ms, mhi = me - 1;  // limbs [ms, stop) get d
+  if (d != 0 || hsee) {
     stop = me;
+    bool have_stop = d == 0;
     const uint64_t wraps = d > 0 ? ~0ull : 0ull;
     // 4 x 32 limbs in flight per step: a run of wrapping limbs (the full
     // product's zero limbs above the value) costs few round trips
@@ -531,26 +520,59 @@ __global__ void __launch_bounds__(kC2Threads) k_carry_patch(CarryArgs a) {
         const int64_t m = base + 32 * u + lane;
         x[u] = m < me ? *at(m) : wraps;
       }
-      unsigned bal = 0;
-      int u = 0;
+      bool done = false;
 #pragma unroll
-      for (; u < 4; ++u) {
-        bal = __ballot_sync(0xffffffffu, x[u] != wraps);
-        if (bal) break;
+      for (int u = 0; u < 4; ++u) {
+        if (!have_stop) {
+          const unsigned bal = __ballot_sync(0xffffffffu, x[u] != wraps);
+          if (bal) {
+            stop = base + 32 * u + __ffs(bal);
+            have_stop = true;
+          }
+        }
+        if (hsee) {
+          const unsigned bal = __ballot_sync(0xffffffffu, x[u] + 1 > 1 && base + 32 * u + lane < me);
+          if (bal) {
+            mhi = base + 32 * u + __ffs(bal) - 1;
+            done = true;
+            break;
+          }
+        } else if (have_stop) {
+          done = true;
+          break;
+        }
       }
-      if (bal) {
-        stop = base + 32 * u + __ffs(bal);
-        break;
+      if (done) break;
+    }
+    if (d != 0) {
+      const int lowbits = int(a.n & 63);
+      for (int64_t m = ms + lane; m < stop; m += 32) {
+        if (low && m >= OL) break;
+        uint64_t* p = at(m);
+        const uint64_t x = *p + uint64_t(int64_t(d));
+        *p = (low && m == OL - 1 && lowbits) ? (x & ((1ull << lowbits) - 1)) : x;  // u v mod 2^n
       }
+      __syncwarp();
     }
-    const int lowbits = int(a.n & 63);
-    for (int64_t m = ms + lane; m < stop; m += 32) {
-      if (!full && m >= OL) break;
-      uint64_t* p = at(m);
-      const uint64_t x = *p + uint64_t(int64_t(d));
-      *p = (!full && m == OL - 1 && lowbits) ? (x & ((1ull << lowbits) - 1)) : x;  // u v mod 2^n
+  }
+  if (high) {
+    uint32_t flags = 0, hmin = 0xffffffffu, sticky = 0;
+    if (hsee) {
+      const HighLimbs hl(a);
+      for (int64_t m = ms + lane; m <= mhi; m += 32) hl.see(m, tail[m], hmin, sticky);
+      hmin = __reduce_min_sync(0xffffffffu, hmin);
+      sticky = __reduce_or_sync(0xffffffffu, sticky);
     }
-    __syncwarp();
+    if (blk == nblk - 1 && lane == 0) {
+      const int dend = (d != 0 && stop == me) ? d : 0;
+      if (int64_t(tail[a.ML]) + dend < 0) flags |= kFlagHighRange;  // sign of t
+    }
+    if (lane == 0) {
+      if (hmin < __ldcg(a.hstop)) atomicMin(a.hstop, hmin);
+      if (sticky) atomicOr(&a.status->high_sticky, 1u);
+      if (flags) atomicOr(&a.status->flags, flags);
+    }
+    return;
   }
   if (!full || me <= OL - 1) return;
   uint32_t flags = 0;
@@ -594,7 +616,6 @@ CarryLanesFn lanes_pt(int lam) {
 }
 
 CarryLanesFn carry_lanes_kernel(int lam, int pt) { return pt == 4 ? lanes_pt<4>(lam) : lanes_pt<2>(lam); }
-CarryLanesFn carry_apply_kernel(int pt) { return pt == 4 ? k_carry_apply<4> : k_carry_apply<2>; }
 CarryLanesFn carry_patch_kernel(int pt) { return pt == 4 ? k_carry_patch<4> : k_carry_patch<2>; }
 
 }  // namespace tmg

@@ -13,7 +13,7 @@
 //   k_ilast_ct    inverse column DFTs over A -> convolution coefficients;
 //                 k_ilast / k_ilast_pp otherwise
 //   k_carry       single-pass look-back carry (fallback; the default is
-//                 k_carry_lanes + k_carry_apply in k_carry2.cu)
+//                 k_carry_lanes + k_carry_patch in k_carry2.cu)
 //   k_high_agg / k_high_round  round(t / 2^s) of the high product
 //
 // Reference path: products_f64.cpp:106-171 with the FFTW convolution of
@@ -1245,7 +1245,7 @@ __device__ __forceinline__ uint64_t high_shifted(const HighRoundArgs& a, int64_t
 
 // The first limb of w0 = t >> s that is not all ones (atomicMin into
 // ticket[1]): the limb that stops the rounding increment.  The two-kernel
-// carry path computes it in k_carry_apply; this kernel serves the
+// carry path computes it in k_carry_lanes / k_carry_patch; this kernel serves the
 // single-pass k_carry path.
 __global__ void __launch_bounds__(kCarryThreads)
 k_high_agg(HighRoundArgs a) {
@@ -1262,7 +1262,7 @@ k_high_agg(HighRoundArgs a) {
 }
 
 // w = w0 + inc: the increment enters limb 0 and carries through the all-ones
-// limbs below the first stopping limb f (k_high_agg / k_carry_apply), so
+// limbs below the first stopping limb f (k_high_agg / k_carry_lanes + k_carry_patch), so
 // limb j adds inc exactly when j <= f.
 __global__ void __launch_bounds__(kCarryThreads)
 k_high_round(HighRoundArgs a) {

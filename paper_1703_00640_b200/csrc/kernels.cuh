@@ -223,6 +223,7 @@ struct CarryArgs {
   uint32_t* ticket; // completion counter of k_carry_lanes (zero between launches)
   FastDiv fb;       // division by b
   uint32_t* hstop;  // high: first limb of t >> s that is not all ones (atomicMin; ~0 before)
+  int32_t lanes_cins; // 1: the last k_carry_lanes block writes cins; 0: k_carry_patch scans aggs
 };
 constexpr int kCarryThreads = 256;
 constexpr int kCarryPerThread = 2;
@@ -231,7 +232,6 @@ size_t carry_smem(int b);
 constexpr int kC2Threads = 256;
 typedef void (*CarryLanesFn)(CarryArgs);
 CarryLanesFn carry_lanes_kernel(int lam, int pt);
-CarryLanesFn carry_apply_kernel(int pt);
 CarryLanesFn carry_patch_kernel(int pt);
 size_t carry2_smem(int b, int lam, int pt, bool hbuf);
 

@@ -517,6 +517,34 @@ def test_generic_passes_at_compiled_lengths():
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
 
+_CARRY_SNIPPET = """
+import sys
+sys.path.insert(0, '.')
+import paper_1703_00640_b200 as tm
+from oracle import port
+ctx = tm.Context(0)
+for n in (1 << 20, (1 << 22) + 448):
+    u, v = port.config_operands(3, (n + 63) // 64)
+    P = port.limbs_to_int(port.oracle_full(u, v))
+    assert tm.from_limbs(ctx.product_limbs(tm.Mode.FULL, u, v, tm.select_params(n, tm.Mode.FULL))) == P
+    assert tm.from_limbs(ctx.product_limbs(tm.Mode.LOW, u, v, tm.select_params(n, tm.Mode.LOW))) == P % (1 << n)
+print("ok")
+"""
+
+
+def test_carry_in_from_the_lanes_ticket():
+    """TMG_PATCH_SCAN_MAX=0: full and low products take the carry-ins the
+    last k_carry_lanes block scans (the path above 4096 carry blocks, n >~
+    2^27) instead of k_carry_patch's own scan; both must be exact."""
+    import subprocess
+    import sys
+    env = dict(os.environ, TMG_PATCH_SCAN_MAX="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _CARRY_SNIPPET], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
 def test_batched_graph_replay(ctx):
     """Repeated multi-pass batch shapes run eagerly, then are captured, then
     replayed as a CUDA graph; every call uploads new operands into the same
