@@ -25,7 +25,7 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1
 res, order, mode = {}, ["full", "low", "high"], -1
 for r in rows[2:]:
     name = r[ki]
-    base = re.sub(r"^void ", "", name).replace("<unnamed>::", "").replace("(anonymous namespace)::", "").split("(")[0]
+    base = re.sub(r"^void ", "", name).replace("<unnamed>::", "").replace("unnamed>::", "").replace("(anonymous namespace)::", "").split("(")[0]
     base = re.sub(r"^(\w+::)*", "", base.split("<")[0]) if "<" in base else re.sub(r"^(\w+::)*", "", base)
     if base == "k_zstat":
         mode += 1
