@@ -217,6 +217,31 @@ __device__ __forceinline__ void coeffs_block(const CarryArgs& a, const double* _
   }
 }
 
+// Bulk global -> shared copy completing on an mbarrier (cp.async.bulk; the
+// sizes and addresses are multiples of 16 bytes).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  const uint32_t a = uint32_t(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  const uint32_t a = uint32_t(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  const uint32_t d = uint32_t(__cvta_generic_to_shared(dst));
+  const uint32_t b = uint32_t(__cvta_generic_to_shared(bar));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = uint32_t(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "MBW%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MBW%=;\n}" ::"r"(a), "r"(phase) : "memory");
+}
+
 // High product: limb m of t feeds w0_{m-q} (bits r..63) and w0_{m-q-1}
 // (bits 0..r-1) of w0 = t >> s, q = s / 64, r = s % 64; a limb nominates the
 // w0 limbs its bits prove not all ones (the first such limb stops the
@@ -266,9 +291,11 @@ __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
   const int64_t kbase = kfirst(ms > 0 ? ms - 1 : 0, a.fb, K);
   const int64_t kend = kfirst(me, a.fb, K);
   // staged convolution window (post-map neighbourhood: lambda below, one above)
+  // (16-byte aligned ends for the bulk copy; w holds L >= nwt + 1 values
+  // when nwt is odd, since L is even)
   const int64_t nwt = (mc.mode == kModeFull) ? K : mc.N;
-  const int64_t wlo = max(int64_t(0), kbase - LAM - 1);
-  const int64_t whi = min(nwt, kend + 2);
+  const int64_t wlo = max(int64_t(0), kbase - LAM - 1) & ~int64_t(1);
+  const int64_t whi = (min(nwt, kend + 2) + 1) & ~int64_t(1);
   // (the full product reads its coefficients once: no window)
   const int64_t nw = (LAM > 0 && whi > wlo) ? whi - wlo : 0;
   double* sww = reinterpret_cast<double*>(smem_raw);
@@ -279,20 +306,13 @@ __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
   const bool hmode = mc.mode == kModeHigh;
   long long* se = hmode ? reinterpret_cast<long long*>(sww)
                         : reinterpret_cast<long long*>(sww + (nw + 1));
-  {
-    // all loads of a thread in flight before the stores
-    constexpr int U = 8;
-    const double* wg = a.w + wlo;
-    const int32_t nw32 = int32_t(nw);
-    int32_t o = tid;
-    for (; o + (U - 1) * kT < nw32; o += U * kT) {
-      double v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = __ldg(wg + o + u * kT);
-#pragma unroll
-      for (int u = 0; u < U; ++u) sww[o + u * kT] = v[u];
-    }
-    for (; o < nw32; o += kT) sww[o] = __ldg(wg + o);
+  // the window arrives by one bulk copy (TMA engine) on an mbarrier, issued
+  // before the block's set-up so the two overlap
+  __shared__ __align__(8) uint64_t s_mbar;
+  if (tid == 0 && nw > 0) {
+    mbar_init(&s_mbar, 1);
+    mbar_expect_tx(&s_mbar, uint32_t(nw * 8));
+    bulk_g2s(sww, a.w + wlo, uint32_t(nw * 8), &s_mbar);
   }
   __shared__ uint32_t s_first, s_hmin, s_sticky;
   if (tid == 0) {
@@ -306,6 +326,7 @@ __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
     s_psi = need_psi ? high_psi(mc, [&](int64_t j) { return __ldg(a.w + j); }, a.aux[0]) : 0.0;
   }
   __syncthreads();
+  if (nw > 0) mbar_wait(&s_mbar, 0);
   RoundAcc ra;
   uint32_t flags = 0;
   const int64_t m0 = ms + int64_t(tid) * kPT;
