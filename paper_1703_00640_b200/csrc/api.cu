@@ -145,6 +145,17 @@ struct Context {
   }
   int32_t last_kernels = 0;
   int64_t last_L = 0;
+  // Output bytes of the products enqueued on the stream since it was last
+  // synchronized, as one address range: k_zstat reads its operands before
+  // waiting for its predecessor (programmatic launch) only when they lie
+  // outside it, since kernels of earlier products may still be writing there
+  // (device-pointer products chained output -> input).
+  uintptr_t out_lo = UINTPTR_MAX, out_hi = 0;
+  bool zstat_early = false;
+  void drained() {
+    out_lo = UINTPTR_MAX;
+    out_hi = 0;
+  }
   int32_t last_passes = 0;
 
   Plan& plan_for(const Params& p) {
@@ -323,6 +334,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.status = status;
       w.zaggs.ensure(size_t(blocks) * 4 + 16);
       a.aggs = w.zaggs.as<uint32_t>();
+      a.early = cx.zstat_early ? 1 : 0;
       {
         KTimer kt(cx, "k_zstat", double(2 * pl.nlimbs) * 8.0, int(p.mode), st);
         launch(k_zstat, dim3((blocks + 255) / 256), dim3(256), 0, st, a, "zstat");
@@ -606,6 +618,20 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
   const Params& p = pl.params;
   cudaStream_t st = cx.stream;
   DevStatus* status = cx.status.as<DevStatus>();
+  {
+    const uintptr_t ol = reinterpret_cast<uintptr_t>(dout);
+    const uintptr_t oh = ol + uintptr_t(count * pl.out_limbs) * 8;
+    cx.out_lo = std::min(cx.out_lo, ol);
+    cx.out_hi = std::max(cx.out_hi, oh);
+    const uintptr_t ob = uintptr_t(count * pl.nlimbs) * 8;
+    auto clear = [&](const uint64_t* x) {
+      const uintptr_t xl = reinterpret_cast<uintptr_t>(x);
+      return xl + ob <= cx.out_lo || xl >= cx.out_hi;
+    };
+    // TMG_ZSTAT_EARLY (testing): 1 always reads early (unsafe for chains), 0 never
+    static const int force_early = getenv("TMG_ZSTAT_EARLY") ? atoi(getenv("TMG_ZSTAT_EARLY")) : -1;
+    cx.zstat_early = force_early >= 0 ? force_early == 1 : (clear(du) && clear(dv));
+  }
   cx.last_L = pl.L;
   cx.last_passes = pl.kind;
   if (pl.kind == 0)
@@ -777,6 +803,7 @@ int finish(Context& cx, const Plan* pl, tmg_stats* stats) {
   TMG_CUDA(cudaMemcpyAsync(cx.h_status, cx.status.p, sizeof(DevStatus),
                            cudaMemcpyDeviceToHost, cx.stream));
   TMG_CUDA(cudaStreamSynchronize(cx.stream));
+  cx.drained();
   DevStatus s = *cx.h_status;
   double e, m;
   std::memcpy(&e, &s.max_err_bits, 8);
@@ -890,6 +917,7 @@ int host_product_once(Context& cx, const Params& p, int32_t want_mode,
     std::vector<uint64_t> h(size_t(count * 2 * nl));
     TMG_CUDA(cudaMemcpyAsync(h.data(), prod.p, h.size() * 8, cudaMemcpyDeviceToHost, cx.stream));
     TMG_CUDA(cudaStreamSynchronize(cx.stream));
+    cx.drained();
     cx.last_kernels = int32_t(count);
     cx.last_L = 0;
     cx.last_passes = 0;
@@ -1053,7 +1081,7 @@ int tmg_context_create(int device, tmg_context** out) {
 void tmg_context_destroy(tmg_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->cx.device);
-  cudaStreamSynchronize(ctx->cx.stream);
+  if (cudaStreamSynchronize(ctx->cx.stream) == cudaSuccess) ctx->cx.drained();
   if (ctx->cx.own_stream && ctx->cx.stream) cudaStreamDestroy(ctx->cx.stream);
   if (ctx->cx.h_status) cudaFreeHost(ctx->cx.h_status);
   delete ctx;
@@ -1071,6 +1099,7 @@ int tmg_context_set_stream(tmg_context* ctx, void* stream) {
 int tmg_synchronize(tmg_context* ctx) {
   return guarded([&] {
     TMG_CUDA(cudaStreamSynchronize(ctx->cx.stream));
+    ctx->cx.drained();
     return TMG_OK;
   });
 }
@@ -1175,6 +1204,7 @@ int tmg_debug_read(tmg_context* ctx, int which, void* host, size_t* bytes) {
     *bytes = std::min(*bytes, B.bytes);
     TMG_CUDA(cudaMemcpyAsync(host, B.p, *bytes, cudaMemcpyDeviceToHost, cx.stream));
     TMG_CUDA(cudaStreamSynchronize(cx.stream));
+    cx.drained();
     return TMG_OK;
   });
 }
@@ -1191,6 +1221,7 @@ int tmg_profile_read(tmg_context* ctx, char* names, int name_stride, double* ms,
   return guarded([&] {
     Profiler& P = ctx->cx.prof;
     TMG_CUDA(cudaStreamSynchronize(ctx->cx.stream));
+    ctx->cx.drained();
     int n = 0;
     for (auto& r : P.recs) {
       if (n < max_records) {

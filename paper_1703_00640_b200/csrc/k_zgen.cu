@@ -96,7 +96,10 @@ k_zstat(ZgenArgs a) {
   // runs under the predecessor's tail and waits for it at the end instead:
   // its completion still implies the predecessor's, which keeps the
   // programmatic-launch chain intact for k_zgen and everything after it.
+  // When the operands may be outputs of products still in flight on the
+  // stream (a.early = 0, decided by the host), it waits first.
   pdl_trigger();
+  if (!a.early) pdl_wait();
   const int64_t blk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t count = a.count;
   const int64_t nblk = (count + kZgenChunks - 1) / kZgenChunks;

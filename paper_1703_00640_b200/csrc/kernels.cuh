@@ -105,6 +105,7 @@ struct ZgenArgs {
   DevStatus* status;
   uint32_t* aggs;  // per-block carry transfer functions (k_zstat)
   ZTile zt;        // layout of z as k_f1 reads it
+  int32_t early;   // k_zstat: operands not written by in-flight kernels (read before pdl_wait)
 };
 constexpr int kZgenThreads = 256;
 constexpr int kZgenPer = 16;

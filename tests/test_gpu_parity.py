@@ -241,6 +241,53 @@ def test_device_path_matches_host_path(ctx):
     assert np.array_equal(out.cpu().numpy().view(np.uint64), host)
 
 
+_CHAIN_SNIPPET = """
+import sys
+sys.path.insert(0, '.')
+import numpy as np
+import torch
+import paper_1703_00640_b200 as tm
+from oracle import port
+ctx = tm.Context(0)
+bad = 0
+for n in (1 << 20, 1 << 22):
+    nl = n // 64
+    rng = np.random.default_rng(n)
+    p = tm.select_params(n, tm.Mode.LOW)
+    for rep in range(4):
+        a = rng.integers(0, 2**64, nl, dtype=np.uint64)
+        b = rng.integers(0, 2**64, nl, dtype=np.uint64)
+        bufs = [torch.from_numpy(x.view(np.int64)).cuda() for x in (a, b)]
+        bufs += [torch.zeros(nl, dtype=torch.int64, device="cuda") for _ in range(6)]
+        torch.cuda.synchronize()
+        # x_{k+2} = x_k x_{k+1} mod 2^n, each product reading the previous outputs
+        for k in range(6):
+            ctx.product_device(p, bufs[k].data_ptr(), bufs[k + 1].data_ptr(), bufs[k + 2].data_ptr(), 1)
+        ctx.check()
+        M = (1 << n) - 1
+        xs = [port.limbs_to_int(a), port.limbs_to_int(b)]
+        for k in range(6):
+            xs.append(xs[k] * xs[k + 1] & M)
+        got = [port.limbs_to_int(t.cpu().numpy().view(np.uint64)) for t in bufs]
+        bad += sum(g != x for g, x in zip(got, xs))
+print("bad", bad)
+print("ok" if bad == 0 else "mismatch")
+"""
+
+
+def test_chained_device_products():
+    """Device-pointer products chained output -> input on one stream with no
+    synchronisation in between: each product's operands are the previous
+    ones' outputs, which kernels still in flight may be writing, so k_zstat
+    must not read them before its predecessor completes."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _CHAIN_SNIPPET], cwd=root, env=dict(os.environ),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-500:] + r.stderr[-2000:]
+
+
 # --------------------------------------------------------------------------
 # BASELINE.json configurations
 
