@@ -212,9 +212,12 @@ bool pdl_skip(const char* site) {
   return list.find(std::string(",") + site + ",") != std::string::npos;
 }
 
+// Kernels without griddepcontrol.wait (the fused small-product kernels) go
+// out with pdl = false: launched programmatically they could start under a
+// predecessor that triggered early and read its unfinished outputs.
 template <class Arg>
 void launch(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-            const Arg& arg, const char* site = nullptr) {
+            const Arg& arg, const char* site = nullptr, bool pdl = true) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -222,7 +225,7 @@ void launch(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = (g_pdl && !pdl_skip(site)) ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = (pdl && g_pdl && !pdl_skip(site)) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   TMG_CUDA(cudaLaunchKernelEx(&cfg, kernel, arg));
@@ -675,7 +678,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     set_smem(sk, pl.small_smem);
     {
       KTimer kt(cx, "k_small_product", double(count) * double(2 * pl.nlimbs + pl.out_limbs) * 8.0, int(p.mode));
-      launch(sk, dim3(unsigned(count)), dim3(threads), pl.small_smem, st, a, "small");
+      launch(sk, dim3(unsigned(count)), dim3(threads), pl.small_smem, st, a, "small", false);
     }
     check_launch("k_small_product");
     cx.last_kernels = 1;

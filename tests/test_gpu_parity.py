@@ -270,6 +270,28 @@ for n in (1 << 20, 1 << 22):
             xs.append(xs[k] * xs[k + 1] & M)
         got = [port.limbs_to_int(t.cpu().numpy().view(np.uint64)) for t in bufs]
         bad += sum(g != x for g, x in zip(got, xs))
+# a multi-pass product, then fused small products reading its output
+n1, n2 = 1 << 20, 1 << 16
+p1, p2 = tm.select_params(n1, tm.Mode.LOW), tm.select_params(n2, tm.Mode.LOW)
+rng = np.random.default_rng(5)
+for rep in range(4):
+    a = rng.integers(0, 2**64, n1 // 64, dtype=np.uint64)
+    b = rng.integers(0, 2**64, n1 // 64, dtype=np.uint64)
+    da, db = (torch.from_numpy(x.view(np.int64)).cuda() for x in (a, b))
+    o1 = torch.zeros(n1 // 64, dtype=torch.int64, device="cuda")
+    o2 = torch.zeros(n2 // 64, dtype=torch.int64, device="cuda")
+    o3 = torch.zeros(n2 // 64, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    ctx.product_device(p1, da.data_ptr(), db.data_ptr(), o1.data_ptr(), 1)
+    ctx.product_device(p2, o1.data_ptr(), db.data_ptr(), o2.data_ptr(), 1)
+    ctx.product_device(p2, o2.data_ptr(), o1.data_ptr(), o3.data_ptr(), 1)
+    ctx.check()
+    x1 = port.limbs_to_int(a) * port.limbs_to_int(b) % (1 << n1)
+    m2 = (1 << n2) - 1
+    x2 = (x1 & m2) * (port.limbs_to_int(b) & m2) & m2
+    x3 = x2 * (x1 & m2) & m2
+    got = [port.limbs_to_int(t.cpu().numpy().view(np.uint64)) for t in (o1, o2, o3)]
+    bad += sum(g != x for g, x in zip(got, (x1, x2, x3)))
 print("bad", bad)
 print("ok" if bad == 0 else "mismatch")
 """
