@@ -205,6 +205,10 @@ bool g_pdl = getenv("TMG_NO_PDL") == nullptr;
 // Launch sites that go without PDL: the first column pass, whose 150-190 KB
 // CTAs scheduled early share SMs with the draining split kernel (measured
 // +7 % on the 2^26 full product).  TMG_PDL_SKIP (testing) replaces the list.
+// The fully serialized F1 launch also bounds how far a product's chain can
+// run ahead: the next product's k_zstat, which writes the split aggregates
+// before its grid-dependency wait, cannot start before this product's k_zgen
+// (their reader) has completed.
 bool pdl_skip(const char* site) {
   static const char* skip = getenv("TMG_PDL_SKIP") ? getenv("TMG_PDL_SKIP") : "f1";
   if (!site) return false;
