@@ -223,14 +223,29 @@ def coeff_table(fam: str, lam: int, N: int, b: int) -> np.ndarray:
 FFT_WORKERS = None
 
 
+# Where the 1/L of the convolution is applied.  "spectrum" is the reference's
+# order (convolution.cpp:186-192): the product spectrum is multiplied by the
+# rounded double 1.0/n and FFTW's unnormalised c2r plan runs on it.  "end"
+# is pocketfft's normalised irfft (1/n on the outputs), kept for error
+# studies: on structured operands it rounds less (Numerics).
+SCALE_AT = "spectrum"
+
+
 def cyclic_convolve(a: np.ndarray, c: np.ndarray) -> np.ndarray:
-    """convolution.cpp:175-195 (FFTW r2c, pointwise product, c2r, 1/L)."""
+    """convolution.cpp:175-195: r2c of both inputs, pointwise product
+    (re = a0 b0 - a1 b1, im = a0 b1 + a1 b0) times scale = 1.0 / n, c2r."""
     n = len(a)
     if FFT_WORKERS:
         import scipy.fft as sf
-        return sf.irfft(sf.rfft(a, workers=FFT_WORKERS) * sf.rfft(c, workers=FFT_WORKERS),
-                        n=n, workers=FFT_WORKERS)
-    return np.fft.irfft(np.fft.rfft(a) * np.fft.rfft(c), n=n)
+        fa = sf.rfft(a, workers=FFT_WORKERS)
+        fc = sf.rfft(c, workers=FFT_WORKERS)
+        if SCALE_AT == "end":
+            return sf.irfft(fa * fc, n=n, workers=FFT_WORKERS)
+        return sf.irfft((fa * fc) * (1.0 / n), n=n, norm="forward", workers=FFT_WORKERS)
+    fa, fc = np.fft.rfft(a), np.fft.rfft(c)
+    if SCALE_AT == "end":
+        return np.fft.irfft(fa * fc, n=n)
+    return np.fft.irfft((fa * fc) * (1.0 / n), n=n, norm="forward")
 
 
 def _accumulate(vals: np.ndarray, scale: int, b: int, nout: int):

@@ -428,7 +428,6 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.inv = pl.iC;
       a.tw = pl.twL;
       a.L = uint32_t(L);
-      spectral_scale(L, &a.scale, &a.scale_lo);
       const unsigned npairs = (pl.A * pl.B) / 2 + 1;
       static const bool no_ct = getenv("TMG_NO_CT") != nullptr;
       if (pl.C == 4096 && pl.mid_shared_table && !no_ct) {
@@ -481,6 +480,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.g.ncols = pl.B * (pl.C / 2);
       a.logc = pl.logc_il;
       a.fft = pl.iA;
+      spectral_scale(L, &a.scale, &a.scale_lo);
       auto ilk = pl.colct_il ? pl.colct_il->ilast : pl.colpp ? k_ilast_pp : k_ilast;
       set_smem(ilk, pl.smem_il);
       {

@@ -526,8 +526,7 @@ k_mid(MidArgs a) {
     const double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
     const double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
     const double2 pq = cmul(p, q);
-    const double2 w = make_double2(mul_hl(pq.y, a.scale, a.scale_lo),
-                                   -mul_hl(pq.x, a.scale, a.scale_lo));
+    const double2 w = make_double2(pq.y, -pq.x);  // unscaled (see CoefSink)
     sbuf[lay.idx(0, k)] = w;
     if (!(nrows == 1 && kp == k)) sbuf[lay.idx(ip, kp)] = cconj(w);
   }
@@ -588,7 +587,7 @@ __device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restr
     const double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
     const double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
     const double2 pq = cmul(p, q);
-    return make_double2(mul_hl(pq.y, a.scale, a.scale_lo), -mul_hl(pq.x, a.scale, a.scale_lo));
+    return make_double2(pq.y, -pq.x);  // -i pq, unscaled (see CoefSink)
   };
   auto repack_w = [&](double2 w1, double2 w2, double2 t) {
     const double2 ev = cadd(w1, w2);
@@ -676,11 +675,21 @@ k_mid_4096(MidArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// The convolution's 1 / (4 L) is applied here, to the inverse transform's
+// outputs, and not to the spectrum before it (where FFTW's c2r plan of the
+// reference receives it, convolution.cpp:186-192): structured operands (long
+// runs of equal limbs, BASELINE config 5) give spectra and partial sums with
+// few significant bits, which the unscaled inverse keeps exact; a
+// non-dyadic scale on the spectrum makes every one of them round, and the
+// roundings add up coherently (2^22 alternating low: 3 -> 1 ulp of the
+// largest coefficient).  One rounding against the exact constant (hi + lo).
 struct CoefSink {
   double2* coef;
   uint32_t ncols, col0;
+  double scale, scale_lo;
   __device__ __forceinline__ void operator()(uint32_t item, uint32_t ma, double2 v) const {
-    coef[int64_t(ma) * ncols + col0 + item] = v;
+    coef[int64_t(ma) * ncols + col0 + item] =
+        make_double2(mul_hl(v.x, scale, scale_lo), mul_hl(v.y, scale, scale_lo));
   }
 };
 
@@ -698,7 +707,7 @@ k_ilast(ILastArgs a) {
   tile_load<kColU>(sbuf, lay, a.fft.R, c, ColSrc{a.data, a.g, 0, col0}, tid, nthr);
   __syncthreads();
   fft_smem_compact<true>(sbuf, lay, a.fft, tw, tid, nthr);
-  tile_store<kColU>(sbuf, lay, a.fft.R, c, CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
+  tile_store<kColU>(sbuf, lay, a.fft.R, c, CoefSink{a.coef, a.g.ncols, col0, a.scale, a.scale_lo}, tid, nthr);
 }
 
 __global__ void __launch_bounds__(kColPPThreads, 1)
@@ -715,7 +724,7 @@ k_ilast_pp(ILastArgs a) {
   tile_load<4>(b0, lay, a.fft.R, c, ColSrc{a.data, a.g, 0, col0}, tid, nthr);
   __syncthreads();
   const double2* res = fft_pp<true>(b0, b1, lay, a.fft, tid, nthr);
-  tile_store<4>(res, lay, a.fft.R, c, CoefSink{a.coef, a.g.ncols, col0}, tid, nthr);
+  tile_store<4>(res, lay, a.fft.R, c, CoefSink{a.coef, a.g.ncols, col0, a.scale, a.scale_lo}, tid, nthr);
 }
 
 
@@ -925,7 +934,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 288 ? 2 : 1)) k_ilast_ct(ILastA
     }
     double2 x[P];
     cc_stages<true, SC, 0, LOGC, NTHR, P>(x, sbuf, lay, stab, a.fft, ColSrc{a.data, a.g, 0, col0},
-                                          CoefSink{a.coef, a.g.ncols, col0}, tid);
+                                          CoefSink{a.coef, a.g.ncols, col0, a.scale, a.scale_lo}, tid);
   }
 }
 

@@ -227,7 +227,7 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
     double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
     double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
     double2 pq = cmul(p, q);
-    double2 w = make_double2(mul_hl(pq.y, a.scale, a.scale_lo), -mul_hl(pq.x, a.scale, a.scale_lo));  // -i * pq * s
+    double2 w = make_double2(pq.y, -pq.x);  // -i * pq; 1/(4L) after the inverse (W below)
     buf[padidx(k)] = w;
     if (k2 != k) buf[padidx(k2)] = cconj(w);
   }
@@ -249,9 +249,11 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
   }
 
   // 7. post-map and rounding.
+  // the convolution's 1/(4L) is applied to the inverse transform's outputs
+  // (CoefSink, k_multipass.cu, says why)
   auto W = [&](int64_t j) {
     double2 y = buf[padidx(uint32_t(j >> 1))];
-    return (j & 1) ? y.y : y.x;
+    return mul_hl((j & 1) ? y.y : y.x, a.scale, a.scale_lo);
   };
   const int64_t M = (mc.mode == kModeFull) ? L : (mc.mode == kModeLow ? N : N + 1);
   double psi = 0.0;

@@ -167,7 +167,6 @@ struct MidArgs {
   SubFft inv;   // length C / 2
   TwGlobal tw;  // omega_L
   uint32_t L;
-  double scale, scale_lo;  // 1 / (4 L) as hi + lo
 };
 __global__ void k_mid(MidArgs a);
 // C = 4096 row pass with compile-time schedules, persistent over row pairs.
@@ -180,6 +179,7 @@ struct ILastArgs {
   ColGeom g;
   uint32_t logc;
   SubFft fft;  // length A (inverse)
+  double scale, scale_lo;  // 1 / (4 L) as hi + lo, applied to the outputs
 };
 __global__ void k_ilast(ILastArgs a);
 __global__ void k_ilast_pp(ILastArgs a);

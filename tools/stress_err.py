@@ -42,11 +42,15 @@ def main():
                         f"L={s.transform_length} passes={s.passes} gpu_err={s.max_round_err:.4f} "
                         f"maxabs=2^{np.log2(max(s.max_abs, 1)):.2f} {ok} ({time.time() - t:.1f}s)")
                 if do_port:
-                    try:
-                        r = port.product(mode.name.lower(), u, u, n, p.b, p.N, p.lam)
-                        line += f" port_err={r.max_err:.4f}"
-                    except port.ConvolutionPrecisionFailure as e:
-                        line += f" port=TRIP({e})"
+                    # the reference's scaling order (1/n on the spectrum) and
+                    # pocketfft's normalised irfft (1/n on the outputs)
+                    for sa in ("spectrum", "end"):
+                        port.SCALE_AT = sa
+                        try:
+                            r = port.product(mode.name.lower(), u, u, n, p.b, p.N, p.lam)
+                            line += f" port[{sa}]={r.max_err:.4f}"
+                        except port.ConvolutionPrecisionFailure:
+                            line += f" port[{sa}]=TRIP"
                 print(line, flush=True)
 
 
