@@ -35,6 +35,11 @@ LOG2N = 26
 SEED = 3
 METRIC = "low/high/full product input Gbit/s on 1 B200 at n=2^26; % HBM roofline"
 WORKLOAD = "config3: full/low/high product, n=2^26 bits, u,v = mt19937_64(seed 3) words"
+# (b, N, lambda) of the three products at n = 2^26: the accurate policy's
+# choice (Numerics; the reference's own b = 13 for low/high trips
+# its 0.25 tripwire on these operands).  Both arms run these literals; the
+# GPU arm checks that select_params still returns them.
+CONFIG3_PARAMS = {"full": (19, 3538944, 0), "low": (12, 5898240, 5), "high": (12, 5898240, 5)}
 
 
 def _peaks():
@@ -171,7 +176,9 @@ def run_ours(args, world, rank, local):
     # launch order of the concurrent products (TMG_BENCH_ORDER, e.g. "high,full,low")
     corder = [getattr(tm.Mode, x.strip().upper()) for x in
               os.environ.get("TMG_BENCH_ORDER", "low,high,full").split(",")]
-    params = {m: tm.select_params(n, m) for m in modes}
+    params = {m: tm.select_params(n, m, policy=tm.Policy.ACCURATE) for m in modes}
+    for m in modes:
+        assert (params[m].b, params[m].N, params[m].lam) == CONFIG3_PARAMS[m.name.lower()], params[m]
     ctx = tm.Context(local)
     stream = torch.cuda.Stream(device=dev)
     ctx.set_stream(stream.cuda_stream)
@@ -499,7 +506,7 @@ def run_ours(args, world, rank, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(u, v, n, params)
+        cpu = cpu_baseline(u, v, n)
 
     if rank == 0:
         med = {m.name.lower(): statistics.median(mode_ms[m]) for m in modes}
@@ -570,15 +577,16 @@ def run_ours(args, world, rank, local):
         torch.distributed.destroy_process_group()
 
 
-def _port_step(u, v, n, params, modes=("full", "low", "high")):
+def _port_step(u, v, n, modes=("full", "low", "high")):
+    """One step of the oracle port (no import of the product package: the
+    parameters are the CONFIG3_PARAMS literals)."""
     from oracle import port
-    import paper_1703_00640_b200 as tm
     for mname in modes:
-        p = params[tm.Mode[mname.upper()]]
-        port.product(mname, u, v, n, p.b, p.N, p.lam)
+        b, N, lam = CONFIG3_PARAMS[mname]
+        port.product(mname, u, v, n, b, N, lam)
 
 
-def cpu_baseline(u, v, n, params, min_seconds=10.0):
+def cpu_baseline(u, v, n, min_seconds=10.0):
     """The oracle port of the reference pipeline (pocketfft for the
     reference's FFTW, C for its maps and recombination) on whole steps of the
     same workload, repeated until at least min_seconds of CPU work."""
@@ -589,7 +597,7 @@ def cpu_baseline(u, v, n, params, min_seconds=10.0):
         steps, dt = 0, 0.0
         while dt < min_seconds or steps < 1:
             t0 = time.perf_counter()
-            _port_step(u, v, n, params)
+            _port_step(u, v, n)
             dt += time.perf_counter() - t0
             steps += 1
     finally:
@@ -604,36 +612,41 @@ def cpu_baseline(u, v, n, params, min_seconds=10.0):
 
 
 def run_reference(args, world, rank):
-    """Reference arm: the reference's CPU path (its oracle port)
-    on the host cores, same metric and config; rank 0 only under torchrun."""
+    """Reference arm: the reference's CPU path on the host cores -- its oracle
+    restatement (oracle/port.py: the reference's split, maps and checked
+    recombination in C, pocketfft on every host thread for its FFTW plans,
+    the spectrum scaled as convolution.cpp:186-192), because the reference
+    itself does not build here (no gmp.h / FFTW3).  Same metric, config,
+    parameters (CONFIG3_PARAMS literals) and step count as the GPU arm; this
+    arm imports nothing of the product package.  Rank 0 only under torchrun."""
     if rank != 0:
         return
-    import paper_1703_00640_b200 as tm
     from oracle import port
     n = 1 << LOG2N
     u, v = port.config_operands(SEED, n // 64)
-    params = {m: tm.select_params(n, m) for m in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH)}
     threads = os.cpu_count() or 1
     port.FFT_WORKERS = threads
-    _port_step(u, v, n, params, ("full",))  # warm-up (plans, page-in)
-    steps = max(1, min(args.steps, 5))
+    for _ in range(max(1, args.warmup)):
+        _port_step(u, v, n)
     times = []
-    for _ in range(steps):
+    for _ in range(args.steps):
         t0 = time.perf_counter()
-        _port_step(u, v, n, params)
+        _port_step(u, v, n)
         times.append(time.perf_counter() - t0)
-    value = 3 * 2 * n * steps / sum(times) / 1e9
+    value = 3 * 2 * n * args.steps / sum(times) / 1e9
     line = {
         "impl": "reference",
         "metric": METRIC,
-        "value": round(value, 4), "unit": "Gbit/s", "n_gpus": world, "steps": steps,
-        "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / steps, 2),
+        "value": round(value, 4), "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / args.steps, 2),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "n_bits": n},
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_bits": n,
+                   "params": {k: {"b": b, "N": N, "lambda": lam} for k, (b, N, lam) in CONFIG3_PARAMS.items()}},
         "cpu_baseline": {"value": round(value, 4), "unit": "Gbit/s", "cores": threads, "kind": "port",
-                         "sample": f"{steps} whole step(s) of full+low+high at n=2^{LOG2N} by the oracle "
-                                   f"port (pocketfft on {threads} threads for FFTW; C maps); the "
-                                   "reference needs gmp.h/FFTW3/CMake"},
+                         "sample": f"{args.steps} whole step(s) of full+low+high at n=2^{LOG2N} by the oracle "
+                                   f"port (pocketfft on {threads} threads for FFTW; C maps and "
+                                   "recombination); the reference needs gmp.h/FFTW3/CMake"},
         "e2e": {"value": round(value, 4), "unit": "Gbit/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

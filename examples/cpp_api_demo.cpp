@@ -61,6 +61,15 @@ int main() {
   CHECK(pf.lambda == 0 && pl.lambda > 0 && ph.lambda > 0);
   CHECK(tb::required_precision(pl.mode, pl.b, pl.N) == pl.p);
   CHECK(tb::select_params(1000, tb::Mode::kLow).mode == tb::Mode::kOracleFallback);
+  // the default policy is the reference's params.cpp (test_products.cpp:179-197,
+  // products.hpp:60-61); the accurate policy is an explicit opt-in
+  {
+    const tb::Params r = tb::select_params(1000000, tb::Mode::kLow, tb::Backend::kFft);
+    CHECK(r.b == 14 && r.N == 71680 && r.lambda == 4 && r.p == 65);
+    const tb::Params a = tb::select_params(1000000, tb::Mode::kLow, tb::Backend::kFft,
+                                           tb::kDefaultFallbackCutoff, tb::Policy::kAccurate);
+    CHECK(a.b == 13);
+  }
   bool threw = false;
   try {
     tb::Params bad = pl;

@@ -177,6 +177,33 @@ int tmg_profile_enable(tmg_context* ctx, int on);
 int tmg_profile_read(tmg_context* ctx, char* names, int name_stride, double* ms,
                      double* bytes, int max_records, int* count);
 
+/* ---- testing and diagnostics ----
+ * Alternative code paths a context can select so that tests reach them
+ * (none is needed in normal use; every default is the measured-best
+ * configuration, and the library reads nothing from the environment).
+ * Setting an option synchronises the context and drops its cached plans. */
+enum {
+  TMG_OPT_GENERIC_COLUMN_PASSES = 1, /* runtime-dispatched column passes, not the compiled shapes */
+  TMG_OPT_FORCE_THREE_PASS = 2,      /* three-pass plans for short column lengths (>= 64) */
+  TMG_OPT_GENERIC_ROW_PASS = 3,      /* generic row pass instead of the compiled C = 4096 one */
+  TMG_OPT_LOOKBACK_CARRY = 4,        /* single-pass decoupled look-back carry (k_carry + k_high_agg);
+                                        the default path uses it only beyond 2^32 carry bits */
+  TMG_OPT_PATCH_SCAN_MAX = 5,        /* most carry blocks k_carry_patch scans itself (default 4096;
+                                        above, the last k_carry_lanes block scans them) */
+  TMG_OPT_NO_PDL = 6,                /* launches without programmatic dependent launch */
+  TMG_OPT_DEBUG_SYNC = 7,            /* synchronise and check after every launch */
+  TMG_OPT_NO_GRAPH = 8,              /* multi-pass batches always enqueued eagerly */
+  TMG_OPT_Z_NATURAL = 9,             /* pre-mapped coefficients stored in natural order */
+  TMG_OPT_GENERIC_SMALL = 10         /* runtime-dispatched stages in the fused small-product kernel */
+};
+int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value);
+
+/* Copies the last single product's pre-mapped coefficients (which = 0; in
+ * natural order under TMG_OPT_Z_NATURAL) or convolution coefficients
+ * (which = 1) to host memory; *bytes is the buffer size in, the bytes
+ * copied out. */
+int tmg_debug_read(tmg_context* ctx, int which, void* host, size_t* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,8 +84,9 @@ inline void check(int rc) {
 // ---- parameters (products.hpp:14-61) ----
 enum class Mode : std::int32_t { kFull = 0, kLow = 1, kHigh = 2, kOracleFallback = 3 };
 enum class Backend : std::int32_t { kExact = TMG_BACKEND_EXACT, kFft = TMG_BACKEND_FFT };
-// kReference reproduces the reference's params.cpp; kAccurate (the default)
-// adds the predicted-error bound and the GPU cost model.
+// kReference (the default, as products.hpp:60-61) reproduces the reference's
+// params.cpp; kAccurate is an opt-in that adds the predicted-error bound and
+// the GPU cost model (Numerics).
 enum class Policy : std::int32_t { kReference = TMG_POLICY_REFERENCE, kAccurate = TMG_POLICY_ACCURATE };
 
 inline constexpr std::int64_t kDefaultFallbackCutoff = 4096;
@@ -146,7 +147,7 @@ inline void validate_params(const Params& params) {
 
 inline Params select_params(std::int64_t n, Mode mode, Backend backend = Backend::kFft,
                             std::int64_t fallback_cutoff = kDefaultFallbackCutoff,
-                            Policy policy = Policy::kAccurate) {
+                            Policy policy = Policy::kReference) {
   tmg_params q{};
   check(tmg_select_params(n, static_cast<std::int32_t>(mode), static_cast<std::int32_t>(backend),
                           fallback_cutoff, static_cast<std::int32_t>(policy), &q));

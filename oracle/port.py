@@ -106,6 +106,18 @@ def mt19937_64(seed: int, count: int) -> np.ndarray:
     return out
 
 
+def random_bits_pairs(seed: int, n: int, count: int):
+    """The operand pairs of the reference's FFT product tests: u, v =
+    testsup::random_bits(rng, n) in turn (test_support.hpp:17-22: ceil(n/64)
+    mt19937_64 words, little-endian, low n bits) from std::mt19937_64(seed),
+    as in test_products.cpp:371-406."""
+    nl = (n + 63) // 64
+    w = mt19937_64(seed, 2 * count * nl).reshape(count, 2, nl)
+    if n % 64:
+        w[:, :, -1] &= np.uint64((1 << (n % 64)) - 1)
+    return [(w[i, 0].copy(), w[i, 1].copy()) for i in range(count)]
+
+
 def config_operands(seed: int, nlimbs: int, force_top_bit: bool = False):
     """u = words[0:nl], v = words[nl:2nl] of mt19937_64(seed)."""
     w = mt19937_64(seed, 2 * nlimbs)

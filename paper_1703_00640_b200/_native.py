@@ -56,6 +56,18 @@ class tmg_stats(ctypes.Structure):
 
 TMG_STAT_ESCALATED = 1 << 24
 
+# tmg_context_set_option (testing and diagnostics)
+TMG_OPT_GENERIC_COLUMN_PASSES = 1
+TMG_OPT_FORCE_THREE_PASS = 2
+TMG_OPT_GENERIC_ROW_PASS = 3
+TMG_OPT_LOOKBACK_CARRY = 4
+TMG_OPT_PATCH_SCAN_MAX = 5
+TMG_OPT_NO_PDL = 6
+TMG_OPT_DEBUG_SYNC = 7
+TMG_OPT_NO_GRAPH = 8
+TMG_OPT_Z_NATURAL = 9
+TMG_OPT_GENERIC_SMALL = 10
+
 
 def header_functions() -> list[str]:
     """Names of every function the C header declares."""
@@ -113,6 +125,7 @@ def load():
     L.tmg_profile_read.argtypes = [vp, ctypes.c_char_p, ctypes.c_int, P(ctypes.c_double),
                                    P(ctypes.c_double), ctypes.c_int, P(ctypes.c_int)]
     L.tmg_debug_read.argtypes = [vp, ctypes.c_int, vp, P(ctypes.c_size_t)]
+    L.tmg_context_set_option.argtypes = [vp, i32, i64]
     _lib = L
     return L
 

@@ -96,19 +96,37 @@ constexpr int kMaxBatchStreams = 32;
 constexpr unsigned kPatchScanMaxBlocks = 4096;
 constexpr int64_t kGraphMinBatch = 4;  // batches replayed as graphs from this size
 
+// Alternative code paths a context can select for testing and diagnostics
+// (tmg_context_set_option, TMG_OPT_*); every default is the measured-best
+// configuration, and nothing is read from the environment.
+struct Options {
+  PlanOptions plan;             // TMG_OPT_GENERIC_COLUMN_PASSES, TMG_OPT_FORCE_THREE_PASS
+  bool generic_row = false;     // TMG_OPT_GENERIC_ROW_PASS
+  bool lookback_carry = false;  // TMG_OPT_LOOKBACK_CARRY
+  long patch_scan_max = long(kPatchScanMaxBlocks);  // TMG_OPT_PATCH_SCAN_MAX
+  bool no_pdl = false;          // TMG_OPT_NO_PDL
+  bool debug_sync = false;      // TMG_OPT_DEBUG_SYNC
+  bool no_graph = false;        // TMG_OPT_NO_GRAPH
+  bool z_natural = false;       // TMG_OPT_Z_NATURAL
+  bool generic_small = false;   // TMG_OPT_GENERIC_SMALL
+};
+
 struct Context {
   int device = 0;
   int num_sms = 148;
   int escalations = 0;  // re-runs at b - 1 after a precision failure
+  Options opt;
   Profiler prof;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   TwiddleCache tw;
-  std::map<std::tuple<int64_t, int32_t, int64_t, int64_t, int32_t>, std::unique_ptr<Plan>> plans;
+  // keyed on every Params field, so a cache hit never skips validate_params
+  std::map<std::tuple<int64_t, int32_t, int64_t, int64_t, int32_t, int32_t, int32_t, int32_t>,
+           std::unique_ptr<Plan>>
+      plans;
   DevBuf status, dop_u, dop_v, dop_out, pflags;
   Workspace ws0;                                  // single products (context stream)
   std::vector<std::unique_ptr<Workspace>> wsb;    // batch workspaces (own streams)
-  bool debug_sync = false;
   DevStatus* h_status = nullptr;  // pinned
   // Multi-pass batches replayed as CUDA graphs: a batch shape seen once runs
   // eagerly (allocating every workspace buffer), the second time it is
@@ -145,25 +163,23 @@ struct Context {
   }
   int32_t last_kernels = 0;
   int64_t last_L = 0;
-  // Output bytes of the products enqueued on the stream since it was last
-  // synchronized, as one address range: k_zstat reads its operands before
-  // waiting for its predecessor (programmatic launch) only when they lie
-  // outside it, since kernels of earlier products may still be writing there
-  // (device-pointer products chained output -> input).
-  uintptr_t out_lo = UINTPTR_MAX, out_hi = 0;
+  // k_zstat may read its operands before waiting for its predecessor
+  // (programmatic launch) only when no kernel still in flight can be writing
+  // them: on the host-buffer path, where the library's own H2D copies wrote
+  // them after the context's previous work.  Device-pointer products never
+  // read early -- another context sharing the stream, or any kernel that
+  // triggers its dependents early, may still be producing the operands.
   bool zstat_early = false;
-  void drained() {
-    out_lo = UINTPTR_MAX;
-    out_hi = 0;
-  }
+  void drained() {}
   int32_t last_passes = 0;
 
   Plan& plan_for(const Params& p) {
-    auto key = std::make_tuple(p.n, p.b, p.N, p.lambda, int32_t(p.mode));
+    auto key = std::make_tuple(p.n, p.b, p.N, p.lambda, int32_t(p.mode), p.p, int32_t(p.backend),
+                               int32_t(p.signed_split));
     auto it = plans.find(key);
     if (it != plans.end()) return *it->second;
     validate_params(p);
-    auto pl = build_plan(p, tw);
+    auto pl = build_plan(p, tw, opt.plan);
     Plan& ref = *pl;
     plans.emplace(key, std::move(pl));
     return ref;
@@ -182,8 +198,7 @@ void spectral_scale(int64_t L, double* hi, double* lo) {
 }
 
 // z layout shared by k_zgen (writer) and k_f1 (reader).
-ZTile ztile(const Plan& pl, int64_t L) {
-  static const bool natural = getenv("TMG_Z_NATURAL") != nullptr;
+ZTile ztile(const Plan& pl, int64_t L, bool natural) {
   ZTile t;
   const uint32_t ncols = uint32_t(L / pl.A);
   t.fdcols = make_fastdiv(ncols);
@@ -196,32 +211,24 @@ ZTile ztile(const Plan& pl, int64_t L) {
 
 
 // Every kernel of a product goes out through launch(): with programmatic
-// dependent launch (default; TMG_NO_PDL turns it off) the next kernel on the
-// stream is scheduled while the current one drains and waits in pdl_wait()
-// (common.cuh) for its data, which hides the launch gap between the
-// pipeline's dependent kernels.
-bool g_pdl = getenv("TMG_NO_PDL") == nullptr;
-
-// Launch sites that go without PDL: the first column pass, whose 150-190 KB
-// CTAs scheduled early share SMs with the draining split kernel (measured
-// +7 % on the 2^26 full product).  TMG_PDL_SKIP (testing) replaces the list.
-// The fully serialized F1 launch also bounds how far a product's chain can
-// run ahead: the next product's k_zstat, which writes the split aggregates
-// before its grid-dependency wait, cannot start before this product's k_zgen
-// (their reader) has completed.
-bool pdl_skip(const char* site) {
-  static const char* skip = getenv("TMG_PDL_SKIP") ? getenv("TMG_PDL_SKIP") : "f1";
-  if (!site) return false;
-  const std::string list = std::string(",") + skip + ",";
-  return list.find(std::string(",") + site + ",") != std::string::npos;
-}
-
+// dependent launch (default; TMG_OPT_NO_PDL turns it off) the next kernel on
+// the stream is scheduled while the current one drains and waits in
+// pdl_wait() (common.cuh) for its data, which hides the launch gap between
+// the pipeline's dependent kernels.
+//
+// The first column pass goes without PDL (site "f1"): its 150-190 KB CTAs
+// scheduled early share SMs with the draining split kernel (measured +7 % on
+// the 2^26 full product).  The fully serialized F1 launch also bounds how far
+// a product's chain can run ahead: the next product's k_zstat, which writes
+// the split aggregates before its grid-dependency wait, cannot start before
+// this product's k_zgen (their reader) has completed.
+//
 // Kernels without griddepcontrol.wait (the fused small-product kernels) go
 // out with pdl = false: launched programmatically they could start under a
 // predecessor that triggered early and read its unfinished outputs.
 template <class Arg>
-void launch(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-            const Arg& arg, const char* site = nullptr, bool pdl = true) {
+void launch(const Context& cx, void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem,
+            cudaStream_t st, const Arg& arg, const char* site = nullptr, bool pdl = true) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -229,19 +236,18 @@ void launch(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = (pdl && g_pdl && !pdl_skip(site)) ? 1 : 0;
+  const bool skip = site && std::strcmp(site, "f1") == 0;
+  attr[0].val.programmaticStreamSerializationAllowed = (pdl && !cx.opt.no_pdl && !skip) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   TMG_CUDA(cudaLaunchKernelEx(&cfg, kernel, arg));
 }
 
-bool g_debug_sync = getenv("TMG_DEBUG_SYNC") != nullptr;
-
-void check_launch(const char* what) {
+void check_launch(const Context& cx, const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     throw Error(TMG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-  if (g_debug_sync) {
+  if (cx.opt.debug_sync) {
     e = cudaDeviceSynchronize();
     fprintf(stderr, "[tmg] %s done: %s\n", what, cudaGetErrorString(e));
     if (e != cudaSuccess)
@@ -336,7 +342,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.cbits_v = w.cbv.as<uint32_t>();
       a.z = w.work_z.as<double2>();
       a.mc = pl.mc;
-      a.zt = ztile(pl, L);
+      a.zt = ztile(pl, L, cx.opt.z_natural);
       const unsigned blocks = unsigned((pl.count + kZgenChunks - 1) / kZgenChunks);
       a.status = status;
       w.zaggs.ensure(size_t(blocks) * 4 + 16);
@@ -344,23 +350,23 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.early = cx.zstat_early ? 1 : 0;
       {
         KTimer kt(cx, "k_zstat", double(2 * pl.nlimbs) * 8.0, int(p.mode), st);
-        launch(k_zstat, dim3((blocks + 255) / 256), dim3(256), 0, st, a, "zstat");
+        launch(cx, k_zstat, dim3((blocks + 255) / 256), dim3(256), 0, st, a, "zstat");
       }
-      check_launch("k_zstat");
+      check_launch(cx, "k_zstat");
       ZgenFn zg = zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda));
       set_smem(zg, pl.smem_zgen);
       {
         KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * 16.0, int(p.mode), st);
-        launch(zg, dim3(blocks), dim3(kZgenThreads), pl.smem_zgen, st, a, "zgen");
+        launch(cx, zg, dim3(blocks), dim3(kZgenThreads), pl.smem_zgen, st, a, "zgen");
       }
-      check_launch("k_zgen");
+      check_launch(cx, "k_zgen");
       kernels += 2;
     }
     double2* T = w.work_t.as<double2>();
     {
       F1Args a;
       a.z = w.work_z.as<double2>();
-      a.zt = ztile(pl, L);
+      a.zt = ztile(pl, L, cx.opt.z_natural);
       a.out = T;
       a.ncols = uint32_t(L / pl.A);
       a.logc = pl.logc_f1;
@@ -381,17 +387,14 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       set_smem(f1k, pl.smem_f1);
       {
         KTimer kt(cx, "k_f1", double(p.N) * 16.0 + double(L) * 16.0, int(p.mode), st);
-        // the compile-time passes are persistent (one wave of CTAs)
-        // TMG_F1_WAVES (testing): persistent CTAs per SM slot (0: one per tile)
-        static const int f1w = getenv("TMG_F1_WAVES") ? atoi(getenv("TMG_F1_WAVES")) : 1;
+        // the compile-time pass is persistent (one wave of CTAs)
         const unsigned tiles = a.ncols >> a.logc;
         const unsigned grid =
-            (pl.colct && f1w > 0)
-                ? std::min<unsigned>(tiles, unsigned(f1w * cx.num_sms * (pl.colct->nthr <= 288 ? 2 : 1)))
-                : tiles;
-        launch(f1k, dim3(grid), dim3(pl.thr_f1), pl.smem_f1, st, a, "f1");
+            pl.colct ? std::min<unsigned>(tiles, unsigned(cx.num_sms * (pl.colct->nthr <= 288 ? 2 : 1)))
+                     : tiles;
+        launch(cx, f1k, dim3(grid), dim3(pl.thr_f1), pl.smem_f1, st, a, "f1");
       }
-      check_launch("k_f1");
+      check_launch(cx, "k_f1");
       ++kernels;
     }
     if (pl.kind == 3) {
@@ -413,9 +416,9 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       set_smem(colk, pl.smem_f2);
       {
         KTimer kt(cx, "k_col_f2", double(L) * 32.0, int(p.mode), st);
-        launch(colk, dim3(dim3(pl.C >> a.logc, pl.A)), dim3(pl.thr_f2), pl.smem_f2, st, a, "col");
+        launch(cx, colk, dim3(dim3(pl.C >> a.logc, pl.A)), dim3(pl.thr_f2), pl.smem_f2, st, a, "col");
       }
-      check_launch("k_col(f2)");
+      check_launch(cx, "k_col(f2)");
       ++kernels;
     }
     {
@@ -429,19 +432,18 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.tw = pl.twL;
       a.L = uint32_t(L);
       const unsigned npairs = (pl.A * pl.B) / 2 + 1;
-      static const bool no_ct = getenv("TMG_NO_CT") != nullptr;
-      if (pl.C == 4096 && pl.mid_shared_table && !no_ct) {
+      if (pl.C == 4096 && pl.mid_shared_table && !cx.opt.generic_row) {
         // compile-time schedule, persistent over row pairs
         set_smem(k_mid_4096, pl.smem_mid);
         const unsigned grid = std::min<unsigned>(npairs, unsigned(cx.num_sms));
         KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode), st);
-        launch(k_mid_4096, dim3(grid), dim3(kMidCtThreads), pl.smem_mid, st, a, "mid");
+        launch(cx, k_mid_4096, dim3(grid), dim3(kMidCtThreads), pl.smem_mid, st, a, "mid");
       } else {
         set_smem(k_mid, pl.smem_mid);
         KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode), st);
-        launch(k_mid, dim3(npairs), dim3(pl.thr_mid), pl.smem_mid, st, a, "mid");
+        launch(cx, k_mid, dim3(npairs), dim3(pl.thr_mid), pl.smem_mid, st, a, "mid");
       }
-      check_launch("k_mid");
+      check_launch(cx, "k_mid");
       ++kernels;
     }
     if (pl.kind == 3) {
@@ -463,9 +465,9 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       set_smem(colk, pl.smem_i2);
       {
         KTimer kt(cx, "k_col_i2", double(L) * 16.0, int(p.mode), st);
-        launch(colk, dim3(dim3((pl.C / 2) >> a.logc, pl.A)), dim3(pl.thr_i2), pl.smem_i2, st, a, "col");
+        launch(cx, colk, dim3(dim3((pl.C / 2) >> a.logc, pl.A)), dim3(pl.thr_i2), pl.smem_i2, st, a, "col");
       }
-      check_launch("k_col(i2)");
+      check_launch(cx, "k_col(i2)");
       ++kernels;
     }
     double2* coef = w.work_c.as<double2>();
@@ -485,16 +487,11 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       set_smem(ilk, pl.smem_il);
       {
         KTimer kt(cx, "k_ilast", double(L) * 16.0, int(p.mode), st);
-        // TMG_IL_WAVES (testing): persistent CTAs per SM slot (0: one per tile)
-        static const int ilw = getenv("TMG_IL_WAVES") ? atoi(getenv("TMG_IL_WAVES")) : 0;
-        const unsigned tiles = a.g.ncols >> a.logc;
-        const unsigned grid =
-            (pl.colct_il && ilw > 0)
-                ? std::min<unsigned>(tiles, unsigned(ilw * cx.num_sms * (pl.colct_il->nthr <= 288 ? 2 : 1)))
-                : tiles;
-        launch(ilk, dim3(grid), dim3(pl.thr_il), pl.smem_il, st, a, "ilast");
+        // one CTA per tile (a persistent ilast measured 49 against 45 us)
+        const unsigned grid = a.g.ncols >> a.logc;
+        launch(cx, ilk, dim3(grid), dim3(pl.thr_il), pl.smem_il, st, a, "ilast");
       }
-      check_launch("k_ilast");
+      check_launch(cx, "k_ilast");
       ++kernels;
     }
     // high: k_carry_lanes and k_carry_patch nominate the limb that stops the
@@ -527,16 +524,12 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       } else {
         a.tbuf = nullptr;
       }
-      static const bool old_carry = getenv("TMG_OLD_CARRY") != nullptr;
+      const bool old_carry = cx.opt.lookback_carry;
       const int lam = (p.mode == PMode::kFull) ? 0 : int(pl.mc.lambda);
       // limbs per thread: 4 when the block's coefficient window stays small
       // (wide chunks), else 2 (more CTAs per SM for narrow chunks)
       const bool hb = p.mode == PMode::kHigh;
-      // TMG_CARRY_PT (testing): force 2 or 4 limbs per thread
-      static const int force_pt = getenv("TMG_CARRY_PT") ? atoi(getenv("TMG_CARRY_PT")) : 0;
-      const int pt = (force_pt == 2 || force_pt == 4)
-                         ? force_pt
-                         : (carry2_smem(int(p.b), lam, 4, hb) <= size_t(64) * 1024 ? 4 : 2);
+      const int pt = carry2_smem(int(p.b), lam, 4, hb) <= size_t(64) * 1024 ? 4 : 2;
       const size_t smem2 = carry2_smem(int(p.b), lam, pt, hb);
       if (!old_carry && smem2 <= kMaxDynSmem && 64 * pl.ML + 64 < (int64_t(1) << 32)) {
         high_stop_fused = p.mode == PMode::kHigh;
@@ -555,33 +548,31 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         // k_carry_patch composes the block functions itself while that stays
         // cheap (each patch CTA reads the aggregates before it); above, the
         // last lanes block scans them into cins
-        // TMG_PATCH_SCAN_MAX (testing) overrides the limit
-        static const long patch_scan_max =
-            getenv("TMG_PATCH_SCAN_MAX") ? atol(getenv("TMG_PATCH_SCAN_MAX")) : long(kPatchScanMaxBlocks);
-        a.lanes_cins = long(blocks2) > patch_scan_max ? 1 : 0;
+        // (TMG_OPT_PATCH_SCAN_MAX lowers the limit for testing)
+        a.lanes_cins = long(blocks2) > cx.opt.patch_scan_max ? 1 : 0;
         CarryLanesFn lanes = carry_lanes_kernel(lam, pt);
         set_smem(lanes, smem2);
         {
           KTimer kt(cx, "k_carry_lanes", double(pl.K) * 8.0 + double(hb ? pl.ML : pl.out_limbs) * 8.0, int(p.mode),
                     st);
-          launch(lanes, dim3(blocks2), dim3(kC2Threads), smem2, st, a, "lanes");
+          launch(cx, lanes, dim3(blocks2), dim3(kC2Threads), smem2, st, a, "lanes");
         }
-        check_launch("k_carry_lanes");
+        check_launch(cx, "k_carry_lanes");
         {
           // the lanes kernel wrote the limbs; one warp per block adds its carry-in
           KTimer kt(cx, "k_carry_patch", 0.0, int(p.mode), st);
-          launch(carry_patch_kernel(pt), dim3((blocks2 + kC2Threads / 32 - 1) / (kC2Threads / 32)), dim3(kC2Threads),
+          launch(cx, carry_patch_kernel(pt), dim3((blocks2 + kC2Threads / 32 - 1) / (kC2Threads / 32)), dim3(kC2Threads),
                  0, st, a, "patch");
-          check_launch("k_carry_patch");
+          check_launch(cx, "k_carry_patch");
         }
         kernels += 2;
       } else {
         set_smem(k_carry, pl.smem_carry);
         {
           KTimer kt(cx, "k_carry", double(pl.K) * 8.0 + double(pl.mc.mode == 2 ? pl.ML : pl.out_limbs) * 8.0, int(p.mode), st);
-          launch(k_carry, dim3(blocks), dim3(kCarryThreads), pl.smem_carry, st, a, "carry");
+          launch(cx, k_carry, dim3(blocks), dim3(kCarryThreads), pl.smem_carry, st, a, "carry");
         }
-        check_launch("k_carry");
+        check_launch(cx, "k_carry");
         ++kernels;
       }
     }
@@ -604,15 +595,15 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.ticket = w.hticket.as<uint32_t>();
       if (!high_stop_fused) {
         KTimer kt(cx, "k_high_agg", double(pl.ML) * 8.0, int(p.mode), st);
-        launch(k_high_agg, dim3(blocks), dim3(kCarryThreads), 0, st, a, "hagg");
-        check_launch("k_high_agg");
+        launch(cx, k_high_agg, dim3(blocks), dim3(kCarryThreads), 0, st, a, "hagg");
+        check_launch(cx, "k_high_agg");
         ++kernels;
       }
       {
         KTimer kt(cx, "k_high_round", double(pl.ML) * 8.0 + double(pl.out_limbs) * 8.0, int(p.mode), st);
-        launch(k_high_round, dim3(blocks), dim3(kCarryThreads), 0, st, a, "hround");
+        launch(cx, k_high_round, dim3(blocks), dim3(kCarryThreads), 0, st, a, "hround");
       }
-      check_launch("k_high_round");
+      check_launch(cx, "k_high_round");
       ++kernels;
     }
   }
@@ -620,25 +611,14 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
 }
 
 // Enqueue one batch of products (device pointers) on the context stream.
+// own_operands: the library's own H2D copies wrote du and dv (host-buffer
+// path), so k_zstat may read them before its grid-dependency wait.
 void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
-             uint64_t* dout, int64_t count, uint32_t* pflags) {
+             uint64_t* dout, int64_t count, uint32_t* pflags, bool own_operands) {
   const Params& p = pl.params;
   cudaStream_t st = cx.stream;
   DevStatus* status = cx.status.as<DevStatus>();
-  {
-    const uintptr_t ol = reinterpret_cast<uintptr_t>(dout);
-    const uintptr_t oh = ol + uintptr_t(count * pl.out_limbs) * 8;
-    cx.out_lo = std::min(cx.out_lo, ol);
-    cx.out_hi = std::max(cx.out_hi, oh);
-    const uintptr_t ob = uintptr_t(count * pl.nlimbs) * 8;
-    auto clear = [&](const uint64_t* x) {
-      const uintptr_t xl = reinterpret_cast<uintptr_t>(x);
-      return xl + ob <= cx.out_lo || xl >= cx.out_hi;
-    };
-    // TMG_ZSTAT_EARLY (testing): 1 always reads early (unsafe for chains), 0 never
-    static const int force_early = getenv("TMG_ZSTAT_EARLY") ? atoi(getenv("TMG_ZSTAT_EARLY")) : -1;
-    cx.zstat_early = force_early >= 0 ? force_early == 1 : (clear(du) && clear(dv));
-  }
+  cx.zstat_early = own_operands;
   cx.last_L = pl.L;
   cx.last_passes = pl.kind;
   if (pl.kind == 0)
@@ -663,15 +643,14 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     a.inv = pl.inv;
     a.mc = pl.mc;
     a.status = status;
-    static const bool one_cta = getenv("TMG_SMALL_1CTA") != nullptr;
     // the 2-CTA variant only pays when two CTAs' shared memory fits an SM
     // (228 KB, 1 KB reserved per CTA); otherwise its spills cost for nothing
     const bool two = pl.small_threads <= 384 && 2 * (pl.small_smem + 1024) <= size_t(228) * 1024;
     auto sk = pl.small_threads > 512 ? k_small_product_big
-                                     : (two && !one_cta) ? k_small_product_2 : k_small_product;
+                                     : two ? k_small_product_2 : k_small_product;
     unsigned threads = unsigned(pl.small_threads);
-    // TMG_SMALL_GENERIC (testing): the runtime-dispatched stages at every length
-    static const bool small_generic = getenv("TMG_SMALL_GENERIC") != nullptr;
+    // TMG_OPT_GENERIC_SMALL (testing): the runtime-dispatched stages at every length
+    const bool small_generic = cx.opt.generic_small;
     // (a 640-thread 8 x 8 x 8 x 10 variant for the low/high L = 5120 was
     // slower than the 2-CTA generic kernel: 1.57 / 2.12 ms against 1.40 /
     // 1.68 ms for 4096 products; the maps prefer two smaller CTAs per SM)
@@ -682,9 +661,9 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     set_smem(sk, pl.small_smem);
     {
       KTimer kt(cx, "k_small_product", double(count) * double(2 * pl.nlimbs + pl.out_limbs) * 8.0, int(p.mode));
-      launch(sk, dim3(unsigned(count)), dim3(threads), pl.small_smem, st, a, "small", false);
+      launch(cx, sk, dim3(unsigned(count)), dim3(threads), pl.small_smem, st, a, "small", false);
     }
-    check_launch("k_small_product");
+    check_launch(cx, "k_small_product");
     cx.last_kernels = 1;
     return;
   }
@@ -694,7 +673,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     cx.last_kernels = enqueue_product(cx, cx.ws0, st, status, pl, du, dv, dout);
     if (pflags) {
       k_status_publish<<<1, 1, 0, st>>>(status, pflags, nullptr);
-      check_launch("k_status_publish");
+      check_launch(cx, "k_status_publish");
     }
     return;
   }
@@ -703,8 +682,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
   // into pflags and merged into the context status.  Repeated batch shapes
   // replay a captured graph (the launches of a batch of small multi-pass
   // products cost more host time than their kernels run).
-  static const bool no_graph = getenv("TMG_NO_GRAPH") != nullptr;
-  const bool graphable = !no_graph && !cx.graphs_off && !cx.prof.on && !g_debug_sync &&
+  const bool graphable = !cx.opt.no_graph && !cx.graphs_off && !cx.prof.on && !cx.opt.debug_sync &&
                          count >= kGraphMinBatch;
   Context::BatchKey key{&pl, count, du, dv, dout, pflags};
   bool capture = false;
@@ -774,7 +752,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     kernels += enqueue_product(cx, w, w.stream, ws, pl, du + i * pl.nlimbs, dv + i * pl.nlimbs,
                                dout + i * pl.out_limbs);
     k_status_publish<<<1, 1, 0, w.stream>>>(ws, pflags ? pflags + i : nullptr, status);
-    check_launch("k_status_publish");
+    check_launch(cx, "k_status_publish");
   }
   for (int s2 = 0; s2 < S; ++s2) {
     Workspace& w = *cx.wsb[s2];
@@ -793,7 +771,7 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
       // capture unsupported here: run this batch eagerly, stop capturing
       (void)cudaGetLastError();
       cx.graphs_off = true;
-      enqueue(cx, pl, du, dv, dout, count, pflags);
+      enqueue(cx, pl, du, dv, dout, count, pflags, own_operands);
       return;
     }
     cx.graphs[key] = Context::BatchGraph{exec, kernels};
@@ -805,13 +783,16 @@ void reset_status(Context& cx) {
   TMG_CUDA(cudaMemsetAsync(cx.status.p, 0, sizeof(DevStatus), cx.stream));
 }
 
-// Reads the status word and maps device flags onto the reference's errors.
+// Reads the status word, clears it for the next products on the stream, and
+// maps device flags onto the reference's errors.  The clear comes before any
+// throw: a refused product must not leave its flags behind for the next
+// tmg_check of good products.
 int finish(Context& cx, const Plan* pl, tmg_stats* stats) {
   TMG_CUDA(cudaMemcpyAsync(cx.h_status, cx.status.p, sizeof(DevStatus),
                            cudaMemcpyDeviceToHost, cx.stream));
   TMG_CUDA(cudaStreamSynchronize(cx.stream));
-  cx.drained();
   DevStatus s = *cx.h_status;
+  reset_status(cx);
   double e, m;
   std::memcpy(&e, &s.max_err_bits, 8);
   std::memcpy(&m, &s.max_abs_bits, 8);
@@ -919,7 +900,7 @@ int host_product_once(Context& cx, const Params& p, int32_t want_mode,
       BaseArgs a{cx.dop_u.as<uint64_t>() + i * nl, cx.dop_v.as<uint64_t>() + i * nl,
                  prod.as<uint64_t>() + i * 2 * nl, nl};
       k_basecase<<<1, 256, size_t(6 * nl) * 8 + 64, cx.stream>>>(a);
-      check_launch("k_basecase");
+      check_launch(cx, "k_basecase");
     }
     std::vector<uint64_t> h(size_t(count * 2 * nl));
     TMG_CUDA(cudaMemcpyAsync(h.data(), prod.p, h.size() * 8, cudaMemcpyDeviceToHost, cx.stream));
@@ -961,7 +942,7 @@ int host_product_once(Context& cx, const Params& p, int32_t want_mode,
     return TMG_OK;
   }
   enqueue(cx, pl, cx.dop_u.as<uint64_t>(), cx.dop_v.as<uint64_t>(), cx.dop_out.as<uint64_t>(),
-          count, flags_out ? cx.pflags.as<uint32_t>() : nullptr);
+          count, flags_out ? cx.pflags.as<uint32_t>() : nullptr, true);
   TMG_CUDA(cudaMemcpyAsync(out, cx.dop_out.p, size_t(count * pl.out_limbs) * 8,
                            cudaMemcpyDeviceToHost, cx.stream));
   if (flags_out)
@@ -1149,17 +1130,13 @@ int tmg_product_device(tmg_context* ctx, const tmg_params* params, const uint64_
     if (q.mode == PMode::kOracleFallback)
       throw Error(TMG_ERR_UNSUPPORTED, "device path needs a pipeline parameter set");
     Plan& pl = ctx->cx.plan_for(q);
-    enqueue(ctx->cx, pl, d_u, d_v, d_out, count, nullptr);
+    enqueue(ctx->cx, pl, d_u, d_v, d_out, count, nullptr, false);
     return TMG_OK;
   });
 }
 
 int tmg_check(tmg_context* ctx, tmg_stats* stats) {
-  return guarded([&] {
-    int r = finish(ctx->cx, nullptr, stats);
-    reset_status(ctx->cx);
-    return r;
-  });
+  return guarded([&] { return finish(ctx->cx, nullptr, stats); });
 }
 
 int tmg_host_alloc(size_t bytes, void** out) {
@@ -1199,6 +1176,34 @@ int tmg_context_set_escalation(tmg_context* ctx, int max_escalations) {
     if (max_escalations < 0 || max_escalations > 8)
       throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "escalation count must be in [0, 8]");
     ctx->cx.escalations = max_escalations;
+    return TMG_OK;
+  });
+}
+
+int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value) {
+  return guarded([&] {
+    Options& o = ctx->cx.opt;
+    const bool on = value != 0;
+    switch (option) {
+      case TMG_OPT_GENERIC_COLUMN_PASSES: o.plan.generic_columns = on; break;
+      case TMG_OPT_FORCE_THREE_PASS: o.plan.force_three_pass = on; break;
+      case TMG_OPT_GENERIC_ROW_PASS: o.generic_row = on; break;
+      case TMG_OPT_LOOKBACK_CARRY: o.lookback_carry = on; break;
+      case TMG_OPT_PATCH_SCAN_MAX:
+        if (value < 0) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "patch scan limit must be >= 0");
+        o.patch_scan_max = long(value);
+        break;
+      case TMG_OPT_NO_PDL: o.no_pdl = on; break;
+      case TMG_OPT_DEBUG_SYNC: o.debug_sync = on; break;
+      case TMG_OPT_NO_GRAPH: o.no_graph = on; break;
+      case TMG_OPT_Z_NATURAL: o.z_natural = on; break;
+      case TMG_OPT_GENERIC_SMALL: o.generic_small = on; break;
+      default: throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "unknown context option");
+    }
+    // plans and captured batch graphs were built under the old options
+    TMG_CUDA(cudaStreamSynchronize(ctx->cx.stream));
+    ctx->cx.plans.clear();
+    ctx->cx.clear_graphs();
     return TMG_OK;
   });
 }

@@ -1039,15 +1039,8 @@ static const ColCtShape kColCtShapes[] = {
 #undef TMG_COLCT
 
 const ColCtShape* colct_for(uint32_t R, int role) {
-  static const bool off = getenv("TMG_NO_COLCT") != nullptr;
-  // TMG_COLCT_LOGC (testing): the shape with this many columns per CTA, for
-  // both passes
-  static const int want_logc = getenv("TMG_COLCT_LOGC") ? atoi(getenv("TMG_COLCT_LOGC")) : -1;
-  if (off) return nullptr;
-  for (const ColCtShape& sh : kColCtShapes) {
-    if (sh.R != R) continue;
-    if (want_logc >= 0 ? sh.logc == want_logc : (sh.uses & role) != 0) return &sh;
-  }
+  for (const ColCtShape& sh : kColCtShapes)
+    if (sh.R == R && (sh.uses & role) != 0) return &sh;
   return nullptr;
 }
 

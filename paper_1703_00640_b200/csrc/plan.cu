@@ -345,7 +345,7 @@ MapConsts make_map_consts(const Params& p) {
   return m;
 }
 
-std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
+std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw, const PlanOptions& opt) {
   auto pl = std::make_unique<Plan>();
   pl->params = p;
   pl->nlimbs = (p.n + 63) / 64;
@@ -425,9 +425,8 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   if (C == 0) throw Error(TMG_ERR_UNSUPPORTED, "no row length divides L");
   const uint64_t AB = UL / C;
   uint32_t A = 0, B = 1;
-  // TMG_FORCE_3PASS (testing): split even short column lengths into A x B
-  static const bool force3 = getenv("TMG_FORCE_3PASS") != nullptr;
-  if (AB <= 2048 && !(force3 && AB >= 64)) {
+  // opt.force_three_pass (testing): split even short column lengths into A x B
+  if (AB <= 2048 && !(opt.force_three_pass && AB >= 64)) {
     A = uint32_t(AB);
     pl->kind = 2;
   } else {
@@ -455,8 +454,7 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   pl->fC = make_subfft(C, tC, 1, &tw);
   pl->iC = make_subfft(C / 2, tC, 2, &tw);
   pl->mid_shared_table = map_stages(pl->iC, pl->fC);
-  // TMG_COL_LOGC (testing): cap the columns per CTA of the column passes
-  static const int col_logc_cap = getenv("TMG_COL_LOGC") ? atoi(getenv("TMG_COL_LOGC")) : 6;
+  const int col_logc_cap = 6;  // columns per CTA of the column passes: at most 64
   pl->logc_f1 = std::min<uint32_t>(pick_logc(A, UL / A, cap), uint32_t(col_logc_cap));
   pl->thr_f1 = threads_for(uint64_t(A) << pl->logc_f1);
   pl->smem_f1 = f1_smem_bytes(A, 1u << pl->logc_f1) +
@@ -477,8 +475,7 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   }
   // Ping-pong column passes (k_*_pp): radix <= 8 schedules, two tiles in
   // shared memory, up to 1024 threads.  Used whenever the two tiles of at
-  // least one column fit (TMG_NO_PP keeps the single-buffer passes).
-  static const bool no_pp = getenv("TMG_NO_PP") != nullptr;
+  // least one column fit.
   auto pp_logc = [&](uint32_t R, uint64_t ncols) -> int {
     const uint32_t p2 = largest_pow2_divisor(ncols);
     int best = -1;
@@ -491,7 +488,7 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
     return int(std::min<uint64_t>(kColPPThreads, std::max<uint64_t>(128, t)));
   };
   pl->colpp = false;
-  if (!no_pp) {
+  {
     const int lf1 = pp_logc(A, UL / A), lil = pp_logc(A, C / 2);
     int lf2 = 0, li2 = 0;
     if (pl->kind == 3) {
@@ -529,7 +526,7 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw) {
   pl->colct = nullptr;
   pl->colct_il = nullptr;
   pl->colct_b = nullptr;
-  if (pl->kind == 2 || pl->kind == 3) {
+  if ((pl->kind == 2 || pl->kind == 3) && !opt.generic_columns) {
     const ColCtShape* sf1 = colct_for(A, 1);
     const ColCtShape* sil = colct_for(A, 2);
     // three-pass plans also need the middle passes' shape over B

@@ -85,6 +85,13 @@ struct Plan {
   int kernels = 0;
 };
 
-std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw);
+// Plan-shape choices a context can switch for testing (tmg_context_set_option);
+// the defaults are the measured-best shapes.
+struct PlanOptions {
+  bool generic_columns = false;  // runtime-dispatched column passes, not the compiled shapes
+  bool force_three_pass = false; // three-pass plans for short column lengths
+};
+
+std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw, const PlanOptions& opt);
 
 }  // namespace tmg

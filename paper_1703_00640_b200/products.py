@@ -97,8 +97,8 @@ class Backend(enum.IntEnum):
 
 
 class Policy(enum.IntEnum):
-    REFERENCE = 0  # params.cpp exactly
-    ACCURATE = 1   # + FP64 error model and GPU cost ranking
+    REFERENCE = 0  # params.cpp exactly (the default, as products.hpp:60-61)
+    ACCURATE = 1   # opt-in: + FP64 error model and GPU cost ranking
 
 
 DEFAULT_FALLBACK_CUTOFF = 4096  # products.hpp:37
@@ -148,7 +148,7 @@ def validate_params(params: Params) -> None:
 
 def select_params(n: int, mode: Mode, backend: Backend = Backend.FFT,
                   fallback_cutoff: int = DEFAULT_FALLBACK_CUTOFF,
-                  policy: Policy = Policy.ACCURATE) -> Params:
+                  policy: Policy = Policy.REFERENCE) -> Params:
     out = tmg_params()
     _check(_native.load().tmg_select_params(n, int(mode), int(backend), fallback_cutoff,
                                             int(policy), ctypes.byref(out)))
@@ -242,6 +242,11 @@ class Context:
         """Recompute a refused single product at b - 1 (up to n times);
         0 keeps the reference behaviour (raise ConvolutionPrecisionFailure)."""
         _check(self._lib.tmg_context_set_escalation(self._h, int(max_escalations)))
+
+    def set_option(self, option: int, value: int = 1) -> None:
+        """Testing and diagnostics: select an alternative code path
+        (_native.TMG_OPT_*; include/truncmul_b200.h lists them)."""
+        _check(self._lib.tmg_context_set_option(self._h, int(option), int(value)))
 
     def close(self) -> None:
         if self._h:
@@ -388,7 +393,7 @@ def high_product(u, v, params: Params, ctx: Context | None = None) -> int:
 
 
 def multiply(mode: Mode, u, v, n: int | None = None, backend: Backend = Backend.FFT,
-             policy: Policy = Policy.ACCURATE, ctx: Context | None = None) -> int:
+             policy: Policy = Policy.REFERENCE, ctx: Context | None = None) -> int:
     """Convenience: select parameters like the reference CLI (truncmul_cli.cpp:
     99-150: n defaults to the longer operand, the oracle fallback below the
     cutoff) and run the product."""

@@ -24,6 +24,12 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden")
 TRIP = 0.25  # reference tripwire (products_f64.cpp:22)
 
 
+def sp(n, mode):
+    """The accurate policy's parameters (Numerics) -- an explicit
+    opt-in; select_params' default is the reference's params.cpp."""
+    return tm.select_params(n, mode, policy=tm.Policy.ACCURATE)
+
+
 def _check(mode, u, v, n, r):
     P = port.limbs_to_int(port.oracle_full(u, v))
     if mode == tm.Mode.FULL:
@@ -49,7 +55,7 @@ def test_random_products_match_exact(ctx, n):
     for _ in range(3):
         u, v = _rand(rng, n), _rand(rng, n)
         for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-            p = tm.select_params(n, mode)
+            p = sp(n, mode)
             r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
             _check(mode, u, v, n, r)
             assert ctx.last_stats.max_round_err <= TRIP
@@ -66,7 +72,7 @@ def test_golden_vectors(ctx):
         u = port.int_to_limbs(int(e["u"], 16), nl)
         v = port.int_to_limbs(int(e["v"], 16), nl)
         for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-            p = tm.select_params(n, mode)
+            p = sp(n, mode)
             try:
                 r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
             except tm.ConvolutionPrecisionFailure:
@@ -103,7 +109,7 @@ def test_gpu_agrees_with_port_on_tripwire(ctx):
         u = port.int_to_limbs(int(e["u"], 16), nl)
         v = port.int_to_limbs(int(e["v"], 16), nl)
         for mode in (tm.Mode.FULL, tm.Mode.LOW):
-            p = tm.select_params(n, mode)
+            p = sp(n, mode)
             try:
                 pe = port.product(mode.name.lower(), u, v, n, p.b, p.N, p.lam).max_err
             except port.ConvolutionPrecisionFailure:
@@ -121,7 +127,7 @@ def test_commutativity_and_consistency(ctx):
     rng = np.random.default_rng(11)
     n = 200000
     u, v = _rand(rng, n), _rand(rng, n)
-    pl, pf, ph = (tm.select_params(n, m) for m in (tm.Mode.LOW, tm.Mode.FULL, tm.Mode.HIGH))
+    pl, pf, ph = (sp(n, m) for m in (tm.Mode.LOW, tm.Mode.FULL, tm.Mode.HIGH))
     lo = tm.from_limbs(ctx.product_limbs(tm.Mode.LOW, u, v, pl))
     assert lo == tm.from_limbs(ctx.product_limbs(tm.Mode.LOW, v, u, pl))
     fu = tm.from_limbs(ctx.product_limbs(tm.Mode.FULL, u, v, pf))
@@ -142,7 +148,7 @@ def test_structured_operands(ctx, n):
         for b_ in (vals[0], vals[1], vals[-2], a):
             u, v = port.int_to_limbs(a, nl), port.int_to_limbs(b_, nl)
             for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-                r = tm.from_limbs(ctx.product_limbs(mode, u, v, tm.select_params(n, mode)))
+                r = tm.from_limbs(ctx.product_limbs(mode, u, v, sp(n, mode)))
                 _check(mode, u, v, n, r)
 
 
@@ -161,7 +167,7 @@ def test_carry_chains_across_blocks(esc_ctx, n):
     for a, b_ in cases:
         u, v = port.int_to_limbs(a, nl), port.int_to_limbs(b_, nl)
         for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-            r = tm.from_limbs(esc_ctx.product_limbs(mode, u, v, tm.select_params(n, mode)))
+            r = tm.from_limbs(esc_ctx.product_limbs(mode, u, v, sp(n, mode)))
             _check(mode, u, v, n, r)
 
 
@@ -179,7 +185,7 @@ def test_unsigned_split_products(ctx):
     rng = np.random.default_rng(5)
     u, v = _rand(rng, n), _rand(rng, n)
     for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-        ref = tm.select_params(n, mode)
+        ref = sp(n, mode)
         b = ref.b - 4
         cover = -(-n // b)
         N = next(x for x in range(cover + (4 if mode == tm.Mode.HIGH else 0), 4 * cover)
@@ -201,7 +207,7 @@ def _factors(x):
 
 
 def test_input_out_of_range(ctx):
-    p = tm.select_params(8192, tm.Mode.LOW)
+    p = sp(8192, tm.Mode.LOW)
     with pytest.raises(tm.InputOutOfRange):
         tm.low_product(1 << 8192, 3, p, ctx)
     with pytest.raises(tm.InputOutOfRange):
@@ -213,7 +219,7 @@ def test_fallback_below_cutoff(ctx):
     for n in (1, 7, 64, 65, 1000, 4095):
         u, v = _rand(rng, n), _rand(rng, n)
         for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-            p = tm.select_params(n, mode)
+            p = sp(n, mode)
             assert p.mode == tm.Mode.ORACLE_FALLBACK
             r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
             P = port.limbs_to_int(u) * port.limbs_to_int(v)
@@ -230,7 +236,7 @@ def test_device_path_matches_host_path(ctx):
     n = 1 << 20
     rng = np.random.default_rng(9)
     u, v = _rand(rng, n), _rand(rng, n)
-    p = tm.select_params(n, tm.Mode.LOW)
+    p = sp(n, tm.Mode.LOW)
     host = ctx.product_limbs(tm.Mode.LOW, u, v, p)
     du = torch.from_numpy(u.view(np.int64)).cuda()
     dv = torch.from_numpy(v.view(np.int64)).cuda()
@@ -248,12 +254,13 @@ import numpy as np
 import torch
 import paper_1703_00640_b200 as tm
 from oracle import port
+sp = lambda n, m: tm.select_params(n, m, policy=tm.Policy.ACCURATE)
 ctx = tm.Context(0)
 bad = 0
 for n in (1 << 20, 1 << 22):
     nl = n // 64
     rng = np.random.default_rng(n)
-    p = tm.select_params(n, tm.Mode.LOW)
+    p = sp(n, tm.Mode.LOW)
     for rep in range(4):
         a = rng.integers(0, 2**64, nl, dtype=np.uint64)
         b = rng.integers(0, 2**64, nl, dtype=np.uint64)
@@ -272,7 +279,7 @@ for n in (1 << 20, 1 << 22):
         bad += sum(g != x for g, x in zip(got, xs))
 # a multi-pass product, then fused small products reading its output
 n1, n2 = 1 << 20, 1 << 16
-p1, p2 = tm.select_params(n1, tm.Mode.LOW), tm.select_params(n2, tm.Mode.LOW)
+p1, p2 = sp(n1, tm.Mode.LOW), sp(n2, tm.Mode.LOW)
 rng = np.random.default_rng(5)
 for rep in range(4):
     a = rng.integers(0, 2**64, n1 // 64, dtype=np.uint64)
@@ -317,7 +324,7 @@ def test_chained_device_products():
 def test_config1_low_2p20_seed1(ctx):
     n = 1 << 20
     u, v = port.config_operands(1, n // 64)
-    p = tm.select_params(n, tm.Mode.LOW)
+    p = sp(n, tm.Mode.LOW)
     r = ctx.product_limbs(tm.Mode.LOW, u, v, p)
     assert np.array_equal(r, port.oracle_low(u, v, n))
     assert ctx.last_stats.max_round_err < TRIP
@@ -326,7 +333,7 @@ def test_config1_low_2p20_seed1(ctx):
 def test_config2_high_2p24_seed2(ctx):
     n = 1 << 24
     u, v = port.config_operands(2, n // 64, force_top_bit=True)
-    p = tm.select_params(n, tm.Mode.HIGH)
+    p = sp(n, tm.Mode.HIGH)
     w = tm.from_limbs(ctx.product_limbs(tm.Mode.HIGH, u, v, p))
     assert port.is_valid_high(u, v, n, w)
     assert ctx.last_stats.max_round_err < TRIP
@@ -342,7 +349,7 @@ def test_config3_full_low_high_2p26_seed3(ctx):
     u, v = port.config_operands(3, n // 64)
     P = port.limbs_to_int(port.oracle_full(u, v))
     for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-        p = tm.select_params(n, mode)
+        p = sp(n, mode)
         r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
         if mode == tm.Mode.FULL:
             assert r == P
@@ -374,7 +381,7 @@ def test_config4_batched_low_2p16_seed4(ctx):
     w = port.mt19937_64(4, 2 * count * nl).reshape(count, 2, nl)
     u = np.ascontiguousarray(w[:, 0, :])
     v = np.ascontiguousarray(w[:, 1, :])
-    p = tm.select_params(n, tm.Mode.LOW)
+    p = sp(n, tm.Mode.LOW)
     out, flags = ctx.product_batched(p, u, v, return_flags=True)
     assert not flags.any()
     for i in range(count):
@@ -389,48 +396,155 @@ def esc_ctx():
     c.close()
 
 
+def _stress_operand(pattern, nl):
+    if pattern == "ones":
+        return np.full(nl, np.uint64(0xFFFFFFFFFFFFFFFF))
+    u = np.zeros(nl, dtype=np.uint64)
+    u[0::2] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    return u
+
+
 @pytest.mark.parametrize("pattern", ["ones", "alternating"])
 @pytest.mark.parametrize("mode", [tm.Mode.LOW, tm.Mode.HIGH])
-def test_config5_stress_2p28(esc_ctx, pattern, mode):
+def test_config5_stress_2p28(ctx, pattern, mode):
     """BASELINE config 5: u = v = 2^n - 1 and alternating all-ones / zero
-    limbs at n = 2^28.  The alternating pattern concentrates the spectrum on
-    a few lines, outside the random-input error model the accurate policy
-    uses; with escalation the product is recomputed at b - 1 when the first
-    attempt refuses, and the result must be exact either way."""
+    limbs at n = 2^28, on the default path (no escalation) at the
+    reference's own parameters (the accurate policy picks the same ones
+    here).  The alternating pattern concentrates the spectrum on a few
+    lines; the result must certify at the first attempt, below the wire
+    (low <= 1/4, high < 1/4), and be exact."""
     n = 1 << 28
-    nl = n // 64
-    if pattern == "ones":
-        u = np.full(nl, np.uint64(0xFFFFFFFFFFFFFFFF))
-    else:
-        u = np.zeros(nl, dtype=np.uint64)
-        u[0::2] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    u = _stress_operand(pattern, n // 64)
     v = u.copy()
     p = tm.select_params(n, mode)
-    r = tm.from_limbs(esc_ctx.product_limbs(mode, u, v, p))
-    st = esc_ctx.last_stats
-    print(f"stress {pattern} {mode.name}: first attempt b={p.b} residual {st.first_round_err:.4f}; "
-          f"result from attempt {st.attempts} (b={st.b}, N={st.N}) residual {st.max_round_err:.4f}")
-    assert st.max_round_err < TRIP
-    assert st.attempts == 1 or (st.escalated and st.b < p.b and st.first_round_err >= TRIP)
+    assert (p.b, p.N, p.lam) == (12, 22937600, 5)
+    assert sp(n, mode) == p
+    r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
+    st = ctx.last_stats
+    print(f"stress {pattern} {mode.name}: b={p.b} N={p.N} residual {st.max_round_err:.4f}")
+    assert st.attempts == 1 and not st.escalated
+    if mode == tm.Mode.LOW:
+        assert st.max_round_err <= TRIP
+    else:
+        assert st.max_round_err < TRIP
     _check(mode, u, v, n, r)
 
 
 def test_escalation_recovers_refused_alternating_product(esc_ctx, ctx):
-    """2^22 alternating limbs: the accurate-policy b = 13 refuses on the GPU
-    (and the reference refuses the same pattern at 2^24); escalation returns
-    the exact low product."""
-    n = 1 << 22
-    u = np.zeros(n // 64, dtype=np.uint64)
-    u[0::2] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    """2^24 alternating limbs at b = 13 refuse on the GPU and in the
+    reference-order port alike; escalation (an opt-in of this library)
+    recomputes at b - 1 and returns the exact low product."""
+    n = 1 << 24
+    u = _stress_operand("alternating", n // 64)
     p = tm.select_params(n, tm.Mode.LOW)
-    try:
-        r0 = ctx.product_limbs(tm.Mode.LOW, u, u, p)
-        assert np.array_equal(r0, port.oracle_low(u, u, n))
-    except tm.ConvolutionPrecisionFailure:
-        pass
+    with pytest.raises(tm.ConvolutionPrecisionFailure):
+        ctx.product_limbs(tm.Mode.LOW, u, u, p)
     r = esc_ctx.product_limbs(tm.Mode.LOW, u, u, p)
     assert np.array_equal(r, port.oracle_low(u, u, n))
-    assert esc_ctx.last_stats.max_round_err < TRIP
+    assert esc_ctx.last_stats.escalated and esc_ctx.last_stats.max_round_err < TRIP
+
+
+# --------------------------------------------------------------------------
+# Certify / refuse parity with the reference at its own parameters
+# (Policy.REFERENCE = params.cpp, the default) on the default context: where
+# the oracle port -- the reference's pipeline in its operation order,
+# convolution.cpp:186-192 -- certifies, the GPU must certify too, be exact,
+# and stay within one 1/16 of the port's residual; where the port refuses,
+# the GPU may refuse or certify, and a certified result must be exact.
+SLACK = 0.0625
+
+
+def _ref_parity(ctx, mode, u, v, n, p=None):
+    p = p or tm.select_params(n, mode)
+    assert p == tm.select_params(n, mode, policy=tm.Policy.REFERENCE)
+    try:
+        pe = port.product(mode.name.lower(), u, v, n, p.b, p.N, p.lam).max_err
+    except port.ConvolutionPrecisionFailure:
+        pe = None
+    try:
+        r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
+        ge = ctx.last_stats.max_round_err
+    except tm.ConvolutionPrecisionFailure:
+        r, ge = None, None
+    if pe is not None:
+        assert ge is not None, (mode.name, n, "port certifies at", pe, "GPU refuses")
+        assert ge <= pe + SLACK, (mode.name, n, ge, pe)
+    if r is not None:
+        _check(mode, u, v, n, r)
+        assert ge <= TRIP
+    return pe, ge
+
+
+def test_reference_fft_products_8192_seed14(ctx):
+    """test_products.cpp:371-391: n = 8192, mt19937_64(0x14), ten random pairs
+    through low / high / full, then the all-ones operand (low, full)."""
+    n = 8192
+    for u, v in port.random_bits_pairs(0x14, n, 10):
+        for mode in (tm.Mode.LOW, tm.Mode.HIGH, tm.Mode.FULL):
+            _ref_parity(ctx, mode, u, v, n)
+    top = _stress_operand("ones", n // 64)
+    for mode in (tm.Mode.LOW, tm.Mode.FULL):
+        pe, ge = _ref_parity(ctx, mode, top, top, n)
+        assert pe is not None and ge is not None
+
+
+def test_reference_fft_products_5001_seed15(ctx):
+    """test_products.cpp:393-406: n = 5001 (covering slack), mt19937_64(0x15),
+    six random pairs through low and high."""
+    n = 5001
+    for u, v in port.random_bits_pairs(0x15, n, 6):
+        for mode in (tm.Mode.LOW, tm.Mode.HIGH):
+            _ref_parity(ctx, mode, u, v, n)
+
+
+def test_reference_policy_config1(ctx):
+    n = 1 << 20
+    u, v = port.config_operands(1, n // 64)
+    _ref_parity(ctx, tm.Mode.LOW, u, v, n)
+
+
+def test_reference_policy_config2(ctx):
+    n = 1 << 24
+    u, v = port.config_operands(2, n // 64, force_top_bit=True)
+    _ref_parity(ctx, tm.Mode.HIGH, u, v, n)
+
+
+@pytest.mark.parametrize("mode", [tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH])
+def test_reference_policy_config3(ctx, mode):
+    n = 1 << 26
+    u, v = port.config_operands(3, n // 64)
+    _ref_parity(ctx, mode, u, v, n)
+
+
+def test_reference_policy_config4(ctx):
+    """4096 x 2^16 low products at the reference's parameters in one batch:
+    per-product flags agree with the port's certify / refuse on a sample,
+    every certified product exact."""
+    n, count = 1 << 16, 4096
+    nl = n // 64
+    w = port.mt19937_64(4, 2 * count * nl).reshape(count, 2, nl)
+    u = np.ascontiguousarray(w[:, 0, :])
+    v = np.ascontiguousarray(w[:, 1, :])
+    p = tm.select_params(n, tm.Mode.LOW)
+    out, flags = ctx.product_batched(p, u, v, return_flags=True)
+    for i in range(count):
+        if not flags[i]:
+            assert np.array_equal(out[i], port.oracle_low(u[i], v[i], n)), i
+    for i in range(0, count, 64):
+        try:
+            port.product("low", u[i], v[i], n, p.b, p.N, p.lam)
+            assert not flags[i], i
+        except port.ConvolutionPrecisionFailure:
+            pass
+
+
+@pytest.mark.parametrize("pattern", ["ones", "alternating"])
+@pytest.mark.parametrize("mode", [tm.Mode.LOW, tm.Mode.HIGH])
+def test_reference_policy_config5(ctx, pattern, mode):
+    n = 1 << 28
+    u = _stress_operand(pattern, n // 64)
+    pe, ge = _ref_parity(ctx, mode, u, u.copy(), n)
+    assert ge is not None  # the default path certifies config 5
 
 
 # --------------------------------------------------------------------------
@@ -518,7 +632,7 @@ def test_batched_multipass_products(ctx, mode, lg):
     w = port.mt19937_64(17 + int(mode), 2 * count * nl).reshape(count, 2, nl)
     u = np.ascontiguousarray(w[:, 0, :])
     v = np.ascontiguousarray(w[:, 1, :])
-    p = tm.select_params(n, mode)
+    p = sp(n, mode)
     out, flags = ctx.product_batched(p, u, v, return_flags=True)
     assert ctx.last_stats.transform_length > 8192
     assert not flags.any()
@@ -551,69 +665,158 @@ def test_compiled_column_shapes_exact(ctx, A):
         assert ctx.last_stats.max_round_err < TRIP
 
 
-_FALLBACK_SNIPPET = r"""
-import sys, numpy as np
-sys.path.insert(0, '.')
-import paper_1703_00640_b200 as tm
-from oracle import port
-ctx = tm.default_context(0)
-n = 1 << 26
-u, v = port.config_operands(3, n // 64)
-P = port.limbs_to_int(port.oracle_full(u, v))
-for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-    p = tm.select_params(n, mode)
-    r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
-    if mode == tm.Mode.FULL:
-        assert r == P
-    elif mode == tm.Mode.LOW:
-        assert r == P & ((1 << n) - 1)
-    else:
-        assert abs(P - (r << n)) < (1 << n) and 0 <= r <= (1 << n)
-print("ok")
-"""
+def _opt_ctx(*opts):
+    c = tm.Context(0)
+    for o, v in opts:
+        c.set_option(o, v)
+    return c
+
+
+def _config3_all_modes(c, n=1 << 26):
+    u, v = port.config_operands(3, (n + 63) // 64)
+    P = port.limbs_to_int(port.oracle_full(u, v))
+    for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+        r = tm.from_limbs(c.product_limbs(mode, u, v, sp(n, mode)))
+        if mode == tm.Mode.FULL:
+            assert r == P
+        elif mode == tm.Mode.LOW:
+            assert r == P & ((1 << n) - 1)
+        else:
+            assert abs(P - (r << n)) < (1 << n) and 0 <= r <= (1 << n)
+        assert c.last_stats.max_round_err < TRIP
 
 
 def test_generic_passes_at_compiled_lengths():
-    """TMG_NO_COLCT: the runtime-dispatched column passes (radix-16/4/3
-    schedules of 1728 and 1440) give the same products as the compiled
-    prime-factor ones (BASELINE config 3 lengths)."""
-    import subprocess
-    import sys
-    env = dict(os.environ, TMG_NO_COLCT="1")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", _FALLBACK_SNIPPET], cwd=root, env=env,
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+    """TMG_OPT_GENERIC_COLUMN_PASSES: the runtime-dispatched column passes
+    (radix-16/4/3 schedules of 1728 and 1440) give the same products as the
+    compiled prime-factor ones (BASELINE config 3 lengths)."""
+    c = _opt_ctx((tm._native.TMG_OPT_GENERIC_COLUMN_PASSES, 1))
+    _config3_all_modes(c)
+    c.close()
 
 
-_CARRY_SNIPPET = """
-import sys
-sys.path.insert(0, '.')
-import paper_1703_00640_b200 as tm
-from oracle import port
-ctx = tm.Context(0)
-for n in (1 << 20, (1 << 22) + 448):
-    u, v = port.config_operands(3, (n + 63) // 64)
-    P = port.limbs_to_int(port.oracle_full(u, v))
-    assert tm.from_limbs(ctx.product_limbs(tm.Mode.FULL, u, v, tm.select_params(n, tm.Mode.FULL))) == P
-    assert tm.from_limbs(ctx.product_limbs(tm.Mode.LOW, u, v, tm.select_params(n, tm.Mode.LOW))) == P % (1 << n)
-    w = tm.from_limbs(ctx.product_limbs(tm.Mode.HIGH, u, v, tm.select_params(n, tm.Mode.HIGH)))
-    assert 0 <= w <= (1 << n) and abs(P - (w << n)) < (1 << n)
-print("ok")
-"""
+def test_generic_row_pass():
+    """TMG_OPT_GENERIC_ROW_PASS: the runtime-dispatched row pass (k_mid) in
+    place of the compiled C = 4096 one, two- and three-pass plans."""
+    c = _opt_ctx((tm._native.TMG_OPT_GENERIC_ROW_PASS, 1))
+    _config3_all_modes(c, 1 << 22)
+    c.close()
+    c = _opt_ctx((tm._native.TMG_OPT_GENERIC_ROW_PASS, 1), (tm._native.TMG_OPT_FORCE_THREE_PASS, 1))
+    _config3_all_modes(c, 1 << 22)
+    assert c.last_stats.passes == 3
+    c.close()
 
 
-def test_carry_in_from_the_lanes_ticket():
-    """TMG_PATCH_SCAN_MAX=0: full, low and high products take the carry-ins the
-    last k_carry_lanes block scans (the path above 4096 carry blocks, n >~
-    2^27) instead of k_carry_patch's own scan; the results must not change."""
-    import subprocess
-    import sys
-    env = dict(os.environ, TMG_PATCH_SCAN_MAX="0")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", _CARRY_SNIPPET], cwd=root, env=env,
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+@pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 448])
+def test_carry_in_from_the_lanes_ticket(n):
+    """TMG_OPT_PATCH_SCAN_MAX = 0: full, low and high products take the
+    carry-ins the last k_carry_lanes block scans (the path above 4096 carry
+    blocks, n >~ 2^27) instead of k_carry_patch's own scan."""
+    c = _opt_ctx((tm._native.TMG_OPT_PATCH_SCAN_MAX, 0))
+    _config3_all_modes(c, n)
+    c.close()
+
+
+@pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 448, 1 << 24])
+def test_lookback_carry_path(n):
+    """TMG_OPT_LOOKBACK_CARRY: the single-pass decoupled look-back carry
+    (k_carry) and the high product's k_high_agg -- the path the library takes
+    beyond 2^32 carry bits -- give the same products."""
+    c = _opt_ctx((tm._native.TMG_OPT_LOOKBACK_CARRY, 1))
+    _config3_all_modes(c, n)
+    c.close()
+
+
+def test_lookback_carry_structured_operands():
+    """Long carry chains through the look-back carry (all-ones operands)."""
+    c = _opt_ctx((tm._native.TMG_OPT_LOOKBACK_CARRY, 1))
+    n = (1 << 20) + 3
+    nl = (n + 63) // 64
+    M = (1 << n) - 1
+    for a, b_ in ((M, M), (M, 1 << (n - 1)), ((1 << n) - (1 << 1000), M - 5)):
+        u, v = port.int_to_limbs(a, nl), port.int_to_limbs(b_, nl)
+        for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+            try:
+                r = tm.from_limbs(c.product_limbs(mode, u, v, sp(n, mode)))
+            except tm.ConvolutionPrecisionFailure:
+                continue
+            _check(mode, u, v, n, r)
+    c.close()
+
+
+def test_check_clears_a_refused_status(ctx):
+    """A refused device-pointer product raises at the next tmg_check, and the
+    check after it -- of good products only -- passes: the status word is
+    cleared before the error is reported."""
+    import torch
+    bad = tm.manual_params(3840, 30, 128, tm.Mode.LOW, tm.Backend.FFT, signed_split=False, lam=4)
+    top = np.full(60, np.uint64(0xFFFFFFFFFFFFFFFF))
+    n = 1 << 20
+    good = sp(n, tm.Mode.LOW)
+    rng = np.random.default_rng(3)
+    u, v = _rand(rng, n), _rand(rng, n)
+    dt = torch.from_numpy(top.view(np.int64)).cuda()
+    dtout = torch.zeros(60, dtype=torch.int64, device="cuda")
+    du = torch.from_numpy(u.view(np.int64)).cuda()
+    dv = torch.from_numpy(v.view(np.int64)).cuda()
+    out = torch.zeros(n // 64, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    c = tm.Context(0)
+    c.product_device(bad, dt.data_ptr(), dt.data_ptr(), dtout.data_ptr(), 1)
+    with pytest.raises(tm.ConvolutionPrecisionFailure):
+        c.check()
+    c.product_device(good, du.data_ptr(), dv.data_ptr(), out.data_ptr(), 1)
+    c.check()
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), port.oracle_low(u, v, n))
+    c.close()
+
+
+def test_contexts_sharing_one_stream_chain():
+    """Two contexts on one caller stream, each product reading the previous
+    one's output (written by the other context's kernels, still in flight):
+    device-pointer products wait for their predecessor before reading."""
+    import torch
+    n = 1 << 20
+    nl = n // 64
+    s = torch.cuda.Stream()
+    c1, c2 = tm.Context(0), tm.Context(0)
+    c1.set_stream(s.cuda_stream)
+    c2.set_stream(s.cuda_stream)
+    p = sp(n, tm.Mode.LOW)
+    rng = np.random.default_rng(17)
+    a, b = _rand(rng, n), _rand(rng, n)
+    bufs = [torch.from_numpy(x.view(np.int64)).cuda() for x in (a, b)]
+    bufs += [torch.zeros(nl, dtype=torch.int64, device="cuda") for _ in range(8)]
+    torch.cuda.synchronize()
+    for k in range(8):
+        (c1 if k % 2 == 0 else c2).product_device(p, bufs[k].data_ptr(), bufs[k + 1].data_ptr(),
+                                                   bufs[k + 2].data_ptr(), 1)
+    c1.check()
+    c2.check()
+    M = (1 << n) - 1
+    xs = [port.limbs_to_int(a), port.limbs_to_int(b)]
+    for k in range(8):
+        xs.append(xs[k] * xs[k + 1] & M)
+    got = [port.limbs_to_int(t.cpu().numpy().view(np.uint64)) for t in bufs]
+    assert got == xs
+    c1.close()
+    c2.close()
+
+
+def test_plan_cache_distinguishes_every_param_field(ctx):
+    """Params equal in (n, b, N, lambda, mode) but not in signed_split or p
+    must not share a cached plan: the unsigned split after the signed one is
+    still exact, and a wrong p is refused on a would-be cache hit."""
+    n = 20000
+    rng = np.random.default_rng(23)
+    u, v = _rand(rng, n), _rand(rng, n)
+    ps = tm.manual_params(n, 10, 2048, tm.Mode.LOW, tm.Backend.FFT, signed_split=True)
+    pu = tm.manual_params(n, 10, 2048, tm.Mode.LOW, tm.Backend.FFT, signed_split=False)
+    for p in (ps, pu):
+        assert np.array_equal(ctx.product_limbs(tm.Mode.LOW, u, v, p), port.oracle_low(u, v, n))
+    from dataclasses import replace
+    with pytest.raises(tm.Error):
+        ctx.product_limbs(tm.Mode.LOW, u, v, replace(ps, p=ps.p + 7))
 
 
 def test_batched_graph_replay(ctx):
@@ -623,7 +826,7 @@ def test_batched_graph_replay(ctx):
     reallocates the workspaces, which must invalidate the captured graph."""
     n, count = 1 << 18, 10
     nl = n // 64
-    p = tm.select_params(n, tm.Mode.LOW)
+    p = sp(n, tm.Mode.LOW)
     # reps 0-2: eager, capture, replay; the larger batch before rep 3
     # reallocates; reps 3-5: eager, capture, replay again
     for rep in range(6):
@@ -632,7 +835,7 @@ def test_batched_graph_replay(ctx):
             nb = 1 << 20
             wb = port.mt19937_64(99, 2 * 4 * (nb // 64)).reshape(4, 2, nb // 64)
             ub, vb = np.ascontiguousarray(wb[:, 0, :]), np.ascontiguousarray(wb[:, 1, :])
-            pb = tm.select_params(nb, tm.Mode.LOW)
+            pb = sp(nb, tm.Mode.LOW)
             outb = ctx.product_batched(pb, ub, vb)
             for i in range(4):
                 _check(tm.Mode.LOW, ub[i], vb[i], nb, tm.from_limbs(outb[i]))
@@ -652,7 +855,7 @@ def test_batched_full_2p16_compiled_small_kernel(ctx):
     nl = n // 64
     w = port.mt19937_64(61, 2 * count * nl).reshape(count, 2, nl)
     u, v = np.ascontiguousarray(w[:, 0, :]), np.ascontiguousarray(w[:, 1, :])
-    p = tm.select_params(n, tm.Mode.FULL)
+    p = sp(n, tm.Mode.FULL)
     out, flags = ctx.product_batched(p, u, v, return_flags=True)
     assert ctx.last_stats.transform_length == 6144
     assert not flags.any()

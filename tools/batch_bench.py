@@ -24,7 +24,7 @@ def main():
     w = port.mt19937_64(4, 2 * count * nl).reshape(count, 2, nl)
     u = np.ascontiguousarray(w[:, 0, :])
     v = np.ascontiguousarray(w[:, 1, :])
-    p = tm.select_params(n, mode)
+    p = tm.select_params(n, mode, policy=tm.Policy.ACCURATE)
     ctx = tm.Context(0)
     dev = torch.device("cuda:0")
     stream = torch.cuda.current_stream(dev)

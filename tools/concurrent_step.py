@@ -12,7 +12,7 @@ dev = torch.device('cuda:0')
 du = torch.from_numpy(u.view(np.int64)).to(dev)
 dv = torch.from_numpy(v.view(np.int64)).to(dev)
 modes = (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH)
-params = {m: tm.select_params(n, m) for m in modes}
+params = {m: tm.select_params(n, m, policy=tm.Policy.ACCURATE) for m in modes}
 outs = {m: torch.zeros(tm.output_limbs(m, n), dtype=torch.int64, device=dev) for m in modes}
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 ctxs = {m: tm.Context(0) for m in modes}

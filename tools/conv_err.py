@@ -58,11 +58,12 @@ def main():
         v = u
     else:
         u, v = port.config_operands(int(pattern), nl)
-    p = tm.select_params(n, mode)
+    p = tm.select_params(n, mode, policy=tm.Policy.ACCURATE)
     if len(sys.argv) > 4:  # manual N (and lambda from the reference rule)
         Nm = int(sys.argv[4])
         p = tm.manual_params(n, p.b, Nm, mode, tm.Backend.FFT, True)
     ctx = tm.Context(0)
+    ctx.set_option(_native.TMG_OPT_Z_NATURAL, 1)  # z read back in natural order
     try:
         ctx.product_limbs(mode, u, v, p)
         st = "ok"

@@ -6,7 +6,7 @@ ctx = tm.Context(0); dev = torch.device('cuda:0'); st = torch.cuda.current_strea
 for lg in (18, 20):
     n = 1 << lg; u, v = port.config_operands(7, n // 64)
     du = torch.from_numpy(u.view(np.int64)).to(dev); dv = torch.from_numpy(v.view(np.int64)).to(dev)
-    p = tm.select_params(n, tm.Mode.LOW); out = torch.zeros(tm.output_limbs(tm.Mode.LOW, n), dtype=torch.int64, device=dev)
+    p = tm.select_params(n, tm.Mode.LOW, policy=tm.Policy.ACCURATE); out = torch.zeros(tm.output_limbs(tm.Mode.LOW, n), dtype=torch.int64, device=dev)
     for _ in range(5): ctx.product_device(p, du.data_ptr(), dv.data_ptr(), out.data_ptr(), 1)
     torch.cuda.synchronize()
     t0 = time.perf_counter(); R = 200

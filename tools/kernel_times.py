@@ -7,7 +7,7 @@ for lg in [int(x) for x in (sys.argv[1:] or ["20", "22"])]:
     n = 1 << lg; u, v = port.config_operands(7, n // 64)
     du = torch.from_numpy(u.view(np.int64)).to(dev); dv = torch.from_numpy(v.view(np.int64)).to(dev)
     for mode in (tm.Mode.LOW, tm.Mode.FULL, tm.Mode.HIGH):
-        p = tm.select_params(n, mode); out = torch.zeros(tm.output_limbs(mode, n), dtype=torch.int64, device=dev)
+        p = tm.select_params(n, mode, policy=tm.Policy.ACCURATE); out = torch.zeros(tm.output_limbs(mode, n), dtype=torch.int64, device=dev)
         for _ in range(3): ctx.product_device(p, du.data_ptr(), dv.data_ptr(), out.data_ptr(), 1)
         ctx.check(); ctx.profile(True)
         for _ in range(5): ctx.product_device(p, du.data_ptr(), dv.data_ptr(), out.data_ptr(), 1)

@@ -10,7 +10,7 @@ n = 1 << int(sys.argv[2])
 seed = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 nl = (n + 63) // 64
 u, v = port.config_operands(seed, nl)
-p = tm.select_params(n, mode)
+p = tm.select_params(n, mode, policy=tm.Policy.ACCURATE)
 print("params", p, flush=True)
 ctx = tm.default_context(0)
 t0 = time.time()

@@ -11,5 +11,5 @@ u, v = port.config_operands(3, n // 64)
 ctx = tm.default_context(0)
 for rep in range(2):
     for m in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-        ctx.product_limbs(m, u, v, tm.select_params(n, m))
+        ctx.product_limbs(m, u, v, tm.select_params(n, m, policy=tm.Policy.ACCURATE))
 print("done")

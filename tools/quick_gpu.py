@@ -14,7 +14,7 @@ for n in [int(x) for x in (sys.argv[1:] or ["8192", "5001", "65536", "262144", "
         u[-1] &= np.uint64((1 << (n % 64)) - 1); v[-1] &= np.uint64((1 << (n % 64)) - 1)
     P = port.limbs_to_int(port.oracle_full(u, v))
     for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-        p = tm.select_params(n, mode)
+        p = tm.select_params(n, mode, policy=tm.Policy.ACCURATE)
         try:
             t0 = time.time()
             r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))

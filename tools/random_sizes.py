@@ -27,7 +27,7 @@ def main():
         v = port.int_to_limbs(int.from_bytes(rng.bytes(nl * 8), "little") & ((1 << n) - 1), nl)
         P = port.limbs_to_int(port.oracle_full(u, v))
         for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-            p = tm.select_params(n, mode)
+            p = tm.select_params(n, mode, policy=tm.Policy.ACCURATE)
             try:
                 r = tm.from_limbs(ctx.product_limbs(mode, u, v, p))
                 if mode == tm.Mode.FULL:

@@ -30,7 +30,7 @@ def main():
         du = torch.from_numpy(u.view(np.int64)).to(dev)
         dv = torch.from_numpy(v.view(np.int64)).to(dev)
         for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
-            p = tm.select_params(n, mode)
+            p = tm.select_params(n, mode, policy=tm.Policy.ACCURATE)
             out = torch.zeros(tm.output_limbs(mode, n), dtype=torch.int64, device=dev)
             reps = max(3, min(200, (1 << 26) // n))
             for _ in range(3):

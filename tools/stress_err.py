@@ -30,7 +30,7 @@ def main():
         for pattern in ("ones", "alternating"):
             u = operands(pattern, n // 64)
             for mode in (tm.Mode.LOW, tm.Mode.HIGH, tm.Mode.FULL):
-                p = tm.select_params(n, mode)
+                p = tm.select_params(n, mode, policy=tm.Policy.ACCURATE)
                 t = time.time()
                 try:
                     ctx.product_limbs(mode, u, u, p)
