@@ -194,7 +194,10 @@ enum {
   TMG_OPT_DEBUG_SYNC = 7,            /* synchronise and check after every launch */
   TMG_OPT_NO_GRAPH = 8,              /* multi-pass batches always enqueued eagerly */
   TMG_OPT_Z_NATURAL = 9,             /* pre-mapped coefficients stored in natural order */
-  TMG_OPT_GENERIC_SMALL = 10         /* runtime-dispatched stages in the fused small-product kernel */
+  TMG_OPT_GENERIC_SMALL = 10,        /* runtime-dispatched stages in the fused small-product kernel */
+  TMG_OPT_PREMAP_IN_SPLIT = 11       /* the split kernel applies the pre-map and stores 16-byte
+                                        coefficients (default: it stores digits and the first
+                                        column pass pre-maps, where a compiled shape allows) */
 };
 int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value);
 

@@ -353,10 +353,13 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         launch(cx, k_zstat, dim3((blocks + 255) / 256), dim3(256), 0, st, a, "zstat");
       }
       check_launch(cx, "k_zstat");
-      ZgenFn zg = zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda));
+      // with k_f1d_ct the split stores digits and the first column pass pre-maps
+      ZgenFn zg = pl.f1d ? zgen_digits_kernel(int(p.b), pl.zdig)
+                         : zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda));
+      const double zbytes = pl.f1d ? (pl.zdig == 1 ? 4.0 : 8.0) : 16.0;
       set_smem(zg, pl.smem_zgen);
       {
-        KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * 16.0, int(p.mode), st);
+        KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * zbytes, int(p.mode), st);
         launch(cx, zg, dim3(blocks), dim3(kZgenThreads), pl.smem_zgen, st, a, "zgen");
       }
       check_launch(cx, "k_zgen");
@@ -383,14 +386,17 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.cbits_u = w.cbu.as<uint32_t>();
       a.cbits_v = w.cbv.as<uint32_t>();
       a.aux = w.aux.as<double>();
-      auto f1k = pl.colct ? pl.colct->f1 : pl.colpp ? k_f1_pp : k_f1;
+      a.dig = w.work_z.p;
+      auto f1k = pl.f1d ? pl.f1d : pl.colct ? pl.colct->f1 : pl.colpp ? k_f1_pp : k_f1;
       set_smem(f1k, pl.smem_f1);
       {
-        KTimer kt(cx, "k_f1", double(p.N) * 16.0 + double(L) * 16.0, int(p.mode), st);
+        // k_f1d_ct reads the digit rows (the pre-map's halo row again, from L2)
+        const double zin = pl.f1d ? (pl.zdig == 1 ? 4.0 : 8.0) : 16.0;
+        KTimer kt(cx, "k_f1", double(p.N) * zin + double(L) * 16.0, int(p.mode), st);
         // the compile-time pass is persistent (one wave of CTAs)
         const unsigned tiles = a.ncols >> a.logc;
         const unsigned grid =
-            pl.colct ? std::min<unsigned>(tiles, unsigned(cx.num_sms * (pl.colct->nthr <= 288 ? 2 : 1)))
+            pl.colct ? std::min<unsigned>(tiles, unsigned(cx.num_sms * (pl.thr_f1 <= 288 ? 2 : 1)))
                      : tiles;
         launch(cx, f1k, dim3(grid), dim3(pl.thr_f1), pl.smem_f1, st, a, "f1");
       }
@@ -1196,8 +1202,9 @@ int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value) {
       case TMG_OPT_NO_PDL: o.no_pdl = on; break;
       case TMG_OPT_DEBUG_SYNC: o.debug_sync = on; break;
       case TMG_OPT_NO_GRAPH: o.no_graph = on; break;
-      case TMG_OPT_Z_NATURAL: o.z_natural = on; break;
+      case TMG_OPT_Z_NATURAL: o.z_natural = o.plan.z_natural = on; break;
       case TMG_OPT_GENERIC_SMALL: o.generic_small = on; break;
+      case TMG_OPT_PREMAP_IN_SPLIT: o.plan.premap_in_zgen = on; break;
       default: throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "unknown context option");
     }
     // plans and captured batch graphs were built under the old options

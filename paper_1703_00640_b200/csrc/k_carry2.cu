@@ -217,31 +217,6 @@ __device__ __forceinline__ void coeffs_block(const CarryArgs& a, const double* _
   }
 }
 
-// Bulk global -> shared copy completing on an mbarrier (cp.async.bulk; the
-// sizes and addresses are multiples of 16 bytes).
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  const uint32_t a = uint32_t(__cvta_generic_to_shared(bar));
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  const uint32_t a = uint32_t(__cvta_generic_to_shared(bar));
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  const uint32_t d = uint32_t(__cvta_generic_to_shared(dst));
-  const uint32_t b = uint32_t(__cvta_generic_to_shared(bar));
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  const uint32_t a = uint32_t(__cvta_generic_to_shared(bar));
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "MBW%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra MBW%=;\n}" ::"r"(a), "r"(phase) : "memory");
-}
-
 // High product: limb m of t feeds w0_{m-q} (bits r..63) and w0_{m-q-1}
 // (bits 0..r-1) of w0 = t >> s, q = s / 64, r = s % 64; a limb nominates the
 // w0 limbs its bits prove not all ones (the first such limb stops the

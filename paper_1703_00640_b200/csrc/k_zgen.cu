@@ -140,8 +140,29 @@ k_zstat(ZgenArgs a) {
 }
 
 // LAM: the series length lambda (rows of the pre-map), 0 for the full
-// product (the digits themselves).
-template <bool W32, int LAM>
+// product (the digits themselves).  DIG (LAM = 0 only): 0 stores the digits
+// as double2 coefficients, 1 as short2 and 2 as int2 (the digit form that
+// k_f1d_ct pre-maps itself).
+template <int DIG>
+struct DigOut;
+template <>
+struct DigOut<0> {
+  __device__ __forceinline__ static void put(void* z, uint32_t i, int2 d) {
+    static_cast<double2*>(z)[i] = make_double2(double(d.x), double(d.y));
+  }
+};
+template <>
+struct DigOut<1> {
+  __device__ __forceinline__ static void put(void* z, uint32_t i, int2 d) {
+    static_cast<short2*>(z)[i] = make_short2(short(d.x), short(d.y));
+  }
+};
+template <>
+struct DigOut<2> {
+  __device__ __forceinline__ static void put(void* z, uint32_t i, int2 d) { static_cast<int2*>(z)[i] = d; }
+};
+
+template <bool W32, int LAM, int DIG = 0>
 __global__ void __launch_bounds__(kZgenThreads)
 k_zgen_t(ZgenArgs a) {
   pdl_trigger();
@@ -350,13 +371,12 @@ k_zgen_t(ZgenArgs a) {
       for (int32_t jl = tid; jl < nloc; jl += kZgenThreads) {
         const int2 d = dig[zpad(jl)];
         const uint32_t col = col0 + uint32_t(jl);
-        a.z[((col >> zt.logc) * zt.zrows + row0) * (cm + 1) + (col & cm)] =
-            make_double2(double(d.x), double(d.y));
+        DigOut<DIG>::put(a.z, ((col >> zt.logc) * zt.zrows + row0) * (cm + 1) + (col & cm), d);
       }
     } else {
       for (int32_t jl = tid; jl < nloc; jl += kZgenThreads) {
         const int2 d = dig[zpad(jl)];
-        a.z[zt.index(uint32_t(c0 + jl))] = make_double2(double(d.x), double(d.y));
+        DigOut<DIG>::put(a.z, zt.index(uint32_t(c0 + jl)), d);
       }
     }
   } else {
@@ -447,6 +467,11 @@ ZgenFn zgen_kernel_l(int lam) {
 
 ZgenFn zgen_kernel(int b, int lam) {
   return b <= 32 ? zgen_kernel_l<true>(lam) : zgen_kernel_l<false>(lam);
+}
+
+ZgenFn zgen_digits_kernel(int b, int dig) {
+  if (b > 32) return nullptr;
+  return dig == 1 ? k_zgen_t<true, 0, 1> : k_zgen_t<true, 0, 2>;
 }
 
 }  // namespace tmg

@@ -113,6 +113,12 @@ constexpr int kZgenChunks = kZgenThreads * kZgenPer;
 __global__ void k_zstat(ZgenArgs a);
 typedef void (*ZgenFn)(ZgenArgs);
 ZgenFn zgen_kernel(int b, int lam);
+// Digit form for the first column pass's own pre-map (k_f1d_ct): the
+// balanced digits of both operands in z's tile order, as short2 (dig = 1,
+// b <= 14) or int2 (dig = 2), no pre-map.
+ZgenFn zgen_digits_kernel(int b, int dig);
+// digit element type of a chunk width for the digit form
+inline int zdig_kind(int b) { return b <= 14 ? 1 : 2; }
 size_t zgen_smem(int b);
 
 // F1: forward column DFTs over A of the pre-mapped coefficients.
@@ -136,6 +142,7 @@ struct F1Args {
   const uint32_t* cbits_u;
   const uint32_t* cbits_v;
   double* aux;  // [0] theta_u * theta_v
+  const void* dig;  // k_f1d_ct: balanced digits in z's tile order (short2 / int2)
 };
 __global__ void k_f1(F1Args a);
 size_t f1_smem_bytes(uint32_t A, uint32_t c);
@@ -196,6 +203,22 @@ struct ColCtShape {
   void (*col)(ColArgs);  // middle column pass (three-pass plans)
   uint32_t radl;  // radix of the last stage (output twiddle table)
 };
+// First column pass with the pre-map folded in (k_f1d.cu): compiled
+// schedules of at least four columns per CTA; fn[f1d_variant(lambda, dig)]
+// (nullptr where the pre-map's halo exceeds the tile).
+struct F1DShape {
+  uint32_t R;
+  int logc, nthr;
+  int rad[4];
+  uint32_t radl;
+  F1Fn fn[5];
+};
+const F1DShape* f1d_for(uint32_t R);
+int f1d_variant(int lam, int dig);
+// its shared memory: the colct tile, stage and twiddle tables, two buffers of
+// digit slabs (zrows x c pairs; two slabs per buffer with a pre-map), barriers
+size_t f1d_smem_bytes(uint32_t R, uint32_t c, uint32_t stablen, uint32_t radl, uint32_t zrows, int lam,
+                      int dig);
 // The compiled shape serving pass `role` (1 = F1, 2 = ilast) for column
 // length R, or nullptr (TMG_NO_COLCT disables them); colct_stages(R) is the
 // F1 shape's stage count (0 without one) for the parameter policy's cost

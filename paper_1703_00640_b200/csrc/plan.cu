@@ -572,6 +572,32 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw, const PlanOp
       }
     }
   }
+  // The first column pass applies the pre-map itself where a compiled shape
+  // with the same schedule and at least lambda - 1 columns per CTA exists:
+  // k_zgen then stores digits (4 or 8 bytes per chunk, not a 16-byte
+  // coefficient) and k_f1d_ct reads them.
+  pl->f1d = nullptr;
+  pl->zdig = 0;
+  if (pl->colct && !opt.premap_in_zgen && !opt.z_natural && b <= 30) {
+    const F1DShape* sd = f1d_for(A);
+    bool same = sd != nullptr;
+    for (int i = 0; same && i < 4; ++i) same = sd->rad[i] == pl->colct->rad[i];
+    const int lam = p.mode == PMode::kFull ? 0 : int(pl->mc.lambda);
+    const int dig = zdig_kind(int(b));
+    const int var = f1d_variant(lam, dig);
+    if (same && var >= 0 && sd->fn[var] && (lam == 0 || p.N == L)) {
+      const uint32_t cd = 1u << sd->logc;
+      const uint32_t zrows = uint32_t((p.N + (UL / A) - 1) / (UL / A));
+      const size_t sf = f1d_smem_bytes(A, cd, pl->fA.stablen, sd->radl, zrows, lam, dig);
+      if ((UL / A) % cd == 0 && sf <= kMaxDynSmem) {
+        pl->f1d = sd->fn[var];
+        pl->zdig = dig;
+        pl->logc_f1 = uint32_t(sd->logc);
+        pl->thr_f1 = sd->nthr;
+        pl->smem_f1 = sf;
+      }
+    }
+  }
   if (pl->colct) {
     pl->f1_stw = false;
   } else {

@@ -78,6 +78,8 @@ struct Plan {
   const ColCtShape* colct = nullptr;     // compile-time first column pass (k_f1_ct)
   const ColCtShape* colct_il = nullptr;  // compile-time last column pass (k_ilast_ct)
   const ColCtShape* colct_b = nullptr;   // three-pass plans: middle column passes (k_col_ct)
+  F1Fn f1d = nullptr;  // first column pass with the pre-map folded in (k_f1d_ct)
+  int zdig = 0;        // with f1d: k_zgen stores digits, 1 short2 / 2 int2
   int thr_f1 = 0, thr_f2 = 0, thr_i2 = 0, thr_il = 0, thr_mid = 0;
   size_t smem_zgen = 0;
   bool mid_shared_table = false;
@@ -90,6 +92,8 @@ struct Plan {
 struct PlanOptions {
   bool generic_columns = false;  // runtime-dispatched column passes, not the compiled shapes
   bool force_three_pass = false; // three-pass plans for short column lengths
+  bool premap_in_zgen = false;   // k_zgen pre-maps (double2 z), k_f1_ct reads z; not k_f1d_ct
+  bool z_natural = false;        // z in natural order (k_f1d_ct needs the tile order)
 };
 
 std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw, const PlanOptions& opt);

@@ -861,3 +861,35 @@ def test_batched_full_2p16_compiled_small_kernel(ctx):
     assert not flags.any()
     for i in range(count):
         _check(tm.Mode.FULL, u[i], v[i], n, tm.from_limbs(out[i]))
+
+
+@pytest.mark.parametrize("n", [1 << 26, (1 << 26) - 4099])
+def test_first_pass_premap_matches_split_premap(ctx, n):
+    """k_f1d_ct (the first column pass pre-maps the split's stored digits)
+    against TMG_OPT_PREMAP_IN_SPLIT (k_zgen pre-maps, k_f1_ct reads the
+    coefficients): same arithmetic in the same order, so identical products
+    and identical rounding residuals; both exact against GMP.  Seeded random
+    operands and the alternating / all-ones structured ones."""
+    old = _opt_ctx((tm._native.TMG_OPT_PREMAP_IN_SPLIT, 1))
+    nl = (n + 63) // 64
+    rng = np.random.default_rng(n)
+    alt = np.array([~0 if i % 2 == 0 else 0 for i in range(nl)], dtype=np.int64).view(np.uint64)
+    ones = np.full(nl, ~np.uint64(0), dtype=np.uint64)
+    if n % 64:
+        alt[-1] &= np.uint64((1 << (n % 64)) - 1)
+        ones[-1] &= np.uint64((1 << (n % 64)) - 1)
+    for u, v in ((_rand(rng, n), _rand(rng, n)), (alt, ones)):
+        for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+            p = sp(n, mode)
+            try:
+                a = ctx.product_limbs(mode, u, v, p)
+            except tm.ConvolutionPrecisionFailure:
+                with pytest.raises(tm.ConvolutionPrecisionFailure):
+                    old.product_limbs(mode, u, v, p)
+                continue
+            ea = ctx.last_stats.max_round_err
+            b = old.product_limbs(mode, u, v, p)
+            assert np.array_equal(a, b), mode
+            assert ea == old.last_stats.max_round_err, mode
+            _check(mode, u, v, n, tm.from_limbs(a))
+    old.close()
