@@ -197,7 +197,10 @@ enum {
   TMG_OPT_GENERIC_SMALL = 10,        /* runtime-dispatched stages in the fused small-product kernel */
   TMG_OPT_PREMAP_IN_SPLIT = 11       /* the split kernel applies the pre-map and stores 16-byte
                                         coefficients (default: it stores digits and the first
-                                        column pass pre-maps, where a compiled shape allows) */
+                                        column pass pre-maps, where a compiled shape allows) */,
+  TMG_OPT_CARRY_KERNELS = 12         /* 1: single-pass look-back carry (k_carry_lb); 2: carry-ins by
+                                        a second kernel (k_carry_lanes + k_carry_patch); 0 (default):
+                                        one kernel while the carry blocks fit one wave, else two */
 };
 int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value);
 

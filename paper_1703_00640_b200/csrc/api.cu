@@ -83,6 +83,7 @@ struct Profiler {
 // to kMaxBatchStreams workspaces, each on its own stream.
 struct Workspace {
   DevBuf work_t, work_c, work_z, cbu, cbv, aux, tbuf, aggs, zaggs, ticket, hticket, status;
+  DevBuf gen;  // look-back generation of k_carry_lb, advanced by k_zstat (zero-initialised)
   ScanSlot scan_c;  // look-back state of the single-pass carry (k_carry)
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
@@ -103,6 +104,7 @@ struct Options {
   PlanOptions plan;             // TMG_OPT_GENERIC_COLUMN_PASSES, TMG_OPT_FORCE_THREE_PASS
   bool generic_row = false;     // TMG_OPT_GENERIC_ROW_PASS
   bool lookback_carry = false;  // TMG_OPT_LOOKBACK_CARRY
+  int carry_kernels = 0;        // TMG_OPT_CARRY_KERNELS (0 by size)
   long patch_scan_max = long(kPatchScanMaxBlocks);  // TMG_OPT_PATCH_SCAN_MAX
   bool no_pdl = false;          // TMG_OPT_NO_PDL
   bool debug_sync = false;      // TMG_OPT_DEBUG_SYNC
@@ -348,6 +350,11 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       w.zaggs.ensure(size_t(blocks) * 4 + 16);
       a.aggs = w.zaggs.as<uint32_t>();
       a.early = cx.zstat_early ? 1 : 0;
+      if (!w.gen.p) {
+        w.gen.ensure(64);
+        TMG_CUDA(cudaMemsetAsync(w.gen.p, 0, 64, st));
+      }
+      a.gen = w.gen.as<uint32_t>();
       {
         KTimer kt(cx, "k_zstat", double(2 * pl.nlimbs) * 8.0, int(p.mode), st);
         launch(cx, k_zstat, dim3((blocks + 255) / 256), dim3(256), 0, st, a, "zstat");
@@ -556,6 +563,26 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         // last lanes block scans them into cins
         // (TMG_OPT_PATCH_SCAN_MAX lowers the limit for testing)
         a.lanes_cins = long(blocks2) > cx.opt.patch_scan_max ? 1 : 0;
+        // one kernel while the blocks fit one wave (4 per SM): their look-back
+        // waits stay short, and a launch is saved (2^20 low 57.9 -> 55.3 us);
+        // beyond, blocks that wait for a predecessor hold their slots, and the
+        // second kernel costs less (2^26 low 271.6 against 278.0 us)
+        const bool one = cx.opt.carry_kernels == 1 ||
+                         (cx.opt.carry_kernels == 0 && blocks2 <= unsigned(4 * cx.num_sms));
+        CarryLanesFn lbk = one ? carry_lb_kernel(lam, pt) : nullptr;
+        if (lbk) {
+          // one kernel: the carry-in by decoupled look-back, every limb written once
+          a.scan = w.scan_c.next(blocks2);
+          a.gen = w.gen.as<uint32_t>();
+          set_smem(lbk, smem2);
+          {
+            KTimer kt(cx, "k_carry_lb", double(pl.K) * 8.0 + double(hb ? pl.ML : pl.out_limbs) * 8.0, int(p.mode),
+                      st);
+            launch(cx, lbk, dim3(blocks2), dim3(kC2Threads), smem2, st, a, "carry_lb");
+          }
+          check_launch(cx, "k_carry_lb");
+          kernels += 1;
+        } else {
         CarryLanesFn lanes = carry_lanes_kernel(lam, pt);
         set_smem(lanes, smem2);
         {
@@ -572,6 +599,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
           check_launch(cx, "k_carry_patch");
         }
         kernels += 2;
+        }
       } else {
         set_smem(k_carry, pl.smem_carry);
         {
@@ -1205,6 +1233,10 @@ int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value) {
       case TMG_OPT_Z_NATURAL: o.z_natural = o.plan.z_natural = on; break;
       case TMG_OPT_GENERIC_SMALL: o.generic_small = on; break;
       case TMG_OPT_PREMAP_IN_SPLIT: o.plan.premap_in_zgen = on; break;
+      case TMG_OPT_CARRY_KERNELS:
+        if (value < 0 || value > 2) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "carry kernels: 0, 1 or 2");
+        o.carry_kernels = int(value);
+        break;
       default: throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "unknown context option");
     }
     // plans and captured batch graphs were built under the old options

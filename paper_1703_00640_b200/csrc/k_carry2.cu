@@ -453,6 +453,199 @@ __global__ void __launch_bounds__(kT, 4) k_carry_lanes(CarryArgs a) {
   }
 }
 
+// Single pass: k_carry_lanes with the block's carry-in taken by a
+// warp-parallel decoupled look-back (lookback_warp) between its block scan
+// and its stores, so every limb is written once with its final value and no
+// second kernel patches carry-ins.  A block's aggregate is published right
+// after its scan and is almost always a constant function (a carry-in
+// changes a block's carry-out only if all its limb sums sit at a wrap
+// boundary), so the look-back usually reads one predecessor's aggregate.
+// Blocks are dispatched in index order (predecessors are resident or done);
+// the look-back words carry a generation that the product's k_zstat
+// advances in device memory, so no state is reset between launches and
+// replayed CUDA graphs stay valid.  The checks that need final limbs
+// (the full product's range, the high product's nominations, sticky bit
+// and sign) run here on the block's own limbs.
+template <int LAM, int kPT>
+__global__ void __launch_bounds__(kT, 4) k_carry_lb(CarryArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int64_t kLimbs = int64_t(kT) * kPT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t sw[32];
+  __shared__ long long s_hi[kT];
+  __shared__ double s_psi;
+  __shared__ uint32_t s_flags, s_gen, s_hmin, s_sticky;
+  __shared__ int s_cin;
+  __shared__ double2 s_red[kT / 32];
+  __shared__ __align__(8) uint64_t s_mbar;
+  const int tid = threadIdx.x;
+  const MapConsts& mc = a.mc;
+  const int b = mc.b;
+  const int64_t K = a.K;
+  if (tid == 0) s_gen = *a.gen;
+  const uint32_t vblk = blockIdx.x;
+  const int64_t blk = vblk;
+  const int64_t ms = blk * kLimbs;
+  const int64_t me = min(a.ML, ms + kLimbs);
+  const int64_t kbase = kfirst(ms > 0 ? ms - 1 : 0, a.fb, K);
+  const int64_t kend = kfirst(me, a.fb, K);
+  const int64_t nwt = (mc.mode == kModeFull) ? K : mc.N;
+  const int64_t wlo = max(int64_t(0), kbase - LAM - 1) & ~int64_t(1);
+  const int64_t whi = (min(nwt, kend + 2) + 1) & ~int64_t(1);
+  const int64_t nw = (LAM > 0 && whi > wlo) ? whi - wlo : 0;
+  double* sww = reinterpret_cast<double*>(smem_raw);
+  const bool hmode = mc.mode == kModeHigh;
+  long long* se = hmode ? reinterpret_cast<long long*>(sww)
+                        : reinterpret_cast<long long*>(sww + (nw + 1));
+  if (tid == 0 && nw > 0) {
+    mbar_init(&s_mbar, 1);
+    mbar_expect_tx(&s_mbar, uint32_t(nw * 8));
+    bulk_g2s(sww, a.w + wlo, uint32_t(nw * 8), &s_mbar);
+  }
+  if (tid == 0) {
+    s_flags = 0;
+    s_hmin = 0xffffffffu;
+    s_sticky = 0;
+    const bool need_psi = mc.mode == kModeHigh && (kbase < mc.nfold || kend > mc.N);
+    s_psi = need_psi ? high_psi(mc, [&](int64_t j) { return __ldg(a.w + j); }, a.aux[0]) : 0.0;
+  }
+  __syncthreads();
+  if (nw > 0) mbar_wait(&s_mbar, 0);
+  RoundAcc ra;
+  uint32_t flags = 0;
+  const int64_t m0 = ms + int64_t(tid) * kPT;
+  double* shb = sww + (nw + 1);
+  coeffs_block<LAM>(a, sww, wlo, nw, kbase, kend, se, shb, ra, s_psi, flags, tid);
+  __syncthreads();
+  unsigned long long lo[kPT];
+  long long hi[kPT];
+  {
+    int64_t ka = kfirst(m0, a.fb, K);
+#pragma unroll
+    for (int q = 0; q < kPT; ++q) {
+      const int64_t m = m0 + q;
+      lo[q] = 0;
+      hi[q] = 0;
+      if (m < me) {
+        const int64_t kb = kfirst(m + 1, a.fb, K);
+        lane_of(se, kbase, m, ka, kb, b, lo[q], hi[q]);
+        ka = kb;
+      }
+    }
+  }
+  long long hin = 0;  // hi(lane_{m0 - 1})
+  if (tid == 0 && ms > 0) {
+    unsigned long long l0;
+    lane_of(se, kbase, ms - 1, kbase, kfirst(ms, a.fb, K), b, l0, hin);
+  }
+  s_hi[tid] = hi[kPT - 1];
+  __syncthreads();
+  if (tid > 0) hin = s_hi[tid - 1];
+  uint32_t f = kTfIdentity;
+  uint32_t tfq[kPT];
+#pragma unroll
+  for (int q = 0; q < kPT; ++q) {
+    const int64_t m = m0 + q;
+    tfq[q] = kTfIdentity;
+    if (m < me) {
+      const __int128 sm = (__int128)lo[q] + (__int128)(q == 0 ? hin : hi[q - 1]);
+      tfq[q] = limb_tf(sm, flags);
+      f = tf_compose(f, tfq[q]);
+      lo[q] = (unsigned long long)sm;
+    }
+  }
+  uint32_t agg;
+  const uint32_t ex = block_scan_tf(f, sw, &agg);
+  // publish the aggregate first, so that successors' look-backs can start
+  if (tid == 0 && vblk != 0)
+    *(volatile unsigned long long*)(a.scan.state + vblk) =
+        (static_cast<unsigned long long>(s_gen) << 32) | (1ull << 30) | agg;
+  const int64_t OL = a.out_limbs;
+  const bool full = mc.mode == kModeFull, low = mc.mode == kModeLow;
+  const int hb = int((2 * a.n) & 63);
+  auto store = [&](int64_t m, uint64_t x) {
+    if (hmode) {
+      a.tbuf[m] = x;
+    } else if (m < OL) {
+      a.out[m] = (low && m == OL - 1 && (a.n & 63)) ? (x & ((1ull << (a.n & 63)) - 1)) : x;
+    }
+  };
+  // the limbs for a zero carry into the block go out before the look-back
+  // (whose wait then overlaps their drain); the threads whose carry-in
+  // differs once the block's carry-in is known store again (with a nonzero
+  // carry-in: the first thread, and the few behind a run of wrapping limbs)
+  const int c0 = tf_apply(ex, 0);
+  {
+    int c = c0;
+#pragma unroll
+    for (int q = 0; q < kPT; ++q) {
+      const int64_t m = m0 + q;
+      if (m < me) {
+        store(m, lo[q] + uint64_t(int64_t(c)));
+        c = tf_apply(tfq[q], c);
+      }
+    }
+  }
+  if (tid < 32) {
+    const int cin = lookback_warp(a.scan.state, vblk, agg, s_gen, 0, true);
+    if (tid == 0) s_cin = cin;
+  }
+  __syncthreads();
+  int c = tf_apply(ex, s_cin);
+  const bool restore = c != c0;
+#pragma unroll
+  for (int q = 0; q < kPT; ++q) {
+    const int64_t m = m0 + q;
+    if (m < me) {
+      const uint64_t x = lo[q] + uint64_t(int64_t(c));
+      c = tf_apply(tfq[q], c);
+      lo[q] = x;
+      if (restore) store(m, x);
+      if (full && m >= OL - 1 && (m == OL - 1 ? (hb && (x >> hb)) : x != 0)) flags |= kFlagFullOverflow;
+      // sign of the recombined value: the carry out of the top limb
+      if (m == a.ML - 1 && c < 0) flags |= full ? uint32_t(kFlagNegative) : hmode ? uint32_t(kFlagHighRange) : 0u;
+    }
+  }
+  flags |= ra.all_flags();
+  {
+    const double e = warp_max_nonneg(ra.max_err), mx = warp_max_nonneg(ra.max_abs);
+    if ((tid & 31) == 0) s_red[tid >> 5] = make_double2(e, mx);
+  }
+  if (hmode) {
+    const HighLimbs hl(a);
+    uint32_t hmin = 0xffffffffu, sticky = 0;
+#pragma unroll
+    for (int q = 0; q < kPT; ++q) {
+      const int64_t m = m0 + q;
+      if (m < me) hl.see(m, lo[q], hmin, sticky);
+    }
+    // w0's top limb has zero fill above bit 64 - r: never all ones
+    if (hl.hr != 0 && blk == 0 && tid == 0 && hl.WL > 0) hmin = min(hmin, uint32_t(hl.WL - 1));
+    hmin = __reduce_min_sync(0xffffffffu, hmin);
+    sticky = __reduce_or_sync(0xffffffffu, sticky);
+    if ((tid & 31) == 0) {
+      if (hmin != 0xffffffffu) atomicMin(&s_hmin, hmin);
+      if (sticky) s_sticky = 1;
+    }
+  }
+  if (flags) atomicOr(&s_flags, flags);
+  __syncthreads();
+  if (tid == 0) {
+    if (hmode) {
+      if (s_hmin != 0xffffffffu) atomicMin(a.hstop, s_hmin);
+      if (s_sticky) atomicOr(&a.status->high_sticky, 1u);
+    }
+    double e = 0.0, mx = 0.0;
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) {
+      e = fmax(e, s_red[w].x);
+      mx = fmax(mx, s_red[w].y);
+    }
+    status_merge(a.status, e, mx, s_flags);
+  }
+}
+
 }  // namespace
 
 // k_carry_lanes wrote every limb for a zero carry into its block.  A
@@ -612,6 +805,17 @@ CarryLanesFn lanes_pt(int lam) {
 }
 
 CarryLanesFn carry_lanes_kernel(int lam, int pt) { return pt == 4 ? lanes_pt<4>(lam) : lanes_pt<2>(lam); }
+
+template <int PT>
+CarryLanesFn lb_pt(int lam) {
+  switch (lam) {
+    case 0: return k_carry_lb<0, PT>;
+    case 4: return k_carry_lb<4, PT>;
+    case 5: return k_carry_lb<5, PT>;
+    default: return nullptr;
+  }
+}
+CarryLanesFn carry_lb_kernel(int lam, int pt) { return pt == 4 ? lb_pt<4>(lam) : lb_pt<2>(lam); }
 CarryLanesFn carry_patch_kernel(int pt) { return pt == 4 ? k_carry_patch<4> : k_carry_patch<2>; }
 
 }  // namespace tmg

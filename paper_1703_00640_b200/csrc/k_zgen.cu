@@ -137,6 +137,9 @@ k_zstat(ZgenArgs a) {
   }
   a.aggs[blk] = fu | (fv << 2);
   pdl_wait();
+  // a new look-back generation for this product's k_carry_lb (after the
+  // wait: the previous product's carry kernel has completed)
+  if (blk == 0) *a.gen += 1u;
 }
 
 // LAM: the series length lambda (rows of the pre-map), 0 for the full

@@ -106,6 +106,7 @@ struct ZgenArgs {
   uint32_t* aggs;  // per-block carry transfer functions (k_zstat)
   ZTile zt;        // layout of z as k_f1 reads it
   int32_t early;   // k_zstat: operands not written by in-flight kernels (read before pdl_wait)
+  uint32_t* gen;   // k_zstat advances the look-back generation of k_carry_lb
 };
 constexpr int kZgenThreads = 256;
 constexpr int kZgenPer = 16;
@@ -248,6 +249,7 @@ struct CarryArgs {
   FastDiv fb;       // division by b
   uint32_t* hstop;  // high: first limb of t >> s that is not all ones (atomicMin; ~0 before)
   int32_t lanes_cins; // 1: the last k_carry_lanes block writes cins; 0: k_carry_patch scans aggs
+  const uint32_t* gen;  // k_carry_lb: look-back generation (advanced by this product's k_zstat)
 };
 constexpr int kCarryThreads = 256;
 constexpr int kCarryPerThread = 2;
@@ -257,6 +259,10 @@ constexpr int kC2Threads = 256;
 typedef void (*CarryLanesFn)(CarryArgs);
 CarryLanesFn carry_lanes_kernel(int lam, int pt);
 CarryLanesFn carry_patch_kernel(int pt);
+// single-pass lanes kernel with a decoupled look-back carry-in (k_carry_lb;
+// nullptr for lambda outside {0, 4, 5}); a.scan: look-back words, ctr
+// [0] ticket, [1] done, [2] generation
+CarryLanesFn carry_lb_kernel(int lam, int pt);
 size_t carry2_smem(int b, int lam, int pt, bool hbuf);
 
 struct HighRoundArgs {

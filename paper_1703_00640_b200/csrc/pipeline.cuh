@@ -378,17 +378,18 @@ __device__ __forceinline__ uint32_t block_scan_kgp(uint32_t f, uint32_t* sw, uin
 // Warp-parallel decoupled look-back (called by all 32 lanes of one warp):
 // each round reads the state words of the 32 nearest unresolved
 // predecessors at once, composes their aggregates with a warp reduction and
-// stops at the nearest inclusive prefix.  carry0 is the carry into block 0.
+// stops at the nearest inclusive prefix or constant aggregate.  carry0 is the carry into block 0.
 // Returns the carry into block blk (same value in every lane) and publishes
 // this block's inclusive carry.
 __device__ __forceinline__ int lookback_warp(unsigned long long* state,
                                              uint32_t blk, uint32_t agg,
-                                             uint32_t epoch, int carry0) {
+                                             uint32_t epoch, int carry0,
+                                             bool published = false) {
   const int lane = threadIdx.x & 31;
   const unsigned long long ep = (unsigned long long)epoch << 32;
   int carry_in = carry0;
   if (blk != 0) {
-    if (lane == 0)
+    if (lane == 0 && !published)
       *(volatile unsigned long long*)(state + blk) = ep | (1ull << 30) | agg;
     uint32_t E = kTfIdentity;
     int64_t base = int64_t(blk) - 1;
@@ -397,7 +398,14 @@ __device__ __forceinline__ int lookback_warp(unsigned long long* state,
       unsigned long long w = 0;
       if (j >= 0) w = *(volatile unsigned long long*)(state + j);
       const bool valid = (j >= 0) && ((w >> 32) == epoch) && (((w >> 30) & 3u) != 0);
-      const bool incl = valid && (((w >> 30) & 3u) == 2);
+      // the walk stops at an inclusive prefix or at an aggregate that is a
+      // constant function (its carry-out does not depend on its carry-in --
+      // almost every block's), so it rarely goes past the nearest predecessor
+      const uint32_t wf = uint32_t(w & 0xFFFFFFu);
+      const bool cst = valid && (((w >> 30) & 3u) == 1) && ((wf & 0xFFu) == ((wf >> 8) & 0xFFu)) &&
+                       ((wf & 0xFFu) == (wf >> 16));
+      const bool incl = valid && ((((w >> 30) & 3u) == 2) || cst);
+      if (cst) w = (w & ~0xFFFFFFull) | (wf & 0xFFu);  // its carry-out + 1, like an inclusive word
       const uint32_t bi = __ballot_sync(0xffffffffu, incl);
       const uint32_t bv = __ballot_sync(0xffffffffu, valid);
       const int first = bi ? (__ffs(bi) - 1) : 32;

@@ -893,3 +893,24 @@ def test_first_pass_premap_matches_split_premap(ctx, n):
             assert ea == old.last_stats.max_round_err, mode
             _check(mode, u, v, n, tm.from_limbs(a))
     old.close()
+
+
+@pytest.mark.parametrize("kernels", [1, 2])
+@pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 448, 1 << 24])
+def test_carry_kernel_paths(n, kernels):
+    """TMG_OPT_CARRY_KERNELS: the single-pass look-back k_carry_lb (1) and
+    k_carry_lanes + k_carry_patch (2) at sizes where the default takes the
+    other; random and structured (long carry chains) operands, both paths
+    identical to the default and exact."""
+    c = _opt_ctx((tm._native.TMG_OPT_CARRY_KERNELS, kernels))
+    _config3_all_modes(c, n)
+    nl = (n + 63) // 64
+    M = (1 << n) - 1
+    for a, b_ in ((M, M), (M, 1 << (n - 1)), ((1 << n) - (1 << 1000), M - 5)):
+        u, v = port.int_to_limbs(a, nl), port.int_to_limbs(b_, nl)
+        for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+            r1 = c.product_limbs(mode, u, v, sp(n, mode))
+            r0 = tm.default_context(0).product_limbs(mode, u, v, sp(n, mode))
+            assert np.array_equal(r0, r1)
+            _check(mode, u, v, n, tm.from_limbs(r0))
+    c.close()
