@@ -200,7 +200,8 @@ enum {
                                         column pass pre-maps, where a compiled shape allows) */,
   TMG_OPT_CARRY_KERNELS = 12         /* 1: single-pass look-back carry (k_carry_lb); 2: carry-ins by
                                         a second kernel (k_carry_lanes + k_carry_patch); 0 (default):
-                                        one kernel while the carry blocks fit one wave, else two */
+                                        one kernel while the carry blocks fit one wave, else two */,
+  TMG_OPT_MAX_ROW = 13               /* longest row length C of multi-pass plans (0: 4096) */
 };
 int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value);
 

@@ -68,7 +68,9 @@ struct SinkPrep {
   static constexpr bool value = false;
 };
 
-template <int RAD, bool INV, uint32_t R, uint32_t NS, int NTHR, class Sink>
+// TMUL: stage-table index stride (2: a length-R/2 inverse reading the
+// forward stage table of length R at every second entry).
+template <int RAD, bool INV, uint32_t R, uint32_t NS, int NTHR, class Sink, uint32_t TMUL = 1>
 __device__ __forceinline__ void ct_store(double2 (&x)[16], const RowPair& lay,
                                          const double2* __restrict__ stab, uint32_t qmul,
                                          const Sink& sink, int tid) {
@@ -86,7 +88,7 @@ __device__ __forceinline__ void ct_store(double2 (&x)[16], const RowPair& lay,
         if (NS > 1 && j != 0) {
 #pragma unroll
           for (int q = 1; q < RAD; ++q) {
-            const double2 w = stab[(uint32_t(q) * qmul - 1) * NS + j];
+            const double2 w = stab[TMUL * ((uint32_t(q) * qmul - 1) * NS + j)];
             xv[q] = INV ? cmulc(xv[q], w) : cmul(xv[q], w);
           }
         }
@@ -97,7 +99,7 @@ __device__ __forceinline__ void ct_store(double2 (&x)[16], const RowPair& lay,
         if (NS > 1 && j != 0) {
 #pragma unroll
           for (int q = 1; q < RAD; ++q) {
-            const double2 w = stab[(uint32_t(q) * qmul - 1) * NS + j];
+            const double2 w = stab[TMUL * ((uint32_t(q) * qmul - 1) * NS + j)];
             xv[q] = INV ? cmulc(xv[q], w) : cmul(xv[q], w);
           }
         }
@@ -115,7 +117,7 @@ __device__ __forceinline__ void ct_store(double2 (&x)[16], const RowPair& lay,
 // writes sink, the others exchange through buf (RowPair layout).  toff and
 // qmul of each stage come from the plan (the inverse of a row pass reads the
 // forward table through the qmul mapping, plan.cu map_stages).
-template <bool INV, class SC, int S, int NTHR, class Src, class Sink>
+template <bool INV, class SC, int S, int NTHR, class Src, class Sink, uint32_t TMUL = 1>
 __device__ __forceinline__ void ct_stages(double2 (&x)[16], double2* __restrict__ buf,
                                           const RowPair& lay, const double2* __restrict__ stab,
                                           const SubFft& p, const Src& src, const Sink& sink,
@@ -132,11 +134,12 @@ __device__ __forceinline__ void ct_stages(double2 (&x)[16], double2* __restrict_
   ct_sync<NTHR>(tid);
   const double2* st = stab + p.toff[S];
   if constexpr (last) {
-    ct_store<RAD, INV, R, NS, NTHR>(x, lay, st, p.qmul[S], sink, tid);
+    ct_store<RAD, INV, R, NS, NTHR, Sink, TMUL>(x, lay, st, p.qmul[S], sink, tid);
   } else {
-    ct_store<RAD, INV, R, NS, NTHR>(x, lay, st, p.qmul[S], SmemSink<RowPair>{buf, lay}, tid);
+    ct_store<RAD, INV, R, NS, NTHR, SmemSink<RowPair>, TMUL>(x, lay, st, p.qmul[S], SmemSink<RowPair>{buf, lay},
+                                                             tid);
     ct_sync<NTHR>(tid);
-    ct_stages<INV, SC, S + 1, NTHR>(x, buf, lay, stab, p, src, sink, tid);
+    ct_stages<INV, SC, S + 1, NTHR, Src, Sink, TMUL>(x, buf, lay, stab, p, src, sink, tid);
   }
 }
 

@@ -1,19 +1,24 @@
 // Multi-pass product pipeline for transform lengths beyond one CTA.
 //
-//   k_zstat/k_zgen (k_zgen.cu) balanced split + pre-map; carries composed
-//                 from per-block aggregates
-//   k_f1_ct       first column pass (DFTs over A of the pre-mapped
-//                 coefficients, output twiddle) with a compile-time schedule
-//                 for the hot column lengths; k_f1 / k_f1_pp otherwise
+//   k_zstat/k_zgen (k_zgen.cu) balanced split (+ pre-map where k_f1d_ct
+//                 does not apply it); carries composed from per-block
+//                 aggregates
+//   k_f1d_ct      (k_f1d.cu) first column pass on the split's stored digits,
+//                 pre-map in its first stage; k_f1_ct reads pre-mapped
+//                 coefficients, with a compile-time schedule for the hot
+//                 column lengths; k_f1 / k_f1_pp otherwise
 //   k_col_ct      middle column passes of three-pass plans (over B, in
 //                 place); k_col / the ping-pong variants otherwise
 //   k_mid_4096    row DFTs over C = 4096 for a conjugate row pair, spectral
-//                 product and repack, half-length inverse, output twiddle
-//                 (persistent); k_mid for other row lengths
+//                 product and repack in registers (shuffles between the
+//                 pair's lanes), half-length inverse, output twiddle
+//                 (persistent, next pair's row 0 staged by TMA); k_mid for
+//                 other row lengths
 //   k_ilast_ct    inverse column DFTs over A -> convolution coefficients;
 //                 k_ilast / k_ilast_pp otherwise
-//   k_carry       single-pass look-back carry (fallback; the default is
-//                 k_carry_lanes + k_carry_patch in k_carry2.cu)
+//   k_carry       single-pass look-back carry beyond 2^32 carry bits (the
+//                 default is k_carry_lb, or k_carry_lanes + k_carry_patch,
+//                 in k_carry2.cu)
 //   k_high_agg / k_high_round  round(t / 2^s) of the high product
 //
 // Reference path: products_f64.cpp:106-171 with the FFTW convolution of
@@ -519,25 +524,54 @@ k_mid(MidArgs a) {
 
 // ---------------------------------------------------------------------------
 // Row pass specialised for C = 4096 (forward 16 x 16 x 16, inverse
-// 2048 = 16 x 16 x 8 reading the forward stage table): persistent CTAs (one
+// 2048 = 8 x 16 x 16 reading the forward stage table): persistent CTAs (one
 // per SM, the row pair fills shared memory), the stage table staged once per
-// CTA, and the next pair's two rows prefetched into L2 while the current
-// pair computes, so the first stage's loads do not wait on HBM.
-template <int NTHR, class Fwd, class Inv>
-__device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restrict__ sbuf,
-                                              const double2* __restrict__ stab,
-                                              double2* __restrict__ qt, uint32_t r0, int tid,
-                                              double2 wc0, double2 wc1) {
-  constexpr uint32_t C = 4096, H = 2048;
+// CTA, the next pair's row 1 prefetched into L2 while the current pair
+// computes.  Row 0 of the next pair is copied (cp.async.bulk, two 32 KB halves) into
+// the upper halves of the two row buffers, which nothing reads after the
+// last forward stage, while the current pair's inverse runs in the lower
+// halves; the next pair's first stage reads row 0 from there.
+constexpr uint32_t kMidStage = 2176;  // padidx(2048): first slot of a row's upper half
+struct RowSrcStaged {
+  const double2* data;
+  const double2* stg;  // staged row 0: e < 2048 at stg[e], else stg[rowstride + e - 2048]
+  int64_t base0, base1;
+  uint32_t rowstride;
+  bool staged;
+  __device__ __forceinline__ double2 operator()(uint32_t item, uint32_t e) const {
+    if (item == 0 && staged) return stg[e < 2048u ? e : rowstride + e - 2048u];
+    return data[(item ? base1 : base0) + e];
+  }
+};
+
+template <int NTHR>
+__device__ __forceinline__ void mid_pair_4096_reg(const MidArgs& a, double2* __restrict__ sbuf,
+                                                  const double2* __restrict__ stab,
+                                                  double2* __restrict__ qt, uint32_t r0, int tid,
+                                                  double2 wct, bool staged, uint32_t phase,
+                                                  const double2* next_row0, uint64_t* bar) {
+  using Fwd = Sched<16, 16, 16>;
+  using Inv = Sched<8, 16, 16>;
+  constexpr uint32_t C = 4096;
   const uint32_t AB = a.A * a.B;
   const uint32_t r1 = (AB - r0) % AB;
-  const uint32_t nrows = (r1 == r0) ? 1 : 2;
+  // self-paired rows (0 and AB/2): one row, both lane halves on it
+  const uint32_t nrows = (r1 == r0) ? 1u : 2u;
   const RowPair lay{padded_len(C) + 4, nrows};
   const int64_t base0 = (int64_t(r0 % a.A) * a.B + (r0 / a.A)) * int64_t(C);
   const int64_t base1 = (int64_t(r1 % a.A) * a.B + (r1 / a.A)) * int64_t(C);
   double2 x[16];
-  ct_stages<false, Fwd, 0, NTHR>(x, sbuf, lay, stab, a.fwd, RowSrc{a.data, base0, base1},
-                                 SmemSink<RowPair>{sbuf, lay}, tid);
+  // forward stages 0 and 1 (half of the CTA per row)
+  if (staged && tid < NTHR / 2) mbar_wait(bar, phase);
+  ct_load<16, C, NTHR>(x, lay,
+                       RowSrcStaged{a.data, sbuf + kMidStage, base0, base1, lay.rowstride, staged}, tid);
+  __syncthreads();  // row 1's stores overwrite the staged row's second half
+  ct_store<16, false, C, 1, NTHR>(x, lay, stab + a.fwd.toff[0], a.fwd.qmul[0], SmemSink<RowPair>{sbuf, lay}, tid);
+  ct_sync<NTHR>(tid);
+  ct_load<16, C, NTHR>(x, lay, SmemSrc<RowPair>{sbuf, lay}, tid);
+  ct_sync<NTHR>(tid);
+  ct_store<16, false, C, 16, NTHR>(x, lay, stab + a.fwd.toff[1], a.fwd.qmul[1], SmemSink<RowPair>{sbuf, lay},
+                                   tid);
   __syncthreads();
   // per-pair table of the output twiddles' second factor (RowSinkQ)
   constexpr uint32_t RL = uint32_t(Inv::rad(Inv::nst - 1));
@@ -548,67 +582,80 @@ __device__ __forceinline__ void mid_pair_4096(const MidArgs& a, double2* __restr
     const uint32_t xq = 2u * (it ? r1 : r0) * NSL * q;
     qt[tid] = xq ? a.tw.get(xq) : make_double2(1.0, 0.0);
   }
-  // spectral product over the pair (see k_mid) fused with the half-length
-  // repack.  For a pair of distinct rows the partner of row 0's index k is
-  // row 1's C-1-k, so one thread reads Z0_k, Z0_{k+H}, Z1_{C-1-k}, Z1_{H-1-k},
-  // forms W0_k, W0_{k+H} (and W1 = conj W0 at the partner indices) and
-  // writes Y0_k and Y1_{H-1-k}: the four slots it reads are read by no other
-  // thread, so the step is in place with one barrier (same arithmetic as the
-  // two-pass form).  The self-paired rows 0 and AB/2 take the two passes.
-  auto spec = [&](double2 z1, double2 z2) {
+  // forward stage 2 on the lane assignment above
+  const int lane = tid & 31, w = tid >> 5;
+  const uint32_t row = lane >> 4;
+  const uint32_t phys = nrows == 2 ? row : 0u;
+  const uint32_t t = row ? 255u - uint32_t(16 * w + (lane & 15)) : uint32_t(16 * w + lane);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) x[q] = sbuf[lay.idx(phys, t + 256u * uint32_t(q))];
+  if (t != 0) {
+    const double2* st2 = stab + a.fwd.toff[2];
+#pragma unroll
+    for (int q = 1; q < 16; ++q) x[q] = cmul(x[q], st2[(uint32_t(q) * a.fwd.qmul[2] - 1) * 256u + t]);
+  }
+  dft<16, false>(x);
+  // spectral product and repack: Y_r[k] for k = t + 256 q, q < 8, into x[q]
+  auto spec = [](double2 z1, double2 z2) {
     const double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
     const double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
     const double2 pq = cmul(p, q);
     return make_double2(pq.y, -pq.x);  // -i pq, unscaled (see CoefSink)
   };
-  auto repack_w = [&](double2 w1, double2 w2, double2 t) {
+  auto repack_w = [](double2 w1, double2 w2, double2 tk) {
     const double2 ev = cadd(w1, w2);
-    const double2 o = cmulc(csub(w1, w2), t);
+    const double2 o = cmulc(csub(w1, w2), tk);
     return make_double2(ev.x - o.y, ev.y + o.x);
   };
-  auto repack = [&](double2 w1, double2 w2, uint32_t r, uint32_t k) {
-    return repack_w(w1, w2, a.tw.get(r + AB * k));
+  auto shfl2 = [](double2 v) {
+    return make_double2(__shfl_xor_sync(0xffffffffu, v.x, 16), __shfl_xor_sync(0xffffffffu, v.y, 16));
   };
-  if (nrows == 2) {
-    // repack twiddles omega_L^{r + AB k} = omega_L^r omega_C^k: with k = tid +
-    // NTHR s and NTHR = C / 8, omega_C^k = omega_C^tid omega_8^s (row 0), and
-    // row 1's k = H-1-tid-NTHR s gives omega_C^{H-1-tid} omega_8^-s; the
-    // per-thread omega_C factors are fetched once per CTA (wc0, wc1)
-    static_assert(NTHR * 8 == C && H % NTHR == 0, "repack twiddle layout");
-    const double2 t0 = cmul(a.tw.get(r0), wc0), t1 = cmul(a.tw.get(r1), wc1);
+  // repack twiddle omega_L^{r + AB k} = omega_L^r omega_C^t omega_16^q
+  const double2 tb = cmul(a.tw.get(row ? r1 : r0), wct);
+  if (r0 != 0) {
+    // partner (same row when self-paired, AB/2): Z_-k-1 = lane ^ 16
 #pragma unroll
-    for (int si = 0; si < int(H / NTHR); ++si) {
-      const uint32_t k = uint32_t(tid) + NTHR * uint32_t(si);
-      const uint32_t kq = H - 1 - k;
-      const double2 a0 = sbuf[lay.idx(0, k)], a1 = sbuf[lay.idx(0, k + H)];
-      const double2 b0 = sbuf[lay.idx(1, C - 1 - k)], b1 = sbuf[lay.idx(1, kq)];
-      const double2 wk = spec(a0, b0), wkh = spec(a1, b1);
-      const double2 tk = si == 0 ? t0 : si == 1 ? w8_1<false>(t0) : si == 2 ? mul_mi<false>(t0)
-                                                                            : w8_3<false>(t0);
-      const double2 tq = si == 0 ? t1 : si == 1 ? w8_1<true>(t1) : si == 2 ? mul_mi<true>(t1)
-                                                                           : w8_3<true>(t1);
-      sbuf[lay.idx(0, k)] = repack_w(wk, wkh, tk);
-      sbuf[lay.idx(1, kq)] = repack_w(cconj(wkh), cconj(wk), tq);
+    for (int q = 0; q < 4; ++q) {
+      const int qb = 7 - q;
+      // partner's Z at q' = 15 - q, 7 - q (for Y[q]) and 8 + q, q (for Y[7 - q])
+      const double2 p15 = shfl2(x[15 - q]), p7 = shfl2(x[7 - q]);
+      const double2 p8 = shfl2(x[8 + q]), p0 = shfl2(x[q]);
+      const double2 ya = repack_w(spec(x[q], p15), spec(x[q + 8], p7), w16<false>(tb, q));
+      const double2 yb = repack_w(spec(x[qb], p8), spec(x[qb + 8], p0), w16<false>(tb, qb));
+      x[q] = ya;
+      x[qb] = yb;
     }
   } else {
-    const uint32_t brw = (r0 != 0) ? 1u : 0u;
-    for (uint32_t k = tid; k < C; k += NTHR) {
-      const uint32_t kp = (C - k - brw) & (C - 1);
-      if (kp < k) continue;
-      const double2 w = spec(sbuf[lay.idx(0, k)], sbuf[lay.idx(0, kp)]);
-      sbuf[lay.idx(0, k)] = w;
-      if (kp != k) sbuf[lay.idx(0, kp)] = cconj(w);
-    }
+    // row 0 pairs index k with -k (no borrow): through shared memory
     __syncthreads();
-    for (uint32_t k = tid; k < H; k += NTHR)
-      sbuf[lay.idx(0, k)] = repack(sbuf[lay.idx(0, k)], sbuf[lay.idx(0, k + H)], r0, k);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) sbuf[lay.idx(0, t + 256u * uint32_t(q))] = x[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t k = t + 256u * uint32_t(q);
+      const double2 zm = sbuf[lay.idx(0, (C - k) & (C - 1))], zh = sbuf[lay.idx(0, C / 2 - k)];
+      x[q] = repack_w(spec(x[q], zm), spec(x[q + 8], zh), w16<false>(tb, q));
+    }
   }
+  // inverse stage 0 (radix 8, butterfly t, no twiddles): outputs 8 t + q
+  dft<8, true>(x);
+  __syncthreads();  // every thread has read its forward stage-2 inputs
+  if (tid == 0 && next_row0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar, 2048u * 16u * 2u);
+    bulk_g2s(sbuf + kMidStage, next_row0, 2048u * 16u, bar);
+    bulk_g2s(sbuf + lay.rowstride + kMidStage, next_row0 + 2048, 2048u * 16u, bar);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) sbuf[lay.idx(phys, 8u * t + uint32_t(q))] = x[q];
   __syncthreads();
-  ct_stages<true, Inv, 0, NTHR>(x, sbuf, lay, stab, a.inv, SmemSrc<RowPair>{sbuf, lay},
-                                RowSinkQ<RL>{a.data, base0, base1, r0, r1, a.tw, qt}, tid);
+  ct_stages<true, Inv, 1, NTHR, SmemSrc<RowPair>, RowSinkQ<RL>, 2>(
+      x, sbuf, lay, stab, a.fwd, SmemSrc<RowPair>{sbuf, lay},
+      RowSinkQ<RL>{a.data, base0, base1, r0, r1, a.tw, qt}, tid);
 }
 
-template <int NTHR, class Fwd, class Inv>
+template <int NTHR>
 __device__ __forceinline__ void mid_4096_body(const MidArgs& a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* sbuf = reinterpret_cast<double2*>(smem_raw);
@@ -623,27 +670,32 @@ __device__ __forceinline__ void mid_4096_body(const MidArgs& a) {
   auto row_base = [&](uint32_t r) {
     return a.data + (int64_t(r % a.A) * a.B + (r / a.A)) * int64_t(C);
   };
-  // this thread's omega_C^tid and omega_C^{H-1-tid} (repack twiddles)
-  const double2 wc0 = tid ? a.tw.get(AB * uint32_t(tid)) : make_double2(1.0, 0.0);
-  const double2 wc1 = a.tw.get(AB * (C / 2 - 1 - uint32_t(tid)));
-  if (tid == 0 && blockIdx.x < npairs) {
-    prefetch_l2(row_base(blockIdx.x), C * 16);
-    prefetch_l2(row_base((AB - blockIdx.x) % AB), C * 16);
+  // omega_C^t of this thread's last-forward-stage butterfly (repack twiddles)
+  const uint32_t lane = uint32_t(tid) & 31u, wp = uint32_t(tid) >> 5;
+  const uint32_t treg = (lane >> 4) ? 255u - (16u * wp + (lane & 15u)) : 16u * wp + lane;
+  const double2 wct = treg ? a.tw.get(AB * treg) : make_double2(1.0, 0.0);
+  __shared__ __align__(8) uint64_t s_bar;
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    if (blockIdx.x < npairs) {
+      prefetch_l2(row_base(blockIdx.x), C * 16);
+      prefetch_l2(row_base((AB - blockIdx.x) % AB), C * 16);
+    }
   }
   __syncthreads();
-  for (uint32_t r0 = blockIdx.x; r0 < npairs; r0 += gridDim.x) {
+  uint32_t it = 0;
+  for (uint32_t r0 = blockIdx.x; r0 < npairs; r0 += gridDim.x, ++it) {
     const uint32_t nx = r0 + gridDim.x;
-    if (tid == 0 && nx < npairs) {
-      prefetch_l2(row_base(nx), C * 16);
-      prefetch_l2(row_base((AB - nx) % AB), C * 16);
-    }
-    mid_pair_4096<NTHR, Fwd, Inv>(a, sbuf, stw, stw + C, r0, tid, wc0, wc1);
+    if (tid == 0 && nx < npairs) prefetch_l2(row_base((AB - nx) % AB), C * 16);
+    // row 0 of this pair was staged by the previous one (phase it - 1)
+    mid_pair_4096_reg<NTHR>(a, sbuf, stw, stw + C, r0, tid, wct, it > 0, (it - 1) & 1u,
+                            nx < npairs ? row_base(nx) : nullptr, &s_bar);
   }
 }
 
 __global__ void __launch_bounds__(kMidCtThreads)
 k_mid_4096(MidArgs a) {
-  mid_4096_body<kMidCtThreads, Sched<16, 16, 16>, Sched<16, 16, 8>>(a);
+  mid_4096_body<kMidCtThreads>(a);
 }
 
 // ---------------------------------------------------------------------------

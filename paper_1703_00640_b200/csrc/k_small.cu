@@ -88,26 +88,65 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a);
 // products of L <= 6144 (config 4's 2^16-bit batch) are latency-bound at one
 // 10-warp CTA per SM.
 __global__ void __launch_bounds__(512, 1)
-k_small_product(SmallArgs a) {
+k_small_product(const __grid_constant__ SmallArgs a) {
   small_product_body<512, 1>(a);
 }
 __global__ void __launch_bounds__(384, 2)
-k_small_product_2(SmallArgs a) {
+k_small_product_2(const __grid_constant__ SmallArgs a) {
   small_product_body<384, 2>(a);
 }
 // The full product of BASELINE config 4's size (2^16 bits, L = 6144 =
 // 8 x 8 x 8 x 12, inverse 3072 = 8 x 8 x 4 x 12) with compile-time
 // schedules at one 768-thread CTA per SM (4096 products: 1.45 -> 1.07 ms).
 __global__ void __launch_bounds__(768, 1)
-k_small_6144(SmallArgs a) {
+k_small_6144(const __grid_constant__ SmallArgs a) {
   small_product_body<768, 1, Sched<8, 8, 8, 12>, Sched<8, 8, 4, 12>>(a);
 }
 
 // Batches of products just above the single-product cutoff (L <= 12288, the
 // 2^17-bit range): one CTA per product at up to 768 threads.
 __global__ void __launch_bounds__(kSmallBatchMaxThreads, 1)
-k_small_product_big(SmallArgs a) {
+k_small_product_big(const __grid_constant__ SmallArgs a) {
   small_product_body<kSmallBatchMaxThreads, 1>(a);
+}
+
+// Convolution coefficient j from the inverse transform in shared memory:
+// y_m = w_{2m} + i w_{2m+1}, times the convolution's 1 / (4 L).
+struct SmallW {
+  const double2* buf;
+  double scale, scale_lo;
+  __device__ __forceinline__ double operator()(int64_t j) const {
+    const double2 y = buf[padidx(uint32_t(j >> 1))];
+    return mul_hl((j & 1) ? y.y : y.x, scale, scale_lo);
+  }
+};
+
+// The post-map values next to the wraps of the cyclic maps (low: i below
+// lambda; high: the fold region) go through the generic helpers, out of
+// line: inlined into the unrolled per-thread loop they made the kernel
+// about 1 MB of code, and it stalled on instruction fetch.
+__device__ __noinline__ double small_postmap_low_slow(const MapConsts& mc, SmallW W, int64_t i) {
+  return postmap_low(mc, W, i);
+}
+__device__ __noinline__ double small_high_buf_slow(const MapConsts& mc, SmallW W, int64_t i) {
+  return high_buf(mc, W, i);
+}
+
+// post_flat(mc, W, i) for lambda - 1 <= i < N (no term leaves [0, N)): the
+// same operation order.
+__device__ __forceinline__ double small_post_flat_in(const MapConsts& mc, const SmallW& W, int64_t i) {
+  const double Nd = double(mc.N);
+  const int fam = (mc.mode == kModeLow) ? 1 : 3;
+  const int lam = mc.lambda;
+  const double jd = double(i);
+  double acc = 0.0;
+  RowLoopDown<kMaxLambda>::run([&](auto rc) {
+    constexpr int r = decltype(rc)::value;
+    if constexpr (r > 0) {
+      if (r < lam) acc += W(i - r) * coef_r<r>(fam, jd - double(r), Nd, mc.cpost[r]);
+    }
+  });
+  return acc + W(i);
 }
 
 template <int MAXT, int MINB, class SCF, class SCI>
@@ -251,10 +290,7 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
   // 7. post-map and rounding.
   // the convolution's 1/(4L) is applied to the inverse transform's outputs
   // (CoefSink, k_multipass.cu, says why)
-  auto W = [&](int64_t j) {
-    double2 y = buf[padidx(uint32_t(j >> 1))];
-    return mul_hl((j & 1) ? y.y : y.x, a.scale, a.scale_lo);
-  };
+  const SmallW W{buf, a.scale, a.scale_lo};
   const int64_t M = (mc.mode == kModeFull) ? L : (mc.mode == kModeLow ? N : N + 1);
   double psi = 0.0;
   if (mc.mode == kModeHigh) {
@@ -274,7 +310,7 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
   double hprev = 0.0;
   if (runs && int64_t(tid) * kMaxPer < M) {
     const int64_t i0 = int64_t(tid) * kMaxPer;
-    hprev = (i0 >= 1 && i0 - 1 < N) ? high_buf(mc, W, i0 - 1) : 0.0;
+    hprev = (i0 >= 1 && i0 - 1 < N) ? small_high_buf_slow(mc, W, i0 - 1) : 0.0;
   }
 #pragma unroll
   for (int k = 0; k < kMaxPer; ++k) {
@@ -284,10 +320,14 @@ __device__ __forceinline__ void small_product_body(const SmallArgs& a) {
       if (mc.mode == kModeFull) {
         x = W(i);
       } else if (mc.mode == kModeLow) {
-        x = postmap_low(mc, W, i);
+        x = (i >= mc.lambda) ? small_post_flat_in(mc, W, i) * mc.scale_out : small_postmap_low_slow(mc, W, i);
       } else {
-        // postmap_high (maps_f64.cpp:372-383) with hbuf(i - 1) carried over
-        const double hk = (i < N) ? high_buf(mc, W, i) : 0.0;
+        // postmap_high (maps_f64.cpp:372-383) with hbuf(i - 1) carried over;
+        // hbuf(i) = post_flat(i) from nfold + lambda - 2 on
+        const double hk = (i >= N) ? 0.0
+                          : (i >= int64_t(mc.nfold) + mc.lambda - 2 && i >= mc.lambda - 1)
+                              ? small_post_flat_in(mc, W, i)
+                              : small_high_buf_slow(mc, W, i);
         double v;
         if (i == N) v = psi - hprev * mc.step;
         else if (i == 0) v = hk;

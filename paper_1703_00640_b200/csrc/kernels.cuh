@@ -44,11 +44,11 @@ constexpr size_t kMaxDynSmem = 232448;
 size_t mid_smem_bytes(uint32_t C, uint32_t inv_stablen);
 size_t col_smem_bytes(uint32_t R, uint32_t c);
 
-__global__ void k_small_product(SmallArgs a);
-__global__ void k_small_product_2(SmallArgs a);  // <= 384 threads, 2 CTAs per SM
-__global__ void k_small_product_big(SmallArgs a);  // <= 768 threads (batched L <= 12288)
+__global__ void k_small_product(const __grid_constant__ SmallArgs a);
+__global__ void k_small_product_2(const __grid_constant__ SmallArgs a);  // <= 384 threads, 2 CTAs per SM
+__global__ void k_small_product_big(const __grid_constant__ SmallArgs a);  // <= 768 threads (batched L <= 12288)
 // compile-time schedules for the full product at 2^16 bits (768 threads)
-__global__ void k_small_6144(SmallArgs a);
+__global__ void k_small_6144(const __grid_constant__ SmallArgs a);
 
 // ---------------------------------------------------------------------------
 // Multi-pass pipeline.  The complex transform of length L = A * B * C runs as

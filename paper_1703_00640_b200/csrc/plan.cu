@@ -413,7 +413,7 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw, const PlanOp
   // twiddles, shared between the forward and inverse schedules when they
   // line up) fits in one CTA's shared memory
   uint32_t C = 0;
-  for (uint32_t c = 4096; c >= 16; --c) {
+  for (uint32_t c = opt.max_row ? std::min<uint32_t>(4096, opt.max_row) : 4096; c >= 16; --c) {
     if (c % 2 || UL % c) continue;
     SubFft f = make_subfft(c, nullptr, 1, nullptr);
     SubFft i = make_subfft(c / 2, nullptr, 2, nullptr);

@@ -94,6 +94,7 @@ struct PlanOptions {
   bool force_three_pass = false; // three-pass plans for short column lengths
   bool premap_in_zgen = false;   // k_zgen pre-maps (double2 z), k_f1_ct reads z; not k_f1d_ct
   bool z_natural = false;        // z in natural order (k_f1d_ct needs the tile order)
+  uint32_t max_row = 0;          // longest row length C (0: 4096)
 };
 
 std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw, const PlanOptions& opt);
