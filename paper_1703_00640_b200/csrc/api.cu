@@ -345,7 +345,14 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.z = w.work_z.as<double2>();
       a.mc = pl.mc;
       a.zt = ztile(pl, L, cx.opt.z_natural);
-      const unsigned blocks = unsigned((pl.count + kZgenChunks - 1) / kZgenChunks);
+      // chunks per thread of the split: 16, or 4 / 1 when the blocks of 16
+      // would not fill the GPU twice (mid-size products are latency-bound
+      // per block)
+      int per = 16;  // (the 64-bit window path, b > 32, has only this one)
+      if (p.b <= 32 && (pl.count + 16 * kZgenThreads - 1) / (16 * kZgenThreads) < 2 * cx.num_sms) per = 4;
+      if (per == 4 && (pl.count + 4 * kZgenThreads - 1) / (4 * kZgenThreads) < 2 * cx.num_sms) per = 1;
+      a.bchunks = per * kZgenThreads;
+      const unsigned blocks = unsigned((pl.count + a.bchunks - 1) / a.bchunks);
       a.status = status;
       w.zaggs.ensure(size_t(blocks) * 4 + 16);
       a.aggs = w.zaggs.as<uint32_t>();
@@ -361,13 +368,14 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       }
       check_launch(cx, "k_zstat");
       // with k_f1d_ct the split stores digits and the first column pass pre-maps
-      ZgenFn zg = pl.f1d ? zgen_digits_kernel(int(p.b), pl.zdig)
-                         : zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda));
+      ZgenFn zg = pl.f1d ? zgen_digits_kernel(int(p.b), pl.zdig, per)
+                         : zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda), per);
       const double zbytes = pl.f1d ? (pl.zdig == 1 ? 4.0 : 8.0) : 16.0;
-      set_smem(zg, pl.smem_zgen);
+      const size_t zsm = zgen_smem(int(p.b), per);
+      set_smem(zg, zsm);
       {
         KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * zbytes, int(p.mode), st);
-        launch(cx, zg, dim3(blocks), dim3(kZgenThreads), pl.smem_zgen, st, a, "zgen");
+        launch(cx, zg, dim3(blocks), dim3(kZgenThreads), zsm, st, a, "zgen");
       }
       check_launch(cx, "k_zgen");
       kernels += 2;
@@ -542,7 +550,13 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       // limbs per thread: 4 when the block's coefficient window stays small
       // (wide chunks), else 2 (more CTAs per SM for narrow chunks)
       const bool hb = p.mode == PMode::kHigh;
-      const int pt = carry2_smem(int(p.b), lam, 4, hb) <= size_t(64) * 1024 ? 4 : 2;
+      int pt = carry2_smem(int(p.b), lam, 4, hb) <= size_t(64) * 1024 ? 4 : 2;
+      // products whose carry blocks cannot fill the GPU twice over take one
+      // limb per thread: twice the blocks, each with half the latency
+      // (single-pass kernel, mid-size products)
+      if (cx.opt.carry_kernels != 2 && carry_lb_kernel(lam, 1) &&
+          (pl.ML + int64_t(kC2Threads) * pt - 1) / (int64_t(kC2Threads) * pt) < int64_t(2 * cx.num_sms))
+        pt = 1;
       const size_t smem2 = carry2_smem(int(p.b), lam, pt, hb);
       if (!old_carry && smem2 <= kMaxDynSmem && 64 * pl.ML + 64 < (int64_t(1) << 32)) {
         high_stop_fused = p.mode == PMode::kHigh;

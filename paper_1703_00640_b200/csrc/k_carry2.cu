@@ -815,7 +815,9 @@ CarryLanesFn lb_pt(int lam) {
     default: return nullptr;
   }
 }
-CarryLanesFn carry_lb_kernel(int lam, int pt) { return pt == 4 ? lb_pt<4>(lam) : lb_pt<2>(lam); }
+CarryLanesFn carry_lb_kernel(int lam, int pt) {
+  return pt == 4 ? lb_pt<4>(lam) : pt == 2 ? lb_pt<2>(lam) : lb_pt<1>(lam);
+}
 CarryLanesFn carry_patch_kernel(int pt) { return pt == 4 ? k_carry_patch<4> : k_carry_patch<2>; }
 
 }  // namespace tmg

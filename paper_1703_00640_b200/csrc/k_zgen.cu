@@ -67,24 +67,24 @@ __device__ __forceinline__ typename StagedBits<W32>::Word load_word(const uint64
 
 // Staged words per operand: the chunks of one block plus the lambda-1 digits
 // of the next, the sub-word offset and one word of look-ahead.
-__host__ __device__ inline int64_t zgen_words(int b, int kw) {
-  return (int64_t(kZgenChunks + kMaxLambda) * b + kw - 1) / kw + 3;
+__host__ __device__ inline int64_t zgen_words(int b, int kw, int ch) {
+  return (int64_t(ch + kMaxLambda) * b + kw - 1) / kw + 3;
 }
 // staged words reserved per operand: the 16-byte loads of interior blocks
 // start up to 3 words early and round up to a multiple of 4
-__host__ __device__ inline int64_t zgen_words_alloc(int b, int kw) {
-  return (zgen_words(b, kw) + 8 + 3) / 4 * 4;  // keeps the second operand 16-byte aligned
+__host__ __device__ inline int64_t zgen_words_alloc(int b, int kw, int ch) {
+  return (zgen_words(b, kw, ch) + 8 + 3) / 4 * 4;  // keeps the second operand 16-byte aligned
 }
 
 }  // namespace
 
-size_t zgen_smem(int b) {
+size_t zgen_smem(int b, int per) {
   const int kw = b <= 32 ? 32 : 64;
-  return 2 * size_t(zgen_words_alloc(b, kw)) * (kw / 8) +
-         size_t((kZgenChunks + kMaxLambda) * 17 / 16 + 2) * 8 + 64;
+  const int ch = kZgenThreads * per;
+  return 2 * size_t(zgen_words_alloc(b, kw, ch)) * (kw / 8) + size_t((ch + kMaxLambda) * 17 / 16 + 2) * 8 + 64;
 }
 
-// Carry transfer function of each block of kZgenChunks chunks for both
+// Carry transfer function of each block of a.bchunks chunks for both
 // operands' balanced-split chains (split.cpp:88-95).  A chunk whose window
 // differs from 2^{b-1} decides its carry-out (1 above, 0 below) whatever
 // comes in, so a block's aggregate is fixed by its last such chunk: one
@@ -102,16 +102,17 @@ k_zstat(ZgenArgs a) {
   if (!a.early) pdl_wait();
   const int64_t blk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t count = a.count;
-  const int64_t nblk = (count + kZgenChunks - 1) / kZgenChunks;
+  const int64_t bch = a.bchunks;
+  const int64_t nblk = (count + bch - 1) / bch;
   if (blk >= nblk) {
     pdl_wait();
     return;
   }
   const int b = a.b;
   const uint64_t half = 1ull << (b - 1);
-  const int64_t c0 = blk * kZgenChunks;
+  const int64_t c0 = blk * bch;
   // statuses exist for chunks below the (unbalanced) top chunk only
-  const int64_t c1 = min(count - 1, c0 + kZgenChunks);
+  const int64_t c1 = min(count - 1, c0 + bch);
   uint32_t fu = 2, fv = 2;  // propagate (identity)
   if (a.mc.balanced) {
     bool du = false, dv = false;
@@ -165,9 +166,12 @@ struct DigOut<2> {
   __device__ __forceinline__ static void put(void* z, uint32_t i, int2 d) { static_cast<int2*>(z)[i] = d; }
 };
 
-template <bool W32, int LAM, int DIG = 0>
+// PER: chunks per thread (16, or 4 / 1 for short products, whose blocks
+// then fill more SMs); a block owns kZgenThreads * PER chunks.
+template <bool W32, int LAM, int DIG = 0, int PER = 16>
 __global__ void __launch_bounds__(kZgenThreads)
 k_zgen_t(ZgenArgs a) {
+  constexpr int kCh = kZgenThreads * PER;
   pdl_trigger();
   pdl_wait();
   using SB = StagedBits<W32>;
@@ -183,15 +187,15 @@ k_zgen_t(ZgenArgs a) {
   const int64_t count = a.count;
   constexpr int lam = LAM > 0 ? LAM : 1;
   constexpr int ext = lam - 1;
-  const int64_t nwd = zgen_words(b, SB::kW);
+  const int64_t nwd = zgen_words(b, SB::kW, kCh);
   Word* su = reinterpret_cast<Word*>(smem_raw);
-  Word* sv = su + zgen_words_alloc(b, SB::kW);
+  Word* sv = su + zgen_words_alloc(b, SB::kW, kCh);
   // digits of the block's chunks (and the next lam-1), u and v packed
-  int2* dig = reinterpret_cast<int2*>(sv + zgen_words_alloc(b, SB::kW));
+  int2* dig = reinterpret_cast<int2*>(sv + zgen_words_alloc(b, SB::kW, kCh));
 
   const uint32_t blk = blockIdx.x;
-  const int64_t c0 = int64_t(blk) * kZgenChunks;
-  const int64_t c1 = min(count, c0 + int64_t(kZgenChunks));
+  const int64_t c0 = int64_t(blk) * kCh;
+  const int64_t c1 = min(count, c0 + int64_t(kCh));
   const int64_t bit0 = c0 * b - a.lead;
   int64_t wbase = bit0 >> SB::kLog;  // floor, bit0 may be negative
   uint32_t off0 = uint32_t(bit0 - (wbase << SB::kLog));
@@ -202,7 +206,7 @@ k_zgen_t(ZgenArgs a) {
   bool interior = false;
   if constexpr (W32) {
     const int64_t w4 = wbase & ~int64_t(3);
-    interior = mc.balanced && b <= 30 && c1 == c0 + kZgenChunks && c1 + ext < count - 1 &&
+    interior = mc.balanced && b <= 30 && c1 == c0 + kCh && c1 + ext < count - 1 &&
                w4 >= 0 && w4 + 4 * ((nwd + 6) / 4) <= 2 * a.nlimbs &&
                ((reinterpret_cast<uintptr_t>(a.u) | reinterpret_cast<uintptr_t>(a.v)) & 15) == 0;
     if (interior) {
@@ -230,13 +234,13 @@ k_zgen_t(ZgenArgs a) {
   const uint64_t half = 1ull << (b - 1);
   const uint64_t mask = (1ull << b) - 1;
 
-  // this thread's kZgenPer windows, taken once
-  const uint32_t q0 = uint32_t(tid) * kZgenPer;  // chunk offset in the block
+  // this thread's PER windows, taken once
+  const uint32_t q0 = uint32_t(tid) * PER;  // chunk offset in the block
   const int64_t t0 = c0 + q0;
   using Win = typename std::conditional<W32, uint32_t, uint64_t>::type;
-  Win wu[kZgenPer], wv[kZgenPer];
+  Win wu[PER], wv[PER];
 #pragma unroll
-  for (int q = 0; q < kZgenPer; ++q) {
+  for (int q = 0; q < PER; ++q) {
     const uint32_t rel = off0 + (q0 + q) * uint32_t(b);
     wu[q] = Win(Lu.window(rel, mask));
     wv[q] = Win(Lv.window(rel, mask));
@@ -244,7 +248,7 @@ k_zgen_t(ZgenArgs a) {
   uint32_t gu = 0, pu = 0, gv = 0, pv = 0;
   if (interior) {
 #pragma unroll
-    for (int q = 0; q < kZgenPer; ++q) {
+    for (int q = 0; q < PER; ++q) {
       gu |= uint32_t(wu[q] > half) << q;
       pu |= uint32_t(wu[q] == half) << q;
       gv |= uint32_t(wv[q] > half) << q;
@@ -252,7 +256,7 @@ k_zgen_t(ZgenArgs a) {
     }
   } else if (mc.balanced) {
 #pragma unroll
-    for (int q = 0; q < kZgenPer; ++q) {
+    for (int q = 0; q < PER; ++q) {
       const int64_t j = t0 + q;
       if (j < c1 && j < count - 1) {
         gu |= uint32_t(wu[q] > half) << q;
@@ -264,7 +268,7 @@ k_zgen_t(ZgenArgs a) {
   }
   // kill / generate / propagate of this thread's run: its last non-P chunk
   auto kgp_of = [](uint32_t g, uint32_t p) -> uint32_t {
-    const uint32_t np = ~p & 0xffffu;
+    const uint32_t np = ~p & ((PER >= 32) ? ~0u : ((1u << PER) - 1u));
     if (!np) return 2u;
     const int last = 31 - __clz(np);
     return (g >> last) & 1u;
@@ -291,7 +295,7 @@ k_zgen_t(ZgenArgs a) {
   if (interior) {
     const int32_t hb = int32_t(half), full = int32_t(1) << b;
 #pragma unroll
-    for (int q = 0; q < kZgenPer; ++q) {
+    for (int q = 0; q < PER; ++q) {
       bu |= uint32_t(cu) << q;
       bv |= uint32_t(cv) << q;
       int32_t xu = int32_t(wu[q]) + cu, xv = int32_t(wv[q]) + cv;
@@ -303,7 +307,7 @@ k_zgen_t(ZgenArgs a) {
     }
   } else {
 #pragma unroll
-  for (int q = 0; q < kZgenPer; ++q) {
+  for (int q = 0; q < PER; ++q) {
     const int64_t j = t0 + q;
     if (j < c1) {
       bu |= uint32_t(cu) << q;
@@ -317,7 +321,7 @@ k_zgen_t(ZgenArgs a) {
   }
   }
   // the next block's first lam-1 digits (carry out of this block known)
-  if (t0 < c1 && t0 + kZgenPer >= c1) {
+  if (t0 < c1 && t0 + PER >= c1) {
     for (int q = 0; q < ext; ++q) {
       const int64_t j = c1 + q;
       if (j >= N) break;
@@ -331,11 +335,17 @@ k_zgen_t(ZgenArgs a) {
     }
   }
   {
-    const uint32_t ou = __shfl_xor_sync(0xffffffffu, bu, 1);
-    const uint32_t ov = __shfl_xor_sync(0xffffffffu, bv, 1);
-    if ((tid & 1) == 0 && t0 < count) {
-      a.cbits_u[t0 >> 5] = bu | (ou << 16);
-      a.cbits_v[t0 >> 5] = bv | (ov << 16);
+    // 32 / PER consecutive threads fill one 32-bit word of carry bits
+    constexpr int G = 32 / PER;
+    uint32_t wu32 = bu << ((tid % G) * PER), wv32 = bv << ((tid % G) * PER);
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) {
+      wu32 |= __shfl_xor_sync(0xffffffffu, wu32, off);
+      wv32 |= __shfl_xor_sync(0xffffffffu, wv32, off);
+    }
+    if ((tid % G) == 0 && t0 < count) {
+      a.cbits_u[t0 >> 5] = wu32;
+      a.cbits_v[t0 >> 5] = wv32;
     }
   }
   if (blk == 0 && tid == 0 && (a.n & 63)) {
@@ -453,28 +463,31 @@ k_zgen_t(ZgenArgs a) {
   }
 }
 
-template <bool W32>
+template <bool W32, int PER>
 ZgenFn zgen_kernel_l(int lam) {
   switch (lam) {
-    case 0: return k_zgen_t<W32, 0>;
-    case 1: return k_zgen_t<W32, 1>;
-    case 2: return k_zgen_t<W32, 2>;
-    case 3: return k_zgen_t<W32, 3>;
-    case 4: return k_zgen_t<W32, 4>;
-    case 5: return k_zgen_t<W32, 5>;
-    case 6: return k_zgen_t<W32, 6>;
-    case 7: return k_zgen_t<W32, 7>;
-    default: return k_zgen_t<W32, 8>;
+    case 0: return k_zgen_t<W32, 0, 0, PER>;
+    case 1: return k_zgen_t<W32, 1, 0, PER>;
+    case 2: return k_zgen_t<W32, 2, 0, PER>;
+    case 3: return k_zgen_t<W32, 3, 0, PER>;
+    case 4: return k_zgen_t<W32, 4, 0, PER>;
+    case 5: return k_zgen_t<W32, 5, 0, PER>;
+    case 6: return k_zgen_t<W32, 6, 0, PER>;
+    case 7: return k_zgen_t<W32, 7, 0, PER>;
+    default: return k_zgen_t<W32, 8, 0, PER>;
   }
 }
 
-ZgenFn zgen_kernel(int b, int lam) {
-  return b <= 32 ? zgen_kernel_l<true>(lam) : zgen_kernel_l<false>(lam);
+ZgenFn zgen_kernel(int b, int lam, int per) {
+  if (b > 32) return zgen_kernel_l<false, 16>(lam);
+  return per == 1 ? zgen_kernel_l<true, 1>(lam) : per == 4 ? zgen_kernel_l<true, 4>(lam) : zgen_kernel_l<true, 16>(lam);
 }
 
-ZgenFn zgen_digits_kernel(int b, int dig) {
+ZgenFn zgen_digits_kernel(int b, int dig, int per) {
   if (b > 32) return nullptr;
-  return dig == 1 ? k_zgen_t<true, 0, 1> : k_zgen_t<true, 0, 2>;
+  if (per == 1) return dig == 1 ? k_zgen_t<true, 0, 1, 1> : k_zgen_t<true, 0, 2, 1>;
+  if (per == 4) return dig == 1 ? k_zgen_t<true, 0, 1, 4> : k_zgen_t<true, 0, 2, 4>;
+  return dig == 1 ? k_zgen_t<true, 0, 1, 16> : k_zgen_t<true, 0, 2, 16>;
 }
 
 }  // namespace tmg

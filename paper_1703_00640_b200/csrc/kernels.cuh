@@ -107,20 +107,21 @@ struct ZgenArgs {
   ZTile zt;        // layout of z as k_f1 reads it
   int32_t early;   // k_zstat: operands not written by in-flight kernels (read before pdl_wait)
   uint32_t* gen;   // k_zstat advances the look-back generation of k_carry_lb
+  int32_t bchunks; // chunks per k_zgen block (kZgenThreads * per)
 };
 constexpr int kZgenThreads = 256;
 constexpr int kZgenPer = 16;
 constexpr int kZgenChunks = kZgenThreads * kZgenPer;
 __global__ void k_zstat(ZgenArgs a);
 typedef void (*ZgenFn)(ZgenArgs);
-ZgenFn zgen_kernel(int b, int lam);
+ZgenFn zgen_kernel(int b, int lam, int per = 16);
 // Digit form for the first column pass's own pre-map (k_f1d_ct): the
 // balanced digits of both operands in z's tile order, as short2 (dig = 1,
 // b <= 14) or int2 (dig = 2), no pre-map.
-ZgenFn zgen_digits_kernel(int b, int dig);
+ZgenFn zgen_digits_kernel(int b, int dig, int per = 16);
 // digit element type of a chunk width for the digit form
 inline int zdig_kind(int b) { return b <= 14 ? 1 : 2; }
-size_t zgen_smem(int b);
+size_t zgen_smem(int b, int per = 16);
 
 // F1: forward column DFTs over A of the pre-mapped coefficients.
 struct F1Args {

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python tools/kernel_times.py 24 26 > gpurun_out/ktimes.log 2>&1
+timeout 300 python tools/kernel_times.py 18 20 22 24 26 > gpurun_out/ktimes.log 2>&1
