@@ -201,7 +201,9 @@ enum {
   TMG_OPT_CARRY_KERNELS = 12         /* 1: single-pass look-back carry (k_carry_lb); 2: carry-ins by
                                         a second kernel (k_carry_lanes + k_carry_patch); 0 (default):
                                         one kernel while the carry blocks fit one wave, else two */,
-  TMG_OPT_MAX_ROW = 13               /* longest row length C of multi-pass plans (0: 4096) */
+  TMG_OPT_MAX_ROW = 13,               /* longest row length C of multi-pass plans (0: 4096) */
+  TMG_OPT_SPLIT_AGGREGATES = 14      /* the split's block carry-ins always from k_zstat's aggregates
+                                        (default: a look-back inside k_zgen for one-wave grids) */
 };
 int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value);
 

@@ -83,7 +83,8 @@ struct Profiler {
 // to kMaxBatchStreams workspaces, each on its own stream.
 struct Workspace {
   DevBuf work_t, work_c, work_z, cbu, cbv, aux, tbuf, aggs, zaggs, ticket, hticket, status;
-  DevBuf gen;  // look-back generation of k_carry_lb, advanced by k_zstat (zero-initialised)
+  DevBuf gen;  // look-back generation of k_zgen / k_carry_lb, advanced by the row pass (zeroed)
+  DevBuf zlb;  // k_zgen look-back words (zeroed)
   ScanSlot scan_c;  // look-back state of the single-pass carry (k_carry)
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
@@ -105,6 +106,7 @@ struct Options {
   bool generic_row = false;     // TMG_OPT_GENERIC_ROW_PASS
   bool lookback_carry = false;  // TMG_OPT_LOOKBACK_CARRY
   int carry_kernels = 0;        // TMG_OPT_CARRY_KERNELS (0 by size)
+  bool zstat_split = false;     // TMG_OPT_SPLIT_AGGREGATES
   long patch_scan_max = long(kPatchScanMaxBlocks);  // TMG_OPT_PATCH_SCAN_MAX
   bool no_pdl = false;          // TMG_OPT_NO_PDL
   bool debug_sync = false;      // TMG_OPT_DEBUG_SYNC
@@ -362,11 +364,26 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         TMG_CUDA(cudaMemsetAsync(w.gen.p, 0, 64, st));
       }
       a.gen = w.gen.as<uint32_t>();
-      {
-        KTimer kt(cx, "k_zstat", double(2 * pl.nlimbs) * 8.0, int(p.mode), st);
-        launch(cx, k_zstat, dim3((blocks + 255) / 256), dim3(256), 0, st, a, "zstat");
+      // grids of one wave (4 CTAs per SM) take their carry-ins by look-back
+      // inside k_zgen: no k_zstat launch; larger ones compose k_zstat's
+      // aggregates (a block waiting on an unscheduled predecessor would hold
+      // its slot)
+      const bool zlb = !cx.opt.zstat_split && blocks <= unsigned(4 * cx.num_sms);
+      a.lbstate = nullptr;
+      if (zlb) {
+        if (w.zlb.bytes < size_t(blocks) * 8) {
+          w.zlb.ensure(size_t(blocks) * 8);
+          TMG_CUDA(cudaMemsetAsync(w.zlb.p, 0, w.zlb.bytes, st));
+        }
+        a.lbstate = w.zlb.as<unsigned long long>();
+      } else {
+        {
+          KTimer kt(cx, "k_zstat", double(2 * pl.nlimbs) * 8.0, int(p.mode), st);
+          launch(cx, k_zstat, dim3((blocks + 255) / 256), dim3(256), 0, st, a, "zstat");
+        }
+        check_launch(cx, "k_zstat");
+        ++kernels;
       }
-      check_launch(cx, "k_zstat");
       // with k_f1d_ct the split stores digits and the first column pass pre-maps
       ZgenFn zg = pl.f1d ? zgen_digits_kernel(int(p.b), pl.zdig, per)
                          : zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda), per);
@@ -378,7 +395,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         launch(cx, zg, dim3(blocks), dim3(kZgenThreads), zsm, st, a, "zgen");
       }
       check_launch(cx, "k_zgen");
-      kernels += 2;
+      ++kernels;
     }
     double2* T = w.work_t.as<double2>();
     {
@@ -452,6 +469,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.inv = pl.iC;
       a.tw = pl.twL;
       a.L = uint32_t(L);
+      a.gen = w.gen.as<uint32_t>();
       const unsigned npairs = (pl.A * pl.B) / 2 + 1;
       if (pl.C == 4096 && pl.mid_shared_table && !cx.opt.generic_row) {
         // compile-time schedule, persistent over row pairs
@@ -1247,6 +1265,11 @@ int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value) {
       case TMG_OPT_Z_NATURAL: o.z_natural = o.plan.z_natural = on; break;
       case TMG_OPT_GENERIC_SMALL: o.generic_small = on; break;
       case TMG_OPT_PREMAP_IN_SPLIT: o.plan.premap_in_zgen = on; break;
+      case TMG_OPT_SPLIT_AGGREGATES: o.zstat_split = on; break;
+      case TMG_OPT_MAX_ROW:
+        if (value < 0 || value > 4096) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "row length cap in [0, 4096]");
+        o.plan.max_row = uint32_t(value);
+        break;
       case TMG_OPT_CARRY_KERNELS:
         if (value < 0 || value > 2) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "carry kernels: 0, 1 or 2");
         o.carry_kernels = int(value);

@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(512)
 k_mid(MidArgs a) {
   pdl_trigger();
   pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.gen += 1u;  // next look-backs' generation
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -667,6 +668,10 @@ __device__ __forceinline__ void mid_4096_body(const MidArgs& a) {
   pdl_trigger();
   for (uint32_t i = tid; i < a.fwd.stablen; i += NTHR) stw[i] = __ldg(a.fwd.stab + i);
   pdl_wait();
+  // a new generation for the look-backs after this kernel (this product's
+  // carry, the next product's split): they follow it in stream order, the
+  // split and the carry of this product that precede it have completed
+  if (blockIdx.x == 0 && tid == 0) *a.gen += 1u;
   auto row_base = [&](uint32_t r) {
     return a.data + (int64_t(r % a.A) * a.B + (r / a.A)) * int64_t(C);
   };

@@ -138,9 +138,6 @@ k_zstat(ZgenArgs a) {
   }
   a.aggs[blk] = fu | (fv << 2);
   pdl_wait();
-  // a new look-back generation for this product's k_carry_lb (after the
-  // wait: the previous product's carry kernel has completed)
-  if (blk == 0) *a.gen += 1u;
 }
 
 // LAM: the series length lambda (rows of the pre-map), 0 for the full
@@ -275,9 +272,34 @@ k_zgen_t(ZgenArgs a) {
   };
   uint32_t agg2;
   const uint32_t ex2 = block_scan_kgp(kgp_of(gu, pu) | (kgp_of(gv, pv) << 2), sw, &agg2);
-  // carry into the block: the aggregates of the blocks before it (k_zstat),
-  // composed in order by the whole block
-  {
+  // carry into the block: by a look-back over the predecessors' published
+  // aggregates (one-wave grids, no k_zstat), or the aggregates of the blocks
+  // before it (k_zstat) composed in order by the whole block
+  if (a.lbstate) {
+    if (tid == 0) {
+      const unsigned long long ep = (unsigned long long)(*a.gen) << 32;
+      volatile unsigned long long* st = a.lbstate;
+      if (blk != 0) st[blk] = ep | (1ull << 30) | agg2;
+      // G = F_{blk-1} o ... o F_j until it has no propagate field (its value
+      // no longer depends on the carries before) or an inclusive word
+      uint32_t G = kKgpIdentity, cin = 0u;
+      for (int64_t j = int64_t(blk) - 1; j >= 0; --j) {
+        unsigned long long w;
+        do {
+          w = st[j];
+        } while ((w >> 32) != (ep >> 32) || ((w >> 30) & 3u) == 0);
+        if (((w >> 30) & 3u) == 2) {
+          G = kgp_compose(uint32_t(w & 0xFu), G);
+          break;
+        }
+        G = kgp_compose(uint32_t(w & 0xFu), G);
+        if (((G >> 1) & 0x5u) == 0) break;  // no propagate field left
+      }
+      cin = kgp_compose(0u, G);  // both chains start with carry 0
+      st[blk] = ep | (2ull << 30) | kgp_compose(cin, agg2);
+      s_cin = cin;
+    }
+  } else {
     uint32_t g = kKgpIdentity;
     const uint32_t Q = (blk + kZgenThreads - 1) / kZgenThreads;
     const uint32_t i0 = uint32_t(tid) * Q, i1 = min(blk, i0 + Q);

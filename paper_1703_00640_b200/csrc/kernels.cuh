@@ -106,8 +106,11 @@ struct ZgenArgs {
   uint32_t* aggs;  // per-block carry transfer functions (k_zstat)
   ZTile zt;        // layout of z as k_f1 reads it
   int32_t early;   // k_zstat: operands not written by in-flight kernels (read before pdl_wait)
-  uint32_t* gen;   // k_zstat advances the look-back generation of k_carry_lb
+  uint32_t* gen;   // look-back generation (advanced by the row pass, k_mid*)
   int32_t bchunks; // chunks per k_zgen block (kZgenThreads * per)
+  // k_zgen without k_zstat: each block's carry-in by a decoupled look-back
+  // over these words (grids of one wave); null: composed from k_zstat's aggs
+  unsigned long long* lbstate;
 };
 constexpr int kZgenThreads = 256;
 constexpr int kZgenPer = 16;
@@ -176,6 +179,7 @@ struct MidArgs {
   SubFft inv;   // length C / 2
   TwGlobal tw;  // omega_L
   uint32_t L;
+  uint32_t* gen;  // look-back generation of the split and the carry (advanced here)
 };
 __global__ void k_mid(MidArgs a);
 // C = 4096 row pass with compile-time schedules, persistent over row pairs.

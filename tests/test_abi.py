@@ -128,3 +128,22 @@ def test_cpp_api_products(tmp_path):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK" in r.stdout.splitlines()[-1]
+
+
+@pytest.mark.gpu
+def test_every_context_option_is_accepted():
+    """Every TMG_OPT_* the header declares is handled by
+    tmg_context_set_option (and an unknown one is refused)."""
+    import re
+    import paper_1703_00640_b200 as tm
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    hdr = open(os.path.join(root, "include", "truncmul_b200.h")).read()
+    opts = {m.group(1): int(m.group(2)) for m in re.finditer(r"(TMG_OPT_\w+)\s*=\s*(\d+)", hdr)}
+    assert len(opts) >= 14
+    c = tm.Context(0)
+    for name, val in opts.items():
+        assert getattr(tm._native, name) == val, name
+        c.set_option(val, 0)
+    with pytest.raises(tm.InputOutOfRange):
+        c.set_option(999, 1)
+    c.close()

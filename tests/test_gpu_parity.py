@@ -914,3 +914,31 @@ def test_carry_kernel_paths(n, kernels):
             assert np.array_equal(r0, r1)
             _check(mode, u, v, n, tm.from_limbs(r0))
     c.close()
+
+
+@pytest.mark.parametrize("n", [1 << 18, 1 << 20, (1 << 22) + 448])
+def test_split_carry_in_paths(n):
+    """TMG_OPT_SPLIT_AGGREGATES: the split's block carry-ins composed from
+    k_zstat's aggregates, against the default look-back inside k_zgen for
+    one-wave grids; random operands and long balanced-carry chains (windows
+    equal to 2^{b-1} over many blocks: limbs 0x8080...)."""
+    c = _opt_ctx((tm._native.TMG_OPT_SPLIT_AGGREGATES, 1))
+    _config3_all_modes(c, n)
+    nl = (n + 63) // 64
+    M = (1 << n) - 1
+    chain = int.from_bytes(bytes([0x80]) * (nl * 8), "little") & M
+    for a, b_ in ((M, M), (chain, chain), (chain, M - 5)):
+        u, v = port.int_to_limbs(a, nl), port.int_to_limbs(b_, nl)
+        for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+            try:
+                r0 = tm.default_context(0).product_limbs(mode, u, v, sp(n, mode))
+            except tm.ConvolutionPrecisionFailure:
+                # a structured spectrum the policy's b cannot certify: the
+                # other path refuses it the same way
+                with pytest.raises(tm.ConvolutionPrecisionFailure):
+                    c.product_limbs(mode, u, v, sp(n, mode))
+                continue
+            r1 = c.product_limbs(mode, u, v, sp(n, mode))
+            assert np.array_equal(r0, r1)
+            _check(mode, u, v, n, tm.from_limbs(r0))
+    c.close()
