@@ -471,7 +471,14 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.L = uint32_t(L);
       a.gen = w.gen.as<uint32_t>();
       const unsigned npairs = (pl.A * pl.B) / 2 + 1;
-      if (pl.C == 4096 && pl.mid_shared_table && !cx.opt.generic_row) {
+      if (pl.mid_ct) {
+        // compiled shorter rows, persistent over the row pairs
+        auto mk = pl.C == 2048 ? k_mid_2048 : k_mid_1024;
+        set_smem(mk, pl.smem_mid);
+        const unsigned grid = std::min<unsigned>(npairs, unsigned(cx.num_sms));
+        KTimer kt(cx, "k_mid", double(L) * 16.0 + double(L) * 8.0, int(p.mode), st);
+        launch(cx, mk, dim3(grid), dim3(kMidCtThreads), pl.smem_mid, st, a, "mid");
+      } else if (pl.C == 4096 && pl.mid_shared_table && !cx.opt.generic_row) {
         // compile-time schedule, persistent over row pairs
         set_smem(k_mid_4096, pl.smem_mid);
         const unsigned grid = std::min<unsigned>(npairs, unsigned(cx.num_sms));
@@ -1253,7 +1260,7 @@ int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value) {
     switch (option) {
       case TMG_OPT_GENERIC_COLUMN_PASSES: o.plan.generic_columns = on; break;
       case TMG_OPT_FORCE_THREE_PASS: o.plan.force_three_pass = on; break;
-      case TMG_OPT_GENERIC_ROW_PASS: o.generic_row = on; break;
+      case TMG_OPT_GENERIC_ROW_PASS: o.generic_row = o.plan.generic_row = on; break;
       case TMG_OPT_LOOKBACK_CARRY: o.lookback_carry = on; break;
       case TMG_OPT_PATCH_SCAN_MAX:
         if (value < 0) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "patch scan limit must be >= 0");

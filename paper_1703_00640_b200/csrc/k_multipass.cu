@@ -23,6 +23,8 @@
 //
 // Reference path: products_f64.cpp:106-171 with the FFTW convolution of
 // convolution.cpp:175-195.
+#include <vector>
+
 #include "kernels.cuh"
 #include "fft_ct.cuh"
 #include "colct.cuh"
@@ -701,6 +703,133 @@ __device__ __forceinline__ void mid_4096_body(const MidArgs& a) {
 __global__ void __launch_bounds__(kMidCtThreads)
 k_mid_4096(MidArgs a) {
   mid_4096_body<kMidCtThreads>(a);
+}
+
+// ---------------------------------------------------------------------------
+// Row pass for the shorter rows of mid-size products (C = 2048, 1024: more
+// row pairs, each a fraction of a 4096-point pair's latency).  Forward
+// (8|4) x 16 x 16 and inverse (4|2) x 16 x 16 with one butterfly per thread
+// and stage (512 threads, half a CTA per row), the inverse reading the
+// forward stage table at every second entry; the spectral product and
+// repack in shared memory between them, one thread per four slots.
+// Persistent over the row pairs.
+template <uint32_t M>
+__device__ __forceinline__ double2 rot_m(double2 t, int si) {
+  // t omega_M^si (forward sign), M in {2, 4, 8}, si < M / ... via omega_8
+  const int e = si * int(8 / M);
+  return e == 0 ? t : e == 1 ? w8_1<false>(t) : e == 2 ? mul_mi<false>(t) : w8_3<false>(t);
+}
+template <uint32_t M>
+__device__ __forceinline__ double2 rot_m_inv(double2 t, int si) {
+  const int e = si * int(8 / M);
+  return e == 0 ? t : e == 1 ? w8_1<true>(t) : e == 2 ? mul_mi<true>(t) : w8_3<true>(t);
+}
+
+template <uint32_t C, int NTHR, class Fwd, class Inv>
+__device__ __forceinline__ void mid_pair_ct(const MidArgs& a, double2* __restrict__ sbuf,
+                                            const double2* __restrict__ stab, double2* __restrict__ qt,
+                                            uint32_t r0, int tid, double2 wc0, double2 wc1) {
+  constexpr uint32_t H = C / 2;
+  const uint32_t AB = a.A * a.B;
+  const uint32_t r1 = (AB - r0) % AB;
+  const uint32_t nrows = (r1 == r0) ? 1 : 2;
+  const RowPair lay{padded_len(C) + 4, nrows};
+  const int64_t base0 = (int64_t(r0 % a.A) * a.B + (r0 / a.A)) * int64_t(C);
+  const int64_t base1 = (int64_t(r1 % a.A) * a.B + (r1 / a.A)) * int64_t(C);
+  double2 x[16];
+  ct_stages<false, Fwd, 0, NTHR>(x, sbuf, lay, stab, a.fwd, RowSrc{a.data, base0, base1},
+                                 SmemSink<RowPair>{sbuf, lay}, tid);
+  __syncthreads();
+  constexpr uint32_t RL = uint32_t(Inv::rad(Inv::nst - 1));
+  constexpr uint32_t NSL = Inv::ns(Inv::nst - 1);
+  static_assert(2 * RL <= kMidQEntries, "output twiddle table");
+  if (uint32_t(tid) < 2 * RL) {
+    const uint32_t it = uint32_t(tid) / RL, q = uint32_t(tid) - it * RL;
+    const uint32_t xq = 2u * (it ? r1 : r0) * NSL * q;
+    qt[tid] = xq ? a.tw.get(xq) : make_double2(1.0, 0.0);
+  }
+  auto spec = [&](double2 z1, double2 z2) {
+    const double2 p = make_double2(z1.x + z2.x, z1.y - z2.y);
+    const double2 q = make_double2(z1.x - z2.x, z1.y + z2.y);
+    const double2 pq = cmul(p, q);
+    return make_double2(pq.y, -pq.x);  // -i pq, unscaled (see CoefSink)
+  };
+  auto repack_w = [&](double2 w1, double2 w2, double2 t) {
+    const double2 ev = cadd(w1, w2);
+    const double2 o = cmulc(csub(w1, w2), t);
+    return make_double2(ev.x - o.y, ev.y + o.x);
+  };
+  if (nrows == 2) {
+    // (the pairing and twiddle factorisation of mid_pair_4096_reg's
+    // smem form: thread k reads Z0_k, Z0_{k+H}, Z1_{C-1-k}, Z1_{H-1-k} and
+    // writes Y0_k, Y1_{H-1-k}; omega_C^{NTHR si} = omega_{C/NTHR}^si)
+    static_assert(H % NTHR == 0, "repack twiddle layout");
+    const double2 t0 = cmul(a.tw.get(r0), wc0), t1 = cmul(a.tw.get(r1), wc1);
+#pragma unroll
+    for (int si = 0; si < int(H / NTHR); ++si) {
+      const uint32_t k = uint32_t(tid) + NTHR * uint32_t(si);
+      const uint32_t kq = H - 1 - k;
+      const double2 a0 = sbuf[lay.idx(0, k)], a1 = sbuf[lay.idx(0, k + H)];
+      const double2 b0 = sbuf[lay.idx(1, C - 1 - k)], b1 = sbuf[lay.idx(1, kq)];
+      const double2 wk = spec(a0, b0), wkh = spec(a1, b1);
+      sbuf[lay.idx(0, k)] = repack_w(wk, wkh, rot_m<C / NTHR>(t0, si));
+      sbuf[lay.idx(1, kq)] = repack_w(cconj(wkh), cconj(wk), rot_m_inv<C / NTHR>(t1, si));
+    }
+  } else {
+    const uint32_t brw = (r0 != 0) ? 1u : 0u;
+    for (uint32_t k = tid; k < C; k += NTHR) {
+      const uint32_t kp = (C - k - brw) & (C - 1);
+      if (kp < k) continue;
+      const double2 w = spec(sbuf[lay.idx(0, k)], sbuf[lay.idx(0, kp)]);
+      sbuf[lay.idx(0, k)] = w;
+      if (kp != k) sbuf[lay.idx(0, kp)] = cconj(w);
+    }
+    __syncthreads();
+    for (uint32_t k = tid; k < H; k += NTHR)
+      sbuf[lay.idx(0, k)] = repack_w(sbuf[lay.idx(0, k)], sbuf[lay.idx(0, k + H)], a.tw.get(r0 + AB * k));
+  }
+  __syncthreads();
+  ct_stages<true, Inv, 0, NTHR, SmemSrc<RowPair>, RowSinkQ<RL>, 2>(
+      x, sbuf, lay, stab, a.fwd, SmemSrc<RowPair>{sbuf, lay},
+      RowSinkQ<RL>{a.data, base0, base1, r0, r1, a.tw, qt}, tid);
+}
+
+template <uint32_t C, class Fwd, class Inv>
+__device__ __forceinline__ void mid_ct_body(const MidArgs& a) {
+  constexpr int NTHR = kMidCtThreads;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sbuf = reinterpret_cast<double2*>(smem_raw);
+  const int tid = threadIdx.x;
+  const uint32_t AB = a.A * a.B;
+  const uint32_t npairs = AB / 2 + 1;
+  double2* stw = sbuf + 2 * (padded_len(C) + 4);
+  pdl_trigger();
+  for (uint32_t i = tid; i < a.fwd.stablen; i += NTHR) stw[i] = __ldg(a.fwd.stab + i);
+  pdl_wait();
+  if (blockIdx.x == 0 && tid == 0) *a.gen += 1u;  // next look-backs' generation
+  // omega_C^tid and omega_C^{H-1-tid} (repack twiddles, tid < H)
+  const double2 wc0 = tid ? a.tw.get(AB * uint32_t(tid)) : make_double2(1.0, 0.0);
+  const double2 wc1 = a.tw.get(AB * (C / 2 - 1 - uint32_t(tid) % (C / 2)));
+  __syncthreads();
+  for (uint32_t r0 = blockIdx.x; r0 < npairs; r0 += gridDim.x)
+    mid_pair_ct<C, NTHR, Fwd, Inv>(a, sbuf, stw, stw + C, r0, tid, wc0, wc1);
+}
+
+__global__ void __launch_bounds__(kMidCtThreads)
+k_mid_2048(MidArgs a) {
+  mid_ct_body<2048, Sched<8, 16, 16>, Sched<4, 16, 16>>(a);
+}
+__global__ void __launch_bounds__(kMidCtThreads)
+k_mid_1024(MidArgs a) {
+  mid_ct_body<1024, Sched<4, 16, 16>, Sched<2, 16, 16>>(a);
+}
+
+// radices of the compiled row passes' forward schedules (plan.cu builds the
+// stage table with them); empty for other lengths
+std::vector<int> mid_ct_radices(uint32_t C) {
+  if (C == 2048) return {8, 16, 16};
+  if (C == 1024) return {4, 16, 16};
+  return {};
 }
 
 // ---------------------------------------------------------------------------

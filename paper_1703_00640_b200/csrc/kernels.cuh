@@ -10,6 +10,7 @@ namespace tmg {
 
 // Transform lengths up to this run as one fused CTA per product.
 constexpr int64_t kSmallMaxL = 8192;
+constexpr int64_t kSmallSingleMaxL = 4096;  // single products above: multi-pass (plan.cu)
 // Batches of products up to this length (that fit one CTA's shared memory)
 // run the fused single-CTA kernel, one CTA per product, instead of a
 // multi-pass chain per product (plan.small_batch).
@@ -185,6 +186,9 @@ __global__ void k_mid(MidArgs a);
 // C = 4096 row pass with compile-time schedules, persistent over row pairs.
 constexpr int kMidCtThreads = 512;
 __global__ void k_mid_4096(MidArgs a);
+// compiled row passes of the shorter rows (mid-size products)
+__global__ void k_mid_2048(MidArgs a);
+__global__ void k_mid_1024(MidArgs a);
 
 struct ILastArgs {
   const double2* data;  // S[k_a][...] with geometry g (outer = 0)

@@ -11,6 +11,7 @@
 #include "../../include/truncmul_b200.h"
 
 namespace tmg {
+std::vector<int> mid_ct_radices(uint32_t C);  // k_multipass.cu
 
 #define TMG_CUDA(call)                                                     \
   do {                                                                     \
@@ -383,7 +384,10 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw, const PlanOp
     pl->ML = std::max<int64_t>(pl->ML, pl->out_limbs + (pl->shift_s >> 6) + 2);
   }
 
-  if (L <= kSmallMaxL) {
+  // One CTA computes the whole product up to L = 4096; a single product of
+  // 4096 < L <= 8192 runs the multi-pass pipeline over many SMs (2^16 low:
+  // 78 us in one CTA), and batches of it the fused kernel (small_batch).
+  if (L <= kSmallSingleMaxL) {
     pl->kind = 1;
     const double2* t = tw.table(uint32_t(L));
     pl->fwd = make_subfft(uint32_t(L), t, 1, nullptr);
@@ -413,7 +417,29 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw, const PlanOp
   // twiddles, shared between the forward and inverse schedules when they
   // line up) fits in one CTA's shared memory
   uint32_t C = 0;
-  for (uint32_t c = opt.max_row ? std::min<uint32_t>(4096, opt.max_row) : 4096; c >= 16; --c) {
+  // Mid-size products have few 4096-point row pairs (11 at 2^20), and the
+  // row pass then costs one pair's latency.  Below 32 pairs the compiled
+  // 2048- / 1024-point row passes are taken: among the lengths with at
+  // least 20 pairs (else all), the longest whose column length has a
+  // compiled column pass, else the longest (else the shortest)
+  // (tools/kernel_times.py with TMG_OPT_MAX_ROW: 2^20 low 45.4 -> 39.9 us,
+  // full 58.2 -> 40.6, 2^18 low 40.7 -> 37.8).
+  if (!opt.max_row && !opt.generic_row && UL <= (uint64_t(1) << 21) &&
+      !(UL % 4096 == 0 && UL / 4096 / 2 + 1 >= 32)) {
+    uint32_t pick = 0, pick_col = 0, smallest = 0;
+    bool any20 = false;
+    for (uint32_t c : {4096u, 2048u, 1024u})
+      if (UL % c == 0 && UL / c / 2 + 1 >= 20) any20 = true;
+    for (uint32_t c : {4096u, 2048u, 1024u}) {
+      if (UL % c || (c != 4096 && mid_ct_radices(c).empty())) continue;
+      smallest = c;
+      if (any20 && UL / c / 2 + 1 < 20) continue;
+      if (!pick) pick = c;
+      if (!pick_col && UL / c <= 2048 && colct_for(uint32_t(UL / c), 1)) pick_col = c;
+    }
+    C = pick_col ? pick_col : (any20 ? pick : smallest);
+  }
+  for (uint32_t c = opt.max_row ? std::min<uint32_t>(4096, opt.max_row) : 4096; C == 0 && c >= 16; --c) {
     if (c % 2 || UL % c) continue;
     SubFft f = make_subfft(c, nullptr, 1, nullptr);
     SubFft i = make_subfft(c / 2, nullptr, 2, nullptr);
@@ -454,6 +480,16 @@ std::unique_ptr<Plan> build_plan(const Params& p, TwiddleCache& tw, const PlanOp
   pl->fC = make_subfft(C, tC, 1, &tw);
   pl->iC = make_subfft(C / 2, tC, 2, &tw);
   pl->mid_shared_table = map_stages(pl->iC, pl->fC);
+  // compiled row passes of 2048 / 1024 (k_mid_2048 / k_mid_1024): their own
+  // forward schedule's stage table; the inverse reads it at every second entry
+  pl->mid_ct = false;
+  if (!opt.generic_row) {
+    const std::vector<int> mr = mid_ct_radices(C);
+    if (!mr.empty()) {
+      pl->fC = make_subfft_rad(C, mr, tC, 1, &tw);
+      pl->mid_ct = true;
+    }
+  }
   const int col_logc_cap = 6;  // columns per CTA of the column passes: at most 64
   pl->logc_f1 = std::min<uint32_t>(pick_logc(A, UL / A, cap), uint32_t(col_logc_cap));
   pl->thr_f1 = threads_for(uint64_t(A) << pl->logc_f1);

@@ -83,6 +83,7 @@ struct Plan {
   int thr_f1 = 0, thr_f2 = 0, thr_i2 = 0, thr_il = 0, thr_mid = 0;
   size_t smem_zgen = 0;
   bool mid_shared_table = false;
+  bool mid_ct = false;  // C = 2048 / 1024 with a compiled row pass (k_mid_2048 / k_mid_1024)
   bool colpp = false;  // column passes use the ping-pong kernels (k_*_pp)
   int kernels = 0;
 };
@@ -91,6 +92,7 @@ struct Plan {
 // the defaults are the measured-best shapes.
 struct PlanOptions {
   bool generic_columns = false;  // runtime-dispatched column passes, not the compiled shapes
+  bool generic_row = false;      // the runtime-dispatched row pass k_mid, not the compiled ones
   bool force_three_pass = false; // three-pass plans for short column lengths
   bool premap_in_zgen = false;   // k_zgen pre-maps (double2 z), k_f1_ct reads z; not k_f1d_ct
   bool z_natural = false;        // z in natural order (k_f1d_ct needs the tile order)
