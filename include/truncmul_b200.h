@@ -203,7 +203,7 @@ enum {
                                         one kernel while the carry blocks fit one wave, else two */,
   TMG_OPT_MAX_ROW = 13,               /* longest row length C of multi-pass plans (0: 4096) */
   TMG_OPT_SPLIT_AGGREGATES = 14      /* the split's block carry-ins always from k_zstat's aggregates
-                                        (default: a look-back inside k_zgen for one-wave grids) */
+                                        (default: a look-back inside k_zgen) */
 };
 int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value);
 

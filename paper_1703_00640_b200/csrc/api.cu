@@ -364,11 +364,12 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         TMG_CUDA(cudaMemsetAsync(w.gen.p, 0, 64, st));
       }
       a.gen = w.gen.as<uint32_t>();
-      // grids of one wave (4 CTAs per SM) take their carry-ins by look-back
-      // inside k_zgen: no k_zstat launch; larger ones compose k_zstat's
-      // aggregates (a block waiting on an unscheduled predecessor would hold
-      // its slot)
-      const bool zlb = !cx.opt.zstat_split && blocks <= unsigned(4 * cx.num_sms);
+      // the split blocks take their carry-ins by a look-back inside k_zgen
+      // (no k_zstat launch): a block's aggregate is published early (after
+      // its windows), and its predecessor was dispatched before it, so the
+      // waits are short (2^26 low 271.4 -> 267.2 us, 2^24 high 104.2 -> 101.1);
+      // TMG_OPT_SPLIT_AGGREGATES composes k_zstat's aggregates instead
+      const bool zlb = !cx.opt.zstat_split;
       a.lbstate = nullptr;
       if (zlb) {
         if (w.zlb.bytes < size_t(blocks) * 8) {
@@ -579,8 +580,10 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       // products whose carry blocks cannot fill the GPU twice over take one
       // limb per thread: twice the blocks, each with half the latency
       // (single-pass kernel, mid-size products)
+      // (the single-pass kernel only: its one-wave rule must still hold)
       if (cx.opt.carry_kernels != 2 && carry_lb_kernel(lam, 1) &&
-          (pl.ML + int64_t(kC2Threads) * pt - 1) / (int64_t(kC2Threads) * pt) < int64_t(2 * cx.num_sms))
+          (pl.ML + int64_t(kC2Threads) * pt - 1) / (int64_t(kC2Threads) * pt) < int64_t(2 * cx.num_sms) &&
+          (pl.ML + kC2Threads - 1) / kC2Threads <= int64_t(4 * cx.num_sms))
         pt = 1;
       const size_t smem2 = carry2_smem(int(p.b), lam, pt, hb);
       if (!old_carry && smem2 <= kMaxDynSmem && 64 * pl.ML + 64 < (int64_t(1) << 32)) {
@@ -606,7 +609,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         // waits stay short, and a launch is saved (2^20 low 57.9 -> 55.3 us);
         // beyond, blocks that wait for a predecessor hold their slots, and the
         // second kernel costs less (2^26 low 271.6 against 278.0 us)
-        const bool one = cx.opt.carry_kernels == 1 ||
+        const bool one = pt == 1 || cx.opt.carry_kernels == 1 ||
                          (cx.opt.carry_kernels == 0 && blocks2 <= unsigned(4 * cx.num_sms));
         CarryLanesFn lbk = one ? carry_lb_kernel(lam, pt) : nullptr;
         if (lbk) {
@@ -623,6 +626,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
           kernels += 1;
         } else {
         CarryLanesFn lanes = carry_lanes_kernel(lam, pt);
+        if (!lanes) throw Error(TMG_ERR_UNSUPPORTED, "carry lanes kernel: no instantiation for this block shape");
         set_smem(lanes, smem2);
         {
           KTimer kt(cx, "k_carry_lanes", double(pl.K) * 8.0 + double(hb ? pl.ML : pl.out_limbs) * 8.0, int(p.mode),

@@ -804,7 +804,9 @@ CarryLanesFn lanes_pt(int lam) {
   }
 }
 
-CarryLanesFn carry_lanes_kernel(int lam, int pt) { return pt == 4 ? lanes_pt<4>(lam) : lanes_pt<2>(lam); }
+CarryLanesFn carry_lanes_kernel(int lam, int pt) {
+  return pt == 4 ? lanes_pt<4>(lam) : pt == 2 ? lanes_pt<2>(lam) : nullptr;
+}
 
 template <int PT>
 CarryLanesFn lb_pt(int lam) {

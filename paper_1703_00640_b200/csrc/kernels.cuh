@@ -110,7 +110,7 @@ struct ZgenArgs {
   uint32_t* gen;   // look-back generation (advanced by the row pass, k_mid*)
   int32_t bchunks; // chunks per k_zgen block (kZgenThreads * per)
   // k_zgen without k_zstat: each block's carry-in by a decoupled look-back
-  // over these words (grids of one wave); null: composed from k_zstat's aggs
+  // over these words (the default); null: composed from k_zstat's aggs
   unsigned long long* lbstate;
 };
 constexpr int kZgenThreads = 256;

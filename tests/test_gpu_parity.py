@@ -49,7 +49,8 @@ def _rand(rng, n):
     return a
 
 
-@pytest.mark.parametrize("n", [4096, 5001, 8192, 20011, 65536, 100003, 262144, 1000000, 1 << 22])
+@pytest.mark.parametrize("n", [4096, 5001, 8192, 20011, 65536, 100003, 105078, 262144, 1000000, 1 << 22,
+                               4748529])
 def test_random_products_match_exact(ctx, n):
     rng = np.random.default_rng(n)
     for _ in range(3):
