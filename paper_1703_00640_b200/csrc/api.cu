@@ -734,6 +734,9 @@ void enqueue(Context& cx, Plan& pl, const uint64_t* du, const uint64_t* dv,
     if (!small_generic && pl.L == 6144 && p.mode == PMode::kFull) {
       sk = k_small_6144;
       threads = 768;
+    } else if (!small_generic && pl.L == 5120 && p.mode != PMode::kFull && two) {
+      sk = k_small_5120;
+      threads = 384;
     }
     set_smem(sk, pl.small_smem);
     {

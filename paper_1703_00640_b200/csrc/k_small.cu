@@ -103,6 +103,14 @@ k_small_6144(const __grid_constant__ SmallArgs a) {
   small_product_body<768, 1, Sched<8, 8, 8, 12>, Sched<8, 8, 4, 12>>(a);
 }
 
+// The truncated products of BASELINE config 4 (2^16 bits, L = 5120 =
+// 16 x 16 x 5 x 4, inverse 2560 = 16 x 16 x 10) with compile-time schedules
+// at two 384-thread CTAs per SM.
+__global__ void __launch_bounds__(384, 2)
+k_small_5120(const __grid_constant__ SmallArgs a) {
+  small_product_body<384, 2, Sched<16, 16, 5, 4>, Sched<16, 16, 10>>(a);
+}
+
 // Batches of products just above the single-product cutoff (L <= 12288, the
 // 2^17-bit range): one CTA per product at up to 768 threads.
 __global__ void __launch_bounds__(kSmallBatchMaxThreads, 1)

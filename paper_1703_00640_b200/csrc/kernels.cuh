@@ -50,6 +50,8 @@ __global__ void k_small_product_2(const __grid_constant__ SmallArgs a);  // <= 3
 __global__ void k_small_product_big(const __grid_constant__ SmallArgs a);  // <= 768 threads (batched L <= 12288)
 // compile-time schedules for the full product at 2^16 bits (768 threads)
 __global__ void k_small_6144(const __grid_constant__ SmallArgs a);
+// compile-time schedules for the low / high products at 2^16 bits (384 threads)
+__global__ void k_small_5120(const __grid_constant__ SmallArgs a);
 
 // ---------------------------------------------------------------------------
 // Multi-pass pipeline.  The complex transform of length L = A * B * C runs as

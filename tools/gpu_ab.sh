@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-timeout 300 python tools/dbg_case.py 4748529 105078 > gpurun_out/dbg.log 2>&1
-timeout 1500 python tools/random_sizes.py 200 9 > gpurun_out/random_sizes.log 2>&1
-timeout 600 python tools/shape_sweep.py 120 > gpurun_out/shape_sweep.log 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q -k "config4 or batch or small" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python tools/batch_bench.py 4096 16 low > gpurun_out/batch.log 2>&1
+timeout 300 python tools/batch_bench.py 4096 16 high >> gpurun_out/batch.log 2>&1
