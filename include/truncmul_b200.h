@@ -199,11 +199,16 @@ enum {
                                         coefficients (default: it stores digits and the first
                                         column pass pre-maps, where a compiled shape allows) */,
   TMG_OPT_CARRY_KERNELS = 12         /* 1: single-pass look-back carry (k_carry_lb); 2: carry-ins by
-                                        a second kernel (k_carry_lanes + k_carry_patch); 0 (default):
-                                        one kernel while the carry blocks fit one wave, else two */,
+                                        a second kernel, per-limb lanes (k_carry_lanes +
+                                        k_carry_patch); 3: the same with the runs kernel
+                                        (k_carry_runs + k_carry_patch) at every size; 0 (default):
+                                        one kernel while the carry blocks fit one wave, else
+                                        k_carry_runs + k_carry_patch */,
   TMG_OPT_MAX_ROW = 13,               /* longest row length C of multi-pass plans (0: 4096) */
-  TMG_OPT_SPLIT_AGGREGATES = 14      /* the split's block carry-ins always from k_zstat's aggregates
+  TMG_OPT_SPLIT_AGGREGATES = 14,     /* the split's block carry-ins always from k_zstat's aggregates
                                         (default: a look-back inside k_zgen) */
+  TMG_OPT_GENERIC_RUNS = 15          /* k_carry_runs with the chunk width as a run-time value
+                                        (default: a compiled width where one exists) */
 };
 int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value);
 

@@ -71,6 +71,7 @@ TMG_OPT_PREMAP_IN_SPLIT = 11
 TMG_OPT_CARRY_KERNELS = 12
 TMG_OPT_MAX_ROW = 13
 TMG_OPT_SPLIT_AGGREGATES = 14
+TMG_OPT_GENERIC_RUNS = 15
 
 
 def header_functions() -> list[str]:

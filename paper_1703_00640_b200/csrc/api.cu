@@ -106,6 +106,7 @@ struct Options {
   bool generic_row = false;     // TMG_OPT_GENERIC_ROW_PASS
   bool lookback_carry = false;  // TMG_OPT_LOOKBACK_CARRY
   int carry_kernels = 0;        // TMG_OPT_CARRY_KERNELS (0 by size)
+  bool generic_runs = false;    // TMG_OPT_GENERIC_RUNS
   bool zstat_split = false;     // TMG_OPT_SPLIT_AGGREGATES
   long patch_scan_max = long(kPatchScanMaxBlocks);  // TMG_OPT_PATCH_SCAN_MAX
   bool no_pdl = false;          // TMG_OPT_NO_PDL
@@ -561,6 +562,8 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.shift_s = pl.shift_s;
       a.mc = pl.mc;
       a.aux = w.aux.as<double>();
+      a.wlen = pl.L;
+      a.blk_limbs = 0;
       const int64_t LB = kCarryThreads * kCarryPerThread;
       const unsigned blocks = unsigned((pl.ML + LB - 1) / LB);
       a.scan = w.scan_c.next(blocks);
@@ -581,7 +584,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       // limb per thread: twice the blocks, each with half the latency
       // (single-pass kernel, mid-size products)
       // (the single-pass kernel only: its one-wave rule must still hold)
-      if (cx.opt.carry_kernels != 2 && carry_lb_kernel(lam, 1) &&
+      if (cx.opt.carry_kernels != 2 && cx.opt.carry_kernels != 3 && carry_lb_kernel(lam, 1) &&
           (pl.ML + int64_t(kC2Threads) * pt - 1) / (int64_t(kC2Threads) * pt) < int64_t(2 * cx.num_sms) &&
           (pl.ML + kC2Threads - 1) / kC2Threads <= int64_t(4 * cx.num_sms))
         pt = 1;
@@ -625,19 +628,45 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
           check_launch(cx, "k_carry_lb");
           kernels += 1;
         } else {
-        CarryLanesFn lanes = carry_lanes_kernel(lam, pt);
-        if (!lanes) throw Error(TMG_ERR_UNSUPPORTED, "carry lanes kernel: no instantiation for this block shape");
-        set_smem(lanes, smem2);
-        {
-          KTimer kt(cx, "k_carry_lanes", double(pl.K) * 8.0 + double(hb ? pl.ML : pl.out_limbs) * 8.0, int(p.mode),
-                    st);
-          launch(cx, lanes, dim3(blocks2), dim3(kC2Threads), smem2, st, a, "lanes");
+        // runs kernel: one thread per run of 64 coefficients (b limbs); the
+        // lanes kernel where it has no instantiation
+        CarryLanesFn runs = (cx.opt.carry_kernels == 2 || p.b < 8 || pl.L >= (int64_t(1) << 31))
+                                ? nullptr
+                                : carry_runs_kernel(int(pl.mc.mode), lam, int(p.b), !cx.opt.generic_runs);
+        unsigned blocksp = blocks2;
+        if (runs) {
+          const int64_t rl = int64_t(kRunThreads) * p.b;
+          blocksp = unsigned((pl.ML + rl - 1) / rl);
+          a.blk_limbs = rl;
+          a.wlen = pl.L;
+          a.lanes_cins = long(blocksp) > cx.opt.patch_scan_max ? 1 : 0;
+          w.aggs.ensure(size_t(blocksp) * 8 + 16);
+          a.aggs = w.aggs.as<uint32_t>();
+          a.cins = reinterpret_cast<int*>(a.aggs + blocksp);
+          const size_t smem3 = carry_runs_smem(int(pl.mc.mode), lam);
+          set_smem(runs, smem3);
+          {
+            KTimer kt(cx, "k_carry_runs", double(pl.K) * 8.0 + double(hb ? pl.ML : pl.out_limbs) * 8.0, int(p.mode),
+                      st);
+            launch(cx, runs, dim3(blocksp), dim3(kRunThreads), smem3, st, a, "runs");
+          }
+          check_launch(cx, "k_carry_runs");
+        } else {
+          CarryLanesFn lanes = carry_lanes_kernel(lam, pt);
+          if (!lanes) throw Error(TMG_ERR_UNSUPPORTED, "carry lanes kernel: no instantiation for this block shape");
+          set_smem(lanes, smem2);
+          {
+            KTimer kt(cx, "k_carry_lanes", double(pl.K) * 8.0 + double(hb ? pl.ML : pl.out_limbs) * 8.0, int(p.mode),
+                      st);
+            launch(cx, lanes, dim3(blocks2), dim3(kC2Threads), smem2, st, a, "lanes");
+          }
+          check_launch(cx, "k_carry_lanes");
         }
-        check_launch(cx, "k_carry_lanes");
         {
-          // the lanes kernel wrote the limbs; one warp per block adds its carry-in
+          // the limbs are written for a zero carry into each block; one warp
+          // per block adds its carry-in
           KTimer kt(cx, "k_carry_patch", 0.0, int(p.mode), st);
-          launch(cx, carry_patch_kernel(pt), dim3((blocks2 + kC2Threads / 32 - 1) / (kC2Threads / 32)), dim3(kC2Threads),
+          launch(cx, carry_patch_kernel(pt), dim3((blocksp + kC2Threads / 32 - 1) / (kC2Threads / 32)), dim3(kC2Threads),
                  0, st, a, "patch");
           check_launch(cx, "k_carry_patch");
         }
@@ -1280,12 +1309,13 @@ int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value) {
       case TMG_OPT_GENERIC_SMALL: o.generic_small = on; break;
       case TMG_OPT_PREMAP_IN_SPLIT: o.plan.premap_in_zgen = on; break;
       case TMG_OPT_SPLIT_AGGREGATES: o.zstat_split = on; break;
+      case TMG_OPT_GENERIC_RUNS: o.generic_runs = on; break;
       case TMG_OPT_MAX_ROW:
         if (value < 0 || value > 4096) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "row length cap in [0, 4096]");
         o.plan.max_row = uint32_t(value);
         break;
       case TMG_OPT_CARRY_KERNELS:
-        if (value < 0 || value > 2) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "carry kernels: 0, 1 or 2");
+        if (value < 0 || value > 3) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "carry kernels: 0 to 3");
         o.carry_kernels = int(value);
         break;
       default: throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "unknown context option");

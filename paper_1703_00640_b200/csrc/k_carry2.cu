@@ -662,7 +662,7 @@ template <int kPT>
 __global__ void __launch_bounds__(kC2Threads) k_carry_patch(CarryArgs a) {
   pdl_trigger();
   pdl_wait();
-  constexpr int64_t kLimbs = int64_t(kT) * kPT;
+  const int64_t kLimbs = a.blk_limbs ? a.blk_limbs : int64_t(kT) * kPT;
   const int64_t nblk = (a.ML + kLimbs - 1) / kLimbs;
   const int64_t blk = (int64_t(blockIdx.x) * kT + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;

@@ -261,6 +261,9 @@ struct CarryArgs {
   uint32_t* hstop;  // high: first limb of t >> s that is not all ones (atomicMin; ~0 before)
   int32_t lanes_cins; // 1: the last k_carry_lanes block writes cins; 0: k_carry_patch scans aggs
   const uint32_t* gen;  // k_carry_lb: look-back generation (advanced by this product's k_zstat)
+  // k_carry_runs (k_carry3.cu)
+  int64_t wlen;       // doubles of w that may be read (L)
+  int64_t blk_limbs;  // limbs per carry block for k_carry_patch (0: 256 x PT)
 };
 constexpr int kCarryThreads = 256;
 constexpr int kCarryPerThread = 2;
@@ -275,6 +278,11 @@ CarryLanesFn carry_patch_kernel(int pt);
 // [0] ticket, [1] done, [2] generation
 CarryLanesFn carry_lb_kernel(int lam, int pt);
 size_t carry2_smem(int b, int lam, int pt, bool hbuf);
+// runs kernel (k_carry3.cu): one thread per run of 64 coefficients, b limbs;
+// nullptr without an instantiation for (mode, lambda)
+constexpr int kRunThreads = 128;
+CarryLanesFn carry_runs_kernel(int mode, int lam, int b, bool compiled_b);
+size_t carry_runs_smem(int mode, int lam);
 
 struct HighRoundArgs {
   const uint64_t* tbuf;
