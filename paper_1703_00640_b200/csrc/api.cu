@@ -564,6 +564,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.aux = w.aux.as<double>();
       a.wlen = pl.L;
       a.blk_limbs = 0;
+      a.runs_lb = 0;
       const int64_t LB = kCarryThreads * kCarryPerThread;
       const unsigned blocks = unsigned((pl.ML + LB - 1) / LB);
       a.scan = w.scan_c.next(blocks);
@@ -584,7 +585,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       // limb per thread: twice the blocks, each with half the latency
       // (single-pass kernel, mid-size products)
       // (the single-pass kernel only: its one-wave rule must still hold)
-      if (cx.opt.carry_kernels != 2 && cx.opt.carry_kernels != 3 && carry_lb_kernel(lam, 1) &&
+      if (cx.opt.carry_kernels < 2 && carry_lb_kernel(lam, 1) &&
           (pl.ML + int64_t(kC2Threads) * pt - 1) / (int64_t(kC2Threads) * pt) < int64_t(2 * cx.num_sms) &&
           (pl.ML + kC2Threads - 1) / kC2Threads <= int64_t(4 * cx.num_sms))
         pt = 1;
@@ -634,6 +635,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
                                 ? nullptr
                                 : carry_runs_kernel(int(pl.mc.mode), lam, int(p.b), !cx.opt.generic_runs);
         unsigned blocksp = blocks2;
+        bool runs_lb = false;
         if (runs) {
           const int64_t rl = int64_t(kRunThreads) * p.b;
           blocksp = unsigned((pl.ML + rl - 1) / rl);
@@ -645,6 +647,14 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
           a.cins = reinterpret_cast<int*>(a.aggs + blocksp);
           const size_t smem3 = carry_runs_smem(int(pl.mc.mode), lam);
           set_smem(runs, smem3);
+          // one kernel: the block carry-ins by a decoupled look-back over the
+          // published aggregates (TMG_OPT_CARRY_KERNELS 3 keeps k_carry_patch)
+          runs_lb = cx.opt.carry_kernels != 3;
+          if (runs_lb) {
+            a.runs_lb = 1;
+            a.scan = w.scan_c.next(blocksp);
+            a.gen = w.gen.as<uint32_t>();
+          }
           {
             KTimer kt(cx, "k_carry_runs", double(pl.K) * 8.0 + double(hb ? pl.ML : pl.out_limbs) * 8.0, int(p.mode),
                       st);
@@ -662,7 +672,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
           }
           check_launch(cx, "k_carry_lanes");
         }
-        {
+        if (!runs_lb) {
           // the limbs are written for a zero carry into each block; one warp
           // per block adds its carry-in
           KTimer kt(cx, "k_carry_patch", 0.0, int(p.mode), st);
@@ -670,7 +680,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
                  0, st, a, "patch");
           check_launch(cx, "k_carry_patch");
         }
-        kernels += 2;
+        kernels += runs_lb ? 1 : 2;
         }
       } else {
         set_smem(k_carry, pl.smem_carry);
@@ -1315,7 +1325,7 @@ int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value) {
         o.plan.max_row = uint32_t(value);
         break;
       case TMG_OPT_CARRY_KERNELS:
-        if (value < 0 || value > 3) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "carry kernels: 0 to 3");
+        if (value < 0 || value > 4) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "carry kernels: 0 to 4");
         o.carry_kernels = int(value);
         break;
       default: throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "unknown context option");

@@ -45,6 +45,8 @@ namespace {
 
 constexpr int kRT = kRunThreads;  // threads (runs) per block
 constexpr int kRun = 64;          // coefficients per run
+constexpr int kHaloBelow = 16;    // window of the limb below the block: 8 coefficients, their post-map inputs
+constexpr int kHaloWin = kHaloBelow + 2;
 
 // Slot geometry (doubles): [k0 - hlo, k0 + 64 + hhi) plus padding so that
 // slot / 2 is odd.
@@ -200,6 +202,25 @@ struct HighLimbs3 {
   }
 };
 
+// Flat post-map output j from a window: W[c - r] = w_{j - r}, jd = j as an
+// exact double (the gather form of k_carry_lanes: same operations, same order).
+template <int LAM>
+__device__ __forceinline__ double pfd_w(double jd, const double* W, int c, double st, const double* cr) {
+  double acc = 0.0;
+#pragma unroll
+  for (int r = LAM - 1; r >= 1; --r) {
+    const double id = jd - double(r);
+    double p = id, f = id + st;
+#pragma unroll
+    for (int t = 1; t < r; ++t) {
+      p *= f;
+      f += st;
+    }
+    acc = fma(W[c - r], p * cr[r], acc);
+  }
+  return acc + W[c];
+}
+
 // The walk's accumulator state of one run.
 struct RunAcc {
   unsigned long long lo = 0;
@@ -243,8 +264,10 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
   __shared__ uint32_t sw[32];
   __shared__ long long s_lanehi[kRT / 32];
   __shared__ long long s_halo[8];
+  __shared__ __align__(16) double s_hw[kHaloWin];  // w_{kblk - 16} .. w_{kblk + 1} (interior blocks)
   __shared__ double s_psi;
   __shared__ uint32_t s_flags, s_first, s_hmin, s_sticky, s_last;
+  __shared__ int s_cin;
   __shared__ double2 s_red[kRT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const MapConsts& mc = a.mc;
@@ -260,6 +283,11 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
   double* slots = reinterpret_cast<double*>(smem_raw);
   double* slot = slots + size_t(tid) * G::slot;
   constexpr bool hmode = MODE == kModeHigh, lowm = MODE == kModeLow, fullm = MODE == kModeFull;
+  // single pass (a.runs_lb): the block's carry-in by a decoupled look-back;
+  // the look-back words carry the product's generation (advanced by the row pass)
+  const bool lb = a.runs_lb != 0;
+  uint32_t gen = 0;
+  if (lb && warp == 0) gen = *a.gen;
 
   // interior runs: every post-map input inside [0, N) away from the wrap
   // outputs and the fold region, all 64 coefficients below K
@@ -271,22 +299,6 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
     interior = k0 >= kRun && k0 + kRun + 1 <= N && k0 + kRun <= K && (lowm || k0 - 1 >= hs0);
   }
   const bool live = m0 < a.ML && k0 < K;  // the run has limbs to write and coefficients
-  // the run's window by one bulk copy per thread on the warp's mbarrier
-  {
-    uint32_t bytes = 0;
-    if (interior && live) {
-      int64_t hi_idx = k0 + kRun + G::hhi;
-      if (hi_idx > a.wlen) hi_idx = a.wlen;
-      bytes = uint32_t(hi_idx - (k0 - G::hlo)) * 8u;
-    }
-    const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
-    if (lane == 0) {
-      mbar_init(&s_mbar[warp], 1);
-      mbar_expect_tx(&s_mbar[warp], total);
-    }
-    __syncwarp();
-    if (bytes) bulk_g2s(slot, a.w + (k0 - G::hlo), bytes, &s_mbar[warp]);
-  }
   // Blocks whose runs are all interior (block-uniform, from the block's
   // range alone) go straight to the walk: nothing to evaluate generically,
   // no psi, no barrier before the walk.
@@ -298,6 +310,25 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
     const int64_t hs0 = int64_t(mc.nfold) + LAM - 2;
     blk_interior = kblk >= kRun && kblk_end + 1 <= N && kblk_end <= K && ms + bl <= a.ML &&
                    (lowm || kblk - 1 >= hs0) && kblk - 8 >= mc.nfold;
+  }
+  // the run's window by one bulk copy per thread on the warp's mbarrier
+  {
+    uint32_t bytes = 0;
+    if (interior && live) {
+      int64_t hi_idx = k0 + kRun + G::hhi;
+      if (hi_idx > a.wlen) hi_idx = a.wlen;
+      bytes = uint32_t(hi_idx - (k0 - G::hlo)) * 8u;
+    }
+    // (interior blocks: the first warp also takes the window of the limb below the block)
+    const bool halo_win = blk_interior && ms > 0 && warp == 0;
+    const uint32_t total = __reduce_add_sync(0xffffffffu, bytes) + (halo_win ? uint32_t(kHaloWin) * 8u : 0u);
+    if (lane == 0) {
+      mbar_init(&s_mbar[warp], 1);
+      mbar_expect_tx(&s_mbar[warp], total);
+    }
+    __syncwarp();
+    if (bytes) bulk_g2s(slot, a.w + (k0 - G::hlo), bytes, &s_mbar[warp]);
+    if (halo_win && lane == 0) bulk_g2s(s_hw, a.w + (kblk - kHaloBelow), uint32_t(kHaloWin) * 8u, &s_mbar[0]);
   }
   if (tid == 0) {
     s_flags = 0;
@@ -388,22 +419,7 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
         double cr[LAM];
 #pragma unroll
         for (int r = 0; r < LAM; ++r) cr[r] = mc.cpost[r];
-        // flat post-map output j from the window: W[c - r] = w_{j - r}
-        auto pfd = [&](double jd, const double* W, int c) -> double {
-          double acc = 0.0;
-#pragma unroll
-          for (int r = LAM - 1; r >= 1; --r) {
-            const double id = jd - double(r);
-            double p = id, f = id + st;
-#pragma unroll
-            for (int t = 1; t < r; ++t) {
-              p *= f;
-              f += st;
-            }
-            acc = fma(W[c - r], p * cr[r], acc);
-          }
-          return acc + W[c];
-        };
+        auto pfd = [&](double jd, const double* W, int c) -> double { return pfd_w<LAM>(jd, W, c, st, cr); };
         // jd: the first post-map output index of the run as an exact double
         double jd = double(k0 + (lowm ? 1 : 0));
         double hprev = 0.0;  // high: the previous flat output
@@ -464,8 +480,28 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
     long long e = 0;
     if (k < kblk && k < K) {
       RoundAcc rh;  // counted by the run that owns k
-      uint32_t fh = 0;
-      e = coef_generic<MODE, LAM>(a, k, s_psi, rh, fh);
+      if (blk_interior) {
+        // from the staged window: s_hw[x] = w_{kblk - 16 + x}
+        const int c = int(k - (kblk - kHaloBelow));
+        if constexpr (fullm) {
+          e = rh.round(s_hw[c]);
+        } else {
+          const double st = lowm ? double(N) : -double(N);
+          double cr[LAM];
+#pragma unroll
+          for (int r = 0; r < LAM; ++r) cr[r] = mc.cpost[r];
+          if constexpr (lowm) {
+            e = rh.round(pfd_w<LAM>(double(k + 1), s_hw, c + 1, st, cr) * mc.scale_out);
+          } else {
+            const double h1 = pfd_w<LAM>(double(k), s_hw, c, st, cr);
+            const double h0 = pfd_w<LAM>(double(k - 1), s_hw, c - 1, st, cr);
+            e = rh.round((h1 - h0 * mc.step) * mc.scale_out);
+          }
+        }
+      } else {
+        uint32_t fh = 0;
+        e = coef_generic<MODE, LAM>(a, k, s_psi, rh, fh);
+      }
     }
     s_halo[tid] = e;
   }
@@ -551,16 +587,37 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
   }
   uint32_t agg;
   const uint32_t ex = block_scan_tf(f, sw, &agg);
-  if (tid == 0) a.aggs[blk] = agg;
-  // fix the run's limbs for a zero carry into the block
+  // publish the aggregate (single pass) or leave it to k_carry_patch
+  if (tid == 0) {
+    if (!lb) {
+      a.aggs[blk] = agg;
+    } else if (blk != 0) {
+      *(volatile unsigned long long*)(a.scan.state + blk) =
+          (static_cast<unsigned long long>(gen) << 32) | (1ull << 30) | agg;
+    }
+  }
+  // fix the run's limbs for a zero carry into the block; the carry-in is
+  // added afterwards (single pass: below, once the look-back has it; two
+  // kernels: by k_carry_patch)
   const bool haslimbs = m0 < a.ML;
-  const uint32_t nlw = haslimbs ? uint32_t(min(int64_t(b), a.ML - m0)) : 0u;
+  const uint32_t nlw = haslimbs ? uint32_t(min(int64_t(b), a.ML - m0)) : 0u;  // limbs below ML
   (void)nl;
+  const int cin0 = tf_apply(ex, 0);
+  const bool top = haslimbs && a.ML - 1 < m0 + int64_t(b);  // owns the top limb
+  // what flows above the top limb for the carry cin into the run (the sign
+  // of the recombined value)
+  auto top_carry = [&](int cin) -> long long {
+    const uint32_t lt = uint32_t(a.ML - 1 - m0);
+    long long ct = (lt == b - 1u) ? lane_hi + tf_apply(f, cin) : __double_as_longlong(slot[lt + 1]);
+    if (ct < -1 || ct > 1) {
+      flags |= kFlagCarryRange;
+      ct = 0;
+    }
+    return ct;
+  };
   if (haslimbs) {
-    const int cin = tf_apply(ex, 0);
-    slot[0] = __longlong_as_double((long long)(x0 + (unsigned long long)(long long)cin));
-    int c = tf_apply(tf0, cin);
-    const bool top = a.ML - 1 >= m0 && a.ML - 1 < m0 + int64_t(b);  // owns the top limb
+    slot[0] = __longlong_as_double((long long)(x0 + (unsigned long long)(long long)cin0));
+    int c = tf_apply(tf0, cin0);
     if (c != 0) {
       for (uint32_t i = 1; i < b; ++i) {
         const unsigned long long l = (unsigned long long)__double_as_longlong(slot[i]);
@@ -571,89 +628,119 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
         }
       }
     }
-    if (top && !lowm) {
-      // what flows above the top limb (the sign of the recombined value)
-      const uint32_t lt = uint32_t(a.ML - 1 - m0);
-      long long ct;
-      if (lt == b - 1u) {
-        ct = lane_hi + tf_apply(f, cin);
-      } else {
-        ct = __double_as_longlong(slot[lt + 1]);
-      }
-      if (ct < -1 || ct > 1) {
-        flags |= kFlagCarryRange;
-        ct = 0;
-      }
+    if (top && !lowm && !lb) {
       uint64_t* tail = hmode ? a.tbuf : reinterpret_cast<uint64_t*>(a.sbuf);
-      tail[a.ML] = uint64_t(ct);
+      tail[a.ML] = uint64_t(top_carry(cin0));
     }
   }
-  (void)nlw;
   flags |= ra.all_flags();
   {
     const double e = warp_max_nonneg(ra.max_err), m = warp_max_nonneg(ra.max_abs);
     if (lane == 0) s_red[warp] = make_double2(e, m);
   }
-  if (flags) atomicOr(&s_flags, flags);
   if (tid == 0) {
     s_last = 0;
-    if (a.lanes_cins) {
+    if (a.lanes_cins && !lb) {
       __threadfence();
       s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
     }
   }
   __syncthreads();
   // ---- coalesced stores of the block's limbs ----
-  {
-    const int64_t OL = a.out_limbs;
-    uint64_t* tail = hmode ? a.tbuf : reinterpret_cast<uint64_t*>(a.sbuf);
-    const uint32_t nlb = uint32_t(me - ms);
-    uint32_t first = 0xffffffffu;
-    for (uint32_t ml = tid; ml < nlb; ml += kRT) {
-      const uint32_t g = fdiv(ml, a.fb);
-      const uint64_t x = uint64_t(__double_as_longlong(slots[size_t(g) * G::slot + (ml - g * b)]));
-      const int64_t m = ms + ml;
-      if constexpr (hmode) {
-        tail[m] = x;
-        // a carry-in changes no limb above the first one that is neither 0
-        // nor all ones
-        if (x + 1 > 1 && first == 0xffffffffu) first = ml;
-      } else if (m < OL) {
-        a.out[m] = (lowm && m == OL - 1 && (a.n & 63)) ? (x & ((1ull << (a.n & 63)) - 1)) : x;
-      } else {
-        tail[m] = x;
+  const int64_t OL = a.out_limbs;
+  uint64_t* tail = hmode ? a.tbuf : reinterpret_cast<uint64_t*>(a.sbuf);
+  const uint32_t nlb = uint32_t(me - ms);
+  auto limb_at = [&](uint32_t ml) -> uint64_t {
+    const uint32_t g = B ? ml / uint32_t(B ? B : 1) : fdiv(ml, a.fb);
+    return uint64_t(__double_as_longlong(slots[size_t(g) * G::slot + (ml - g * b)]));
+  };
+  auto store_limb = [&](int64_t m, uint64_t x) {
+    if constexpr (hmode) {
+      tail[m] = x;
+    } else if (m < OL) {
+      a.out[m] = (lowm && m == OL - 1 && (a.n & 63)) ? (x & ((1ull << (a.n & 63)) - 1)) : x;
+    } else if (!lb) {
+      tail[m] = x;
+    }
+  };
+  uint32_t first = 0xffffffffu;
+  for (uint32_t ml = tid; ml < nlb; ml += kRT) {
+    const uint64_t x = limb_at(ml);
+    store_limb(ms + ml, x);
+    // two kernels, high: a carry-in changes no limb above the first one that
+    // is neither 0 nor all ones
+    if (hmode && x + 1 > 1 && first == 0xffffffffu) first = ml;
+  }
+  if (lb) {
+    // ---- single pass: the block's carry-in, taken after the stores (the
+    // blocks before have had that time to publish) ----
+    if (warp == 0) {
+      const int c = lookback_warp(a.scan.state, uint32_t(blk), agg, gen, 0, true);
+      if (lane == 0) s_cin = c;
+    }
+    __syncthreads();
+    const int cin_blk = s_cin;
+    const int cin = tf_apply(ex, cin_blk);
+    if (haslimbs && cin != cin0) {
+      // add the difference to the run's limbs up to the first that does not
+      // wrap, and store those again (the next run's carry-in already counts
+      // a carry through this one)
+      int dl = cin - cin0;
+      for (uint32_t i = 0; i < nlw && dl != 0; ++i) {
+        const unsigned long long l = (unsigned long long)__double_as_longlong(slot[i]);
+        const unsigned long long x = l + (unsigned long long)(long long)dl;
+        slot[i] = __longlong_as_double((long long)x);
+        store_limb(m0 + i, x);
+        dl = dl > 0 ? (x < l ? 1 : 0) : (x > l ? -1 : 0);
       }
     }
-    if constexpr (hmode) {
-      first = __reduce_min_sync(0xffffffffu, first);
-      if (lane == 0 && first != 0xffffffffu) atomicMin(&s_first, first);
+    if (top && !lowm) {
+      // (reads the limb above the top one: after this thread's own patch)
+      if (top_carry(cin) < 0) flags |= fullm ? uint32_t(kFlagNegative) : uint32_t(kFlagHighRange);
+    }
+    // the checks on final limbs: the full product's range, the high
+    // product's nominations and sticky bits (below)
+    if (fullm && me > OL - 1) {
       __syncthreads();
-      // nominations and sticky bits of the limbs no carry-in can change (all
-      // of block 0's, which has none); k_carry_patch sees the others
-      const HighLimbs3 hl(a);
-      const uint32_t lfix = blk == 0 ? 0u : (s_first == 0xffffffffu ? 0xffffffffu : s_first + 1u);
-      uint32_t hmin = 0xffffffffu, sticky = 0;
+      const int hb = int((2 * a.n) & 63);
       for (uint32_t ml = tid; ml < nlb; ml += kRT) {
-        if (ml >= lfix) {
-          const uint32_t g = fdiv(ml, a.fb);
-          const uint64_t x = uint64_t(__double_as_longlong(slots[size_t(g) * G::slot + (ml - g * b)]));
-          hl.see(ms + ml, x, hmin, sticky);
+        const int64_t m = ms + ml;
+        if (m >= OL - 1) {
+          const uint64_t x = limb_at(ml);
+          if (m == OL - 1 ? (hb && (x >> hb)) : x != 0) flags |= kFlagFullOverflow;
         }
       }
-      // w0's top limb has zero fill above bit 64 - r: never all ones
-      if (hl.hr != 0 && blk == 0 && tid == 0 && hl.WL > 0) hmin = min(hmin, uint32_t(hl.WL - 1));
-      hmin = __reduce_min_sync(0xffffffffu, hmin);
-      sticky = __reduce_or_sync(0xffffffffu, sticky);
-      if (lane == 0) {
-        if (hmin != 0xffffffffu) atomicMin(&s_hmin, hmin);
-        if (sticky) s_sticky = 1;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        if (s_hmin != 0xffffffffu) atomicMin(a.hstop, s_hmin);
-        if (s_sticky) atomicOr(&a.status->high_sticky, 1u);
-      }
     }
+  }
+  if (flags) atomicOr(&s_flags, flags);
+  if constexpr (hmode) {
+    if (!lb) {
+      first = __reduce_min_sync(0xffffffffu, first);
+      if (lane == 0 && first != 0xffffffffu) atomicMin(&s_first, first);
+    }
+    __syncthreads();
+    // nominations and sticky bits: single pass, of every limb; two kernels,
+    // of the limbs no carry-in can change (all of block 0's, which has
+    // none), k_carry_patch sees the others
+    const HighLimbs3 hl(a);
+    const uint32_t lfix = (blk == 0 || lb) ? 0u : (s_first == 0xffffffffu ? 0xffffffffu : s_first + 1u);
+    uint32_t hmin = 0xffffffffu, sticky = 0;
+    for (uint32_t ml = tid; ml < nlb; ml += kRT) {
+      if (ml >= lfix) hl.see(ms + ml, limb_at(ml), hmin, sticky);
+    }
+    // w0's top limb has zero fill above bit 64 - r: never all ones
+    if (hl.hr != 0 && blk == 0 && tid == 0 && hl.WL > 0) hmin = min(hmin, uint32_t(hl.WL - 1));
+    hmin = __reduce_min_sync(0xffffffffu, hmin);
+    sticky = __reduce_or_sync(0xffffffffu, sticky);
+    if (lane == 0) {
+      if (hmin != 0xffffffffu) atomicMin(&s_hmin, hmin);
+      if (sticky) s_sticky = 1;
+    }
+  }
+  __syncthreads();
+  if (hmode && tid == 0) {
+    if (s_hmin != 0xffffffffu) atomicMin(a.hstop, s_hmin);
+    if (s_sticky) atomicOr(&a.status->high_sticky, 1u);
   }
   if (tid == 0) {
     double e = 0.0, m = 0.0;

@@ -264,6 +264,7 @@ struct CarryArgs {
   // k_carry_runs (k_carry3.cu)
   int64_t wlen;       // doubles of w that may be read (L)
   int64_t blk_limbs;  // limbs per carry block for k_carry_patch (0: 256 x PT)
+  int32_t runs_lb;    // 1: single pass, block carry-ins by look-back (a.scan, a.gen); 0: k_carry_patch follows
 };
 constexpr int kCarryThreads = 256;
 constexpr int kCarryPerThread = 2;

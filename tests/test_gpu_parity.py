@@ -896,14 +896,19 @@ def test_first_pass_premap_matches_split_premap(ctx, n):
     old.close()
 
 
-@pytest.mark.parametrize("kernels", [1, 2])
+@pytest.mark.parametrize("kernels", [1, 2, 3, 4, 5])
 @pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 448, 1 << 24])
 def test_carry_kernel_paths(n, kernels):
-    """TMG_OPT_CARRY_KERNELS: the single-pass look-back k_carry_lb (1) and
-    k_carry_lanes + k_carry_patch (2) at sizes where the default takes the
-    other; random and structured (long carry chains) operands, both paths
-    identical to the default and exact."""
-    c = _opt_ctx((tm._native.TMG_OPT_CARRY_KERNELS, kernels))
+    """TMG_OPT_CARRY_KERNELS: the single-pass look-back k_carry_lb (1),
+    k_carry_lanes + k_carry_patch (2), k_carry_runs + k_carry_patch (3) and
+    the single-pass k_carry_runs (4; 5 here: with TMG_OPT_GENERIC_RUNS, the
+    chunk width a run-time value) at sizes where the default takes another;
+    random and structured (long carry chains) operands, every path identical
+    to the default and exact."""
+    opts = [(tm._native.TMG_OPT_CARRY_KERNELS, min(kernels, 4))]
+    if kernels == 5:
+        opts.append((tm._native.TMG_OPT_GENERIC_RUNS, 1))
+    c = _opt_ctx(*opts)
     _config3_all_modes(c, n)
     nl = (n + 63) // 64
     M = (1 << n) - 1

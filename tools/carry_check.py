@@ -12,7 +12,8 @@ count = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 11)
 c3 = tm.Context(0); c3.set_option(_native.TMG_OPT_CARRY_KERNELS, 3)
 c2 = tm.Context(0); c2.set_option(_native.TMG_OPT_CARRY_KERNELS, 2)
-cg = tm.Context(0); cg.set_option(_native.TMG_OPT_CARRY_KERNELS, 3); cg.set_option(_native.TMG_OPT_GENERIC_RUNS, 1)
+cg = tm.Context(0); cg.set_option(_native.TMG_OPT_CARRY_KERNELS, 4); cg.set_option(_native.TMG_OPT_GENERIC_RUNS, 1)
+c4 = tm.Context(0); c4.set_option(_native.TMG_OPT_CARRY_KERNELS, 4)
 bad = 0
 def operands(n, kind):
     nl = (n + 63) // 64
@@ -38,14 +39,14 @@ for i in range(count):
         for pol in (tm.Policy.ACCURATE, tm.Policy.REFERENCE):
             p = tm.select_params(n, mode, policy=pol)
             res = []
-            for c in (c3, c2, cg):
+            for c in (c3, c2, cg, c4):
                 try:
                     r = tm.from_limbs(c.product_limbs(mode, u, v, p)); err = c.last_stats.max_round_err
                 except Exception as e:  # noqa: BLE001
                     r = None; err = str(e)[:60]
                 res.append((r, err))
-            (r3, e3), (r2, e2), (rg, eg) = res
-            if r3 != r2 or e3 != e2 or rg != r2 or eg != e2:
+            (r3, e3), (r2, e2), (rg, eg), (r4, e4) = res
+            if r3 != r2 or e3 != e2 or rg != r2 or eg != e2 or r4 != r2 or e4 != e2:
                 bad += 1; print("DIFF", n, kind, mode.name, pol.name, p, e3, e2, flush=True); continue
             if r3 is None: continue
             if mode == tm.Mode.FULL: ok = r3 == P
