@@ -252,6 +252,38 @@ __device__ __forceinline__ void run_step(RunAcc& s, long long e, uint32_t b, dou
   }
 }
 
+
+__host__ __device__ constexpr int gcd64(int b) { return b % 64 == 0 ? 64 : b % 32 == 0 ? 32 : b % 16 == 0 ? 16 : b % 8 == 0 ? 8 : b % 4 == 0 ? 4 : b % 2 == 0 ? 2 : 1; }
+
+// Drives a run's eight-coefficient bodies.  With a compiled chunk width the
+// shift pattern repeats every 64 / gcd(B, 64) coefficients (a whole number
+// of limbs): one period is unrolled (static shifts, emission steps and limb
+// offsets) and looped over, the last period apart (it holds the snapshot
+// of the last limb's lane).  With a run-time width: a loop over the bodies.
+template <int B, class Body>
+__device__ __forceinline__ void walk_periods(RunAcc& s, double* slot, Body& body) {
+  if constexpr (B == 0) {
+#pragma unroll 1
+    for (uint32_t i0 = 0; i0 < kRun - 8; i0 += 8) body(i0, slot, std::false_type{});
+    body(kRun - 8, slot, std::true_type{});
+  } else {
+    constexpr uint32_t g = uint32_t(gcd64(B)), PER = 64u / g, LPP = uint32_t(B) / g, NP = g;
+    static_assert(PER >= 8 && PER % 8 == 0, "period of whole bodies");
+#pragma unroll 1
+    for (uint32_t it = 0; it + 1 < NP; ++it) {
+      s.sh = 0;
+      s.li = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < PER; j += 8) body(it * PER + j, slot + it * LPP, std::false_type{});
+    }
+    s.sh = 0;
+    s.li = 0;
+#pragma unroll
+    for (uint32_t j = 0; j + 8 < PER; j += 8) body((NP - 1) * PER + j, slot + (NP - 1) * LPP, std::false_type{});
+    body(kRun - 8, slot + (NP - 1) * LPP, std::true_type{});
+  }
+}
+
 // B: the chunk width as a compile-time constant (the walk unrolls fully and
 // every shift, emission step and slot offset is static), or 0 for any b.
 template <int MODE, int LAM, int B>
@@ -384,7 +416,7 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
       mbar_wait(&s_mbar[warp], 0);
       const double2* s2 = reinterpret_cast<const double2*>(slot);
       if constexpr (fullm) {
-        auto body = [&](uint32_t i0, auto lastc) {
+        auto body = [&](uint32_t i0, double* limbs, auto lastc) {
           constexpr bool LASTB = decltype(lastc)::value;
           double x[8];
 #pragma unroll
@@ -396,16 +428,9 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
           long long ev[8];
           round8(ra, x, ev);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) run_step<LASTB>(s, ev[q], b, slot, i0 + q, ilast);
+          for (int q = 0; q < 8; ++q) run_step<LASTB>(s, ev[q], b, limbs, i0 + q, ilast);
         };
-        if constexpr (B != 0) {
-#pragma unroll
-          for (uint32_t i0 = 0; i0 < kRun - 8; i0 += 8) body(i0, std::false_type{});
-        } else {
-#pragma unroll 1
-          for (uint32_t i0 = 0; i0 < kRun - 8; i0 += 8) body(i0, std::false_type{});
-        }
-        body(kRun - 8, std::true_type{});
+        walk_periods<B>(s, slot, body);
       } else {
         // slot position of w_j for the body's first output: j0 - (LAM - 1),
         // j0 = k0 + i0 + (low: 1), minus the slot origin k0 - hlo
@@ -423,7 +448,11 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
         // jd: the first post-map output index of the run as an exact double
         double jd = double(k0 + (lowm ? 1 : 0));
         double hprev = 0.0;  // high: the previous flat output
-        auto body = [&](uint32_t i0, auto lastc) {
+        if constexpr (hmode) {
+          // flat output k0 - 1 from the slot's head: w_{k0 - 1 - r} at slot[hlo - 1 - r]
+          hprev = pfd(jd - 1.0, slot, G::hlo - 1);
+        }
+        auto body = [&](uint32_t i0, double* limbs, auto lastc) {
           constexpr bool LASTB = decltype(lastc)::value;
           double W[2 * nv2];
 #pragma unroll
@@ -435,9 +464,6 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
           // W[pe + x] = w_{j0 - (LAM - 1) - (high: 1) + x}
           constexpr int c0 = pe + (LAM - 1) + (hmode ? 1 : 0);  // W index of w_{j0}
           static_assert((off - pe) + (kRun - 8) + 2 * nv2 <= G::slot, "window beyond the slot");
-          if constexpr (hmode) {
-            if (i0 == 0) hprev = pfd(jd - 1.0, W, c0 - 1);
-          }
           double x[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -453,16 +479,9 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
           long long ev[8];
           round8(ra, x, ev);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) run_step<LASTB>(s, ev[q], b, slot, i0 + q, ilast);
+          for (int q = 0; q < 8; ++q) run_step<LASTB>(s, ev[q], b, limbs, i0 + q, ilast);
         };
-        if constexpr (B != 0) {
-#pragma unroll
-          for (uint32_t i0 = 0; i0 < kRun - 8; i0 += 8) body(i0, std::false_type{});
-        } else {
-#pragma unroll 1
-          for (uint32_t i0 = 0; i0 < kRun - 8; i0 += 8) body(i0, std::false_type{});
-        }
-        body(kRun - 8, std::true_type{});
+        walk_periods<B>(s, slot, body);
       }
     } else {
       // rounded coefficients from the slot (written above)
