@@ -207,8 +207,10 @@ enum {
   TMG_OPT_MAX_ROW = 13,               /* longest row length C of multi-pass plans (0: 4096) */
   TMG_OPT_SPLIT_AGGREGATES = 14,     /* the split's block carry-ins always from k_zstat's aggregates
                                         (default: a look-back inside k_zgen) */
-  TMG_OPT_GENERIC_RUNS = 15          /* k_carry_runs with the chunk width as a run-time value
+  TMG_OPT_GENERIC_RUNS = 15,         /* k_carry_runs with the chunk width as a run-time value
                                         (default: a compiled width where one exists) */
+  TMG_OPT_SPLIT_KERNEL = 16          /* 1: the block-scan split k_zgen at every size (default: the
+                                        split by runs, k_zsplit, for large products) */
 };
 int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value);
 

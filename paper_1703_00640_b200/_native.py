@@ -72,6 +72,7 @@ TMG_OPT_CARRY_KERNELS = 12
 TMG_OPT_MAX_ROW = 13
 TMG_OPT_SPLIT_AGGREGATES = 14
 TMG_OPT_GENERIC_RUNS = 15
+TMG_OPT_SPLIT_KERNEL = 16
 
 
 def header_functions() -> list[str]:

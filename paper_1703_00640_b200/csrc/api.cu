@@ -107,6 +107,7 @@ struct Options {
   bool lookback_carry = false;  // TMG_OPT_LOOKBACK_CARRY
   int carry_kernels = 0;        // TMG_OPT_CARRY_KERNELS (0 by size)
   bool generic_runs = false;    // TMG_OPT_GENERIC_RUNS
+  bool old_split = false;       // TMG_OPT_SPLIT_KERNEL
   bool zstat_split = false;     // TMG_OPT_SPLIT_AGGREGATES
   long patch_scan_max = long(kPatchScanMaxBlocks);  // TMG_OPT_PATCH_SCAN_MAX
   bool no_pdl = false;          // TMG_OPT_NO_PDL
@@ -348,6 +349,39 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.z = w.work_z.as<double2>();
       a.mc = pl.mc;
       a.zt = ztile(pl, L, cx.opt.z_natural);
+      a.status = status;
+      if (!w.gen.p) {
+        w.gen.ensure(64);
+        TMG_CUDA(cudaMemsetAsync(w.gen.p, 0, 64, st));
+      }
+      a.gen = w.gen.as<uint32_t>();
+      a.lbstate = nullptr;
+      a.aggs = nullptr;
+      a.early = 0;
+      // Split by runs (k_zsplit): every thread finds its carry-in from the
+      // window below its run, so there are no aggregates and no look-back.
+      // Digit form, balanced split, compiled chunk widths, runs inside one
+      // row of z's tiles; TMG_OPT_SPLIT_KERNEL 1 keeps k_zgen.
+      ZgenFn zs = nullptr;
+      {
+        const uint32_t ncols = a.zt.fdcols.d;
+        const int minlog = pl.zdig == 1 ? 2 : 1;
+        if (pl.f1d && pl.mc.balanced && !cx.opt.zstat_split && !cx.opt.old_split && pl.count < (int64_t(1) << 31) &&
+            (a.zt.natural || (ncols % 32 == 0 && int(a.zt.logc) >= minlog)) &&
+            pl.count >= int64_t(zsplit_chunks()) * cx.num_sms / 2)
+          zs = zsplit_kernel(int(p.b), pl.zdig);
+      }
+      if (zs) {
+        const unsigned blocks = unsigned((pl.count + zsplit_chunks() - 1) / zsplit_chunks());
+        const size_t zsm = zsplit_smem(int(p.b));
+        set_smem(zs, zsm);
+        {
+          KTimer kt(cx, "k_zsplit", double(2 * pl.nlimbs) * 8.0 + double(p.N) * (pl.zdig == 1 ? 4.0 : 8.0), int(p.mode), st);
+          launch(cx, zs, dim3(blocks), dim3(256), zsm, st, a, "zgen");
+        }
+        check_launch(cx, "k_zsplit");
+        ++kernels;
+      } else {
       // chunks per thread of the split: 16, or 4 / 1 when the blocks of 16
       // would not fill the GPU twice (mid-size products are latency-bound
       // per block)
@@ -356,22 +390,15 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       if (per == 4 && (pl.count + 4 * kZgenThreads - 1) / (4 * kZgenThreads) < 2 * cx.num_sms) per = 1;
       a.bchunks = per * kZgenThreads;
       const unsigned blocks = unsigned((pl.count + a.bchunks - 1) / a.bchunks);
-      a.status = status;
       w.zaggs.ensure(size_t(blocks) * 4 + 16);
       a.aggs = w.zaggs.as<uint32_t>();
       a.early = cx.zstat_early ? 1 : 0;
-      if (!w.gen.p) {
-        w.gen.ensure(64);
-        TMG_CUDA(cudaMemsetAsync(w.gen.p, 0, 64, st));
-      }
-      a.gen = w.gen.as<uint32_t>();
       // the split blocks take their carry-ins by a look-back inside k_zgen
       // (no k_zstat launch): a block's aggregate is published early (after
       // its windows), and its predecessor was dispatched before it, so the
       // waits are short (2^26 low 271.4 -> 267.2 us, 2^24 high 104.2 -> 101.1);
       // TMG_OPT_SPLIT_AGGREGATES composes k_zstat's aggregates instead
       const bool zlb = !cx.opt.zstat_split;
-      a.lbstate = nullptr;
       if (zlb) {
         if (w.zlb.bytes < size_t(blocks) * 8) {
           w.zlb.ensure(size_t(blocks) * 8);
@@ -398,6 +425,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       }
       check_launch(cx, "k_zgen");
       ++kernels;
+      }
     }
     double2* T = w.work_t.as<double2>();
     {
@@ -1320,6 +1348,7 @@ int tmg_context_set_option(tmg_context* ctx, int32_t option, int64_t value) {
       case TMG_OPT_PREMAP_IN_SPLIT: o.plan.premap_in_zgen = on; break;
       case TMG_OPT_SPLIT_AGGREGATES: o.zstat_split = on; break;
       case TMG_OPT_GENERIC_RUNS: o.generic_runs = on; break;
+      case TMG_OPT_SPLIT_KERNEL: o.old_split = on; break;
       case TMG_OPT_MAX_ROW:
         if (value < 0 || value > 4096) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "row length cap in [0, 4096]");
         o.plan.max_row = uint32_t(value);

@@ -128,6 +128,11 @@ ZgenFn zgen_digits_kernel(int b, int dig, int per = 16);
 // digit element type of a chunk width for the digit form
 inline int zdig_kind(int b) { return b <= 14 ? 1 : 2; }
 size_t zgen_smem(int b, int per = 16);
+// Split by runs (k_zsplit.cu): digit form, balanced split, compiled chunk
+// widths (nullptr otherwise); no carry aggregates, no look-back.
+ZgenFn zsplit_kernel(int b, int dig);
+size_t zsplit_smem(int b);
+int zsplit_chunks();
 
 // F1: forward column DFTs over A of the pre-mapped coefficients.
 struct F1Args {
