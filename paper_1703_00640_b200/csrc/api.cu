@@ -372,7 +372,16 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
           zs = zsplit_kernel(int(p.b), pl.zdig);
       }
       if (zs) {
-        const unsigned blocks = unsigned((pl.count + zsplit_chunks() - 1) / zsplit_chunks());
+        // blocks of 8 rows by 1024 columns of z's tiles (a warp's 16-byte
+        // digit pieces then fill whole lines), or of 8192 consecutive chunks
+        const uint32_t ncols = a.zt.fdcols.d;
+        const int64_t zch = zsplit_chunks();
+        a.zs_rb = (!a.zt.natural && ncols % uint32_t(zch / 8) == 0) ? 8 : 1;
+        unsigned blocks = unsigned((pl.count + zch - 1) / zch);
+        if (a.zs_rb == 8) {
+          const int64_t rows = (pl.count + ncols - 1) / ncols;
+          blocks = unsigned(((rows + 7) / 8) * (ncols / uint32_t(zch / 8)));
+        }
         const size_t zsm = zsplit_smem(int(p.b));
         set_smem(zs, zsm);
         {

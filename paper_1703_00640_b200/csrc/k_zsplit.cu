@@ -30,8 +30,10 @@ constexpr int kZsThreads = 256;
 constexpr int kZsRun = 32;
 constexpr int kZsChunks = kZsThreads * kZsRun;
 
-__host__ __device__ constexpr int zs_words(int b) { return (kZsChunks * b + b + 31) / 32 + 8; }
-__host__ __device__ constexpr int zs_words_alloc(int b) { return (zs_words(b) + 3) / 4 * 4; }
+// staged words per operand: the block's chunks and, for each of up to 8 row
+// segments, the window below, the sub-word offset and the look-ahead
+__host__ __device__ constexpr int zs_seg_words(int b) { return ((((kZsChunks / 8 + 1) * b + 31) / 32 + 12) + 3) / 4 * 4; }
+__host__ __device__ constexpr int zs_words_alloc(int b) { return 8 * zs_seg_words(b); }
 
 __device__ __forceinline__ uint32_t ld_word(const uint64_t* limbs, int64_t nlimbs, int64_t wi) {
   return (wi >= 0 && wi < 2 * nlimbs) ? __ldg(reinterpret_cast<const uint32_t*>(limbs) + wi) : 0u;
@@ -74,30 +76,74 @@ __global__ void __launch_bounds__(kZsThreads) k_zsplit(ZgenArgs a) {
   uint32_t* sv = su + zs_words_alloc(B);
   const int tid = threadIdx.x;
   const int64_t count = a.count, N = a.N;
-  const int64_t c0 = int64_t(blockIdx.x) * kZsChunks;
-  const int64_t c1 = min(count, c0 + int64_t(kZsChunks));
-  // staged bits: from the window below the block's first chunk
-  const int64_t bitlo = (c0 - 1) * B - a.lead;
-  const int64_t w4 = (bitlo >> 5) & ~int64_t(3);  // floor, 16-byte aligned
-  const uint32_t off0 = uint32_t(bitlo - (w4 << 5));  // < 128
-  const int nwd = int((off0 + uint32_t(c1 - c0 + 1) * uint32_t(B) + 31u) >> 5) + 2;
+  // Block geometry: rb rows of z's tiles by cb = 8192 / rb columns (a.zs_rb =
+  // 8 where the column count allows: the threads of a warp then own runs of
+  // adjacent rows, whose 16-byte digit pieces are adjacent in a tile), or
+  // 8192 consecutive chunks (rb = 1).  A row segment is cb consecutive chunks.
+  const uint32_t rb = uint32_t(a.zs_rb), cb = uint32_t(kZsChunks) / rb;
+  const uint32_t ncols = a.zt.fdcols.d;
+  const uint32_t nbands = rb > 1 ? ncols / cb : 1u;
+  const uint32_t band = blockIdx.x % nbands, rg = blockIdx.x / nbands;
+  auto seg_first = [&](uint32_t sgm) -> int64_t {
+    return rb > 1 ? int64_t(rg * rb + sgm) * ncols + int64_t(band) * cb : int64_t(blockIdx.x) * kZsChunks;
+  };
+  // staged bits of a segment: from the window below its first chunk
+  const uint32_t SW = uint32_t(zs_words_alloc(B)) / rb;  // words per segment (multiple of 4: rb divides 8)
+  auto seg_geom = [&](uint32_t sgm, int64_t& w4, uint32_t& off0, int& n4) {
+    const int64_t cs = seg_first(sgm);
+    const int64_t ce = min(count, cs + int64_t(cb));
+    const int64_t bitlo = (cs - 1) * B - a.lead;
+    w4 = (bitlo >> 5) & ~int64_t(3);  // floor, 16-byte aligned
+    off0 = uint32_t(bitlo - (w4 << 5));  // < 128
+    const int nwd = ce > cs ? int((off0 + uint32_t(ce - cs + 1) * uint32_t(B) + 31u) >> 5) + 2 : 0;
+    n4 = (nwd + 3) / 4;
+  };
   {
-    const int n4 = (nwd + 3) / 4;
-    const bool vec = w4 >= 0 && w4 + 4 * int64_t(n4) <= 2 * a.nlimbs &&
-                     ((reinterpret_cast<uintptr_t>(a.u) | reinterpret_cast<uintptr_t>(a.v)) & 15) == 0;
-    if (vec) {
-      const uint4* gu4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.u) + w4);
-      const uint4* gv4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.v) + w4);
-      uint4* su4 = reinterpret_cast<uint4*>(su);
-      uint4* sv4 = reinterpret_cast<uint4*>(sv);
-      for (int i = tid; i < n4; i += kZsThreads) {
-        su4[i] = __ldg(gu4 + i);
-        sv4[i] = __ldg(gv4 + i);
+    // every segment's slot is filled whole (a few words more than its
+    // windows need), all of a thread's loads in flight at once; 16-byte loads
+    // where the four words lie inside the operand, else word by word with
+    // zeros outside
+    const bool al = ((reinterpret_cast<uintptr_t>(a.u) | reinterpret_cast<uintptr_t>(a.v)) & 15) == 0;
+    constexpr uint32_t NS4 = uint32_t(zs_seg_words(B)) / 4;  // 16-byte pieces per segment slot (rb = 8)
+    constexpr uint32_t TOT4 = 8 * NS4;                         // per operand
+    constexpr int NIT = int((TOT4 + kZsThreads - 1) / kZsThreads);
+    int64_t w40;
+    uint32_t off0;
+    int n40;
+    seg_geom(0, w40, off0, n40);
+    // (segments start ncols B bits apart: their 16-byte aligned first words follow from their own bit offsets)
+    uint4 vu[NIT], vv[NIT];
+    bool vec[NIT];
+    int64_t wq[NIT];
+#pragma unroll
+    for (int k = 0; k < NIT; ++k) {
+      const uint32_t i = uint32_t(tid) + uint32_t(k) * kZsThreads;
+      const uint32_t sgm = rb == 1 ? 0u : i / NS4;
+      const uint32_t e = rb == 1 ? i : i - sgm * NS4;
+      int64_t w4s = w40;
+      if (sgm) {
+        const int64_t bitlo = (seg_first(sgm) - 1) * B - a.lead;
+        w4s = (bitlo >> 5) & ~int64_t(3);
       }
-    } else {
-      for (int i = tid; i < 4 * n4; i += kZsThreads) {
-        su[i] = ld_word(a.u, a.nlimbs, w4 + i);
-        sv[i] = ld_word(a.v, a.nlimbs, w4 + i);
+      wq[k] = w4s + 4 * int64_t(e);
+      vec[k] = i < TOT4 && al && wq[k] >= 0 && wq[k] + 4 <= 2 * a.nlimbs;
+      if (vec[k]) {
+        vu[k] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.u) + wq[k]));
+        vv[k] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.v) + wq[k]));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NIT; ++k) {
+      const uint32_t i = uint32_t(tid) + uint32_t(k) * kZsThreads;
+      if (i < TOT4) {
+        if (!vec[k]) {
+          vu[k] = make_uint4(ld_word(a.u, a.nlimbs, wq[k]), ld_word(a.u, a.nlimbs, wq[k] + 1),
+                             ld_word(a.u, a.nlimbs, wq[k] + 2), ld_word(a.u, a.nlimbs, wq[k] + 3));
+          vv[k] = make_uint4(ld_word(a.v, a.nlimbs, wq[k]), ld_word(a.v, a.nlimbs, wq[k] + 1),
+                             ld_word(a.v, a.nlimbs, wq[k] + 2), ld_word(a.v, a.nlimbs, wq[k] + 3));
+        }
+        reinterpret_cast<uint4*>(su)[i] = vu[k];
+        reinterpret_cast<uint4*>(sv)[i] = vv[k];
       }
     }
   }
@@ -107,12 +153,23 @@ __global__ void __launch_bounds__(kZsThreads) k_zsplit(ZgenArgs a) {
       atomicOr(&a.status->flags, uint32_t(kFlagInputRange));
   }
   __syncthreads();
-  const int64_t j0 = c0 + int64_t(tid) * kZsRun;
+  // consecutive threads: consecutive rows of the group, then the next run
+  const uint32_t lr = uint32_t(tid) % rb, rc = uint32_t(tid) / rb;
+  const int64_t j0 = seg_first(lr) + int64_t(rc) * kZsRun;
   if (j0 >= count) return;
+  su += lr * SW;
+  sv += lr * SW;
   constexpr uint32_t mask = (1u << B) - 1u, half = 1u << (B - 1);
   constexpr int32_t full = int32_t(1) << B;
   // the window below the run and the run's first window, in staged bits
-  const uint32_t relp = off0 + uint32_t(tid) * uint32_t(kZsRun * B);
+  uint32_t relp;
+  {
+    int64_t w4;
+    uint32_t off0;
+    int n4;
+    seg_geom(lr, w4, off0, n4);
+    relp = off0 + rc * uint32_t(kZsRun * B);
+  }
   const uint32_t rel0 = relp + uint32_t(B);
   int cu, cv;
   {
@@ -129,7 +186,7 @@ __global__ void __launch_bounds__(kZsThreads) k_zsplit(ZgenArgs a) {
   const ZTile& zt = a.zt;
   if (j0 + kZsRun <= N && j0 + kZsRun <= count - 1) {
     // every chunk of the run is a balanced, stored chunk
-    const uint32_t wi0 = rel0 >> 5, dl = rel0 & 31u;  // dl: block-uniform
+    const uint32_t wi0 = rel0 >> 5, dl = rel0 & 31u;
     uint32_t Wu[B], Wv[B];
     {
       uint32_t lu = su[wi0], lv = sv[wi0];

@@ -114,6 +114,7 @@ struct ZgenArgs {
   // k_zgen without k_zstat: each block's carry-in by a decoupled look-back
   // over these words (the default); null: composed from k_zstat's aggs
   unsigned long long* lbstate;
+  int32_t zs_rb;   // k_zsplit: rows of z's tiles per block (8 or 1)
 };
 constexpr int kZgenThreads = 256;
 constexpr int kZgenPer = 16;
