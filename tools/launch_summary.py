@@ -3,8 +3,8 @@ per-kernel shares of the product step.
 
     python tools/launch_summary.py LAUNCHES.csv > profiles/rNN_launch_summary.md
 
-Products are the runs of tmg:: kernels that start at k_zstat (the split's
-carry aggregates); bench.py issues them as full, low, high per step (high is
+Products are the runs of tmg:: kernels that start at the split (k_zsplit,
+k_zgen, or k_zstat where the split's carry aggregates are a kernel of their own); bench.py issues them as full, low, high per step (high is
 the run containing k_high_round).
 """
 import collections
@@ -33,7 +33,7 @@ def main():
     for k, t in seq:
         if not k.startswith("k_"):
             continue
-        starts = k in ("k_zstat", "k_small_product", "k_basecase") or (k.startswith("k_zgen") and prev != "k_zstat")
+        starts = k in ("k_zstat", "k_small_product", "k_basecase") or ((k.startswith("k_zgen") or k.startswith("k_zsplit")) and prev != "k_zstat")
         if starts and cur:
             groups.append(cur)
             cur = []

@@ -23,13 +23,15 @@ ti = hdr.index("gpu__time_duration.sum")
 units = rows[1]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 res, order, mode = {}, ["full", "low", "high"], -1
+prev = None
 for r in rows[2:]:
     name = r[ki]
     base = re.sub(r"^void ", "", name).replace("<unnamed>::", "").replace("unnamed>::", "").replace("(anonymous namespace)::", "").split("(")[0]
     base = re.sub(r"^(\w+::)*", "", base.split("<")[0]) if "<" in base else re.sub(r"^(\w+::)*", "", base)
-    if base == "k_zstat":
+    if base in ("k_zstat", "k_zsplit") or (base == "k_zgen_t" and prev != "k_zstat"):
         mode += 1
-    short = {"k_zgen_t": "k_zgen", "k_f1_ct": "k_f1", "k_f1_pp": "k_f1", "k_ilast_ct": "k_ilast",
+    prev = base
+    short = {"k_zgen_t": "k_zgen", "k_f1d_ct": "k_f1", "k_f1_ct": "k_f1", "k_f1_pp": "k_f1", "k_ilast_ct": "k_ilast",
              "k_ilast_pp": "k_ilast", "k_mid_4096": "k_mid"}.get(base, base)
     by = float(r[ri]) * scale.get(units[ri], 1) + float(r[wi]) * scale.get(units[wi], 1)
     res[f"{order[mode % 3]}:{short}"] = {"dram_bytes": by, "kernel": name, "us": float(r[ti])}

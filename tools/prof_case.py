@@ -1,5 +1,5 @@
 """One warm-up and one measured product of each mode at n = 2^LOG2N, for ncu:
-python tools/prof_case.py [log2n]  (kernels per product: full 5, low 5, high 6)"""
+python tools/prof_case.py [log2n]  (kernels per product at 2^26: full 5, low 5, high 6)"""
 import sys
 sys.path.insert(0, '.')
 import numpy as np
