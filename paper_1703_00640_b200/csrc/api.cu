@@ -674,7 +674,8 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         unsigned blocksp = blocks2;
         bool runs_lb = false;
         if (runs) {
-          const int64_t rl = int64_t(kRunThreads) * p.b;
+          const int runlen = carry_runs_len(int(pl.mc.mode), lam, int(p.b), !cx.opt.generic_runs);
+          const int64_t rl = int64_t(kRunThreads) * p.b * runlen / 64;
           blocksp = unsigned((pl.ML + rl - 1) / rl);
           a.blk_limbs = rl;
           a.wlen = pl.L;
@@ -682,7 +683,7 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
           w.aggs.ensure(size_t(blocksp) * 8 + 16);
           a.aggs = w.aggs.as<uint32_t>();
           a.cins = reinterpret_cast<int*>(a.aggs + blocksp);
-          const size_t smem3 = carry_runs_smem(int(pl.mc.mode), lam);
+          const size_t smem3 = carry_runs_smem(int(pl.mc.mode), lam, runlen);
           set_smem(runs, smem3);
           // one kernel: the block carry-ins by a decoupled look-back over the
           // published aggregates (TMG_OPT_CARRY_KERNELS 3 keeps k_carry_patch)

@@ -50,15 +50,15 @@ constexpr int kHaloWin = kHaloBelow + 2;
 
 // Slot geometry (doubles): [k0 - hlo, k0 + 64 + hhi) plus padding so that
 // slot / 2 is odd.
-template <int MODE, int LAM>
+template <int MODE, int LAM, int RUN = 64>
 struct RunGeom {
   static constexpr int need_lo = MODE == kModeFull ? 0 : MODE == kModeLow ? (LAM > 2 ? LAM - 2 : 0) : LAM;
   static constexpr int hhi = MODE == kModeLow ? 2 : 0;
   static constexpr int hlo0 = (need_lo + 1) & ~1;
   static constexpr int pad0 = MODE == kModeFull ? 2 : 0;
   // slot / 2 odd: grow the lower halo by 2 when needed
-  static constexpr int hlo = (((kRun + hlo0 + hhi + pad0) / 2) & 1) ? hlo0 : hlo0 + 2;
-  static constexpr int slot = kRun + hlo + hhi + pad0;
+  static constexpr int hlo = (((RUN + hlo0 + hhi + pad0) / 2) & 1) ? hlo0 : hlo0 + 2;
+  static constexpr int slot = RUN + hlo + hhi + pad0;
   static_assert((slot / 2) % 2 == 1 && slot % 2 == 0, "slot stride must be an odd multiple of 16 bytes");
 };
 
@@ -260,15 +260,15 @@ __host__ __device__ constexpr int gcd64(int b) { return b % 64 == 0 ? 64 : b % 3
 // of limbs): one period is unrolled (static shifts, emission steps and limb
 // offsets) and looped over, the last period apart (it holds the snapshot
 // of the last limb's lane).  With a run-time width: a loop over the bodies.
-template <int B, class Body>
+template <int B, int RUN, class Body>
 __device__ __forceinline__ void walk_periods(RunAcc& s, double* slot, Body& body) {
   if constexpr (B == 0) {
 #pragma unroll 1
-    for (uint32_t i0 = 0; i0 < kRun - 8; i0 += 8) body(i0, slot, std::false_type{});
-    body(kRun - 8, slot, std::true_type{});
+    for (uint32_t i0 = 0; i0 < RUN - 8; i0 += 8) body(i0, slot, std::false_type{});
+    body(RUN - 8, slot, std::true_type{});
   } else {
-    constexpr uint32_t g = uint32_t(gcd64(B)), PER = 64u / g, LPP = uint32_t(B) / g, NP = g;
-    static_assert(PER >= 8 && PER % 8 == 0, "period of whole bodies");
+    constexpr uint32_t g = uint32_t(gcd64(B)), PER = 64u / g, LPP = uint32_t(B) / g, NP = uint32_t(RUN) / PER;
+    static_assert(PER >= 8 && PER % 8 == 0 && RUN % PER == 0, "period of whole bodies");
 #pragma unroll 1
     for (uint32_t it = 0; it + 1 < NP; ++it) {
       s.sh = 0;
@@ -280,15 +280,19 @@ __device__ __forceinline__ void walk_periods(RunAcc& s, double* slot, Body& body
     s.li = 0;
 #pragma unroll
     for (uint32_t j = 0; j + 8 < PER; j += 8) body((NP - 1) * PER + j, slot + (NP - 1) * LPP, std::false_type{});
-    body(kRun - 8, slot + (NP - 1) * LPP, std::true_type{});
+    body(RUN - 8, slot + (NP - 1) * LPP, std::true_type{});
   }
 }
 
 // B: the chunk width as a compile-time constant (the walk unrolls fully and
 // every shift, emission step and slot offset is static), or 0 for any b.
-template <int MODE, int LAM, int B>
-__global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ CarryArgs a) {
-  using G = RunGeom<MODE, LAM>;
+// RUN: coefficients per run, 64, or 32 for an even compiled width (b / 2
+// limbs per run, smaller slots, more resident warps).
+template <int MODE, int LAM, int B, int RUN = 64>
+__global__ void __launch_bounds__(kRT, (RUN == 32 ? 5 : 3)) k_carry_runs(const __grid_constant__ CarryArgs a) {
+  using G = RunGeom<MODE, LAM, RUN>;
+  static_assert(RUN == 64 || (RUN == 32 && B != 0 && B % 2 == 0), "runs are whole limbs");
+  constexpr int kRun = RUN;  // (shadows the 64-coefficient default)
   pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -304,14 +308,15 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const MapConsts& mc = a.mc;
   const uint32_t b = B ? uint32_t(B) : uint32_t(mc.b);
+  const uint32_t rl = b * uint32_t(RUN) / 64u;  // limbs per run
   const int64_t K = a.K, N = mc.N;
   const int64_t blk = blockIdx.x;
-  const int64_t bl = int64_t(kRT) * b;  // limbs per block
+  const int64_t bl = int64_t(kRT) * rl;  // limbs per block
   const int64_t ms = blk * bl;
   const int64_t me = min(a.ML, ms + bl);
   const int64_t kblk = blk * int64_t(kRT) * kRun;  // first coefficient of the block
   const int64_t k0 = kblk + int64_t(tid) * kRun;
-  const int64_t m0 = ms + int64_t(tid) * b;
+  const int64_t m0 = ms + int64_t(tid) * rl;
   double* slots = reinterpret_cast<double*>(smem_raw);
   double* slot = slots + size_t(tid) * G::slot;
   constexpr bool hmode = MODE == kModeHigh, lowm = MODE == kModeLow, fullm = MODE == kModeFull;
@@ -406,11 +411,12 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
     ra.flags = rg.flags;
     flags = fg;
   }
-  const int64_t khalo = ms > 0 ? (64 * (ms - 1) + b - 1) / b : kblk;  // ceil(64 (ms - 1) / b)
+  // first coefficient of the limb below the block: ceil(64 (ms - 1) / b), and 64 ms = b kblk
+  const int64_t khalo = ms > 0 ? kblk - int64_t(64u / b) : kblk;
   // ---- the walk ----
   RunAcc s;
   // first coefficient of the run's last limb: ceil(64 (b - 1) / b)
-  const uint32_t ilast = (64u * (b - 1u) + b - 1u) / b;
+  const uint32_t ilast = (64u * (rl - 1u) + b - 1u) / b;
   if (live) {
     if (interior) {
       mbar_wait(&s_mbar[warp], 0);
@@ -430,7 +436,7 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
 #pragma unroll
           for (int q = 0; q < 8; ++q) run_step<LASTB>(s, ev[q], b, limbs, i0 + q, ilast);
         };
-        walk_periods<B>(s, slot, body);
+        walk_periods<B, RUN>(s, slot, body);
       } else {
         // slot position of w_j for the body's first output: j0 - (LAM - 1),
         // j0 = k0 + i0 + (low: 1), minus the slot origin k0 - hlo
@@ -481,7 +487,7 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
 #pragma unroll
           for (int q = 0; q < 8; ++q) run_step<LASTB>(s, ev[q], b, limbs, i0 + q, ilast);
         };
-        walk_periods<B>(s, slot, body);
+        walk_periods<B, RUN>(s, slot, body);
       }
     } else {
       // rounded coefficients from the slot (written above)
@@ -528,7 +534,7 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
   long long lane_hi, cout = (long long)s.lo;  // after b emissions the accumulator is the carry out
   {
     // lane = acc_final - rho, acc_final = (last limb, cout)
-    const unsigned long long last = live ? (unsigned long long)__double_as_longlong(slot[b - 1]) : 0ull;
+    const unsigned long long last = live ? (unsigned long long)__double_as_longlong(slot[rl - 1]) : 0ull;
     lane_hi = cout - s.rhi - (last < s.rlo ? 1 : 0);
   }
   const int d = int(cout - lane_hi);
@@ -559,14 +565,14 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
   uint32_t tf0 = kTfIdentity, f = kTfIdentity;
   unsigned long long x0 = 0;
   bool allones = true, allzero = true;
-  const uint32_t nl = live ? uint32_t(min(int64_t(b), a.ML - m0)) : 0u;  // limbs of the run below ML
+  const uint32_t nl = live ? uint32_t(min(int64_t(rl), a.ML - m0)) : 0u;  // limbs of the run below ML
   if (live) {
     const unsigned long long l0 = (unsigned long long)__double_as_longlong(slot[0]);
     const __int128 s0 = (__int128)l0 + (__int128)hin;
     tf0 = limb_tf(s0, flags);
     x0 = (unsigned long long)s0;
     unsigned long long ov = 0, av = ~0ull;
-    for (uint32_t i = 1; i < b; ++i) {
+    for (uint32_t i = 1; i < rl; ++i) {
       const unsigned long long l = (unsigned long long)__double_as_longlong(slot[i]);
       ov |= l;
       av &= l;
@@ -589,7 +595,7 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
     f = enc;
   } else if (m0 < a.ML) {
     // a run above the coefficients: zero limbs (they pass the carries of the sign)
-    for (uint32_t i = 0; i < b; ++i) slot[i] = 0.0;
+    for (uint32_t i = 0; i < rl; ++i) slot[i] = 0.0;
     const __int128 s0 = (__int128)hin;
     tf0 = limb_tf(s0, flags);
     x0 = (unsigned long long)s0;
@@ -619,15 +625,15 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
   // added afterwards (single pass: below, once the look-back has it; two
   // kernels: by k_carry_patch)
   const bool haslimbs = m0 < a.ML;
-  const uint32_t nlw = haslimbs ? uint32_t(min(int64_t(b), a.ML - m0)) : 0u;  // limbs below ML
+  const uint32_t nlw = haslimbs ? uint32_t(min(int64_t(rl), a.ML - m0)) : 0u;  // limbs below ML
   (void)nl;
   const int cin0 = tf_apply(ex, 0);
-  const bool top = haslimbs && a.ML - 1 < m0 + int64_t(b);  // owns the top limb
+  const bool top = haslimbs && a.ML - 1 < m0 + int64_t(rl);  // owns the top limb
   // what flows above the top limb for the carry cin into the run (the sign
   // of the recombined value)
   auto top_carry = [&](int cin) -> long long {
     const uint32_t lt = uint32_t(a.ML - 1 - m0);
-    long long ct = (lt == b - 1u) ? lane_hi + tf_apply(f, cin) : __double_as_longlong(slot[lt + 1]);
+    long long ct = (lt == rl - 1u) ? lane_hi + tf_apply(f, cin) : __double_as_longlong(slot[lt + 1]);
     if (ct < -1 || ct > 1) {
       flags |= kFlagCarryRange;
       ct = 0;
@@ -638,7 +644,7 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
     slot[0] = __longlong_as_double((long long)(x0 + (unsigned long long)(long long)cin0));
     int c = tf_apply(tf0, cin0);
     if (c != 0) {
-      for (uint32_t i = 1; i < b; ++i) {
+      for (uint32_t i = 1; i < rl; ++i) {
         const unsigned long long l = (unsigned long long)__double_as_longlong(slot[i]);
         slot[i] = __longlong_as_double((long long)(l + (unsigned long long)(long long)c));
         if (c > 0 ? l != ~0ull : l != 0ull) {
@@ -670,8 +676,8 @@ __global__ void __launch_bounds__(kRT, 3) k_carry_runs(const __grid_constant__ C
   uint64_t* tail = hmode ? a.tbuf : reinterpret_cast<uint64_t*>(a.sbuf);
   const uint32_t nlb = uint32_t(me - ms);
   auto limb_at = [&](uint32_t ml) -> uint64_t {
-    const uint32_t g = B ? ml / uint32_t(B ? B : 1) : fdiv(ml, a.fb);
-    return uint64_t(__double_as_longlong(slots[size_t(g) * G::slot + (ml - g * b)]));
+    const uint32_t g = B ? ml / uint32_t(B ? B * RUN / 64 : 1) : fdiv(ml, a.fb);
+    return uint64_t(__double_as_longlong(slots[size_t(g) * G::slot + (ml - g * rl)]));
   };
   auto store_limb = [&](int64_t m, uint64_t x) {
     if constexpr (hmode) {
@@ -793,7 +799,7 @@ template <int MODE>
 CarryLanesFn runs_mode(int lam, int b) {
   // compiled chunk widths: what select_params picks from 2^22 to 2^30 bits
   if (lam == 4 && b == 13) return k_carry_runs<MODE, 4, 13>;
-  if (lam == 5 && b == 12) return k_carry_runs<MODE, 5, 12>;
+  if (lam == 5 && b == 12) return k_carry_runs<MODE, 5, 12, 32>;
   if (lam == 5 && b == 11) return k_carry_runs<MODE, 5, 11>;
   switch (lam) {
     case 3: return k_carry_runs<MODE, 3, 0>;
@@ -830,7 +836,15 @@ CarryLanesFn carry_runs_kernel(int mode, int lam, int b, bool compiled_b) {
   return mode == kModeLow ? runs_mode<kModeLow>(lam, b) : runs_mode<kModeHigh>(lam, b);
 }
 
-size_t carry_runs_smem(int mode, int lam) {
+// coefficients per run of the kernel carry_runs_kernel returns
+int carry_runs_len(int mode, int lam, int b, bool compiled_b) {
+  return (compiled_b && mode != kModeFull && lam == 5 && b == 12) ? 32 : 64;
+}
+
+size_t carry_runs_smem(int mode, int lam, int run) {
+  if (run == 32) {
+    return size_t(kRT) * (mode == kModeLow ? RunGeom<kModeLow, 5, 32>::slot : RunGeom<kModeHigh, 5, 32>::slot) * 8;
+  }
   if (mode == kModeFull) return size_t(kRT) * RunGeom<kModeFull, 0>::slot * 8;
   return mode == kModeLow ? runs_smem_mode<kModeLow>(lam) : runs_smem_mode<kModeHigh>(lam);
 }

@@ -289,7 +289,8 @@ size_t carry2_smem(int b, int lam, int pt, bool hbuf);
 // nullptr without an instantiation for (mode, lambda)
 constexpr int kRunThreads = 128;
 CarryLanesFn carry_runs_kernel(int mode, int lam, int b, bool compiled_b);
-size_t carry_runs_smem(int mode, int lam);
+size_t carry_runs_smem(int mode, int lam, int run);
+int carry_runs_len(int mode, int lam, int b, bool compiled_b);
 
 struct HighRoundArgs {
   const uint64_t* tbuf;
