@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(kRT, (RUN == 32 ? 5 : 3)) k_carry_runs(const _
   __shared__ uint32_t sw[32];
   __shared__ long long s_lanehi[kRT / 32];
   __shared__ long long s_halo[8];
+  __shared__ double s_terms[kMaxRootTerms + 1];
   __shared__ __align__(16) double s_hw[kHaloWin];  // w_{kblk - 16} .. w_{kblk + 1} (interior blocks)
   __shared__ double s_psi;
   __shared__ uint32_t s_flags, s_first, s_hmin, s_sticky, s_last;
@@ -377,12 +378,20 @@ __global__ void __launch_bounds__(kRT, (RUN == 32 ? 5 : 3)) k_carry_runs(const _
   RoundAcc ra;
   uint32_t flags = 0;
   if (!blk_interior) {
-    if (tid == 0) {
-      // psi enters only x_N and the fold region k < nfold (delta+,
-      // maps_f64.cpp:363-383): the first and the last block (the halo lane of
-      // the block's first limb included)
-      const bool need_psi = hmode && (kblk - 8 < mc.nfold || kblk_end > N);
-      if (need_psi) s_psi = high_psi(mc, [&](int64_t j) { return __ldg(a.w + j); }, a.aux[0]);
+    // psi enters only x_N and the fold region k < nfold (delta+,
+    // maps_f64.cpp:363-383): the first and the last block (the halo lane of
+    // the block's first limb included).  Its hrho terms (high_psi,
+    // pipeline.cuh) are chains of dependent loads: one term per thread, then
+    // summed in high_psi's order.
+    if (hmode && (kblk - 8 < mc.nfold || kblk_end > N)) {
+      auto WS = [&](int64_t j) { return __ldg(a.w + j); };
+      for (int d = 1 + tid; d <= mc.nhrho && d <= N; d += kRT) s_terms[d] = high_buf(mc, WS, N - d);
+      __syncthreads();
+      if (tid == 0) {
+        double hrho = 0.0;
+        for (int d = 1; d <= mc.nhrho && d <= N; ++d) hrho += s_terms[d] * mc.ipow[d];
+        s_psi = (a.aux[0] - hrho * mc.root_neg_n) / mc.cofactor_scaled;
+      }
     }
     // (the generic evaluator is out of line: it gets its own accumulator, so
     // that the walk's stays in registers)
@@ -750,8 +759,16 @@ __global__ void __launch_bounds__(kRT, (RUN == 32 ? 5 : 3)) k_carry_runs(const _
     const HighLimbs3 hl(a);
     const uint32_t lfix = (blk == 0 || lb) ? 0u : (s_first == 0xffffffffu ? 0xffffffffu : s_first + 1u);
     uint32_t hmin = 0xffffffffu, sticky = 0;
-    for (uint32_t ml = tid; ml < nlb; ml += kRT) {
-      if (ml >= lfix) hl.see(ms + ml, limb_at(ml), hmin, sticky);
+    // single pass: a block above the sticky bits whose lowest possible
+    // nomination (limb ms - hq - 1 of t >> s) cannot lower the one already
+    // made by a block below it has nothing to add
+    bool skip = false;
+    if (lb && ms - hl.hq - 1 > 0 && 64 * ms >= hl.sb)
+      skip = __ldcg(a.hstop) <= uint32_t(ms - hl.hq - 1);
+    if (!skip) {
+      for (uint32_t ml = tid; ml < nlb; ml += kRT) {
+        if (ml >= lfix) hl.see(ms + ml, limb_at(ml), hmin, sticky);
+      }
     }
     // w0's top limb has zero fill above bit 64 - r: never all ones
     if (hl.hr != 0 && blk == 0 && tid == 0 && hl.WL > 0) hmin = min(hmin, uint32_t(hl.WL - 1));
