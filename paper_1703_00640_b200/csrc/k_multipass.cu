@@ -1328,8 +1328,30 @@ k_high_round(HighRoundArgs a) {
   const int64_t me = min(a.WL, ms + LB);
   uint32_t flags = 0, topbit = 0, lownz = 0;
   const int64_t OL = a.out_limbs;
-  // limbs interleaved over the block (m = ms + tid + i * threads): the
-  // loads of t and the stores of w are coalesced; all loads first
+  // Blocks whose limbs all lie below bit n, inside t and below the last
+  // output limb (block-uniform; all but the top block): no bounds or range
+  // tests per limb, 32-bit indices, the upper word from the neighbouring lane.
+  if (me == ms + LB && me + q + 1 <= a.ML && 64 * me <= a.n && me <= OL - 1 && a.ML < (int64_t(1) << 31)) {
+    const uint64_t* tq = t + q + ms;
+    uint64_t* op = a.out + ms;
+    uint64_t lo[kHighPerThread];
+#pragma unroll
+    for (int i = 0; i < kHighPerThread; ++i) lo[i] = tq[tid + i * kCarryThreads];
+    const uint32_t f0 = first >= uint32_t(ms) ? first - uint32_t(ms) : 0u;  // limbs ms + j <= first: j <= f0
+    const bool anyinc = inc && uint64_t(first) >= uint64_t(ms);
+    uint64_t nz = 0;
+#pragma unroll
+    for (int i = 0; i < kHighPerThread; ++i) {
+      const uint32_t j = uint32_t(tid) + uint32_t(i) * kCarryThreads;
+      uint64_t hi = __shfl_down_sync(0xffffffffu, lo[i], 1);
+      if ((tid & 31) == 31) hi = tq[j + 1];
+      const uint64_t w0 = r ? ((lo[i] >> r) | (hi << (64 - r))) : lo[i];
+      const uint64_t x = w0 + uint64_t((anyinc && j <= f0) ? 1 : 0);
+      nz |= x;
+      op[j] = x;
+    }
+    if (nz) atomicOr(&s_low, 1u);
+  } else {
   uint64_t tlo[kHighPerThread], thi[kHighPerThread];
 #pragma unroll
   for (int i = 0; i < kHighPerThread; ++i) {
@@ -1349,6 +1371,7 @@ k_high_round(HighRoundArgs a) {
       high_classify(x, m, a.n, topbit, lownz, flags);
       if (m < OL) a.out[m] = x & high_mask(m, OL, a.n);
     }
+  }
   }
   if (flags) atomicOr(&s_flags, flags);
   if (topbit) atomicOr(&s_top, 1u);
