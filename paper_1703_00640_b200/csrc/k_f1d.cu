@@ -280,6 +280,9 @@ constexpr F1Fn f1d_fn() {
 static const F1DShape kF1DShapes[] = {
     TMG_F1D(1728, 2, 576, 12, 12, 12, 12),
     TMG_F1D(1440, 2, 576, 12, 12, 12, 10),
+    // 2^24 (BASELINE config 2): 448 x 4096 full, 320 x 4096 low/high
+    TMG_F1D(448, 4, 512, 16, 16, 4, 7),
+    TMG_F1D(320, 4, 512, 16, 16, 5, 4),
 };
 #undef TMG_F1D
 
