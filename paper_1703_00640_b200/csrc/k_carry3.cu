@@ -447,49 +447,73 @@ __global__ void __launch_bounds__(kRT, (RUN == 32 ? 5 : 3)) k_carry_runs(const _
         };
         walk_periods<B, RUN>(s, slot, body);
       } else {
-        // slot position of w_j for the body's first output: j0 - (LAM - 1),
-        // j0 = k0 + i0 + (low: 1), minus the slot origin k0 - hlo
-        constexpr int off = G::hlo + (lowm ? 1 : 0) - (LAM - 1) - (hmode ? 1 : 0);
+        // The flat post-map in scatter form: input w_i adds its row-r term
+        // w_i (P_r(i) c_r), P_r(i) = i (i + st) ... (i + (r - 1) st), to the
+        // pending sum of output i + r for r = lambda-1 .. 1 and closes output
+        // i with + w_i.  Each output receives its rows in the gather form's
+        // order (r = lambda-1 first, row 0 last) and the prefix products
+        // P_1 .. P_{lambda-1} of one input are the gather form's own
+        // products, so the values are bit-identical -- with one chain of
+        // products per input instead of one per output and row (about 16
+        // FP64 instructions per coefficient against 26 at lambda 5).
+        // First input: lambda - 1 below the run's first output (low: j = k0 + 1;
+        // high: k0 - 1, for the first difference).
+        constexpr int off = G::hlo + (lowm ? 1 : 0) - (LAM - 1) - (hmode ? 1 : 0);  // its slot position
         static_assert(off >= 0, "window below the slot");
-        constexpr int pe = off & 1;                      // start one lower when odd
-        constexpr int nv = 8 + (LAM - 1) + (hmode ? 1 : 0) + pe;  // doubles per body
-        constexpr int nv2 = (nv + 1) / 2;
+        constexpr int P0 = off + (LAM - 1) + (hmode ? 1 : 0);  // slot position of the run's first own input
+        constexpr int pe = P0 & 1;                             // start one lower when odd
+        constexpr int nv2 = (8 + pe + 1) / 2;                  // 16-byte loads per body
+        static_assert((P0 - pe) + (kRun - 8) + 2 * nv2 <= G::slot, "window beyond the slot");
         const double st = lowm ? double(N) : -double(N);
         const double step = mc.step, sc = mc.scale_out;
         double cr[LAM];
 #pragma unroll
         for (int r = 0; r < LAM; ++r) cr[r] = mc.cpost[r];
-        auto pfd = [&](double jd, const double* W, int c) -> double { return pfd_w<LAM>(jd, W, c, st, cr); };
-        // jd: the first post-map output index of the run as an exact double
-        double jd = double(k0 + (lowm ? 1 : 0));
+        double pend[LAM > 1 ? LAM - 1 : 1];  // pend[r - 1]: sum of output (next input + r - 1), rows >= r
+#pragma unroll
+        for (int r = 0; r < LAM - 1; ++r) pend[r] = 0.0;
+        double idd = double(k0 + (lowm ? 1 : 0) - (LAM - 1) - (hmode ? 1 : 0));  // next input's index, exact
+        auto step_in = [&](double w) -> double {
+          const double out = pend[0] + w;
+          double p = idd, f = idd + st;
+          double np[LAM > 1 ? LAM - 1 : 1];
+#pragma unroll
+          for (int r = 1; r < LAM; ++r) {
+            if (r > 1) {
+              p *= f;
+              f += st;
+            }
+            np[r - 1] = fma(w, p * cr[r], r < LAM - 1 ? pend[r] : 0.0);
+          }
+#pragma unroll
+          for (int r = 0; r < LAM - 1; ++r) pend[r] = np[r];
+          idd += 1.0;
+          return out;
+        };
+        // the inputs below the run's own: their outputs are the run below's
+#pragma unroll
+        for (int q = 0; q < LAM - 1; ++q) (void)step_in(slot[off + q]);
         double hprev = 0.0;  // high: the previous flat output
-        if constexpr (hmode) {
-          // flat output k0 - 1 from the slot's head: w_{k0 - 1 - r} at slot[hlo - 1 - r]
-          hprev = pfd(jd - 1.0, slot, G::hlo - 1);
-        }
+        if constexpr (hmode) hprev = step_in(slot[off + LAM - 1]);
         auto body = [&](uint32_t i0, double* limbs, auto lastc) {
           constexpr bool LASTB = decltype(lastc)::value;
           double W[2 * nv2];
 #pragma unroll
           for (int q = 0; q < nv2; ++q) {
-            const double2 t = s2[(off - pe) / 2 + i0 / 2 + q];
+            const double2 t = s2[(P0 - pe) / 2 + i0 / 2 + q];
             W[2 * q] = t.x;
             W[2 * q + 1] = t.y;
           }
-          // W[pe + x] = w_{j0 - (LAM - 1) - (high: 1) + x}
-          constexpr int c0 = pe + (LAM - 1) + (hmode ? 1 : 0);  // W index of w_{j0}
-          static_assert((off - pe) + (kRun - 8) + 2 * nv2 <= G::slot, "window beyond the slot");
           double x[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const double h = pfd(jd, W, c0 + q);
+            const double h = step_in(W[pe + q]);
             if constexpr (lowm) {
               x[q] = h * sc;
             } else {
               x[q] = (h - hprev * step) * sc;
               hprev = h;
             }
-            jd += 1.0;
           }
           long long ev[8];
           round8(ra, x, ev);
