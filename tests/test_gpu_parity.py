@@ -948,3 +948,41 @@ def test_split_carry_in_paths(n):
             assert np.array_equal(r0, r1)
             _check(mode, u, v, n, tm.from_limbs(r0))
     c.close()
+
+
+@pytest.mark.parametrize("n", [1 << 24, (1 << 24) + 12345])
+def test_split_by_runs_carry_chains(n):
+    """k_zsplit (the split by runs, default from about 2^23 bits) against
+    the block-scan split k_zgen (TMG_OPT_SPLIT_KERNEL = 1) and GMP: random
+    operands with stretches of windows equal to 2^{b-1} -- the windows through
+    which a run's carry-in comes from further below (carry_below) -- placed
+    across run, block and tile-row boundaries, both with a carry arriving at
+    the stretch (the window below it above 2^{b-1}) and without."""
+    c = _opt_ctx((tm._native.TMG_OPT_SPLIT_KERNEL, 1))
+    rng = np.random.default_rng(n & 0xffff)
+    nl = (n + 63) // 64
+    for mode in (tm.Mode.FULL, tm.Mode.LOW, tm.Mode.HIGH):
+        p = sp(n, mode)
+        b, N = p.b, p.N
+        lead = (N + 1) * b - n if mode == tm.Mode.HIGH else 0
+        ops = []
+        for carry_first in (False, True):
+            x = int.from_bytes(rng.bytes(nl * 8), "little") & ((1 << n) - 1)
+            # stretches [j1, j2) of chunks (of the operand shifted up by lead)
+            for j1, length in ((31, 3), (8190, 70), (4096 * 3 - 40, 100), (8192 * 5 + 33, 64), (100000, 1)):
+                for j in range(j1, j1 + length):
+                    pos = j * b - lead
+                    if pos < 0 or pos + b > n:
+                        continue
+                    x &= ~(((1 << b) - 1) << pos)
+                    x |= (1 << (b - 1)) << pos
+                pos = (j1 - 1) * b - lead
+                if carry_first and pos >= 0:
+                    x |= ((1 << b) - 1) << pos  # all ones: above 2^{b-1}, a carry enters the stretch
+            ops.append(port.int_to_limbs(x, nl))
+        u, v = ops
+        r0 = tm.default_context(0).product_limbs(mode, u, v, p)
+        r1 = c.product_limbs(mode, u, v, p)
+        assert np.array_equal(r0, r1)
+        _check(mode, u, v, n, tm.from_limbs(r0))
+    c.close()
