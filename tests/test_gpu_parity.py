@@ -708,12 +708,14 @@ def test_generic_row_pass():
     c.close()
 
 
+@pytest.mark.parametrize("kernels", [0, 2, 3])
 @pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 448])
-def test_carry_in_from_the_lanes_ticket(n):
+def test_carry_in_from_the_lanes_ticket(n, kernels):
     """TMG_OPT_PATCH_SCAN_MAX = 0: full, low and high products take the
-    carry-ins the last k_carry_lanes block scans (the path above 4096 carry
-    blocks, n >~ 2^27) instead of k_carry_patch's own scan."""
-    c = _opt_ctx((tm._native.TMG_OPT_PATCH_SCAN_MAX, 0))
+    carry-ins the last block of k_carry_lanes (TMG_OPT_CARRY_KERNELS 2) or
+    of k_carry_runs (3) scans -- the two-kernel path above 4096 carry blocks
+    -- instead of k_carry_patch's own scan; 0: whatever the size picks."""
+    c = _opt_ctx((tm._native.TMG_OPT_PATCH_SCAN_MAX, 0), (tm._native.TMG_OPT_CARRY_KERNELS, kernels))
     _config3_all_modes(c, n)
     c.close()
 
