@@ -572,8 +572,11 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       set_smem(ilk, pl.smem_il);
       {
         KTimer kt(cx, "k_ilast", double(L) * 16.0, int(p.mode), st);
-        // one CTA per tile (a persistent ilast measured 49 against 45 us)
-        const unsigned grid = a.g.ncols >> a.logc;
+        // the compiled pass is persistent (it stages its next tile in shared
+        // memory behind its last stage); the others take one CTA per tile
+        const unsigned tiles = a.g.ncols >> a.logc;
+        const unsigned grid = pl.colct_il ? std::min<unsigned>(tiles, unsigned(cx.num_sms * (pl.thr_il <= 288 ? 2 : 1)))
+                                          : tiles;
         launch(cx, ilk, dim3(grid), dim3(pl.thr_il), pl.smem_il, st, a, "ilast");
       }
       check_launch(cx, "k_ilast");

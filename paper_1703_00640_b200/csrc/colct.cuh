@@ -107,11 +107,17 @@ __device__ __forceinline__ void cc_store(double2 (&x)[P], const double2* __restr
   }
 }
 
-template <bool INV, class SC, int S, int LOGC, int NTHR, int P, class Src, class Sink>
+// hook: called by every thread once the last stage has taken its inputs from
+// the tile (behind that stage's barrier): the tile's shared memory is free
+// from there on, e.g. for staging the next tile.
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+template <bool INV, class SC, int S, int LOGC, int NTHR, int P, class Src, class Sink, class Hook = NoHook>
 __device__ __forceinline__ void cc_stages(double2 (&x)[P], double2* __restrict__ buf,
                                           const LayCols& lay, const double2* __restrict__ stab,
                                           const SubFft& p, const Src& src, const Sink& sink,
-                                          int tid) {
+                                          int tid, const Hook& hook = Hook{}) {
   constexpr int RAD = SC::rad(S);
   constexpr uint32_t NS = SC::ns(S);
   constexpr uint32_t R = SC::R;
@@ -127,11 +133,12 @@ __device__ __forceinline__ void cc_stages(double2 (&x)[P], double2* __restrict__
   __syncthreads();
   const double2* st = stab + p.toff[S];
   if constexpr (last) {
+    hook();
     cc_store<RAD, NB, INV, R, NS, LOGC, NTHR, P>(x, st, p.qmul[S], sink, tid);
   } else {
     cc_store<RAD, NB, INV, R, NS, LOGC, NTHR, P>(x, st, p.qmul[S], SmemSink<LayCols>{buf, lay}, tid);
     __syncthreads();
-    cc_stages<INV, SC, S + 1, LOGC, NTHR, P>(x, buf, lay, stab, p, src, sink, tid);
+    cc_stages<INV, SC, S + 1, LOGC, NTHR, P>(x, buf, lay, stab, p, src, sink, tid, hook);
   }
 }
 

@@ -948,6 +948,21 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 288 ? 2 : 1)) k_f1_ct(F1Args a)
   }
 }
 
+// The tile's raw rows as staged by cp.async: row e, item i at e c + i.
+struct RawTileSrc {
+  const double2* raw;
+  uint32_t logc;
+  __device__ __forceinline__ double2 operator()(uint32_t item, uint32_t e) const {
+    return raw[(e << logc) + item];
+  }
+};
+
+// Persistent over the tiles.  A tile's rows (c columns of 16 bytes each)
+// arrive by cp.async in the tile's own shared memory, issued once the
+// previous tile's last stage has taken its inputs into registers -- the
+// buffer is dead from there on -- so the copies fly while that stage
+// computes and stores, and the first stage reads shared memory instead of
+// waiting on global loads.
 template <class SC, int LOGC, int NTHR, int P>
 __global__ void __launch_bounds__(NTHR, (NTHR <= 288 ? 2 : 1)) k_ilast_ct(ILastArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -960,17 +975,31 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 288 ? 2 : 1)) k_ilast_ct(ILastA
   for (uint32_t i = tid; i < a.fft.stablen; i += NTHR) stab[i] = __ldg(a.fft.stab + i);
   pdl_wait();
   const LayCols lay{uint32_t(LOGC), c - 1};
+  auto stage_tile = [&](uint32_t tile) {
+    const uint32_t col0 = tile * c;
+    for (uint32_t i = tid; i < R * c; i += NTHR)
+      cp_async16(sbuf + i, a.data + col_off(a.g, 0, i >> LOGC, col0 + (i & (c - 1))));
+    cp_async_commit();
+  };
+  bool first = true;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint32_t col0 = tile * c;
     const uint32_t nx = tile + gridDim.x;
-    if (nx < ntiles) {
-      // the next tile's row segments (c consecutive columns each) into L2
-      for (uint32_t e = tid; e < R; e += NTHR)
-        prefetch_l2(a.data + col_off(a.g, 0, e, nx * c), c * 16);
-    }
+    auto hook = [&]() {
+      if (nx < ntiles) stage_tile(nx);
+    };
+    const CoefSink sink{a.coef, a.g.ncols, col0, a.scale, a.scale_lo};
     double2 x[P];
-    cc_stages<true, SC, 0, LOGC, NTHR, P>(x, sbuf, lay, stab, a.fft, ColSrc{a.data, a.g, 0, col0},
-                                          CoefSink{a.coef, a.g.ncols, col0, a.scale, a.scale_lo}, tid);
+    if (first) {
+      // the CTA's first tile: straight from global memory (nothing to overlap with)
+      first = false;
+      cc_stages<true, SC, 0, LOGC, NTHR, P>(x, sbuf, lay, stab, a.fft, ColSrc{a.data, a.g, 0, col0}, sink, tid, hook);
+    } else {
+      cp_async_wait_all();
+      __syncthreads();
+      cc_stages<true, SC, 0, LOGC, NTHR, P>(x, sbuf, lay, stab, a.fft, RawTileSrc{sbuf, uint32_t(LOGC)}, sink, tid,
+                                            hook);
+    }
   }
 }
 
