@@ -107,12 +107,9 @@ __device__ __forceinline__ void cc_store(double2 (&x)[P], const double2* __restr
   }
 }
 
-// hook: called by every thread once the last stage has taken its inputs from
-// the tile (behind that stage's barrier): the tile's shared memory is free
-// from there on, e.g. for staging the next tile.
-struct NoHook {
-  __device__ __forceinline__ void operator()() const {}
-};
+// hook (NoHook, fft_ct.cuh): called by every thread once the last stage has
+// taken its inputs from the tile (behind that stage's barrier): the tile's
+// shared memory is free from there on, e.g. for staging the next tile.
 template <bool INV, class SC, int S, int LOGC, int NTHR, int P, class Src, class Sink, class Hook = NoHook>
 __device__ __forceinline__ void cc_stages(double2 (&x)[P], double2* __restrict__ buf,
                                           const LayCols& lay, const double2* __restrict__ stab,

@@ -117,11 +117,17 @@ __device__ __forceinline__ void ct_store(double2 (&x)[16], const RowPair& lay,
 // writes sink, the others exchange through buf (RowPair layout).  toff and
 // qmul of each stage come from the plan (the inverse of a row pass reads the
 // forward table through the qmul mapping, plan.cu map_stages).
-template <bool INV, class SC, int S, int NTHR, class Src, class Sink, uint32_t TMUL = 1>
+// hook: called by every thread of a half once the last stage has taken its
+// inputs (behind that stage's barrier of the half): the half's row buffer is
+// free from there on.
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+template <bool INV, class SC, int S, int NTHR, class Src, class Sink, uint32_t TMUL = 1, class Hook = NoHook>
 __device__ __forceinline__ void ct_stages(double2 (&x)[16], double2* __restrict__ buf,
                                           const RowPair& lay, const double2* __restrict__ stab,
                                           const SubFft& p, const Src& src, const Sink& sink,
-                                          int tid) {
+                                          int tid, const Hook& hook = Hook{}) {
   constexpr int RAD = SC::rad(S);
   constexpr uint32_t NS = SC::ns(S);
   constexpr uint32_t R = SC::R;
@@ -134,12 +140,13 @@ __device__ __forceinline__ void ct_stages(double2 (&x)[16], double2* __restrict_
   ct_sync<NTHR>(tid);
   const double2* st = stab + p.toff[S];
   if constexpr (last) {
+    hook();
     ct_store<RAD, INV, R, NS, NTHR, Sink, TMUL>(x, lay, st, p.qmul[S], sink, tid);
   } else {
     ct_store<RAD, INV, R, NS, NTHR, SmemSink<RowPair>, TMUL>(x, lay, st, p.qmul[S], SmemSink<RowPair>{buf, lay},
                                                              tid);
     ct_sync<NTHR>(tid);
-    ct_stages<INV, SC, S + 1, NTHR, Src, Sink, TMUL>(x, buf, lay, stab, p, src, sink, tid);
+    ct_stages<INV, SC, S + 1, NTHR, Src, Sink, TMUL, Hook>(x, buf, lay, stab, p, src, sink, tid, hook);
   }
 }
 
