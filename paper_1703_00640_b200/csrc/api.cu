@@ -653,8 +653,12 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
         // waits stay short, and a launch is saved (2^20 low 57.9 -> 55.3 us);
         // beyond, blocks that wait for a predecessor hold their slots, and the
         // second kernel costs less (2^26 low 271.6 against 278.0 us)
+        // (the full product, whose runs have no post-map, takes the runs kernel
+        // from 1.5 M coefficients: 2^24 full 18.8 -> 14.8 us; the truncated
+        // products' runs are too long a chain below a full wave of them)
+        const bool full_runs = p.mode == PMode::kFull && pl.K >= 1500000;
         const bool one = pt == 1 || cx.opt.carry_kernels == 1 ||
-                         (cx.opt.carry_kernels == 0 && blocks2 <= unsigned(4 * cx.num_sms));
+                         (cx.opt.carry_kernels == 0 && blocks2 <= unsigned(4 * cx.num_sms) && !full_runs);
         CarryLanesFn lbk = one ? carry_lb_kernel(lam, pt) : nullptr;
         if (lbk) {
           // one kernel: the carry-in by decoupled look-back, every limb written once
