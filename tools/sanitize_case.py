@@ -10,7 +10,9 @@ runs split and runs carry (2^24 and above) and, with max_log2n >= 28, the
 three-pass plans.  Both parameter policies, a small batch through the fused
 kernel and through graph-replayed multi-pass products, and ragged sizes.
 Every result is checked against the exact product (oracle), so a run under
-the sanitizer is also a parity run.
+the sanitizer is also a parity run; where the sanitizer is unavailable (it
+is closed on the round's GPU pool) the script alone is a parity run over
+every plan family.
 """
 import os
 import sys
