@@ -122,6 +122,36 @@ int main() {
               static_cast<long long>(n), ctx.last_stats().max_round_err,
               ctx.last_stats().max_round_err);
 
+  // the machine-word splitters (products.hpp:77-79): the reference's documented
+  // examples (test_products.cpp:52-78), and a low split of u reassembled
+  {
+    tb::Params sp;
+    sp.n = 6; sp.b = 2; sp.N = 3; sp.mode = tb::Mode::kFull; sp.backend = tb::Backend::kExact;
+    sp.signed_split = false;  // like the reference tests' manual_params
+    const std::vector<std::int64_t> w = ctx.split_low_i64(tb::Limbs{13}, sp);
+    CHECK(w.size() == 3 && w[0] == 1 && w[1] == 3 && w[2] == 0);
+    tb::Params hp;
+    hp.n = 10; hp.b = 4; hp.N = 3; hp.mode = tb::Mode::kHigh; hp.backend = tb::Backend::kExact;
+    hp.signed_split = false;
+    const std::vector<std::int64_t> h = tb::split_high_i64(tb::Limbs{1023}, hp);
+    CHECK(h.size() == 4 && h[0] == 0 && h[1] == 12 && h[2] == 15 && h[3] == 15);
+    const std::vector<std::int64_t> z = ctx.split_low_i64(u, pl);
+    CHECK(static_cast<std::int64_t>(z.size()) == pl.N);
+    // sum_i z_i 2^{i b} == u, accumulated limb by limb with signed carries
+    tb::Limbs back(nl + 1, 0);
+    for (size_t i = 0; i < z.size(); ++i) {
+      const std::int64_t pos = static_cast<std::int64_t>(i) * pl.b;
+      __int128 val = static_cast<__int128>(z[i]) << (pos & 63);
+      for (size_t m = static_cast<size_t>(pos >> 6); m <= nl && val != 0; ++m) {
+        const __int128 t = static_cast<__int128>(back[m]) + static_cast<std::uint64_t>(val);
+        back[m] = static_cast<std::uint64_t>(t);
+        val = (val >> 64) + static_cast<__int128>(t >> 64);
+      }
+    }
+    for (size_t i = 0; i < nl; ++i) CHECK(back[i] == u[i]);
+    std::printf("splits OK\n");
+  }
+
   // the reference's exceptions
   threw = false;
   try {

@@ -140,6 +140,20 @@ int tmg_product_batched(tmg_context* ctx, const tmg_params* params,
                         const uint64_t* u, const uint64_t* v, int64_t count,
                         uint64_t* out, uint32_t* flags_out, tmg_stats* stats);
 
+/* ---- the splitters on their own (products.hpp:68-79, split.cpp:147-158) ----
+ * split_low_i64: out receives params->N chunks of params->b bits of u
+ * (ceil(n/64) host limbs), u = sum_i out[i] 2^{i b}; with signed_split the
+ * chunks below the top lie in (-2^{b-1}, 2^{b-1}] and the top one absorbs the
+ * carries.  split_high_i64: the N + 1 chunks of u 2^sigma,
+ * sigma = (N + 1) b - n (top-aligned; needs (N+1) b >= n + lg N + 2).
+ * Only n, b, N and signed_split of params are read, like the reference.
+ * TMG_ERR_INPUT_OUT_OF_RANGE with the reference's messages for b > 62, a
+ * covering violation, or an operand outside [0, 2^n). */
+int tmg_split_low_i64(tmg_context* ctx, const tmg_params* params,
+                      const uint64_t* u, int64_t* out);
+int tmg_split_high_i64(tmg_context* ctx, const tmg_params* params,
+                       const uint64_t* u, int64_t* out);
+
 /* ---- device-resident variants (enqueue only; no host synchronisation) ----
  * d_u, d_v, d_out are device pointers.  Errors detected on the device are
  * reported by the next tmg_check(). */

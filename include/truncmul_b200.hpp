@@ -190,6 +190,15 @@ class Context {
     return run(tmg_high_product, Mode::kHigh, u, v, p);
   }
 
+  // The machine-word splitters (products.hpp:77-79): N chunks of u, or the
+  // N + 1 chunks of the top-aligned u 2^sigma, sigma = (N + 1) b - n.
+  std::vector<std::int64_t> split_low_i64(const Limbs& u, const Params& p) {
+    return split(tmg_split_low_i64, u, p, p.N);
+  }
+  std::vector<std::int64_t> split_high_i64(const Limbs& u, const Params& p) {
+    return split(tmg_split_high_i64, u, p, p.N + 1);
+  }
+
   // Device-pointer variant: enqueue `count` products on the context stream;
   // device-side errors surface at the next check().
   void product_device(const Params& p, const std::uint64_t* d_u, const std::uint64_t* d_v,
@@ -218,6 +227,16 @@ class Context {
     return out;
   }
 
+  using SplitFn = int (*)(tmg_context*, const tmg_params*, const std::uint64_t*, std::int64_t*);
+  std::vector<std::int64_t> split(SplitFn fn, const Limbs& u, const Params& p, std::int64_t count) {
+    if (p.n >= 1 && static_cast<std::int64_t>(u.size()) != (p.n + 63) / 64)
+      throw InputOutOfRange("operands must hold ceil(n/64) limbs");
+    std::vector<std::int64_t> out(static_cast<size_t>(count > 0 ? count : 0));
+    const tmg_params q = p.to_c();
+    check(fn(h_, &q, u.data(), out.data()));
+    return out;
+  }
+
   tmg_context* h_ = nullptr;
   Stats stats_{};
 };
@@ -237,4 +256,10 @@ inline Limbs high_product(const Limbs& u, const Limbs& v, const Params& p) {
   return default_context().high_product(u, v, p);
 }
 
+inline std::vector<std::int64_t> split_low_i64(const Limbs& u, const Params& p) {
+  return default_context().split_low_i64(u, p);
+}
+inline std::vector<std::int64_t> split_high_i64(const Limbs& u, const Params& p) {
+  return default_context().split_high_i64(u, p);
+}
 }  // namespace truncmul_b200

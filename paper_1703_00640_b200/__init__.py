@@ -34,6 +34,8 @@ from .products import (  # noqa: F401
     predicted_sigma,
     required_precision,
     select_params,
+    split_high_i64,
+    split_low_i64,
     to_limbs,
     validate_params,
 )

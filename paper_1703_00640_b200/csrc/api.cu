@@ -1157,6 +1157,45 @@ int host_product(Context& cx, const Params& p, int32_t want_mode,
   }
 }
 
+// split_low_i64 / split_high_i64 (products.hpp:68-79): the chunks of one host
+// operand as int64 words.  The shape checks and their messages follow
+// split.cpp:104-158 (check_low_shape / check_high_shape, check_operand,
+// chunk_store's b <= 62).
+int split_i64_host(Context& cx, const Params& p, bool high, const uint64_t* u, int64_t* out) {
+  if (p.b < 1 || p.N < (high ? 2 : 1))
+    throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "split: chunk width and count must be positive");
+  if (!high && p.N * int64_t(p.b) < p.n)
+    throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "split: N b >= n is required");
+  if (high && (p.N + 1) * int64_t(p.b) < p.n + lg_ceil(uint64_t(p.N)) + 2)
+    throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "split: (N+1) b >= n + lg N + 2 is required");
+  if (p.n < 1) throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "split: bit length must be positive");
+  if (p.b > 62)
+    throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "split: chunk width too large for int64 chunks");
+  const int64_t count = high ? p.N + 1 : p.N;
+  const int64_t lead = high ? (p.N + 1) * int64_t(p.b) - p.n : 0;
+  const int64_t nl = (p.n + 63) / 64;
+  TMG_CUDA(cudaSetDevice(cx.device));
+  cx.dop_u.ensure(size_t(nl) * 8 + 8);
+  cx.dop_out.ensure(size_t(count) * 8 + 8);
+  cx.pflags.ensure(8);
+  TMG_CUDA(cudaMemsetAsync(cx.pflags.p, 0, 4, cx.stream));
+  TMG_CUDA(cudaMemcpyAsync(cx.dop_u.p, u, size_t(nl) * 8, cudaMemcpyHostToDevice, cx.stream));
+  {
+    KTimer kt(cx, "k_split_i64", double(nl) * 8.0 + double(count) * 8.0);
+    launch_split_i64(cx.dop_u.as<uint64_t>(), nl, p.n, p.b, count, p.signed_split, lead,
+                     cx.dop_out.as<int64_t>(), cx.pflags.as<uint32_t>(), cx.stream);
+  }
+  TMG_CUDA(cudaGetLastError());
+  uint32_t flags = 0;
+  TMG_CUDA(cudaMemcpyAsync(out, cx.dop_out.p, size_t(count) * 8, cudaMemcpyDeviceToHost, cx.stream));
+  TMG_CUDA(cudaMemcpyAsync(&flags, cx.pflags.p, 4, cudaMemcpyDeviceToHost, cx.stream));
+  TMG_CUDA(cudaStreamSynchronize(cx.stream));
+  cx.last_kernels = 1;
+  if (flags & kFlagInputRange)
+    throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "split: operand outside [0, 2^n)");
+  return TMG_OK;
+}
+
 template <class F>
 int guarded(F&& f) {
   try {
@@ -1285,6 +1324,16 @@ int tmg_product_batched(tmg_context* ctx, const tmg_params* params, const uint64
     const int32_t m = q.mode == PMode::kOracleFallback ? TMG_MODE_FULL : int32_t(q.mode);
     return host_product(ctx->cx, q, m, u, v, count, out, flags_out, stats);
   });
+}
+
+int tmg_split_low_i64(tmg_context* ctx, const tmg_params* params, const uint64_t* u,
+                      int64_t* out) {
+  return guarded([&] { return split_i64_host(ctx->cx, from_c(params), false, u, out); });
+}
+
+int tmg_split_high_i64(tmg_context* ctx, const tmg_params* params, const uint64_t* u,
+                       int64_t* out) {
+  return guarded([&] { return split_i64_host(ctx->cx, from_c(params), true, u, out); });
 }
 
 int tmg_product_device(tmg_context* ctx, const tmg_params* params, const uint64_t* d_u,

@@ -320,4 +320,10 @@ struct BaseArgs {
 };
 __global__ void k_basecase(BaseArgs a);
 
+// The reference's int64 splitters as an entry point of their own
+// (k_split_i64.cu; products.hpp:68-79).
+void launch_split_i64(const uint64_t* d_limbs, int64_t nlimbs, int64_t n, int b, int64_t count,
+                      bool balanced, int64_t lead, int64_t* d_out, uint32_t* d_flags,
+                      cudaStream_t st);
+
 }  // namespace tmg

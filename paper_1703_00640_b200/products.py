@@ -310,6 +310,22 @@ class Context:
         self._stats(st)
         return (out, flags) if return_flags else out
 
+    def split_i64(self, u, params: Params, high: bool = False) -> np.ndarray:
+        """The chunks of one operand as int64 words (split_low_i64 /
+        split_high_i64, products.hpp:77-79): N of them, or the N + 1 chunks
+        of the top-aligned u 2^sigma.  u: exactly ceil(n/64) limbs; the range
+        check u < 2^n runs on the device."""
+        ul = np.ascontiguousarray(u, dtype=np.uint64)
+        if params.n >= 1 and len(ul) != (params.n + 63) // 64:
+            raise InputOutOfRange("operands must hold ceil(n/64) limbs")
+        count = params.N + 1 if high else params.N
+        out = np.zeros(max(count, 0), dtype=np.int64)
+        c = params.to_c()
+        fn = self._lib.tmg_split_high_i64 if high else self._lib.tmg_split_low_i64
+        _check(fn(self._h, ctypes.byref(c), ul.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+        return out
+
     def product_device(self, params: Params, d_u: int, d_v: int, d_out: int, count: int = 1):
         """Enqueue on device pointers (ints); no synchronisation."""
         c = params.to_c()
@@ -390,6 +406,21 @@ def low_product(u, v, params: Params, ctx: Context | None = None) -> int:
 def high_product(u, v, params: Params, ctx: Context | None = None) -> int:
     """w with |u v - 2^n w| < 2^n, 0 <= w <= 2^n (Alg. 3, products.hpp:93)."""
     return from_limbs(high_product_limbs(u, v, params, ctx))
+
+
+def split_low_i64(u, params: Params, ctx: Context | None = None) -> np.ndarray:
+    """u = sum_i chunk_i 2^{i b}, N chunks (products.hpp:77; balanced below the
+    top chunk when params.signed_split)."""
+    if params.n < 1:
+        raise InputOutOfRange("split: bit length must be positive")
+    return (ctx or default_context()).split_i64(to_limbs(u, params.n), params, high=False)
+
+
+def split_high_i64(u, params: Params, ctx: Context | None = None) -> np.ndarray:
+    """The N + 1 chunks of u 2^sigma, sigma = (N + 1) b - n (products.hpp:78-79)."""
+    if params.n < 1:
+        raise InputOutOfRange("split: bit length must be positive")
+    return (ctx or default_context()).split_i64(to_limbs(u, params.n), params, high=True)
 
 
 def multiply(mode: Mode, u, v, n: int | None = None, backend: Backend = Backend.FFT,
