@@ -140,6 +140,17 @@ int tmg_product_batched(tmg_context* ctx, const tmg_params* params,
                         const uint64_t* u, const uint64_t* v, int64_t count,
                         uint64_t* out, uint32_t* flags_out, tmg_stats* stats);
 
+/* ---- the FP64 cyclic convolution on its own (convolution.hpp:64-67,
+ * cyclic_convolve_f64 on an FFT plan of length n: make_plan(n, p, kFft)) ----
+ * out[k] = sum_j f[j] g[(k - j) mod n] for host arrays of n doubles; out may
+ * not alias f or g.  n must be {2,3,5,7}-smooth (TMG_ERR_UNSUPPORTED_LENGTH
+ * with make_plan's message otherwise, convolution.cpp:92-105).  Lengths above
+ * 4096 run the products' transform passes and must be multiples of 4 (every
+ * length select_params picks is); shorter ones, and other lengths up to
+ * 32768, are summed directly. */
+int tmg_cyclic_convolve_f64(tmg_context* ctx, int64_t n, const double* f,
+                            const double* g, double* out);
+
 /* ---- the splitters on their own (products.hpp:68-79, split.cpp:147-158) ----
  * split_low_i64: out receives params->N chunks of params->b bits of u
  * (ceil(n/64) host limbs), u = sum_i out[i] 2^{i b}; with signed_split the

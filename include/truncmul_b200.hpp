@@ -190,6 +190,17 @@ class Context {
     return run(tmg_high_product, Mode::kHigh, u, v, p);
   }
 
+  // FP64 cyclic convolution of two sequences of one {2,3,5,7}-smooth length
+  // (cyclic_convolve_f64 on an FFT plan, convolution.hpp:64-67)
+  std::vector<double> cyclic_convolve_f64(const std::vector<double>& f,
+                                          const std::vector<double>& g) {
+    if (f.size() != g.size()) throw PlanMismatch("cyclic_convolve_f64: operand lengths differ");
+    std::vector<double> out(f.size());
+    check(tmg_cyclic_convolve_f64(h_, static_cast<std::int64_t>(f.size()), f.data(), g.data(),
+                                  out.data()));
+    return out;
+  }
+
   // The machine-word splitters (products.hpp:77-79): N chunks of u, or the
   // N + 1 chunks of the top-aligned u 2^sigma, sigma = (N + 1) b - n.
   std::vector<std::int64_t> split_low_i64(const Limbs& u, const Params& p) {
@@ -256,6 +267,10 @@ inline Limbs high_product(const Limbs& u, const Limbs& v, const Params& p) {
   return default_context().high_product(u, v, p);
 }
 
+inline std::vector<double> cyclic_convolve_f64(const std::vector<double>& f,
+                                               const std::vector<double>& g) {
+  return default_context().cyclic_convolve_f64(f, g);
+}
 inline std::vector<std::int64_t> split_low_i64(const Limbs& u, const Params& p) {
   return default_context().split_low_i64(u, p);
 }

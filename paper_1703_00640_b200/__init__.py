@@ -19,6 +19,7 @@ from .products import (  # noqa: F401
     Stats,
     Unsupported,
     UnsupportedLength,
+    cyclic_convolve_f64,
     default_context,
     default_lambda,
     from_limbs,

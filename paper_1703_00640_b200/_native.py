@@ -115,6 +115,8 @@ def load():
         getattr(L, name).argtypes = [vp, P(tmg_params), u64p, u64p, u64p, P(tmg_stats)]
     L.tmg_product_batched.argtypes = [vp, P(tmg_params), u64p, u64p, i64, u64p,
                                       P(ctypes.c_uint32), P(tmg_stats)]
+    L.tmg_cyclic_convolve_f64.argtypes = [vp, i64, P(ctypes.c_double), P(ctypes.c_double),
+                                          P(ctypes.c_double)]
     for name in ("tmg_split_low_i64", "tmg_split_high_i64"):
         getattr(L, name).argtypes = [vp, P(tmg_params), u64p, P(ctypes.c_int64)]
     L.tmg_product_device.argtypes = [vp, P(tmg_params), vp, vp, vp, i64]

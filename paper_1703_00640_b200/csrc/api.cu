@@ -6,6 +6,7 @@
 //   products_f64.cpp:16-27 and 137-169 reported through a device status word.
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -179,6 +180,9 @@ struct Context {
   void drained() {}
   int32_t last_passes = 0;
 
+  // plans of the stand-alone convolution, by length (tmg_cyclic_convolve_f64)
+  std::map<int64_t, std::unique_ptr<Plan>> conv_plans;
+
   Plan& plan_for(const Params& p) {
     auto key = std::make_tuple(p.n, p.b, p.N, p.lambda, int32_t(p.mode), p.p, int32_t(p.backend),
                                int32_t(p.signed_split));
@@ -324,123 +328,22 @@ void ensure_workspace(Workspace& w, const Plan& pl) {
   w.aux.ensure(64);
 }
 
-// One multi-pass product on stream st with workspace w; device flags,
-// residuals and the high product's range words go to status.  Returns the
-// number of kernels launched.
-int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* status, Plan& pl,
-                    const uint64_t* u, const uint64_t* v, uint64_t* out) {
+// The transform passes of one product or convolution: first column pass
+// (reading z), the middle column passes of three-pass plans, the row pass
+// with the spectral product, and the inverse column passes, which leave the
+// convolution coefficients in w.work_c.  Returns the kernels launched.
+// out_scale (a power of two) multiplies the coefficients on their way out.
+int enqueue_fft_passes(Context& cx, Workspace& w, cudaStream_t st, Plan& pl, const uint64_t* u,
+                       const uint64_t* v, bool z_natural, double out_scale = 1.0) {
   const Params& p = pl.params;
   const int64_t L = pl.L;
   int kernels = 0;
   {
-    // balanced split + pre-map (both operands)
-    {
-      ZgenArgs a;
-      a.u = u;
-      a.v = v;
-      a.nlimbs = pl.nlimbs;
-      a.n = p.n;
-      a.b = p.b;
-      a.count = pl.count;
-      a.N = p.N;
-      a.lead = pl.lead;
-      a.cbits_u = w.cbu.as<uint32_t>();
-      a.cbits_v = w.cbv.as<uint32_t>();
-      a.z = w.work_z.as<double2>();
-      a.mc = pl.mc;
-      a.zt = ztile(pl, L, cx.opt.z_natural);
-      a.status = status;
-      if (!w.gen.p) {
-        w.gen.ensure(64);
-        TMG_CUDA(cudaMemsetAsync(w.gen.p, 0, 64, st));
-      }
-      a.gen = w.gen.as<uint32_t>();
-      a.lbstate = nullptr;
-      a.aggs = nullptr;
-      a.early = 0;
-      // Split by runs (k_zsplit): every thread finds its carry-in from the
-      // window below its run, so there are no aggregates and no look-back.
-      // Digit form, balanced split, compiled chunk widths, runs inside one
-      // row of z's tiles; TMG_OPT_SPLIT_KERNEL 1 keeps k_zgen.
-      ZgenFn zs = nullptr;
-      {
-        const uint32_t ncols = a.zt.fdcols.d;
-        const int minlog = pl.zdig == 1 ? 2 : 1;
-        if (pl.f1d && pl.mc.balanced && !cx.opt.zstat_split && !cx.opt.old_split && pl.count < (int64_t(1) << 31) &&
-            (a.zt.natural || (ncols % 32 == 0 && int(a.zt.logc) >= minlog)) &&
-            pl.count >= int64_t(zsplit_chunks()) * cx.num_sms / 2)
-          zs = zsplit_kernel(int(p.b), pl.zdig);
-      }
-      if (zs) {
-        // blocks of 8 rows by 1024 columns of z's tiles (a warp's 16-byte
-        // digit pieces then fill whole lines), or of 8192 consecutive chunks
-        const uint32_t ncols = a.zt.fdcols.d;
-        const int64_t zch = zsplit_chunks();
-        a.zs_rb = (!a.zt.natural && ncols % uint32_t(zch / 8) == 0) ? 8 : 1;
-        unsigned blocks = unsigned((pl.count + zch - 1) / zch);
-        if (a.zs_rb == 8) {
-          const int64_t rows = (pl.count + ncols - 1) / ncols;
-          blocks = unsigned(((rows + 7) / 8) * (ncols / uint32_t(zch / 8)));
-        }
-        const size_t zsm = zsplit_smem(int(p.b));
-        set_smem(zs, zsm);
-        {
-          KTimer kt(cx, "k_zsplit", double(2 * pl.nlimbs) * 8.0 + double(p.N) * (pl.zdig == 1 ? 4.0 : 8.0), int(p.mode), st);
-          launch(cx, zs, dim3(blocks), dim3(256), zsm, st, a, "zgen");
-        }
-        check_launch(cx, "k_zsplit");
-        ++kernels;
-      } else {
-      // chunks per thread of the split: 16, or 4 / 1 when the blocks of 16
-      // would not fill the GPU twice (mid-size products are latency-bound
-      // per block)
-      int per = 16;  // (the 64-bit window path, b > 32, has only this one)
-      if (p.b <= 32 && (pl.count + 16 * kZgenThreads - 1) / (16 * kZgenThreads) < 2 * cx.num_sms) per = 4;
-      if (per == 4 && (pl.count + 4 * kZgenThreads - 1) / (4 * kZgenThreads) < 2 * cx.num_sms) per = 1;
-      a.bchunks = per * kZgenThreads;
-      const unsigned blocks = unsigned((pl.count + a.bchunks - 1) / a.bchunks);
-      w.zaggs.ensure(size_t(blocks) * 4 + 16);
-      a.aggs = w.zaggs.as<uint32_t>();
-      a.early = cx.zstat_early ? 1 : 0;
-      // the split blocks take their carry-ins by a look-back inside k_zgen
-      // (no k_zstat launch): a block's aggregate is published early (after
-      // its windows), and its predecessor was dispatched before it, so the
-      // waits are short (2^26 low 271.4 -> 267.2 us, 2^24 high 104.2 -> 101.1);
-      // TMG_OPT_SPLIT_AGGREGATES composes k_zstat's aggregates instead
-      const bool zlb = !cx.opt.zstat_split;
-      if (zlb) {
-        if (w.zlb.bytes < size_t(blocks) * 8) {
-          w.zlb.ensure(size_t(blocks) * 8);
-          TMG_CUDA(cudaMemsetAsync(w.zlb.p, 0, w.zlb.bytes, st));
-        }
-        a.lbstate = w.zlb.as<unsigned long long>();
-      } else {
-        {
-          KTimer kt(cx, "k_zstat", double(2 * pl.nlimbs) * 8.0, int(p.mode), st);
-          launch(cx, k_zstat, dim3((blocks + 255) / 256), dim3(256), 0, st, a, "zstat");
-        }
-        check_launch(cx, "k_zstat");
-        ++kernels;
-      }
-      // with k_f1d_ct the split stores digits and the first column pass pre-maps
-      ZgenFn zg = pl.f1d ? zgen_digits_kernel(int(p.b), pl.zdig, per)
-                         : zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda), per);
-      const double zbytes = pl.f1d ? (pl.zdig == 1 ? 4.0 : 8.0) : 16.0;
-      const size_t zsm = zgen_smem(int(p.b), per);
-      set_smem(zg, zsm);
-      {
-        KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * zbytes, int(p.mode), st);
-        launch(cx, zg, dim3(blocks), dim3(kZgenThreads), zsm, st, a, "zgen");
-      }
-      check_launch(cx, "k_zgen");
-      ++kernels;
-      }
-    }
     double2* T = w.work_t.as<double2>();
     {
       F1Args a;
       a.z = w.work_z.as<double2>();
-      a.zt = ztile(pl, L, cx.opt.z_natural);
+      a.zt = ztile(pl, L, z_natural);
       a.out = T;
       a.ncols = uint32_t(L / pl.A);
       a.logc = pl.logc_f1;
@@ -568,6 +471,8 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       a.logc = pl.logc_il;
       a.fft = pl.iA;
       spectral_scale(L, &a.scale, &a.scale_lo);
+      a.scale *= out_scale;
+      a.scale_lo *= out_scale;
       auto ilk = pl.colct_il ? pl.colct_il->ilast : pl.colpp ? k_ilast_pp : k_ilast;
       set_smem(ilk, pl.smem_il);
       {
@@ -582,6 +487,124 @@ int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* statu
       check_launch(cx, "k_ilast");
       ++kernels;
     }
+  }
+  return kernels;
+}
+
+// One multi-pass product on stream st with workspace w; device flags,
+// residuals and the high product's range words go to status.  Returns the
+// number of kernels launched.
+int enqueue_product(Context& cx, Workspace& w, cudaStream_t st, DevStatus* status, Plan& pl,
+                    const uint64_t* u, const uint64_t* v, uint64_t* out) {
+  const Params& p = pl.params;
+  const int64_t L = pl.L;
+  int kernels = 0;
+  {
+    // balanced split + pre-map (both operands)
+    {
+      ZgenArgs a;
+      a.u = u;
+      a.v = v;
+      a.nlimbs = pl.nlimbs;
+      a.n = p.n;
+      a.b = p.b;
+      a.count = pl.count;
+      a.N = p.N;
+      a.lead = pl.lead;
+      a.cbits_u = w.cbu.as<uint32_t>();
+      a.cbits_v = w.cbv.as<uint32_t>();
+      a.z = w.work_z.as<double2>();
+      a.mc = pl.mc;
+      a.zt = ztile(pl, L, cx.opt.z_natural);
+      a.status = status;
+      if (!w.gen.p) {
+        w.gen.ensure(64);
+        TMG_CUDA(cudaMemsetAsync(w.gen.p, 0, 64, st));
+      }
+      a.gen = w.gen.as<uint32_t>();
+      a.lbstate = nullptr;
+      a.aggs = nullptr;
+      a.early = 0;
+      // Split by runs (k_zsplit): every thread finds its carry-in from the
+      // window below its run, so there are no aggregates and no look-back.
+      // Digit form, balanced split, compiled chunk widths, runs inside one
+      // row of z's tiles; TMG_OPT_SPLIT_KERNEL 1 keeps k_zgen.
+      ZgenFn zs = nullptr;
+      {
+        const uint32_t ncols = a.zt.fdcols.d;
+        const int minlog = pl.zdig == 1 ? 2 : 1;
+        if (pl.f1d && pl.mc.balanced && !cx.opt.zstat_split && !cx.opt.old_split && pl.count < (int64_t(1) << 31) &&
+            (a.zt.natural || (ncols % 32 == 0 && int(a.zt.logc) >= minlog)) &&
+            pl.count >= int64_t(zsplit_chunks()) * cx.num_sms / 2)
+          zs = zsplit_kernel(int(p.b), pl.zdig);
+      }
+      if (zs) {
+        // blocks of 8 rows by 1024 columns of z's tiles (a warp's 16-byte
+        // digit pieces then fill whole lines), or of 8192 consecutive chunks
+        const uint32_t ncols = a.zt.fdcols.d;
+        const int64_t zch = zsplit_chunks();
+        a.zs_rb = (!a.zt.natural && ncols % uint32_t(zch / 8) == 0) ? 8 : 1;
+        unsigned blocks = unsigned((pl.count + zch - 1) / zch);
+        if (a.zs_rb == 8) {
+          const int64_t rows = (pl.count + ncols - 1) / ncols;
+          blocks = unsigned(((rows + 7) / 8) * (ncols / uint32_t(zch / 8)));
+        }
+        const size_t zsm = zsplit_smem(int(p.b));
+        set_smem(zs, zsm);
+        {
+          KTimer kt(cx, "k_zsplit", double(2 * pl.nlimbs) * 8.0 + double(p.N) * (pl.zdig == 1 ? 4.0 : 8.0), int(p.mode), st);
+          launch(cx, zs, dim3(blocks), dim3(256), zsm, st, a, "zgen");
+        }
+        check_launch(cx, "k_zsplit");
+        ++kernels;
+      } else {
+      // chunks per thread of the split: 16, or 4 / 1 when the blocks of 16
+      // would not fill the GPU twice (mid-size products are latency-bound
+      // per block)
+      int per = 16;  // (the 64-bit window path, b > 32, has only this one)
+      if (p.b <= 32 && (pl.count + 16 * kZgenThreads - 1) / (16 * kZgenThreads) < 2 * cx.num_sms) per = 4;
+      if (per == 4 && (pl.count + 4 * kZgenThreads - 1) / (4 * kZgenThreads) < 2 * cx.num_sms) per = 1;
+      a.bchunks = per * kZgenThreads;
+      const unsigned blocks = unsigned((pl.count + a.bchunks - 1) / a.bchunks);
+      w.zaggs.ensure(size_t(blocks) * 4 + 16);
+      a.aggs = w.zaggs.as<uint32_t>();
+      a.early = cx.zstat_early ? 1 : 0;
+      // the split blocks take their carry-ins by a look-back inside k_zgen
+      // (no k_zstat launch): a block's aggregate is published early (after
+      // its windows), and its predecessor was dispatched before it, so the
+      // waits are short (2^26 low 271.4 -> 267.2 us, 2^24 high 104.2 -> 101.1);
+      // TMG_OPT_SPLIT_AGGREGATES composes k_zstat's aggregates instead
+      const bool zlb = !cx.opt.zstat_split;
+      if (zlb) {
+        if (w.zlb.bytes < size_t(blocks) * 8) {
+          w.zlb.ensure(size_t(blocks) * 8);
+          TMG_CUDA(cudaMemsetAsync(w.zlb.p, 0, w.zlb.bytes, st));
+        }
+        a.lbstate = w.zlb.as<unsigned long long>();
+      } else {
+        {
+          KTimer kt(cx, "k_zstat", double(2 * pl.nlimbs) * 8.0, int(p.mode), st);
+          launch(cx, k_zstat, dim3((blocks + 255) / 256), dim3(256), 0, st, a, "zstat");
+        }
+        check_launch(cx, "k_zstat");
+        ++kernels;
+      }
+      // with k_f1d_ct the split stores digits and the first column pass pre-maps
+      ZgenFn zg = pl.f1d ? zgen_digits_kernel(int(p.b), pl.zdig, per)
+                         : zgen_kernel(int(p.b), p.mode == PMode::kFull ? 0 : int(pl.mc.lambda), per);
+      const double zbytes = pl.f1d ? (pl.zdig == 1 ? 4.0 : 8.0) : 16.0;
+      const size_t zsm = zgen_smem(int(p.b), per);
+      set_smem(zg, zsm);
+      {
+        KTimer kt(cx, "k_zgen", double(2 * pl.nlimbs) * 8.0 + double(p.N) * zbytes, int(p.mode), st);
+        launch(cx, zg, dim3(blocks), dim3(kZgenThreads), zsm, st, a, "zgen");
+      }
+      check_launch(cx, "k_zgen");
+      ++kernels;
+      }
+    }
+    kernels += enqueue_fft_passes(cx, w, st, pl, u, v, cx.opt.z_natural);
+    double2* coef = w.work_c.as<double2>();
     // high: k_carry_lanes and k_carry_patch nominate the limb that stops the
     // rounding increment (else k_high_agg does, after the single-pass k_carry)
     bool high_stop_fused = false;
@@ -1157,6 +1180,117 @@ int host_product(Context& cx, const Params& p, int32_t want_mode,
   }
 }
 
+// cyclic_convolve_f64 (convolution.hpp:64-67): out = f (*) g, cyclic of length
+// n, host arrays.  The length checks and messages follow make_plan
+// (convolution.cpp:92-105).  Lengths above 4096 that are multiples of 4 run
+// the products' transform passes on a plan of their own (a low-product shape
+// with N = L whose z is read as is: no pre-map in the first column pass, and
+// the passes end at the convolution coefficients); the others are summed
+// directly.
+constexpr int64_t kConvDirectMax = 4096;       // direct below the multi-pass plans
+constexpr int64_t kConvDirectMaxOdd = 32768;   // direct for lengths the passes do not take
+int conv_f64_host(Context& cx, int64_t n, const double* f, const double* g, double* out) {
+  if (n < 1) throw Error(TMG_ERR_UNSUPPORTED_LENGTH, "make_plan: length must be positive");
+  if (!is_2357_smooth(uint64_t(n)))
+    throw Error(TMG_ERR_UNSUPPORTED_LENGTH,
+                "make_plan: FFT backend needs a {2,3,5,7}-smooth length, got " + std::to_string(n));
+  const bool direct = n <= kConvDirectMax || (n % 4 != 0 && n <= kConvDirectMaxOdd);
+  if (!direct && n % 4 != 0)
+    throw Error(TMG_ERR_UNSUPPORTED_LENGTH,
+                "cyclic_convolve_f64: GPU transform lengths above " +
+                    std::to_string(kConvDirectMaxOdd) + " must be multiples of 4, got " +
+                    std::to_string(n));
+  TMG_CUDA(cudaSetDevice(cx.device));
+  cx.dop_u.ensure(size_t(n) * 8 + 16);
+  cx.dop_v.ensure(size_t(n) * 8 + 16);
+  TMG_CUDA(cudaMemcpyAsync(cx.dop_u.p, f, size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
+  TMG_CUDA(cudaMemcpyAsync(cx.dop_v.p, g, size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
+  const double* res = nullptr;
+  if (direct) {
+    cx.dop_out.ensure(size_t(n) * 8 + 16);
+    {
+      KTimer kt(cx, "k_conv_direct", double(n) * 24.0);
+      launch_conv_direct(cx.dop_u.as<double>(), cx.dop_v.as<double>(), n, cx.dop_out.as<double>(),
+                         cx.stream);
+    }
+    TMG_CUDA(cudaGetLastError());
+    cx.last_kernels = 1;
+    res = cx.dop_out.as<double>();
+  } else {
+    auto it = cx.conv_plans.find(n);
+    if (it == cx.conv_plans.end()) {
+      Params q;
+      q.mode = PMode::kLow;
+      q.backend = Backend::kFft;
+      q.b = 8;
+      q.N = n;
+      q.n = n * 8;
+      q.lambda = 1;  // one series row: the identity map
+      q.p = required_precision(PMode::kLow, q.b, q.N);
+      q.signed_split = true;
+      PlanOptions po;
+      po.premap_in_zgen = true;  // the first column pass reads 16-byte z entries as they are
+      po.z_natural = true;
+      std::unique_ptr<Plan> pl;
+      try {
+        pl = build_plan(q, cx.tw, po);
+      } catch (const Error& e) {
+        throw Error(TMG_ERR_UNSUPPORTED_LENGTH,
+                    std::string("cyclic_convolve_f64: no GPU plan for length ") +
+                        std::to_string(n) + " (" + e.what() + ")");
+      }
+      if (pl->kind < 2)
+        throw Error(TMG_ERR_INTERNAL, "cyclic_convolve_f64: expected a multi-pass plan");
+      it = cx.conv_plans.emplace(n, std::move(pl)).first;
+    }
+    Plan& pl = *it->second;
+    Workspace& w = cx.ws0;
+    ensure_workspace(w, pl);
+    if (!w.gen.p) {
+      w.gen.ensure(64);
+      TMG_CUDA(cudaMemsetAsync(w.gen.p, 0, 64, cx.stream));
+    }
+    // g times the power of two that brings max |g| to max |f| (k_conv.cu)
+    cx.pflags.ensure(16);
+    TMG_CUDA(cudaMemsetAsync(cx.pflags.p, 0, 16, cx.stream));
+    {
+      KTimer kt(cx, "k_conv_absmax", double(n) * 16.0);
+      launch_conv_absmax(cx.dop_u.as<double>(), cx.dop_v.as<double>(), n, cx.pflags.as<uint64_t>(),
+                         cx.num_sms, cx.stream);
+    }
+    TMG_CUDA(cudaGetLastError());
+    double mx[2] = {0.0, 0.0};
+    TMG_CUDA(cudaMemcpyAsync(mx, cx.pflags.p, 16, cudaMemcpyDeviceToHost, cx.stream));
+    TMG_CUDA(cudaStreamSynchronize(cx.stream));
+    if (mx[0] == 0.0 || mx[1] == 0.0) {
+      // a zero operand: the packed transform would return rounding noise of the other one
+      std::memset(out, 0, size_t(n) * 8);
+      cx.last_kernels = 1;
+      return TMG_OK;
+    }
+    double gs = 1.0;
+    if (std::isfinite(mx[0]) && std::isfinite(mx[1]) && mx[0] > 0.0 && mx[1] > 0.0) {
+      int ef = 0, eg = 0;
+      std::frexp(mx[0], &ef);
+      std::frexp(mx[1], &eg);
+      gs = std::ldexp(1.0, std::max(-500, std::min(500, ef - eg)));
+    }
+    {
+      KTimer kt(cx, "k_conv_pack", double(n) * 32.0);
+      launch_conv_pack(cx.dop_u.as<double>(), cx.dop_v.as<double>(), n, gs, w.work_z.as<double2>(),
+                       cx.stream);
+    }
+    TMG_CUDA(cudaGetLastError());
+    cx.last_kernels =
+        2 + enqueue_fft_passes(cx, w, cx.stream, pl, nullptr, nullptr, true, 1.0 / gs);
+    cx.last_L = pl.L;
+    res = w.work_c.as<double>();
+  }
+  TMG_CUDA(cudaMemcpyAsync(out, res, size_t(n) * 8, cudaMemcpyDeviceToHost, cx.stream));
+  TMG_CUDA(cudaStreamSynchronize(cx.stream));
+  return TMG_OK;
+}
+
 // split_low_i64 / split_high_i64 (products.hpp:68-79): the chunks of one host
 // operand as int64 words.  The shape checks and their messages follow
 // split.cpp:104-158 (check_low_shape / check_high_shape, check_operand,
@@ -1324,6 +1458,11 @@ int tmg_product_batched(tmg_context* ctx, const tmg_params* params, const uint64
     const int32_t m = q.mode == PMode::kOracleFallback ? TMG_MODE_FULL : int32_t(q.mode);
     return host_product(ctx->cx, q, m, u, v, count, out, flags_out, stats);
   });
+}
+
+int tmg_cyclic_convolve_f64(tmg_context* ctx, int64_t n, const double* f, const double* g,
+                            double* out) {
+  return guarded([&] { return conv_f64_host(ctx->cx, n, f, g, out); });
 }
 
 int tmg_split_low_i64(tmg_context* ctx, const tmg_params* params, const uint64_t* u,

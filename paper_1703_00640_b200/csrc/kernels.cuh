@@ -326,4 +326,12 @@ void launch_split_i64(const uint64_t* d_limbs, int64_t nlimbs, int64_t n, int b,
                       bool balanced, int64_t lead, int64_t* d_out, uint32_t* d_flags,
                       cudaStream_t st);
 
+// Stand-alone cyclic convolution (k_conv.cu; convolution.hpp:64-67).
+void launch_conv_absmax(const double* d_f, const double* d_g, int64_t n, uint64_t* d_mx,
+                        int num_sms, cudaStream_t st);
+void launch_conv_pack(const double* d_f, const double* d_g, int64_t n, double gscale,
+                      double2* d_z, cudaStream_t st);
+void launch_conv_direct(const double* d_f, const double* d_g, int64_t n, double* d_out,
+                        cudaStream_t st);
+
 }  // namespace tmg

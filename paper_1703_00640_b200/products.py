@@ -310,6 +310,20 @@ class Context:
         self._stats(st)
         return (out, flags) if return_flags else out
 
+    def cyclic_convolve_f64(self, f, g) -> np.ndarray:
+        """out[k] = sum_j f[j] g[(k - j) mod n] in FP64 (cyclic_convolve_f64 on an
+        FFT plan, convolution.hpp:64-67).  n must be {2,3,5,7}-smooth
+        (UnsupportedLength otherwise, like make_plan)."""
+        fa = np.ascontiguousarray(f, dtype=np.float64)
+        ga = np.ascontiguousarray(g, dtype=np.float64)
+        if fa.ndim != 1 or fa.shape != ga.shape:
+            raise PlanMismatch("cyclic_convolve_f64: operands must be two sequences of one length")
+        out = np.empty(len(fa), dtype=np.float64)
+        PD = ctypes.POINTER(ctypes.c_double)
+        _check(self._lib.tmg_cyclic_convolve_f64(self._h, len(fa), fa.ctypes.data_as(PD),
+                                                 ga.ctypes.data_as(PD), out.ctypes.data_as(PD)))
+        return out
+
     def split_i64(self, u, params: Params, high: bool = False) -> np.ndarray:
         """The chunks of one operand as int64 words (split_low_i64 /
         split_high_i64, products.hpp:77-79): N of them, or the N + 1 chunks
@@ -406,6 +420,12 @@ def low_product(u, v, params: Params, ctx: Context | None = None) -> int:
 def high_product(u, v, params: Params, ctx: Context | None = None) -> int:
     """w with |u v - 2^n w| < 2^n, 0 <= w <= 2^n (Alg. 3, products.hpp:93)."""
     return from_limbs(high_product_limbs(u, v, params, ctx))
+
+
+def cyclic_convolve_f64(f, g, ctx: Context | None = None) -> np.ndarray:
+    """FP64 cyclic convolution of two equally long sequences
+    (convolution.hpp:64-67)."""
+    return (ctx or default_context()).cyclic_convolve_f64(f, g)
 
 
 def split_low_i64(u, params: Params, ctx: Context | None = None) -> np.ndarray:
