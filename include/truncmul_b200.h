@@ -140,6 +140,25 @@ int tmg_product_batched(tmg_context* ctx, const tmg_params* params,
                         const uint64_t* u, const uint64_t* v, int64_t count,
                         uint64_t* out, uint32_t* flags_out, tmg_stats* stats);
 
+/* ---- the ring-change maps on their own (maps_f64.hpp: alpha_star_f64,
+ * beta_star_f64, gamma_dagger_f64, delta_dagger_f64 on the tables of
+ * build_map_tables_f64(N, b, lambda, ..); maps_f64.cpp:245-384) ----
+ * Host arrays of doubles.  alpha*: N -> N and beta*: N -> N (low product);
+ * gamma-dagger: N + 1 -> N, *aux receives the root channel, and
+ * delta-dagger: N and aux -> N + 1 (high product).  lambda <= 8 and
+ * N >= 2 lambda + 2; the high-mode maps need N b >= 64 (power-of-two root).
+ * The series coefficients are computed on the fly from the closed forms of
+ * series.cpp:146-183, so results agree with the table-driven reference to a
+ * few ulps of the largest term, not bit for bit. */
+int tmg_alpha_star_f64(tmg_context* ctx, int64_t N, int32_t b, int64_t lambda,
+                       const double* in, double* out);
+int tmg_beta_star_f64(tmg_context* ctx, int64_t N, int32_t b, int64_t lambda,
+                      const double* in, double* out);
+int tmg_gamma_dagger_f64(tmg_context* ctx, int64_t N, int32_t b, int64_t lambda,
+                         const double* in, double* out, double* aux);
+int tmg_delta_dagger_f64(tmg_context* ctx, int64_t N, int32_t b, int64_t lambda,
+                         const double* in, double aux, double* out);
+
 /* ---- the FP64 cyclic convolution on its own (convolution.hpp:64-67,
  * cyclic_convolve_f64 on an FFT plan of length n: make_plan(n, p, kFft)) ----
  * out[k] = sum_j f[j] g[(k - j) mod n] for host arrays of n doubles; out may

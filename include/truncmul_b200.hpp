@@ -201,6 +201,38 @@ class Context {
     return out;
   }
 
+  // The ring-change maps on FP64 sequences (maps_f64.hpp): alpha* and beta*
+  // (N -> N), gamma-dagger (N + 1 -> N and the root channel), delta-dagger
+  // (N and aux -> N + 1), for the series tables of (N, b, lambda).
+  std::vector<double> alpha_star_f64(std::int64_t N, std::int32_t b, std::int64_t lambda,
+                                     const std::vector<double>& in) {
+    need(in, N, "alpha_star_f64");
+    std::vector<double> out(static_cast<size_t>(N));
+    check(tmg_alpha_star_f64(h_, N, b, lambda, in.data(), out.data()));
+    return out;
+  }
+  std::vector<double> beta_star_f64(std::int64_t N, std::int32_t b, std::int64_t lambda,
+                                    const std::vector<double>& in) {
+    need(in, N, "beta_star_f64");
+    std::vector<double> out(static_cast<size_t>(N));
+    check(tmg_beta_star_f64(h_, N, b, lambda, in.data(), out.data()));
+    return out;
+  }
+  std::vector<double> gamma_dagger_f64(std::int64_t N, std::int32_t b, std::int64_t lambda,
+                                       const std::vector<double>& in, double* aux) {
+    need(in, N + 1, "gamma_dagger_f64");
+    std::vector<double> out(static_cast<size_t>(N));
+    check(tmg_gamma_dagger_f64(h_, N, b, lambda, in.data(), out.data(), aux));
+    return out;
+  }
+  std::vector<double> delta_dagger_f64(std::int64_t N, std::int32_t b, std::int64_t lambda,
+                                       const std::vector<double>& in, double aux) {
+    need(in, N, "delta_dagger_f64");
+    std::vector<double> out(static_cast<size_t>(N + 1));
+    check(tmg_delta_dagger_f64(h_, N, b, lambda, in.data(), aux, out.data()));
+    return out;
+  }
+
   // The machine-word splitters (products.hpp:77-79): N chunks of u, or the
   // N + 1 chunks of the top-aligned u 2^sigma, sigma = (N + 1) b - n.
   std::vector<std::int64_t> split_low_i64(const Limbs& u, const Params& p) {
@@ -238,6 +270,10 @@ class Context {
     return out;
   }
 
+  static void need(const std::vector<double>& v, std::int64_t count, const char* what) {
+    if (count < 0 || static_cast<std::int64_t>(v.size()) != count)
+      throw PlanMismatch(std::string(what) + ": wrong input length");
+  }
   using SplitFn = int (*)(tmg_context*, const tmg_params*, const std::uint64_t*, std::int64_t*);
   std::vector<std::int64_t> split(SplitFn fn, const Limbs& u, const Params& p, std::int64_t count) {
     if (p.n >= 1 && static_cast<std::int64_t>(u.size()) != (p.n + 63) / 64)

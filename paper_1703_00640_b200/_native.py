@@ -117,6 +117,11 @@ def load():
                                       P(ctypes.c_uint32), P(tmg_stats)]
     L.tmg_cyclic_convolve_f64.argtypes = [vp, i64, P(ctypes.c_double), P(ctypes.c_double),
                                           P(ctypes.c_double)]
+    PDbl = P(ctypes.c_double)
+    L.tmg_alpha_star_f64.argtypes = [vp, i64, ctypes.c_int32, i64, PDbl, PDbl]
+    L.tmg_beta_star_f64.argtypes = [vp, i64, ctypes.c_int32, i64, PDbl, PDbl]
+    L.tmg_gamma_dagger_f64.argtypes = [vp, i64, ctypes.c_int32, i64, PDbl, PDbl, PDbl]
+    L.tmg_delta_dagger_f64.argtypes = [vp, i64, ctypes.c_int32, i64, PDbl, ctypes.c_double, PDbl]
     for name in ("tmg_split_low_i64", "tmg_split_high_i64"):
         getattr(L, name).argtypes = [vp, P(tmg_params), u64p, P(ctypes.c_int64)]
     L.tmg_product_device.argtypes = [vp, P(tmg_params), vp, vp, vp, i64]

@@ -1291,6 +1291,59 @@ int conv_f64_host(Context& cx, int64_t n, const double* f, const double* g, doub
   return TMG_OK;
 }
 
+// alpha* / beta* / gamma-dagger / delta-dagger on host sequences
+// (maps_f64.hpp: alpha_star_f64, beta_star_f64, gamma_dagger_f64,
+// delta_dagger_f64 on the tables of build_map_tables_f64(N, b, lambda, ..)).
+// which: 0 alpha*, 1 beta*, 2 gamma-dagger, 3 delta-dagger.
+//   alpha*:        in N         -> out N
+//   beta*:         in N         -> out N
+//   gamma-dagger:  in N + 1     -> out N, *aux = the root channel
+//   delta-dagger:  in N, aux    -> out N + 1
+int map_f64_host(Context& cx, int which, int64_t N, int32_t b, int64_t lambda, const double* in,
+                 double aux_in, double* out, double* aux_out) {
+  if (N < 1 || b < 1 || b > 62 || lambda < 1)
+    throw Error(TMG_ERR_INPUT_OUT_OF_RANGE, "maps: N, b and lambda must be positive (b <= 62)");
+  const bool high = which >= 2;
+  if (N < 2 * lambda + 2)
+    throw Error(TMG_ERR_UNSUPPORTED, "maps: N below 2 lambda + 2");
+  if (high && N * int64_t(b) < 64)
+    throw Error(TMG_ERR_UNSUPPORTED, "maps: the high-mode maps need N b >= 64 on the GPU");
+  Params q;
+  q.mode = high ? PMode::kHigh : PMode::kLow;
+  q.backend = Backend::kFft;
+  q.b = b;
+  q.N = N;
+  q.lambda = lambda;
+  q.n = N * int64_t(b);
+  q.signed_split = true;
+  MapConsts mc = make_map_consts(q);  // lambda above the GPU limit throws here
+  mc.scale_out = 1.0;                 // the products fold 2^b in; the maps do not
+  const bool pre = (which == 0 || which == 2);
+  const int64_t nin = N + (which == 2 ? 1 : 0), nout = N + (which == 3 ? 1 : 0);
+  TMG_CUDA(cudaSetDevice(cx.device));
+  cx.dop_u.ensure(size_t(nin) * 8 + 16);
+  cx.dop_out.ensure(size_t(nout) * 8 + 16);
+  cx.pflags.ensure(16);
+  TMG_CUDA(cudaMemcpyAsync(cx.dop_u.p, in, size_t(nin) * 8, cudaMemcpyHostToDevice, cx.stream));
+  {
+    KTimer kt(cx, pre ? "k_map_pre" : "k_map_post", double(nin + nout) * 8.0);
+    if (pre)
+      launch_map_pre(mc, cx.dop_u.as<double>(), cx.dop_out.as<double>(), cx.pflags.as<double>(),
+                     cx.stream);
+    else
+      launch_map_post(mc, cx.dop_u.as<double>(), aux_in, cx.dop_out.as<double>(), cx.stream);
+  }
+  TMG_CUDA(cudaGetLastError());
+  TMG_CUDA(cudaMemcpyAsync(out, cx.dop_out.p, size_t(nout) * 8, cudaMemcpyDeviceToHost, cx.stream));
+  double aux = 0.0;
+  if (which == 2)
+    TMG_CUDA(cudaMemcpyAsync(&aux, cx.pflags.p, 8, cudaMemcpyDeviceToHost, cx.stream));
+  TMG_CUDA(cudaStreamSynchronize(cx.stream));
+  if (which == 2 && aux_out) *aux_out = aux;
+  cx.last_kernels = 1;
+  return TMG_OK;
+}
+
 // split_low_i64 / split_high_i64 (products.hpp:68-79): the chunks of one host
 // operand as int64 words.  The shape checks and their messages follow
 // split.cpp:104-158 (check_low_shape / check_high_shape, check_operand,
@@ -1458,6 +1511,26 @@ int tmg_product_batched(tmg_context* ctx, const tmg_params* params, const uint64
     const int32_t m = q.mode == PMode::kOracleFallback ? TMG_MODE_FULL : int32_t(q.mode);
     return host_product(ctx->cx, q, m, u, v, count, out, flags_out, stats);
   });
+}
+
+int tmg_alpha_star_f64(tmg_context* ctx, int64_t N, int32_t b, int64_t lambda, const double* in,
+                       double* out) {
+  return guarded([&] { return map_f64_host(ctx->cx, 0, N, b, lambda, in, 0.0, out, nullptr); });
+}
+
+int tmg_beta_star_f64(tmg_context* ctx, int64_t N, int32_t b, int64_t lambda, const double* in,
+                      double* out) {
+  return guarded([&] { return map_f64_host(ctx->cx, 1, N, b, lambda, in, 0.0, out, nullptr); });
+}
+
+int tmg_gamma_dagger_f64(tmg_context* ctx, int64_t N, int32_t b, int64_t lambda, const double* in,
+                         double* out, double* aux) {
+  return guarded([&] { return map_f64_host(ctx->cx, 2, N, b, lambda, in, 0.0, out, aux); });
+}
+
+int tmg_delta_dagger_f64(tmg_context* ctx, int64_t N, int32_t b, int64_t lambda, const double* in,
+                         double aux, double* out) {
+  return guarded([&] { return map_f64_host(ctx->cx, 3, N, b, lambda, in, aux, out, nullptr); });
 }
 
 int tmg_cyclic_convolve_f64(tmg_context* ctx, int64_t n, const double* f, const double* g,

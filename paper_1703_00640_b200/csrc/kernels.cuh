@@ -334,4 +334,10 @@ void launch_conv_pack(const double* d_f, const double* d_g, int64_t n, double gs
 void launch_conv_direct(const double* d_f, const double* d_g, int64_t n, double* d_out,
                         cudaStream_t st);
 
+// The ring-change maps on their own (k_maps.cu; maps_f64.hpp).
+void launch_map_pre(const MapConsts& mc, const double* d_in, double* d_out, double* d_aux,
+                    cudaStream_t st);
+void launch_map_post(const MapConsts& mc, const double* d_in, double aux, double* d_out,
+                     cudaStream_t st);
+
 }  // namespace tmg

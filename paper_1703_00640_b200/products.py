@@ -324,6 +324,41 @@ class Context:
                                                  ga.ctypes.data_as(PD), out.ctypes.data_as(PD)))
         return out
 
+    def _map(self, name: str, N: int, b: int, lam: int, x, nin: int, nout: int, aux=None):
+        xa = np.ascontiguousarray(x, dtype=np.float64)
+        if xa.ndim != 1 or len(xa) != nin:
+            raise PlanMismatch(f"{name}: the input must hold {nin} doubles")
+        out = np.empty(nout, dtype=np.float64)
+        PD = ctypes.POINTER(ctypes.c_double)
+        fn = getattr(self._lib, "tmg_" + name)
+        if name == "gamma_dagger_f64":
+            au = ctypes.c_double(0.0)
+            _check(fn(self._h, N, b, lam, xa.ctypes.data_as(PD), out.ctypes.data_as(PD), ctypes.byref(au)))
+            return out, float(au.value)
+        if name == "delta_dagger_f64":
+            _check(fn(self._h, N, b, lam, xa.ctypes.data_as(PD), float(aux), out.ctypes.data_as(PD)))
+            return out
+        _check(fn(self._h, N, b, lam, xa.ctypes.data_as(PD), out.ctypes.data_as(PD)))
+        return out
+
+    def alpha_star_f64(self, N: int, b: int, lam: int, x) -> np.ndarray:
+        """alpha* of the low product's pre-map (maps_f64.hpp alpha_star_f64): N -> N."""
+        return self._map("alpha_star_f64", N, b, lam, x, N, N)
+
+    def beta_star_f64(self, N: int, b: int, lam: int, w) -> np.ndarray:
+        """beta* of the low product's post-map (beta_star_f64): N -> N."""
+        return self._map("beta_star_f64", N, b, lam, w, N, N)
+
+    def gamma_dagger_f64(self, N: int, b: int, lam: int, x):
+        """gamma-dagger of the high product's pre-map (gamma_dagger_f64): N + 1
+        chunks -> (N values, the root channel aux)."""
+        return self._map("gamma_dagger_f64", N, b, lam, x, N + 1, N)
+
+    def delta_dagger_f64(self, N: int, b: int, lam: int, w, aux: float) -> np.ndarray:
+        """delta-dagger of the high product's post-map (delta_dagger_f64): N
+        convolution values and aux = theta_u theta_v -> N + 1 values."""
+        return self._map("delta_dagger_f64", N, b, lam, w, N, N + 1, aux)
+
     def split_i64(self, u, params: Params, high: bool = False) -> np.ndarray:
         """The chunks of one operand as int64 words (split_low_i64 /
         split_high_i64, products.hpp:77-79): N of them, or the N + 1 chunks
