@@ -166,7 +166,10 @@ int tmg_delta_dagger_f64(tmg_context* ctx, int64_t N, int32_t b, int64_t lambda,
  * with make_plan's message otherwise, convolution.cpp:92-105).  Lengths above
  * 4096 run the products' transform passes and must be multiples of 4 (every
  * length select_params picks is); shorter ones, and other lengths up to
- * 32768, are summed directly. */
+ * 32768, are summed directly.  Three-pass lengths (above 4096 x 2048) whose
+ * column part has no factorisation A x B with 4 | A and both at most 2048 --
+ * lengths with very few factors of two, e.g. 2^2 3 5^9 -- are refused with
+ * TMG_ERR_UNSUPPORTED_LENGTH as well. */
 int tmg_cyclic_convolve_f64(tmg_context* ctx, int64_t n, const double* f,
                             const double* g, double* out);
 
