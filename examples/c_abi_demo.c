@@ -132,6 +132,36 @@ int main(void) {
   printf("escalated: rc=%d attempts=%d b=%d residual %.4f %s\n", rc, st.attempts, st.b,
          st.max_round_err, ok ? "exact" : "WRONG");
   bad |= !ok;
+  /* the stages of the pipeline as entry points of their own: the documented
+   * split of 13 into 2-bit chunks (test_products.cpp:52-64), a cyclic
+   * convolution with a shifted delta, and alpha* with one series row (the
+   * identity map) */
+  {
+    tmg_params sp = {6, 2, 3, 0, 8, TMG_MODE_FULL, TMG_BACKEND_EXACT, 0};
+    const uint64_t thirteen = 13;
+    int64_t chunks[3] = {-1, -1, -1};
+    CHECK(tmg_split_low_i64(ctx, &sp, &thirteen, chunks));
+    int sok = chunks[0] == 1 && chunks[1] == 3 && chunks[2] == 0;
+    enum { CN = 8192 };
+    static double f[CN], g[CN], c[CN];
+    for (int i = 0; i < CN; ++i) {
+      f[i] = (double)((i * 37) % 101 - 50);
+      g[i] = 0.0;
+    }
+    g[3] = 2.0;
+    CHECK(tmg_cyclic_convolve_f64(ctx, CN, f, g, c));
+    int cok = 1;
+    for (int i = 0; i < CN; ++i) {
+      const double want = 2.0 * f[(i + CN - 3) % CN], d = c[i] - want;
+      cok &= d < 1e-9 && d > -1e-9;
+    }
+    CHECK(tmg_alpha_star_f64(ctx, CN, 12, 1, f, c));
+    int aok = 1;
+    for (int i = 0; i < CN; ++i) aok &= c[i] == f[i];
+    printf("entry points: split %s, convolution %s, alpha* %s\n", sok ? "ok" : "WRONG",
+           cok ? "ok" : "WRONG", aok ? "ok" : "WRONG");
+    bad |= !(sok && cok && aok);
+  }
   tmg_context_destroy(ctx);
   printf(bad ? "FAILED\n" : "OK\n");
   return bad;
