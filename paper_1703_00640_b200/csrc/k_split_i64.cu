@@ -17,8 +17,10 @@
 // passes"; a lane's carry-in comes from the nearest lane below it that does
 // not pass, and when every lane below passes from the tile's carry-in: the
 // tile before it in the warp decides that the same way, and for the warp's
-// first tile lane 0 walks down from the chunk below it through windows equal
-// to 2^{b-1} (one in 2^b for random operands).  Algorithmic bytes: n / 8
+// first tile the warp walks down from the chunk below it, 32 windows per
+// trip, through windows equal to 2^{b-1} (one in 2^b for random operands; an
+// operand made of such windows only costs every warp a walk to chunk 0:
+// 2^24 bits at b = 13 take 359 ms with a one-window walk).  Algorithmic bytes: n / 8
 // read, 8 per chunk written.
 //
 // The products' own split (k_zsplit / k_zgen) stores FFT-ordered digit
@@ -55,16 +57,18 @@ k_split_i64(const uint64_t* __restrict__ limbs, int64_t nlimbs, int64_t n, int b
   // the warp's carry-in: the chunk below its first, walked down through passing windows
   int cin = 0;
   if (balanced) {
-    if (lane == 0) {
-      for (int64_t j = base - 1; j >= 0; --j) {
-        const uint64_t x = window_bits(limbs, nlimbs, j * b - lead, b);
-        if (x != half) {
-          cin = x > half ? 1 : 0;
-          break;
-        }
+    // the whole warp walks: 32 windows per trip, the highest lane whose
+    // window does not pass decides (a window below chunk 0 reads 0: no carry)
+    for (int64_t j = base - 1; j >= 0; j -= 32) {
+      const int64_t jj = j - lane;
+      const uint64_t x = jj >= 0 ? window_bits(limbs, nlimbs, jj * b - lead, b) : 0ull;
+      const uint32_t dec = __ballot_sync(0xffffffffu, x != half);
+      if (dec) {
+        const int first = __ffs(dec) - 1;  // lane 0 holds the chunk nearest to the warp
+        cin = int((__ballot_sync(0xffffffffu, x > half) >> first) & 1u);
+        break;
       }
     }
-    cin = __shfl_sync(0xffffffffu, cin, 0);
   }
 #pragma unroll
   for (int k = 0; k < kSplitPer; ++k) {
