@@ -9,8 +9,9 @@
 // balanced split (split.cpp:88-95) enters a run from the window below it: a
 // window other than 2^{b-1} decides its carry-out whatever comes in (1 above,
 // 0 below), so the run reads that one window (and walks further down only
-// through windows equal to 2^{b-1}) -- no block scan, no aggregates, no
-// look-back, every run independent.  The thread then walks its chunks with
+// through windows equal to 2^{b-1}, inside its row segment; below the segment
+// one warp per segment has walked for the block) -- no block scan, no
+// aggregates, no look-back.  The thread then walks its chunks with
 // the carry in a register and stores the digit pairs of both operands
 // (short2 for b <= 14, else int2) in 16-byte pieces in z's tile order, plus
 // its 32 carry-in bits per operand (one word: the few places that re-derive
@@ -41,13 +42,17 @@ __device__ __forceinline__ uint32_t ld_word(const uint64_t* limbs, int64_t nlimb
 
 // Carry out of chunk j (>= 0, below the top chunk): its window decides it
 // unless it equals 2^{b-1}; then the chunk below does.
-__device__ __noinline__ int carry_below(const uint64_t* limbs, int64_t nlimbs, int64_t lead, int b, int64_t j) {
+// The walk stays inside the thread's row segment (chunks >= cs): below it the
+// carry into chunk cs is segcin, which one warp per segment has walked for
+// the whole block (see the kernel).
+__device__ __noinline__ int carry_below(const uint64_t* limbs, int64_t nlimbs, int64_t lead, int b, int64_t j,
+                                        int64_t cs, int segcin) {
   const uint64_t half = 1ull << (b - 1);
-  for (; j >= 0; --j) {
+  for (; j >= cs; --j) {
     const uint64_t w = window_bits(limbs, nlimbs, j * b - lead, b);
     if (w != half) return w > half ? 1 : 0;
   }
-  return 0;
+  return segcin;
 }
 
 template <int DIG>
@@ -147,6 +152,34 @@ __global__ void __launch_bounds__(kZsThreads) k_zsplit(ZgenArgs a) {
       }
     }
   }
+  // Carry into the first chunk of each row segment, for the runs whose walk
+  // through windows equal to 2^{b-1} reaches the segment's start: warp w
+  // walks below segment w with 32 windows per trip (the lane nearest to the
+  // segment that does not pass decides; windows below chunk 0 read 0: no
+  // carry).  One trip for random operands; an operand made of such windows
+  // costs the block 8 warp walks to chunk 0 and not one per run.
+  __shared__ int s_segcin[2][8];
+  if (uint32_t(tid) >> 5 < rb) {
+    const uint32_t wp = uint32_t(tid) >> 5, ln = uint32_t(tid) & 31u;
+    const int64_t cs = seg_first(wp);
+    constexpr uint64_t halfw = 1ull << (B - 1);
+#pragma unroll 1
+    for (int op = 0; op < 2; ++op) {
+      const uint64_t* lp = op ? a.v : a.u;
+      int cin = 0;
+#pragma unroll 1
+      for (int64_t j = cs - 1; j >= 0; j -= 32) {
+        const int64_t jj = j - int64_t(ln);
+        const uint64_t x = jj >= 0 ? window_bits(lp, a.nlimbs, jj * B - a.lead, B) : 0ull;
+        const uint32_t dec = __ballot_sync(0xffffffffu, x != halfw);
+        if (dec) {
+          cin = int((__ballot_sync(0xffffffffu, x > halfw) >> (__ffs(dec) - 1)) & 1u);
+          break;
+        }
+      }
+      if (ln == 0) s_segcin[op][wp] = cin;
+    }
+  }
   if (blockIdx.x == 0 && tid == 0 && (a.n & 63)) {
     const uint64_t hm = ~0ull << (a.n & 63);
     if ((__ldg(a.u + a.nlimbs - 1) | __ldg(a.v + a.nlimbs - 1)) & hm)
@@ -179,8 +212,8 @@ __global__ void __launch_bounds__(kZsThreads) k_zsplit(ZgenArgs a) {
     cu = pu > half ? 1 : 0;
     cv = pv > half ? 1 : 0;
     // a window equal to 2^{b-1} passes the carry of the chunk below it on
-    if (pu == half) cu = carry_below(a.u, a.nlimbs, a.lead, B, j0 - 2);
-    if (pv == half) cv = carry_below(a.v, a.nlimbs, a.lead, B, j0 - 2);
+    if (pu == half) cu = carry_below(a.u, a.nlimbs, a.lead, B, j0 - 2, seg_first(lr), s_segcin[0][lr]);
+    if (pv == half) cv = carry_below(a.v, a.nlimbs, a.lead, B, j0 - 2, seg_first(lr), s_segcin[1][lr]);
     if (j0 == 0) cu = cv = 0;
   }
   const ZTile& zt = a.zt;
