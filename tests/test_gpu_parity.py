@@ -988,3 +988,64 @@ def test_split_by_runs_carry_chains(n):
         assert np.array_equal(r0, r1)
         _check(mode, u, v, n, tm.from_limbs(r0))
     c.close()
+
+
+@pytest.mark.parametrize("mode", [tm.Mode.LOW, tm.Mode.HIGH])
+def test_split_by_runs_long_half_window_stretches(mode):
+    """Carry walks that leave a run's row segment and its block: stretches of
+    several thousand to a million windows equal to 2^{b-1} (one of them down
+    to chunk 0), with and without a carry arriving below them; the carry into
+    a segment's first chunk then comes from the block's per-segment warp walk
+    (k_zsplit).  Against the block-scan split k_zgen and GMP; the second
+    operand is random so that the product certifies."""
+    n = 1 << 24
+    c = _opt_ctx((tm._native.TMG_OPT_SPLIT_KERNEL, 1))
+    rng = np.random.default_rng(77 + int(mode))
+    nl = n // 64
+    # the 2^26 products' chunk width and length (b = 12, N = 5 898 240): the
+    # long runs of equal digits concentrate the spectrum, and 2^24's own b = 13
+    # refuses them; one bit less certifies all but the longest
+    p26 = sp(1 << 26, mode)
+    p = tm.manual_params(n, p26.b, p26.N, mode, lam=p26.lam)
+    b, N = p.b, p.N
+    lead = (N + 1) * b - n if mode == tm.Mode.HIGH else 0
+    v = _rand(rng, n)
+    refused = 0
+    for stretches, carry in ((((0, 20000),), False), (((5000, 1200000),), True),
+                             (((3, 9000), (40000, 300000), (700001, 2500)), True)):
+        x = int.from_bytes(rng.bytes(nl * 8), "little") & ((1 << n) - 1)
+        off = -(-lead // b)  # first chunk that holds operand bits (the high split is top-aligned)
+        for j1, length in stretches:
+            lo = max((j1 + off) * b - lead, 0)
+            hi = min((j1 + off + length) * b - lead, n - (n % b) - b)
+            # whole windows [lo, hi) (aligned to the chunk grid) set to 2^{b-1}
+            lo += (-(lo + lead)) % b
+            hi -= (hi + lead) % b
+            k = (hi - lo) // b
+            pat = (((1 << (b * k)) - 1) // ((1 << b) - 1)) << (b - 1)
+            x &= ~(((1 << (hi - lo)) - 1) << lo)
+            x |= pat << lo
+            if carry and lo >= b:
+                x |= ((1 << b) - 1) << (lo - b)
+        u = port.int_to_limbs(x & ((1 << n) - 1), nl)
+        d = tm.default_context(0)
+        try:
+            r0 = d.product_limbs(mode, u, v, p)
+        except tm.ConvolutionPrecisionFailure:
+            # a million equal digits of full magnitude: the transform's coherent
+            # error refuses the product (DESIGN.md, Numerics); the two splits
+            # must then refuse alike, with the same residual
+            e0 = d.last_stats.max_round_err
+            with pytest.raises(tm.ConvolutionPrecisionFailure):
+                c.product_limbs(mode, u, v, p)
+            assert c.last_stats.max_round_err == e0
+            refused += 1
+            continue
+        e0 = d.last_stats.max_round_err
+        r1 = c.product_limbs(mode, u, v, p)
+        assert np.array_equal(r0, r1) and c.last_stats.max_round_err == e0
+        _check(mode, u, v, n, tm.from_limbs(r0))
+        r2 = d.product_limbs(mode, v, u, p)
+        assert np.array_equal(r0, r2)
+    assert refused <= 1  # the first and the last operand certify (residuals 0.012 and 0.10)
+    c.close()
